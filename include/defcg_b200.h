@@ -1,0 +1,237 @@
+/*
+ * defcg_b200.h — C ABI of the B200-native deflated-CG (def-CG) hot path.
+ *
+ * The reference (`defcg`, arXiv 1706.00241) is a single-process CPU package
+ * whose only plugin point is the kernel backend selected by DEFCG_BACKEND
+ * (/root/reference/pkg/src/defcg/_kernels/__init__.py:11-45).  That per-kernel
+ * boundary is too fine for a GPU (the solver loop would ship the n x n matrix
+ * every iteration, solvers.py:169), so this ABI exposes two layers:
+ *
+ *   L0  dcg_k_*      device twins of the eight backend kernels
+ *                    (_kernels/_core.pyx:16-177), for unit parity;
+ *   L1-L4            the solver API one level up (linalg.py, solvers.py,
+ *                    recycle.py, gpc.py): operator apply, Gram factor with
+ *                    pruning, the whole CG / def-CG loop as ONE persistent
+ *                    kernel, harmonic-Ritz extraction, the small dense
+ *                    eigensolvers, RBF Gram assembly and the GPC Newton glue.
+ *
+ * Conventions
+ *   - Every pointer argument named d_* is DEVICE memory (cudaMalloc / torch).
+ *     Matrices are row-major fp64 with an explicit leading dimension; vectors
+ *     are contiguous fp64.  The library never frees caller memory.
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *   - Every entry point returns an int status (DCG_OK == 0).  Entry points
+ *     whose outcome depends on device data (pivot failures, breakdown,
+ *     convergence) synchronise `stream` before returning; their payload
+ *     (pivot index, iteration, remaining columns, sweeps) is written to
+ *     *info when info != NULL — the same payloads the reference exceptions
+ *     carry (errors.py:8-93).
+ *   - A dcg_context owns the device workspace and must be used from one host
+ *     thread at a time.
+ */
+#ifndef DEFCG_B200_H
+#define DEFCG_B200_H
+
+#if defined(__GNUC__)
+#define DCG_API __attribute__((visibility("default")))
+#else
+#define DCG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DCG_ABI_VERSION 1
+
+/* ---- status codes: one per reference exception type (errors.py) ---------- */
+enum dcg_status {
+    DCG_OK = 0,
+    DCG_E_DIMENSION = 1,        /* DimensionMismatch            errors.py:24 */
+    DCG_E_NOT_PD = 2,           /* NotPositiveDefinite(pivot)   errors.py:28-33 */
+    DCG_E_BREAKDOWN = 3,        /* BreakdownZeroCurvature(it)   errors.py:44-49 */
+    DCG_E_GRAM_NOT_SPD = 4,     /* GramNotSpd                   errors.py:52-53 */
+    DCG_E_BASIS_DEFICIENT = 5,  /* BasisDeficient(remaining)    errors.py:56-61 */
+    DCG_E_NO_CONVERGENCE = 6,   /* NoConvergence(sweeps)        errors.py:36-41 */
+    DCG_E_ASYMMETRIC = 7,       /* ValueError from require_symmetric, linalg.py:49-55 */
+    DCG_E_CONFIG = 8,           /* ValueError from bad arguments / SolverConfig */
+    DCG_E_CUDA = 9,             /* CUDA runtime failure (info = cudaError_t) */
+    DCG_E_UNSUPPORTED = 10      /* size outside the compiled limits (k > DCG_MAX_K ...) */
+};
+
+#define DCG_MAX_K 64            /* deflation basis columns handled by the fused kernels */
+#define DCG_MAX_T 112           /* harmonic pencil order k_prev + m handled on device   */
+
+/* ---- operator: A = shift * I + diag(s) * K * diag(s) --------------------- */
+/* The reference always materialises A (gpc.py:178 builds K * outer(s,s) + I).
+ * Here A stays implicit: the Newton system is (K, s = sqrt(h), shift = 1);
+ * an explicit matrix is (K = A, s = NULL, shift = 0).  `row0/rows` select the
+ * locally stored row slab for row-sharded operators (rows == n on one GPU). */
+enum dcg_op_kind { DCG_OP_DENSE = 0, DCG_OP_RBF = 1 };
+
+typedef struct dcg_operator {
+    int kind;                 /* dcg_op_kind                                     */
+    long long n;              /* global order                                    */
+    long long row0;           /* first global row held by this rank              */
+    long long rows;           /* number of rows held (== n unsharded)            */
+    const double* d_k;        /* DENSE: rows x ldk slab of K (row-major)         */
+    long long ldk;            /* DENSE: leading dimension (>= n, even)           */
+    const double* d_x;        /* RBF: n x dim points, row-major (all points)     */
+    long long dim;            /* RBF: point dimension                            */
+    double var;               /* RBF: signal variance                            */
+    double inv_two_ell2;      /* RBF: 1 / (2 lengthscale^2)                      */
+    double diag;              /* RBF: diagonal value (var + jitter)              */
+    const double* d_s;        /* optional symmetric scaling s (n), NULL = ones   */
+    double shift;             /* identity shift                                  */
+} dcg_operator;
+
+/* ---- deflation basis (solvers.py:84-115 RecycleBasis) -------------------- */
+typedef struct dcg_basis {
+    long long k;              /* columns (0 = plain CG)                          */
+    const double* d_w;        /* n x k row-major W                               */
+    const double* d_aw;       /* n x k row-major AW                              */
+    const double* d_chol;     /* k x k row-major lower Cholesky factor of W'AW   */
+} dcg_basis;
+
+/* ---- SolverConfig (solvers.py:28-51) ------------------------------------- */
+typedef struct dcg_solver_config {
+    double tol;
+    long long max_iters;      /* <= 0 selects the reference default 10 n         */
+    long long ell;
+    long long recompute_residual_every;
+} dcg_solver_config;
+
+/* ---- KrylovLog (solvers.py:54-72), caller-owned device buffers ----------- */
+typedef struct dcg_krylov_log {
+    long long ell;            /* capacity in logged iterations                   */
+    double* d_p;              /* ell x n      search directions p_0..p_{m-1}     */
+    double* d_r;              /* (ell+1) x n  residuals r_0..r_m                 */
+    double* d_d;              /* ell          p'Ap                               */
+    double* d_alpha;          /* ell                                             */
+    double* d_beta;           /* ell                                             */
+    double* d_mu;             /* ell x k      deflation coefficients (k > 0)     */
+} dcg_krylov_log;
+
+/* ---- SolveReport (solvers.py:75-81) -------------------------------------- */
+typedef struct dcg_solve_info {
+    long long iterations;
+    long long stored;         /* m = logged iterations                           */
+    int converged;
+    int termination;          /* 0 = "converged", 1 = "max_iters"               */
+    double rel_residual;      /* final recurrence residual                       */
+    double norm_b;
+    double device_ms;         /* solve-kernel time measured with CUDA events     */
+} dcg_solve_info;
+
+/* ---- context ------------------------------------------------------------- */
+typedef struct dcg_context dcg_context;
+
+DCG_API int dcg_version(void);
+DCG_API const char* dcg_status_string(int status);
+DCG_API int dcg_context_create(int device, dcg_context** out);
+DCG_API int dcg_context_destroy(dcg_context* ctx);
+/* number of CTAs of the persistent solve kernel (one per SM) */
+DCG_API int dcg_context_grid(dcg_context* ctx, int* blocks, int* sm_count);
+
+/* ---- L0: device twins of the backend kernels (_core.pyx) ----------------- */
+/* y = A x                                          _core.pyx:16-28  matvec   */
+DCG_API int dcg_k_matvec(dcg_context* ctx, void* stream, const double* d_a, long long m,
+                 long long n, long long lda, const double* d_x, double* d_y);
+/* C(m x n) = A(m x kk) B(kk x n), all row-major   _core.pyx:31-44  gemm     */
+DCG_API int dcg_k_gemm(dcg_context* ctx, void* stream, const double* d_a, const double* d_b,
+               double* d_c, long long m, long long kk, long long n);
+/* lower L with pivot rule acc <= pivot_tol -> fail   _core.pyx:47-66        */
+DCG_API int dcg_k_cholesky(dcg_context* ctx, void* stream, const double* d_a, long long n,
+                   double pivot_tol, double* d_l, long long* fail_index);
+/*                                                  _core.pyx:69-94          */
+DCG_API int dcg_k_solve_lower(dcg_context* ctx, void* stream, const double* d_l, long long n,
+                      const double* d_b, double* d_y);
+DCG_API int dcg_k_solve_lower_trans(dcg_context* ctx, void* stream, const double* d_l,
+                            long long n, const double* d_b, double* d_x);
+/* rows [row0, row0+rows) of the RBF Gram            _core.pyx:97-114        */
+DCG_API int dcg_k_rbf_gram(dcg_context* ctx, void* stream, const double* d_x, long long n,
+                   long long dim, double signal_var, double inv_two_ell2, double jitter,
+                   double* d_k, long long ldk, long long row0, long long rows);
+/*                                                  _core.pyx:117-132        */
+DCG_API int dcg_k_rbf_cross(dcg_context* ctx, void* stream, const double* d_xa, long long na,
+                    const double* d_xb, long long nb, long long dim, double signal_var,
+                    double inv_two_ell2, double* d_k);
+/* one cyclic Jacobi sweep in place                  _core.pyx:135-177       */
+DCG_API int dcg_k_jacobi_sweep(dcg_context* ctx, void* stream, double* d_a, double* d_v,
+                       long long n, long long* rotations);
+
+/* ---- L1: dense linear algebra (linalg.py) -------------------------------- */
+/* max|A - A'| <= rtol * max|A|  -> *symmetric = 1     linalg.py:49-55       */
+DCG_API int dcg_check_symmetric(dcg_context* ctx, void* stream, const double* d_a, long long n,
+                        long long lda, double rtol, int* symmetric);
+/* cyclic-Jacobi eigen-decomposition, ascending      linalg.py:139-165        */
+DCG_API int dcg_sym_eigen(dcg_context* ctx, void* stream, const double* d_a, long long n,
+                  long long max_sweeps, double rtol, double* d_values, double* d_vectors,
+                  long long* info);
+/* G u = theta F u via F = L L'                       linalg.py:168-191        */
+DCG_API int dcg_gen_sym_eigen(dcg_context* ctx, void* stream, const double* d_g, const double* d_f,
+                      long long n, long long max_sweeps, double* d_values,
+                      double* d_vectors, long long* info);
+
+/* ---- L2: operator and Krylov solvers (solvers.py) ------------------------ */
+/* y = A x (rows of this rank only: y has op->rows entries)                    */
+DCG_API int dcg_op_apply(dcg_context* ctx, void* stream, const dcg_operator* op,
+                 const double* d_x, double* d_y);
+/* Y = A X for a row-major n x k block (multi-vector, FP64 MMA)  recycle.py:90 */
+DCG_API int dcg_op_apply_block(dcg_context* ctx, void* stream, const dcg_operator* op,
+                       const double* d_x, long long k, double* d_y);
+/* Gram = sym(W'AW); Cholesky with pivot 1e-14*max diag.  prune != 0 deletes the
+ * failing-pivot column of W and AW in place and retries (recycle.py:66-77);
+ * prune == 0 fails with DCG_E_GRAM_NOT_SPD (solvers.py:107-115).  d_chol gets
+ * the k_out x k_out factor.                                                  */
+DCG_API int dcg_gram_factor(dcg_context* ctx, void* stream, double* d_w, double* d_aw,
+                    long long n, long long k, int prune, double* d_chol,
+                    long long* k_out, long long* info);
+/* refresh_basis (recycle.py:80-92): AW = A W for the new operator (FP64 MMA,
+ * one pass over K), Gram factorisation with failing-pivot pruning; the
+ * surviving columns are written compacted to d_w_out / d_aw_out (n x k_out). */
+DCG_API int dcg_refresh_basis(dcg_context* ctx, void* stream, const dcg_operator* op,
+                      const double* d_w, long long k, double* d_w_out, double* d_aw_out,
+                      double* d_chol, long long* k_out, long long* info);
+/* CG (basis == NULL or basis->k == 0, solvers.py:207-219) or deflated CG with
+ * the x_prev warm-start correction (solvers.py:222-239); the whole
+ * _run_loop (solvers.py:131-204) runs as one persistent cooperative kernel.
+ * d_history needs max_iters + 1 entries.                                      */
+DCG_API int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_b,
+              const double* d_x0, const dcg_basis* basis, const dcg_solver_config* cfg,
+              double* d_x, dcg_krylov_log* log, double* d_history,
+              dcg_solve_info* out, long long* info);
+/* v - AW (W'AW)^-1 W' v                              solvers.py:242-256       */
+DCG_API int dcg_deflation_project(dcg_context* ctx, void* stream, long long n,
+                          const dcg_basis* basis, const double* d_v, double* d_out);
+
+/* ---- L3: recycling (recycle.py) ------------------------------------------ */
+enum dcg_selection { DCG_SELECT_SMALLEST = 0, DCG_SELECT_LARGEST = 1 };
+/* harmonic Ritz extraction (recycle.py:95-159).  prev may be NULL.  Outputs:
+ * theta (k), u (T x k row-major, T = columns kept), z (n x T), w_next, aw_next
+ * (n x k).  z/u may be NULL.  *t_out = T after zero-column dropping/pruning.
+ * DCG_E_BASIS_DEFICIENT carries the reference's `remaining` in *info.        */
+DCG_API int dcg_ritz_extract(dcg_context* ctx, void* stream, long long n, const dcg_krylov_log* log,
+                     long long m, const dcg_basis* prev, long long k, int selection,
+                     double* d_theta, double* d_u, double* d_z, double* d_w_next,
+                     double* d_aw_next, long long* t_out, long long* info);
+
+/* ---- L4: GPC Laplace-Newton glue (gpc.py) -------------------------------- */
+/* loglik, grad, h of the logistic likelihood          gpc.py:126-157          */
+DCG_API int dcg_gpc_derivs(dcg_context* ctx, void* stream, long long n, const double* d_f,
+                   const double* d_y, double* d_grad, double* d_h, double* loglik);
+/* s = sqrt(h); inner = h f + grad; b = s * (K inner)   gpc.py:175-183          */
+DCG_API int dcg_gpc_newton_system(dcg_context* ctx, void* stream, const dcg_operator* kop,
+                          const double* d_f, const double* d_grad, const double* d_h,
+                          double* d_s, double* d_inner, double* d_b);
+/* a = inner - s x; f = K a; (loglik, grad, h)(f); psi = loglik - f'a / 2
+ *                                                     gpc.py:186-209          */
+DCG_API int dcg_gpc_newton_update(dcg_context* ctx, void* stream, const dcg_operator* kop,
+                          const double* d_inner, const double* d_s, const double* d_x,
+                          const double* d_y, double* d_a, double* d_f, double* d_grad,
+                          double* d_h, double* loglik, double* psi);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DEFCG_B200_H */

@@ -1,0 +1,86 @@
+"""Device plumbing: torch tensors for HBM allocation, the current stream, and
+conversions at the drop-in boundary (numpy in -> numpy out, torch in -> torch out)."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native
+from .errors import DeviceError, DimensionMismatch
+
+F64 = torch.float64
+LD_ALIGN = 32  # row pitch of device matrices in doubles (256 B)
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the def-CG B200 path has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def ctx() -> int:
+    return _native.context(device().index)
+
+
+def stream() -> int:
+    return torch.cuda.current_stream(device()).cuda_stream
+
+
+def is_torch(a) -> bool:
+    return isinstance(a, torch.Tensor)
+
+
+def to_dev(a, ndim: int | None = None) -> torch.Tensor:
+    """Contiguous fp64 device tensor (copies host data; shares device data when possible)."""
+    if isinstance(a, torch.Tensor):
+        t = a.to(device=device(), dtype=F64)
+    else:
+        arr = np.ascontiguousarray(a, dtype=np.float64)
+        t = torch.from_numpy(arr).to(device(), non_blocking=False)
+    if ndim is not None and t.ndim != ndim:
+        kind = "vector" if ndim == 1 else "matrix"
+        raise DimensionMismatch(f"expected a {kind}, got ndim={t.ndim}")
+    return t.contiguous()
+
+
+def as_host_vector(v) -> np.ndarray:
+    out = np.ascontiguousarray(v, dtype=np.float64)
+    if out.ndim != 1:
+        raise DimensionMismatch(f"expected a vector, got ndim={out.ndim}")
+    return out
+
+
+def padded_ld(n: int) -> int:
+    return max(LD_ALIGN, (n + LD_ALIGN - 1) // LD_ALIGN * LD_ALIGN)
+
+
+def to_dev_padded(a) -> tuple[torch.Tensor, int]:
+    """Row-major device copy with a 256-byte row pitch (zero padding)."""
+    t = to_dev(a, 2)
+    rows, cols = t.shape
+    ld = padded_ld(cols)
+    if ld == cols:
+        return t, ld
+    buf = torch.zeros((rows, ld), dtype=F64, device=t.device)
+    buf[:, :cols].copy_(t)
+    return buf, ld
+
+
+def out_like(x_dev: torch.Tensor, template):
+    """Return device data in the caller's flavour (numpy unless torch was passed)."""
+    if is_torch(template):
+        return x_dev
+    return x_dev.detach().cpu().numpy()
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def empty(*shape) -> torch.Tensor:
+    return torch.empty(shape, dtype=F64, device=device())
+
+
+def zeros(*shape) -> torch.Tensor:
+    return torch.zeros(shape, dtype=F64, device=device())

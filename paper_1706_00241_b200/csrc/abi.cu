@@ -1,0 +1,817 @@
+// C ABI entry points (include/defcg_b200.h): context, workspace, the L0
+// kernel twins, operator application, basis refresh / Gram factorisation,
+// harmonic-Ritz extraction, eigensolvers and the GPC glue.  Each entry point
+// mirrors one reference function (cited per function) and maps its failure
+// modes to the status codes of errors.py.
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "common.cuh"
+
+thread_local cudaError_t dcg_last_cuda_error = cudaSuccess;
+
+// launchers implemented in the other translation units
+int dcg_gemv_launch(dcg_context*, cudaStream_t, const double*, long long, long long, long long, const double*,
+                    const double*, const double*, double, const double*, double*);
+size_t dcg_block_apply_scratch_doubles(long long n, long long rows, int k);
+int dcg_block_apply(dcg_context*, cudaStream_t, const double*, long long, long long, long long, const double*, int,
+                    const double*, const double*, double, const double*, double*, double*);
+int dcg_xty(dcg_context*, cudaStream_t, const double*, long long, const double*, long long, long long, int, int,
+            double*, double*);
+size_t dcg_xty_scratch_doubles(dcg_context* ctx, int p, int q);
+int dcg_gemm_lr(dcg_context*, cudaStream_t, const double*, long long, const double*, long long, double*, long long,
+                long long, long long, long long);
+int dcg_gram_factor_launch(cudaStream_t, const double*, int, int, double*, double*, int*, DevStatus*);
+size_t dcg_pencil_smem(int T);
+int dcg_ritz_pencil_launch(cudaStream_t, const double*, const double*, int, int, int, int, double*, double*,
+                           double*, int*, DevStatus*);
+int dcg_sym_eigen_launch(cudaStream_t, const double*, int, int, double, double*, double*, DevStatus*);
+int dcg_gen_sym_eigen_launch(cudaStream_t, const double*, const double*, int, int, double*, double*, double*,
+                             DevStatus*);
+int dcg_k_cholesky_launch(cudaStream_t, const double*, int, double, double*, DevStatus*);
+int dcg_k_solve_lower_launch(cudaStream_t, const double*, int, const double*, double*);
+int dcg_k_solve_lower_trans_launch(cudaStream_t, const double*, int, const double*, double*);
+int dcg_k_jacobi_sweep_launch(cudaStream_t, double*, double*, int, DevStatus*);
+int dcg_rbf_launch(cudaStream_t, const double*, long long, const double*, long long, long long, double, double,
+                   double, int, long long, long long, double*, long long);
+int dcg_derivs_launch(dcg_context*, cudaStream_t, long long, const double*, const double*, const double*, double*,
+                      double*, double*, DevStatus*);
+int dcg_newton_prep_launch(dcg_context*, cudaStream_t, long long, const double*, const double*, const double*,
+                           double*, double*);
+int dcg_newton_a_launch(dcg_context*, cudaStream_t, long long, const double*, const double*, const double*,
+                        double*);
+
+// ---------------------------------------------------------------------------
+// context and workspace
+// ---------------------------------------------------------------------------
+extern "C" int dcg_version(void) { return DCG_ABI_VERSION; }
+
+extern "C" const char* dcg_status_string(int status) {
+    switch (status) {
+        case DCG_OK: return "ok";
+        case DCG_E_DIMENSION: return "dimension mismatch";
+        case DCG_E_NOT_PD: return "non-positive pivot (not positive definite)";
+        case DCG_E_BREAKDOWN: return "non-positive curvature p'Ap <= 0";
+        case DCG_E_GRAM_NOT_SPD: return "W'AW not SPD";
+        case DCG_E_BASIS_DEFICIENT: return "basis deficient";
+        case DCG_E_NO_CONVERGENCE: return "Jacobi eigensolver did not converge";
+        case DCG_E_ASYMMETRIC: return "matrix is not symmetric within tolerance";
+        case DCG_E_CONFIG: return "invalid argument";
+        case DCG_E_CUDA: return dcg_last_cuda_error != cudaSuccess ? cudaGetErrorString(dcg_last_cuda_error)
+                                                                    : "CUDA error";
+        case DCG_E_UNSUPPORTED: return "size outside compiled limits";
+        default: return "unknown status";
+    }
+}
+
+extern "C" int dcg_context_create(int device, dcg_context** out) {
+    if (!out) return DCG_E_CONFIG;
+    *out = nullptr;
+    DCG_CUDA(cudaSetDevice(device));
+    dcg_context* c = new dcg_context();
+    memset(c, 0, sizeof(*c));
+    c->device = device;
+    cudaDeviceProp prop;
+    DCG_CUDA(cudaGetDeviceProperties(&prop, device));
+    c->sm_count = prop.multiProcessorCount;
+    c->smem_optin = prop.sharedMemPerBlockOptin;
+    c->solve_blocks = prop.multiProcessorCount;   // one persistent CTA per SM
+    DCG_CUDA(cudaEventCreate(&c->ev0));
+    DCG_CUDA(cudaEventCreate(&c->ev1));
+    *out = c;
+    return DCG_OK;
+}
+
+extern "C" int dcg_context_destroy(dcg_context* ctx) {
+    if (!ctx) return DCG_OK;
+    cudaDeviceSynchronize();
+    if (ctx->ws) cudaFree(ctx->ws);
+    if (ctx->host) cudaFreeHost(ctx->host);
+    cudaEventDestroy(ctx->ev0);
+    cudaEventDestroy(ctx->ev1);
+    delete ctx;
+    return DCG_OK;
+}
+
+extern "C" int dcg_context_grid(dcg_context* ctx, int* blocks, int* sm_count) {
+    if (!ctx) return DCG_E_CONFIG;
+    if (blocks) *blocks = ctx->solve_blocks;
+    if (sm_count) *sm_count = ctx->sm_count;
+    return DCG_OK;
+}
+
+int dcg_ws_reserve(dcg_context* ctx, size_t bytes) {
+    if (bytes <= ctx->ws_bytes) return DCG_OK;
+    if (ctx->ws) {
+        cudaDeviceSynchronize();   // outstanding work may still use the old buffer
+        cudaFree(ctx->ws);
+        ctx->ws = nullptr;
+        ctx->ws_bytes = 0;
+    }
+    size_t want = bytes + bytes / 4 + (1 << 20);
+    DCG_CUDA(cudaMalloc(&ctx->ws, want));
+    ctx->ws_bytes = want;
+    return DCG_OK;
+}
+
+int dcg_host_reserve(dcg_context* ctx, size_t bytes) {
+    if (bytes <= ctx->host_bytes) return DCG_OK;
+    if (ctx->host) cudaFreeHost(ctx->host);
+    ctx->host = nullptr;
+    DCG_CUDA(cudaMallocHost(&ctx->host, bytes + 4096));
+    ctx->host_bytes = bytes + 4096;
+    return DCG_OK;
+}
+
+// bump allocator over ctx->ws (reserve the total first)
+struct Arena {
+    char* base;
+    size_t off;
+    template <class T>
+    T* take(size_t count) {
+        off = (off + 255) & ~size_t(255);
+        T* p = reinterpret_cast<T*>(base + off);
+        off += sizeof(T) * count;
+        return p;
+    }
+};
+static inline size_t al(size_t bytes) { return (bytes + 255) & ~size_t(255); }
+
+static int read_status(dcg_context* ctx, cudaStream_t st, const DevStatus* dev, DevStatus* out) {
+    int rc = dcg_host_reserve(ctx, sizeof(DevStatus));
+    if (rc) return rc;
+    DevStatus* hs = static_cast<DevStatus*>(ctx->host);
+    DCG_CUDA(cudaMemcpyAsync(hs, dev, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+    DCG_CUDA(cudaStreamSynchronize(st));
+    *out = *hs;
+    return DCG_OK;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ---------------------------------------------------------------------------
+// L0 twins
+// ---------------------------------------------------------------------------
+extern "C" int dcg_k_matvec(dcg_context* ctx, void* stream, const double* d_a, long long m, long long n,
+                            long long lda, const double* d_x, double* d_y) {
+    if (!ctx || m < 0 || n < 0 || lda < n) return DCG_E_CONFIG;
+    if (m == 0) return DCG_OK;
+    if ((lda & 1) || !aligned16(d_a)) return DCG_E_CONFIG;
+    return dcg_gemv_launch(ctx, as_stream(stream), d_a, lda, n, m, d_x, nullptr, nullptr, 0.0, nullptr, d_y);
+}
+
+extern "C" int dcg_k_gemm(dcg_context* ctx, void* stream, const double* d_a, const double* d_b, double* d_c,
+                          long long m, long long kk, long long n) {
+    if (!ctx || m < 0 || kk < 0 || n < 0) return DCG_E_CONFIG;
+    cudaStream_t st = as_stream(stream);
+    if (kk == 0 && m * n > 0) {
+        DCG_CUDA(cudaMemsetAsync(d_c, 0, sizeof(double) * m * n, st));
+        return DCG_OK;
+    }
+    return dcg_gemm_lr(ctx, st, d_a, kk, d_b, n, d_c, n, m, kk, n);
+}
+
+extern "C" int dcg_k_cholesky(dcg_context* ctx, void* stream, const double* d_a, long long n, double pivot_tol,
+                              double* d_l, long long* fail_index) {
+    if (!ctx || n < 0) return DCG_E_CONFIG;
+    cudaStream_t st = as_stream(stream);
+    if (n == 0) {
+        if (fail_index) *fail_index = -1;
+        return DCG_OK;
+    }
+    int rc = dcg_ws_reserve(ctx, sizeof(DevStatus));
+    if (rc) return rc;
+    DevStatus* ds = static_cast<DevStatus*>(ctx->ws);
+    rc = dcg_k_cholesky_launch(st, d_a, (int)n, pivot_tol, d_l, ds);
+    if (rc) return rc;
+    DevStatus hs;
+    rc = read_status(ctx, st, ds, &hs);
+    if (rc) return rc;
+    if (fail_index) *fail_index = hs.info;
+    return DCG_OK;
+}
+
+extern "C" int dcg_k_solve_lower(dcg_context* ctx, void* stream, const double* d_l, long long n, const double* d_b,
+                                 double* d_y) {
+    if (!ctx || n < 0) return DCG_E_CONFIG;
+    if (n == 0) return DCG_OK;
+    return dcg_k_solve_lower_launch(as_stream(stream), d_l, (int)n, d_b, d_y);
+}
+
+extern "C" int dcg_k_solve_lower_trans(dcg_context* ctx, void* stream, const double* d_l, long long n,
+                                       const double* d_b, double* d_x) {
+    if (!ctx || n < 0) return DCG_E_CONFIG;
+    if (n == 0) return DCG_OK;
+    return dcg_k_solve_lower_trans_launch(as_stream(stream), d_l, (int)n, d_b, d_x);
+}
+
+extern "C" int dcg_k_rbf_gram(dcg_context* ctx, void* stream, const double* d_x, long long n, long long dim,
+                              double signal_var, double inv_two_ell2, double jitter, double* d_k, long long ldk,
+                              long long row0, long long rows) {
+    if (!ctx || n < 0 || dim < 0 || ldk < n || row0 < 0 || rows < 0 || row0 + rows > n) return DCG_E_CONFIG;
+    return dcg_rbf_launch(as_stream(stream), d_x, n, d_x, n, dim, signal_var, inv_two_ell2, jitter, 1, row0, rows,
+                          d_k, ldk);
+}
+
+extern "C" int dcg_k_rbf_cross(dcg_context* ctx, void* stream, const double* d_xa, long long na, const double* d_xb,
+                               long long nb, long long dim, double signal_var, double inv_two_ell2, double* d_k) {
+    if (!ctx || na < 0 || nb < 0 || dim < 0) return DCG_E_CONFIG;
+    return dcg_rbf_launch(as_stream(stream), d_xa, na, d_xb, nb, dim, signal_var, inv_two_ell2, 0.0, 0, 0, na, d_k,
+                          nb);
+}
+
+extern "C" int dcg_k_jacobi_sweep(dcg_context* ctx, void* stream, double* d_a, double* d_v, long long n,
+                                  long long* rotations) {
+    if (!ctx || n < 0) return DCG_E_CONFIG;
+    cudaStream_t st = as_stream(stream);
+    if (n == 0) {
+        if (rotations) *rotations = 0;
+        return DCG_OK;
+    }
+    int rc = dcg_ws_reserve(ctx, sizeof(DevStatus));
+    if (rc) return rc;
+    DevStatus* ds = static_cast<DevStatus*>(ctx->ws);
+    rc = dcg_k_jacobi_sweep_launch(st, d_a, d_v, (int)n, ds);
+    if (rc) return rc;
+    DevStatus hs;
+    rc = read_status(ctx, st, ds, &hs);
+    if (rc) return rc;
+    if (rotations) *rotations = hs.count;
+    return DCG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// L1: symmetry check and eigensolvers
+// ---------------------------------------------------------------------------
+#define SYM_T 32
+__global__ void symcheck_kernel(const double* a, long long n, long long lda, unsigned long long* maxes) {
+    __shared__ double t1[SYM_T][SYM_T + 1];
+    __shared__ double t2[SYM_T][SYM_T + 1];
+    const long long I = blockIdx.y, J = blockIdx.x;
+    if (J < I) return;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+    for (int r = ty; r < SYM_T; r += 8) {
+        const long long i1 = I * SYM_T + r, j1 = J * SYM_T + tx;
+        t1[r][tx] = (i1 < n && j1 < n) ? a[i1 * lda + j1] : 0.0;
+        const long long i2 = J * SYM_T + r, j2 = I * SYM_T + tx;
+        t2[r][tx] = (i2 < n && j2 < n) ? a[i2 * lda + j2] : 0.0;
+    }
+    __syncthreads();
+    double dmax = 0.0, amax = 0.0;
+    for (int r = ty; r < SYM_T; r += 8) {
+        const double v = t1[r][tx];
+        const double d = fabs(v - t2[tx][r]);
+        dmax = (d > dmax || d != d) ? d : dmax;
+        const double av = fabs(v), aw = fabs(t2[r][tx]);
+        amax = (av > amax || av != av) ? av : amax;
+        amax = (aw > amax || aw != aw) ? aw : amax;
+    }
+    // non-negative doubles (and NaN) order like their bit patterns
+    atomicMax(&maxes[0], (unsigned long long)__double_as_longlong(dmax));
+    atomicMax(&maxes[1], (unsigned long long)__double_as_longlong(amax));
+}
+
+extern "C" int dcg_check_symmetric(dcg_context* ctx, void* stream, const double* d_a, long long n, long long lda,
+                                   double rtol, int* symmetric) {
+    if (!ctx || !symmetric || n < 0 || lda < n) return DCG_E_CONFIG;
+    *symmetric = 1;
+    if (n == 0) return DCG_OK;
+    cudaStream_t st = as_stream(stream);
+    int rc = dcg_ws_reserve(ctx, 64);
+    if (rc) return rc;
+    unsigned long long* mx = static_cast<unsigned long long*>(ctx->ws);
+    DCG_CUDA(cudaMemsetAsync(mx, 0, 16, st));
+    const long long tiles = (n + SYM_T - 1) / SYM_T;
+    symcheck_kernel<<<dim3((unsigned)tiles, (unsigned)tiles), 256, 0, st>>>(d_a, n, lda, mx);
+    DCG_CUDA(cudaGetLastError());
+    rc = dcg_host_reserve(ctx, 16);
+    if (rc) return rc;
+    unsigned long long* h = static_cast<unsigned long long*>(ctx->host);
+    DCG_CUDA(cudaMemcpyAsync(h, mx, 16, cudaMemcpyDeviceToHost, st));
+    DCG_CUDA(cudaStreamSynchronize(st));
+    double dmax, amax;
+    memcpy(&dmax, &h[0], 8);
+    memcpy(&amax, &h[1], 8);
+    const double scale = amax > 1e-300 ? amax : 1e-300;   // max(scale, 1e-300), linalg.py:53
+    *symmetric = (dmax > rtol * scale) ? 0 : 1;
+    return DCG_OK;
+}
+
+extern "C" int dcg_sym_eigen(dcg_context* ctx, void* stream, const double* d_a, long long n, long long max_sweeps,
+                             double rtol, double* d_values, double* d_vectors, long long* info) {
+    if (!ctx || n < 0) return DCG_E_CONFIG;
+    if (info) *info = 0;
+    if (n == 0) return DCG_OK;
+    if (n > DCG_MAX_T) return DCG_E_UNSUPPORTED;
+    cudaStream_t st = as_stream(stream);
+    int rc = dcg_ws_reserve(ctx, 256);
+    if (rc) return rc;
+    DevStatus* ds = static_cast<DevStatus*>(ctx->ws);
+    DCG_CUDA(cudaMemsetAsync(ds, 0, sizeof(DevStatus), st));
+    rc = dcg_sym_eigen_launch(st, d_a, (int)n, (int)max_sweeps, rtol, d_values, d_vectors, ds);
+    if (rc) return rc;
+    DevStatus hs;
+    rc = read_status(ctx, st, ds, &hs);
+    if (rc) return rc;
+    if (hs.status != DCG_OK && info) *info = hs.info;
+    return hs.status;
+}
+
+extern "C" int dcg_gen_sym_eigen(dcg_context* ctx, void* stream, const double* d_g, const double* d_f, long long n,
+                                 long long max_sweeps, double* d_values, double* d_vectors, long long* info) {
+    if (!ctx || n < 0) return DCG_E_CONFIG;
+    if (info) *info = 0;
+    if (n == 0) return DCG_OK;
+    if (n > DCG_MAX_T) return DCG_E_UNSUPPORTED;
+    cudaStream_t st = as_stream(stream);
+    int rc = dcg_ws_reserve(ctx, al(sizeof(DevStatus)) + al(sizeof(double) * 2 * n * n));
+    if (rc) return rc;
+    Arena ar{static_cast<char*>(ctx->ws), 0};
+    DevStatus* ds = ar.take<DevStatus>(1);
+    double* wk = ar.take<double>(2 * n * n);
+    DCG_CUDA(cudaMemsetAsync(ds, 0, sizeof(DevStatus), st));
+    rc = dcg_gen_sym_eigen_launch(st, d_g, d_f, (int)n, (int)max_sweeps, wk, d_values, d_vectors, ds);
+    if (rc) return rc;
+    DevStatus hs;
+    rc = read_status(ctx, st, ds, &hs);
+    if (rc) return rc;
+    if (hs.status != DCG_OK && info) *info = hs.info;
+    return hs.status;
+}
+
+// ---------------------------------------------------------------------------
+// L2: operator application
+// ---------------------------------------------------------------------------
+static int check_dense_op(const dcg_operator* op) {
+    if (!op) return DCG_E_CONFIG;
+    if (op->kind != DCG_OP_DENSE) return DCG_E_UNSUPPORTED;
+    if (op->n < 0 || op->row0 < 0 || op->rows < 0 || op->row0 + op->rows > op->n) return DCG_E_CONFIG;
+    if (op->ldk < op->n || (op->ldk & 1) || !aligned16(op->d_k)) return DCG_E_CONFIG;
+    return DCG_OK;
+}
+
+extern "C" int dcg_op_apply(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_x,
+                            double* d_y) {
+    if (!ctx) return DCG_E_CONFIG;
+    int rc = check_dense_op(op);
+    if (rc) return rc;
+    const double* s_out = op->d_s ? op->d_s + op->row0 : nullptr;
+    return dcg_gemv_launch(ctx, as_stream(stream), op->d_k, op->ldk, op->n, op->rows, d_x, op->d_s, s_out,
+                           op->shift, d_x + op->row0, d_y);
+}
+
+extern "C" int dcg_op_apply_block(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_x,
+                                  long long k, double* d_y) {
+    if (!ctx || k < 0) return DCG_E_CONFIG;
+    int rc = check_dense_op(op);
+    if (rc) return rc;
+    if (k == 0) return DCG_OK;
+    if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
+    rc = dcg_ws_reserve(ctx, sizeof(double) * dcg_block_apply_scratch_doubles(op->n, op->rows, (int)k) + 256);
+    if (rc) return rc;
+    const double* s_out = op->d_s ? op->d_s + op->row0 : nullptr;
+    return dcg_block_apply(ctx, as_stream(stream), op->d_k, op->ldk, op->rows, op->n, d_x, (int)k, op->d_s, s_out,
+                           op->shift, d_x + op->row0 * k, d_y, static_cast<double*>(ctx->ws));
+}
+
+// ---------------------------------------------------------------------------
+// Gram factor / basis refresh
+// ---------------------------------------------------------------------------
+__global__ void gather_cols_kernel(const double* src, long long n, int k, const int* cols, int kk, double* dst) {
+    const long long total = n * kk;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long i = e / kk;
+        const int c = (int)(e % kk);
+        dst[e] = src[i * k + cols[c]];
+    }
+}
+
+// Gram = W'AW -> (sym) -> Cholesky [-> prune].  Writes L (k_out x k_out) and
+// the surviving column list (device ints) and returns k_out via *k_out.
+static int gram_core(dcg_context* ctx, cudaStream_t st, const double* W, const double* AW, long long n, int k,
+                     int prune, double* L_out, int* d_active, long long* k_out, long long* info, Arena& ar) {
+    double* graw = ar.take<double>((size_t)k * k);
+    double* gsym = ar.take<double>((size_t)k * k);
+    double* lwork = ar.take<double>((size_t)2 * k * k);
+    double* parts = ar.take<double>(dcg_xty_scratch_doubles(ctx, k, k));
+    DevStatus* ds = ar.take<DevStatus>(1);
+    DCG_CUDA(cudaMemsetAsync(ds, 0, sizeof(DevStatus), st));
+    int rc = dcg_xty(ctx, st, W, k, AW, k, n, k, k, graw, parts);
+    if (rc) return rc;
+    rc = dcg_gram_factor_launch(st, graw, k, prune, gsym, lwork, d_active, ds);
+    if (rc) return rc;
+    DevStatus hs;
+    rc = read_status(ctx, st, ds, &hs);
+    if (rc) return rc;
+    if (hs.status != DCG_OK) {
+        if (info) *info = hs.info;
+        return hs.status;
+    }
+    const long long kk = hs.count;
+    DCG_CUDA(cudaMemcpyAsync(L_out, lwork, sizeof(double) * kk * kk, cudaMemcpyDeviceToDevice, st));
+    *k_out = kk;
+    return DCG_OK;
+}
+
+static size_t gram_scratch_bytes(dcg_context* ctx, int k) {
+    return al(sizeof(double) * k * k) * 2 + al(sizeof(double) * 2 * k * k) +
+           al(sizeof(double) * dcg_xty_scratch_doubles(ctx, k, k)) + al(sizeof(DevStatus)) + al(sizeof(int) * 64) +
+           4096;
+}
+
+// RecycleBasis.ensure_factored (solvers.py:107-115): no pruning, GramNotSpd.
+extern "C" int dcg_gram_factor(dcg_context* ctx, void* stream, double* d_w, double* d_aw, long long n, long long k,
+                               int prune, double* d_chol, long long* k_out, long long* info) {
+    if (!ctx || n < 0 || k < 0) return DCG_E_CONFIG;
+    if (info) *info = 0;
+    if (k_out) *k_out = k;
+    if (k == 0) return DCG_OK;
+    if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
+    cudaStream_t st = as_stream(stream);
+    const size_t nk = sizeof(double) * n * k;
+    int rc = dcg_ws_reserve(ctx, gram_scratch_bytes(ctx, (int)k) + (prune ? 2 * al(nk) : 0));
+    if (rc) return rc;
+    Arena ar{static_cast<char*>(ctx->ws), 0};
+    int* active = ar.take<int>(DCG_MAX_K);
+    long long kk = k;
+    rc = gram_core(ctx, st, d_w, d_aw, n, (int)k, prune, d_chol, active, &kk, info, ar);
+    if (rc) return rc;
+    if (prune && kk != k) {
+        // compact W and AW in place through scratch copies
+        double* wtmp = ar.take<double>(n * k);
+        double* awtmp = ar.take<double>(n * k);
+        DCG_CUDA(cudaMemcpyAsync(wtmp, d_w, nk, cudaMemcpyDeviceToDevice, st));
+        DCG_CUDA(cudaMemcpyAsync(awtmp, d_aw, nk, cudaMemcpyDeviceToDevice, st));
+        gather_cols_kernel<<<ctx->sm_count * 2, 256, 0, st>>>(wtmp, n, (int)k, active, (int)kk, d_w);
+        gather_cols_kernel<<<ctx->sm_count * 2, 256, 0, st>>>(awtmp, n, (int)k, active, (int)kk, d_aw);
+        DCG_CUDA(cudaGetLastError());
+    }
+    if (k_out) *k_out = kk;
+    DCG_CUDA(cudaStreamSynchronize(st));
+    return DCG_OK;
+}
+
+// refresh_basis (recycle.py:80-92): AW = A W, then pruning Gram factorisation.
+// d_w_out / d_aw_out receive n x k_out compacted columns.
+extern "C" int dcg_refresh_basis(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_w,
+                                 long long k, double* d_w_out, double* d_aw_out, double* d_chol, long long* k_out,
+                                 long long* info) {
+    if (!ctx || k < 0) return DCG_E_CONFIG;
+    if (info) *info = 0;
+    int rc = check_dense_op(op);
+    if (rc) return rc;
+    if (op->row0 != 0 || op->rows != op->n) return DCG_E_UNSUPPORTED;
+    const long long n = op->n;
+    if (k_out) *k_out = k;
+    if (k == 0) return DCG_OK;
+    if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
+    cudaStream_t st = as_stream(stream);
+    const size_t nk = sizeof(double) * n * k;
+    const size_t need = al(sizeof(double) * dcg_block_apply_scratch_doubles(n, n, (int)k)) + al(nk) +
+                        gram_scratch_bytes(ctx, (int)k);
+    rc = dcg_ws_reserve(ctx, need);
+    if (rc) return rc;
+    Arena ar{static_cast<char*>(ctx->ws), 0};
+    double* aw = ar.take<double>(n * k);
+    int* active = ar.take<int>(DCG_MAX_K);
+    double* scratch = ar.take<double>(dcg_block_apply_scratch_doubles(n, n, (int)k));
+    rc = dcg_block_apply(ctx, st, op->d_k, op->ldk, n, n, d_w, (int)k, op->d_s, op->d_s, op->shift, d_w, aw, scratch);
+    if (rc) return rc;
+    long long kk = k;
+    rc = gram_core(ctx, st, d_w, aw, n, (int)k, 1, d_chol, active, &kk, info, ar);
+    if (rc) return rc;
+    if (kk == k) {
+        DCG_CUDA(cudaMemcpyAsync(d_w_out, d_w, nk, cudaMemcpyDeviceToDevice, st));
+        DCG_CUDA(cudaMemcpyAsync(d_aw_out, aw, nk, cudaMemcpyDeviceToDevice, st));
+    } else {
+        gather_cols_kernel<<<ctx->sm_count * 2, 256, 0, st>>>(d_w, n, (int)k, active, (int)kk, d_w_out);
+        gather_cols_kernel<<<ctx->sm_count * 2, 256, 0, st>>>(aw, n, (int)k, active, (int)kk, d_aw_out);
+        DCG_CUDA(cudaGetLastError());
+    }
+    if (k_out) *k_out = kk;
+    DCG_CUDA(cudaStreamSynchronize(st));
+    return DCG_OK;
+}
+
+// P_W v = v - AW (W'AW)^-1 W' v   (solvers.py:242-256)
+__global__ void project_kernel(long long n, int k, const double* L, const double* c, const double* v,
+                               const double* AW, double* out) {
+    __shared__ double y[DCG_MAX_K];
+    if (threadIdx.x == 0 && blockIdx.x >= 0) {
+        // forward / back substitution (k <= 64), reference order
+        double t[DCG_MAX_K];
+        for (int i = 0; i < k; ++i) {
+            double acc = c[i];
+            for (int j = 0; j < i; ++j) acc = sub_rn(acc, mul_rn(L[i * k + j], t[j]));
+            t[i] = div_rn(acc, L[i * k + i]);
+        }
+        for (int i = k - 1; i >= 0; --i) {
+            double acc = t[i];
+            for (int j = i + 1; j < k; ++j) acc = sub_rn(acc, mul_rn(L[j * k + i], y[j]));
+            y[i] = div_rn(acc, L[i * k + i]);
+        }
+    }
+    __syncthreads();
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int j = 0; j < k; ++j) acc = fma(AW[i * k + j], y[j], acc);
+        out[i] = sub_rn(v[i], acc);
+    }
+}
+
+extern "C" int dcg_deflation_project(dcg_context* ctx, void* stream, long long n, const dcg_basis* basis,
+                                     const double* d_v, double* d_out) {
+    if (!ctx || n < 0) return DCG_E_CONFIG;
+    cudaStream_t st = as_stream(stream);
+    const long long k = basis ? basis->k : 0;
+    if (k == 0) {
+        if (n) DCG_CUDA(cudaMemcpyAsync(d_out, d_v, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        return DCG_OK;
+    }
+    if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
+    int rc = dcg_ws_reserve(ctx, al(sizeof(double) * k) + al(sizeof(double) * dcg_xty_scratch_doubles(ctx, (int)k, 1)));
+    if (rc) return rc;
+    Arena ar{static_cast<char*>(ctx->ws), 0};
+    double* c = ar.take<double>(k);
+    double* parts = ar.take<double>(dcg_xty_scratch_doubles(ctx, (int)k, 1));
+    rc = dcg_xty(ctx, st, basis->d_w, k, d_v, 1, n, (int)k, 1, c, parts);
+    if (rc) return rc;
+    project_kernel<<<ctx->sm_count, 256, 0, st>>>(n, (int)k, basis->d_chol, c, d_v, basis->d_aw, d_out);
+    DCG_CUDA(cudaGetLastError());
+    return DCG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// L3: harmonic Ritz extraction (recycle.py:95-159)
+// ---------------------------------------------------------------------------
+// column c of Z: prev W column (c < kp) or log p_{c-kp}; sum of squares per CTA
+__global__ void zcol_norm_kernel(long long n, int kp, const double* Wp, int m, const double* P, double* part) {
+    const int T = kp + m;
+    const long long r0 = part_begin(n, gridDim.x, blockIdx.x), r1 = part_begin(n, gridDim.x, blockIdx.x + 1);
+    for (int c = threadIdx.x; c < T; c += blockDim.x) {
+        double acc = 0.0;
+        if (c < kp)
+            for (long long i = r0; i < r1; ++i) acc = fma(Wp[i * kp + c], Wp[i * kp + c], acc);
+        else
+            for (long long i = r0; i < r1; ++i) {
+                const double v = P[(long long)(c - kp) * n + i];
+                acc = fma(v, v, acc);
+            }
+        part[(long long)blockIdx.x * T + c] = acc;
+    }
+}
+
+// keep = norms > 0 (fixed order), Tk in st->count
+__global__ void zplan_kernel(const double* part, int nb, int T, double* norms, int* keep, DevStatus* st) {
+    __shared__ double nrm[DCG_MAX_T];
+    for (int c = threadIdx.x; c < T; c += blockDim.x) {
+        double acc = 0.0;
+        for (int b = 0; b < nb; ++b) acc += part[(long long)b * T + c];
+        nrm[c] = sqrt(acc);
+        norms[c] = nrm[c];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int c = 0; c < T; ++c)
+            if (nrm[c] > 0.0) keep[t++] = c;
+        st->status = DCG_OK;
+        st->count = t;
+    }
+}
+
+// Zs[i][c'] = z[i][keep c'] / norm ; AZs likewise with az = (r_j - r_{j+1}) / alpha_j
+__global__ void zbuild_kernel(long long n, int kp, const double* Wp, const double* AWp, const double* P,
+                              const double* R, const double* alpha, const double* norms, const int* keep, int Tk,
+                              double* Zs, double* AZs) {
+    const long long total = n * Tk;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long i = e / Tk;
+        const int cc = (int)(e % Tk);
+        const int c = keep[cc];
+        const double nv = norms[c];
+        double z, az;
+        if (c < kp) {
+            z = Wp[i * kp + c];
+            az = AWp[i * kp + c];
+        } else {
+            const int j = c - kp;
+            z = P[(long long)j * n + i];
+            az = div_rn(sub_rn(R[(long long)j * n + i], R[(long long)(j + 1) * n + i]), alpha[j]);
+        }
+        Zs[e] = div_rn(z, nv);
+        AZs[e] = div_rn(az, nv);
+    }
+}
+
+// Uexp (Tk x k): rows of the surviving columns get U, pruned rows zero
+__global__ void uexpand_kernel(const double* U, const int* active, int na, int Tk, int k, double* Uexp) {
+    for (int e = threadIdx.x; e < Tk * k; e += blockDim.x) Uexp[e] = 0.0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < na * k; e += blockDim.x) {
+        const int r = e / k, j = e % k;
+        Uexp[active[r] * k + j] = U[e];
+    }
+}
+
+__global__ void colnorm_part_kernel(const double* V, long long n, int k, double* part) {
+    const long long r0 = part_begin(n, gridDim.x, blockIdx.x), r1 = part_begin(n, gridDim.x, blockIdx.x + 1);
+    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+        double acc = 0.0;
+        for (long long i = r0; i < r1; ++i) acc = fma(V[i * k + c], V[i * k + c], acc);
+        part[(long long)blockIdx.x * k + c] = acc;
+    }
+}
+
+// u[:, j] /= ||Z u_j|| when positive (recycle.py:150-153), on Uexp and U
+__global__ void uscale_kernel(const double* part, int nb, int k, double* Uexp, int Tk, double* U, int na) {
+    __shared__ double sc[DCG_MAX_K];
+    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+        double acc = 0.0;
+        for (int b = 0; b < nb; ++b) acc += part[(long long)b * k + c];
+        sc[c] = sqrt(acc);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < Tk * k; e += blockDim.x) {
+        const double s = sc[e % k];
+        if (s > 0.0) Uexp[e] = div_rn(Uexp[e], s);
+    }
+    for (int e = threadIdx.x; e < na * k; e += blockDim.x) {
+        const double s = sc[e % k];
+        if (s > 0.0) U[e] = div_rn(U[e], s);
+    }
+}
+
+extern "C" int dcg_ritz_extract(dcg_context* ctx, void* stream, long long n, const dcg_krylov_log* log, long long m,
+                                const dcg_basis* prev, long long k, int selection, double* d_theta, double* d_u,
+                                double* d_z, double* d_w_next, double* d_aw_next, long long* t_out,
+                                long long* info) {
+    if (!ctx || n < 0 || m < 0 || k < 0) return DCG_E_CONFIG;
+    if (selection != DCG_SELECT_SMALLEST && selection != DCG_SELECT_LARGEST) return DCG_E_CONFIG;
+    if (info) *info = 0;
+    const long long kp = prev ? prev->k : 0;
+    const long long T = kp + m;
+    if (t_out) *t_out = T;
+    if (k > T) {   // recycle.py:104-108
+        if (info) *info = T;
+        return DCG_E_BASIS_DEFICIENT;
+    }
+    if (k == 0) return DCG_OK;
+    if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
+    if (T > DCG_MAX_T) return DCG_E_UNSUPPORTED;
+    if (m > 0 && (!log || log->ell < m || !log->d_p || !log->d_r || !log->d_alpha)) return DCG_E_CONFIG;
+    cudaStream_t st = as_stream(stream);
+    const int nb = ctx->sm_count;
+    const size_t nT = (size_t)n * T;
+    const size_t need = al(sizeof(double) * nT) * 2 + al(sizeof(double) * (size_t)nb * T) * 2 +
+                        al(sizeof(double) * T * T) * 2 + al(sizeof(double) * dcg_xty_scratch_doubles(ctx, T, T)) +
+                        al(sizeof(double) * 5 * T * T) + al(sizeof(double) * T * k) * 2 + al(sizeof(double) * n * k) +
+                        al(sizeof(double) * T) + al(sizeof(int) * T) * 2 + al(sizeof(DevStatus)) * 2 + 8192;
+    int rc = dcg_ws_reserve(ctx, need);
+    if (rc) return rc;
+    Arena ar{static_cast<char*>(ctx->ws), 0};
+    double* Zs = ar.take<double>(nT);
+    double* AZs = ar.take<double>(nT);
+    double* part = ar.take<double>((size_t)nb * T);
+    double* norms = ar.take<double>(T);
+    int* keep = ar.take<int>(T);
+    int* active = ar.take<int>(T);
+    double* Fraw = ar.take<double>(T * T);
+    double* Graw = ar.take<double>(T * T);
+    double* xparts = ar.take<double>(dcg_xty_scratch_doubles(ctx, T, T));
+    double* wk = ar.take<double>(5 * T * T);
+    double* U = ar.take<double>(T * k);
+    double* Uexp = ar.take<double>(T * k);
+    double* V = ar.take<double>(n * k);
+    double* part2 = ar.take<double>((size_t)nb * T);
+    DevStatus* ds = ar.take<DevStatus>(1);
+    DevStatus* ds2 = ar.take<DevStatus>(1);
+    DCG_CUDA(cudaMemsetAsync(ds, 0, 2 * al(sizeof(DevStatus)), st));
+    const double* Wp = kp ? prev->d_w : nullptr;
+    const double* AWp = kp ? prev->d_aw : nullptr;
+    const double* P = m ? log->d_p : nullptr;
+    const double* R = m ? log->d_r : nullptr;
+    const double* alpha = m ? log->d_alpha : nullptr;
+
+    zcol_norm_kernel<<<nb, 128, 0, st>>>(n, (int)kp, Wp, (int)m, P, part);
+    DCG_CUDA(cudaGetLastError());
+    zplan_kernel<<<1, 128, 0, st>>>(part, nb, (int)T, norms, keep, ds);
+    DCG_CUDA(cudaGetLastError());
+    DevStatus hs;
+    rc = read_status(ctx, st, ds, &hs);
+    if (rc) return rc;
+    const int Tk = (int)hs.count;
+    if (Tk < k) {   // first check of the pruning loop (recycle.py:131-132)
+        if (info) *info = Tk;
+        if (t_out) *t_out = Tk;
+        return DCG_E_BASIS_DEFICIENT;
+    }
+    zbuild_kernel<<<nb * 4, 256, 0, st>>>(n, (int)kp, Wp, AWp, P, R, alpha, norms, keep, Tk, Zs, AZs);
+    DCG_CUDA(cudaGetLastError());
+    rc = dcg_xty(ctx, st, AZs, Tk, Zs, Tk, n, Tk, Tk, Fraw, xparts);
+    if (rc) return rc;
+    rc = dcg_xty(ctx, st, AZs, Tk, AZs, Tk, n, Tk, Tk, Graw, xparts);
+    if (rc) return rc;
+    rc = dcg_ritz_pencil_launch(st, Fraw, Graw, Tk, (int)k, selection == DCG_SELECT_LARGEST, 60, wk,
+                                d_theta, U, active, ds2);
+    if (rc) return rc;
+    rc = read_status(ctx, st, ds2, &hs);
+    if (rc) return rc;
+    if (hs.status != DCG_OK) {
+        if (info) *info = hs.info;
+        if (t_out) *t_out = hs.count;
+        return hs.status;
+    }
+    const int na = (int)hs.count;
+    uexpand_kernel<<<1, 256, 0, st>>>(U, active, na, Tk, (int)k, Uexp);
+    DCG_CUDA(cudaGetLastError());
+    rc = dcg_gemm_lr(ctx, st, Zs, Tk, Uexp, k, V, k, n, Tk, k);
+    if (rc) return rc;
+    colnorm_part_kernel<<<nb, 64, 0, st>>>(V, n, (int)k, part2);
+    DCG_CUDA(cudaGetLastError());
+    uscale_kernel<<<1, 256, 0, st>>>(part2, nb, (int)k, Uexp, Tk, U, na);
+    DCG_CUDA(cudaGetLastError());
+    rc = dcg_gemm_lr(ctx, st, Zs, Tk, Uexp, k, d_w_next, k, n, Tk, k);
+    if (rc) return rc;
+    rc = dcg_gemm_lr(ctx, st, AZs, Tk, Uexp, k, d_aw_next, k, n, Tk, k);
+    if (rc) return rc;
+    if (d_u) DCG_CUDA(cudaMemcpyAsync(d_u, U, sizeof(double) * na * k, cudaMemcpyDeviceToDevice, st));
+    if (d_z) {
+        // z keeps the surviving columns only: gather by active (indices into Zs)
+        gather_cols_kernel<<<nb * 2, 256, 0, st>>>(Zs, n, Tk, active, na, d_z);
+        DCG_CUDA(cudaGetLastError());
+    }
+    if (t_out) *t_out = na;
+    DCG_CUDA(cudaStreamSynchronize(st));
+    return DCG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// L4: GPC glue
+// ---------------------------------------------------------------------------
+extern "C" int dcg_gpc_derivs(dcg_context* ctx, void* stream, long long n, const double* d_f, const double* d_y,
+                              double* d_grad, double* d_h, double* loglik) {
+    if (!ctx || n < 0) return DCG_E_CONFIG;
+    cudaStream_t st = as_stream(stream);
+    const size_t need = al(sizeof(double) * 2 * ctx->sm_count * 2) + al(sizeof(DevStatus));
+    int rc = dcg_ws_reserve(ctx, need);
+    if (rc) return rc;
+    Arena ar{static_cast<char*>(ctx->ws), 0};
+    double* part = ar.take<double>(4 * ctx->sm_count);
+    DevStatus* ds = ar.take<DevStatus>(1);
+    rc = dcg_derivs_launch(ctx, st, n, d_f, d_y, nullptr, d_grad, d_h, part, ds);
+    if (rc) return rc;
+    DevStatus hs;
+    rc = read_status(ctx, st, ds, &hs);
+    if (rc) return rc;
+    if (loglik) *loglik = hs.value;
+    return DCG_OK;
+}
+
+extern "C" int dcg_gpc_newton_system(dcg_context* ctx, void* stream, const dcg_operator* kop, const double* d_f,
+                                     const double* d_grad, const double* d_h, double* d_s, double* d_inner,
+                                     double* d_b) {
+    if (!ctx) return DCG_E_CONFIG;
+    int rc = check_dense_op(kop);
+    if (rc) return rc;
+    cudaStream_t st = as_stream(stream);
+    const long long n = kop->n;
+    rc = dcg_newton_prep_launch(ctx, st, n, d_f, d_grad, d_h, d_s, d_inner);
+    if (rc) return rc;
+    // b = s (.) (K inner): K's own scaling/shift are ignored here (K is the kernel matrix)
+    return dcg_gemv_launch(ctx, st, kop->d_k, kop->ldk, n, kop->rows, d_inner, nullptr, d_s + kop->row0, 0.0,
+                           nullptr, d_b);
+}
+
+extern "C" int dcg_gpc_newton_update(dcg_context* ctx, void* stream, const dcg_operator* kop, const double* d_inner,
+                                     const double* d_s, const double* d_x, const double* d_y, double* d_a,
+                                     double* d_f, double* d_grad, double* d_h, double* loglik, double* psi) {
+    if (!ctx) return DCG_E_CONFIG;
+    int rc = check_dense_op(kop);
+    if (rc) return rc;
+    if (kop->row0 != 0 || kop->rows != kop->n) return DCG_E_UNSUPPORTED;
+    cudaStream_t st = as_stream(stream);
+    const long long n = kop->n;
+    const size_t need = al(sizeof(double) * 2 * ctx->sm_count * 2) + al(sizeof(DevStatus));
+    rc = dcg_ws_reserve(ctx, need);
+    if (rc) return rc;
+    Arena ar{static_cast<char*>(ctx->ws), 0};
+    double* part = ar.take<double>(4 * ctx->sm_count);
+    DevStatus* ds = ar.take<DevStatus>(1);
+    rc = dcg_newton_a_launch(ctx, st, n, d_inner, d_s, d_x, d_a);
+    if (rc) return rc;
+    rc = dcg_gemv_launch(ctx, st, kop->d_k, kop->ldk, n, n, d_a, nullptr, nullptr, 0.0, nullptr, d_f);
+    if (rc) return rc;
+    rc = dcg_derivs_launch(ctx, st, n, d_f, d_y, d_a, d_grad, d_h, part, ds);
+    if (rc) return rc;
+    DevStatus hs;
+    rc = read_status(ctx, st, ds, &hs);
+    if (rc) return rc;
+    if (loglik) *loglik = hs.value;
+    if (psi) *psi = hs.value2;
+    return DCG_OK;
+}

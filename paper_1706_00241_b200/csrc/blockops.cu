@@ -1,0 +1,382 @@
+// Operator application and block products.
+//
+//   gemv_kernel      y = shift v + s_out (.) K (s_in (.) v)   (K1, standalone)
+//   dmma_gemm_kernel Y = K V on FP64 tensor cores            (K3, A.W refresh, recycle.py:90)
+//   xty_kernel       C = X' Y tall-skinny products           (K4, W'AW, F, G; solvers.py:109,
+//                                                              recycle.py:71,133-136)
+//   gemm_lr_kernel   C = A B with the reference's i-k-j order (K4, Z.U; _core.pyx:31-44)
+#include "common.cuh"
+#include "gemv.cuh"
+
+// =============================================================================
+// K1 standalone GEMV: one CTA per contiguous row range (grid = #SM).
+// =============================================================================
+__global__ void __launch_bounds__(DCG_NT, 1)
+    gemv_kernel(const double* __restrict__ K, long long ldk, long long n, long long rows,
+                const double* v, const double* s_in, const double* s_out, double shift,
+                const double* v_rows, double* y) {
+    extern __shared__ __align__(16) double smem[];
+    const int xt = (int)min(n, (long long)DCG_QT) + 2;
+    double* s_x = smem;
+    double* s_red = s_x + xt;
+    const long long r0 = part_begin(rows, gridDim.x, blockIdx.x);
+    const long long r1 = part_begin(rows, gridDim.x, blockIdx.x + 1);
+    block_gemv<false>(K, ldk, n, v, s_in, r0, r1, s_x, s_red, [&](long long i, double t) {
+        double val = s_out ? mul_rn(s_out[i], t) : t;
+        if (shift != 0.0) val = add_rn(mul_rn(shift, v_rows[i]), val);
+        y[i] = val;
+    });
+}
+
+static size_t gemv_smem(long long n) {
+    const long long xt = (n < DCG_QT ? n : DCG_QT) + 2;
+    return sizeof(double) * (size_t)(xt + DCG_NW * DCG_RB);
+}
+
+int dcg_gemv_launch(dcg_context* ctx, cudaStream_t st, const double* K, long long ldk, long long n,
+                    long long rows, const double* v, const double* s_in, const double* s_out,
+                    double shift, const double* v_rows, double* y) {
+    if (rows <= 0) return DCG_OK;
+    if ((ldk & 1) || (reinterpret_cast<uintptr_t>(K) & 15)) return DCG_E_CONFIG;
+    const size_t smem = gemv_smem(n);
+    DCG_CUDA(cudaFuncSetAttribute(gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    long long blocks = ctx->sm_count;
+    if (blocks > rows) blocks = rows;
+    gemv_kernel<<<(unsigned)blocks, DCG_NT, smem, st>>>(K, ldk, n, rows, v, s_in, s_out, shift, v_rows, y);
+    DCG_CUDA(cudaGetLastError());
+    return DCG_OK;
+}
+
+// =============================================================================
+// K3: Y(rows x k) = K(rows x n) V(n x k) with mma.sync.m8n8k4 FP64.
+// CTA = 8 warps = 64 rows x all k columns; blockIdx.y splits the inner
+// dimension (partials reduced in a fixed order by yscale_reduce_kernel).
+// Operand tiles are staged with cp.async double buffering; the inner index is
+// permuted inside each 8-chunk (thread loads a 16-byte pair for two MMAs),
+// which leaves every dot product unchanged.
+// =============================================================================
+#define GM_BM 64
+#define GM_BK 32
+#define GM_SA (GM_BK + 4)        // A row stride (doubles): conflict-free 16 B fragment loads
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, int src_bytes) {
+    const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gsrc),
+                 "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <int NTILE>
+__global__ void __launch_bounds__(256)
+    dmma_gemm_kernel(const double* __restrict__ K, long long ldk, long long rows, long long n,
+                     const double* __restrict__ V, int kcols, long long split_cols, double* P) {
+    constexpr int KP = NTILE * 8;          // padded k
+    constexpr int SB = KP + 4;             // B row stride
+    extern __shared__ __align__(16) double sm[];
+    double* sA = sm;                       // 2 x GM_BM x GM_SA
+    double* sB = sA + 2 * GM_BM * GM_SA;   // 2 x GM_BK x SB
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const long long row0 = (long long)blockIdx.x * GM_BM;
+    const long long cbeg = (long long)blockIdx.y * split_cols;
+    long long cend = cbeg + split_cols;
+    if (cend > n) cend = n;
+    const int ntiles = (int)((cend - cbeg + GM_BK - 1) / GM_BK);
+
+    auto load_tile = [&](int buf, long long c0) {
+        double* a = sA + buf * GM_BM * GM_SA;
+        // A: 64 rows x 32 cols = 1024 16-byte chunks
+        for (int ch = tid; ch < GM_BM * (GM_BK / 2); ch += 256) {
+            const int r = ch / (GM_BK / 2), cc = (ch % (GM_BK / 2)) * 2;
+            const long long gr = row0 + r, gc = c0 + cc;
+            int bytes = 0;
+            const double* src = K;
+            if (gr < rows && gc < cend) {
+                bytes = (gc + 1 < cend) ? 16 : 8;
+                src = K + gr * ldk + gc;
+            }
+            cp_async16(a + r * GM_SA + cc, src, bytes);
+        }
+        double* bsm = sB + buf * GM_BK * SB;
+        // B: 32 rows x KP cols (kcols valid)
+        for (int ch = tid; ch < GM_BK * (KP / 2); ch += 256) {
+            const int r = ch / (KP / 2), cc = (ch % (KP / 2)) * 2;
+            const long long gr = c0 + r;
+            int bytes = 0;
+            const double* src = V;
+            if (gr < cend && cc < kcols) {
+                bytes = (cc + 1 < kcols) ? 16 : 8;
+                src = V + gr * kcols + cc;
+            }
+            // V rows are kcols long; 16-byte alignment needs kcols even (checked on host)
+            cp_async16(bsm + r * SB + cc, src, bytes);
+        }
+    };
+
+    double acc[NTILE][2];
+#pragma unroll
+    for (int j = 0; j < NTILE; ++j) acc[j][0] = acc[j][1] = 0.0;
+
+    if (ntiles > 0) {
+        load_tile(0, cbeg);
+        cp_async_commit();
+    }
+    for (int tI = 0; tI < ntiles; ++tI) {
+        const int buf = tI & 1;
+        if (tI + 1 < ntiles) {
+            load_tile(buf ^ 1, cbeg + (long long)(tI + 1) * GM_BK);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double* a = sA + buf * GM_BM * GM_SA + (warp * 8 + g) * GM_SA;
+        const double* bsm = sB + buf * GM_BK * SB;
+#pragma unroll
+        for (int kk = 0; kk < GM_BK / 8; ++kk) {
+            const double2 av = *reinterpret_cast<const double2*>(a + kk * 8 + 2 * t);
+            const double* b0 = bsm + (kk * 8 + 2 * t) * SB + g;
+#pragma unroll
+            for (int j = 0; j < NTILE; ++j) {
+                dmma(acc[j][0], acc[j][1], av.x, b0[j * 8]);
+                dmma(acc[j][0], acc[j][1], av.y, b0[SB + j * 8]);
+            }
+        }
+        __syncthreads();
+    }
+    // D fragment: row = g, cols 2t, 2t+1 of each n-tile
+    const long long r = row0 + warp * 8 + g;
+    if (r < rows) {
+        double* out = P + ((long long)blockIdx.y * rows + r) * kcols;
+#pragma unroll
+        for (int j = 0; j < NTILE; ++j) {
+            const int c = j * 8 + 2 * t;
+            if (c < kcols) out[c] = acc[j][0];
+            if (c + 1 < kcols) out[c + 1] = acc[j][1];
+        }
+    }
+}
+
+// V = s (.) X  (row scaling of an n x k block)
+__global__ void rowscale_kernel(const double* X, const double* s, long long n, int k, double* V) {
+    const long long total = n * k;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long i = e / k;
+        V[e] = s ? mul_rn(s[i], X[e]) : X[e];
+    }
+}
+
+// Y[i][j] = shift X[i][j] + s_out[i] * sum_split P[split][i][j]   (fixed split order)
+__global__ void yscale_reduce_kernel(const double* P, int splits, long long rows, int k,
+                                     const double* X_rows, const double* s_out, double shift,
+                                     double* Y) {
+    const long long total = rows * k;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        double acc = P[e];
+        for (int sp = 1; sp < splits; ++sp) acc += P[(long long)sp * total + e];
+        const long long i = e / k;
+        double val = s_out ? mul_rn(s_out[i], acc) : acc;
+        if (shift != 0.0) val = add_rn(mul_rn(shift, X_rows[e]), val);
+        Y[e] = val;
+    }
+}
+
+template <int NTILE>
+static int launch_dmma(dcg_context* ctx, cudaStream_t st, const double* K, long long ldk,
+                       long long rows, long long n, const double* V, int k, double* P,
+                       int& splits_out) {
+    constexpr int KP = NTILE * 8;
+    const size_t smem = sizeof(double) * (size_t)(2 * GM_BM * GM_SA + 2 * GM_BK * (KP + 4));
+    DCG_CUDA(cudaFuncSetAttribute(dmma_gemm_kernel<NTILE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    int per_sm = 0;
+    DCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmma_gemm_kernel<NTILE>, 256, smem));
+    if (per_sm < 1) per_sm = 1;
+    const long long row_tiles = (rows + GM_BM - 1) / GM_BM;
+    const long long target = 2LL * per_sm * ctx->sm_count;          // ~2 waves
+    long long splits = (target + row_tiles - 1) / row_tiles;
+    const long long max_splits = (n + GM_BK - 1) / GM_BK;
+    if (splits > max_splits) splits = max_splits;
+    if (splits > 64) splits = 64;
+    if (splits < 1) splits = 1;
+    long long split_cols = (n + splits - 1) / splits;
+    split_cols = (split_cols + GM_BK - 1) / GM_BK * GM_BK;
+    splits = (n + split_cols - 1) / split_cols;
+    splits_out = (int)splits;
+    dim3 grid((unsigned)row_tiles, (unsigned)splits);
+    dmma_gemm_kernel<NTILE><<<grid, 256, smem, st>>>(K, ldk, rows, n, V, k, split_cols, P);
+    DCG_CUDA(cudaGetLastError());
+    return DCG_OK;
+}
+
+// Y = shift X_rows + s_out (.) K (s_in (.) X); X is n x k, Y rows x k.
+size_t dcg_block_apply_scratch_doubles(long long n, long long rows, int k) {
+    const long long kk = (k + 1) & ~1;
+    return (size_t)(n * kk + 64 * rows * kk);
+}
+
+// `scratch` holds dcg_block_apply_scratch_doubles(n, rows, k) doubles.
+int dcg_block_apply(dcg_context* ctx, cudaStream_t st, const double* K, long long ldk,
+                    long long rows, long long n, const double* X, int k, const double* s_in,
+                    const double* s_out, double shift, const double* X_rows, double* Y,
+                    double* scratch) {
+    if (k <= 0 || rows <= 0) return DCG_OK;
+    if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
+    if ((ldk & 1) || (reinterpret_cast<uintptr_t>(K) & 15)) return DCG_E_CONFIG;
+    const int kk = (k + 1) & ~1;   // even width for 16-byte staging of V
+    const size_t vbytes = sizeof(double) * (size_t)(n * kk);
+    int rc = DCG_OK;
+    double* V = scratch;
+    double* P = V + n * kk;
+    // V = s_in (.) X, padded to an even column count
+    if (kk != k || s_in) {
+        DCG_CUDA(cudaMemsetAsync(V, 0, vbytes, st));
+        // scatter into padded layout via a 2D copy, then scale in place
+        DCG_CUDA(cudaMemcpy2DAsync(V, sizeof(double) * kk, X, sizeof(double) * k, sizeof(double) * k, n,
+                                   cudaMemcpyDeviceToDevice, st));
+        if (s_in) {
+            rowscale_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(V, s_in, n, kk, V);
+            DCG_CUDA(cudaGetLastError());
+        }
+    } else {
+        DCG_CUDA(cudaMemcpyAsync(V, X, vbytes, cudaMemcpyDeviceToDevice, st));
+    }
+    int splits = 1;
+    const int ntile = (kk + 7) / 8;
+    switch (ntile) {
+        case 1: rc = launch_dmma<1>(ctx, st, K, ldk, rows, n, V, kk, P, splits); break;
+        case 2: rc = launch_dmma<2>(ctx, st, K, ldk, rows, n, V, kk, P, splits); break;
+        case 3: rc = launch_dmma<3>(ctx, st, K, ldk, rows, n, V, kk, P, splits); break;
+        case 4: rc = launch_dmma<4>(ctx, st, K, ldk, rows, n, V, kk, P, splits); break;
+        case 5: rc = launch_dmma<5>(ctx, st, K, ldk, rows, n, V, kk, P, splits); break;
+        case 6: rc = launch_dmma<6>(ctx, st, K, ldk, rows, n, V, kk, P, splits); break;
+        case 7: rc = launch_dmma<7>(ctx, st, K, ldk, rows, n, V, kk, P, splits); break;
+        default: rc = launch_dmma<8>(ctx, st, K, ldk, rows, n, V, kk, P, splits); break;
+    }
+    if (rc) return rc;
+    if (kk == k) {
+        yscale_reduce_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(P, splits, rows, k, X_rows, s_out, shift, Y);
+        DCG_CUDA(cudaGetLastError());
+    } else {
+        // reduce into the padded layout of V (no longer needed), then compact
+        yscale_reduce_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(P, splits, rows, kk, nullptr, s_out, 0.0, V);
+        DCG_CUDA(cudaGetLastError());
+        DCG_CUDA(cudaMemcpy2DAsync(Y, sizeof(double) * k, V, sizeof(double) * kk, sizeof(double) * k, rows,
+                                   cudaMemcpyDeviceToDevice, st));
+        if (shift != 0.0) {
+            // Y += shift X_rows (separate pass keeps the reference's (s*t) + shift*x order)
+            yscale_reduce_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(Y, 1, rows, k, X_rows, nullptr, shift, Y);
+            DCG_CUDA(cudaGetLastError());
+        }
+    }
+    return DCG_OK;
+}
+
+// =============================================================================
+// K4: C(p x q) = X(n x p)' Y(n x q), tall-skinny, deterministic two-stage.
+// =============================================================================
+#define XTY_ROWS 32
+#define XTY_PPT 8     // pairs per thread
+__global__ void __launch_bounds__(256)
+    xty_kernel(const double* __restrict__ X, long long ldx, const double* __restrict__ Y, long long ldy,
+               long long n, int p, int q, double* part) {
+    extern __shared__ double xty_sm[];
+    double* sx = xty_sm;                      // XTY_ROWS x p
+    double* sy = xty_sm + XTY_ROWS * p;       // XTY_ROWS x q
+    const int tid = threadIdx.x;
+    const long long r0 = part_begin(n, gridDim.x, blockIdx.x);
+    const long long r1 = part_begin(n, gridDim.x, blockIdx.x + 1);
+    const int pq = p * q;
+    const int pair0 = blockIdx.y * (256 * XTY_PPT);
+    double acc[XTY_PPT];
+    int pa[XTY_PPT], pb[XTY_PPT];
+#pragma unroll
+    for (int u = 0; u < XTY_PPT; ++u) {
+        acc[u] = 0.0;
+        const int e = pair0 + u * 256 + tid;
+        pa[u] = (e < pq) ? e / q : -1;
+        pb[u] = (e < pq) ? e % q : 0;
+    }
+    for (long long rb = r0; rb < r1; rb += XTY_ROWS) {
+        const int nr = (int)min((long long)XTY_ROWS, r1 - rb);
+        __syncthreads();
+        for (int e = tid; e < nr * p; e += 256) sx[e] = X[(rb + e / p) * ldx + e % p];
+        for (int e = tid; e < nr * q; e += 256) sy[e] = Y[(rb + e / q) * ldy + e % q];
+        __syncthreads();
+        for (int r = 0; r < nr; ++r) {
+#pragma unroll
+            for (int u = 0; u < XTY_PPT; ++u)
+                if (pa[u] >= 0) acc[u] = fma(sx[r * p + pa[u]], sy[r * q + pb[u]], acc[u]);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < XTY_PPT; ++u) {
+        const int e = pair0 + u * 256 + tid;
+        if (e < pq) part[(long long)blockIdx.x * pq + e] = acc[u];
+    }
+}
+
+__global__ void reduce_parts_kernel(const double* part, int nparts, int m, double* out) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int b = 0; b < nparts; ++b) acc += part[(long long)b * m + e];
+        out[e] = acc;
+    }
+}
+
+int dcg_xty(dcg_context* ctx, cudaStream_t st, const double* X, long long ldx, const double* Y,
+            long long ldy, long long n, int p, int q, double* C, double* scratch_parts) {
+    if (p <= 0 || q <= 0) return DCG_OK;
+    if (p > DCG_MAX_T || q > DCG_MAX_T) return DCG_E_UNSUPPORTED;
+    int nb = ctx->sm_count;
+    if (n < (long long)nb * XTY_ROWS) nb = (int)max(1LL, (n + XTY_ROWS - 1) / XTY_ROWS);
+    const int pq = p * q;
+    dim3 grid(nb, (pq + 256 * XTY_PPT - 1) / (256 * XTY_PPT));
+    const size_t smem = sizeof(double) * XTY_ROWS * (size_t)(p + q);
+    DCG_CUDA(cudaFuncSetAttribute(xty_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    xty_kernel<<<grid, 256, smem, st>>>(X, ldx, Y, ldy, n, p, q, scratch_parts);
+    DCG_CUDA(cudaGetLastError());
+    reduce_parts_kernel<<<(pq + 255) / 256, 256, 0, st>>>(scratch_parts, nb, pq, C);
+    DCG_CUDA(cudaGetLastError());
+    return DCG_OK;
+}
+
+size_t dcg_xty_scratch_doubles(dcg_context* ctx, int p, int q) { return (size_t)ctx->sm_count * p * q; }
+
+// =============================================================================
+// C(m x n) = A(m x kk) B(kk x n) in the reference's i-k-j accumulation order
+// (each C[i][j] sums k ascending with separate multiply and add, _core.pyx:31-44).
+// =============================================================================
+__global__ void gemm_lr_kernel(const double* __restrict__ A, long long lda, const double* __restrict__ B,
+                               long long ldb, double* C, long long ldc, long long m, long long kk,
+                               long long n) {
+    const long long total = m * n;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long i = e / n, j = e % n;
+        double acc = 0.0;
+        for (long long t = 0; t < kk; ++t) acc = add_rn(acc, mul_rn(A[i * lda + t], B[t * ldb + j]));
+        C[i * ldc + j] = acc;
+    }
+}
+
+int dcg_gemm_lr(dcg_context* ctx, cudaStream_t st, const double* A, long long lda, const double* B,
+                long long ldb, double* C, long long ldc, long long m, long long kk, long long n) {
+    if (m <= 0 || n <= 0) return DCG_OK;
+    long long blocks = (m * n + 255) / 256;
+    if (blocks > ctx->sm_count * 16LL) blocks = ctx->sm_count * 16LL;
+    gemm_lr_kernel<<<(unsigned)blocks, 256, 0, st>>>(A, lda, B, ldb, C, ldc, m, kk, n);
+    DCG_CUDA(cudaGetLastError());
+    return DCG_OK;
+}

@@ -1,0 +1,131 @@
+// Shared device helpers for the def-CG B200 kernels.
+//
+// Rounding policy: element-wise updates that the reference performs as numpy
+// array expressions (x += alpha*p, r = r - alpha*Ap, p = beta*p + r - W mu,
+// solvers.py:174-193) use explicit __dmul_rn/__dadd_rn so nvcc cannot contract
+// them into FMAs; they then round exactly like the reference.  Reductions
+// (dot products, GEMV rows) necessarily use a different summation order than
+// BLAS / the reference's left-to-right loops; they are deterministic (fixed
+// tree, no atomics), so repeated calls are bit-identical like the reference
+// (README.md:49-53, test_kernels.py:83-105).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/defcg_b200.h"
+
+#define DCG_NT 512                      // threads of the persistent / GEMV CTAs
+#define DCG_NW (DCG_NT / 32)            // warps per CTA
+#define DCG_RB 128                      // rows per GEMV batch (smem partials)
+#define DCG_RG 4                        // rows streamed concurrently per thread
+#define DCG_QT 16384                    // x-tile (doubles) staged in smem per pass
+
+struct dcg_context {
+    int device;
+    int sm_count;
+    int solve_blocks;        // CTAs of the persistent solve kernel
+    size_t smem_optin;
+    void* ws;                // device workspace
+    size_t ws_bytes;
+    void* host;              // pinned host scratch for status read-back
+    size_t host_bytes;
+    cudaEvent_t ev0, ev1;
+};
+
+// ---- status plumbing --------------------------------------------------------
+// Device-side status block written by single-CTA / persistent kernels.
+struct DevStatus {
+    int status;
+    int pad;
+    long long info;
+    long long count;         // k_out / T / iterations depending on kernel
+    long long aux;
+    double value;            // rel residual / loglik ...
+    double value2;           // norm_b / psi ...
+};
+
+#define DCG_CUDA(call)                                                   \
+    do {                                                                  \
+        cudaError_t _e = (call);                                          \
+        if (_e != cudaSuccess) {                                          \
+            dcg_last_cuda_error = _e;                                     \
+            return DCG_E_CUDA;                                            \
+        }                                                                 \
+    } while (0)
+
+extern thread_local cudaError_t dcg_last_cuda_error;
+
+int dcg_ws_reserve(dcg_context* ctx, size_t bytes);
+int dcg_host_reserve(dcg_context* ctx, size_t bytes);
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- arithmetic without FMA contraction --------------------------------------
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+
+// ---- loads -----------------------------------------------------------------
+// Streamed, read-only for the kernel's lifetime (the Gram slab): no L1 allocation.
+__device__ __forceinline__ double2 ld_stream2(const double* p) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+// Data written by other CTAs of the same launch (after a grid barrier): L2 only.
+__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+// ---- reductions (deterministic: fixed butterfly, identical on every lane) ---
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide sum; every thread receives the same value.  `red` holds >= 33
+// doubles of shared scratch.  Contains two __syncthreads.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double t = (lane < nw) ? red[lane] : 0.0;
+    t = warp_sum(t);
+    return t;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ double block_max(double v, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+    v = warp_max(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double t = (lane < nw) ? red[lane] : -INFINITY;
+    return warp_max(t);
+}
+
+// Row partition of [0, n) over `parts` contiguous, balanced ranges.
+__host__ __device__ __forceinline__ long long part_begin(long long n, long long parts, long long i) {
+    return (n * i) / parts;
+}
+
+// ---- host launch helpers ----------------------------------------------------
+int dcg_launch_check();

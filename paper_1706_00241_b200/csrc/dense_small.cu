@@ -1,0 +1,645 @@
+// Small dense linear algebra on one CTA (kernel K5 of SURVEY.md section 2).
+//
+// Everything here is at most DCG_MAX_T x DCG_MAX_T (the harmonic pencil is
+// k_prev + m <= k + ell).  The reference runs these as scalar Cython loops
+// (_core.pyx:47-94, 135-177) driven from linalg.py:74-191; the device versions
+// keep the reference's thresholds and operation order where it is inherently
+// serial (Cholesky pivots, forward substitution) with non-contracted fp64
+// arithmetic, and parallelise only independent work:
+//   - Cholesky: column j serial, rows i > j in parallel (same per-element sum order);
+//   - triangular solves of many right-hand sides: one warp per column;
+//   - the symmetric eigensolver is Jacobi with the reference's skip rule and
+//     convergence test (linalg.py:139-165) but a parallel round-robin pair
+//     ordering (T/2 disjoint rotations per step), so a sweep costs T-1 barrier
+//     rounds instead of T(T-1)/2 sequential rotations.  Eigenpairs agree with
+//     the cyclic order to rounding; spans, not signs, are what callers use.
+#include "common.cuh"
+
+#define SD_NT 512
+
+// ---------------------------------------------------------------------------
+// Cholesky with the reference's pivot rule (acc <= pivot_tol fails at j).
+// A, L: row-major with leading dimensions; L's upper triangle is zeroed.
+// Returns -1 on success or the failing pivot index.  All CTA threads call.
+// ---------------------------------------------------------------------------
+__device__ int cta_cholesky(const double* A, int lda, int n, double pivot_tol, double* L, int ldl,
+                            double* s_scal) {
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const int i = e / n, j = e % n;
+        if (j > i) L[i * ldl + j] = 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < n; ++j) {
+        if (threadIdx.x == 0) {
+            double acc = A[j * lda + j];
+            for (int t = 0; t < j; ++t) acc = sub_rn(acc, mul_rn(L[j * ldl + t], L[j * ldl + t]));
+            if (acc <= pivot_tol) {
+                s_scal[0] = 1.0;
+            } else {
+                s_scal[0] = 0.0;
+                const double ljj = sqrt(acc);
+                s_scal[1] = ljj;
+                L[j * ldl + j] = ljj;
+            }
+        }
+        __syncthreads();
+        if (s_scal[0] != 0.0) {
+            __syncthreads();
+            return j;
+        }
+        const double ljj = s_scal[1];
+        for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) {
+            double acc = A[i * lda + j];
+            for (int t = 0; t < j; ++t) acc = sub_rn(acc, mul_rn(L[i * ldl + t], L[j * ldl + t]));
+            L[i * ldl + j] = div_rn(acc, ljj);
+        }
+        __syncthreads();
+    }
+    return -1;
+}
+
+// 1e-14 * max(max(diag), 0)   (linalg.py:74-76), diag of A restricted to idx[0..n)
+__device__ double cta_pivot_tol(const double* A, int lda, const int* idx, int n, double* red) {
+    double m = -INFINITY;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int ii = idx ? idx[i] : i;
+        m = fmax(m, A[ii * lda + ii]);
+    }
+    m = block_max(m, red);
+    if (n == 0) m = 0.0;
+    return 1e-14 * fmax(m, 0.0);
+}
+
+// Warp-level forward substitution: y = L^-1 b for one right-hand side
+// (b, y with strides), reference order per element (_core.pyx:69-80).
+// Lanes own rows lane + 32u.
+__device__ void warp_solve_lower(const double* L, int ldl, int n, const double* b, int bstride,
+                                 double* y, int ystride) {
+    const int lane = threadIdx.x & 31;
+    double a[(DCG_MAX_T + 31) / 32];
+#pragma unroll
+    for (int u = 0; u < (DCG_MAX_T + 31) / 32; ++u) {
+        const int i = lane + 32 * u;
+        a[u] = (i < n) ? b[i * bstride] : 0.0;
+    }
+    for (int j = 0; j < n; ++j) {
+        const int uj = j >> 5;
+        double accj = 0.0;
+#pragma unroll
+        for (int u = 0; u < (DCG_MAX_T + 31) / 32; ++u)
+            if (u == uj) accj = __shfl_sync(0xffffffffu, a[u], j & 31);
+        const double yj = div_rn(accj, L[j * ldl + j]);
+#pragma unroll
+        for (int u = 0; u < (DCG_MAX_T + 31) / 32; ++u) {
+            const int i = lane + 32 * u;
+            if (i == j) a[u] = yj;
+            else if (i > j && i < n) a[u] = sub_rn(a[u], mul_rn(L[i * ldl + j], yj));
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < (DCG_MAX_T + 31) / 32; ++u) {
+        const int i = lane + 32 * u;
+        if (i < n) y[i * ystride] = a[u];
+    }
+}
+
+// Warp-level back substitution x = L^-T b (wavefront order).
+__device__ void warp_solve_lower_trans(const double* L, int ldl, int n, const double* b, int bstride,
+                                       double* x, int xstride) {
+    const int lane = threadIdx.x & 31;
+    double a[(DCG_MAX_T + 31) / 32];
+#pragma unroll
+    for (int u = 0; u < (DCG_MAX_T + 31) / 32; ++u) {
+        const int i = lane + 32 * u;
+        a[u] = (i < n) ? b[i * bstride] : 0.0;
+    }
+    for (int j = n - 1; j >= 0; --j) {
+        const int uj = j >> 5;
+        double accj = 0.0;
+#pragma unroll
+        for (int u = 0; u < (DCG_MAX_T + 31) / 32; ++u)
+            if (u == uj) accj = __shfl_sync(0xffffffffu, a[u], j & 31);
+        const double xj = div_rn(accj, L[j * ldl + j]);
+#pragma unroll
+        for (int u = 0; u < (DCG_MAX_T + 31) / 32; ++u) {
+            const int i = lane + 32 * u;
+            if (i == j) a[u] = xj;
+            else if (i < j) a[u] = sub_rn(a[u], mul_rn(L[j * ldl + i], xj));
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < (DCG_MAX_T + 31) / 32; ++u) {
+        const int i = lane + 32 * u;
+        if (i < n) x[i * xstride] = a[u];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Parallel-order Jacobi eigensolver on a symmetric T x T matrix A (row-major,
+// leading dimension T, typically shared memory); V receives eigenvectors as
+// columns (unsorted).  Returns 0, or the sweep budget on NoConvergence.
+// ---------------------------------------------------------------------------
+__device__ int cta_jacobi(double* A, double* V, int T, int max_sweeps, double rtol, double* red,
+                          double* s_c, double* s_s, int* s_mode) {
+    const int tid = threadIdx.x;
+    for (int e = tid; e < T * T; e += blockDim.x) V[e] = (e / T == e % T) ? 1.0 : 0.0;
+    // frob = sqrt(sum a^2) of the input; off = sqrt(sum offdiag^2)
+    double f2 = 0.0;
+    for (int e = tid; e < T * T; e += blockDim.x) f2 = fma(A[e], A[e], f2);
+    const double frob = sqrt(block_sum(f2, red));
+    if (frob == 0.0) return 0;   // zeros and identity (linalg.py:153-154)
+    auto offdiag = [&]() {
+        double o2 = 0.0;
+        for (int e = tid; e < T * T; e += blockDim.x)
+            if (e / T != e % T) o2 = fma(A[e], A[e], o2);
+        return sqrt(block_sum(o2, red));
+    };
+    bool converged = offdiag() <= rtol * frob;
+    const int Te = T + (T & 1);
+    const int npairs = Te / 2;
+    for (int sweep = 0; sweep < max_sweeps && !converged; ++sweep) {
+        for (int round = 0; round < Te - 1; ++round) {
+            // circle method: position 0 holds player Te-1, others rotate
+            if (tid < npairs) {
+                auto player = [&](int pos) { return pos == 0 ? Te - 1 : ((pos - 1 + round) % (Te - 1)); };
+                int pa = player(tid), pb = player(Te - 1 - tid);
+                const int p = min(pa, pb), q = max(pa, pb);
+                double c = 1.0, s = 0.0;
+                int mode = 0;   // 0 identity, 1 zero a_pq, 2 rotate
+                if (q < T) {
+                    const double apq = A[p * T + q];
+                    const double app = A[p * T + p], aqq = A[q * T + q];
+                    const double g = 100.0 * fabs(apq);
+                    if (add_rn(fabs(app), g) == fabs(app) && add_rn(fabs(aqq), g) == fabs(aqq)) {
+                        mode = 1;
+                    } else if (apq != 0.0) {
+                        const double tau = div_rn(sub_rn(aqq, app), mul_rn(2.0, apq));
+                        double t;
+                        if (tau >= 0.0)
+                            t = div_rn(1.0, add_rn(tau, sqrt(add_rn(1.0, mul_rn(tau, tau)))));
+                        else
+                            t = div_rn(-1.0, add_rn(-tau, sqrt(add_rn(1.0, mul_rn(tau, tau)))));
+                        c = div_rn(1.0, sqrt(add_rn(1.0, mul_rn(t, t))));
+                        s = mul_rn(t, c);
+                        mode = 2;
+                    }
+                }
+                // slot tid describes the pair (p, q)
+                s_c[tid] = c;
+                s_s[tid] = s;
+                s_mode[tid] = mode;
+                s_mode[npairs + 2 * tid] = p;
+                s_mode[npairs + 2 * tid + 1] = q;
+            }
+            __syncthreads();
+            // A <- R A R' applied on 2x2 blocks of (pair a rows) x (pair b cols)
+            for (int e = tid; e < npairs * npairs; e += blockDim.x) {
+                const int pa = e / npairs, pb = e % npairs;
+                const int ra0 = s_mode[npairs + 2 * pa], ra1 = s_mode[npairs + 2 * pa + 1];
+                const int cb0 = s_mode[npairs + 2 * pb], cb1 = s_mode[npairs + 2 * pb + 1];
+                const bool ra1v = ra1 < T, cb1v = cb1 < T;
+                const double ca = s_c[pa], sa = s_s[pa], cbv = s_c[pb], sbv = s_s[pb];
+                double x00 = A[ra0 * T + cb0];
+                double x01 = cb1v ? A[ra0 * T + cb1] : 0.0;
+                double x10 = ra1v ? A[ra1 * T + cb0] : 0.0;
+                double x11 = (ra1v && cb1v) ? A[ra1 * T + cb1] : 0.0;
+                // columns (R_b on the right): a'_ip = c a_ip - s a_iq ; a'_iq = s a_ip + c a_iq
+                if (s_mode[pb] == 2) {
+                    const double y00 = sub_rn(mul_rn(cbv, x00), mul_rn(sbv, x01));
+                    const double y01 = add_rn(mul_rn(sbv, x00), mul_rn(cbv, x01));
+                    const double y10 = sub_rn(mul_rn(cbv, x10), mul_rn(sbv, x11));
+                    const double y11 = add_rn(mul_rn(sbv, x10), mul_rn(cbv, x11));
+                    x00 = y00; x01 = y01; x10 = y10; x11 = y11;
+                }
+                // rows (R_a on the left)
+                if (s_mode[pa] == 2) {
+                    const double y00 = sub_rn(mul_rn(ca, x00), mul_rn(sa, x10));
+                    const double y10 = add_rn(mul_rn(sa, x00), mul_rn(ca, x10));
+                    const double y01 = sub_rn(mul_rn(ca, x01), mul_rn(sa, x11));
+                    const double y11 = add_rn(mul_rn(sa, x01), mul_rn(ca, x11));
+                    x00 = y00; x01 = y01; x10 = y10; x11 = y11;
+                }
+                if (pa == pb && s_mode[pa] != 0) { x01 = 0.0; x10 = 0.0; }
+                A[ra0 * T + cb0] = x00;
+                if (cb1v) A[ra0 * T + cb1] = x01;
+                if (ra1v) A[ra1 * T + cb0] = x10;
+                if (ra1v && cb1v) A[ra1 * T + cb1] = x11;
+            }
+            // V <- V R'
+            for (int e = tid; e < T * npairs; e += blockDim.x) {
+                const int i = e / npairs, pb = e % npairs;
+                if (s_mode[pb] != 2) continue;
+                const int c0 = s_mode[npairs + 2 * pb], c1 = s_mode[npairs + 2 * pb + 1];
+                const double cbv = s_c[pb], sbv = s_s[pb];
+                const double vp = V[i * T + c0], vq = V[i * T + c1];
+                V[i * T + c0] = sub_rn(mul_rn(cbv, vp), mul_rn(sbv, vq));
+                V[i * T + c1] = add_rn(mul_rn(sbv, vp), mul_rn(cbv, vq));
+            }
+            __syncthreads();
+        }
+        converged = offdiag() <= rtol * frob;
+    }
+    return converged ? 0 : max_sweeps;
+}
+
+// order[r] = index of the r-th smallest value, ties by index (stable argsort)
+__device__ void cta_stable_argsort(const double* vals, int stride, int n, int* order) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double vi = vals[i * stride];
+        int rank = 0;
+        for (int j = 0; j < n; ++j) {
+            const double vj = vals[j * stride];
+            if (vj < vi || (vj == vi && j < i)) ++rank;
+        }
+        order[rank] = i;
+    }
+    __syncthreads();
+}
+
+// ===========================================================================
+// Gram factorisation with optional failing-pivot pruning.
+// Graw: k x k (W'AW, unsymmetrised).  Outputs L (kk x kk, leading dim kk),
+// active column list, status.  solvers.py:107-115 (no prune -> GramNotSpd),
+// recycle.py:66-77 (prune; empty -> BasisDeficient(0)).
+// ===========================================================================
+__global__ void __launch_bounds__(SD_NT) gram_factor_kernel(const double* Graw, int k, int prune,
+                                                            double* Gsym, double* L, int* active,
+                                                            DevStatus* st) {
+    __shared__ double red[40];
+    __shared__ double s_scal[4];
+    __shared__ int s_act[DCG_MAX_K];
+    __shared__ int s_na;
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+        const int i = e / k, j = e % k;
+        Gsym[e] = mul_rn(0.5, add_rn(Graw[i * k + j], Graw[j * k + i]));
+    }
+    if (threadIdx.x < k) s_act[threadIdx.x] = threadIdx.x;
+    if (threadIdx.x == 0) s_na = k;
+    __syncthreads();
+    // compact sub-matrix lives in L's own storage region "sub" right after L (kk*kk)
+    double* sub = L + k * k;
+    while (true) {
+        const int na = s_na;
+        if (na == 0) {
+            if (threadIdx.x == 0) { st->status = DCG_E_BASIS_DEFICIENT; st->info = 0; st->count = 0; }
+            return;
+        }
+        for (int e = threadIdx.x; e < na * na; e += blockDim.x) {
+            const int i = e / na, j = e % na;
+            sub[e] = Gsym[s_act[i] * k + s_act[j]];
+        }
+        __syncthreads();
+        const double tol = cta_pivot_tol(sub, na, nullptr, na, red);
+        const int fail = cta_cholesky(sub, na, na, tol, L, na, s_scal);
+        if (fail < 0) {
+            if (threadIdx.x == 0) { st->status = DCG_OK; st->count = na; }
+            if (threadIdx.x < na) active[threadIdx.x] = s_act[threadIdx.x];
+            return;
+        }
+        if (!prune) {
+            if (threadIdx.x == 0) { st->status = DCG_E_GRAM_NOT_SPD; st->info = fail; st->count = na; }
+            return;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int i = fail; i < na - 1; ++i) s_act[i] = s_act[i + 1];
+            s_na = na - 1;
+        }
+        __syncthreads();
+    }
+}
+
+// ===========================================================================
+// Harmonic pencil: symmetrise F, G; prune F's failing-pivot columns; solve
+// G u = theta F u (gen_sym_eigen, linalg.py:168-191); select k values.
+// Global scratch `wk` holds 5 * T * T doubles.  Outputs: theta (k), U (na x k,
+// row-major over the surviving columns), active list, status (count = na).
+// ===========================================================================
+__global__ void __launch_bounds__(SD_NT) ritz_pencil_kernel(const double* Fraw, const double* Graw, int T,
+                                                            int k, int largest, int max_sweeps,
+                                                            double* wk, double* theta, double* U,
+                                                            int* active, DevStatus* st) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ double red[40];
+    __shared__ double s_scal[4];
+    __shared__ double s_c[DCG_MAX_T / 2 + 1], s_s[DCG_MAX_T / 2 + 1];
+    __shared__ int s_mode[DCG_MAX_T / 2 + 1 + DCG_MAX_T + 2];
+    __shared__ int s_act[DCG_MAX_T];
+    __shared__ int s_order[DCG_MAX_T];
+    __shared__ int s_na;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nw = blockDim.x >> 5;
+    double* F = wk;
+    double* G = F + T * T;
+    double* L = G + T * T;
+    double* Y = L + T * T;
+    double* Fa = Y + T * T;
+    for (int e = tid; e < T * T; e += blockDim.x) {
+        const int i = e / T, j = e % T;
+        F[e] = mul_rn(0.5, add_rn(Fraw[i * T + j], Fraw[j * T + i]));
+        G[e] = mul_rn(0.5, add_rn(Graw[i * T + j], Graw[j * T + i]));
+    }
+    if (tid < T) s_act[tid] = tid;
+    if (tid == 0) s_na = T;
+    __syncthreads();
+    int na;
+    while (true) {
+        na = s_na;
+        if (na < k) {
+            if (tid == 0) { st->status = DCG_E_BASIS_DEFICIENT; st->info = na; st->count = na; }
+            return;
+        }
+        for (int e = tid; e < na * na; e += blockDim.x) {
+            const int i = e / na, j = e % na;
+            Fa[e] = F[s_act[i] * T + s_act[j]];
+        }
+        __syncthreads();
+        const double tol = cta_pivot_tol(Fa, na, nullptr, na, red);
+        const int fail = cta_cholesky(Fa, na, na, tol, L, na, s_scal);
+        if (fail < 0) break;
+        __syncthreads();
+        if (tid == 0) {
+            for (int i = fail; i < na - 1; ++i) s_act[i] = s_act[i + 1];
+            s_na = na - 1;
+        }
+        __syncthreads();
+    }
+    // Ga -> Fa storage (F no longer needed in compact form)
+    double* Ga = Fa;
+    for (int e = tid; e < na * na; e += blockDim.x) {
+        const int i = e / na, j = e % na;
+        Ga[e] = G[s_act[i] * T + s_act[j]];
+    }
+    __syncthreads();
+    // Y = L^-1 Ga  (solve_lower_matrix: column by column)
+    for (int c = warp; c < na; c += nw) warp_solve_lower(L, na, na, Ga + c, na, Y + c, na);
+    __syncthreads();
+    // C = L^-1 Y'  -> into shared A
+    double* A = sm;
+    double* V = sm + na * na;
+    for (int c = warp; c < na; c += nw) warp_solve_lower(L, na, na, Y + c * na, 1, A + c, na);
+    __syncthreads();
+    // symmetrise
+    for (int e = tid; e < na * na; e += blockDim.x) {
+        const int i = e / na, j = e % na;
+        if (i < j) {
+            const double v = mul_rn(0.5, add_rn(A[i * na + j], A[j * na + i]));
+            A[i * na + j] = v;
+            A[j * na + i] = v;
+        }
+    }
+    __syncthreads();
+    const int nc = cta_jacobi(A, V, na, max_sweeps, 1e-14, red, s_c, s_s, s_mode);
+    if (nc) {
+        if (tid == 0) { st->status = DCG_E_NO_CONVERGENCE; st->info = nc; st->count = na; }
+        return;
+    }
+    cta_stable_argsort(A, na + 1, na, s_order);
+    // selected eigen-pairs: u = L^-T w, normalised
+    const int off = largest ? (na - k) : 0;
+    for (int j = warp; j < k; j += nw) {
+        const int col = s_order[off + j];
+        warp_solve_lower_trans(L, na, na, V + col, na, U + j, k);
+        __syncwarp();
+        double s2 = 0.0;
+        for (int i = lane; i < na; i += 32) s2 = fma(U[i * k + j], U[i * k + j], s2);
+        const double nrm = sqrt(warp_sum(s2));
+        if (nrm > 0.0)
+            for (int i = lane; i < na; i += 32) U[i * k + j] = div_rn(U[i * k + j], nrm);
+        if (lane == 0) theta[j] = A[col * na + col];
+    }
+    if (tid < na) active[tid] = s_act[tid];
+    if (tid == 0) { st->status = DCG_OK; st->count = na; }
+}
+
+// ===========================================================================
+// Standalone eigensolvers (dcg_sym_eigen / dcg_gen_sym_eigen).
+// ===========================================================================
+__global__ void __launch_bounds__(SD_NT) sym_eigen_kernel(const double* Ain, int n, int max_sweeps, double rtol,
+                                                          double* values, double* vectors, DevStatus* st) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ double red[40];
+    __shared__ double s_c[DCG_MAX_T / 2 + 1], s_s[DCG_MAX_T / 2 + 1];
+    __shared__ int s_mode[DCG_MAX_T / 2 + 1 + DCG_MAX_T + 2];
+    __shared__ int s_order[DCG_MAX_T];
+    double* A = sm;
+    double* V = sm + n * n;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) A[e] = Ain[e];
+    __syncthreads();
+    const int nc = cta_jacobi(A, V, n, max_sweeps, rtol, red, s_c, s_s, s_mode);
+    if (nc) {
+        if (threadIdx.x == 0) { st->status = DCG_E_NO_CONVERGENCE; st->info = nc; }
+        return;
+    }
+    __syncthreads();
+    cta_stable_argsort(A, n + 1, n, s_order);
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const int i = e / n, r = e % n;
+        vectors[i * n + r] = V[i * n + s_order[r]];
+    }
+    for (int r = threadIdx.x; r < n; r += blockDim.x) values[r] = A[s_order[r] * (n + 1)];
+    if (threadIdx.x == 0) st->status = DCG_OK;
+}
+
+__global__ void __launch_bounds__(SD_NT) gen_sym_eigen_kernel(const double* g, const double* f, int n,
+                                                              int max_sweeps, double* wk, double* values,
+                                                              double* vectors, DevStatus* st) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ double red[40];
+    __shared__ double s_scal[4];
+    __shared__ double s_c[DCG_MAX_T / 2 + 1], s_s[DCG_MAX_T / 2 + 1];
+    __shared__ int s_mode[DCG_MAX_T / 2 + 1 + DCG_MAX_T + 2];
+    __shared__ int s_order[DCG_MAX_T];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+    double* L = wk;
+    double* Y = wk + n * n;
+    const double tol = cta_pivot_tol(f, n, nullptr, n, red);
+    const int fail = cta_cholesky(f, n, n, tol, L, n, s_scal);
+    if (fail >= 0) {
+        if (tid == 0) { st->status = DCG_E_NOT_PD; st->info = fail; }
+        return;
+    }
+    for (int c = warp; c < n; c += nw) warp_solve_lower(L, n, n, g + c, n, Y + c, n);
+    __syncthreads();
+    double* A = sm;
+    double* V = sm + n * n;
+    for (int c = warp; c < n; c += nw) warp_solve_lower(L, n, n, Y + c * n, 1, A + c, n);
+    __syncthreads();
+    for (int e = tid; e < n * n; e += blockDim.x) {
+        const int i = e / n, j = e % n;
+        if (i < j) {
+            const double v = mul_rn(0.5, add_rn(A[i * n + j], A[j * n + i]));
+            A[i * n + j] = v;
+            A[j * n + i] = v;
+        }
+    }
+    __syncthreads();
+    const int nc = cta_jacobi(A, V, n, max_sweeps, 1e-14, red, s_c, s_s, s_mode);
+    if (nc) {
+        if (tid == 0) { st->status = DCG_E_NO_CONVERGENCE; st->info = nc; }
+        return;
+    }
+    cta_stable_argsort(A, n + 1, n, s_order);
+    for (int j = warp; j < n; j += nw) {
+        const int col = s_order[j];
+        warp_solve_lower_trans(L, n, n, V + col, n, vectors + j, n);
+        __syncwarp();
+        double s2 = 0.0;
+        for (int i = lane; i < n; i += 32) s2 = fma(vectors[i * n + j], vectors[i * n + j], s2);
+        const double nrm = sqrt(warp_sum(s2));
+        if (nrm > 0.0)
+            for (int i = lane; i < n; i += 32) vectors[i * n + j] = div_rn(vectors[i * n + j], nrm);
+        if (lane == 0) values[j] = A[col * (n + 1)];
+    }
+    if (tid == 0) st->status = DCG_OK;
+}
+
+// ===========================================================================
+// L0 twins with the reference's exact operation order.
+// ===========================================================================
+__global__ void __launch_bounds__(SD_NT) k_cholesky_kernel(const double* a, int n, double tol, double* l,
+                                                           DevStatus* st) {
+    __shared__ double s_scal[4];
+    const int fail = cta_cholesky(a, n, n, tol, l, n, s_scal);
+    if (threadIdx.x == 0) st->info = fail;
+}
+
+__global__ void k_solve_lower_kernel(const double* l, int n, const double* b, double* y) {
+    // single thread: exact reference order (_core.pyx:69-80)
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    for (int i = 0; i < n; ++i) {
+        double acc = b[i];
+        for (int j = 0; j < i; ++j) acc = sub_rn(acc, mul_rn(l[(long long)i * n + j], y[j]));
+        y[i] = div_rn(acc, l[(long long)i * n + i]);
+    }
+}
+
+__global__ void k_solve_lower_trans_kernel(const double* l, int n, const double* b, double* x) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    for (int i = n - 1; i >= 0; --i) {
+        double acc = b[i];
+        for (int j = i + 1; j < n; ++j) acc = sub_rn(acc, mul_rn(l[(long long)j * n + i], x[j]));
+        x[i] = div_rn(acc, l[(long long)i * n + i]);
+    }
+}
+
+// One cyclic Jacobi sweep in the reference's exact order (_core.pyx:135-177);
+// the three inner loops run in parallel over i.
+__global__ void __launch_bounds__(SD_NT) k_jacobi_sweep_kernel(double* a, double* v, int n, DevStatus* st) {
+    __shared__ double s_cs[2];
+    __shared__ int s_mode;
+    long long rotations = 0;
+    for (int p = 0; p < n - 1; ++p) {
+        for (int q = p + 1; q < n; ++q) {
+            if (threadIdx.x == 0) {
+                const double apq = a[p * n + q];
+                const double g = 100.0 * fabs(apq);
+                const double app = a[p * n + p], aqq = a[q * n + q];
+                if (add_rn(fabs(app), g) == fabs(app) && add_rn(fabs(aqq), g) == fabs(aqq)) {
+                    a[p * n + q] = 0.0;
+                    a[q * n + p] = 0.0;
+                    s_mode = 0;
+                } else if (apq == 0.0) {
+                    s_mode = 0;
+                } else {
+                    const double tau = div_rn(sub_rn(aqq, app), mul_rn(2.0, apq));
+                    double t;
+                    if (tau >= 0.0) t = div_rn(1.0, add_rn(tau, sqrt(add_rn(1.0, mul_rn(tau, tau)))));
+                    else t = div_rn(-1.0, add_rn(-tau, sqrt(add_rn(1.0, mul_rn(tau, tau)))));
+                    const double c = div_rn(1.0, sqrt(add_rn(1.0, mul_rn(t, t))));
+                    s_cs[0] = c;
+                    s_cs[1] = mul_rn(t, c);
+                    s_mode = 1;
+                }
+            }
+            __syncthreads();
+            if (s_mode) {
+                const double c = s_cs[0], s = s_cs[1];
+                for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                    const double aip = a[i * n + p], aiq = a[i * n + q];
+                    a[i * n + p] = sub_rn(mul_rn(c, aip), mul_rn(s, aiq));
+                    a[i * n + q] = add_rn(mul_rn(s, aip), mul_rn(c, aiq));
+                }
+                __syncthreads();
+                for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                    const double aip = a[p * n + i], aiq = a[q * n + i];
+                    a[p * n + i] = sub_rn(mul_rn(c, aip), mul_rn(s, aiq));
+                    a[q * n + i] = add_rn(mul_rn(s, aip), mul_rn(c, aiq));
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    a[p * n + q] = 0.0;
+                    a[q * n + p] = 0.0;
+                }
+                for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                    const double vp = v[i * n + p], vq = v[i * n + q];
+                    v[i * n + p] = sub_rn(mul_rn(c, vp), mul_rn(s, vq));
+                    v[i * n + q] = add_rn(mul_rn(s, vp), mul_rn(c, vq));
+                }
+                ++rotations;
+            }
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) st->count = rotations;
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+int dcg_gram_factor_launch(cudaStream_t st, const double* Graw, int k, int prune, double* Gsym, double* L,
+                           int* active, DevStatus* ds) {
+    gram_factor_kernel<<<1, SD_NT, 0, st>>>(Graw, k, prune, Gsym, L, active, ds);
+    DCG_CUDA(cudaGetLastError());
+    return DCG_OK;
+}
+
+size_t dcg_pencil_smem(int T) { return sizeof(double) * 2 * (size_t)T * T; }
+
+int dcg_ritz_pencil_launch(cudaStream_t st, const double* Fraw, const double* Graw, int T, int k, int largest,
+                           int max_sweeps, double* wk, double* theta, double* U, int* active, DevStatus* ds) {
+    const size_t smem = dcg_pencil_smem(T);
+    DCG_CUDA(cudaFuncSetAttribute(ritz_pencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ritz_pencil_kernel<<<1, SD_NT, smem, st>>>(Fraw, Graw, T, k, largest, max_sweeps, wk, theta, U, active, ds);
+    DCG_CUDA(cudaGetLastError());
+    return DCG_OK;
+}
+
+int dcg_sym_eigen_launch(cudaStream_t st, const double* A, int n, int max_sweeps, double rtol, double* values,
+                         double* vectors, DevStatus* ds) {
+    const size_t smem = dcg_pencil_smem(n);
+    DCG_CUDA(cudaFuncSetAttribute(sym_eigen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    sym_eigen_kernel<<<1, SD_NT, smem, st>>>(A, n, max_sweeps, rtol, values, vectors, ds);
+    DCG_CUDA(cudaGetLastError());
+    return DCG_OK;
+}
+
+int dcg_gen_sym_eigen_launch(cudaStream_t st, const double* g, const double* f, int n, int max_sweeps, double* wk,
+                             double* values, double* vectors, DevStatus* ds) {
+    const size_t smem = dcg_pencil_smem(n);
+    DCG_CUDA(cudaFuncSetAttribute(gen_sym_eigen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    gen_sym_eigen_kernel<<<1, SD_NT, smem, st>>>(g, f, n, max_sweeps, wk, values, vectors, ds);
+    DCG_CUDA(cudaGetLastError());
+    return DCG_OK;
+}
+
+int dcg_k_cholesky_launch(cudaStream_t st, const double* a, int n, double tol, double* l, DevStatus* ds) {
+    k_cholesky_kernel<<<1, SD_NT, 0, st>>>(a, n, tol, l, ds);
+    DCG_CUDA(cudaGetLastError());
+    return DCG_OK;
+}
+int dcg_k_solve_lower_launch(cudaStream_t st, const double* l, int n, const double* b, double* y) {
+    k_solve_lower_kernel<<<1, 32, 0, st>>>(l, n, b, y);
+    DCG_CUDA(cudaGetLastError());
+    return DCG_OK;
+}
+int dcg_k_solve_lower_trans_launch(cudaStream_t st, const double* l, int n, const double* b, double* x) {
+    k_solve_lower_trans_kernel<<<1, 32, 0, st>>>(l, n, b, x);
+    DCG_CUDA(cudaGetLastError());
+    return DCG_OK;
+}
+int dcg_k_jacobi_sweep_launch(cudaStream_t st, double* a, double* v, int n, DevStatus* ds) {
+    k_jacobi_sweep_kernel<<<1, SD_NT, 0, st>>>(a, v, n, ds);
+    DCG_CUDA(cudaGetLastError());
+    return DCG_OK;
+}

@@ -1,0 +1,168 @@
+// RBF Gram assembly (K6) and the GPC Laplace-Newton element-wise glue (K8).
+//
+// rbf_tile_kernel restates _core.rbf_gram / rbf_cross (_core.pyx:97-132):
+// squared distances accumulate left to right over dimensions with separate
+// multiply/add, the diagonal is exactly var + jitter, and every entry is
+// evaluated directly from (x_i, x_j).  Because (a-b)^2 == (b-a)^2 bit for bit,
+// K[i][j] == K[j][i] exactly without mirroring, so a row slab [row0, row0+rows)
+// can be built independently on each rank of a row-sharded operator.
+//
+// The GPC kernels restate gpc.py:126-209 (sigmoid, logaddexp, curvature,
+// Newton right-hand side and update, psi) with deterministic reductions.
+#include "common.cuh"
+
+#define RBF_T 32
+
+__global__ void __launch_bounds__(256)
+    rbf_tile_kernel(const double* __restrict__ xr, long long nr_total, const double* __restrict__ xc,
+                    long long nc, long long dim, double var, double inv2l2, double jitter, int gram,
+                    long long row0, long long rows, double* out, long long ldo) {
+    __shared__ double sr[RBF_T][RBF_T + 1];
+    __shared__ double sc[RBF_T][RBF_T + 1];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+    const long long i0 = (long long)blockIdx.y * RBF_T;        // local row tile
+    const long long j0 = (long long)blockIdx.x * RBF_T;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (long long t0 = 0; t0 < dim; t0 += RBF_T) {
+        const int tn = (int)min((long long)RBF_T, dim - t0);
+        for (int e = threadIdx.x; e < RBF_T * RBF_T; e += 256) {
+            const int r = e / RBF_T, t = e % RBF_T;
+            const long long gi = row0 + i0 + r, gj = j0 + r;
+            sr[r][t] = (t < tn && i0 + r < rows) ? xr[gi * dim + t0 + t] : 0.0;
+            sc[r][t] = (t < tn && gj < nc) ? xc[gj * dim + t0 + t] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+            const int r = ty + 8 * rr;
+            for (int t = 0; t < tn; ++t) {
+                const double diff = sub_rn(sr[r][t], sc[tx][t]);
+                acc[rr] = add_rn(acc[rr], mul_rn(diff, diff));
+            }
+        }
+        __syncthreads();
+    }
+    const long long j = j0 + tx;
+    if (j >= nc) return;
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+        const long long li = i0 + ty + 8 * rr;
+        if (li >= rows) continue;
+        const long long gi = row0 + li;
+        double val;
+        if (gram && gi == j) val = add_rn(var, jitter);
+        else val = mul_rn(var, exp(mul_rn(-acc[rr], inv2l2)));
+        out[li * ldo + j] = val;
+    }
+}
+
+int dcg_rbf_launch(cudaStream_t st, const double* xr, long long nr_total, const double* xc, long long nc,
+                   long long dim, double var, double inv2l2, double jitter, int gram, long long row0,
+                   long long rows, double* out, long long ldo) {
+    if (rows <= 0 || nc <= 0) return DCG_OK;
+    dim3 grid((unsigned)((nc + RBF_T - 1) / RBF_T), (unsigned)((rows + RBF_T - 1) / RBF_T));
+    rbf_tile_kernel<<<grid, 256, 0, st>>>(xr, nr_total, xc, nc, dim, var, inv2l2, jitter, gram, row0, rows,
+                                          out, ldo);
+    DCG_CUDA(cudaGetLastError());
+    return DCG_OK;
+}
+
+// ----------------------------------------------------------------------------
+// logistic likelihood pieces (gpc.py:126-157)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ double sigmoid_ref(double z) {
+    if (z >= 0.0) return div_rn(1.0, add_rn(1.0, exp(-z)));
+    const double ez = exp(z);
+    return div_rn(ez, add_rn(1.0, ez));
+}
+
+// numpy logaddexp(0, z)
+__device__ __forceinline__ double logaddexp0(double z) {
+    const double x = 0.0;
+    if (x == z) return x + 0.69314718055994530942;
+    const double tmp = x - z;
+    if (tmp > 0.0) return add_rn(x, log1p(exp(-tmp)));
+    if (tmp <= 0.0) return add_rn(z, log1p(exp(tmp)));
+    return tmp;   // NaN
+}
+
+// grad/h for f; per-CTA partials of  -sum logaddexp(0, -y f)  and  f'a (a may be NULL)
+__global__ void derivs_kernel(long long n, const double* f, const double* y, const double* a, double* grad,
+                              double* h, double* part) {
+    __shared__ double red[40];
+    double ll = 0.0, fa = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double fi = f[i], yi = y[i];
+        ll += logaddexp0(mul_rn(-yi, fi));
+        const double pi = sigmoid_ref(fi);
+        grad[i] = sub_rn(mul_rn(add_rn(yi, 1.0), 0.5), pi);
+        h[i] = mul_rn(pi, sigmoid_ref(-fi));
+        if (a) fa = fma(fi, a[i], fa);
+    }
+    ll = block_sum(ll, red);
+    fa = block_sum(fa, red);
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = ll;
+        part[2 * blockIdx.x + 1] = fa;
+    }
+}
+
+__global__ void derivs_finalize_kernel(const double* part, int nb, DevStatus* st) {
+    __shared__ double red[40];
+    double ll = 0.0, fa = 0.0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        ll += part[2 * b];
+        fa += part[2 * b + 1];
+    }
+    ll = block_sum(ll, red);
+    fa = block_sum(fa, red);
+    if (threadIdx.x == 0) {
+        const double loglik = -ll;
+        st->status = DCG_OK;
+        st->value = loglik;
+        st->value2 = sub_rn(loglik, mul_rn(0.5, fa));   // psi = loglik - f'a/2 (gpc.py:209)
+    }
+}
+
+// s = sqrt(h); inner = h f + grad   (gpc.py:177,181)
+__global__ void newton_prep_kernel(long long n, const double* f, const double* grad, const double* h, double* s,
+                                   double* inner) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        s[i] = sqrt(h[i]);
+        inner[i] = add_rn(mul_rn(h[i], f[i]), grad[i]);
+    }
+}
+
+// a = inner - s x   (gpc.py:190)
+__global__ void newton_a_kernel(long long n, const double* inner, const double* s, const double* x, double* a) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        a[i] = sub_rn(inner[i], mul_rn(s[i], x[i]));
+}
+
+int dcg_derivs_launch(dcg_context* ctx, cudaStream_t st, long long n, const double* f, const double* y,
+                      const double* a, double* grad, double* h, double* part, DevStatus* ds) {
+    int nb = ctx->sm_count * 2;
+    if ((long long)nb * 256 > n) nb = (int)max(1LL, (n + 255) / 256);
+    derivs_kernel<<<nb, 256, 0, st>>>(n, f, y, a, grad, h, part);
+    DCG_CUDA(cudaGetLastError());
+    derivs_finalize_kernel<<<1, 256, 0, st>>>(part, nb, ds);
+    DCG_CUDA(cudaGetLastError());
+    return DCG_OK;
+}
+
+int dcg_newton_prep_launch(dcg_context* ctx, cudaStream_t st, long long n, const double* f, const double* grad,
+                           const double* h, double* s, double* inner) {
+    newton_prep_kernel<<<ctx->sm_count * 2, 256, 0, st>>>(n, f, grad, h, s, inner);
+    DCG_CUDA(cudaGetLastError());
+    return DCG_OK;
+}
+
+int dcg_newton_a_launch(dcg_context* ctx, cudaStream_t st, long long n, const double* inner, const double* s,
+                        const double* x, double* a) {
+    newton_a_kernel<<<ctx->sm_count * 2, 256, 0, st>>>(n, inner, s, x, a);
+    DCG_CUDA(cudaGetLastError());
+    return DCG_OK;
+}

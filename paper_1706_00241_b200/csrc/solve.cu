@@ -1,0 +1,476 @@
+// The whole CG / deflated-CG solve as ONE persistent cooperative kernel.
+//
+// Restates solvers.py:_run_loop (131-204) together with the warm-start
+// correction of deflated_cg_solve (222-239): there is no host round trip per
+// iteration.  One CTA per SM owns a contiguous, balanced row range of the
+// system.  Per iteration:
+//   phase G  Ap = shift p + s (.) K (s (.) p) for own rows, partial p'Ap   | grid barrier
+//   phase U  alpha; x += alpha p; r -= alpha Ap (or true residual every
+//            `recompute` iterations); partial r'r and AW'r (k dots)         | grid barrier
+//   phase P  beta, mu = L^-T L^-1 AW'r (each CTA, redundantly), p update,
+//            residual history / Krylov log writes                           | grid barrier
+// Scalars are reduced from per-CTA partials in a fixed order by every CTA,
+// so all CTAs take identical control-flow decisions (convergence, breakdown,
+// max_iters) without a second barrier, and results are bit-reproducible.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "gemv.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+struct SolveArgs {
+    const double* K;
+    long long ldk;
+    long long n;
+    const double* s;
+    double shift;
+    const double* b;
+    const double* x0;
+    double* x;
+    int k;
+    const double* W;
+    const double* AW;
+    const double* L;
+    int warm;
+    double tol;
+    long long max_iters;
+    long long ell;
+    long long recompute;
+    double* logP;
+    double* logR;
+    double* logD;
+    double* logAlpha;
+    double* logBeta;
+    double* logMu;
+    double* history;
+    double* r;
+    double* p;
+    double* ap;
+    double* partials;
+    int ps;   // partial stride (doubles)
+    DevStatus* st;
+};
+
+// x = L^-T L^-1 c for a k x k row-major lower factor in shared memory, by one
+// warp (lanes own rows lane and lane+32).  Substitution follows the reference
+// order for the forward sweep (_core.pyx:69-80); the backward sweep runs as a
+// wavefront.  `rdiag` holds 1/L[j][j].
+__device__ void warp_chol_solve(const double* L, const double* rdiag, int k, const double* c,
+                                double* out) {
+    const int lane = threadIdx.x & 31;
+    const int i0 = lane, i1 = lane + 32;
+    double a0 = (i0 < k) ? c[i0] : 0.0;
+    double a1 = (i1 < k) ? c[i1] : 0.0;
+    for (int j = 0; j < k; ++j) {
+        const double accj = __shfl_sync(0xffffffffu, (j < 32) ? a0 : a1, j & 31);
+        const double yj = mul_rn(accj, rdiag[j]);
+        if (lane == (j & 31)) {
+            if (j < 32) a0 = yj; else a1 = yj;
+        }
+        if (i0 > j && i0 < k) a0 = sub_rn(a0, mul_rn(L[i0 * k + j], yj));
+        if (i1 > j && i1 < k) a1 = sub_rn(a1, mul_rn(L[i1 * k + j], yj));
+    }
+    for (int j = k - 1; j >= 0; --j) {
+        const double accj = __shfl_sync(0xffffffffu, (j < 32) ? a0 : a1, j & 31);
+        const double xj = mul_rn(accj, rdiag[j]);
+        if (lane == (j & 31)) {
+            if (j < 32) a0 = xj; else a1 = xj;
+        }
+        if (i0 < j) a0 = sub_rn(a0, mul_rn(L[j * k + i0], xj));
+        if (i1 < j && i1 < k) a1 = sub_rn(a1, mul_rn(L[j * k + i1], xj));
+    }
+    if (i0 < k) out[i0] = a0;
+    if (i1 < k) out[i1] = a1;
+}
+
+// Fixed-order reduction of the per-CTA partials into shared memory (every CTA
+// computes the identical values).
+__device__ __forceinline__ void reduce_partials(const double* partials, int G, int ps, int nslots,
+                                                double* out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int v = warp; v < nslots; v += DCG_NW) {
+        double acc = 0.0;
+        for (int g = lane; g < G; g += 32) acc += ld_cg(partials + (long long)g * ps + v);
+        acc = warp_sum(acc);
+        if (lane == 0) out[v] = acc;
+    }
+    __syncthreads();
+}
+
+// Sum per-warp partial rows s_wp[w][0..nslots) over warps and publish.
+__device__ __forceinline__ void publish_partials(const double* s_wp, int nslots, double* partials,
+                                                 int ps) {
+    __syncthreads();
+    for (int v = threadIdx.x; v < nslots; v += blockDim.x) {
+        double acc = 0.0;
+        for (int w = 0; w < DCG_NW; ++w) acc += s_wp[w * (DCG_MAX_K + 1) + v];
+        partials[(long long)blockIdx.x * ps + v] = acc;
+    }
+}
+
+// Per-warp accumulation of  slot0 += a_i^2  and  slot(1+j) += M[i][j] * a_i
+// over the rows this warp owns; leaves results in s_wp[warp][*].
+struct WarpAcc {
+    double sq;
+    double c0, c1;
+};
+
+__global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) double smem[];
+    const long long n = a.n;
+    const int k = a.k;
+    const int G = gridDim.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int xt = (int)min(n, (long long)DCG_QT) + 2;
+    double* s_x = smem;                                  // xt
+    double* s_red = s_x + xt;                            // DCG_NW * DCG_RB
+    double* s_L = s_red + DCG_NW * DCG_RB;               // k*k
+    double* s_rd = s_L + k * k;                          // k   (1/L_jj)
+    double* s_c = s_rd + DCG_MAX_K;                      // 1 + DCG_MAX_K reduced slots
+    double* s_mu = s_c + DCG_MAX_K + 2;                  // DCG_MAX_K
+    double* s_wp = s_mu + DCG_MAX_K;                     // DCG_NW * (DCG_MAX_K + 1)
+    double* s_tmp = s_wp + DCG_NW * (DCG_MAX_K + 1);     // 64 scratch
+
+    const long long r0 = part_begin(n, G, blockIdx.x);
+    const long long r1 = part_begin(n, G, blockIdx.x + 1);
+    const bool deflate = k > 0;
+    const int nslots = 1 + k;
+    const double* __restrict__ K = a.K;
+    const double* s = a.s;
+    const double shift = a.shift;
+
+    for (int i = tid; i < k * k; i += blockDim.x) s_L[i] = a.L[i];
+    __syncthreads();
+    for (int j = tid; j < k; j += blockDim.x) s_rd[j] = 1.0 / s_L[j * k + j];
+    __syncthreads();
+
+    // Accumulate over own rows (warp-per-row): sq += u_i^2 and c_j += M[i][j] * u_i,
+    // u_i produced by `rowfn(i)` executed on all lanes (value must be uniform).
+    auto warp_rows_partials = [&](auto rowfn, const double* M, bool with_sq) {
+        double sq = 0.0, c0 = 0.0, c1 = 0.0;
+        for (long long i = r0 + warp; i < r1; i += DCG_NW) {
+            const double u = rowfn(i);
+            if (with_sq) sq = add_rn(sq, mul_rn(u, u));
+            if (M) {
+                if (lane < k) c0 = fma(M[i * k + lane], u, c0);
+                if (lane + 32 < k) c1 = fma(M[i * k + lane + 32], u, c1);
+            }
+        }
+        if (lane == 0) s_wp[warp * (DCG_MAX_K + 1)] = sq;
+        if (M) {
+            if (lane < k) s_wp[warp * (DCG_MAX_K + 1) + 1 + lane] = c0;
+            if (lane + 32 < k) s_wp[warp * (DCG_MAX_K + 1) + 33 + lane] = c1;
+        }
+    };
+    // sum_j M[i][j] * v[j] for row i, uniform across the warp.
+    auto row_dot = [&](const double* M, long long i, const double* v) {
+        double t = 0.0;
+        if (lane < k) t = M[i * k + lane] * v[lane];
+        if (lane + 32 < k) t = fma(M[i * k + lane + 32], v[lane + 32], t);
+        return warp_sum(t);
+    };
+
+    // ---------------- prologue: norm_b and the warm-start correction ----------
+    // deflated_cg_solve: r_prev = b - A x_prev ; x0 = x_prev + W chol_solve(L, W' r_prev)
+    if (a.warm && deflate) {
+        block_gemv<false>(K, a.ldk, n, a.x0, s, r0, r1, s_x, s_red, [&](long long i, double t) {
+            const double ax = s ? add_rn(mul_rn(shift, a.x0[i]), mul_rn(s[i], t))
+                                : add_rn(mul_rn(shift, a.x0[i]), t);
+            a.r[i] = sub_rn(a.b[i], ax);
+        });
+        __syncthreads();
+        // slot0 = b'b, slots 1.. = W' r_prev
+        {
+            double sq = 0.0, c0 = 0.0, c1 = 0.0;
+            for (long long i = r0 + warp; i < r1; i += DCG_NW) {
+                const double bi = a.b[i];
+                const double ri = a.r[i];
+                sq = fma(bi, bi, sq);
+                if (lane < k) c0 = fma(a.W[i * k + lane], ri, c0);
+                if (lane + 32 < k) c1 = fma(a.W[i * k + lane + 32], ri, c1);
+            }
+            if (lane == 0) s_wp[warp * (DCG_MAX_K + 1)] = sq;
+            if (lane < k) s_wp[warp * (DCG_MAX_K + 1) + 1 + lane] = c0;
+            if (lane + 32 < k) s_wp[warp * (DCG_MAX_K + 1) + 33 + lane] = c1;
+        }
+        publish_partials(s_wp, nslots, a.partials, a.ps);
+    } else {
+        double sq = 0.0;
+        for (long long i = r0 + tid; i < r1; i += blockDim.x) sq = fma(a.b[i], a.b[i], sq);
+        sq = block_sum(sq, s_tmp);
+        if (tid == 0) a.partials[(long long)blockIdx.x * a.ps] = sq;
+    }
+    grid.sync();
+    reduce_partials(a.partials, G, a.ps, (a.warm && deflate) ? nslots : 1, s_c);
+    const double norm_b = sqrt(s_c[0]);
+    if (norm_b == 0.0) {
+        // solvers.py:142-147: x = 0 (not x0), history [0.0], log.r = [0]
+        for (long long i = r0 + tid; i < r1; i += blockDim.x) {
+            a.x[i] = 0.0;
+            if (a.logR) a.logR[i] = 0.0;
+        }
+        if (blockIdx.x == 0 && tid == 0) {
+            a.history[0] = 0.0;
+            a.st->status = DCG_OK;
+            a.st->info = 0;
+            a.st->count = 0;   // iterations
+            a.st->aux = 0;     // stored
+            a.st->value = 0.0;
+            a.st->value2 = 0.0;
+        }
+        return;
+    }
+    if (a.warm && deflate) {
+        if (warp == 0) warp_chol_solve(s_L, s_rd, k, s_c + 1, s_mu);
+        __syncthreads();
+        for (long long i = r0 + warp; i < r1; i += DCG_NW) {
+            const double wy = row_dot(a.W, i, s_mu);
+            if (lane == 0) a.x[i] = add_rn(a.x0[i], wy);
+        }
+    } else {
+        for (long long i = r0 + tid; i < r1; i += blockDim.x) a.x[i] = a.x0[i];
+    }
+    grid.sync();
+
+    // ---------------- r0 = b - A x0 ; mu ; p0 ------------------------------------
+    block_gemv<true>(K, a.ldk, n, a.x, s, r0, r1, s_x, s_red, [&](long long i, double t) {
+        const double xi = a.x[i];
+        const double ax = s ? add_rn(mul_rn(shift, xi), mul_rn(s[i], t)) : add_rn(mul_rn(shift, xi), t);
+        a.r[i] = sub_rn(a.b[i], ax);
+    });
+    __syncthreads();
+    warp_rows_partials([&](long long i) { return a.r[i]; }, deflate ? a.AW : nullptr, true);
+    publish_partials(s_wp, nslots, a.partials, a.ps);
+    grid.sync();
+    reduce_partials(a.partials, G, a.ps, nslots, s_c);
+    double rr = s_c[0];
+    if (deflate) {
+        if (warp == 0) warp_chol_solve(s_L, s_rd, k, s_c + 1, s_mu);
+        __syncthreads();
+    }
+    double rel = sqrt(rr) / norm_b;
+    long long it = 0;
+    const long long ell = a.ell;
+    bool cont = (rel > a.tol) && (it < a.max_iters);
+    // p0 (+ log r0, p0, mu0)
+    for (long long i = r0 + warp; i < r1; i += DCG_NW) {
+        const double ri = a.r[i];
+        double pi;
+        if (deflate) {
+            const double wm = row_dot(a.W, i, s_mu);
+            pi = sub_rn(ri, wm);
+        } else {
+            pi = ri;
+        }
+        if (lane == 0) {
+            a.p[i] = pi;
+            if (a.logR) a.logR[i] = ri;
+            if (cont && it < ell) a.logP[i] = pi;
+        }
+    }
+    if (blockIdx.x == 0) {
+        if (tid == 0) a.history[0] = rel;
+        if (deflate && cont && it < ell && tid < k) a.logMu[tid] = s_mu[tid];
+    }
+    grid.sync();
+
+    // ---------------- main loop ------------------------------------------------
+    while (cont) {
+        // phase G: Ap, partial p'Ap
+        double dpart = 0.0;
+        block_gemv<true>(K, a.ldk, n, a.p, s, r0, r1, s_x, s_red, [&](long long i, double t) {
+            const double pi = ld_cg(a.p + i);
+            const double api = s ? add_rn(mul_rn(shift, pi), mul_rn(s[i], t)) : add_rn(mul_rn(shift, pi), t);
+            a.ap[i] = api;
+            dpart = fma(pi, api, dpart);
+        });
+        dpart = block_sum(dpart, s_tmp);
+        if (tid == 0) a.partials[(long long)blockIdx.x * a.ps] = dpart;
+        grid.sync();
+        reduce_partials(a.partials, G, a.ps, 1, s_c);
+        const double d = s_c[0];
+        if (d <= 0.0) {   // solvers.py:170-172 (NaN falls through, as in numpy)
+            if (blockIdx.x == 0 && tid == 0) {
+                a.st->status = DCG_E_BREAKDOWN;
+                a.st->info = it;
+                a.st->count = it;
+            }
+            return;
+        }
+        const double alpha = rr / d;
+        for (long long i = r0 + tid; i < r1; i += blockDim.x)
+            a.x[i] = add_rn(a.x[i], mul_rn(alpha, a.p[i]));
+        ++it;
+        const bool recompute = (a.recompute > 0) && (it % a.recompute == 0);
+        if (recompute) {
+            grid.sync();
+            block_gemv<true>(K, a.ldk, n, a.x, s, r0, r1, s_x, s_red, [&](long long i, double t) {
+                const double xi = a.x[i];
+                const double ax = s ? add_rn(mul_rn(shift, xi), mul_rn(s[i], t)) : add_rn(mul_rn(shift, xi), t);
+                a.r[i] = sub_rn(a.b[i], ax);
+            });
+        } else {
+            for (long long i = r0 + tid; i < r1; i += blockDim.x)
+                a.r[i] = sub_rn(a.r[i], mul_rn(alpha, a.ap[i]));
+        }
+        __syncthreads();
+        const bool log_r = (it - 1) < ell;
+        warp_rows_partials(
+            [&](long long i) {
+                const double ri = a.r[i];
+                if (log_r && lane == 0) a.logR[it * n + i] = ri;
+                return ri;
+            },
+            deflate ? a.AW : nullptr, true);
+        publish_partials(s_wp, nslots, a.partials, a.ps);
+        grid.sync();
+        reduce_partials(a.partials, G, a.ps, nslots, s_c);
+        const double rr_new = s_c[0];
+        const double beta = rr_new / rr;
+        rel = sqrt(rr_new) / norm_b;
+        if (blockIdx.x == 0 && tid == 0) {
+            a.history[it] = rel;
+            if (log_r) {
+                a.logD[it - 1] = d;
+                a.logAlpha[it - 1] = alpha;
+                a.logBeta[it - 1] = beta;
+            }
+        }
+        if (deflate) {
+            if (warp == 0) warp_chol_solve(s_L, s_rd, k, s_c + 1, s_mu);
+            __syncthreads();
+        }
+        cont = (rel > a.tol) && (it < a.max_iters);
+        const bool log_p = cont && it < ell;
+        for (long long i = r0 + warp; i < r1; i += DCG_NW) {
+            const double ri = a.r[i];
+            double pi;
+            if (deflate) {
+                const double wm = row_dot(a.W, i, s_mu);
+                pi = sub_rn(add_rn(mul_rn(beta, a.p[i]), ri), wm);   // beta*p + r - W mu
+            } else {
+                pi = add_rn(ri, mul_rn(beta, a.p[i]));               // r + beta*p
+            }
+            if (lane == 0) {
+                a.p[i] = pi;
+                if (log_p) a.logP[it * n + i] = pi;
+            }
+        }
+        if (log_p && deflate && blockIdx.x == 0 && tid < k) a.logMu[it * k + tid] = s_mu[tid];
+        rr = rr_new;
+        grid.sync();
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        a.st->status = DCG_OK;
+        a.st->info = 0;
+        a.st->count = it;
+        a.st->aux = (it < ell) ? it : ell;
+        a.st->value = rel;
+        a.st->value2 = norm_b;
+    }
+}
+
+}  // namespace
+
+size_t dcg_solve_smem_bytes(long long n, int k) {
+    const long long xt = (n < DCG_QT ? n : DCG_QT) + 2;
+    return sizeof(double) * (size_t)(xt + DCG_NW * DCG_RB + k * k + DCG_MAX_K + DCG_MAX_K + 2 +
+                                     DCG_MAX_K + DCG_NW * (DCG_MAX_K + 1) + 64);
+}
+
+extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_b,
+                         const double* d_x0, const dcg_basis* basis, const dcg_solver_config* cfg,
+                         double* d_x, dcg_krylov_log* log, double* d_history, dcg_solve_info* out,
+                         long long* info) {
+    if (!ctx || !op || !cfg || !d_b || !d_x0 || !d_x || !d_history) return DCG_E_CONFIG;
+    if (info) *info = 0;
+    const long long n = op->n;
+    if (op->kind != DCG_OP_DENSE) return DCG_E_UNSUPPORTED;
+    if (op->row0 != 0 || op->rows != n) return DCG_E_UNSUPPORTED;   // sharded solves: host loop
+    if (op->ldk < n || (op->ldk & 1) || (reinterpret_cast<uintptr_t>(op->d_k) & 15)) return DCG_E_CONFIG;
+    if (!(cfg->tol > 0.0) || cfg->ell < 0 || cfg->recompute_residual_every < 0) return DCG_E_CONFIG;
+    const int k = basis ? (int)basis->k : 0;
+    if (k < 0) return DCG_E_CONFIG;
+    if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
+    if (k > 0 && (!basis->d_w || !basis->d_aw || !basis->d_chol)) return DCG_E_CONFIG;
+    const long long ell = log ? log->ell : 0;
+    if (cfg->ell > 0 && (!log || ell < cfg->ell || !log->d_p || !log->d_r || !log->d_d ||
+                         !log->d_alpha || !log->d_beta || (k > 0 && !log->d_mu)))
+        return DCG_E_CONFIG;
+    const long long max_iters = cfg->max_iters > 0 ? cfg->max_iters : 10 * n;
+
+    const int G = ctx->solve_blocks;
+    const int ps = ((1 + k) + 1) & ~1;
+    const size_t vec = sizeof(double) * (size_t)((n + 31) & ~31LL);
+    const size_t need = 3 * vec + sizeof(double) * (size_t)G * ps + 256;
+    int rc = dcg_ws_reserve(ctx, need);
+    if (rc) return rc;
+    char* w = static_cast<char*>(ctx->ws);
+    SolveArgs a;
+    a.K = op->d_k;
+    a.ldk = op->ldk;
+    a.n = n;
+    a.s = op->d_s;
+    a.shift = op->shift;
+    a.b = d_b;
+    a.x0 = d_x0;
+    a.x = d_x;
+    a.k = k;
+    a.W = k ? basis->d_w : nullptr;
+    a.AW = k ? basis->d_aw : nullptr;
+    a.L = k ? basis->d_chol : nullptr;
+    a.warm = k > 0;
+    a.tol = cfg->tol;
+    a.max_iters = max_iters;
+    a.ell = cfg->ell;
+    a.recompute = cfg->recompute_residual_every;
+    a.logP = log ? log->d_p : nullptr;
+    a.logR = log ? log->d_r : nullptr;
+    a.logD = log ? log->d_d : nullptr;
+    a.logAlpha = log ? log->d_alpha : nullptr;
+    a.logBeta = log ? log->d_beta : nullptr;
+    a.logMu = log ? log->d_mu : nullptr;
+    a.history = d_history;
+    a.r = reinterpret_cast<double*>(w);
+    a.p = reinterpret_cast<double*>(w + vec);
+    a.ap = reinterpret_cast<double*>(w + 2 * vec);
+    a.partials = reinterpret_cast<double*>(w + 3 * vec);
+    a.ps = ps;
+    a.st = reinterpret_cast<DevStatus*>(w + 3 * vec + sizeof(double) * (size_t)G * ps);
+
+    cudaStream_t st = as_stream(stream);
+    const size_t smem = dcg_solve_smem_bytes(n, k);
+    DCG_CUDA(cudaFuncSetAttribute(dcg_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    DCG_CUDA(cudaMemsetAsync(a.st, 0, sizeof(DevStatus), st));
+    void* args[] = {&a};
+    DCG_CUDA(cudaEventRecord(ctx->ev0, st));
+    DCG_CUDA(cudaLaunchCooperativeKernel((const void*)dcg_solve_kernel, dim3(G), dim3(DCG_NT), args,
+                                         smem, st));
+    DCG_CUDA(cudaEventRecord(ctx->ev1, st));
+    rc = dcg_host_reserve(ctx, sizeof(DevStatus));
+    if (rc) return rc;
+    DevStatus* hs = static_cast<DevStatus*>(ctx->host);
+    DCG_CUDA(cudaMemcpyAsync(hs, a.st, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+    DCG_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    if (hs->status != DCG_OK) {
+        if (info) *info = hs->info;
+        return hs->status;
+    }
+    if (out) {
+        out->iterations = hs->count;
+        out->stored = hs->aux;
+        out->rel_residual = hs->value;
+        out->norm_b = hs->value2;
+        out->converged = hs->value <= cfg->tol ? 1 : 0;
+        out->termination = out->converged ? 0 : 1;
+        out->device_ms = ms;
+    }
+    return DCG_OK;
+}

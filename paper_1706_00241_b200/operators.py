@@ -1,0 +1,146 @@
+"""SPD operators resident in HBM.
+
+The reference accepts only an explicit dense ndarray for A and rebuilds it
+for every Newton system (``gpc.py:178``: ``K * outer(s, s)`` plus the unit
+diagonal), then re-validates its symmetry twice per solve (``solvers.py:123``,
+``recycle.py:86``).  Here the matrix lives in HBM once, with a 256-byte row
+pitch, and a Newton system is the same K viewed as
+
+    A = shift * I + diag(s) K diag(s)        (Newton: s = sqrt(h), shift = 1)
+
+so no n x n array is ever re-materialised.  Raw matrices (numpy or torch) are
+still accepted everywhere and wrapped with a one-time on-device symmetry check
+(the reference's ``require_symmetric`` semantics, ``linalg.py:49-55``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _device as D
+from . import _native as N
+from .errors import DimensionMismatch
+
+SYMMETRY_RTOL = 1e-12
+
+
+class DenseOperator:
+    """A = shift*I + diag(s) K diag(s) over a dense fp64 K in HBM."""
+
+    __array_priority__ = 100
+
+    def __init__(self, kbuf: torch.Tensor, n: int, ldk: int, s: torch.Tensor | None = None, shift: float = 0.0,
+                 row0: int = 0, rows: int | None = None):
+        self.kbuf = kbuf
+        self.n = int(n)
+        self.ldk = int(ldk)
+        self.s = s
+        self.shift = float(shift)
+        self.row0 = int(row0)
+        self.rows = self.n if rows is None else int(rows)
+
+    # -- construction ---------------------------------------------------------
+    @classmethod
+    def from_matrix(cls, a, check_symmetric: bool = True, rtol: float = SYMMETRY_RTOL) -> "DenseOperator":
+        """Upload a square matrix; raises DimensionMismatch / ValueError like
+        ``require_symmetric`` (linalg.py:28-55)."""
+        if isinstance(a, DenseOperator):
+            return a
+        if not isinstance(a, torch.Tensor):
+            a = np.ascontiguousarray(a, dtype=np.float64)
+        if a.ndim != 2:
+            raise DimensionMismatch(f"expected a matrix, got ndim={a.ndim}")
+        if a.shape[0] != a.shape[1]:
+            raise DimensionMismatch(f"expected square matrix, got {tuple(a.shape)}")
+        kbuf, ld = D.to_dev_padded(a)
+        op = cls(kbuf, a.shape[0], ld)
+        if check_symmetric:
+            op.require_symmetric(rtol)
+        return op
+
+    def require_symmetric(self, rtol: float = SYMMETRY_RTOL) -> "DenseOperator":
+        if self.n == 0:
+            return self
+        ok = ctypes.c_int()
+        N.check(N.lib().dcg_check_symmetric(D.ctx(), D.stream(), self.kbuf.data_ptr(), self.n, self.ldk, rtol,
+                                            ctypes.byref(ok)), what="check_symmetric")
+        if not ok.value:
+            raise ValueError("matrix is not symmetric within tolerance")
+        return self
+
+    def scaled(self, s, shift: float) -> "DenseOperator":
+        """Same K, new diagonal scaling and shift (the Newton system of gpc.py:175-183)."""
+        s_dev = None if s is None else D.to_dev(s, 1)
+        return DenseOperator(self.kbuf, self.n, self.ldk, s_dev, shift, self.row0, self.rows)
+
+    # -- views ------------------------------------------------------------------
+    @property
+    def shape(self):
+        return (self.n, self.n)
+
+    @property
+    def ndim(self):
+        return 2
+
+    def c_struct(self) -> N.COperator:
+        op = N.COperator()
+        op.kind = N.DCG_OP_DENSE
+        op.n = self.n
+        op.row0 = self.row0
+        op.rows = self.rows
+        op.d_k = self.kbuf.data_ptr() if self.n else None
+        op.ldk = self.ldk
+        op.d_s = None if self.s is None else self.s.data_ptr()
+        op.shift = self.shift
+        return op
+
+    def kernel_view(self) -> "DenseOperator":
+        """K itself (no scaling, no shift)."""
+        return DenseOperator(self.kbuf, self.n, self.ldk, None, 0.0, self.row0, self.rows)
+
+    def matvec_dev(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        y = D.empty(self.rows) if out is None else out
+        if self.rows:
+            op = self.c_struct()
+            N.check(N.lib().dcg_op_apply(D.ctx(), D.stream(), ctypes.byref(op), x.data_ptr(), y.data_ptr()),
+                    what="op_apply")
+        return y
+
+    def apply_block_dev(self, w: torch.Tensor) -> torch.Tensor:
+        k = w.shape[1]
+        y = D.empty(self.rows, k)
+        if self.rows and k:
+            op = self.c_struct()
+            N.check(N.lib().dcg_op_apply_block(D.ctx(), D.stream(), ctypes.byref(op), w.data_ptr(), k,
+                                               y.data_ptr()), what="op_apply_block")
+        return y
+
+    def dense_dev(self) -> torch.Tensor:
+        """Explicit A on device (tests / small problems only)."""
+        a = self.kbuf[: self.rows, : self.n].clone()
+        if self.s is not None:
+            a = a * self.s[self.row0 : self.row0 + self.rows, None] * self.s[None, :]
+        if self.shift:
+            idx = torch.arange(self.rows, device=a.device)
+            a[idx, idx + self.row0] += self.shift
+        return a
+
+    def __array__(self, dtype=None, copy=None):
+        arr = self.dense_dev().cpu().numpy()
+        return arr if dtype is None else arr.astype(dtype)
+
+    def __matmul__(self, other):
+        """A @ x for a vector or n x k block (numpy in -> numpy out)."""
+        x = D.to_dev(other)
+        y = self.matvec_dev(x) if x.ndim == 1 else self.apply_block_dev(x)
+        return D.out_like(y, other)
+
+
+def as_operator(a) -> DenseOperator:
+    """Operator for any accepted matrix argument (validates raw matrices once)."""
+    if isinstance(a, DenseOperator):
+        return a
+    return DenseOperator.from_matrix(a)

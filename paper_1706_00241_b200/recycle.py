@@ -1,0 +1,172 @@
+"""Subspace recycling — the drop-in for defcg.recycle.
+
+``refresh_basis``, ``harmonic_ritz_extract``, ``SequenceState`` and
+``solve_next`` keep the reference's names, defaults and semantics
+(/root/reference/pkg/src/defcg/recycle.py:31-203), including the two places
+where ``BasisDeficient`` is swallowed (recycle.py:178-179, 194-195) so the
+sequence silently degrades to plain CG exactly when the reference does.
+W, AW, the Krylov log and the warm start stay in HBM across the sequence:
+
+  refresh   AW = A W in one pass over K on FP64 tensor cores, W'AW and the
+            failing-pivot pruning Cholesky in one CTA      (dcg_refresh_basis)
+  solve     the persistent CG / def-CG kernel              (dcg_solve)
+  extract   Z = [W, P_m], AZ = [AW, (r_j - r_j+1)/alpha_j] normalised, the
+            harmonic pencil F, G, pruning + Jacobi in one CTA, W_next = Z U
+                                                           (dcg_ritz_extract)
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from . import _device as D
+from . import _native as N
+from .errors import BasisDeficient, DimensionMismatch
+from .operators import as_operator
+from .solvers import KrylovLog, RecycleBasis, SolverConfig, _solve_dev
+
+SELECT_SMALLEST = "smallest"
+SELECT_LARGEST = "largest"
+
+
+class RitzExtraction:
+    """Harmonic Ritz values/vectors chosen for the next basis (recycle.py:31-46).
+
+    Device tensors ``*_dev``; numpy views ``theta``, ``u``, ``z``, ``w_next``,
+    ``aw_next`` materialise on access."""
+
+    def __init__(self, theta, u, z, w_next, aw_next, selection):
+        self.theta_dev, self.u_dev, self.z_dev = theta, u, z
+        self.w_next_dev, self.aw_next_dev = w_next, aw_next
+        self.selection = selection
+
+    theta = property(lambda self: self.theta_dev.cpu().numpy())
+    u = property(lambda self: self.u_dev.cpu().numpy())
+    z = property(lambda self: self.z_dev.cpu().numpy())
+    w_next = property(lambda self: self.w_next_dev.cpu().numpy())
+    aw_next = property(lambda self: self.aw_next_dev.cpu().numpy())
+
+
+@dataclass
+class SequenceState:
+    """Carry-over between solves of a sequence (recycle.py:49-63)."""
+
+    k: int
+    cfg: SolverConfig = field(default_factory=SolverConfig)
+    selection: str = SELECT_SMALLEST
+    basis: RecycleBasis | None = None
+    x_last: object | None = None
+    history: list = field(default_factory=list)
+
+
+def _refresh_dev(op, w_dev: torch.Tensor) -> RecycleBasis:
+    n, k = w_dev.shape
+    if k == 0:
+        return RecycleBasis(w_dev, w_dev.clone(), D.empty(0, 0))
+    if op.n != n:
+        raise DimensionMismatch(f"basis rows {n} vs operator size {op.n}")
+    w_out, aw_out, chol = D.empty(n, k), D.empty(n, k), D.empty(k, k)
+    kout, info = ctypes.c_longlong(k), ctypes.c_longlong(0)
+    cop = op.c_struct()
+    rc = N.lib().dcg_refresh_basis(D.ctx(), D.stream(), ctypes.byref(cop), w_dev.data_ptr(), k, w_out.data_ptr(),
+                                   aw_out.data_ptr(), chol.data_ptr(), ctypes.byref(kout), ctypes.byref(info))
+    N.check(rc, info.value, "refresh_basis")
+    kk = int(kout.value)
+    basis = RecycleBasis.__new__(RecycleBasis)
+    basis.w_dev = w_out[:, :kk].contiguous() if kk != k else w_out
+    basis.aw_dev = aw_out[:, :kk].contiguous() if kk != k else aw_out
+    basis.chol_dev = chol.view(-1)[: kk * kk].view(kk, kk)
+    return basis
+
+
+def refresh_basis(a_next, w):
+    """Rebuild a RecycleBasis for a new matrix: AW against a_next, W'AW
+    factored with failing-pivot pruning (recycle.py:80-92).  Raises
+    BasisDeficient(0) when nothing survives."""
+    op = as_operator(a_next)
+    if not isinstance(w, torch.Tensor):
+        w = np.ascontiguousarray(w, dtype=np.float64)
+    if w.ndim != 2:
+        raise DimensionMismatch(f"expected a matrix, got ndim={w.ndim}")
+    return _refresh_dev(op, D.to_dev(w, 2))
+
+
+def _extract_dev(log: KrylovLog, prev: RecycleBasis | None, k: int, selection: str) -> RitzExtraction:
+    if selection not in (SELECT_SMALLEST, SELECT_LARGEST):
+        raise ValueError(f"unknown selection {selection!r}")
+    m = log.stored_iterations
+    kp = prev.k if prev is not None else 0
+    total = kp + m
+    if k > total:
+        raise BasisDeficient(total)
+    n = log.n
+    if k == 0:
+        e = D.empty(n, 0)
+        return RitzExtraction(D.empty(0), D.empty(total, 0), e, e, e.clone(), selection)
+    theta = D.empty(k)
+    u = D.empty(total, k)
+    z = D.empty(n, total)
+    w_next, aw_next = D.empty(n, k), D.empty(n, k)
+    t_out, info = ctypes.c_longlong(total), ctypes.c_longlong(0)
+    clog = log.c_struct()
+    cprev = prev.c_struct() if kp else None
+    rc = N.lib().dcg_ritz_extract(D.ctx(), D.stream(), n, ctypes.byref(clog), m,
+                                  ctypes.byref(cprev) if cprev is not None else None, k,
+                                  N.DCG_SELECT_LARGEST if selection == SELECT_LARGEST else N.DCG_SELECT_SMALLEST,
+                                  theta.data_ptr(), u.data_ptr(), z.data_ptr(), w_next.data_ptr(), aw_next.data_ptr(),
+                                  ctypes.byref(t_out), ctypes.byref(info))
+    N.check(rc, info.value, "ritz_extract")
+    t = int(t_out.value)
+    return RitzExtraction(theta, u.view(-1)[: t * k].view(t, k), z.view(-1)[: n * t].view(n, t), w_next, aw_next,
+                          selection)
+
+
+def harmonic_ritz_extract(log, prev_basis, k, selection=SELECT_SMALLEST):
+    """Extract k approximate eigenvectors from a finished solve (recycle.py:95-159).
+
+    Raises BasisDeficient when fewer than k independent columns remain."""
+    return _extract_dev(log, prev_basis, int(k), selection)
+
+
+def solve_next(state, a, b):
+    """Solve the next system of a sequence, recycling the deflation basis
+    (recycle.py:162-203).  Returns (x, new_state)."""
+    host = not isinstance(b, torch.Tensor)
+    if host:
+        b = np.ascontiguousarray(b, dtype=np.float64)
+    op = as_operator(a)
+    bd = D.to_dev(b, 1)
+    n = bd.shape[0]
+    if op.n != n:
+        raise DimensionMismatch(f"system shapes {op.shape}, {tuple(bd.shape)}")
+    x_prev = D.zeros(n) if state.x_last is None else D.to_dev(state.x_last, 1)
+    if x_prev.shape[0] != n:
+        raise DimensionMismatch(f"system shapes {op.shape}, {tuple(bd.shape)}, {tuple(x_prev.shape)}")
+
+    used = None
+    if state.basis is not None and state.basis.k > 0:
+        try:
+            used = _refresh_dev(op, state.basis.w_dev)
+        except BasisDeficient:
+            used = None
+    t0 = time.perf_counter()
+    x, report, log = _solve_dev(op, bd, x_prev, used if (used is not None and used.k > 0) else None, state.cfg, t0)
+
+    nxt = None
+    if state.k > 0:
+        try:
+            ext = _extract_dev(log, used, state.k, state.selection)
+            if ext.w_next_dev.shape[1] > 0:
+                nb = RecycleBasis.__new__(RecycleBasis)
+                nb.w_dev, nb.aw_dev, nb.chol_dev = ext.w_next_dev, ext.aw_next_dev, None
+                nxt = nb
+        except BasisDeficient:
+            nxt = None
+    x_out = x.cpu().numpy() if host else x
+    new_state = replace(state, basis=nxt, x_last=x_out if host else x, history=state.history + [report])
+    return x_out, new_state
