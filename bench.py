@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""Benchmark of the def-CG hot path on B200 (driver contract: one JSON line).
+
+Workload (BASELINE.json configs[1], "config 2"): GPC Laplace-Newton sequence,
+n = 10,000 points x ~ N(0, I_10), labels y = sign(sum sin(2x) + 0.1 N(0,1)),
+RBF lengthscale 1.5, signal variance 1, 8 Newton steps (newton_tol = -inf),
+each system (I + H^1/2 K H^1/2) x = b solved by def-CG with k = 16 recycled
+harmonic-Ritz vectors (ell = k + 4 = 20, selection "largest"), rtol 1e-8,
+fp64, seed 0.  Synthetic inputs generated exactly as SURVEY.md section 8d
+prescribes (X drawn first, then the noise vector).
+
+  step    = one complete 8-step Newton sequence on the device-resident Gram
+            matrix (800 MB fp64 > 126 MB L2, so no L2 flush is needed);
+  metric  = def-CG iterations per second over the whole sequence (refresh,
+            solve, extraction and Newton glue all inside the timed region);
+  e2e     = the same metric through the public API from pinned host buffers
+            (rbf_kernel(X) + laplace_newton(...) + records back to the host);
+  --impl reference = the reference's CPU algorithm (the oracle restatement,
+            numpy backend, all host threads), one Newton system per step.
+
+Multi-GPU (torchrun, N > 1): every rank runs an independent replica of the
+workload (weak scaling); timing is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIG2 = dict(n=10_000, d=10, lengthscale=1.5, k=16, ell=20, tol=1e-8, newton_steps=8)
+METRIC = "def-CG iters/sec (config 2: GPC Laplace-Newton sequence, n=10000, k=16, fp64)"
+UNIT = "iters/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--n", type=int, default=CONFIG2["n"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-steps", type=int, default=2)
+    return ap.parse_args()
+
+
+def inputs(n, d, seed=0):
+    from oracle.defcg_oracle import gpc_inputs
+
+    return gpc_inputs(n, d, seed)
+
+
+def workload(args):
+    c = dict(CONFIG2)
+    c["n"] = args.n
+    return {
+        "workload": f"config2 GPC Laplace-Newton def-CG sequence n={c['n']} d={c['d']} "
+                    f"ell={c['lengthscale']} k={c['k']} ell_log={c['ell']} tol={c['tol']} steps={c['newton_steps']}",
+        "n": c["n"], "d": c["d"], "k": c["k"], "ell_log": c["ell"], "tol": c["tol"],
+        "newton_steps": c["newton_steps"], "selection": "largest", "seed": 0,
+        "l2": "inputs larger than L2 (8 n^2 B Gram = %.0f MB > 126 MB)" % (8 * c["n"] ** 2 / 1e6),
+    }
+
+
+# ----------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ----------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# CPU baseline: the oracle restatement of the reference (numpy backend)
+# ----------------------------------------------------------------------------
+def cpu_baseline(n, steps):
+    """Time the reference algorithm on the host: the first `steps` Newton
+    systems of the config (solve_time_s as the reference measures it,
+    gpc.py:246-268).  Returns (iters/s, cores, sample description)."""
+    from oracle import defcg_oracle as O
+
+    c = CONFIG2
+    x, y = inputs(n, c["d"])
+    kmat = O.rbf_kernel(x, 1.0, c["lengthscale"], be="numpy")
+    _, _, recs = O.laplace_newton(kmat, y, "defcg", O.Cfg(tol=c["tol"], ell=c["ell"]), newton_tol=-np.inf,
+                                  max_newton=c["newton_steps"], k=c["k"], selection="largest", be="numpy",
+                                  max_steps_timed=steps)
+    its = sum(r.solver_iterations for r in recs)
+    secs = sum(r.solve_time_s for r in recs)
+    return its / secs, os.cpu_count(), (f"first {len(recs)} Newton systems of the config (oracle restatement of "
+                                        f"defcg, numpy backend, {its} def-CG iterations in {secs:.2f} s)")
+
+
+# ----------------------------------------------------------------------------
+# reference arm
+# ----------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from oracle import defcg_oracle as O
+
+    c = CONFIG2
+    n = args.n
+    x, y = inputs(n, c["d"])
+    kmat = O.rbf_kernel(x, 1.0, c["lengthscale"], be="numpy")
+    cfg = O.Cfg(tol=c["tol"], ell=c["ell"])
+    # Stream the Newton sequence system by system: each bench step solves the
+    # next Newton system with the reference's solve_next (refresh + def-CG +
+    # extraction), restarting the sequence after the last Newton step.
+    state = {"f": np.zeros(n), "h": None, "grad": None, "seq": None, "it": 0}
+
+    def reset():
+        ll, g, h = O.likelihood_derivs(np.zeros(n), y)
+        state.update(f=np.zeros(n), grad=g, h=h, seq=O.Sequence(k=c["k"], cfg=cfg, selection="largest"), it=0)
+
+    def one_step():
+        if state["it"] >= c["newton_steps"]:
+            reset()
+        f, h, g = state["f"], state["h"], state["grad"]
+        s = np.sqrt(h)
+        amat = kmat * np.outer(s, s)
+        amat[np.arange(n), np.arange(n)] += 1.0
+        inner = h * f + g
+        b = s * (kmat @ inner)
+        t0 = time.perf_counter()
+        xs, state["seq"] = O.solve_next(state["seq"], amat, b, be="numpy")
+        dt = time.perf_counter() - t0
+        a = inner - s * xs
+        f = kmat @ a
+        _, g, h = O.likelihood_derivs(f, y)
+        state.update(f=f, grad=g, h=h, it=state["it"] + 1)
+        return state["seq"].history[-1].iterations, dt
+
+    reset()
+    for _ in range(args.warmup):
+        one_step()
+    its, secs = 0, 0.0
+    for _ in range(args.steps):
+        i, dt = one_step()
+        its += i
+        secs += dt
+    value = its / secs if secs > 0 else 0.0
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(args.steps, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload(args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                         "sample": f"{args.steps} Newton systems streamed through the oracle restatement of "
+                                   f"defcg.recycle.solve_next (numpy backend, all host threads); {its} iterations"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------
+# native arm
+# ----------------------------------------------------------------------------
+def solve_traffic_from_profile():
+    p = ROOT / "profiles" / "solve_kernel_dram.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except ValueError:
+            return None
+    return None
+
+
+def run_native(args, rank, world):
+    import torch
+
+    import paper_1706_00241_b200 as P
+    from paper_1706_00241_b200 import _native
+
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    c = CONFIG2
+    n, k = args.n, c["k"]
+    x, y = inputs(n, c["d"])
+    cfg = P.SolverConfig(tol=c["tol"], ell=c["ell"])
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.from_numpy(y).cuda()
+    gram = P.rbf_kernel(xd, P.KernelParams(1.0, c["lengthscale"]))
+    torch.cuda.synchronize()
+
+    solve_ms, solve_its, solve_mv = [], [], []
+    orig = P.solvers._solve_dev
+
+    def traced(op, b, x0, basis, cfg_, t0):
+        out = orig(op, b, x0, basis, cfg_, t0)
+        rep = out[1]
+        kk = basis.k if basis is not None else 0
+        its = rep.iterations
+        # matvec-equivalents streamed by the solve kernel: prologue (1, or 2 with
+        # the warm-start correction), one per iteration, true-residual refreshes
+        mv = (2 if kk else 1) + its + (its // cfg_.recompute_residual_every if cfg_.recompute_residual_every else 0)
+        solve_ms.append(rep.device_ms)
+        solve_its.append((its, kk))
+        solve_mv.append(mv)
+        return out
+
+    P.solvers._solve_dev = traced
+    P.recycle._solve_dev = traced
+    P.gpc._solve_dev = traced
+
+    def sequence():
+        _, recs = P.laplace_newton(gram, yd, "defcg", cfg, newton_tol=-np.inf, max_newton=c["newton_steps"], k=k,
+                                   selection="largest")
+        return sum(r.solver_iterations for r in recs), recs
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        sequence()
+    solve_ms.clear(), solve_its.clear(), solve_mv.clear()
+    clocks = Clocks(dev)
+    barrier()
+    clocks.start()
+    launches0 = _native.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    total_its = 0
+    its_lists = []
+    for _ in range(args.steps):
+        its, recs = sequence()
+        total_its += its
+        its_lists.append([r.solver_iterations for r in recs])
+    ev1.record()
+    barrier()
+    launches = _native.launch_count() - launches0
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * total_its / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (the persistent solve kernel) -------
+    import json as _json
+
+    peaks = {}
+    pk = ROOT / "MEASURED_PEAKS.json"
+    if pk.exists():
+        peaks = _json.loads(pk.read_text())
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    vec_bytes = lambda its, kk: 8 * n * (2 * kk + 10) * its
+    alg_bytes = [mv * 8 * n * n + vec_bytes(i, kk) for mv, (i, kk) in zip(solve_mv, solve_its)]
+    tot_ms = sum(solve_ms)
+    achieved = (sum(alg_bytes) / (tot_ms / 1e3)) / 1e9 if tot_ms > 0 else None
+    prof = solve_traffic_from_profile()
+    traffic = None
+    if prof and prof.get("n") == n and prof.get("dram_bytes") and prof.get("alg_bytes"):
+        traffic = prof["dram_bytes"] / prof["alg_bytes"] * (sum(alg_bytes) / len(alg_bytes))
+    roofline = {
+        "kernel": "dcg_solve_kernel (persistent CG/def-CG loop; stored-Gram GEMV + fused vector phases)",
+        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": (achieved / peak) if achieved else None, "peak_source": peak_src,
+        "traffic": traffic, "alg_bytes_per_launch": sum(alg_bytes) / max(len(alg_bytes), 1),
+        "avg_launch_ms": tot_ms / max(len(solve_ms), 1), "launches": len(solve_ms),
+        "share_of_step": (tot_ms / args.steps) / ms_per_step if ms_per_step else None,
+        "bytes_model": "per launch: matvec-equivalents x 8 n^2 + 8 n (2k + 10) per iteration",
+    }
+
+    # ---- e2e through the public API from pinned host buffers ----------------
+    P.solvers._solve_dev = orig
+    P.recycle._solve_dev = orig
+    P.gpc._solve_dev = orig
+    xh = torch.from_numpy(x).pin_memory()
+    yh = torch.from_numpy(y).pin_memory()
+    e2e_steps = max(1, min(args.steps, 3))
+
+    def e2e_once():
+        xg = xh.to("cuda", non_blocking=True)
+        yg = yh.to("cuda", non_blocking=True)
+        g2 = P.rbf_kernel(xg, P.KernelParams(1.0, c["lengthscale"]))
+        st, recs = P.laplace_newton(g2, yg, "defcg", cfg, newton_tol=-np.inf, max_newton=c["newton_steps"], k=k,
+                                    selection="largest")
+        fh = st.f.cpu()   # final latent back to the host (records' f already host numpy)
+        d2h = fh.numel() * 8 + sum(r.f.nbytes for r in recs) + sum(8 * len(r.residual_history) for r in recs)
+        return sum(r.solver_iterations for r in recs), d2h
+
+    e2e_once()
+    barrier()
+    t0 = time.perf_counter()
+    e_its, d2h = 0, 0
+    for _ in range(e2e_steps):
+        i, d2h = e2e_once()
+        e_its += i
+    torch.cuda.synchronize()
+    e_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_s = float(t.item())
+    e2e = {"value": world * e_its / e_s, "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 8 + yh.numel() * 8),
+           "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
+           "includes": "H2D of X and y, on-device Gram assembly, 8-step Newton sequence, records D2H"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8d recipe)",
+        "config": workload(args) | {"parallelism": "replicas" if world > 1 else "single-gpu"},
+        "iterations_per_sequence": its_lists[-1], "sequence_ms": ms_per_step,
+        "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, sample = cpu_baseline(n, args.cpu_sample_steps)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_native(args, rank, world)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -130,6 +130,8 @@ DCG_API int dcg_version(void);
 DCG_API const char* dcg_status_string(int status);
 DCG_API int dcg_context_create(int device, dcg_context** out);
 DCG_API int dcg_context_destroy(dcg_context* ctx);
+/* kernels this process has launched through the library (benchmark accounting) */
+DCG_API long long dcg_launch_count(void);
 /* number of CTAs of the persistent solve kernel (one per SM) */
 DCG_API int dcg_context_grid(dcg_context* ctx, int* blocks, int* sm_count);
 

@@ -103,6 +103,7 @@ class CSolveInfo(ctypes.Structure):
 # name -> argtypes (restype is always c_int unless listed)
 SIGNATURES = {
     "dcg_version": [],
+    "dcg_launch_count": [],
     "dcg_status_string": [ctypes.c_int],
     "dcg_context_create": [ctypes.c_int, ctypes.POINTER(_P)],
     "dcg_context_destroy": [_P],
@@ -179,7 +180,8 @@ def load_library():
                 for name, args in SIGNATURES.items():
                     fn = getattr(lib, name)
                     fn.argtypes = args
-                    fn.restype = ctypes.c_char_p if name == "dcg_status_string" else ctypes.c_int
+                    fn.restype = {"dcg_status_string": ctypes.c_char_p, "dcg_launch_count": ctypes.c_longlong}.get(
+                        name, ctypes.c_int)
                 _lib = lib
     return _lib
 
@@ -234,3 +236,8 @@ def grid(device: int) -> tuple[int, int]:
     b, s = ctypes.c_int(), ctypes.c_int()
     check(lib().dcg_context_grid(context(device), ctypes.byref(b), ctypes.byref(s)))
     return b.value, s.value
+
+
+def launch_count() -> int:
+    """Kernels launched by this process through the library so far."""
+    return int(lib().dcg_launch_count())

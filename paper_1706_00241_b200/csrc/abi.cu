@@ -9,7 +9,12 @@
 
 #include "common.cuh"
 
+#include <atomic>
+
 thread_local cudaError_t dcg_last_cuda_error = cudaSuccess;
+static std::atomic<long long> g_launches{0};
+void dcg_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+extern "C" long long dcg_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 // launchers implemented in the other translation units
 int dcg_gemv_launch(dcg_context*, cudaStream_t, const double*, long long, long long, long long, const double*,
@@ -284,7 +289,7 @@ extern "C" int dcg_check_symmetric(dcg_context* ctx, void* stream, const double*
     DCG_CUDA(cudaMemsetAsync(mx, 0, 16, st));
     const long long tiles = (n + SYM_T - 1) / SYM_T;
     symcheck_kernel<<<dim3((unsigned)tiles, (unsigned)tiles), 256, 0, st>>>(d_a, n, lda, mx);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     rc = dcg_host_reserve(ctx, 16);
     if (rc) return rc;
     unsigned long long* h = static_cast<unsigned long long*>(ctx->host);
@@ -446,7 +451,7 @@ extern "C" int dcg_gram_factor(dcg_context* ctx, void* stream, double* d_w, doub
         DCG_CUDA(cudaMemcpyAsync(awtmp, d_aw, nk, cudaMemcpyDeviceToDevice, st));
         gather_cols_kernel<<<ctx->sm_count * 2, 256, 0, st>>>(wtmp, n, (int)k, active, (int)kk, d_w);
         gather_cols_kernel<<<ctx->sm_count * 2, 256, 0, st>>>(awtmp, n, (int)k, active, (int)kk, d_aw);
-        DCG_CUDA(cudaGetLastError());
+        DCG_LAUNCHED();
     }
     if (k_out) *k_out = kk;
     DCG_CUDA(cudaStreamSynchronize(st));
@@ -488,7 +493,7 @@ extern "C" int dcg_refresh_basis(dcg_context* ctx, void* stream, const dcg_opera
     } else {
         gather_cols_kernel<<<ctx->sm_count * 2, 256, 0, st>>>(d_w, n, (int)k, active, (int)kk, d_w_out);
         gather_cols_kernel<<<ctx->sm_count * 2, 256, 0, st>>>(aw, n, (int)k, active, (int)kk, d_aw_out);
-        DCG_CUDA(cudaGetLastError());
+        DCG_LAUNCHED();
     }
     if (k_out) *k_out = kk;
     DCG_CUDA(cudaStreamSynchronize(st));
@@ -540,7 +545,7 @@ extern "C" int dcg_deflation_project(dcg_context* ctx, void* stream, long long n
     rc = dcg_xty(ctx, st, basis->d_w, k, d_v, 1, n, (int)k, 1, c, parts);
     if (rc) return rc;
     project_kernel<<<ctx->sm_count, 256, 0, st>>>(n, (int)k, basis->d_chol, c, d_v, basis->d_aw, d_out);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     return DCG_OK;
 }
 
@@ -698,9 +703,9 @@ extern "C" int dcg_ritz_extract(dcg_context* ctx, void* stream, long long n, con
     const double* alpha = m ? log->d_alpha : nullptr;
 
     zcol_norm_kernel<<<nb, 128, 0, st>>>(n, (int)kp, Wp, (int)m, P, part);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     zplan_kernel<<<1, 128, 0, st>>>(part, nb, (int)T, norms, keep, ds);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     DevStatus hs;
     rc = read_status(ctx, st, ds, &hs);
     if (rc) return rc;
@@ -711,7 +716,7 @@ extern "C" int dcg_ritz_extract(dcg_context* ctx, void* stream, long long n, con
         return DCG_E_BASIS_DEFICIENT;
     }
     zbuild_kernel<<<nb * 4, 256, 0, st>>>(n, (int)kp, Wp, AWp, P, R, alpha, norms, keep, Tk, Zs, AZs);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     rc = dcg_xty(ctx, st, AZs, Tk, Zs, Tk, n, Tk, Tk, Fraw, xparts);
     if (rc) return rc;
     rc = dcg_xty(ctx, st, AZs, Tk, AZs, Tk, n, Tk, Tk, Graw, xparts);
@@ -728,13 +733,13 @@ extern "C" int dcg_ritz_extract(dcg_context* ctx, void* stream, long long n, con
     }
     const int na = (int)hs.count;
     uexpand_kernel<<<1, 256, 0, st>>>(U, active, na, Tk, (int)k, Uexp);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     rc = dcg_gemm_lr(ctx, st, Zs, Tk, Uexp, k, V, k, n, Tk, k);
     if (rc) return rc;
     colnorm_part_kernel<<<nb, 64, 0, st>>>(V, n, (int)k, part2);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     uscale_kernel<<<1, 256, 0, st>>>(part2, nb, (int)k, Uexp, Tk, U, na);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     rc = dcg_gemm_lr(ctx, st, Zs, Tk, Uexp, k, d_w_next, k, n, Tk, k);
     if (rc) return rc;
     rc = dcg_gemm_lr(ctx, st, AZs, Tk, Uexp, k, d_aw_next, k, n, Tk, k);
@@ -743,7 +748,7 @@ extern "C" int dcg_ritz_extract(dcg_context* ctx, void* stream, long long n, con
     if (d_z) {
         // z keeps the surviving columns only: gather by active (indices into Zs)
         gather_cols_kernel<<<nb * 2, 256, 0, st>>>(Zs, n, Tk, active, na, d_z);
-        DCG_CUDA(cudaGetLastError());
+        DCG_LAUNCHED();
     }
     if (t_out) *t_out = na;
     DCG_CUDA(cudaStreamSynchronize(st));

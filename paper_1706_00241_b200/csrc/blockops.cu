@@ -43,7 +43,7 @@ int dcg_gemv_launch(dcg_context* ctx, cudaStream_t st, const double* K, long lon
     long long blocks = ctx->sm_count;
     if (blocks > rows) blocks = rows;
     gemv_kernel<<<(unsigned)blocks, DCG_NT, smem, st>>>(K, ldk, n, rows, v, s_in, s_out, shift, v_rows, y);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     return DCG_OK;
 }
 
@@ -216,7 +216,7 @@ static int launch_dmma(dcg_context* ctx, cudaStream_t st, const double* K, long 
     splits_out = (int)splits;
     dim3 grid((unsigned)row_tiles, (unsigned)splits);
     dmma_gemm_kernel<NTILE><<<grid, 256, smem, st>>>(K, ldk, rows, n, V, k, split_cols, P);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     return DCG_OK;
 }
 
@@ -247,7 +247,7 @@ int dcg_block_apply(dcg_context* ctx, cudaStream_t st, const double* K, long lon
                                    cudaMemcpyDeviceToDevice, st));
         if (s_in) {
             rowscale_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(V, s_in, n, kk, V);
-            DCG_CUDA(cudaGetLastError());
+            DCG_LAUNCHED();
         }
     } else {
         DCG_CUDA(cudaMemcpyAsync(V, X, vbytes, cudaMemcpyDeviceToDevice, st));
@@ -267,17 +267,17 @@ int dcg_block_apply(dcg_context* ctx, cudaStream_t st, const double* K, long lon
     if (rc) return rc;
     if (kk == k) {
         yscale_reduce_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(P, splits, rows, k, X_rows, s_out, shift, Y);
-        DCG_CUDA(cudaGetLastError());
+        DCG_LAUNCHED();
     } else {
         // reduce into the padded layout of V (no longer needed), then compact
         yscale_reduce_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(P, splits, rows, kk, nullptr, s_out, 0.0, V);
-        DCG_CUDA(cudaGetLastError());
+        DCG_LAUNCHED();
         DCG_CUDA(cudaMemcpy2DAsync(Y, sizeof(double) * k, V, sizeof(double) * kk, sizeof(double) * k, rows,
                                    cudaMemcpyDeviceToDevice, st));
         if (shift != 0.0) {
             // Y += shift X_rows (separate pass keeps the reference's (s*t) + shift*x order)
             yscale_reduce_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(Y, 1, rows, k, X_rows, nullptr, shift, Y);
-            DCG_CUDA(cudaGetLastError());
+            DCG_LAUNCHED();
         }
     }
     return DCG_OK;
@@ -346,9 +346,9 @@ int dcg_xty(dcg_context* ctx, cudaStream_t st, const double* X, long long ldx, c
     const size_t smem = sizeof(double) * XTY_ROWS * (size_t)(p + q);
     DCG_CUDA(cudaFuncSetAttribute(xty_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     xty_kernel<<<grid, 256, smem, st>>>(X, ldx, Y, ldy, n, p, q, scratch_parts);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     reduce_parts_kernel<<<(pq + 255) / 256, 256, 0, st>>>(scratch_parts, nb, pq, C);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     return DCG_OK;
 }
 
@@ -377,6 +377,6 @@ int dcg_gemm_lr(dcg_context* ctx, cudaStream_t st, const double* A, long long ld
     long long blocks = (m * n + 255) / 256;
     if (blocks > ctx->sm_count * 16LL) blocks = ctx->sm_count * 16LL;
     gemm_lr_kernel<<<(unsigned)blocks, 256, 0, st>>>(A, lda, B, ldb, C, ldc, m, kk, n);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     return DCG_OK;
 }

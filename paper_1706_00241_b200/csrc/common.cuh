@@ -56,6 +56,15 @@ struct DevStatus {
 
 extern thread_local cudaError_t dcg_last_cuda_error;
 
+// Kernel-launch accounting (dcg_launch_count): every launch site checks the
+// launch and bumps the process-wide counter the benchmark reports.
+void dcg_count_launch();
+#define DCG_LAUNCHED()                          \
+    do {                                        \
+        DCG_CUDA(cudaGetLastError());           \
+        dcg_count_launch();                     \
+    } while (0)
+
 int dcg_ws_reserve(dcg_context* ctx, size_t bytes);
 int dcg_host_reserve(dcg_context* ctx, size_t bytes);
 

@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(SD_NT) k_jacobi_sweep_kernel(double* a, double
 int dcg_gram_factor_launch(cudaStream_t st, const double* Graw, int k, int prune, double* Gsym, double* L,
                            int* active, DevStatus* ds) {
     gram_factor_kernel<<<1, SD_NT, 0, st>>>(Graw, k, prune, Gsym, L, active, ds);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     return DCG_OK;
 }
 
@@ -601,7 +601,7 @@ int dcg_ritz_pencil_launch(cudaStream_t st, const double* Fraw, const double* Gr
     const size_t smem = dcg_pencil_smem(T);
     DCG_CUDA(cudaFuncSetAttribute(ritz_pencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ritz_pencil_kernel<<<1, SD_NT, smem, st>>>(Fraw, Graw, T, k, largest, max_sweeps, wk, theta, U, active, ds);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     return DCG_OK;
 }
 
@@ -610,7 +610,7 @@ int dcg_sym_eigen_launch(cudaStream_t st, const double* A, int n, int max_sweeps
     const size_t smem = dcg_pencil_smem(n);
     DCG_CUDA(cudaFuncSetAttribute(sym_eigen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     sym_eigen_kernel<<<1, SD_NT, smem, st>>>(A, n, max_sweeps, rtol, values, vectors, ds);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     return DCG_OK;
 }
 
@@ -619,27 +619,27 @@ int dcg_gen_sym_eigen_launch(cudaStream_t st, const double* g, const double* f, 
     const size_t smem = dcg_pencil_smem(n);
     DCG_CUDA(cudaFuncSetAttribute(gen_sym_eigen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     gen_sym_eigen_kernel<<<1, SD_NT, smem, st>>>(g, f, n, max_sweeps, wk, values, vectors, ds);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     return DCG_OK;
 }
 
 int dcg_k_cholesky_launch(cudaStream_t st, const double* a, int n, double tol, double* l, DevStatus* ds) {
     k_cholesky_kernel<<<1, SD_NT, 0, st>>>(a, n, tol, l, ds);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     return DCG_OK;
 }
 int dcg_k_solve_lower_launch(cudaStream_t st, const double* l, int n, const double* b, double* y) {
     k_solve_lower_kernel<<<1, 32, 0, st>>>(l, n, b, y);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     return DCG_OK;
 }
 int dcg_k_solve_lower_trans_launch(cudaStream_t st, const double* l, int n, const double* b, double* x) {
     k_solve_lower_trans_kernel<<<1, 32, 0, st>>>(l, n, b, x);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     return DCG_OK;
 }
 int dcg_k_jacobi_sweep_launch(cudaStream_t st, double* a, double* v, int n, DevStatus* ds) {
     k_jacobi_sweep_kernel<<<1, SD_NT, 0, st>>>(a, v, n, ds);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     return DCG_OK;
 }

@@ -63,7 +63,7 @@ int dcg_rbf_launch(cudaStream_t st, const double* xr, long long nr_total, const 
     dim3 grid((unsigned)((nc + RBF_T - 1) / RBF_T), (unsigned)((rows + RBF_T - 1) / RBF_T));
     rbf_tile_kernel<<<grid, 256, 0, st>>>(xr, nr_total, xc, nc, dim, var, inv2l2, jitter, gram, row0, rows,
                                           out, ldo);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     return DCG_OK;
 }
 
@@ -147,22 +147,22 @@ int dcg_derivs_launch(dcg_context* ctx, cudaStream_t st, long long n, const doub
     int nb = ctx->sm_count * 2;
     if ((long long)nb * 256 > n) nb = (int)max(1LL, (n + 255) / 256);
     derivs_kernel<<<nb, 256, 0, st>>>(n, f, y, a, grad, h, part);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     derivs_finalize_kernel<<<1, 256, 0, st>>>(part, nb, ds);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     return DCG_OK;
 }
 
 int dcg_newton_prep_launch(dcg_context* ctx, cudaStream_t st, long long n, const double* f, const double* grad,
                            const double* h, double* s, double* inner) {
     newton_prep_kernel<<<ctx->sm_count * 2, 256, 0, st>>>(n, f, grad, h, s, inner);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     return DCG_OK;
 }
 
 int dcg_newton_a_launch(dcg_context* ctx, cudaStream_t st, long long n, const double* inner, const double* s,
                         const double* x, double* a) {
     newton_a_kernel<<<ctx->sm_count * 2, 256, 0, st>>>(n, inner, s, x, a);
-    DCG_CUDA(cudaGetLastError());
+    DCG_LAUNCHED();
     return DCG_OK;
 }

@@ -451,6 +451,7 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
     DCG_CUDA(cudaEventRecord(ctx->ev0, st));
     DCG_CUDA(cudaLaunchCooperativeKernel((const void*)dcg_solve_kernel, dim3(G), dim3(DCG_NT), args,
                                          smem, st));
+    dcg_count_launch();
     DCG_CUDA(cudaEventRecord(ctx->ev1, st));
     rc = dcg_host_reserve(ctx, sizeof(DevStatus));
     if (rc) return rc;
