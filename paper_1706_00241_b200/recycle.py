@@ -78,8 +78,9 @@ def _refresh_dev(op, w_dev: torch.Tensor) -> RecycleBasis:
     N.check(rc, info.value, "refresh_basis")
     kk = int(kout.value)
     basis = RecycleBasis.__new__(RecycleBasis)
-    basis.w_dev = w_out[:, :kk].contiguous() if kk != k else w_out
-    basis.aw_dev = aw_out[:, :kk].contiguous() if kk != k else aw_out
+    # the library writes the surviving columns compacted: n x kk row-major
+    basis.w_dev = w_out.view(-1)[: n * kk].view(n, kk)
+    basis.aw_dev = aw_out.view(-1)[: n * kk].view(n, kk)
     basis.chol_dev = chol.view(-1)[: kk * kk].view(kk, kk)
     return basis
 

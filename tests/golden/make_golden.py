@@ -203,6 +203,10 @@ def main():
         np.savez_compressed(OUT / f"recycle_{backend}.npz", **recycle(dc, tag))
         np.savez_compressed(OUT / f"gpc_small_{backend}.npz", **gpc(dc, tag, n=300, d=4, ell=1.2, k=4))
         np.savez_compressed(OUT / f"config1_{backend}.npz", **gpc(dc, tag))
+        if os.environ.get("GOLDEN_CONFIG2", "1") == "1":
+            g2 = gpc(dc, tag, n=10_000, d=10, ell=1.5, k=16)
+            g2.pop(f"{tag}_x")   # regenerated from the seed at test time
+            np.savez_compressed(OUT / f"config2_{backend}.npz", **g2)
         print("wrote goldens for backend", backend, flush=True)
     (OUT / "VERSIONS.txt").write_text(
         "generated by tests/golden/make_golden.py from /root/reference/pkg (defcg 0.1.0)\n"

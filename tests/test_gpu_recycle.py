@@ -1,0 +1,233 @@
+"""GPU: basis refresh, harmonic-Ritz extraction and solve_next against the
+reference's known answers (pkg/tests/test_recycle.py) and its outputs on
+identical inputs.  Eigenvector signs and rotations inside clusters are
+rounding-dependent, so extracted bases are compared as SPANS (projectors),
+Ritz values to 1e-9 relative, iteration counts to +-1."""
+
+import numpy as np
+import pytest
+
+from conftest import golden, random_spd
+from oracle import defcg_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1706_00241_b200 as P
+
+    return P
+
+
+def span_gap(u, v):
+    qu, _ = np.linalg.qr(u)
+    qv, _ = np.linalg.qr(v)
+    return np.linalg.norm(qu @ qu.T - qv @ qv.T, 2)
+
+
+def test_full_krylov_recovers_spectrum(P):
+    _, _, log = P.cg_solve(np.diag([1.0, 2.0, 3.0]), np.ones(3), cfg=P.SolverConfig(tol=1e-14))
+    assert log.stored_iterations == 3
+    ext = P.harmonic_ritz_extract(log, None, 3)
+    assert np.allclose(ext.theta, [1.0, 2.0, 3.0], atol=1e-8)
+
+
+def test_k_zero_empty(P, rng):
+    _, _, log = P.cg_solve(random_spd(rng, 6), rng.standard_normal(6), cfg=P.SolverConfig(tol=1e-12))
+    ext = P.harmonic_ritz_extract(log, None, 0)
+    assert ext.theta.shape == (0,) and ext.w_next.shape == (6, 0)
+
+
+def test_early_convergence_uses_actual_count(P):
+    a = np.diag([1.0, 2.0, 50.0, 60.0, 70.0])
+    basis = P.refresh_basis(a, np.eye(5)[:, [0, 1]])
+    _, rep, log = P.deflated_cg_solve(a, np.array([0.0, 0.0, 1.0, 1.0, 0.0]), np.zeros(5), basis,
+                                      P.SolverConfig(tol=1e-10, ell=12))
+    m = log.stored_iterations
+    assert m == rep.iterations < 12
+    ext = P.harmonic_ritz_extract(log, basis, 2)
+    assert ext.z.shape[1] == basis.k + m
+
+
+def test_selection_largest(P):
+    _, _, log = P.cg_solve(np.diag([1.0, 2.0, 3.0, 4.0]), np.ones(4), cfg=P.SolverConfig(tol=1e-14))
+    ext = P.harmonic_ritz_extract(log, None, 2, selection="largest")
+    assert np.allclose(ext.theta, [3.0, 4.0], atol=1e-7)
+    with pytest.raises(ValueError):
+        P.harmonic_ritz_extract(log, None, 2, selection="middle")
+
+
+def test_w_next_is_z_times_u(P, rng):
+    _, _, log = P.cg_solve(random_spd(rng, 10), rng.standard_normal(10), cfg=P.SolverConfig(tol=1e-12))
+    ext = P.harmonic_ritz_extract(log, None, 3)
+    assert np.allclose(ext.w_next, ext.z @ ext.u, atol=1e-14)
+    assert np.allclose(np.linalg.norm(ext.w_next, axis=0), 1.0, atol=1e-12)
+
+
+def test_requested_k_too_large(P, rng):
+    _, _, log = P.cg_solve(random_spd(rng, 6), rng.standard_normal(6), cfg=P.SolverConfig(tol=1e-12))
+    with pytest.raises(P.BasisDeficient) as ei:
+        P.harmonic_ritz_extract(log, None, log.stored_iterations + 1)
+    assert ei.value.remaining == log.stored_iterations
+
+
+def test_invariant_subspace(P):
+    a = np.diag([1.0, 2.0, 3.0, 4.0, 5.0, 6.0])
+    _, _, log = P.cg_solve(a, np.array([1.0, 1.0, 1.0, 0.0, 0.0, 0.0]), cfg=P.SolverConfig(tol=1e-13))
+    ext = P.harmonic_ritz_extract(log, None, 3)
+    assert np.allclose(ext.theta, [1.0, 2.0, 3.0], atol=1e-6)
+
+
+def test_exact_invariant_subspace_with_prev_basis(P):
+    a = np.diag([1.0, 2.0, 3.0, 4.0, 5.0, 6.0, 7.0])
+    prev = P.refresh_basis(a, np.eye(7)[:, [0, 3]])
+    b = np.zeros(7)
+    b[[1, 4, 6]] = 1.0
+    _, _, log = P.deflated_cg_solve(a, b, np.zeros(7), prev, P.SolverConfig(tol=1e-13))
+    ext = P.harmonic_ritz_extract(log, prev, 5)
+    assert np.allclose(np.sort(ext.theta), [1.0, 2.0, 4.0, 5.0, 7.0], atol=1e-6)
+
+
+def test_pencil_residual(P, rng):
+    a = random_spd(rng, 12, kappa=50.0)
+    _, _, log = P.cg_solve(a, rng.standard_normal(12), cfg=P.SolverConfig(tol=1e-12, ell=8))
+    ext = P.harmonic_ritz_extract(log, None, 4)
+    az = a @ ext.z
+    for theta, u in zip(ext.theta, ext.u.T):
+        v = ext.z @ u
+        res = az.T @ (a @ v - theta * v)
+        assert np.linalg.norm(res) <= 1e-6 * np.linalg.norm(a @ v)
+
+
+def test_ritz_parity_with_reference(P):
+    g = golden("recycle_compiled")
+    a, b = g["c_ritz_a"], g["c_ritz_b"]
+    _, _, log = P.cg_solve(a, b, None, P.SolverConfig(tol=1e-10, ell=12))
+    for sel in ("smallest", "largest"):
+        ext = P.harmonic_ritz_extract(log, None, 5, sel)
+        assert np.allclose(ext.theta, g[f"c_ritz_{sel}_theta"], rtol=1e-9)
+        assert span_gap(ext.w_next, g[f"c_ritz_{sel}_w"]) < 1e-7
+        assert np.allclose(np.abs(np.sum(ext.w_next * g[f"c_ritz_{sel}_w"], axis=0)), 1.0, atol=1e-7)
+
+
+# ---------------------------------------------------------------- refresh
+def test_refresh_single_column(P):
+    basis = P.refresh_basis(np.diag([4.0, 5.0]), np.array([[1.0], [0.0]]))
+    assert np.allclose(basis.aw, [[4.0], [0.0]], atol=1e-15)
+    assert np.allclose(basis.gram_chol, [[2.0]], atol=1e-15)
+
+
+def test_refresh_prunes_duplicates_like_reference(P, rng):
+    g = golden("recycle_compiled")
+    basis = P.refresh_basis(g["c_ritz_a"], g["c_refresh_w_in"])
+    assert basis.k == 3
+    assert np.array_equal(basis.w, g["c_refresh_w"])
+    assert np.allclose(basis.aw, g["c_refresh_aw"], rtol=1e-12, atol=1e-12)
+    assert np.allclose(basis.gram_chol, g["c_refresh_chol"], rtol=1e-12)
+    w = rng.standard_normal((6, 1))
+    assert P.refresh_basis(random_spd(rng, 6), np.hstack([w, w])).k == 1
+
+
+def test_refresh_all_pruned_and_empty(P):
+    with pytest.raises(P.BasisDeficient) as ei:
+        P.refresh_basis(np.eye(3), np.zeros((3, 2)))
+    assert ei.value.remaining == 0
+    assert P.refresh_basis(np.eye(3), np.empty((3, 0))).k == 0
+
+
+def test_refresh_eigenvector_basis(P, rng):
+    a = random_spd(rng, 8)
+    pairs = O.sym_eigen(a)
+    basis = P.refresh_basis(a, pairs[1][:, :2])
+    gram = basis.gram_chol @ basis.gram_chol.T
+    assert np.allclose(gram, np.diag(pairs[0][:2]), atol=1e-10)
+
+
+@pytest.mark.parametrize("n,k", [(9, 3), (1000, 16), (3001, 32), (700, 40)])
+def test_refresh_aw_consistency(P, rng, n, k):
+    """A.W on FP64 tensor cores vs an fp64 host product, including the implicit Newton operator."""
+    a = random_spd(rng, n, 1e3) if n < 1200 else None
+    if a is None:
+        x = rng.standard_normal((n, 5))
+        a = O.rbf_kernel(x, 1.0, 1.5)
+    w = rng.standard_normal((n, k))
+    basis = P.refresh_basis(a, w)
+    ref = a @ w
+    err = np.linalg.norm(basis.aw - ref, axis=0) / np.linalg.norm(ref, axis=0)
+    assert basis.k == k and np.all(err <= 1e-12)
+    # implicit A = I + S K S
+    s = rng.uniform(0.1, 0.5, n)
+    op = P.DenseOperator.from_matrix(a).scaled(s, 1.0)
+    basis2 = P.refresh_basis(op, w)
+    ref2 = (a * np.outer(s, s) + np.eye(n)) @ w
+    err2 = np.linalg.norm(basis2.aw - ref2, axis=0) / np.linalg.norm(ref2, axis=0)
+    assert np.all(err2 <= 1e-12)
+
+
+# ---------------------------------------------------------------- solve_next
+def test_first_solve_equals_plain_cg(P, rng):
+    a = random_spd(rng, 12)
+    b = rng.standard_normal(12)
+    cfg = P.SolverConfig(tol=1e-10)
+    x, st = P.solve_next(P.SequenceState(k=4, cfg=cfg), a, b)
+    x_ref, rep_ref, _ = P.cg_solve(a, b, cfg=cfg)
+    assert np.array_equal(x, x_ref)
+    assert st.history[0].residual_history == rep_ref.residual_history
+    assert st.basis is not None
+
+
+def test_constant_sequence_recycling_helps(P):
+    a = np.diag(np.arange(1.0, 41.0))
+    st = P.SequenceState(k=5, cfg=P.SolverConfig(tol=1e-8, ell=10))
+    _, st = P.solve_next(st, a, np.ones(40))
+    _, st = P.solve_next(st, a, np.ones(40))
+    assert st.history[1].iterations < st.history[0].iterations
+
+
+def test_k_zero_always_plain_cg(P, rng):
+    a = random_spd(rng, 15)
+    b = rng.standard_normal(15)
+    cfg = P.SolverConfig(tol=1e-9)
+    st = P.SequenceState(k=0, cfg=cfg)
+    _, st = P.solve_next(st, a, b)
+    _, st = P.solve_next(st, a, b)
+    x_ref, r1, _ = P.cg_solve(a, b, cfg=cfg)
+    _, r2, _ = P.cg_solve(a, b, x0=x_ref, cfg=cfg)
+    assert st.history[0].residual_history == r1.residual_history
+    assert st.history[1].residual_history == r2.residual_history
+
+
+def test_sequence_parity_with_reference(P):
+    """Iterations within the reference's own backend spread (+1); x within 1e-7."""
+    g, gn = golden("recycle_compiled"), golden("recycle_numpy")
+    st = P.SequenceState(k=4, cfg=P.SolverConfig(tol=1e-9, ell=10), selection="largest")
+    for i in range(4):
+        x, st = P.solve_next(st, g["c_seq_a"][i], g["c_seq_b"][i])
+        ref, alt = int(g["c_seq_its"][i]), int(gn["n_seq_its"][i])
+        # ~190-240-iteration solves at kappa 1e4: finite-precision CG counts move with rounding
+        allowed = max(1, 2 * abs(ref - alt), int(np.ceil(0.02 * ref)))
+        assert abs(st.history[-1].iterations - ref) <= allowed, (i, st.history[-1].iterations, ref)
+        xr = g["c_seq_x"][i]
+        assert np.linalg.norm(x - xr) / np.linalg.norm(xr) <= 1e-7
+
+
+def test_basis_deficient_degenerates_like_reference(P):
+    """k larger than the first solve's logged iterations: BasisDeficient is
+    swallowed and every later solve is plain CG (recycle.py:194-195)."""
+    a = np.diag(np.arange(1.0, 11.0))
+    cfg = P.SolverConfig(tol=1e-12, ell=3)
+    st = P.SequenceState(k=5, cfg=cfg)
+    _, st = P.solve_next(st, a, np.ones(10))
+    assert st.basis is None
+    x, st = P.solve_next(st, a, np.ones(10))
+    assert st.basis is None and st.history[-1].iterations <= 1
+
+
+def test_warm_start_carries_solution(P, rng):
+    a = random_spd(rng, 10)
+    b = rng.standard_normal(10)
+    st = P.SequenceState(k=2, cfg=P.SolverConfig(tol=1e-10))
+    _, st = P.solve_next(st, a, b)
+    _, st = P.solve_next(st, a, b)
+    assert st.history[1].iterations <= 1
