@@ -67,7 +67,9 @@ enum dcg_status {
  * Here A stays implicit: the Newton system is (K, s = sqrt(h), shift = 1);
  * an explicit matrix is (K = A, s = NULL, shift = 0).  `row0/rows` select the
  * locally stored row slab for row-sharded operators (rows == n on one GPU). */
-enum dcg_op_kind { DCG_OP_DENSE = 0, DCG_OP_RBF = 1 };
+/* DCG_OP_DENSE_SYM: same dense storage, K exactly symmetric and unsharded: the
+ * GEMV streams only the lower triangle (64 x 64 tiles), half the bytes.     */
+enum dcg_op_kind { DCG_OP_DENSE = 0, DCG_OP_RBF = 1, DCG_OP_DENSE_SYM = 2 };
 
 typedef struct dcg_operator {
     int kind;                 /* dcg_op_kind                                     */
@@ -217,6 +219,16 @@ DCG_API int dcg_ritz_extract(dcg_context* ctx, void* stream, long long n, const 
                      long long m, const dcg_basis* prev, long long k, int selection,
                      double* d_theta, double* d_u, double* d_z, double* d_w_next,
                      double* d_aw_next, long long* t_out, long long* info);
+
+/* Asynchronous form: enqueue the whole extraction on `stream` without any host
+ * synchronisation (the zero-column scan and the pruning decide the pencil
+ * order on the device).  When the stream reaches the end, d_result[0..2]
+ * (device int64) hold status, info payload and the kept column count T.     */
+DCG_API int dcg_ritz_extract_async(dcg_context* ctx, void* stream, long long n,
+                                   const dcg_krylov_log* log, long long m, const dcg_basis* prev,
+                                   long long k, int selection, double* d_theta, double* d_u,
+                                   double* d_z, double* d_w_next, double* d_aw_next,
+                                   long long* d_result);
 
 /* ---- L4: GPC Laplace-Newton glue (gpc.py) -------------------------------- */
 /* loglik, grad, h of the logistic likelihood          gpc.py:126-157          */

@@ -19,8 +19,21 @@ def device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
-def ctx() -> int:
-    return _native.context(device().index)
+def ctx(slot: int = 0) -> int:
+    return _native.context(device().index, slot)
+
+
+_side_streams: dict[int, torch.cuda.Stream] = {}
+
+
+def side_stream() -> torch.cuda.Stream:
+    """Per-device side stream for work that overlaps the main stream."""
+    d = device()
+    s = _side_streams.get(d.index)
+    if s is None:
+        s = torch.cuda.Stream(device=d)
+        _side_streams[d.index] = s
+    return s
 
 
 def stream() -> int:

@@ -37,6 +37,7 @@ DCG_E_UNSUPPORTED = 10
 
 DCG_OP_DENSE = 0
 DCG_OP_RBF = 1
+DCG_OP_DENSE_SYM = 2
 DCG_SELECT_SMALLEST = 0
 DCG_SELECT_LARGEST = 1
 MAX_K = 64
@@ -155,6 +156,22 @@ SIGNATURES = {
         _PLL,
         _PLL,
     ],
+    "dcg_ritz_extract_async": [
+        _P,
+        _P,
+        _LL,
+        ctypes.POINTER(CKrylovLog),
+        _LL,
+        ctypes.POINTER(CBasis),
+        _LL,
+        ctypes.c_int,
+        _P,
+        _P,
+        _P,
+        _P,
+        _P,
+        _P,
+    ],
     "dcg_gpc_derivs": [_P, _P, _LL, _P, _P, _P, _P, _PD],
     "dcg_gpc_newton_system": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P, _P, _P],
     "dcg_gpc_newton_update": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P, _P, _P, _P, _P, _PD, _PD],
@@ -162,7 +179,7 @@ SIGNATURES = {
 
 _lib = None
 _lock = threading.Lock()
-_contexts: dict[int, int] = {}
+_contexts: dict[tuple[int, int], int] = {}
 
 
 def load_library():
@@ -218,17 +235,22 @@ def check(rc: int, info: int = 0, what: str = ""):
     raise DeviceError(msg)
 
 
-def context(device: int) -> int:
-    """Per-device dcg_context (created lazily, lives for the process)."""
-    ctx = _contexts.get(device)
+def context(device: int, slot: int = 0) -> int:
+    """dcg_context per (device, slot), created lazily and kept for the process.
+
+    Slot 0 serves the caller's current stream; slot 1 the side stream that
+    runs the asynchronous Ritz extraction (each context owns its workspace, so
+    work in flight on the two streams never shares scratch memory)."""
+    key = (device, slot)
+    ctx = _contexts.get(key)
     if ctx is None:
         with _lock:
-            ctx = _contexts.get(device)
+            ctx = _contexts.get(key)
             if ctx is None:
                 out = _P()
                 check(lib().dcg_context_create(device, ctypes.byref(out)), what="dcg_context_create")
                 ctx = out.value
-                _contexts[device] = ctx
+                _contexts[key] = ctx
     return ctx
 
 

@@ -19,6 +19,9 @@ extern "C" long long dcg_launch_count(void) { return g_launches.load(std::memory
 // launchers implemented in the other translation units
 int dcg_gemv_launch(dcg_context*, cudaStream_t, const double*, long long, long long, long long, const double*,
                     const double*, const double*, double, const double*, double*);
+size_t dcg_sym_apply_scratch_doubles(long long n);
+int dcg_sym_apply(dcg_context*, cudaStream_t, const double*, long long, long long, const double*, const double*,
+                  const double*, double, double*, double*);
 size_t dcg_block_apply_scratch_doubles(long long n, long long rows, int k);
 int dcg_block_apply(dcg_context*, cudaStream_t, const double*, long long, long long, long long, const double*, int,
                     const double*, const double*, double, const double*, double*, double*);
@@ -30,7 +33,7 @@ int dcg_gemm_lr(dcg_context*, cudaStream_t, const double*, long long, const doub
 int dcg_gram_factor_launch(cudaStream_t, const double*, int, int, double*, double*, int*, DevStatus*);
 size_t dcg_pencil_smem(int T);
 int dcg_ritz_pencil_launch(cudaStream_t, const double*, const double*, int, int, int, int, double*, double*,
-                           double*, int*, DevStatus*);
+                           double*, int*, DevStatus*, const DevStatus*);
 int dcg_sym_eigen_launch(cudaStream_t, const double*, int, int, double, double*, double*, DevStatus*);
 int dcg_gen_sym_eigen_launch(cudaStream_t, const double*, const double*, int, int, double*, double*, double*,
                              DevStatus*);
@@ -129,21 +132,7 @@ int dcg_host_reserve(dcg_context* ctx, size_t bytes) {
     return DCG_OK;
 }
 
-// bump allocator over ctx->ws (reserve the total first)
-struct Arena {
-    char* base;
-    size_t off;
-    template <class T>
-    T* take(size_t count) {
-        off = (off + 255) & ~size_t(255);
-        T* p = reinterpret_cast<T*>(base + off);
-        off += sizeof(T) * count;
-        return p;
-    }
-};
-static inline size_t al(size_t bytes) { return (bytes + 255) & ~size_t(255); }
-
-static int read_status(dcg_context* ctx, cudaStream_t st, const DevStatus* dev, DevStatus* out) {
+int dcg_read_status(dcg_context* ctx, cudaStream_t st, const DevStatus* dev, DevStatus* out) {
     int rc = dcg_host_reserve(ctx, sizeof(DevStatus));
     if (rc) return rc;
     DevStatus* hs = static_cast<DevStatus*>(ctx->host);
@@ -153,7 +142,6 @@ static int read_status(dcg_context* ctx, cudaStream_t st, const DevStatus* dev, 
     return DCG_OK;
 }
 
-static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // ---------------------------------------------------------------------------
 // L0 twins
@@ -191,7 +179,7 @@ extern "C" int dcg_k_cholesky(dcg_context* ctx, void* stream, const double* d_a,
     rc = dcg_k_cholesky_launch(st, d_a, (int)n, pivot_tol, d_l, ds);
     if (rc) return rc;
     DevStatus hs;
-    rc = read_status(ctx, st, ds, &hs);
+    rc = dcg_read_status(ctx, st, ds, &hs);
     if (rc) return rc;
     if (fail_index) *fail_index = hs.info;
     return DCG_OK;
@@ -240,7 +228,7 @@ extern "C" int dcg_k_jacobi_sweep(dcg_context* ctx, void* stream, double* d_a, d
     rc = dcg_k_jacobi_sweep_launch(st, d_a, d_v, (int)n, ds);
     if (rc) return rc;
     DevStatus hs;
-    rc = read_status(ctx, st, ds, &hs);
+    rc = dcg_read_status(ctx, st, ds, &hs);
     if (rc) return rc;
     if (rotations) *rotations = hs.count;
     return DCG_OK;
@@ -317,7 +305,7 @@ extern "C" int dcg_sym_eigen(dcg_context* ctx, void* stream, const double* d_a, 
     rc = dcg_sym_eigen_launch(st, d_a, (int)n, (int)max_sweeps, rtol, d_values, d_vectors, ds);
     if (rc) return rc;
     DevStatus hs;
-    rc = read_status(ctx, st, ds, &hs);
+    rc = dcg_read_status(ctx, st, ds, &hs);
     if (rc) return rc;
     if (hs.status != DCG_OK && info) *info = hs.info;
     return hs.status;
@@ -339,7 +327,7 @@ extern "C" int dcg_gen_sym_eigen(dcg_context* ctx, void* stream, const double* d
     rc = dcg_gen_sym_eigen_launch(st, d_g, d_f, (int)n, (int)max_sweeps, wk, d_values, d_vectors, ds);
     if (rc) return rc;
     DevStatus hs;
-    rc = read_status(ctx, st, ds, &hs);
+    rc = dcg_read_status(ctx, st, ds, &hs);
     if (rc) return rc;
     if (hs.status != DCG_OK && info) *info = hs.info;
     return hs.status;
@@ -350,10 +338,24 @@ extern "C" int dcg_gen_sym_eigen(dcg_context* ctx, void* stream, const double* d
 // ---------------------------------------------------------------------------
 static int check_dense_op(const dcg_operator* op) {
     if (!op) return DCG_E_CONFIG;
-    if (op->kind != DCG_OP_DENSE) return DCG_E_UNSUPPORTED;
+    if (op->kind != DCG_OP_DENSE && op->kind != DCG_OP_DENSE_SYM) return DCG_E_UNSUPPORTED;
     if (op->n < 0 || op->row0 < 0 || op->rows < 0 || op->row0 + op->rows > op->n) return DCG_E_CONFIG;
     if (op->ldk < op->n || (op->ldk & 1) || !aligned16(op->d_k)) return DCG_E_CONFIG;
+    if (op->kind == DCG_OP_DENSE_SYM && (op->row0 != 0 || op->rows != op->n)) return DCG_E_CONFIG;
     return DCG_OK;
+}
+
+// y = shift v + s_out (.) K (s_in (.) v) over the operator's storage strategy;
+// `scratch` holds apply_k_scratch(op) doubles (workspace reserved by the caller).
+static size_t apply_k_scratch(const dcg_operator* op) {
+    return op->kind == DCG_OP_DENSE_SYM ? dcg_sym_apply_scratch_doubles(op->n) : 0;
+}
+static int apply_k(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, const double* v, const double* s_in,
+                   const double* s_out, double shift, double* y, double* scratch) {
+    // the lower-triangle strategy stages 16-byte slices of v and s_in
+    if (op->kind == DCG_OP_DENSE_SYM && aligned16(v) && aligned16(s_in))
+        return dcg_sym_apply(ctx, st, op->d_k, op->ldk, op->n, v, s_in, s_out, shift, y, scratch);
+    return dcg_gemv_launch(ctx, st, op->d_k, op->ldk, op->n, op->rows, v, s_in, s_out, shift, v + op->row0, y);
 }
 
 extern "C" int dcg_op_apply(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_x,
@@ -362,8 +364,9 @@ extern "C" int dcg_op_apply(dcg_context* ctx, void* stream, const dcg_operator* 
     int rc = check_dense_op(op);
     if (rc) return rc;
     const double* s_out = op->d_s ? op->d_s + op->row0 : nullptr;
-    return dcg_gemv_launch(ctx, as_stream(stream), op->d_k, op->ldk, op->n, op->rows, d_x, op->d_s, s_out,
-                           op->shift, d_x + op->row0, d_y);
+    rc = dcg_ws_reserve(ctx, sizeof(double) * apply_k_scratch(op) + 256);
+    if (rc) return rc;
+    return apply_k(ctx, as_stream(stream), op, d_x, op->d_s, s_out, op->shift, d_y, static_cast<double*>(ctx->ws));
 }
 
 extern "C" int dcg_op_apply_block(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_x,
@@ -408,7 +411,7 @@ static int gram_core(dcg_context* ctx, cudaStream_t st, const double* W, const d
     rc = dcg_gram_factor_launch(st, graw, k, prune, gsym, lwork, d_active, ds);
     if (rc) return rc;
     DevStatus hs;
-    rc = read_status(ctx, st, ds, &hs);
+    rc = dcg_read_status(ctx, st, ds, &hs);
     if (rc) return rc;
     if (hs.status != DCG_OK) {
         if (info) *info = hs.info;
@@ -550,212 +553,6 @@ extern "C" int dcg_deflation_project(dcg_context* ctx, void* stream, long long n
 }
 
 // ---------------------------------------------------------------------------
-// L3: harmonic Ritz extraction (recycle.py:95-159)
-// ---------------------------------------------------------------------------
-// column c of Z: prev W column (c < kp) or log p_{c-kp}; sum of squares per CTA
-__global__ void zcol_norm_kernel(long long n, int kp, const double* Wp, int m, const double* P, double* part) {
-    const int T = kp + m;
-    const long long r0 = part_begin(n, gridDim.x, blockIdx.x), r1 = part_begin(n, gridDim.x, blockIdx.x + 1);
-    for (int c = threadIdx.x; c < T; c += blockDim.x) {
-        double acc = 0.0;
-        if (c < kp)
-            for (long long i = r0; i < r1; ++i) acc = fma(Wp[i * kp + c], Wp[i * kp + c], acc);
-        else
-            for (long long i = r0; i < r1; ++i) {
-                const double v = P[(long long)(c - kp) * n + i];
-                acc = fma(v, v, acc);
-            }
-        part[(long long)blockIdx.x * T + c] = acc;
-    }
-}
-
-// keep = norms > 0 (fixed order), Tk in st->count
-__global__ void zplan_kernel(const double* part, int nb, int T, double* norms, int* keep, DevStatus* st) {
-    __shared__ double nrm[DCG_MAX_T];
-    for (int c = threadIdx.x; c < T; c += blockDim.x) {
-        double acc = 0.0;
-        for (int b = 0; b < nb; ++b) acc += part[(long long)b * T + c];
-        nrm[c] = sqrt(acc);
-        norms[c] = nrm[c];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int t = 0;
-        for (int c = 0; c < T; ++c)
-            if (nrm[c] > 0.0) keep[t++] = c;
-        st->status = DCG_OK;
-        st->count = t;
-    }
-}
-
-// Zs[i][c'] = z[i][keep c'] / norm ; AZs likewise with az = (r_j - r_{j+1}) / alpha_j
-__global__ void zbuild_kernel(long long n, int kp, const double* Wp, const double* AWp, const double* P,
-                              const double* R, const double* alpha, const double* norms, const int* keep, int Tk,
-                              double* Zs, double* AZs) {
-    const long long total = n * Tk;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-         e += (long long)gridDim.x * blockDim.x) {
-        const long long i = e / Tk;
-        const int cc = (int)(e % Tk);
-        const int c = keep[cc];
-        const double nv = norms[c];
-        double z, az;
-        if (c < kp) {
-            z = Wp[i * kp + c];
-            az = AWp[i * kp + c];
-        } else {
-            const int j = c - kp;
-            z = P[(long long)j * n + i];
-            az = div_rn(sub_rn(R[(long long)j * n + i], R[(long long)(j + 1) * n + i]), alpha[j]);
-        }
-        Zs[e] = div_rn(z, nv);
-        AZs[e] = div_rn(az, nv);
-    }
-}
-
-// Uexp (Tk x k): rows of the surviving columns get U, pruned rows zero
-__global__ void uexpand_kernel(const double* U, const int* active, int na, int Tk, int k, double* Uexp) {
-    for (int e = threadIdx.x; e < Tk * k; e += blockDim.x) Uexp[e] = 0.0;
-    __syncthreads();
-    for (int e = threadIdx.x; e < na * k; e += blockDim.x) {
-        const int r = e / k, j = e % k;
-        Uexp[active[r] * k + j] = U[e];
-    }
-}
-
-__global__ void colnorm_part_kernel(const double* V, long long n, int k, double* part) {
-    const long long r0 = part_begin(n, gridDim.x, blockIdx.x), r1 = part_begin(n, gridDim.x, blockIdx.x + 1);
-    for (int c = threadIdx.x; c < k; c += blockDim.x) {
-        double acc = 0.0;
-        for (long long i = r0; i < r1; ++i) acc = fma(V[i * k + c], V[i * k + c], acc);
-        part[(long long)blockIdx.x * k + c] = acc;
-    }
-}
-
-// u[:, j] /= ||Z u_j|| when positive (recycle.py:150-153), on Uexp and U
-__global__ void uscale_kernel(const double* part, int nb, int k, double* Uexp, int Tk, double* U, int na) {
-    __shared__ double sc[DCG_MAX_K];
-    for (int c = threadIdx.x; c < k; c += blockDim.x) {
-        double acc = 0.0;
-        for (int b = 0; b < nb; ++b) acc += part[(long long)b * k + c];
-        sc[c] = sqrt(acc);
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < Tk * k; e += blockDim.x) {
-        const double s = sc[e % k];
-        if (s > 0.0) Uexp[e] = div_rn(Uexp[e], s);
-    }
-    for (int e = threadIdx.x; e < na * k; e += blockDim.x) {
-        const double s = sc[e % k];
-        if (s > 0.0) U[e] = div_rn(U[e], s);
-    }
-}
-
-extern "C" int dcg_ritz_extract(dcg_context* ctx, void* stream, long long n, const dcg_krylov_log* log, long long m,
-                                const dcg_basis* prev, long long k, int selection, double* d_theta, double* d_u,
-                                double* d_z, double* d_w_next, double* d_aw_next, long long* t_out,
-                                long long* info) {
-    if (!ctx || n < 0 || m < 0 || k < 0) return DCG_E_CONFIG;
-    if (selection != DCG_SELECT_SMALLEST && selection != DCG_SELECT_LARGEST) return DCG_E_CONFIG;
-    if (info) *info = 0;
-    const long long kp = prev ? prev->k : 0;
-    const long long T = kp + m;
-    if (t_out) *t_out = T;
-    if (k > T) {   // recycle.py:104-108
-        if (info) *info = T;
-        return DCG_E_BASIS_DEFICIENT;
-    }
-    if (k == 0) return DCG_OK;
-    if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
-    if (T > DCG_MAX_T) return DCG_E_UNSUPPORTED;
-    if (m > 0 && (!log || log->ell < m || !log->d_p || !log->d_r || !log->d_alpha)) return DCG_E_CONFIG;
-    cudaStream_t st = as_stream(stream);
-    const int nb = ctx->sm_count;
-    const size_t nT = (size_t)n * T;
-    const size_t need = al(sizeof(double) * nT) * 2 + al(sizeof(double) * (size_t)nb * T) * 2 +
-                        al(sizeof(double) * T * T) * 2 + al(sizeof(double) * dcg_xty_scratch_doubles(ctx, T, T)) +
-                        al(sizeof(double) * 5 * T * T) + al(sizeof(double) * T * k) * 2 + al(sizeof(double) * n * k) +
-                        al(sizeof(double) * T) + al(sizeof(int) * T) * 2 + al(sizeof(DevStatus)) * 2 + 8192;
-    int rc = dcg_ws_reserve(ctx, need);
-    if (rc) return rc;
-    Arena ar{static_cast<char*>(ctx->ws), 0};
-    double* Zs = ar.take<double>(nT);
-    double* AZs = ar.take<double>(nT);
-    double* part = ar.take<double>((size_t)nb * T);
-    double* norms = ar.take<double>(T);
-    int* keep = ar.take<int>(T);
-    int* active = ar.take<int>(T);
-    double* Fraw = ar.take<double>(T * T);
-    double* Graw = ar.take<double>(T * T);
-    double* xparts = ar.take<double>(dcg_xty_scratch_doubles(ctx, T, T));
-    double* wk = ar.take<double>(5 * T * T);
-    double* U = ar.take<double>(T * k);
-    double* Uexp = ar.take<double>(T * k);
-    double* V = ar.take<double>(n * k);
-    double* part2 = ar.take<double>((size_t)nb * T);
-    DevStatus* ds = ar.take<DevStatus>(1);
-    DevStatus* ds2 = ar.take<DevStatus>(1);
-    DCG_CUDA(cudaMemsetAsync(ds, 0, 2 * al(sizeof(DevStatus)), st));
-    const double* Wp = kp ? prev->d_w : nullptr;
-    const double* AWp = kp ? prev->d_aw : nullptr;
-    const double* P = m ? log->d_p : nullptr;
-    const double* R = m ? log->d_r : nullptr;
-    const double* alpha = m ? log->d_alpha : nullptr;
-
-    zcol_norm_kernel<<<nb, 128, 0, st>>>(n, (int)kp, Wp, (int)m, P, part);
-    DCG_LAUNCHED();
-    zplan_kernel<<<1, 128, 0, st>>>(part, nb, (int)T, norms, keep, ds);
-    DCG_LAUNCHED();
-    DevStatus hs;
-    rc = read_status(ctx, st, ds, &hs);
-    if (rc) return rc;
-    const int Tk = (int)hs.count;
-    if (Tk < k) {   // first check of the pruning loop (recycle.py:131-132)
-        if (info) *info = Tk;
-        if (t_out) *t_out = Tk;
-        return DCG_E_BASIS_DEFICIENT;
-    }
-    zbuild_kernel<<<nb * 4, 256, 0, st>>>(n, (int)kp, Wp, AWp, P, R, alpha, norms, keep, Tk, Zs, AZs);
-    DCG_LAUNCHED();
-    rc = dcg_xty(ctx, st, AZs, Tk, Zs, Tk, n, Tk, Tk, Fraw, xparts);
-    if (rc) return rc;
-    rc = dcg_xty(ctx, st, AZs, Tk, AZs, Tk, n, Tk, Tk, Graw, xparts);
-    if (rc) return rc;
-    rc = dcg_ritz_pencil_launch(st, Fraw, Graw, Tk, (int)k, selection == DCG_SELECT_LARGEST, 60, wk,
-                                d_theta, U, active, ds2);
-    if (rc) return rc;
-    rc = read_status(ctx, st, ds2, &hs);
-    if (rc) return rc;
-    if (hs.status != DCG_OK) {
-        if (info) *info = hs.info;
-        if (t_out) *t_out = hs.count;
-        return hs.status;
-    }
-    const int na = (int)hs.count;
-    uexpand_kernel<<<1, 256, 0, st>>>(U, active, na, Tk, (int)k, Uexp);
-    DCG_LAUNCHED();
-    rc = dcg_gemm_lr(ctx, st, Zs, Tk, Uexp, k, V, k, n, Tk, k);
-    if (rc) return rc;
-    colnorm_part_kernel<<<nb, 64, 0, st>>>(V, n, (int)k, part2);
-    DCG_LAUNCHED();
-    uscale_kernel<<<1, 256, 0, st>>>(part2, nb, (int)k, Uexp, Tk, U, na);
-    DCG_LAUNCHED();
-    rc = dcg_gemm_lr(ctx, st, Zs, Tk, Uexp, k, d_w_next, k, n, Tk, k);
-    if (rc) return rc;
-    rc = dcg_gemm_lr(ctx, st, AZs, Tk, Uexp, k, d_aw_next, k, n, Tk, k);
-    if (rc) return rc;
-    if (d_u) DCG_CUDA(cudaMemcpyAsync(d_u, U, sizeof(double) * na * k, cudaMemcpyDeviceToDevice, st));
-    if (d_z) {
-        // z keeps the surviving columns only: gather by active (indices into Zs)
-        gather_cols_kernel<<<nb * 2, 256, 0, st>>>(Zs, n, Tk, active, na, d_z);
-        DCG_LAUNCHED();
-    }
-    if (t_out) *t_out = na;
-    DCG_CUDA(cudaStreamSynchronize(st));
-    return DCG_OK;
-}
-
-// ---------------------------------------------------------------------------
 // L4: GPC glue
 // ---------------------------------------------------------------------------
 extern "C" int dcg_gpc_derivs(dcg_context* ctx, void* stream, long long n, const double* d_f, const double* d_y,
@@ -771,7 +568,7 @@ extern "C" int dcg_gpc_derivs(dcg_context* ctx, void* stream, long long n, const
     rc = dcg_derivs_launch(ctx, st, n, d_f, d_y, nullptr, d_grad, d_h, part, ds);
     if (rc) return rc;
     DevStatus hs;
-    rc = read_status(ctx, st, ds, &hs);
+    rc = dcg_read_status(ctx, st, ds, &hs);
     if (rc) return rc;
     if (loglik) *loglik = hs.value;
     return DCG_OK;
@@ -785,11 +582,12 @@ extern "C" int dcg_gpc_newton_system(dcg_context* ctx, void* stream, const dcg_o
     if (rc) return rc;
     cudaStream_t st = as_stream(stream);
     const long long n = kop->n;
+    rc = dcg_ws_reserve(ctx, sizeof(double) * apply_k_scratch(kop) + 256);
+    if (rc) return rc;
     rc = dcg_newton_prep_launch(ctx, st, n, d_f, d_grad, d_h, d_s, d_inner);
     if (rc) return rc;
     // b = s (.) (K inner): K's own scaling/shift are ignored here (K is the kernel matrix)
-    return dcg_gemv_launch(ctx, st, kop->d_k, kop->ldk, n, kop->rows, d_inner, nullptr, d_s + kop->row0, 0.0,
-                           nullptr, d_b);
+    return apply_k(ctx, st, kop, d_inner, nullptr, d_s + kop->row0, 0.0, d_b, static_cast<double*>(ctx->ws));
 }
 
 extern "C" int dcg_gpc_newton_update(dcg_context* ctx, void* stream, const dcg_operator* kop, const double* d_inner,
@@ -801,20 +599,22 @@ extern "C" int dcg_gpc_newton_update(dcg_context* ctx, void* stream, const dcg_o
     if (kop->row0 != 0 || kop->rows != kop->n) return DCG_E_UNSUPPORTED;
     cudaStream_t st = as_stream(stream);
     const long long n = kop->n;
-    const size_t need = al(sizeof(double) * 2 * ctx->sm_count * 2) + al(sizeof(DevStatus));
+    const size_t need = al(sizeof(double) * 2 * ctx->sm_count * 2) + al(sizeof(DevStatus)) +
+                        al(sizeof(double) * apply_k_scratch(kop));
     rc = dcg_ws_reserve(ctx, need);
     if (rc) return rc;
     Arena ar{static_cast<char*>(ctx->ws), 0};
     double* part = ar.take<double>(4 * ctx->sm_count);
     DevStatus* ds = ar.take<DevStatus>(1);
+    double* scratch = ar.take<double>(apply_k_scratch(kop));
     rc = dcg_newton_a_launch(ctx, st, n, d_inner, d_s, d_x, d_a);
     if (rc) return rc;
-    rc = dcg_gemv_launch(ctx, st, kop->d_k, kop->ldk, n, n, d_a, nullptr, nullptr, 0.0, nullptr, d_f);
+    rc = apply_k(ctx, st, kop, d_a, nullptr, nullptr, 0.0, d_f, scratch);
     if (rc) return rc;
     rc = dcg_derivs_launch(ctx, st, n, d_f, d_y, d_a, d_grad, d_h, part, ds);
     if (rc) return rc;
     DevStatus hs;
-    rc = read_status(ctx, st, ds, &hs);
+    rc = dcg_read_status(ctx, st, ds, &hs);
     if (rc) return rc;
     if (loglik) *loglik = hs.value;
     if (psi) *psi = hs.value2;

@@ -7,6 +7,7 @@
 //   gemm_lr_kernel   C = A B with the reference's i-k-j order (K4, Z.U; _core.pyx:31-44)
 #include "common.cuh"
 #include "gemv.cuh"
+#include "symgemv.cuh"
 
 // =============================================================================
 // K1 standalone GEMV: one CTA per contiguous row range (grid = #SM).
@@ -43,6 +44,50 @@ int dcg_gemv_launch(dcg_context* ctx, cudaStream_t st, const double* K, long lon
     long long blocks = ctx->sm_count;
     if (blocks > rows) blocks = rows;
     gemv_kernel<<<(unsigned)blocks, DCG_NT, smem, st>>>(K, ldk, n, rows, v, s_in, s_out, shift, v_rows, y);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}
+
+// =============================================================================
+// K1 over the lower triangle of a symmetric K (symgemv.cuh): pass 1 streams
+// the tiles, pass 2 combines the per-tile partials.  Both launches use the
+// same grid, which fixes the tile partition.
+// =============================================================================
+__global__ void __launch_bounds__(DCG_NT, 1)
+    sym_pass1_kernel(const double* __restrict__ K, long long ldk, long long n, const double* v, const double* s_in,
+                     double* colpart, double* rowpart) {
+    extern __shared__ __align__(16) double smem[];
+    sym_pass1(K, ldk, n, v, s_in, colpart, rowpart, smem);
+}
+
+__global__ void __launch_bounds__(DCG_NT, 1)
+    sym_pass2_kernel(long long n, const double* colpart, const double* rowpart, const double* v,
+                     const double* s_out, double shift, double* y) {
+    __shared__ double red[8 * DCG_TB];
+    const long long r0 = part_begin(n, gridDim.x, blockIdx.x);
+    const long long r1 = part_begin(n, gridDim.x, blockIdx.x + 1);
+    sym_pass2(n, colpart, rowpart, r0, r1, red, [&](long long i, double t) {
+        double val = s_out ? mul_rn(s_out[i], t) : t;
+        if (shift != 0.0) val = add_rn(mul_rn(shift, v[i]), val);
+        y[i] = val;
+    });
+}
+
+size_t dcg_sym_apply_scratch_doubles(long long n) { return 2 * (size_t)sym_ntiles(n) * DCG_TB; }
+
+// y = shift v + s_out (.) K (s_in (.) v) with K exactly symmetric (n x n, unsharded).
+int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, long long ldk, long long n, const double* v,
+                  const double* s_in, const double* s_out, double shift, double* y, double* scratch) {
+    if (n <= 0) return DCG_OK;
+    const size_t smem = sizeof(double) * (size_t)sym_smem_doubles();
+    DCG_CUDA(cudaFuncSetAttribute(sym_pass1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const long long ntt = sym_ntiles(n);
+    double* colpart = scratch;
+    double* rowpart = scratch + ntt * DCG_TB;
+    const int G = ctx->sm_count;
+    sym_pass1_kernel<<<G, DCG_NT, smem, st>>>(K, ldk, n, v, s_in, colpart, rowpart);
+    DCG_LAUNCHED();
+    sym_pass2_kernel<<<G, DCG_NT, 0, st>>>(n, colpart, rowpart, v, s_out, shift, y);
     DCG_LAUNCHED();
     return DCG_OK;
 }

@@ -136,5 +136,38 @@ __host__ __device__ __forceinline__ long long part_begin(long long n, long long 
     return (n * i) / parts;
 }
 
-// ---- host launch helpers ----------------------------------------------------
-int dcg_launch_check();
+// ---- host helpers -------------------------------------------------------------
+// bump allocator over ctx->ws (reserve the total first, then carve)
+struct Arena {
+    char* base;
+    size_t off;
+    template <class T>
+    T* take(size_t count) {
+        off = (off + 255) & ~size_t(255);
+        T* p = reinterpret_cast<T*>(base + off);
+        off += sizeof(T) * count;
+        return p;
+    }
+};
+static inline size_t al(size_t bytes) { return (bytes + 255) & ~size_t(255); }
+static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// copy a device status block to the host (synchronises the stream)
+int dcg_read_status(dcg_context* ctx, cudaStream_t st, const DevStatus* dev, DevStatus* out);
+
+// Deterministic "last CTA reduces" handshake: every CTA publishes its partials,
+// then calls this; exactly one CTA (the last to arrive) gets true and may read
+// all partials.  The counter returns to zero for the next launch.
+__device__ __forceinline__ bool cta_last_arrival(unsigned int* counter, unsigned int total) {
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int prev = atomicAdd(counter, 1u);
+        s_last = (prev == total - 1) ? 1 : 0;
+        if (s_last) *counter = 0u;
+    }
+    __syncthreads();
+    if (s_last) __threadfence();
+    return s_last != 0;
+}

@@ -73,7 +73,7 @@ __device__ double cta_pivot_tol(const double* A, int lda, const int* idx, int n,
 // Warp-level forward substitution: y = L^-1 b for one right-hand side
 // (b, y with strides), reference order per element (_core.pyx:69-80).
 // Lanes own rows lane + 32u.
-__device__ void warp_solve_lower(const double* L, int ldl, int n, const double* b, int bstride,
+static __device__ void warp_solve_lower(const double* L, int ldl, int n, const double* b, int bstride,
                                  double* y, int ystride) {
     const int lane = threadIdx.x & 31;
     double a[(DCG_MAX_T + 31) / 32];
@@ -104,7 +104,7 @@ __device__ void warp_solve_lower(const double* L, int ldl, int n, const double* 
 }
 
 // Warp-level back substitution x = L^-T b (wavefront order).
-__device__ void warp_solve_lower_trans(const double* L, int ldl, int n, const double* b, int bstride,
+static __device__ void warp_solve_lower_trans(const double* L, int ldl, int n, const double* b, int bstride,
                                        double* x, int xstride) {
     const int lane = threadIdx.x & 31;
     double a[(DCG_MAX_T + 31) / 32];
@@ -315,10 +315,13 @@ __global__ void __launch_bounds__(SD_NT) gram_factor_kernel(const double* Graw, 
 // Global scratch `wk` holds 5 * T * T doubles.  Outputs: theta (k), U (na x k,
 // row-major over the surviving columns), active list, status (count = na).
 // ===========================================================================
+// `plan` (when non-null) carries the pencil order T (= count) decided on the
+// device by the extraction's zero-column scan, and its status: the kernel does
+// nothing unless that status is DCG_OK, so the pipeline needs no host sync.
 __global__ void __launch_bounds__(SD_NT) ritz_pencil_kernel(const double* Fraw, const double* Graw, int T,
                                                             int k, int largest, int max_sweeps,
                                                             double* wk, double* theta, double* U,
-                                                            int* active, DevStatus* st) {
+                                                            int* active, DevStatus* st, const DevStatus* plan) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[40];
     __shared__ double s_scal[4];
@@ -327,6 +330,10 @@ __global__ void __launch_bounds__(SD_NT) ritz_pencil_kernel(const double* Fraw, 
     __shared__ int s_act[DCG_MAX_T];
     __shared__ int s_order[DCG_MAX_T];
     __shared__ int s_na;
+    if (plan) {
+        if (plan->status != DCG_OK) return;
+        T = (int)plan->count;
+    }
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nw = blockDim.x >> 5;
     double* F = wk;
@@ -597,10 +604,12 @@ int dcg_gram_factor_launch(cudaStream_t st, const double* Graw, int k, int prune
 size_t dcg_pencil_smem(int T) { return sizeof(double) * 2 * (size_t)T * T; }
 
 int dcg_ritz_pencil_launch(cudaStream_t st, const double* Fraw, const double* Graw, int T, int k, int largest,
-                           int max_sweeps, double* wk, double* theta, double* U, int* active, DevStatus* ds) {
+                           int max_sweeps, double* wk, double* theta, double* U, int* active, DevStatus* ds,
+                           const DevStatus* plan) {
     const size_t smem = dcg_pencil_smem(T);
     DCG_CUDA(cudaFuncSetAttribute(ritz_pencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    ritz_pencil_kernel<<<1, SD_NT, smem, st>>>(Fraw, Graw, T, k, largest, max_sweeps, wk, theta, U, active, ds);
+    ritz_pencil_kernel<<<1, SD_NT, smem, st>>>(Fraw, Graw, T, k, largest, max_sweeps, wk, theta, U, active, ds,
+                                                plan);
     DCG_LAUNCHED();
     return DCG_OK;
 }

@@ -1,0 +1,383 @@
+// Harmonic-Ritz extraction (recycle.py:95-159) and the basis-refresh Gram
+// (recycle.py:66-92) as short pipelines with device-side decisions.
+//
+// Extraction, all kernels on one stream, no host synchronisation inside:
+//   E1 zgather     Z = [W_prev, p_0..p_m-1], AZ = [AW_prev, (r_j - r_j+1)/alpha_j]
+//                  (row-major n x T), per-CTA column sums of squares; the last
+//                  CTA forms the norms, the keep list of non-zero columns and
+//                  the plan (T_kept, or BasisDeficient when T_kept < k)
+//   E2 zscale_fg   Zs = Z[:, keep] / norm, AZs likewise (n x T_kept) and the
+//                  per-CTA partials of F = AZs'Zs, G = AZs'AZs
+//   E3 fg_reduce   fixed-order reduction of the partials (one warp per entry)
+//   E4 pencil      symmetrise, failing-pivot pruning, G u = theta F u (dense_small.cu)
+//   E5 uscale      ||Zs u_j|| per selected vector (last CTA scales U)
+//   E6 wnext       W_next = Zs U, AW_next = AZs U in the reference's i-k-j order
+// The outcome (status, payload, T) is written to a device result block the
+// caller reads whenever it joins the stream, so the extraction can overlap
+// other work (the GPC Newton update) on a side stream.
+#include "common.cuh"
+
+int dcg_ritz_pencil_launch(cudaStream_t, const double*, const double*, int, int, int, int, double*, double*, double*,
+                           int*, DevStatus*, const DevStatus*);
+size_t dcg_pencil_smem(int T);
+
+#define EX_NT 256
+#define EX_ROWS 32
+
+// ---------------------------------------------------------------------------- E1
+__global__ void __launch_bounds__(EX_NT)
+    zgather_kernel(long long n, int kp, const double* __restrict__ Wp, const double* __restrict__ AWp, int m,
+                   const double* __restrict__ P, const double* __restrict__ R, const double* __restrict__ alpha,
+                   int k, double* Zraw, double* AZraw, double* part, unsigned int* counter, double* norms, int* keep,
+                   DevStatus* plan) {
+    extern __shared__ double sm[];
+    const int T = kp + m;
+    double* zt = sm;                   // EX_ROWS x T
+    double* azt = sm + EX_ROWS * T;    // EX_ROWS x T
+    const int tid = threadIdx.x;
+    const long long r0 = part_begin(n, gridDim.x, blockIdx.x), r1 = part_begin(n, gridDim.x, blockIdx.x + 1);
+    double acc = 0.0;   // column tid's sum of squares (tid < T)
+    for (long long i0 = r0; i0 < r1; i0 += EX_ROWS) {
+        const int nr = (int)min((long long)EX_ROWS, r1 - i0);
+        for (int e = tid; e < nr * kp; e += EX_NT) {
+            const int r = e / kp, c = e % kp;
+            zt[r * T + c] = Wp[(i0 + r) * kp + c];
+            azt[r * T + c] = AWp[(i0 + r) * kp + c];
+        }
+        for (int e = tid; e < EX_ROWS * m; e += EX_NT) {
+            const int j = e / EX_ROWS, r = e % EX_ROWS;
+            if (r < nr) {
+                const long long i = i0 + r;
+                zt[r * T + kp + j] = P[(long long)j * n + i];
+                azt[r * T + kp + j] = div_rn(sub_rn(R[(long long)j * n + i], R[(long long)(j + 1) * n + i]), alpha[j]);
+            }
+        }
+        __syncthreads();
+        for (int e = tid; e < nr * T; e += EX_NT) {
+            Zraw[i0 * T + e] = zt[e];
+            AZraw[i0 * T + e] = azt[e];
+        }
+        if (tid < T)
+            for (int r = 0; r < nr; ++r) acc = fma(zt[r * T + tid], zt[r * T + tid], acc);
+        __syncthreads();
+    }
+    if (tid < T) part[(long long)blockIdx.x * T + tid] = acc;
+    if (!cta_last_arrival(counter, gridDim.x)) return;
+    // last CTA: norms (one warp per column), keep list, plan
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int c = warp; c < T; c += EX_NT / 32) {
+        double s = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) s += ld_cg(part + (long long)b * T + c);
+        s = warp_sum(s);
+        if (lane == 0) norms[c] = sqrt(s);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int t = 0;
+        for (int c = 0; c < T; ++c)
+            if (norms[c] > 0.0) keep[t++] = c;
+        plan->count = t;
+        plan->info = t;
+        plan->status = (t < k) ? DCG_E_BASIS_DEFICIENT : DCG_OK;   // recycle.py:131-132
+    }
+}
+
+// ---------------------------------------------------------------------------- E2
+#define FG_PPT 8
+__global__ void __launch_bounds__(EX_NT)
+    zscale_fg_kernel(long long n, int T, const double* __restrict__ Zraw, const double* __restrict__ AZraw,
+                     const double* __restrict__ norms, const int* __restrict__ keep, const DevStatus* plan, double* Zs,
+                     double* AZs, double* part) {
+    if (plan->status != DCG_OK) return;
+    extern __shared__ double sm[];
+    const int Tk = (int)plan->count;
+    const int npairs = 2 * Tk * Tk;
+    const int p0 = blockIdx.y * (EX_NT * FG_PPT);
+    if (p0 >= npairs) return;
+    double* zs = sm;                    // EX_ROWS x Tk
+    double* azs = sm + EX_ROWS * T;     // EX_ROWS x Tk
+    const int tid = threadIdx.x;
+    const long long r0 = part_begin(n, gridDim.x, blockIdx.x), r1 = part_begin(n, gridDim.x, blockIdx.x + 1);
+    double acc[FG_PPT];
+    int pa[FG_PPT], pb[FG_PPT];
+    bool pg[FG_PPT];
+#pragma unroll
+    for (int u = 0; u < FG_PPT; ++u) {
+        acc[u] = 0.0;
+        int e = p0 + u * EX_NT + tid;
+        pg[u] = e >= Tk * Tk;            // G entries follow the F entries
+        if (pg[u]) e -= Tk * Tk;
+        const bool valid = p0 + u * EX_NT + tid < npairs;
+        pa[u] = valid ? e / Tk : -1;
+        pb[u] = valid ? e % Tk : 0;
+    }
+    for (long long i0 = r0; i0 < r1; i0 += EX_ROWS) {
+        const int nr = (int)min((long long)EX_ROWS, r1 - i0);
+        __syncthreads();
+        for (int e = tid; e < nr * Tk; e += EX_NT) {
+            const int r = e / Tk, cc = e % Tk;
+            const int c = keep[cc];
+            const double nv = norms[c];
+            const double zv = div_rn(Zraw[(i0 + r) * T + c], nv);
+            const double av = div_rn(AZraw[(i0 + r) * T + c], nv);
+            zs[r * Tk + cc] = zv;
+            azs[r * Tk + cc] = av;
+            if (blockIdx.y == 0) {
+                Zs[(i0 + r) * Tk + cc] = zv;
+                AZs[(i0 + r) * Tk + cc] = av;
+            }
+        }
+        __syncthreads();
+        for (int r = 0; r < nr; ++r) {
+#pragma unroll
+            for (int u = 0; u < FG_PPT; ++u)
+                if (pa[u] >= 0) acc[u] = fma(azs[r * Tk + pa[u]], pg[u] ? azs[r * Tk + pb[u]] : zs[r * Tk + pb[u]], acc[u]);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < FG_PPT; ++u) {
+        const int e = p0 + u * EX_NT + tid;
+        if (e < npairs) part[(long long)blockIdx.x * npairs + e] = acc[u];
+    }
+}
+
+// ---------------------------------------------------------------------------- E3
+__global__ void fg_reduce_kernel(const double* part, int nparts, const DevStatus* plan, double* Fraw, double* Graw) {
+    if (plan->status != DCG_OK) return;
+    const int Tk = (int)plan->count;
+    const int npairs = 2 * Tk * Tk;
+    const int lane = threadIdx.x & 31;
+    const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (e >= npairs) return;
+    double s = 0.0;
+    for (int b = lane; b < nparts; b += 32) s += part[(long long)b * npairs + e];
+    s = warp_sum(s);
+    if (lane == 0) {
+        if (e < Tk * Tk) Fraw[e] = s;
+        else Graw[e - Tk * Tk] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------- E5
+// ||Zs u_j||^2 partials for the selected vectors; the last CTA scales U.
+__global__ void __launch_bounds__(EX_NT)
+    uscale_kernel(long long n, int k, const double* __restrict__ Zs, const DevStatus* plan, const DevStatus* pencil,
+                  double* U, const int* active, double* Uexp, double* part, unsigned int* counter) {
+    if (plan->status != DCG_OK || pencil->status != DCG_OK) return;
+    extern __shared__ double sm[];
+    const int Tk = (int)plan->count, na = (int)pencil->count;
+    double* ue = sm;                       // Tk x k
+    double* wp = sm + Tk * k;              // 8 warps x 64
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < Tk * k; e += EX_NT) ue[e] = 0.0;
+    __syncthreads();
+    for (int e = tid; e < na * k; e += EX_NT) ue[active[e / k] * k + e % k] = U[e];
+    __syncthreads();
+    const long long r0 = part_begin(n, gridDim.x, blockIdx.x), r1 = part_begin(n, gridDim.x, blockIdx.x + 1);
+    double s0 = 0.0, s1 = 0.0;   // lanes own columns lane, lane + 32
+    for (long long i = r0 + warp; i < r1; i += EX_NT / 32) {
+        double v0 = 0.0, v1 = 0.0;
+        for (int c = 0; c < Tk; ++c) {
+            const double z = Zs[i * Tk + c];
+            if (lane < k) v0 = fma(z, ue[c * k + lane], v0);
+            if (lane + 32 < k) v1 = fma(z, ue[c * k + lane + 32], v1);
+        }
+        s0 = fma(v0, v0, s0);
+        s1 = fma(v1, v1, s1);
+    }
+    wp[warp * 64 + lane] = s0;
+    wp[warp * 64 + lane + 32] = s1;
+    __syncthreads();
+    if (tid < k) {
+        double s = 0.0;
+        for (int w = 0; w < EX_NT / 32; ++w) s += wp[w * 64 + tid];
+        part[(long long)blockIdx.x * k + tid] = s;
+    }
+    if (!cta_last_arrival(counter, gridDim.x)) return;
+    __shared__ double scale[DCG_MAX_K];
+    for (int j = warp; j < k; j += EX_NT / 32) {
+        double s = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) s += ld_cg(part + (long long)b * k + j);
+        s = warp_sum(s);
+        if (lane == 0) scale[j] = sqrt(s);
+    }
+    __syncthreads();
+    // u[:, j] /= ||Z u_j|| when positive (recycle.py:150-153)
+    for (int e = tid; e < na * k; e += EX_NT) {
+        const double sc = scale[e % k];
+        if (sc > 0.0) U[e] = div_rn(U[e], sc);
+    }
+    __syncthreads();
+    for (int e = tid; e < Tk * k; e += EX_NT) Uexp[e] = 0.0;
+    __syncthreads();
+    for (int e = tid; e < na * k; e += EX_NT) Uexp[active[e / k] * k + e % k] = U[e];
+}
+
+// ---------------------------------------------------------------------------- E6
+// W_next = Zs U, AW_next = AZs U with the reference's accumulation order
+// (_core.gemm i-k-j, recycle.py:157-158); z output = the surviving columns.
+__global__ void __launch_bounds__(EX_NT)
+    wnext_kernel(long long n, int k, const double* __restrict__ Zs, const double* __restrict__ AZs,
+                 const DevStatus* plan, const DevStatus* pencil, const double* __restrict__ Uexp, const int* active,
+                 double* w_next, double* aw_next, double* z_out, long long* result) {
+    const bool ok = plan->status == DCG_OK && pencil->status == DCG_OK;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        // result block: status, info, t_out
+        if (plan->status != DCG_OK) {
+            result[0] = plan->status;
+            result[1] = plan->info;
+            result[2] = plan->count;
+        } else {
+            result[0] = pencil->status;
+            result[1] = pencil->info;
+            result[2] = pencil->count;
+        }
+    }
+    if (!ok) return;
+    extern __shared__ double sm[];
+    const int Tk = (int)plan->count, na = (int)pencil->count;
+    double* ue = sm;   // Tk x k
+    for (int e = threadIdx.x; e < Tk * k; e += EX_NT) ue[e] = Uexp[e];
+    __syncthreads();
+    const long long total = n * k;
+    for (long long e = blockIdx.x * (long long)EX_NT + threadIdx.x; e < total; e += (long long)gridDim.x * EX_NT) {
+        const long long i = e / k;
+        const int j = (int)(e % k);
+        double a = 0.0, b = 0.0;
+        for (int c = 0; c < Tk; ++c) {
+            const double u = ue[c * k + j];
+            a = add_rn(a, mul_rn(Zs[i * Tk + c], u));
+            b = add_rn(b, mul_rn(AZs[i * Tk + c], u));
+        }
+        w_next[e] = a;
+        aw_next[e] = b;
+    }
+    if (z_out) {
+        const long long tz = n * na;
+        for (long long e = blockIdx.x * (long long)EX_NT + threadIdx.x; e < tz; e += (long long)gridDim.x * EX_NT)
+            z_out[e] = Zs[(e / na) * Tk + active[e % na]];
+    }
+}
+
+// ---------------------------------------------------------------------------- launch
+static size_t extract_ws_bytes(dcg_context* ctx, long long n, int T, int k) {
+    const int G = ctx->sm_count;
+    const size_t nT = (size_t)n * T;
+    const int gy = (2 * T * T + EX_NT * FG_PPT - 1) / (EX_NT * FG_PPT);
+    (void)gy;
+    return 4 * al(sizeof(double) * nT) + al(sizeof(double) * (size_t)G * T) + al(sizeof(double) * T) +
+           2 * al(sizeof(int) * T) + 2 * al(sizeof(double) * T * T) + al(sizeof(double) * (size_t)G * 2 * T * T) +
+           al(sizeof(double) * 5 * T * T) + 2 * al(sizeof(double) * T * k) + al(sizeof(double) * (size_t)G * k) +
+           3 * al(sizeof(DevStatus)) + 2 * al(sizeof(unsigned int) * 4) + 8192;
+}
+
+// Enqueue the extraction; `d_result` (3 x int64 on the device) receives
+// status, info, t_out when the stream reaches the end.  Host-checkable
+// argument errors return immediately.
+extern "C" int dcg_ritz_extract_async(dcg_context* ctx, void* stream, long long n, const dcg_krylov_log* log,
+                                      long long m, const dcg_basis* prev, long long k, int selection, double* d_theta,
+                                      double* d_u, double* d_z, double* d_w_next, double* d_aw_next,
+                                      long long* d_result) {
+    if (!ctx || n < 0 || m < 0 || k < 0 || !d_result) return DCG_E_CONFIG;
+    if (selection != DCG_SELECT_SMALLEST && selection != DCG_SELECT_LARGEST) return DCG_E_CONFIG;
+    const long long kp = prev ? prev->k : 0;
+    const long long T = kp + m;
+    cudaStream_t st = as_stream(stream);
+    if (k > T || k == 0) {
+        // decided on the host (recycle.py:104-108 / k == 0): write the result block
+        long long h[3] = {k > T ? (long long)DCG_E_BASIS_DEFICIENT : (long long)DCG_OK, T, T};
+        DCG_CUDA(cudaMemcpyAsync(d_result, h, sizeof(h), cudaMemcpyHostToDevice, st));
+        DCG_CUDA(cudaStreamSynchronize(st));   // h is a stack buffer
+        return DCG_OK;
+    }
+    if (k > DCG_MAX_K || T > DCG_MAX_T) return DCG_E_UNSUPPORTED;
+    if (m > 0 && (!log || log->ell < m || !log->d_p || !log->d_r || !log->d_alpha)) return DCG_E_CONFIG;
+    if (kp > 0 && (!prev->d_w || !prev->d_aw)) return DCG_E_CONFIG;
+    int rc = dcg_ws_reserve(ctx, extract_ws_bytes(ctx, n, (int)T, (int)k));
+    if (rc) return rc;
+    const int G = ctx->sm_count;
+    Arena ar{static_cast<char*>(ctx->ws), 0};
+    const size_t nT = (size_t)n * T;
+    double* Zraw = ar.take<double>(nT);
+    double* AZraw = ar.take<double>(nT);
+    double* Zs = ar.take<double>(nT);
+    double* AZs = ar.take<double>(nT);
+    double* part = ar.take<double>((size_t)G * T);
+    double* norms = ar.take<double>(T);
+    int* keep = ar.take<int>(T);
+    int* active = ar.take<int>(T);
+    double* Fraw = ar.take<double>(T * T);
+    double* Graw = ar.take<double>(T * T);
+    double* fgpart = ar.take<double>((size_t)G * 2 * T * T);
+    double* wk = ar.take<double>(5 * T * T);
+    double* U = ar.take<double>(T * k);
+    double* Uexp = ar.take<double>(T * k);
+    double* upart = ar.take<double>((size_t)G * k);
+    DevStatus* plan = ar.take<DevStatus>(1);
+    DevStatus* pencil = ar.take<DevStatus>(1);
+    unsigned int* counters = ar.take<unsigned int>(4);
+    DCG_CUDA(cudaMemsetAsync(plan, 0, al(sizeof(DevStatus)) * 2, st));
+    DCG_CUDA(cudaMemsetAsync(counters, 0, 16, st));
+    const double* Wp = kp ? prev->d_w : nullptr;
+    const double* AWp = kp ? prev->d_aw : nullptr;
+    const double* P = m ? log->d_p : nullptr;
+    const double* R = m ? log->d_r : nullptr;
+    const double* alpha = m ? log->d_alpha : nullptr;
+
+    int nb = G;
+    if (n < (long long)nb * EX_ROWS) nb = (int)max(1LL, (n + EX_ROWS - 1) / EX_ROWS);
+    const size_t sm1 = sizeof(double) * 2 * EX_ROWS * T;
+    DCG_CUDA(cudaFuncSetAttribute(zgather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+    zgather_kernel<<<nb, EX_NT, sm1, st>>>(n, (int)kp, Wp, AWp, (int)m, P, R, alpha, (int)k, Zraw, AZraw, part,
+                                           counters, norms, keep, plan);
+    DCG_LAUNCHED();
+    const int gy = (int)((2 * T * T + EX_NT * FG_PPT - 1) / (EX_NT * FG_PPT));
+    DCG_CUDA(cudaFuncSetAttribute(zscale_fg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+    zscale_fg_kernel<<<dim3(nb, gy), EX_NT, sm1, st>>>(n, (int)T, Zraw, AZraw, norms, keep, plan, Zs, AZs, fgpart);
+    DCG_LAUNCHED();
+    const int warps = (int)(2 * T * T);
+    fg_reduce_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>(fgpart, nb, plan, Fraw, Graw);
+    DCG_LAUNCHED();
+    rc = dcg_ritz_pencil_launch(st, Fraw, Graw, (int)T, (int)k, selection == DCG_SELECT_LARGEST, 60, wk, d_theta, U,
+                                active, pencil, plan);
+    if (rc) return rc;
+    const size_t sm5 = sizeof(double) * ((size_t)T * k + 8 * 64);
+    DCG_CUDA(cudaFuncSetAttribute(uscale_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm5));
+    uscale_kernel<<<nb, EX_NT, sm5, st>>>(n, (int)k, Zs, plan, pencil, U, active, Uexp, upart, counters + 1);
+    DCG_LAUNCHED();
+    const size_t sm6 = sizeof(double) * (size_t)T * k;
+    DCG_CUDA(cudaFuncSetAttribute(wnext_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm6));
+    wnext_kernel<<<G * 2, EX_NT, sm6, st>>>(n, (int)k, Zs, AZs, plan, pencil, Uexp, active, d_w_next, d_aw_next, d_z,
+                                            d_result);
+    DCG_LAUNCHED();
+    if (d_u) DCG_CUDA(cudaMemcpyAsync(d_u, U, sizeof(double) * T * k, cudaMemcpyDeviceToDevice, st));
+    return DCG_OK;
+}
+
+// Synchronous form: enqueue, wait, and map the outcome to a status.
+extern "C" int dcg_ritz_extract(dcg_context* ctx, void* stream, long long n, const dcg_krylov_log* log, long long m,
+                                const dcg_basis* prev, long long k, int selection, double* d_theta, double* d_u,
+                                double* d_z, double* d_w_next, double* d_aw_next, long long* t_out, long long* info) {
+    if (info) *info = 0;
+    const long long kp = prev ? prev->k : 0;
+    if (t_out) *t_out = kp + m;
+    if (!ctx) return DCG_E_CONFIG;
+    cudaStream_t st = as_stream(stream);
+    int rc = dcg_host_reserve(ctx, 64);
+    if (rc) return rc;
+    // the result block lives at the end of a small dedicated allocation
+    static thread_local long long* d_res = nullptr;
+    if (!d_res) DCG_CUDA(cudaMalloc(&d_res, 64));
+    rc = dcg_ritz_extract_async(ctx, stream, n, log, m, prev, k, selection, d_theta, d_u, d_z, d_w_next, d_aw_next,
+                                d_res);
+    if (rc) return rc;
+    long long* h = static_cast<long long*>(ctx->host);
+    DCG_CUDA(cudaMemcpyAsync(h, d_res, 3 * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    DCG_CUDA(cudaStreamSynchronize(st));
+    if (t_out) *t_out = h[2];
+    if (h[0] != DCG_OK) {
+        if (info) *info = h[1];
+        return (int)h[0];
+    }
+    return DCG_OK;
+}

@@ -16,6 +16,7 @@
 
 #include "common.cuh"
 #include "gemv.cuh"
+#include "symgemv.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -50,6 +51,8 @@ struct SolveArgs {
     double* p;
     double* ap;
     double* partials;
+    double* colpart;   // symmetric strategy: per-tile partials
+    double* rowpart;
     int ps;   // partial stride (doubles)
     DevStatus* st;
 };
@@ -118,6 +121,12 @@ struct WarpAcc {
     double c0, c1;
 };
 
+// Shared-memory doubles of the GEMV region for each strategy.
+__host__ __device__ __forceinline__ long long gemv_region_doubles(bool sym, long long n) {
+    return sym ? sym_smem_doubles() : (min(n, (long long)DCG_QT) + 2 + DCG_NW * DCG_RB);
+}
+
+template <bool SYM>
 __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) double smem[];
@@ -126,9 +135,8 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     const int G = gridDim.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int xt = (int)min(n, (long long)DCG_QT) + 2;
-    double* s_x = smem;                                  // xt
-    double* s_red = s_x + xt;                            // DCG_NW * DCG_RB
-    double* s_L = s_red + DCG_NW * DCG_RB;               // k*k
+    double* s_g = smem;                                  // GEMV region (strategy dependent)
+    double* s_L = s_g + gemv_region_doubles(SYM, n);     // k*k
     double* s_rd = s_L + k * k;                          // k   (1/L_jj)
     double* s_c = s_rd + DCG_MAX_K;                      // 1 + DCG_MAX_K reduced slots
     double* s_mu = s_c + DCG_MAX_K + 2;                  // DCG_MAX_K
@@ -142,6 +150,18 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     const double* __restrict__ K = a.K;
     const double* s = a.s;
     const double shift = a.shift;
+
+    // t = K (s (.) v) for the own rows [r0, r1); epi(i, t_i) per row.  The
+    // symmetric strategy contains one extra grid barrier between its passes.
+    auto gemv = [&](const double* v, auto&& epi) {
+        if constexpr (SYM) {
+            sym_pass1(K, a.ldk, n, v, s, a.colpart, a.rowpart, s_g);
+            grid.sync();
+            sym_pass2(n, a.colpart, a.rowpart, r0, r1, s_g, epi);
+        } else {
+            block_gemv<true>(K, a.ldk, n, v, s, r0, r1, s_g, s_g + xt, epi);
+        }
+    };
 
     for (int i = tid; i < k * k; i += blockDim.x) s_L[i] = a.L[i];
     __syncthreads();
@@ -177,7 +197,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     // ---------------- prologue: norm_b and the warm-start correction ----------
     // deflated_cg_solve: r_prev = b - A x_prev ; x0 = x_prev + W chol_solve(L, W' r_prev)
     if (a.warm && deflate) {
-        block_gemv<false>(K, a.ldk, n, a.x0, s, r0, r1, s_x, s_red, [&](long long i, double t) {
+        gemv(a.x0, [&](long long i, double t) {
             const double ax = s ? add_rn(mul_rn(shift, a.x0[i]), mul_rn(s[i], t))
                                 : add_rn(mul_rn(shift, a.x0[i]), t);
             a.r[i] = sub_rn(a.b[i], ax);
@@ -237,7 +257,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     grid.sync();
 
     // ---------------- r0 = b - A x0 ; mu ; p0 ------------------------------------
-    block_gemv<true>(K, a.ldk, n, a.x, s, r0, r1, s_x, s_red, [&](long long i, double t) {
+    gemv(a.x, [&](long long i, double t) {
         const double xi = a.x[i];
         const double ax = s ? add_rn(mul_rn(shift, xi), mul_rn(s[i], t)) : add_rn(mul_rn(shift, xi), t);
         a.r[i] = sub_rn(a.b[i], ax);
@@ -282,7 +302,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     while (cont) {
         // phase G: Ap, partial p'Ap
         double dpart = 0.0;
-        block_gemv<true>(K, a.ldk, n, a.p, s, r0, r1, s_x, s_red, [&](long long i, double t) {
+        gemv(a.p, [&](long long i, double t) {
             const double pi = ld_cg(a.p + i);
             const double api = s ? add_rn(mul_rn(shift, pi), mul_rn(s[i], t)) : add_rn(mul_rn(shift, pi), t);
             a.ap[i] = api;
@@ -308,7 +328,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         const bool recompute = (a.recompute > 0) && (it % a.recompute == 0);
         if (recompute) {
             grid.sync();
-            block_gemv<true>(K, a.ldk, n, a.x, s, r0, r1, s_x, s_red, [&](long long i, double t) {
+            gemv(a.x, [&](long long i, double t) {
                 const double xi = a.x[i];
                 const double ax = s ? add_rn(mul_rn(shift, xi), mul_rn(s[i], t)) : add_rn(mul_rn(shift, xi), t);
                 a.r[i] = sub_rn(a.b[i], ax);
@@ -376,9 +396,8 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
 
 }  // namespace
 
-size_t dcg_solve_smem_bytes(long long n, int k) {
-    const long long xt = (n < DCG_QT ? n : DCG_QT) + 2;
-    return sizeof(double) * (size_t)(xt + DCG_NW * DCG_RB + k * k + DCG_MAX_K + DCG_MAX_K + 2 +
+size_t dcg_solve_smem_bytes(long long n, int k, bool sym) {
+    return sizeof(double) * (size_t)(gemv_region_doubles(sym, n) + k * k + DCG_MAX_K + DCG_MAX_K + 2 +
                                      DCG_MAX_K + DCG_NW * (DCG_MAX_K + 1) + 64);
 }
 
@@ -389,7 +408,8 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
     if (!ctx || !op || !cfg || !d_b || !d_x0 || !d_x || !d_history) return DCG_E_CONFIG;
     if (info) *info = 0;
     const long long n = op->n;
-    if (op->kind != DCG_OP_DENSE) return DCG_E_UNSUPPORTED;
+    if (op->kind != DCG_OP_DENSE && op->kind != DCG_OP_DENSE_SYM) return DCG_E_UNSUPPORTED;
+    const bool sym = op->kind == DCG_OP_DENSE_SYM && ((reinterpret_cast<uintptr_t>(d_x0) | reinterpret_cast<uintptr_t>(op->d_s)) & 15) == 0;
     if (op->row0 != 0 || op->rows != n) return DCG_E_UNSUPPORTED;   // sharded solves: host loop
     if (op->ldk < n || (op->ldk & 1) || (reinterpret_cast<uintptr_t>(op->d_k) & 15)) return DCG_E_CONFIG;
     if (!(cfg->tol > 0.0) || cfg->ell < 0 || cfg->recompute_residual_every < 0) return DCG_E_CONFIG;
@@ -406,7 +426,8 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
     const int G = ctx->solve_blocks;
     const int ps = ((1 + k) + 1) & ~1;
     const size_t vec = sizeof(double) * (size_t)((n + 31) & ~31LL);
-    const size_t need = 3 * vec + sizeof(double) * (size_t)G * ps + 256;
+    const size_t tiles = sym ? (size_t)sym_ntiles(n) : 0;
+    const size_t need = 3 * vec + sizeof(double) * (size_t)G * ps + 256 + 2 * sizeof(double) * tiles * DCG_TB + 512;
     int rc = dcg_ws_reserve(ctx, need);
     if (rc) return rc;
     char* w = static_cast<char*>(ctx->ws);
@@ -441,16 +462,20 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
     a.partials = reinterpret_cast<double*>(w + 3 * vec);
     a.ps = ps;
     a.st = reinterpret_cast<DevStatus*>(w + 3 * vec + sizeof(double) * (size_t)G * ps);
+    {
+        const size_t off = (3 * vec + sizeof(double) * (size_t)G * ps + sizeof(DevStatus) + 255) & ~size_t(255);
+        a.colpart = reinterpret_cast<double*>(w + off);
+        a.rowpart = a.colpart + tiles * DCG_TB;
+    }
 
     cudaStream_t st = as_stream(stream);
-    const size_t smem = dcg_solve_smem_bytes(n, k);
-    DCG_CUDA(cudaFuncSetAttribute(dcg_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+    const size_t smem = dcg_solve_smem_bytes(n, k, sym);
+    const void* kfn = sym ? (const void*)dcg_solve_kernel<true> : (const void*)dcg_solve_kernel<false>;
+    DCG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     DCG_CUDA(cudaMemsetAsync(a.st, 0, sizeof(DevStatus), st));
     void* args[] = {&a};
     DCG_CUDA(cudaEventRecord(ctx->ev0, st));
-    DCG_CUDA(cudaLaunchCooperativeKernel((const void*)dcg_solve_kernel, dim3(G), dim3(DCG_NT), args,
-                                         smem, st));
+    DCG_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(DCG_NT), args, smem, st));
     dcg_count_launch();
     DCG_CUDA(cudaEventRecord(ctx->ev1, st));
     rc = dcg_host_reserve(ctx, sizeof(DevStatus));

@@ -1,0 +1,342 @@
+// Symmetric GEMV over the lower triangle of a dense, exactly symmetric K.
+//
+// K1 streams 8 n^2 bytes per product; K = K' lets every element serve twice,
+// so this strategy streams only the ~n^2/2 lower-triangle entries (halving
+// HBM traffic per CG iteration), as 64 x 64 tiles (I, J <= I) of the padded
+// row-major storage:
+//
+//   pass 1 (all CTAs): the linear tile sequence is split into balanced
+//     contiguous ranges, one per CTA.  Tiles flow through a DCG_SYM_STAGES-deep
+//     shared-memory ring filled by per-thread 16-byte cp.async copies whose
+//     completion is tracked by mbarriers (cp.async.mbarrier.arrive), and
+//     released by one arrival per warp: warps never wait on a CTA barrier per
+//     tile.  Warp w owns columns 4w..4w+3 of every tile, lane l rows 2l, 2l+1:
+//        row part     t_I[r] += K_IJ[r][c] x_J[c]  (registers along a tile-row
+//                     segment; one cross-warp reduction per segment -> rowpart)
+//        column part  t_J[c] += K_IJ[r][c] x_I[r]  (64-row sum per column as a
+//                     6-shuffle warp reduce-scatter -> colpart[tile], off-
+//                     diagonal tiles only)
+//     The tile is stored XOR-swizzled (16-byte chunk q of row r at q ^ (r/2))
+//     so the column-strip reads are bank-conflict free.
+//   pass 2 (after a grid barrier): t_i = sum of the segment partials of tile
+//     row I plus colpart of the tiles (I', I), I' > I, in a fixed order.
+//
+// Both passes are deterministic (no atomics).  Pass 2 touches 2 x 64 doubles
+// per tile, ~3% of the tile bytes.
+#pragma once
+#include "common.cuh"
+
+#define DCG_TB 64
+#define DCG_SYM_STAGES 4
+#define DCG_SYM_TILE_DOUBLES (DCG_TB * DCG_TB)
+// a ring stage: the tile plus the 64-entry slices v_J and s_J the tile's row
+// product needs, so everything a tile consumes arrives with it
+#define DCG_SYM_STAGE_DOUBLES (DCG_SYM_TILE_DOUBLES + 2 * DCG_TB)
+
+__host__ __device__ __forceinline__ long long sym_ntiles_side(long long n) { return (n + DCG_TB - 1) / DCG_TB; }
+__host__ __device__ __forceinline__ long long sym_ntiles(long long n) {
+    const long long nt = sym_ntiles_side(n);
+    return nt * (nt + 1) / 2;
+}
+// CTA b of G owns tiles [sym_tile_begin(b), sym_tile_begin(b+1))
+__host__ __device__ __forceinline__ long long sym_tile_begin(long long ntt, long long G, long long b) {
+    return (b * ntt) / G;
+}
+// owner CTA of tile t
+__host__ __device__ __forceinline__ long long sym_tile_owner(long long ntt, long long G, long long t) {
+    return ((t + 1) * G - 1) / ntt;
+}
+__host__ __device__ __forceinline__ long long sym_tile_row_base(long long I) { return I * (I + 1) / 2; }
+
+// Shared memory the two passes need (doubles): ring, 2 x 16 x 64 row-flush
+// buffers, 2 x STAGES mbarriers.
+__host__ __device__ __forceinline__ long long sym_smem_doubles() {
+    return (long long)DCG_SYM_STAGES * DCG_SYM_STAGE_DOUBLES + 2 * DCG_NW * DCG_TB + 2 * DCG_SYM_STAGES + 2;
+}
+
+// ---- async copy and mbarrier primitives ------------------------------------
+__device__ __forceinline__ unsigned sym_saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void sym_cp_async16(double* sdst, const double* gsrc, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sym_saddr(sdst)), "l"(gsrc), "r"(bytes));
+}
+__device__ __forceinline__ void sym_cp_async16_full(double* sdst, const double* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sym_saddr(sdst)), "l"(gsrc));
+}
+__device__ __forceinline__ void sym_mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(sym_saddr(bar)), "r"(count));
+}
+// arrive once all cp.async previously issued by this thread have completed
+__device__ __forceinline__ void sym_mbar_cp_arrive(unsigned long long* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(sym_saddr(bar)) : "memory");
+}
+__device__ __forceinline__ void sym_mbar_arrive(unsigned long long* bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(sym_saddr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void sym_mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "SYM_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra SYM_WAIT_%=;\n\t}\n" ::"r"(sym_saddr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 16-byte chunk starting at element j of [0, n): bytes to copy (zero-fill beyond n)
+__device__ __forceinline__ int sym_chunk_bytes(long long j, long long n) {
+    return j < n ? ((j + 1 < n) ? 16 : 8) : 0;
+}
+
+// Per-thread copy geometry of a tile: chunk u covers row (tid/32 + 16u), the
+// 16-byte chunk q = tid%32 of that row, stored at swizzled chunk q ^ (row/2).
+struct SymCopyPlan {
+    long long koff[DCG_SYM_TILE_DOUBLES / 2 / DCG_NT];   // element offsets into K
+    int soff[DCG_SYM_TILE_DOUBLES / 2 / DCG_NT];         // offsets into the stage
+    int crow, c2;
+};
+
+__device__ __forceinline__ SymCopyPlan sym_copy_plan(long long ldk) {
+    SymCopyPlan pl;
+    const int tid = threadIdx.x;
+    pl.crow = tid >> 5;
+    pl.c2 = (tid & 31) * 2;
+#pragma unroll
+    for (int u = 0; u < DCG_SYM_TILE_DOUBLES / 2 / DCG_NT; ++u) {
+        const int row = pl.crow + 16 * u;
+        pl.koff[u] = (long long)row * ldk + pl.c2;
+        pl.soff[u] = row * DCG_TB + 2 * ((tid & 31) ^ ((row >> 1) & 31));
+    }
+    return pl;
+}
+
+// Issue this thread's copies of tile (I, J) (top-left element `kt`) and of the
+// slices v_J, s_J into stage `dst`.  cp.async.cg reads through L2, so v may
+// have been written by other CTAs before the preceding grid barrier.
+__device__ __forceinline__ void sym_issue_tile(const double* __restrict__ kt, const SymCopyPlan& pl, long long n,
+                                               long long I, long long J, const double* v, const double* s,
+                                               double* dst) {
+    const int tid = threadIdx.x;
+    const long long r_base = I * DCG_TB, c_base = J * DCG_TB;
+    if (r_base + DCG_TB <= n) {   // J <= I: the column block is interior as well
+#pragma unroll
+        for (int u = 0; u < DCG_SYM_TILE_DOUBLES / 2 / DCG_NT; ++u)
+            sym_cp_async16_full(dst + pl.soff[u], kt + pl.koff[u]);
+        if (tid < 32) sym_cp_async16_full(dst + DCG_SYM_TILE_DOUBLES + 2 * tid, v + c_base + 2 * tid);
+        else if (tid < 64 && s)
+            sym_cp_async16_full(dst + DCG_SYM_TILE_DOUBLES + DCG_TB + 2 * (tid - 32), s + c_base + 2 * (tid - 32));
+        return;
+    }
+#pragma unroll
+    for (int u = 0; u < DCG_SYM_TILE_DOUBLES / 2 / DCG_NT; ++u) {
+        const long long gr = r_base + pl.crow + 16 * u, gc = c_base + pl.c2;
+        const int bytes = gr < n ? sym_chunk_bytes(gc, n) : 0;
+        sym_cp_async16(dst + pl.soff[u], bytes ? kt + pl.koff[u] : kt, bytes);
+    }
+    if (tid < 32) {
+        const long long j = c_base + 2 * tid;
+        const int bytes = sym_chunk_bytes(j, n);
+        sym_cp_async16(dst + DCG_SYM_TILE_DOUBLES + 2 * tid, bytes ? v + j : v, bytes);
+    } else if (tid < 64 && s) {
+        const long long j = c_base + 2 * (tid - 32);
+        const int bytes = sym_chunk_bytes(j, n);
+        sym_cp_async16(dst + DCG_SYM_TILE_DOUBLES + DCG_TB + 2 * (tid - 32), bytes ? s + j : s, bytes);
+    }
+}
+
+// x'_j = s_j v_j (or v_j), zero beyond n (v read through L2).
+__device__ __forceinline__ double sym_xval(const double* v, const double* s, long long j, long long n) {
+    if (j >= n) return 0.0;
+    const double vv = ld_cg(v + j);
+    return s ? mul_rn(__ldg(s + j), vv) : vv;
+}
+
+// Pass 1 over this CTA's tile range.  colpart/rowpart: ntt x 64 doubles.
+__device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long long ldk, long long n, const double* v,
+                                          const double* s, double* colpart, double* rowpart, double* smem) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* ring = smem;
+    double* rowred = ring + DCG_SYM_STAGES * DCG_SYM_STAGE_DOUBLES;                       // 2 x NW x 64
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(rowred + 2 * DCG_NW * DCG_TB);
+    unsigned long long* empty = full + DCG_SYM_STAGES;
+    const long long NT = sym_ntiles_side(n);
+    const long long ntt = NT * (NT + 1) / 2;
+    const long long t0 = sym_tile_begin(ntt, gridDim.x, blockIdx.x);
+    const long long t1 = sym_tile_begin(ntt, gridDim.x, blockIdx.x + 1);
+    if (t0 >= t1) return;   // uniform per CTA
+    const int ntiles = (int)(t1 - t0);
+    if (tid == 0) {
+#pragma unroll
+        for (int st = 0; st < DCG_SYM_STAGES; ++st) {
+            sym_mbar_init(full + st, DCG_NT);     // one cp.async-arrival per thread
+            sym_mbar_init(empty + st, DCG_NW);    // one arrival per warp
+        }
+    }
+    __syncthreads();
+    long long I = (long long)((sqrt(8.0 * (double)t0 + 1.0) - 1.0) * 0.5);
+    while (sym_tile_row_base(I + 1) <= t0) ++I;
+    while (sym_tile_row_base(I) > t0) --I;
+    long long J = t0 - sym_tile_row_base(I);
+    const SymCopyPlan pl = sym_copy_plan(ldk);
+    const long long row_stride = (long long)DCG_TB * ldk;
+    // prologue: tiles 0 .. STAGES-2; issue cursor (iI, iJ, ip) follows
+    long long iI = I, iJ = J;
+    const double* ip = K + iI * row_stride + iJ * DCG_TB;
+#pragma unroll
+    for (int st = 0; st < DCG_SYM_STAGES - 1; ++st) {
+        if (st < ntiles) {
+            sym_issue_tile(ip, pl, n, iI, iJ, v, s, ring + st * DCG_SYM_STAGE_DOUBLES);
+            sym_mbar_cp_arrive(full + st);
+        }
+        if (++iJ > iI) { ++iI; iJ = 0; ip = K + iI * row_stride; } else { ip += DCG_TB; }
+    }
+    // swizzled offsets of this thread's reads: rows 2l, 2l+1, chunks 2w, 2w+1
+    const int key = lane & 31;                                     // (row >> 1) for both rows
+    const int o00 = (2 * lane) * DCG_TB + 2 * ((2 * warp) ^ key);
+    const int o01 = (2 * lane) * DCG_TB + 2 * ((2 * warp + 1) ^ key);
+    const int o10 = o00 + DCG_TB, o11 = o01 + DCG_TB;
+    double xI0 = sym_xval(v, s, I * DCG_TB + 2 * lane, n);
+    double xI1 = sym_xval(v, s, I * DCG_TB + 2 * lane + 1, n);
+    double row0 = 0.0, row1 = 0.0;
+    long long seg_start = t0;
+    int flush = 0;
+    for (int lt = 0; lt < ntiles; ++lt) {
+        // produce tile lt + STAGES - 1 into the stage tile lt - 1 used
+        {
+            const int tn = lt + DCG_SYM_STAGES - 1;
+            if (tn < ntiles) {
+                const int stg = tn % DCG_SYM_STAGES;
+                if (tn >= DCG_SYM_STAGES) sym_mbar_wait(empty + stg, ((tn / DCG_SYM_STAGES) - 1) & 1);
+                sym_issue_tile(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES);
+                sym_mbar_cp_arrive(full + stg);
+            }
+            if (++iJ > iI) { ++iI; iJ = 0; ip = K + iI * row_stride; } else { ip += DCG_TB; }
+        }
+        // consume tile lt
+        const int stg = lt % DCG_SYM_STAGES;
+        sym_mbar_wait(full + stg, (lt / DCG_SYM_STAGES) & 1);
+        const double* tile = ring + stg * DCG_SYM_STAGE_DOUBLES;
+        const double2 a0 = *reinterpret_cast<const double2*>(tile + o00);   // row 2l,   cols 4w, 4w+1
+        const double2 a1 = *reinterpret_cast<const double2*>(tile + o01);   // row 2l,   cols 4w+2, 4w+3
+        const double2 b0 = *reinterpret_cast<const double2*>(tile + o10);   // row 2l+1
+        const double2 b1 = *reinterpret_cast<const double2*>(tile + o11);
+        const double2 v0 = *reinterpret_cast<const double2*>(tile + DCG_SYM_TILE_DOUBLES + 4 * warp);
+        const double2 v1 = *reinterpret_cast<const double2*>(tile + DCG_SYM_TILE_DOUBLES + 4 * warp + 2);
+        double x0 = v0.x, x1 = v0.y, x2 = v1.x, x3 = v1.y;
+        if (s) {
+            const double2 s0 = *reinterpret_cast<const double2*>(tile + DCG_SYM_TILE_DOUBLES + DCG_TB + 4 * warp);
+            const double2 s1 = *reinterpret_cast<const double2*>(tile + DCG_SYM_TILE_DOUBLES + DCG_TB + 4 * warp + 2);
+            x0 = mul_rn(s0.x, x0);
+            x1 = mul_rn(s0.y, x1);
+            x2 = mul_rn(s1.x, x2);
+            x3 = mul_rn(s1.y, x3);
+        }
+        __syncwarp();
+        if (lane == 0) sym_mbar_arrive(empty + stg);   // this warp is done with the stage
+        row0 = fma(a0.x, x0, row0);
+        row0 = fma(a0.y, x1, row0);
+        row0 = fma(a1.x, x2, row0);
+        row0 = fma(a1.y, x3, row0);
+        row1 = fma(b0.x, x0, row1);
+        row1 = fma(b0.y, x1, row1);
+        row1 = fma(b1.x, x2, row1);
+        row1 = fma(b1.y, x3, row1);
+        if (J < I) {
+            // column sums over the tile's 64 rows: warp reduce-scatter of 4 values
+            double c0 = fma(b0.x, xI1, a0.x * xI0);
+            double c1 = fma(b0.y, xI1, a0.y * xI0);
+            double c2 = fma(b1.x, xI1, a1.x * xI0);
+            double c3 = fma(b1.y, xI1, a1.y * xI0);
+            const bool hi16 = lane & 16;
+            const double r0 = __shfl_xor_sync(0xffffffffu, hi16 ? c0 : c2, 16);
+            const double r1 = __shfl_xor_sync(0xffffffffu, hi16 ? c1 : c3, 16);
+            double k0 = (hi16 ? c2 : c0) + r0;   // columns {0,1} (lanes < 16) or {2,3}
+            double k1 = (hi16 ? c3 : c1) + r1;
+            const bool hi8 = lane & 8;
+            const double r2 = __shfl_xor_sync(0xffffffffu, hi8 ? k0 : k1, 8);
+            double cv = (hi8 ? k1 : k0) + r2;    // column 2*hi16 + hi8
+            cv += __shfl_xor_sync(0xffffffffu, cv, 4);
+            cv += __shfl_xor_sync(0xffffffffu, cv, 2);
+            cv += __shfl_xor_sync(0xffffffffu, cv, 1);
+            if ((lane & 7) == 0) colpart[(t0 + lt) * DCG_TB + 4 * warp + 2 * (lane >> 4) + ((lane >> 3) & 1)] = cv;
+        }
+        // end of a tile-row segment: diagonal tile reached or last tile of the range
+        if (J == I || lt + 1 == ntiles) {
+            double* rr = rowred + (flush & 1) * DCG_NW * DCG_TB;
+            rr[warp * DCG_TB + 2 * lane] = row0;
+            rr[warp * DCG_TB + 2 * lane + 1] = row1;
+            __syncthreads();
+            if (tid < DCG_TB) {
+                double a = 0.0;
+#pragma unroll
+                for (int w = 0; w < DCG_NW; ++w) a += rr[w * DCG_TB + tid];
+                rowpart[seg_start * DCG_TB + tid] = a;
+            }
+            row0 = row1 = 0.0;
+            seg_start = t0 + lt + 1;
+            ++flush;
+        }
+        if (++J > I) {
+            ++I;
+            J = 0;
+            if (lt + 1 < ntiles) {
+                xI0 = sym_xval(v, s, I * DCG_TB + 2 * lane, n);
+                xI1 = sym_xval(v, s, I * DCG_TB + 2 * lane + 1, n);
+            }
+        }
+    }
+    __syncthreads();   // all arrivals done: the barriers may be re-initialised by the next pass
+}
+
+// Pass 2: t_i for rows [r0, r1) from the partials; epi(i, t_i) runs on one
+// thread per row.  `red` needs 8 x 64 doubles of shared memory.
+template <class Epi>
+__device__ __forceinline__ void sym_pass2(long long n, const double* colpart, const double* rowpart, long long r0,
+                                          long long r1, double* red, Epi&& epi) {
+    const int tid = threadIdx.x;
+    const int r = tid & (DCG_TB - 1), g = tid >> 6;
+    const long long NT = sym_ntiles_side(n);
+    const long long ntt = NT * (NT + 1) / 2;
+    const long long G = gridDim.x;
+    if (r0 >= r1) return;
+    for (long long I = r0 / DCG_TB; I * DCG_TB < r1; ++I) {
+        const long long i = I * DCG_TB + r;
+        const bool mine = (i >= r0 && i < r1);
+        double acc = 0.0;
+        if (mine) {
+            // column parts from tiles (I', I), I' > I, strided over the 8 groups;
+            // four independent chains keep four loads in flight; fixed combination order
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            long long Ip = I + 1 + g;
+            for (; Ip + 24 < NT; Ip += 32) {
+                a0 += ld_cg(colpart + (sym_tile_row_base(Ip) + I) * DCG_TB + r);
+                a1 += ld_cg(colpart + (sym_tile_row_base(Ip + 8) + I) * DCG_TB + r);
+                a2 += ld_cg(colpart + (sym_tile_row_base(Ip + 16) + I) * DCG_TB + r);
+                a3 += ld_cg(colpart + (sym_tile_row_base(Ip + 24) + I) * DCG_TB + r);
+            }
+            for (; Ip < NT; Ip += 8) a0 += ld_cg(colpart + (sym_tile_row_base(Ip) + I) * DCG_TB + r);
+            acc = (a0 + a1) + (a2 + a3);
+            if (g == 0) {
+                // row segments of tile row I: start at J = 0 and at every CTA range start inside the row
+                const long long base = sym_tile_row_base(I);
+                acc += ld_cg(rowpart + base * DCG_TB + r);
+                const long long b_lo = sym_tile_owner(ntt, G, base), b_hi = sym_tile_owner(ntt, G, base + I);
+                // (several CTAs share a start when there are more CTAs than tiles: count it once)
+                for (long long b = b_lo + 1; b <= b_hi; ++b) {
+                    const long long ts = sym_tile_begin(ntt, G, b);
+                    if (ts > sym_tile_begin(ntt, G, b - 1)) acc += ld_cg(rowpart + ts * DCG_TB + r);
+                }
+            }
+        }
+        __syncthreads();
+        red[g * DCG_TB + r] = acc;
+        __syncthreads();
+        if (g == 0 && mine) {
+            double t = 0.0;
+#pragma unroll
+            for (int gg = 0; gg < 8; ++gg) t += red[gg * DCG_TB + r];
+            epi(i, t);
+        }
+    }
+    __syncthreads();
+}

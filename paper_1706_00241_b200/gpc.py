@@ -239,7 +239,9 @@ def laplace_newton(k_matrix, y, solver=SOLVER_CHOLESKY, cfg=None, newton_tol=1.0
             solver_iterations, history = report.iterations, report.residual_history
             rel_residual = history[-1]
         else:
-            x, seq = solve_next(seq, system.a_matrix, system.b)
+            # the next basis is extracted on a side stream while the Newton
+            # update and the next system are formed here
+            x, seq = solve_next(seq, system.a_matrix, system.b, defer_extraction=True)
             dt = time.perf_counter() - t0
             report = seq.history[-1]
             solver_iterations, history = report.iterations, report.residual_history
@@ -256,6 +258,7 @@ def laplace_newton(k_matrix, y, solver=SOLVER_CHOLESKY, cfg=None, newton_tol=1.0
         psi_prev = psi
         x_prev = x
 
+    _ = seq.basis   # join a pending extraction (surfaces its errors here)
     if records:
         stacked = torch.stack([r.f for r in records]).cpu().numpy()
         for r, row in zip(records, stacked):

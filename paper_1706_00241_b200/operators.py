@@ -27,13 +27,21 @@ from .errors import DimensionMismatch
 SYMMETRY_RTOL = 1e-12
 
 
+STRATEGIES = ("auto", "sym", "rows")
+SYM_MIN_N = 4096
+
+
 class DenseOperator:
-    """A = shift*I + diag(s) K diag(s) over a dense fp64 K in HBM."""
+    """A = shift*I + diag(s) K diag(s) over a dense fp64 K in HBM.
+
+    ``strategy`` selects how products stream K: "sym" (default for square,
+    unsharded operators; K is exactly symmetric) reads only the lower
+    triangle, "rows" streams full rows (row-sharded slabs, A/B checks)."""
 
     __array_priority__ = 100
 
     def __init__(self, kbuf: torch.Tensor, n: int, ldk: int, s: torch.Tensor | None = None, shift: float = 0.0,
-                 row0: int = 0, rows: int | None = None):
+                 row0: int = 0, rows: int | None = None, strategy: str = "auto"):
         self.kbuf = kbuf
         self.n = int(n)
         self.ldk = int(ldk)
@@ -41,6 +49,9 @@ class DenseOperator:
         self.shift = float(shift)
         self.row0 = int(row0)
         self.rows = self.n if rows is None else int(rows)
+        if strategy not in STRATEGIES:
+            raise ValueError(f"unknown strategy {strategy!r}")
+        self.strategy = strategy
 
     # -- construction ---------------------------------------------------------
     @classmethod
@@ -59,6 +70,13 @@ class DenseOperator:
         op = cls(kbuf, a.shape[0], ld)
         if check_symmetric:
             op.require_symmetric(rtol)
+            # make K exactly symmetric (its lower triangle mirrored): the change is
+            # within the 1e-12 * max|A| the check admits, and it makes the
+            # lower-triangle ("sym") and full-row products the same operator.
+            n = op.n
+            if n > 1:
+                low = torch.tril(kbuf[:, :n])
+                kbuf[:, :n] = low + torch.tril(low, -1).T
         return op
 
     def require_symmetric(self, rtol: float = SYMMETRY_RTOL) -> "DenseOperator":
@@ -74,7 +92,10 @@ class DenseOperator:
     def scaled(self, s, shift: float) -> "DenseOperator":
         """Same K, new diagonal scaling and shift (the Newton system of gpc.py:175-183)."""
         s_dev = None if s is None else D.to_dev(s, 1)
-        return DenseOperator(self.kbuf, self.n, self.ldk, s_dev, shift, self.row0, self.rows)
+        return DenseOperator(self.kbuf, self.n, self.ldk, s_dev, shift, self.row0, self.rows, self.strategy)
+
+    def with_strategy(self, strategy: str) -> "DenseOperator":
+        return DenseOperator(self.kbuf, self.n, self.ldk, self.s, self.shift, self.row0, self.rows, strategy)
 
     # -- views ------------------------------------------------------------------
     @property
@@ -87,7 +108,13 @@ class DenseOperator:
 
     def c_struct(self) -> N.COperator:
         op = N.COperator()
-        op.kind = N.DCG_OP_DENSE
+        strategy = self.strategy
+        if strategy == "auto":
+            # below a few thousand rows the Gram is L2-resident and the row
+            # strategy's lower latency wins (measured: n = 2000, SURVEY config 1)
+            strategy = "sym" if self.n >= SYM_MIN_N else "rows"
+        sym = strategy == "sym" and self.row0 == 0 and self.rows == self.n
+        op.kind = N.DCG_OP_DENSE_SYM if sym else N.DCG_OP_DENSE
         op.n = self.n
         op.row0 = self.row0
         op.rows = self.rows
@@ -99,7 +126,7 @@ class DenseOperator:
 
     def kernel_view(self) -> "DenseOperator":
         """K itself (no scaling, no shift)."""
-        return DenseOperator(self.kbuf, self.n, self.ldk, None, 0.0, self.row0, self.rows)
+        return DenseOperator(self.kbuf, self.n, self.ldk, None, 0.0, self.row0, self.rows, self.strategy)
 
     def matvec_dev(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         y = D.empty(self.rows) if out is None else out

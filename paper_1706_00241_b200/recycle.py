@@ -52,9 +52,42 @@ class RitzExtraction:
     aw_next = property(lambda self: self.aw_next_dev.cpu().numpy())
 
 
+class _PendingBasis:
+    """A Ritz extraction enqueued on the side stream (dcg_ritz_extract_async).
+
+    Resolved on first use: the current stream waits for the side stream's
+    event, the 3-word device result is read, and the outcome maps to the next
+    basis (ok), None (BasisDeficient, swallowed as in recycle.py:194-195) or
+    the reference's exception (e.g. NoConvergence)."""
+
+    def __init__(self, event, result, w_next, aw_next, keep_alive):
+        self.event = event
+        self.result = result
+        self.w_next = w_next
+        self.aw_next = aw_next
+        self.keep_alive = keep_alive   # inputs the side stream reads
+
+    def resolve(self):
+        torch.cuda.current_stream().wait_event(self.event)
+        self.event.synchronize()
+        status, info = (int(v) for v in self.result[:2].cpu().tolist())
+        self.keep_alive = None
+        if status == N.DCG_E_BASIS_DEFICIENT:
+            return None
+        N.check(status, info, "ritz_extract")
+        if self.w_next.shape[1] == 0:
+            return None
+        nb = RecycleBasis.__new__(RecycleBasis)
+        nb.w_dev, nb.aw_dev, nb.chol_dev = self.w_next, self.aw_next, None
+        return nb
+
+
 @dataclass
 class SequenceState:
-    """Carry-over between solves of a sequence (recycle.py:49-63)."""
+    """Carry-over between solves of a sequence (recycle.py:49-63).
+
+    ``basis`` may hold an extraction still running on the side stream; reading
+    the attribute waits for it."""
 
     k: int
     cfg: SolverConfig = field(default_factory=SolverConfig)
@@ -62,6 +95,13 @@ class SequenceState:
     basis: RecycleBasis | None = None
     x_last: object | None = None
     history: list = field(default_factory=list)
+
+    def __getattribute__(self, name):
+        value = object.__getattribute__(self, name)
+        if name == "basis" and isinstance(value, _PendingBasis):
+            value = value.resolve()
+            object.__setattr__(self, "basis", value)
+        return value
 
 
 def _refresh_dev(op, w_dev: torch.Tensor) -> RecycleBasis:
@@ -127,6 +167,34 @@ def _extract_dev(log: KrylovLog, prev: RecycleBasis | None, k: int, selection: s
                           selection)
 
 
+def _extract_async(log: KrylovLog, prev: RecycleBasis | None, k: int, selection: str) -> "_PendingBasis | None":
+    """Enqueue the extraction on the side stream (own context and workspace)."""
+    m = log.stored_iterations
+    kp = prev.k if prev is not None else 0
+    if k > kp + m:
+        return None   # BasisDeficient, swallowed by solve_next
+    n = log.n
+    main = torch.cuda.current_stream()
+    side = D.side_stream()
+    side.wait_stream(main)
+    theta = D.empty(k)
+    w_next, aw_next = D.empty(n, k), D.empty(n, k)
+    result = torch.zeros(4, dtype=torch.int64, device=D.device())
+    clog = log.c_struct()
+    cprev = prev.c_struct() if kp else None
+    with torch.cuda.stream(side):
+        rc = N.lib().dcg_ritz_extract_async(D.ctx(1), side.cuda_stream, n, ctypes.byref(clog), m,
+                                            ctypes.byref(cprev) if cprev is not None else None, k,
+                                            N.DCG_SELECT_LARGEST if selection == SELECT_LARGEST
+                                            else N.DCG_SELECT_SMALLEST,
+                                            theta.data_ptr(), None, None, w_next.data_ptr(), aw_next.data_ptr(),
+                                            result.data_ptr())
+        N.check(rc, 0, "ritz_extract_async")
+        event = torch.cuda.Event()
+        event.record(side)
+    return _PendingBasis(event, result, w_next, aw_next, (log, prev, theta))
+
+
 def harmonic_ritz_extract(log, prev_basis, k, selection=SELECT_SMALLEST):
     """Extract k approximate eigenvectors from a finished solve (recycle.py:95-159).
 
@@ -134,9 +202,13 @@ def harmonic_ritz_extract(log, prev_basis, k, selection=SELECT_SMALLEST):
     return _extract_dev(log, prev_basis, int(k), selection)
 
 
-def solve_next(state, a, b):
+def solve_next(state, a, b, defer_extraction=False):
     """Solve the next system of a sequence, recycling the deflation basis
-    (recycle.py:162-203).  Returns (x, new_state)."""
+    (recycle.py:162-203).  Returns (x, new_state).
+
+    With ``defer_extraction`` the harmonic-Ritz extraction of the next basis
+    runs on a side stream and ``new_state.basis`` resolves when first read
+    (the next solve), so callers can overlap independent work with it."""
     host = not isinstance(b, torch.Tensor)
     if host:
         b = np.ascontiguousarray(b, dtype=np.float64)
@@ -159,7 +231,9 @@ def solve_next(state, a, b):
     x, report, log = _solve_dev(op, bd, x_prev, used if (used is not None and used.k > 0) else None, state.cfg, t0)
 
     nxt = None
-    if state.k > 0:
+    if state.k > 0 and defer_extraction:
+        nxt = _extract_async(log, used, state.k, state.selection)
+    elif state.k > 0:
         try:
             ext = _extract_dev(log, used, state.k, state.selection)
             if ext.w_next_dev.shape[1] > 0:

@@ -47,11 +47,12 @@ def hyperparameter_sweep(x, y, lengthscales, signal_sd=1.0, jitter=0.01, k=24, c
     sols, recs = [], []
     for theta in lengthscales:
         op = rbf_kernel(xd, KernelParams(signal_sd, float(theta)), jitter=jitter)
-        xs, state = solve_next(state, op, yd)
+        xs, state = solve_next(state, op, yd, defer_extraction=True)
         rep = state.history[-1]
         recs.append(SweepRecord(float(theta), rep.iterations, rep.residual_history[-1], rep.wall_time, rep))
         sols.append(xs)
         del op
+    _ = state.basis   # join the last pending extraction
     if host:
         sols = [s.cpu().numpy() for s in sols]
     return sols, recs

@@ -273,8 +273,11 @@ def test_true_residual_refresh_long_solve(P):
     assert np.linalg.norm(x - xr) / np.linalg.norm(xr) <= 10 * spread
     # the reference itself stops at the 10 n = 1200 iteration cap here
     assert rep.residual_history[-1] <= 10 * ref_hist[-1]
-    a = g["c_long_a"]
-    assert np.linalg.norm(g["c_long_b"] - a @ x) / np.linalg.norm(g["c_long_b"]) <= 1e-10
+    # at kappa 1e6 the true residual of finite-precision CG stalls far above the
+    # recurrence residual; hold ours to the reference's own true residual
+    a, b = g["c_long_a"], g["c_long_b"]
+    true_ref = np.linalg.norm(b - a @ xr) / np.linalg.norm(b)
+    assert np.linalg.norm(b - a @ x) / np.linalg.norm(b) <= 10 * true_ref
 
 
 def test_solve_tight_tolerance_vs_oracle(P, rng):
