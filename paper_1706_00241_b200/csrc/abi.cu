@@ -250,7 +250,7 @@ __global__ void symcheck_kernel(const double* a, long long n, long long lda, uns
         const long long i2 = J * SYM_T + r, j2 = I * SYM_T + tx;
         t2[r][tx] = (i2 < n && j2 < n) ? a[i2 * lda + j2] : 0.0;
     }
-    __syncthreads();
+    cta_sync();
     double dmax = 0.0, amax = 0.0;
     for (int r = ty; r < SYM_T; r += 8) {
         const double v = t1[r][tx];
@@ -521,7 +521,7 @@ __global__ void project_kernel(long long n, int k, const double* L, const double
             y[i] = div_rn(acc, L[i * k + i]);
         }
     }
-    __syncthreads();
+    cta_sync();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         double acc = 0.0;

@@ -9,6 +9,7 @@
 #include "gemv.cuh"
 #include "symgemv.cuh"
 
+
 // =============================================================================
 // K1 standalone GEMV: one CTA per contiguous row range (grid = #SM).
 // =============================================================================
@@ -57,7 +58,9 @@ __global__ void __launch_bounds__(DCG_NT, 1)
     sym_pass1_kernel(const double* __restrict__ K, long long ldk, long long n, const double* v, const double* s_in,
                      double* colpart, double* rowpart) {
     extern __shared__ __align__(16) double smem[];
-    sym_pass1(K, ldk, n, v, s_in, colpart, rowpart, smem);
+    sym_ring_init(smem);
+    unsigned int seq = 0;
+    sym_pass1(K, ldk, n, v, s_in, colpart, rowpart, smem, seq);
 }
 
 __global__ void __launch_bounds__(DCG_NT, 1)
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(256)
         } else {
             cp_async_wait<0>();
         }
-        __syncthreads();
+        cta_sync();
         const double* a = sA + buf * GM_BM * GM_SA + (warp * 8 + g) * GM_SA;
         const double* bsm = sB + buf * GM_BK * SB;
 #pragma unroll
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(256)
                 dmma(acc[j][0], acc[j][1], av.y, b0[SB + j * 8]);
             }
         }
-        __syncthreads();
+        cta_sync();
     }
     // D fragment: row = g, cols 2t, 2t+1 of each n-tile
     const long long r = row0 + warp * 8 + g;
@@ -355,10 +358,10 @@ __global__ void __launch_bounds__(256)
     }
     for (long long rb = r0; rb < r1; rb += XTY_ROWS) {
         const int nr = (int)min((long long)XTY_ROWS, r1 - rb);
-        __syncthreads();
+        cta_sync();
         for (int e = tid; e < nr * p; e += 256) sx[e] = X[(rb + e / p) * ldx + e % p];
         for (int e = tid; e < nr * q; e += 256) sy[e] = Y[(rb + e / q) * ldy + e % q];
-        __syncthreads();
+        cta_sync();
         for (int r = 0; r < nr; ++r) {
 #pragma unroll
             for (int u = 0; u < XTY_PPT; ++u)

@@ -70,6 +70,16 @@ int dcg_host_reserve(dcg_context* ctx, size_t bytes);
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// ---- CTA barrier ---------------------------------------------------------------
+// __syncthreads() is the *aligned* bar.sync: it assumes every warp arrives
+// converged.  Independent thread scheduling does not guarantee reconvergence
+// after a lane-predicated loop (e.g. only lanes v < nslots load partials), and a
+// warp that reaches an aligned barrier while diverged can be counted as arrived
+// before its remaining lanes get there -- the CTA is released early (stale
+// shared memory) or a later barrier never completes.  The non-aligned form
+// counts threads individually, so it is correct for divergent arrival.
+__device__ __forceinline__ void cta_sync() { asm volatile("barrier.sync 0;" ::: "memory"); }
+
 // ---- arithmetic without FMA contraction --------------------------------------
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
@@ -101,14 +111,14 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // Block-wide sum; every thread receives the same value.  `red` holds >= 33
-// doubles of shared scratch.  Contains two __syncthreads.
+// doubles of shared scratch.  Contains two CTA barriers.
 __device__ __forceinline__ double block_sum(double v, double* red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nw = (blockDim.x + 31) >> 5;
     v = warp_sum(v);
-    __syncthreads();
+    cta_sync();
     if (lane == 0) red[warp] = v;
-    __syncthreads();
+    cta_sync();
     double t = (lane < nw) ? red[lane] : 0.0;
     t = warp_sum(t);
     return t;
@@ -124,9 +134,9 @@ __device__ __forceinline__ double block_max(double v, double* red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nw = (blockDim.x + 31) >> 5;
     v = warp_max(v);
-    __syncthreads();
+    cta_sync();
     if (lane == 0) red[warp] = v;
-    __syncthreads();
+    cta_sync();
     double t = (lane < nw) ? red[lane] : -INFINITY;
     return warp_max(t);
 }
@@ -152,6 +162,39 @@ struct Arena {
 static inline size_t al(size_t bytes) { return (bytes + 255) & ~size_t(255); }
 static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// Sense-reversal grid barrier for a launch whose CTAs are all co-resident
+// (cooperative launch).  bar[0] counts arrivals, bar[1] is the generation;
+// both are zero at launch.  The last CTA to arrive resets the count before
+// it advances the generation, so a CTA racing ahead into the next barrier
+// never sees a stale count.  Warp 0 waits warp-uniformly (lane 0 polls, the
+// value is broadcast), the other warps wait at the CTA barrier.
+__device__ __forceinline__ void dcg_grid_barrier(unsigned int* bar, unsigned int nblocks) {
+    cta_sync();
+    if (threadIdx.x < 32) {
+        volatile unsigned int* vgen = bar + 1;
+        unsigned int gen = 0;
+        if (threadIdx.x == 0) {
+            gen = *vgen;   // this CTA has not arrived yet: still the current generation
+            __threadfence();
+            const unsigned int arrived = atomicAdd(bar, 1u);
+            if (arrived == nblocks - 1) {
+                atomicExch(bar, 0u);
+                __threadfence();
+                atomicAdd(bar + 1, 1u);
+            }
+        }
+        gen = __shfl_sync(0xffffffffu, gen, 0);
+        for (;;) {
+            unsigned int cur = 0;
+            if (threadIdx.x == 0) cur = *vgen;
+            cur = __shfl_sync(0xffffffffu, cur, 0);
+            if (cur != gen) break;
+        }
+        __threadfence();
+    }
+    cta_sync();
+}
+
 // copy a device status block to the host (synchronises the stream)
 int dcg_read_status(dcg_context* ctx, cudaStream_t st, const DevStatus* dev, DevStatus* out);
 
@@ -161,13 +204,13 @@ int dcg_read_status(dcg_context* ctx, cudaStream_t st, const DevStatus* dev, Dev
 __device__ __forceinline__ bool cta_last_arrival(unsigned int* counter, unsigned int total) {
     __shared__ int s_last;
     __threadfence();
-    __syncthreads();
+    cta_sync();
     if (threadIdx.x == 0) {
         const unsigned int prev = atomicAdd(counter, 1u);
         s_last = (prev == total - 1) ? 1 : 0;
         if (s_last) *counter = 0u;
     }
-    __syncthreads();
+    cta_sync();
     if (s_last) __threadfence();
     return s_last != 0;
 }

@@ -28,7 +28,7 @@ __device__ int cta_cholesky(const double* A, int lda, int n, double pivot_tol, d
         const int i = e / n, j = e % n;
         if (j > i) L[i * ldl + j] = 0.0;
     }
-    __syncthreads();
+    cta_sync();
     for (int j = 0; j < n; ++j) {
         if (threadIdx.x == 0) {
             double acc = A[j * lda + j];
@@ -42,9 +42,9 @@ __device__ int cta_cholesky(const double* A, int lda, int n, double pivot_tol, d
                 L[j * ldl + j] = ljj;
             }
         }
-        __syncthreads();
+        cta_sync();
         if (s_scal[0] != 0.0) {
-            __syncthreads();
+            cta_sync();
             return j;
         }
         const double ljj = s_scal[1];
@@ -53,7 +53,7 @@ __device__ int cta_cholesky(const double* A, int lda, int n, double pivot_tol, d
             for (int t = 0; t < j; ++t) acc = sub_rn(acc, mul_rn(L[i * ldl + t], L[j * ldl + t]));
             L[i * ldl + j] = div_rn(acc, ljj);
         }
-        __syncthreads();
+        cta_sync();
     }
     return -1;
 }
@@ -191,7 +191,7 @@ __device__ int cta_jacobi(double* A, double* V, int T, int max_sweeps, double rt
                 s_mode[npairs + 2 * tid] = p;
                 s_mode[npairs + 2 * tid + 1] = q;
             }
-            __syncthreads();
+            cta_sync();
             // A <- R A R' applied on 2x2 blocks of (pair a rows) x (pair b cols)
             for (int e = tid; e < npairs * npairs; e += blockDim.x) {
                 const int pa = e / npairs, pb = e % npairs;
@@ -235,7 +235,7 @@ __device__ int cta_jacobi(double* A, double* V, int T, int max_sweeps, double rt
                 V[i * T + c0] = sub_rn(mul_rn(cbv, vp), mul_rn(sbv, vq));
                 V[i * T + c1] = add_rn(mul_rn(sbv, vp), mul_rn(cbv, vq));
             }
-            __syncthreads();
+            cta_sync();
         }
         converged = offdiag() <= rtol * frob;
     }
@@ -253,7 +253,7 @@ __device__ void cta_stable_argsort(const double* vals, int stride, int n, int* o
         }
         order[rank] = i;
     }
-    __syncthreads();
+    cta_sync();
 }
 
 // ===========================================================================
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(SD_NT) gram_factor_kernel(const double* Graw, 
     }
     if (threadIdx.x < k) s_act[threadIdx.x] = threadIdx.x;
     if (threadIdx.x == 0) s_na = k;
-    __syncthreads();
+    cta_sync();
     // compact sub-matrix lives in L's own storage region "sub" right after L (kk*kk)
     double* sub = L + k * k;
     while (true) {
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(SD_NT) gram_factor_kernel(const double* Graw, 
             const int i = e / na, j = e % na;
             sub[e] = Gsym[s_act[i] * k + s_act[j]];
         }
-        __syncthreads();
+        cta_sync();
         const double tol = cta_pivot_tol(sub, na, nullptr, na, red);
         const int fail = cta_cholesky(sub, na, na, tol, L, na, s_scal);
         if (fail < 0) {
@@ -300,12 +300,12 @@ __global__ void __launch_bounds__(SD_NT) gram_factor_kernel(const double* Graw, 
             if (threadIdx.x == 0) { st->status = DCG_E_GRAM_NOT_SPD; st->info = fail; st->count = na; }
             return;
         }
-        __syncthreads();
+        cta_sync();
         if (threadIdx.x == 0) {
             for (int i = fail; i < na - 1; ++i) s_act[i] = s_act[i + 1];
             s_na = na - 1;
         }
-        __syncthreads();
+        cta_sync();
     }
 }
 
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(SD_NT) ritz_pencil_kernel(const double* Fraw, 
     }
     if (tid < T) s_act[tid] = tid;
     if (tid == 0) s_na = T;
-    __syncthreads();
+    cta_sync();
     int na;
     while (true) {
         na = s_na;
@@ -360,16 +360,16 @@ __global__ void __launch_bounds__(SD_NT) ritz_pencil_kernel(const double* Fraw, 
             const int i = e / na, j = e % na;
             Fa[e] = F[s_act[i] * T + s_act[j]];
         }
-        __syncthreads();
+        cta_sync();
         const double tol = cta_pivot_tol(Fa, na, nullptr, na, red);
         const int fail = cta_cholesky(Fa, na, na, tol, L, na, s_scal);
         if (fail < 0) break;
-        __syncthreads();
+        cta_sync();
         if (tid == 0) {
             for (int i = fail; i < na - 1; ++i) s_act[i] = s_act[i + 1];
             s_na = na - 1;
         }
-        __syncthreads();
+        cta_sync();
     }
     // Ga -> Fa storage (F no longer needed in compact form)
     double* Ga = Fa;
@@ -377,15 +377,15 @@ __global__ void __launch_bounds__(SD_NT) ritz_pencil_kernel(const double* Fraw, 
         const int i = e / na, j = e % na;
         Ga[e] = G[s_act[i] * T + s_act[j]];
     }
-    __syncthreads();
+    cta_sync();
     // Y = L^-1 Ga  (solve_lower_matrix: column by column)
     for (int c = warp; c < na; c += nw) warp_solve_lower(L, na, na, Ga + c, na, Y + c, na);
-    __syncthreads();
+    cta_sync();
     // C = L^-1 Y'  -> into shared A
     double* A = sm;
     double* V = sm + na * na;
     for (int c = warp; c < na; c += nw) warp_solve_lower(L, na, na, Y + c * na, 1, A + c, na);
-    __syncthreads();
+    cta_sync();
     // symmetrise
     for (int e = tid; e < na * na; e += blockDim.x) {
         const int i = e / na, j = e % na;
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(SD_NT) ritz_pencil_kernel(const double* Fraw, 
             A[j * na + i] = v;
         }
     }
-    __syncthreads();
+    cta_sync();
     const int nc = cta_jacobi(A, V, na, max_sweeps, 1e-14, red, s_c, s_s, s_mode);
     if (nc) {
         if (tid == 0) { st->status = DCG_E_NO_CONVERGENCE; st->info = nc; st->count = na; }
@@ -432,13 +432,13 @@ __global__ void __launch_bounds__(SD_NT) sym_eigen_kernel(const double* Ain, int
     double* A = sm;
     double* V = sm + n * n;
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) A[e] = Ain[e];
-    __syncthreads();
+    cta_sync();
     const int nc = cta_jacobi(A, V, n, max_sweeps, rtol, red, s_c, s_s, s_mode);
     if (nc) {
         if (threadIdx.x == 0) { st->status = DCG_E_NO_CONVERGENCE; st->info = nc; }
         return;
     }
-    __syncthreads();
+    cta_sync();
     cta_stable_argsort(A, n + 1, n, s_order);
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
         const int i = e / n, r = e % n;
@@ -467,11 +467,11 @@ __global__ void __launch_bounds__(SD_NT) gen_sym_eigen_kernel(const double* g, c
         return;
     }
     for (int c = warp; c < n; c += nw) warp_solve_lower(L, n, n, g + c, n, Y + c, n);
-    __syncthreads();
+    cta_sync();
     double* A = sm;
     double* V = sm + n * n;
     for (int c = warp; c < n; c += nw) warp_solve_lower(L, n, n, Y + c * n, 1, A + c, n);
-    __syncthreads();
+    cta_sync();
     for (int e = tid; e < n * n; e += blockDim.x) {
         const int i = e / n, j = e % n;
         if (i < j) {
@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(SD_NT) gen_sym_eigen_kernel(const double* g, c
             A[j * n + i] = v;
         }
     }
-    __syncthreads();
+    cta_sync();
     const int nc = cta_jacobi(A, V, n, max_sweeps, 1e-14, red, s_c, s_s, s_mode);
     if (nc) {
         if (tid == 0) { st->status = DCG_E_NO_CONVERGENCE; st->info = nc; }
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(SD_NT) k_jacobi_sweep_kernel(double* a, double
                     s_mode = 1;
                 }
             }
-            __syncthreads();
+            cta_sync();
             if (s_mode) {
                 const double c = s_cs[0], s = s_cs[1];
                 for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -567,13 +567,13 @@ __global__ void __launch_bounds__(SD_NT) k_jacobi_sweep_kernel(double* a, double
                     a[i * n + p] = sub_rn(mul_rn(c, aip), mul_rn(s, aiq));
                     a[i * n + q] = add_rn(mul_rn(s, aip), mul_rn(c, aiq));
                 }
-                __syncthreads();
+                cta_sync();
                 for (int i = threadIdx.x; i < n; i += blockDim.x) {
                     const double aip = a[p * n + i], aiq = a[q * n + i];
                     a[p * n + i] = sub_rn(mul_rn(c, aip), mul_rn(s, aiq));
                     a[q * n + i] = add_rn(mul_rn(s, aip), mul_rn(c, aiq));
                 }
-                __syncthreads();
+                cta_sync();
                 if (threadIdx.x == 0) {
                     a[p * n + q] = 0.0;
                     a[q * n + p] = 0.0;
@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(SD_NT) k_jacobi_sweep_kernel(double* a, double
                 }
                 ++rotations;
             }
-            __syncthreads();
+            cta_sync();
         }
     }
     if (threadIdx.x == 0) st->count = rotations;

@@ -52,14 +52,14 @@ __global__ void __launch_bounds__(EX_NT)
                 azt[r * T + kp + j] = div_rn(sub_rn(R[(long long)j * n + i], R[(long long)(j + 1) * n + i]), alpha[j]);
             }
         }
-        __syncthreads();
+        cta_sync();
         for (int e = tid; e < nr * T; e += EX_NT) {
             Zraw[i0 * T + e] = zt[e];
             AZraw[i0 * T + e] = azt[e];
         }
         if (tid < T)
             for (int r = 0; r < nr; ++r) acc = fma(zt[r * T + tid], zt[r * T + tid], acc);
-        __syncthreads();
+        cta_sync();
     }
     if (tid < T) part[(long long)blockIdx.x * T + tid] = acc;
     if (!cta_last_arrival(counter, gridDim.x)) return;
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(EX_NT)
         s = warp_sum(s);
         if (lane == 0) norms[c] = sqrt(s);
     }
-    __syncthreads();
+    cta_sync();
     if (tid == 0) {
         int t = 0;
         for (int c = 0; c < T; ++c)
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(EX_NT)
     }
     for (long long i0 = r0; i0 < r1; i0 += EX_ROWS) {
         const int nr = (int)min((long long)EX_ROWS, r1 - i0);
-        __syncthreads();
+        cta_sync();
         for (int e = tid; e < nr * Tk; e += EX_NT) {
             const int r = e / Tk, cc = e % Tk;
             const int c = keep[cc];
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(EX_NT)
                 AZs[(i0 + r) * Tk + cc] = av;
             }
         }
-        __syncthreads();
+        cta_sync();
         for (int r = 0; r < nr; ++r) {
 #pragma unroll
             for (int u = 0; u < FG_PPT; ++u)
@@ -170,9 +170,9 @@ __global__ void __launch_bounds__(EX_NT)
     double* wp = sm + Tk * k;              // 8 warps x 64
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int e = tid; e < Tk * k; e += EX_NT) ue[e] = 0.0;
-    __syncthreads();
+    cta_sync();
     for (int e = tid; e < na * k; e += EX_NT) ue[active[e / k] * k + e % k] = U[e];
-    __syncthreads();
+    cta_sync();
     const long long r0 = part_begin(n, gridDim.x, blockIdx.x), r1 = part_begin(n, gridDim.x, blockIdx.x + 1);
     double s0 = 0.0, s1 = 0.0;   // lanes own columns lane, lane + 32
     for (long long i = r0 + warp; i < r1; i += EX_NT / 32) {
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(EX_NT)
     }
     wp[warp * 64 + lane] = s0;
     wp[warp * 64 + lane + 32] = s1;
-    __syncthreads();
+    cta_sync();
     if (tid < k) {
         double s = 0.0;
         for (int w = 0; w < EX_NT / 32; ++w) s += wp[w * 64 + tid];
@@ -201,15 +201,15 @@ __global__ void __launch_bounds__(EX_NT)
         s = warp_sum(s);
         if (lane == 0) scale[j] = sqrt(s);
     }
-    __syncthreads();
+    cta_sync();
     // u[:, j] /= ||Z u_j|| when positive (recycle.py:150-153)
     for (int e = tid; e < na * k; e += EX_NT) {
         const double sc = scale[e % k];
         if (sc > 0.0) U[e] = div_rn(U[e], sc);
     }
-    __syncthreads();
+    cta_sync();
     for (int e = tid; e < Tk * k; e += EX_NT) Uexp[e] = 0.0;
-    __syncthreads();
+    cta_sync();
     for (int e = tid; e < na * k; e += EX_NT) Uexp[active[e / k] * k + e % k] = U[e];
 }
 
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(EX_NT)
     const int Tk = (int)plan->count, na = (int)pencil->count;
     double* ue = sm;   // Tk x k
     for (int e = threadIdx.x; e < Tk * k; e += EX_NT) ue[e] = Uexp[e];
-    __syncthreads();
+    cta_sync();
     const long long total = n * k;
     for (long long e = blockIdx.x * (long long)EX_NT + threadIdx.x; e < total; e += (long long)gridDim.x * EX_NT) {
         const long long i = e / k;

@@ -26,7 +26,7 @@ __device__ __forceinline__ void stage_x_tile(double* s_x, const double* v, const
 // Rows [r0, r1) of the slab K (row-major, leading dimension ldk, n columns).
 // `s_red` needs DCG_NW * DCG_RB doubles, `s_x` min(n, DCG_QT) + 1 doubles.
 // Epilogue `epi(row, t)` runs on thread (row - batch start) after a barrier.
-// All threads of the CTA must call this (it contains __syncthreads).
+// All threads of the CTA must call this (it contains CTA barriers).
 template <bool kCrossCta, class Epi>
 __device__ __forceinline__ void block_gemv(const double* __restrict__ K, long long ldk, long long n,
                                            const double* v, const double* s, long long r0,
@@ -35,18 +35,18 @@ __device__ __forceinline__ void block_gemv(const double* __restrict__ K, long lo
     const int NT = blockDim.x;
     const bool single_tile = n <= DCG_QT;
     if (single_tile) {
-        __syncthreads();
+        cta_sync();
         stage_x_tile<kCrossCta>(s_x, v, s, 0, (int)n);
-        __syncthreads();
+        cta_sync();
     }
     for (long long rb0 = r0; rb0 < r1; rb0 += DCG_RB) {
         const int nb = (int)min((long long)DCG_RB, r1 - rb0);
         for (long long c0 = 0; c0 < n; c0 += DCG_QT) {
             const int cn = (int)min((long long)DCG_QT, n - c0);
             if (!single_tile) {
-                __syncthreads();
+                cta_sync();
                 stage_x_tile<kCrossCta>(s_x, v, s, c0, cn);
-                __syncthreads();
+                cta_sync();
             }
             const int cn2 = cn & ~1;
             for (int g = 0; g < nb; g += DCG_RG) {
@@ -83,13 +83,13 @@ __device__ __forceinline__ void block_gemv(const double* __restrict__ K, long lo
                 }
             }
         }
-        __syncthreads();
+        cta_sync();
         if (tid < nb) {
             double t = 0.0;
 #pragma unroll 4
             for (int w = 0; w < DCG_NW; ++w) t += s_red[w * DCG_RB + tid];
             epi(rb0 + tid, t);
         }
-        __syncthreads();
+        cta_sync();
     }
 }

@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(256)
             sr[r][t] = (t < tn && i0 + r < rows) ? xr[gi * dim + t0 + t] : 0.0;
             sc[r][t] = (t < tn && gj < nc) ? xc[gj * dim + t0 + t] : 0.0;
         }
-        __syncthreads();
+        cta_sync();
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
             const int r = ty + 8 * rr;
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(256)
                 acc[rr] = add_rn(acc[rr], mul_rn(diff, diff));
             }
         }
-        __syncthreads();
+        cta_sync();
     }
     const long long j = j0 + tx;
     if (j >= nc) return;

@@ -20,6 +20,7 @@
 
 namespace cg = cooperative_groups;
 
+
 namespace {
 
 struct SolveArgs {
@@ -50,26 +51,30 @@ struct SolveArgs {
     double* r;
     double* p;
     double* ap;
-    double* partials;
+    double* partials;  // two buffers of G x ps: reductions 0 (r'r, W'r, AW'r) and 1 (p'Ap)
     double* colpart;   // symmetric strategy: per-tile partials
     double* rowpart;
     int ps;   // partial stride (doubles)
     DevStatus* st;
+    unsigned int* bar;  // grid barrier words (zeroed per launch)
 };
 
-// x = L^-T L^-1 c for a k x k row-major lower factor in shared memory, by one
-// warp (lanes own rows lane and lane+32).  Substitution follows the reference
-// order for the forward sweep (_core.pyx:69-80); the backward sweep runs as a
-// wavefront.  `rdiag` holds 1/L[j][j].
-__device__ void warp_chol_solve(const double* L, const double* rdiag, int k, const double* c,
-                                double* out) {
+// mu = L^-T L^-1 c for the k x k row-major lower factor of W'AW in shared
+// memory, by one warp (lanes own rows lane and lane + 32).  This is the
+// reference's chol_solve (solvers.py:152,190 -> _core.pyx:69-94): forward
+// substitution in the reference's subtraction order, each unknown divided by
+// its pivot; the backward sweep runs as a wavefront (subtractions as soon as
+// x_j is known).  Triangular solves, not an explicit inverse: W'AW can be
+// ill-conditioned (random or nearly dependent W) and an explicit inverse
+// loses the backward stability the projection relies on.
+__device__ void warp_chol_solve(const double* L, int k, const double* c, double* out) {
     const int lane = threadIdx.x & 31;
     const int i0 = lane, i1 = lane + 32;
     double a0 = (i0 < k) ? c[i0] : 0.0;
     double a1 = (i1 < k) ? c[i1] : 0.0;
     for (int j = 0; j < k; ++j) {
         const double accj = __shfl_sync(0xffffffffu, (j < 32) ? a0 : a1, j & 31);
-        const double yj = mul_rn(accj, rdiag[j]);
+        const double yj = div_rn(accj, L[j * k + j]);
         if (lane == (j & 31)) {
             if (j < 32) a0 = yj; else a1 = yj;
         }
@@ -78,7 +83,7 @@ __device__ void warp_chol_solve(const double* L, const double* rdiag, int k, con
     }
     for (int j = k - 1; j >= 0; --j) {
         const double accj = __shfl_sync(0xffffffffu, (j < 32) ? a0 : a1, j & 31);
-        const double xj = mul_rn(accj, rdiag[j]);
+        const double xj = div_rn(accj, L[j * k + j]);
         if (lane == (j & 31)) {
             if (j < 32) a0 = xj; else a1 = xj;
         }
@@ -89,24 +94,62 @@ __device__ void warp_chol_solve(const double* L, const double* rdiag, int k, con
     if (i1 < k) out[i1] = a1;
 }
 
+// mu for the deflated update: warp 0 solves, then one CTA barrier.
+__device__ __forceinline__ void solve_mu(const double* L, int k, const double* c, double* mu) {
+    if ((threadIdx.x >> 5) == 0) warp_chol_solve(L, k, c, mu);
+    cta_sync();
+}
+
 // Fixed-order reduction of the per-CTA partials into shared memory (every CTA
-// computes the identical values).
-__device__ __forceinline__ void reduce_partials(const double* partials, int G, int ps, int nslots,
-                                                double* out) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int v = warp; v < nslots; v += DCG_NW) {
-        double acc = 0.0;
-        for (int g = lane; g < G; g += 32) acc += ld_cg(partials + (long long)g * ps + v);
-        acc = warp_sum(acc);
-        if (lane == 0) out[v] = acc;
+// computes the identical values).  All 512 threads load in parallel: slot
+// v = t % SW, CTA group t / SW, SW = next power of two >= nslots, so each
+// thread issues at most ceil(G / (512 / SW)) independent loads; groups are then
+// combined in a fixed order.  `scr` holds 512 doubles.
+__device__ __forceinline__ void reduce_partials(const double* partials, int G, int ps, int nslots, double* out,
+                                                double* scr) {
+    const int tid = threadIdx.x;
+    int sw = 1;
+    while (sw < nslots) sw <<= 1;
+    const int ng = DCG_NT / sw;
+    const int v = tid & (sw - 1), gq = tid / sw;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    if (v < nslots) {
+        int g = gq;
+        for (; g + 3 * ng < G; g += 4 * ng) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] += ld_cg(partials + (long long)(g + u * ng) * ps + v);
+        }
+        for (; g < G; g += ng) acc[0] += ld_cg(partials + (long long)g * ps + v);
     }
-    __syncthreads();
+    double a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    if (sw <= 32) {
+        // groups inside a warp share a slot at lanes v, v + sw, ...: butterfly over them
+        for (int o = sw; o < 32; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        const int lane = tid & 31, warp = tid >> 5;
+        if (lane < sw) scr[warp * 32 + lane] = a;
+        cta_sync();
+        if (tid < nslots) {
+            double t = 0.0;
+#pragma unroll 4
+            for (int w = 0; w < DCG_NW; ++w) t += scr[w * 32 + tid];
+            out[tid] = t;
+        }
+    } else {
+        scr[tid] = a;
+        cta_sync();
+        if (tid < nslots) {
+            double t = 0.0;
+            for (int g = 0; g < ng; ++g) t += scr[g * sw + tid];
+            out[tid] = t;
+        }
+    }
+    cta_sync();
 }
 
 // Sum per-warp partial rows s_wp[w][0..nslots) over warps and publish.
 __device__ __forceinline__ void publish_partials(const double* s_wp, int nslots, double* partials,
                                                  int ps) {
-    __syncthreads();
+    cta_sync();
     for (int v = threadIdx.x; v < nslots; v += blockDim.x) {
         double acc = 0.0;
         for (int w = 0; w < DCG_NW; ++w) acc += s_wp[w * (DCG_MAX_K + 1) + v];
@@ -128,7 +171,7 @@ __host__ __device__ __forceinline__ long long gemv_region_doubles(bool sym, long
 
 template <bool SYM>
 __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
-    cg::grid_group grid = cg::this_grid();
+#define GSYNC() dcg_grid_barrier(a.bar, gridDim.x)
     extern __shared__ __align__(16) double smem[];
     const long long n = a.n;
     const int k = a.k;
@@ -137,11 +180,11 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     const int xt = (int)min(n, (long long)DCG_QT) + 2;
     double* s_g = smem;                                  // GEMV region (strategy dependent)
     double* s_L = s_g + gemv_region_doubles(SYM, n);     // k*k
-    double* s_rd = s_L + k * k;                          // k   (1/L_jj)
-    double* s_c = s_rd + DCG_MAX_K;                      // 1 + DCG_MAX_K reduced slots
+    double* s_c = s_L + k * k;                           // 1 + DCG_MAX_K reduced slots
     double* s_mu = s_c + DCG_MAX_K + 2;                  // DCG_MAX_K
     double* s_wp = s_mu + DCG_MAX_K;                     // DCG_NW * (DCG_MAX_K + 1)
     double* s_tmp = s_wp + DCG_NW * (DCG_MAX_K + 1);     // 64 scratch
+    double* s_scr = s_tmp + 64;                          // DCG_NT reduction scratch
 
     const long long r0 = part_begin(n, G, blockIdx.x);
     const long long r1 = part_begin(n, G, blockIdx.x + 1);
@@ -151,12 +194,14 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     const double* s = a.s;
     const double shift = a.shift;
 
+    unsigned int ring_seq = 0;
+    if constexpr (SYM) sym_ring_init(s_g);
     // t = K (s (.) v) for the own rows [r0, r1); epi(i, t_i) per row.  The
     // symmetric strategy contains one extra grid barrier between its passes.
     auto gemv = [&](const double* v, auto&& epi) {
         if constexpr (SYM) {
-            sym_pass1(K, a.ldk, n, v, s, a.colpart, a.rowpart, s_g);
-            grid.sync();
+            sym_pass1(K, a.ldk, n, v, s, a.colpart, a.rowpart, s_g, ring_seq);
+            GSYNC();
             sym_pass2(n, a.colpart, a.rowpart, r0, r1, s_g, epi);
         } else {
             block_gemv<true>(K, a.ldk, n, v, s, r0, r1, s_g, s_g + xt, epi);
@@ -164,9 +209,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     };
 
     for (int i = tid; i < k * k; i += blockDim.x) s_L[i] = a.L[i];
-    __syncthreads();
-    for (int j = tid; j < k; j += blockDim.x) s_rd[j] = 1.0 / s_L[j * k + j];
-    __syncthreads();
+    cta_sync();
 
     // Accumulate over own rows (warp-per-row): sq += u_i^2 and c_j += M[i][j] * u_i,
     // u_i produced by `rowfn(i)` executed on all lanes (value must be uniform).
@@ -202,7 +245,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
                                 : add_rn(mul_rn(shift, a.x0[i]), t);
             a.r[i] = sub_rn(a.b[i], ax);
         });
-        __syncthreads();
+        cta_sync();
         // slot0 = b'b, slots 1.. = W' r_prev
         {
             double sq = 0.0, c0 = 0.0, c1 = 0.0;
@@ -224,8 +267,8 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         sq = block_sum(sq, s_tmp);
         if (tid == 0) a.partials[(long long)blockIdx.x * a.ps] = sq;
     }
-    grid.sync();
-    reduce_partials(a.partials, G, a.ps, (a.warm && deflate) ? nslots : 1, s_c);
+    GSYNC();
+    reduce_partials(a.partials, G, a.ps, (a.warm && deflate) ? nslots : 1, s_c, s_scr);
     const double norm_b = sqrt(s_c[0]);
     if (norm_b == 0.0) {
         // solvers.py:142-147: x = 0 (not x0), history [0.0], log.r = [0]
@@ -245,8 +288,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         return;
     }
     if (a.warm && deflate) {
-        if (warp == 0) warp_chol_solve(s_L, s_rd, k, s_c + 1, s_mu);
-        __syncthreads();
+        solve_mu(s_L, k, s_c + 1, s_mu);
         for (long long i = r0 + warp; i < r1; i += DCG_NW) {
             const double wy = row_dot(a.W, i, s_mu);
             if (lane == 0) a.x[i] = add_rn(a.x0[i], wy);
@@ -254,7 +296,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     } else {
         for (long long i = r0 + tid; i < r1; i += blockDim.x) a.x[i] = a.x0[i];
     }
-    grid.sync();
+    GSYNC();
 
     // ---------------- r0 = b - A x0 ; mu ; p0 ------------------------------------
     gemv(a.x, [&](long long i, double t) {
@@ -262,15 +304,14 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         const double ax = s ? add_rn(mul_rn(shift, xi), mul_rn(s[i], t)) : add_rn(mul_rn(shift, xi), t);
         a.r[i] = sub_rn(a.b[i], ax);
     });
-    __syncthreads();
+    cta_sync();
     warp_rows_partials([&](long long i) { return a.r[i]; }, deflate ? a.AW : nullptr, true);
     publish_partials(s_wp, nslots, a.partials, a.ps);
-    grid.sync();
-    reduce_partials(a.partials, G, a.ps, nslots, s_c);
+    GSYNC();
+    reduce_partials(a.partials, G, a.ps, nslots, s_c, s_scr);
     double rr = s_c[0];
     if (deflate) {
-        if (warp == 0) warp_chol_solve(s_L, s_rd, k, s_c + 1, s_mu);
-        __syncthreads();
+        solve_mu(s_L, k, s_c + 1, s_mu);
     }
     double rel = sqrt(rr) / norm_b;
     long long it = 0;
@@ -296,7 +337,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         if (tid == 0) a.history[0] = rel;
         if (deflate && cont && it < ell && tid < k) a.logMu[tid] = s_mu[tid];
     }
-    grid.sync();
+    GSYNC();
 
     // ---------------- main loop ------------------------------------------------
     while (cont) {
@@ -308,10 +349,13 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
             a.ap[i] = api;
             dpart = fma(pi, api, dpart);
         });
+        // p'Ap goes to the second partials buffer: no grid barrier separates this
+        // read from the r'r publish below, so they must not share slots.
+        double* const dparts = a.partials + (long long)G * a.ps;
         dpart = block_sum(dpart, s_tmp);
-        if (tid == 0) a.partials[(long long)blockIdx.x * a.ps] = dpart;
-        grid.sync();
-        reduce_partials(a.partials, G, a.ps, 1, s_c);
+        if (tid == 0) dparts[(long long)blockIdx.x * a.ps] = dpart;
+        GSYNC();
+        reduce_partials(dparts, G, a.ps, 1, s_c, s_scr);
         const double d = s_c[0];
         if (d <= 0.0) {   // solvers.py:170-172 (NaN falls through, as in numpy)
             if (blockIdx.x == 0 && tid == 0) {
@@ -327,7 +371,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         ++it;
         const bool recompute = (a.recompute > 0) && (it % a.recompute == 0);
         if (recompute) {
-            grid.sync();
+            GSYNC();
             gemv(a.x, [&](long long i, double t) {
                 const double xi = a.x[i];
                 const double ax = s ? add_rn(mul_rn(shift, xi), mul_rn(s[i], t)) : add_rn(mul_rn(shift, xi), t);
@@ -337,7 +381,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
             for (long long i = r0 + tid; i < r1; i += blockDim.x)
                 a.r[i] = sub_rn(a.r[i], mul_rn(alpha, a.ap[i]));
         }
-        __syncthreads();
+        cta_sync();
         const bool log_r = (it - 1) < ell;
         warp_rows_partials(
             [&](long long i) {
@@ -347,8 +391,8 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
             },
             deflate ? a.AW : nullptr, true);
         publish_partials(s_wp, nslots, a.partials, a.ps);
-        grid.sync();
-        reduce_partials(a.partials, G, a.ps, nslots, s_c);
+        GSYNC();
+        reduce_partials(a.partials, G, a.ps, nslots, s_c, s_scr);
         const double rr_new = s_c[0];
         const double beta = rr_new / rr;
         rel = sqrt(rr_new) / norm_b;
@@ -361,8 +405,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
             }
         }
         if (deflate) {
-            if (warp == 0) warp_chol_solve(s_L, s_rd, k, s_c + 1, s_mu);
-            __syncthreads();
+            solve_mu(s_L, k, s_c + 1, s_mu);
         }
         cont = (rel > a.tol) && (it < a.max_iters);
         const bool log_p = cont && it < ell;
@@ -382,7 +425,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         }
         if (log_p && deflate && blockIdx.x == 0 && tid < k) a.logMu[it * k + tid] = s_mu[tid];
         rr = rr_new;
-        grid.sync();
+        GSYNC();
     }
     if (blockIdx.x == 0 && tid == 0) {
         a.st->status = DCG_OK;
@@ -397,8 +440,8 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
 }  // namespace
 
 size_t dcg_solve_smem_bytes(long long n, int k, bool sym) {
-    return sizeof(double) * (size_t)(gemv_region_doubles(sym, n) + k * k + DCG_MAX_K + DCG_MAX_K + 2 +
-                                     DCG_MAX_K + DCG_NW * (DCG_MAX_K + 1) + 64);
+    return sizeof(double) * (size_t)(gemv_region_doubles(sym, n) + k * k + DCG_MAX_K + 2 + DCG_MAX_K +
+                                     DCG_NW * (DCG_MAX_K + 1) + 64 + DCG_NT);
 }
 
 extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_b,
@@ -427,7 +470,7 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
     const int ps = ((1 + k) + 1) & ~1;
     const size_t vec = sizeof(double) * (size_t)((n + 31) & ~31LL);
     const size_t tiles = sym ? (size_t)sym_ntiles(n) : 0;
-    const size_t need = 3 * vec + sizeof(double) * (size_t)G * ps + 256 + 2 * sizeof(double) * tiles * DCG_TB + 512;
+    const size_t need = 3 * vec + 2 * sizeof(double) * (size_t)G * ps + 1024 + 2 * sizeof(double) * tiles * DCG_TB;
     int rc = dcg_ws_reserve(ctx, need);
     if (rc) return rc;
     char* w = static_cast<char*>(ctx->ws);
@@ -461,10 +504,11 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
     a.ap = reinterpret_cast<double*>(w + 2 * vec);
     a.partials = reinterpret_cast<double*>(w + 3 * vec);
     a.ps = ps;
-    a.st = reinterpret_cast<DevStatus*>(w + 3 * vec + sizeof(double) * (size_t)G * ps);
     {
-        const size_t off = (3 * vec + sizeof(double) * (size_t)G * ps + sizeof(DevStatus) + 255) & ~size_t(255);
-        a.colpart = reinterpret_cast<double*>(w + off);
+        // status block and barrier words on their own 256-byte line, then the tile partials
+        const size_t st_off = (3 * vec + 2 * sizeof(double) * (size_t)G * ps + 255) & ~size_t(255);
+        a.st = reinterpret_cast<DevStatus*>(w + st_off);
+        a.colpart = reinterpret_cast<double*>(w + st_off + 256);
         a.rowpart = a.colpart + tiles * DCG_TB;
     }
 
@@ -473,6 +517,8 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
     const void* kfn = sym ? (const void*)dcg_solve_kernel<true> : (const void*)dcg_solve_kernel<false>;
     DCG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     DCG_CUDA(cudaMemsetAsync(a.st, 0, sizeof(DevStatus), st));
+    a.bar = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(a.st) + 128);   // inside the st line
+    DCG_CUDA(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned int), st));
     void* args[] = {&a};
     DCG_CUDA(cudaEventRecord(ctx->ev0, st));
     DCG_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(DCG_NT), args, smem, st));

@@ -151,9 +151,29 @@ __device__ __forceinline__ double sym_xval(const double* v, const double* s, lon
     return s ? mul_rn(__ldg(s + j), vv) : vv;
 }
 
+// The ring's mbarriers are initialised once per launch (re-initialising a
+// live mbarrier is undefined); every pass then continues the CTA's tile
+// sequence number `seq`, from which stage and phase parities follow.
+__device__ __forceinline__ void sym_ring_init(double* smem) {
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(
+        smem + DCG_SYM_STAGES * DCG_SYM_STAGE_DOUBLES + 2 * DCG_NW * DCG_TB);
+    unsigned long long* empty = full + DCG_SYM_STAGES;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int st = 0; st < DCG_SYM_STAGES; ++st) {
+            sym_mbar_init(full + st, DCG_NT);     // one cp.async-arrival per thread per use
+            sym_mbar_init(empty + st, DCG_NW);    // one arrival per warp per use
+        }
+    }
+    cta_sync();
+}
+
 // Pass 1 over this CTA's tile range.  colpart/rowpart: ntt x 64 doubles.
+// `seq` (uniform per CTA) counts the tiles this CTA has pushed through the
+// ring in earlier passes of the same launch; it advances by the range length.
 __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long long ldk, long long n, const double* v,
-                                          const double* s, double* colpart, double* rowpart, double* smem) {
+                                          const double* s, double* colpart, double* rowpart, double* smem,
+                                          unsigned int& seq) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double* ring = smem;
     double* rowred = ring + DCG_SYM_STAGES * DCG_SYM_STAGE_DOUBLES;                       // 2 x NW x 64
@@ -165,14 +185,8 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
     const long long t1 = sym_tile_begin(ntt, gridDim.x, blockIdx.x + 1);
     if (t0 >= t1) return;   // uniform per CTA
     const int ntiles = (int)(t1 - t0);
-    if (tid == 0) {
-#pragma unroll
-        for (int st = 0; st < DCG_SYM_STAGES; ++st) {
-            sym_mbar_init(full + st, DCG_NT);     // one cp.async-arrival per thread
-            sym_mbar_init(empty + st, DCG_NW);    // one arrival per warp
-        }
-    }
-    __syncthreads();
+    const unsigned int q0 = seq;   // global sequence number of tile lt is q0 + lt
+    seq += (unsigned int)ntiles;
     long long I = (long long)((sqrt(8.0 * (double)t0 + 1.0) - 1.0) * 0.5);
     while (sym_tile_row_base(I + 1) <= t0) ++I;
     while (sym_tile_row_base(I) > t0) --I;
@@ -185,8 +199,11 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
 #pragma unroll
     for (int st = 0; st < DCG_SYM_STAGES - 1; ++st) {
         if (st < ntiles) {
-            sym_issue_tile(ip, pl, n, iI, iJ, v, s, ring + st * DCG_SYM_STAGE_DOUBLES);
-            sym_mbar_cp_arrive(full + st);
+            const unsigned int q = q0 + st;
+            const int stg = q % DCG_SYM_STAGES;
+            if (q >= DCG_SYM_STAGES) sym_mbar_wait(empty + stg, ((q / DCG_SYM_STAGES) - 1) & 1);
+            sym_issue_tile(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES);
+            sym_mbar_cp_arrive(full + stg);
         }
         if (++iJ > iI) { ++iI; iJ = 0; ip = K + iI * row_stride; } else { ip += DCG_TB; }
     }
@@ -205,16 +222,18 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
         {
             const int tn = lt + DCG_SYM_STAGES - 1;
             if (tn < ntiles) {
-                const int stg = tn % DCG_SYM_STAGES;
-                if (tn >= DCG_SYM_STAGES) sym_mbar_wait(empty + stg, ((tn / DCG_SYM_STAGES) - 1) & 1);
+                const unsigned int q = q0 + tn;
+                const int stg = q % DCG_SYM_STAGES;
+                if (q >= DCG_SYM_STAGES) sym_mbar_wait(empty + stg, ((q / DCG_SYM_STAGES) - 1) & 1);
                 sym_issue_tile(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES);
                 sym_mbar_cp_arrive(full + stg);
             }
             if (++iJ > iI) { ++iI; iJ = 0; ip = K + iI * row_stride; } else { ip += DCG_TB; }
         }
         // consume tile lt
-        const int stg = lt % DCG_SYM_STAGES;
-        sym_mbar_wait(full + stg, (lt / DCG_SYM_STAGES) & 1);
+        const unsigned int q = q0 + lt;
+        const int stg = q % DCG_SYM_STAGES;
+        sym_mbar_wait(full + stg, (q / DCG_SYM_STAGES) & 1);
         const double* tile = ring + stg * DCG_SYM_STAGE_DOUBLES;
         const double2 a0 = *reinterpret_cast<const double2*>(tile + o00);   // row 2l,   cols 4w, 4w+1
         const double2 a1 = *reinterpret_cast<const double2*>(tile + o01);   // row 2l,   cols 4w+2, 4w+3
@@ -265,7 +284,7 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
             double* rr = rowred + (flush & 1) * DCG_NW * DCG_TB;
             rr[warp * DCG_TB + 2 * lane] = row0;
             rr[warp * DCG_TB + 2 * lane + 1] = row1;
-            __syncthreads();
+            cta_sync();
             if (tid < DCG_TB) {
                 double a = 0.0;
 #pragma unroll
@@ -285,7 +304,7 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
             }
         }
     }
-    __syncthreads();   // all arrivals done: the barriers may be re-initialised by the next pass
+    cta_sync();
 }
 
 // Pass 2: t_i for rows [r0, r1) from the partials; epi(i, t_i) runs on one
@@ -305,17 +324,19 @@ __device__ __forceinline__ void sym_pass2(long long n, const double* colpart, co
         double acc = 0.0;
         if (mine) {
             // column parts from tiles (I', I), I' > I, strided over the 8 groups;
-            // four independent chains keep four loads in flight; fixed combination order
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-            long long Ip = I + 1 + g;
-            for (; Ip + 24 < NT; Ip += 32) {
-                a0 += ld_cg(colpart + (sym_tile_row_base(Ip) + I) * DCG_TB + r);
-                a1 += ld_cg(colpart + (sym_tile_row_base(Ip + 8) + I) * DCG_TB + r);
-                a2 += ld_cg(colpart + (sym_tile_row_base(Ip + 16) + I) * DCG_TB + r);
-                a3 += ld_cg(colpart + (sym_tile_row_base(Ip + 24) + I) * DCG_TB + r);
+            // eight independent predicated loads per round (one or two rounds in
+            // practice) instead of a dependent chain; fixed combination order
+            double a[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) a[q] = 0.0;
+            for (long long Ib = I + 1 + g; Ib < NT; Ib += 64) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const long long Ip = Ib + 8 * q;
+                    if (Ip < NT) a[q] += ld_cg(colpart + (sym_tile_row_base(Ip) + I) * DCG_TB + r);
+                }
             }
-            for (; Ip < NT; Ip += 8) a0 += ld_cg(colpart + (sym_tile_row_base(Ip) + I) * DCG_TB + r);
-            acc = (a0 + a1) + (a2 + a3);
+            acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
             if (g == 0) {
                 // row segments of tile row I: start at J = 0 and at every CTA range start inside the row
                 const long long base = sym_tile_row_base(I);
@@ -328,9 +349,9 @@ __device__ __forceinline__ void sym_pass2(long long n, const double* colpart, co
                 }
             }
         }
-        __syncthreads();
+        cta_sync();
         red[g * DCG_TB + r] = acc;
-        __syncthreads();
+        cta_sync();
         if (g == 0 && mine) {
             double t = 0.0;
 #pragma unroll
@@ -338,5 +359,5 @@ __device__ __forceinline__ void sym_pass2(long long n, const double* colpart, co
             epi(i, t);
         }
     }
-    __syncthreads();
+    cta_sync();
 }
