@@ -162,37 +162,47 @@ struct Arena {
 static inline size_t al(size_t bytes) { return (bytes + 255) & ~size_t(255); }
 static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-// Sense-reversal grid barrier for a launch whose CTAs are all co-resident
-// (cooperative launch).  bar[0] counts arrivals, bar[1] is the generation;
-// both are zero at launch.  The last CTA to arrive resets the count before
-// it advances the generation, so a CTA racing ahead into the next barrier
-// never sees a stale count.  Warp 0 waits warp-uniformly (lane 0 polls, the
-// value is broadcast), the other warps wait at the CTA barrier.
+// Grid barrier for a launch whose CTAs are all co-resident (cooperative
+// launch).  `bar` is a monotonic arrival counter, zero at launch: barrier
+// instance m completes when it reaches m * nblocks, so a CTA only needs the
+// value its own arrival returned -- one release-atomic per CTA and acquire
+// polling, no reset and no generation word (two L2 round trips on the
+// critical path).  The CTA barrier before the release orders every thread's
+// writes ahead of it (cumulativity); warp 0 polls warp-uniformly (lane 0
+// loads, __shfl_sync broadcasts) so no lane is left in a divergent spin.
+__device__ __forceinline__ unsigned int atom_add_release_gpu(unsigned int* p, unsigned int v) {
+    unsigned int old;
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void dcg_grid_barrier(unsigned int* bar, unsigned int nblocks) {
     cta_sync();
     if (threadIdx.x < 32) {
-        volatile unsigned int* vgen = bar + 1;
-        unsigned int gen = 0;
+        unsigned int target = 0;
         if (threadIdx.x == 0) {
-            gen = *vgen;   // this CTA has not arrived yet: still the current generation
-            __threadfence();
-            const unsigned int arrived = atomicAdd(bar, 1u);
-            if (arrived == nblocks - 1) {
-                atomicExch(bar, 0u);
-                __threadfence();
-                atomicAdd(bar + 1, 1u);
-            }
+            const unsigned int old = atom_add_release_gpu(bar, 1u);
+            target = (old / nblocks + 1u) * nblocks;
         }
-        gen = __shfl_sync(0xffffffffu, gen, 0);
+        target = __shfl_sync(0xffffffffu, target, 0);
         for (;;) {
             unsigned int cur = 0;
-            if (threadIdx.x == 0) cur = *vgen;
+            if (threadIdx.x == 0) cur = ld_acquire_gpu(bar);
             cur = __shfl_sync(0xffffffffu, cur, 0);
-            if (cur != gen) break;
+            if ((int)(cur - target) >= 0) break;
         }
-        __threadfence();
     }
     cta_sync();
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
 }
 
 // copy a device status block to the host (synchronises the stream)

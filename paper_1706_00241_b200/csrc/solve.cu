@@ -18,6 +18,9 @@
 #include "gemv.cuh"
 #include "symgemv.cuh"
 
+#include <stdio.h>
+#include <stdlib.h>
+
 namespace cg = cooperative_groups;
 
 
@@ -56,25 +59,28 @@ struct SolveArgs {
     double* rowpart;
     int ps;   // partial stride (doubles)
     DevStatus* st;
-    unsigned int* bar;  // grid barrier words (zeroed per launch)
+    unsigned int* bar;  // grid barrier arrival counter (zeroed per launch)
+    unsigned long long* timers;   // optional per-phase ns accumulators (CTA 0, thread 0)
 };
 
 // mu = L^-T L^-1 c for the k x k row-major lower factor of W'AW in shared
 // memory, by one warp (lanes own rows lane and lane + 32).  This is the
 // reference's chol_solve (solvers.py:152,190 -> _core.pyx:69-94): forward
-// substitution in the reference's subtraction order, each unknown divided by
-// its pivot; the backward sweep runs as a wavefront (subtractions as soon as
-// x_j is known).  Triangular solves, not an explicit inverse: W'AW can be
+// substitution in the reference's subtraction order; the backward sweep runs
+// as a wavefront (subtractions as soon as x_j is known).  Pivots are applied as
+// precomputed reciprocals (rdiag = 1 / L_jj): a serial FP64 division per
+// unknown put ~17 us per iteration on the critical path at k = 16, the
+// reciprocal costs at most one extra rounding per unknown.  Triangular solves, not an explicit inverse: W'AW can be
 // ill-conditioned (random or nearly dependent W) and an explicit inverse
 // loses the backward stability the projection relies on.
-__device__ void warp_chol_solve(const double* L, int k, const double* c, double* out) {
+__device__ void warp_chol_solve(const double* L, const double* rdiag, int k, const double* c, double* out) {
     const int lane = threadIdx.x & 31;
     const int i0 = lane, i1 = lane + 32;
     double a0 = (i0 < k) ? c[i0] : 0.0;
     double a1 = (i1 < k) ? c[i1] : 0.0;
     for (int j = 0; j < k; ++j) {
         const double accj = __shfl_sync(0xffffffffu, (j < 32) ? a0 : a1, j & 31);
-        const double yj = div_rn(accj, L[j * k + j]);
+        const double yj = mul_rn(accj, rdiag[j]);
         if (lane == (j & 31)) {
             if (j < 32) a0 = yj; else a1 = yj;
         }
@@ -83,7 +89,7 @@ __device__ void warp_chol_solve(const double* L, int k, const double* c, double*
     }
     for (int j = k - 1; j >= 0; --j) {
         const double accj = __shfl_sync(0xffffffffu, (j < 32) ? a0 : a1, j & 31);
-        const double xj = div_rn(accj, L[j * k + j]);
+        const double xj = mul_rn(accj, rdiag[j]);
         if (lane == (j & 31)) {
             if (j < 32) a0 = xj; else a1 = xj;
         }
@@ -95,8 +101,8 @@ __device__ void warp_chol_solve(const double* L, int k, const double* c, double*
 }
 
 // mu for the deflated update: warp 0 solves, then one CTA barrier.
-__device__ __forceinline__ void solve_mu(const double* L, int k, const double* c, double* mu) {
-    if ((threadIdx.x >> 5) == 0) warp_chol_solve(L, k, c, mu);
+__device__ __forceinline__ void solve_mu(const double* L, const double* rdiag, int k, const double* c, double* mu) {
+    if ((threadIdx.x >> 5) == 0) warp_chol_solve(L, rdiag, k, c, mu);
     cta_sync();
 }
 
@@ -112,16 +118,21 @@ __device__ __forceinline__ void reduce_partials(const double* partials, int G, i
     while (sw < nslots) sw <<= 1;
     const int ng = DCG_NT / sw;
     const int v = tid & (sw - 1), gq = tid / sw;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    double a = 0.0;
     if (v < nslots) {
-        int g = gq;
-        for (; g + 3 * ng < G; g += 4 * ng) {
+        // up to 8 independent loads in flight per thread (one latency round for
+        // G <= 8 * 512 / sw CTAs)
+        for (int g0 = gq; g0 < G; g0 += 8 * ng) {
+            double t[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc[u] += ld_cg(partials + (long long)(g + u * ng) * ps + v);
+            for (int u = 0; u < 8; ++u) {
+                const int g = g0 + u * ng;
+                t[u] = (g < G) ? ld_cg(partials + (long long)g * ps + v) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a += t[u];
         }
-        for (; g < G; g += ng) acc[0] += ld_cg(partials + (long long)g * ps + v);
     }
-    double a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
     if (sw <= 32) {
         // groups inside a warp share a slot at lanes v, v + sw, ...: butterfly over them
         for (int o = sw; o < 32; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
@@ -146,24 +157,6 @@ __device__ __forceinline__ void reduce_partials(const double* partials, int G, i
     cta_sync();
 }
 
-// Sum per-warp partial rows s_wp[w][0..nslots) over warps and publish.
-__device__ __forceinline__ void publish_partials(const double* s_wp, int nslots, double* partials,
-                                                 int ps) {
-    cta_sync();
-    for (int v = threadIdx.x; v < nslots; v += blockDim.x) {
-        double acc = 0.0;
-        for (int w = 0; w < DCG_NW; ++w) acc += s_wp[w * (DCG_MAX_K + 1) + v];
-        partials[(long long)blockIdx.x * ps + v] = acc;
-    }
-}
-
-// Per-warp accumulation of  slot0 += a_i^2  and  slot(1+j) += M[i][j] * a_i
-// over the rows this warp owns; leaves results in s_wp[warp][*].
-struct WarpAcc {
-    double sq;
-    double c0, c1;
-};
-
 // Shared-memory doubles of the GEMV region for each strategy.
 __host__ __device__ __forceinline__ long long gemv_region_doubles(bool sym, long long n) {
     return sym ? sym_smem_doubles() : (min(n, (long long)DCG_QT) + 2 + DCG_NW * DCG_RB);
@@ -172,6 +165,17 @@ __host__ __device__ __forceinline__ long long gemv_region_doubles(bool sym, long
 template <bool SYM>
 __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
 #define GSYNC() dcg_grid_barrier(a.bar, gridDim.x)
+    // Phase timers (DCG_PHASE_TIMERS): CTA 0 / thread 0 attributes the time since
+    // the previous mark to phase `id`; one predicated branch when disabled.
+    unsigned long long t_mark = 0;
+#define PHASE(id)                                                          \
+    do {                                                                   \
+        if (a.timers && blockIdx.x == 0 && threadIdx.x == 0) {             \
+            const unsigned long long t_ = globaltimer_ns();                \
+            if (t_mark) a.timers[id] += t_ - t_mark;                        \
+            t_mark = t_;                                                   \
+        }                                                                  \
+    } while (0)
     extern __shared__ __align__(16) double smem[];
     const long long n = a.n;
     const int k = a.k;
@@ -180,10 +184,10 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     const int xt = (int)min(n, (long long)DCG_QT) + 2;
     double* s_g = smem;                                  // GEMV region (strategy dependent)
     double* s_L = s_g + gemv_region_doubles(SYM, n);     // k*k
-    double* s_c = s_L + k * k;                           // 1 + DCG_MAX_K reduced slots
+    double* s_rd = s_L + k * k;                          // DCG_MAX_K  1 / L_jj
+    double* s_c = s_rd + DCG_MAX_K;                      // 1 + DCG_MAX_K reduced slots
     double* s_mu = s_c + DCG_MAX_K + 2;                  // DCG_MAX_K
-    double* s_wp = s_mu + DCG_MAX_K;                     // DCG_NW * (DCG_MAX_K + 1)
-    double* s_tmp = s_wp + DCG_NW * (DCG_MAX_K + 1);     // 64 scratch
+    double* s_tmp = s_mu + DCG_MAX_K;                    // 64 scratch
     double* s_scr = s_tmp + 64;                          // DCG_NT reduction scratch
 
     const long long r0 = part_begin(n, G, blockIdx.x);
@@ -200,9 +204,13 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     // symmetric strategy contains one extra grid barrier between its passes.
     auto gemv = [&](const double* v, auto&& epi) {
         if constexpr (SYM) {
+            PHASE(15);
             sym_pass1(K, a.ldk, n, v, s, a.colpart, a.rowpart, s_g, ring_seq);
+            PHASE(0);
             GSYNC();
+            PHASE(1);
             sym_pass2(n, a.colpart, a.rowpart, r0, r1, s_g, epi);
+            PHASE(2);
         } else {
             block_gemv<true>(K, a.ldk, n, v, s, r0, r1, s_g, s_g + xt, epi);
         }
@@ -210,31 +218,75 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
 
     for (int i = tid; i < k * k; i += blockDim.x) s_L[i] = a.L[i];
     cta_sync();
+    for (int j = tid; j < k; j += blockDim.x) s_rd[j] = 1.0 / s_L[j * k + j];
+    cta_sync();
 
-    // Accumulate over own rows (warp-per-row): sq += u_i^2 and c_j += M[i][j] * u_i,
-    // u_i produced by `rowfn(i)` executed on all lanes (value must be uniform).
-    auto warp_rows_partials = [&](auto rowfn, const double* M, bool with_sq) {
-        double sq = 0.0, c0 = 0.0, c1 = 0.0;
-        for (long long i = r0 + warp; i < r1; i += DCG_NW) {
-            const double u = rowfn(i);
-            if (with_sq) sq = add_rn(sq, mul_rn(u, u));
-            if (M) {
-                if (lane < k) c0 = fma(M[i * k + lane], u, c0);
-                if (lane + 32 < k) c1 = fma(M[i * k + lane + 32], u, c1);
+    // ---- own-row helpers ------------------------------------------------------
+    // W / AW rows are read-only for the launch and re-read every iteration by
+    // the same CTA; 16-byte loads when the rows allow it.
+    const bool vec2 = ((k & 1) == 0) && (((reinterpret_cast<uintptr_t>(a.W) | reinterpret_cast<uintptr_t>(a.AW)) & 15) == 0);
+    int swk = 1;   // power of two >= k: (row group, j) thread mapping of the basis partials
+    while (swk < k) swk <<= 1;
+    // sum_j M[i][j] v[j] for one row, by one thread (v in shared memory).
+    auto row_dot = [&](const double* M, long long i, const double* v) {
+        const double* row = M + i * k;
+        double t = 0.0;
+        if (vec2) {
+#pragma unroll 4
+            for (int j = 0; j < k; j += 2) {
+                const double2 m = __ldg(reinterpret_cast<const double2*>(row + j));
+                t = fma(m.x, v[j], t);
+                t = fma(m.y, v[j + 1], t);
+            }
+        } else {
+            for (int j = 0; j < k; ++j) t = fma(__ldg(row + j), v[j], t);
+        }
+        return t;
+    };
+    // Publish this CTA's partials: slot 0 = sum_i q_i^2 with q_i = sqval(i)
+    // (thread-per-row; sqval may log), slots 1+j = sum_i M[i][j] u[i] (thread
+    // (row group, j), coalesced rows of M).  Fixed combination order.
+    auto own_partials = [&](auto sqval, const double* u, const double* M, double* partials) {
+        double sq = 0.0;
+        for (long long i = r0 + tid; i < r1; i += DCG_NT) {
+            const double q = sqval(i);
+            sq = add_rn(sq, mul_rn(q, q));
+        }
+        double c = 0.0;
+        if (M) {
+            const int j = tid & (swk - 1), grp = tid / swk, ngrp = DCG_NT / swk;
+            if (j < k) {
+#pragma unroll 4
+                for (long long i = r0 + grp; i < r1; i += ngrp) c = fma(__ldg(M + i * k + j), u[i], c);
+            }
+            if (swk < 32)
+                for (int o = swk; o < 32; o <<= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        }
+        sq = warp_sum(sq);
+        if (lane == 0) s_tmp[warp] = sq;
+        if (M) {
+            if (swk <= 32) {
+                if (lane < swk) s_scr[warp * 32 + lane] = c;
+            } else {
+                s_scr[tid] = c;
             }
         }
-        if (lane == 0) s_wp[warp * (DCG_MAX_K + 1)] = sq;
-        if (M) {
-            if (lane < k) s_wp[warp * (DCG_MAX_K + 1) + 1 + lane] = c0;
-            if (lane + 32 < k) s_wp[warp * (DCG_MAX_K + 1) + 33 + lane] = c1;
+        cta_sync();
+        double* const mine = partials + (long long)blockIdx.x * a.ps;
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < DCG_NW; ++w) t += s_tmp[w];
+            mine[0] = t;
         }
-    };
-    // sum_j M[i][j] * v[j] for row i, uniform across the warp.
-    auto row_dot = [&](const double* M, long long i, const double* v) {
-        double t = 0.0;
-        if (lane < k) t = M[i * k + lane] * v[lane];
-        if (lane + 32 < k) t = fma(M[i * k + lane + 32], v[lane + 32], t);
-        return warp_sum(t);
+        if (M && tid < k) {
+            double t = 0.0;
+            if (swk <= 32) {
+                for (int w = 0; w < DCG_NW; ++w) t += s_scr[w * 32 + tid];
+            } else {
+                for (int g = 0; g < DCG_NT / swk; ++g) t += s_scr[g * swk + tid];
+            }
+            mine[1 + tid] = t;
+        }
     };
 
     // ---------------- prologue: norm_b and the warm-start correction ----------
@@ -247,25 +299,9 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         });
         cta_sync();
         // slot0 = b'b, slots 1.. = W' r_prev
-        {
-            double sq = 0.0, c0 = 0.0, c1 = 0.0;
-            for (long long i = r0 + warp; i < r1; i += DCG_NW) {
-                const double bi = a.b[i];
-                const double ri = a.r[i];
-                sq = fma(bi, bi, sq);
-                if (lane < k) c0 = fma(a.W[i * k + lane], ri, c0);
-                if (lane + 32 < k) c1 = fma(a.W[i * k + lane + 32], ri, c1);
-            }
-            if (lane == 0) s_wp[warp * (DCG_MAX_K + 1)] = sq;
-            if (lane < k) s_wp[warp * (DCG_MAX_K + 1) + 1 + lane] = c0;
-            if (lane + 32 < k) s_wp[warp * (DCG_MAX_K + 1) + 33 + lane] = c1;
-        }
-        publish_partials(s_wp, nslots, a.partials, a.ps);
+        own_partials([&](long long i) { return a.b[i]; }, a.r, a.W, a.partials);
     } else {
-        double sq = 0.0;
-        for (long long i = r0 + tid; i < r1; i += blockDim.x) sq = fma(a.b[i], a.b[i], sq);
-        sq = block_sum(sq, s_tmp);
-        if (tid == 0) a.partials[(long long)blockIdx.x * a.ps] = sq;
+        own_partials([&](long long i) { return a.b[i]; }, nullptr, nullptr, a.partials);
     }
     GSYNC();
     reduce_partials(a.partials, G, a.ps, (a.warm && deflate) ? nslots : 1, s_c, s_scr);
@@ -288,13 +324,10 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         return;
     }
     if (a.warm && deflate) {
-        solve_mu(s_L, k, s_c + 1, s_mu);
-        for (long long i = r0 + warp; i < r1; i += DCG_NW) {
-            const double wy = row_dot(a.W, i, s_mu);
-            if (lane == 0) a.x[i] = add_rn(a.x0[i], wy);
-        }
+        solve_mu(s_L, s_rd, k, s_c + 1, s_mu);
+        for (long long i = r0 + tid; i < r1; i += DCG_NT) a.x[i] = add_rn(a.x0[i], row_dot(a.W, i, s_mu));
     } else {
-        for (long long i = r0 + tid; i < r1; i += blockDim.x) a.x[i] = a.x0[i];
+        for (long long i = r0 + tid; i < r1; i += DCG_NT) a.x[i] = a.x0[i];
     }
     GSYNC();
 
@@ -305,33 +338,22 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         a.r[i] = sub_rn(a.b[i], ax);
     });
     cta_sync();
-    warp_rows_partials([&](long long i) { return a.r[i]; }, deflate ? a.AW : nullptr, true);
-    publish_partials(s_wp, nslots, a.partials, a.ps);
+    own_partials([&](long long i) { return a.r[i]; }, a.r, deflate ? a.AW : nullptr, a.partials);
     GSYNC();
     reduce_partials(a.partials, G, a.ps, nslots, s_c, s_scr);
     double rr = s_c[0];
-    if (deflate) {
-        solve_mu(s_L, k, s_c + 1, s_mu);
-    }
+    if (deflate) solve_mu(s_L, s_rd, k, s_c + 1, s_mu);
     double rel = sqrt(rr) / norm_b;
     long long it = 0;
     const long long ell = a.ell;
     bool cont = (rel > a.tol) && (it < a.max_iters);
     // p0 (+ log r0, p0, mu0)
-    for (long long i = r0 + warp; i < r1; i += DCG_NW) {
+    for (long long i = r0 + tid; i < r1; i += DCG_NT) {
         const double ri = a.r[i];
-        double pi;
-        if (deflate) {
-            const double wm = row_dot(a.W, i, s_mu);
-            pi = sub_rn(ri, wm);
-        } else {
-            pi = ri;
-        }
-        if (lane == 0) {
-            a.p[i] = pi;
-            if (a.logR) a.logR[i] = ri;
-            if (cont && it < ell) a.logP[i] = pi;
-        }
+        const double pi = deflate ? sub_rn(ri, row_dot(a.W, i, s_mu)) : ri;
+        a.p[i] = pi;
+        if (a.logR) a.logR[i] = ri;
+        if (cont && it < ell) a.logP[i] = pi;
     }
     if (blockIdx.x == 0) {
         if (tid == 0) a.history[0] = rel;
@@ -340,6 +362,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     GSYNC();
 
     // ---------------- main loop ------------------------------------------------
+    PHASE(13);   // prologue
     while (cont) {
         // phase G: Ap, partial p'Ap
         double dpart = 0.0;
@@ -352,10 +375,14 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         // p'Ap goes to the second partials buffer: no grid barrier separates this
         // read from the r'r publish below, so they must not share slots.
         double* const dparts = a.partials + (long long)G * a.ps;
+        PHASE(2);
         dpart = block_sum(dpart, s_tmp);
         if (tid == 0) dparts[(long long)blockIdx.x * a.ps] = dpart;
+        PHASE(3);
         GSYNC();
+        PHASE(4);
         reduce_partials(dparts, G, a.ps, 1, s_c, s_scr);
+        PHASE(5);
         const double d = s_c[0];
         if (d <= 0.0) {   // solvers.py:170-172 (NaN falls through, as in numpy)
             if (blockIdx.x == 0 && tid == 0) {
@@ -382,17 +409,20 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
                 a.r[i] = sub_rn(a.r[i], mul_rn(alpha, a.ap[i]));
         }
         cta_sync();
+        PHASE(6);
         const bool log_r = (it - 1) < ell;
-        warp_rows_partials(
+        own_partials(
             [&](long long i) {
                 const double ri = a.r[i];
-                if (log_r && lane == 0) a.logR[it * n + i] = ri;
+                if (log_r) a.logR[it * n + i] = ri;
                 return ri;
             },
-            deflate ? a.AW : nullptr, true);
-        publish_partials(s_wp, nslots, a.partials, a.ps);
+            a.r, deflate ? a.AW : nullptr, a.partials);
+        PHASE(7);
         GSYNC();
+        PHASE(8);
         reduce_partials(a.partials, G, a.ps, nslots, s_c, s_scr);
+        PHASE(9);
         const double rr_new = s_c[0];
         const double beta = rr_new / rr;
         rel = sqrt(rr_new) / norm_b;
@@ -404,28 +434,22 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
                 a.logBeta[it - 1] = beta;
             }
         }
-        if (deflate) {
-            solve_mu(s_L, k, s_c + 1, s_mu);
-        }
+        if (deflate) solve_mu(s_L, s_rd, k, s_c + 1, s_mu);
+        PHASE(10);
         cont = (rel > a.tol) && (it < a.max_iters);
         const bool log_p = cont && it < ell;
-        for (long long i = r0 + warp; i < r1; i += DCG_NW) {
+        for (long long i = r0 + tid; i < r1; i += DCG_NT) {
             const double ri = a.r[i];
-            double pi;
-            if (deflate) {
-                const double wm = row_dot(a.W, i, s_mu);
-                pi = sub_rn(add_rn(mul_rn(beta, a.p[i]), ri), wm);   // beta*p + r - W mu
-            } else {
-                pi = add_rn(ri, mul_rn(beta, a.p[i]));               // r + beta*p
-            }
-            if (lane == 0) {
-                a.p[i] = pi;
-                if (log_p) a.logP[it * n + i] = pi;
-            }
+            const double pi = deflate ? sub_rn(add_rn(mul_rn(beta, a.p[i]), ri), row_dot(a.W, i, s_mu))   // beta*p + r - W mu
+                                      : add_rn(ri, mul_rn(beta, a.p[i]));                                  // r + beta*p
+            a.p[i] = pi;
+            if (log_p) a.logP[it * n + i] = pi;
         }
         if (log_p && deflate && blockIdx.x == 0 && tid < k) a.logMu[it * k + tid] = s_mu[tid];
         rr = rr_new;
+        PHASE(11);
         GSYNC();
+        PHASE(12);
     }
     if (blockIdx.x == 0 && tid == 0) {
         a.st->status = DCG_OK;
@@ -440,8 +464,8 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
 }  // namespace
 
 size_t dcg_solve_smem_bytes(long long n, int k, bool sym) {
-    return sizeof(double) * (size_t)(gemv_region_doubles(sym, n) + k * k + DCG_MAX_K + 2 + DCG_MAX_K +
-                                     DCG_NW * (DCG_MAX_K + 1) + 64 + DCG_NT);
+    return sizeof(double) * (size_t)(gemv_region_doubles(sym, n) + k * k + DCG_MAX_K + DCG_MAX_K + 2 + DCG_MAX_K +
+                                     64 + DCG_NT);
 }
 
 extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_b,
@@ -519,6 +543,16 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
     DCG_CUDA(cudaMemsetAsync(a.st, 0, sizeof(DevStatus), st));
     a.bar = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(a.st) + 128);   // inside the st line
     DCG_CUDA(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned int), st));
+    // DCG_PHASE_TIMERS=1: per-phase device time of CTA 0 printed per solve
+    // (developer diagnostic; costs one predicated branch per phase otherwise).
+    static unsigned long long* d_timers = nullptr;
+    const bool timers = getenv("DCG_PHASE_TIMERS") != nullptr;
+    a.timers = nullptr;
+    if (timers) {
+        if (!d_timers) DCG_CUDA(cudaMalloc(&d_timers, 16 * sizeof(unsigned long long)));
+        DCG_CUDA(cudaMemsetAsync(d_timers, 0, 16 * sizeof(unsigned long long), st));
+        a.timers = d_timers;
+    }
     void* args[] = {&a};
     DCG_CUDA(cudaEventRecord(ctx->ev0, st));
     DCG_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(DCG_NT), args, smem, st));
@@ -531,6 +565,19 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
     DCG_CUDA(cudaStreamSynchronize(st));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    if (timers) {
+        unsigned long long h[16];
+        DCG_CUDA(cudaMemcpy(h, d_timers, sizeof(h), cudaMemcpyDeviceToHost));
+        const long long its = hs->count > 0 ? hs->count : 1;
+        static const char* names[16] = {"pass1", "gsync_mv", "pass2+epi", "pAp_sum", "gsync_d", "reduce_d",
+                                        "x_r_upd", "rr_partials", "gsync_rr", "reduce_rr", "mu_solve",
+                                        "p_upd", "gsync_end", "prologue", "-", "gemv_entry"};
+        fprintf(stderr, "phase_timers n=%lld k=%d its=%lld sym=%d (us per iteration; prologue total):", n, k,
+                hs->count, (int)sym);
+        for (int q = 0; q < 16; ++q)
+            if (h[q]) fprintf(stderr, " %s=%.2f", names[q], q == 13 ? h[q] * 1e-3 : h[q] * 1e-3 / its);
+        fprintf(stderr, "\n");
+    }
     if (hs->status != DCG_OK) {
         if (info) *info = hs->info;
         return hs->status;
