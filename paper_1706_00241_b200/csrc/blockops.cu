@@ -58,18 +58,20 @@ __global__ void __launch_bounds__(DCG_NT, 1)
     sym_pass1_kernel(const double* __restrict__ K, long long ldk, long long n, const double* v, const double* s_in,
                      double* colpart, double* rowpart) {
     extern __shared__ __align__(16) double smem[];
-    sym_ring_init(smem);
+    sym_ring_init(smem, n);
     unsigned int seq = 0;
-    sym_pass1(K, ldk, n, v, s_in, colpart, rowpart, smem, seq);
+    sym_pass1<false>(K, ldk, n, v, s_in, colpart, rowpart, smem, seq);
 }
 
 __global__ void __launch_bounds__(DCG_NT, 1)
     sym_pass2_kernel(long long n, const double* colpart, const double* rowpart, const double* v,
                      const double* s_out, double shift, double* y) {
-    __shared__ double red[8 * DCG_TB];
-    const long long r0 = part_begin(n, gridDim.x, blockIdx.x);
-    const long long r1 = part_begin(n, gridDim.x, blockIdx.x + 1);
-    sym_pass2(n, colpart, rowpart, r0, r1, red, [&](long long i, double t) {
+    __shared__ long long tbl[DCG_SYM_MAX_CTAS + 1];
+    __shared__ double red[DCG_NT];
+    sym_fill_range_table(tbl, n);
+    const long long q0 = sym_row_begin(n, gridDim.x, blockIdx.x);
+    const long long q1 = sym_row_begin(n, gridDim.x, blockIdx.x + 1);
+    sym_pass2(n, colpart, rowpart, q0, q1, tbl, red, [&](long long i, double t) {
         double val = s_out ? mul_rn(s_out[i], t) : t;
         if (shift != 0.0) val = add_rn(mul_rn(shift, v[i]), val);
         y[i] = val;
@@ -87,7 +89,7 @@ int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, long long 
     const long long ntt = sym_ntiles(n);
     double* colpart = scratch;
     double* rowpart = scratch + ntt * DCG_TB;
-    const int G = ctx->sm_count;
+    const int G = ctx->sm_count < DCG_SYM_MAX_CTAS ? ctx->sm_count : DCG_SYM_MAX_CTAS;
     sym_pass1_kernel<<<G, DCG_NT, smem, st>>>(K, ldk, n, v, s_in, colpart, rowpart);
     DCG_LAUNCHED();
     sym_pass2_kernel<<<G, DCG_NT, 0, st>>>(n, colpart, rowpart, v, s_out, shift, y);

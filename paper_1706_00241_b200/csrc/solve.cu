@@ -199,17 +199,30 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     const double shift = a.shift;
 
     unsigned int ring_seq = 0;
-    if constexpr (SYM) sym_ring_init(s_g);
+    // symmetric strategy: pass-2 rows are weighted by their partial count
+    // (sym_row_begin), not the vector-phase rows [r0, r1); pass-2 outputs are
+    // therefore read by other CTAs after a grid barrier, through L2.
+    long long q0 = r0, q1 = r1;
+    if constexpr (SYM) {
+        sym_ring_init(s_g, n);
+        q0 = sym_row_begin(n, G, blockIdx.x);
+        q1 = sym_row_begin(n, G, blockIdx.x + 1);
+    }
     // t = K (s (.) v) for the own rows [r0, r1); epi(i, t_i) per row.  The
     // symmetric strategy contains one extra grid barrier between its passes.
     auto gemv = [&](const double* v, auto&& epi) {
         if constexpr (SYM) {
             PHASE(15);
+            unsigned long long tc0 = 0;
+            if (a.timers && threadIdx.x == 0) tc0 = globaltimer_ns();
             sym_pass1(K, a.ldk, n, v, s, a.colpart, a.rowpart, s_g, ring_seq);
+            if (a.timers && threadIdx.x == 0) a.timers[16 + blockIdx.x] += globaltimer_ns() - tc0;
             PHASE(0);
             GSYNC();
             PHASE(1);
-            sym_pass2(n, a.colpart, a.rowpart, r0, r1, s_g, epi);
+            if (a.timers && threadIdx.x == 0) tc0 = globaltimer_ns();
+            sym_pass2(n, a.colpart, a.rowpart, q0, q1, sym_range_table(s_g), s_g, epi);
+            if (a.timers && threadIdx.x == 0) a.timers[16 + gridDim.x + blockIdx.x] += globaltimer_ns() - tc0;
             PHASE(2);
         } else {
             block_gemv<true>(K, a.ldk, n, v, s, r0, r1, s_g, s_g + xt, epi);
@@ -257,7 +270,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
             const int j = tid & (swk - 1), grp = tid / swk, ngrp = DCG_NT / swk;
             if (j < k) {
 #pragma unroll 4
-                for (long long i = r0 + grp; i < r1; i += ngrp) c = fma(__ldg(M + i * k + j), u[i], c);
+                for (long long i = r0 + grp; i < r1; i += ngrp) c = fma(__ldg(M + i * k + j), ld_cg(u + i), c);
             }
             if (swk < 32)
                 for (int o = swk; o < 32; o <<= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
@@ -297,7 +310,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
                                 : add_rn(mul_rn(shift, a.x0[i]), t);
             a.r[i] = sub_rn(a.b[i], ax);
         });
-        cta_sync();
+        if constexpr (SYM) GSYNC(); else cta_sync();
         // slot0 = b'b, slots 1.. = W' r_prev
         own_partials([&](long long i) { return a.b[i]; }, a.r, a.W, a.partials);
     } else {
@@ -333,12 +346,12 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
 
     // ---------------- r0 = b - A x0 ; mu ; p0 ------------------------------------
     gemv(a.x, [&](long long i, double t) {
-        const double xi = a.x[i];
+        const double xi = ld_cg(a.x + i);
         const double ax = s ? add_rn(mul_rn(shift, xi), mul_rn(s[i], t)) : add_rn(mul_rn(shift, xi), t);
         a.r[i] = sub_rn(a.b[i], ax);
     });
-    cta_sync();
-    own_partials([&](long long i) { return a.r[i]; }, a.r, deflate ? a.AW : nullptr, a.partials);
+    if constexpr (SYM) GSYNC(); else cta_sync();
+    own_partials([&](long long i) { return ld_cg(a.r + i); }, a.r, deflate ? a.AW : nullptr, a.partials);
     GSYNC();
     reduce_partials(a.partials, G, a.ps, nslots, s_c, s_scr);
     double rr = s_c[0];
@@ -349,7 +362,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     bool cont = (rel > a.tol) && (it < a.max_iters);
     // p0 (+ log r0, p0, mu0)
     for (long long i = r0 + tid; i < r1; i += DCG_NT) {
-        const double ri = a.r[i];
+        const double ri = ld_cg(a.r + i);
         const double pi = deflate ? sub_rn(ri, row_dot(a.W, i, s_mu)) : ri;
         a.p[i] = pi;
         if (a.logR) a.logR[i] = ri;
@@ -400,20 +413,21 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         if (recompute) {
             GSYNC();
             gemv(a.x, [&](long long i, double t) {
-                const double xi = a.x[i];
+                const double xi = ld_cg(a.x + i);
                 const double ax = s ? add_rn(mul_rn(shift, xi), mul_rn(s[i], t)) : add_rn(mul_rn(shift, xi), t);
                 a.r[i] = sub_rn(a.b[i], ax);
             });
+            if constexpr (SYM) GSYNC();
         } else {
             for (long long i = r0 + tid; i < r1; i += blockDim.x)
-                a.r[i] = sub_rn(a.r[i], mul_rn(alpha, a.ap[i]));
+                a.r[i] = sub_rn(ld_cg(a.r + i), mul_rn(alpha, ld_cg(a.ap + i)));
         }
         cta_sync();
         PHASE(6);
         const bool log_r = (it - 1) < ell;
         own_partials(
             [&](long long i) {
-                const double ri = a.r[i];
+                const double ri = ld_cg(a.r + i);
                 if (log_r) a.logR[it * n + i] = ri;
                 return ri;
             },
@@ -439,7 +453,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         cont = (rel > a.tol) && (it < a.max_iters);
         const bool log_p = cont && it < ell;
         for (long long i = r0 + tid; i < r1; i += DCG_NT) {
-            const double ri = a.r[i];
+            const double ri = ld_cg(a.r + i);
             const double pi = deflate ? sub_rn(add_rn(mul_rn(beta, a.p[i]), ri), row_dot(a.W, i, s_mu))   // beta*p + r - W mu
                                       : add_rn(ri, mul_rn(beta, a.p[i]));                                  // r + beta*p
             a.p[i] = pi;
@@ -549,8 +563,8 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
     const bool timers = getenv("DCG_PHASE_TIMERS") != nullptr;
     a.timers = nullptr;
     if (timers) {
-        if (!d_timers) DCG_CUDA(cudaMalloc(&d_timers, 16 * sizeof(unsigned long long)));
-        DCG_CUDA(cudaMemsetAsync(d_timers, 0, 16 * sizeof(unsigned long long), st));
+        if (!d_timers) DCG_CUDA(cudaMalloc(&d_timers, 1024 * sizeof(unsigned long long)));
+        DCG_CUDA(cudaMemsetAsync(d_timers, 0, 1024 * sizeof(unsigned long long), st));
         a.timers = d_timers;
     }
     void* args[] = {&a};
@@ -577,6 +591,27 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
         for (int q = 0; q < 16; ++q)
             if (h[q]) fprintf(stderr, " %s=%.2f", names[q], q == 13 ? h[q] * 1e-3 : h[q] * 1e-3 / its);
         fprintf(stderr, "\n");
+        if (sym) {
+            unsigned long long hc[1024];
+            DCG_CUDA(cudaMemcpy(hc, d_timers, sizeof(hc), cudaMemcpyDeviceToHost));
+            for (int ph = 0; ph < 2; ++ph) {
+                const unsigned long long* v = hc + 16 + ph * G;
+                int imin = 0, imax = 0;
+                double sum = 0;
+                for (int b = 0; b < G; ++b) {
+                    sum += v[b];
+                    if (v[b] < v[imin]) imin = b;
+                    if (v[b] > v[imax]) imax = b;
+                }
+                const double nmv = (double)(its + 2);
+                fprintf(stderr, "  pass%d per-CTA us/matvec: min %.2f (cta %d) mean %.2f max %.2f (cta %d); first8:", ph + 1,
+                        v[imin] * 1e-3 / nmv, imin, sum / G * 1e-3 / nmv, v[imax] * 1e-3 / nmv, imax);
+                for (int b = 0; b < 8; ++b) fprintf(stderr, " %.1f", v[b] * 1e-3 / nmv);
+                fprintf(stderr, " last4:");
+                for (int b = G - 4; b < G; ++b) fprintf(stderr, " %.1f", v[b] * 1e-3 / nmv);
+                fprintf(stderr, "\n");
+            }
+        }
     }
     if (hs->status != DCG_OK) {
         if (info) *info = hs->info;

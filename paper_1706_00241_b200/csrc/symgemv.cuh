@@ -5,8 +5,9 @@
 // HBM traffic per CG iteration), as 64 x 64 tiles (I, J <= I) of the padded
 // row-major storage:
 //
-//   pass 1 (all CTAs): the linear tile sequence is split into balanced
-//     contiguous ranges, one per CTA.  Tiles flow through a DCG_SYM_STAGES-deep
+//   pass 1 (all CTAs): the linear tile sequence is split into contiguous
+//     ranges of equal estimated cost (a tile-row segment flush and the partial
+//     last tile row are weighted), one per CTA.  Tiles flow through a DCG_SYM_STAGES-deep
 //     shared-memory ring filled by per-thread 16-byte cp.async copies whose
 //     completion is tracked by mbarriers (cp.async.mbarrier.arrive), and
 //     released by one arrival per warp: warps never wait on a CTA barrier per
@@ -19,7 +20,9 @@
 //     The tile is stored XOR-swizzled (16-byte chunk q of row r at q ^ (r/2))
 //     so the column-strip reads are bank-conflict free.
 //   pass 2 (after a grid barrier): t_i = sum of the segment partials of tile
-//     row I plus colpart of the tiles (I', I), I' > I, in a fixed order.
+//     row I plus colpart of the tiles (I', I), I' > I, in a fixed order.  Row
+//     i of tile row I costs ~NT - I loads, so rows are split by that weight and
+//     each row is reduced by up to 32 lanes of one warp (no CTA barriers).
 //
 // Both passes are deterministic (no atomics).  Pass 2 touches 2 x 64 doubles
 // per tile, ~3% of the tile bytes.
@@ -27,7 +30,9 @@
 #include "common.cuh"
 
 #define DCG_TB 64
+#ifndef DCG_SYM_STAGES
 #define DCG_SYM_STAGES 4
+#endif
 #define DCG_SYM_TILE_DOUBLES (DCG_TB * DCG_TB)
 // a ring stage: the tile plus the 64-entry slices v_J and s_J the tile's row
 // product needs, so everything a tile consumes arrives with it
@@ -38,28 +43,95 @@ __host__ __device__ __forceinline__ long long sym_ntiles(long long n) {
     const long long nt = sym_ntiles_side(n);
     return nt * (nt + 1) / 2;
 }
-// CTA b of G owns tiles [sym_tile_begin(b), sym_tile_begin(b+1))
-__host__ __device__ __forceinline__ long long sym_tile_begin(long long ntt, long long G, long long b) {
-    return (b * ntt) / G;
-}
-// owner CTA of tile t
-__host__ __device__ __forceinline__ long long sym_tile_owner(long long ntt, long long G, long long t) {
-    return ((t + 1) * G - 1) / ntt;
-}
 __host__ __device__ __forceinline__ long long sym_tile_row_base(long long I) { return I * (I + 1) / 2; }
+// tile row of linear tile t (tiles (I, 0..I) are consecutive)
+__host__ __device__ __forceinline__ long long sym_tile_row(long long t) {
+    long long I = (long long)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while (sym_tile_row_base(I + 1) <= t) ++I;
+    while (sym_tile_row_base(I) > t) --I;
+    return I;
+}
 
+// ---- pass-1 partition: equal estimated cost per CTA ---------------------------
+// Cost in quarter tiles of the tiles [0, t) (measured per-CTA pass times):
+// 4 per tile, +4 per tile-row segment flush (one per completed row: a CTA
+// barrier and a 16-way smem sum), +1 per tile of a partial last tile row --
+// those move fewer bytes but hold a ring slot for a full loaded-HBM round trip
+// and measured ~1.2x a full tile.
+__host__ __device__ __forceinline__ long long sym_cost4(long long t, long long n) {
+    const long long NT = sym_ntiles_side(n);
+    const long long last = (n % DCG_TB) ? sym_tile_row_base(NT - 1) : sym_tile_row_base(NT);
+    const long long inlast = t > last ? t - last : 0;
+    return 4 * t + inlast + 4 * sym_tile_row(t);
+}
+// first tile of CTA b of G: smallest t with cost(t) >= ceil(b * total / G)
+__host__ __device__ __forceinline__ long long sym_tile_begin(long long n, long long G, long long b) {
+    const long long NT = sym_ntiles_side(n), ntt = NT * (NT + 1) / 2;
+    if (b <= 0) return 0;
+    if (b >= G) return ntt;
+    const long long total = sym_cost4(ntt, n);
+    const long long goal = (b * total + G - 1) / G;
+    long long lo = 0, hi = ntt;
+    while (lo < hi) {
+        const long long mid = (lo + hi) / 2;
+        if (sym_cost4(mid, n) >= goal) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+// ---- pass-2 partition: rows weighted by their partial count -------------------
+// Row i of tile row I reads NT - 1 - I column partials, ~1 row-segment partial
+// and runs the epilogue: weight NT + 3 - I.  W(i) = weight of rows [0, i).
+__host__ __device__ __forceinline__ long long sym_row_work(long long i, long long n) {
+    const long long NT = sym_ntiles_side(n);
+    const long long I = i / DCG_TB;
+    return DCG_TB * (I * (NT + 3) - I * (I - 1) / 2) + (i - I * DCG_TB) * (NT + 3 - I);
+}
+__host__ __device__ __forceinline__ long long sym_row_begin(long long n, long long G, long long b) {
+    if (b <= 0) return 0;
+    if (b >= G) return n;
+    const long long goal = (b * sym_row_work(n, n) + G - 1) / G;
+    long long lo = 0, hi = n;
+    while (lo < hi) {
+        const long long mid = (lo + hi) / 2;
+        if (sym_row_work(mid, n) >= goal) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+#define DCG_SYM_MAX_CTAS 255
 // Shared memory the two passes need (doubles): ring, 2 x 16 x 64 row-flush
-// buffers, 2 x STAGES mbarriers.
+// buffers, 2 x STAGES mbarriers, the table of G + 1 pass-1 range starts.
 __host__ __device__ __forceinline__ long long sym_smem_doubles() {
-    return (long long)DCG_SYM_STAGES * DCG_SYM_STAGE_DOUBLES + 2 * DCG_NW * DCG_TB + 2 * DCG_SYM_STAGES + 2;
+    return (long long)DCG_SYM_STAGES * DCG_SYM_STAGE_DOUBLES + 2 * DCG_NW * DCG_TB + 2 * DCG_SYM_STAGES + 2 +
+           (DCG_SYM_MAX_CTAS + 1);
+}
+__device__ __forceinline__ long long* sym_range_table(double* smem) {
+    return reinterpret_cast<long long*>(smem + DCG_SYM_STAGES * DCG_SYM_STAGE_DOUBLES + 2 * DCG_NW * DCG_TB +
+                                        2 * DCG_SYM_STAGES + 2);
+}
+// tbl[b] = first tile of CTA b, b = 0..G (all threads call; ends with a barrier)
+__device__ __forceinline__ void sym_fill_range_table(long long* tbl, long long n) {
+    for (int b = threadIdx.x; b <= (int)gridDim.x; b += blockDim.x) tbl[b] = sym_tile_begin(n, gridDim.x, b);
+    cta_sync();
 }
 
 // ---- async copy and mbarrier primitives ------------------------------------
 __device__ __forceinline__ unsigned sym_saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void sym_cp_async16(double* sdst, const double* gsrc, int bytes) {
+// K is streamed once per product and is far larger than L2: its lines are
+// marked evict-first so they do not push out the vectors and the tile
+// partials pass 2 reads back.
+// (the 64-bit L2 cache-policy encoding of createpolicy.fractional.L2::evict_first
+// with fraction 1.0, as a constant so it is materialised in uniform registers)
+__device__ __forceinline__ unsigned long long sym_policy_evict_first() { return 0x12F0000000000000ull; }
+__device__ __forceinline__ void sym_cp_async16_full(double* sdst, const double* gsrc, unsigned long long pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sym_saddr(sdst)), "l"(gsrc),
+                 "l"(pol));
+}
+__device__ __forceinline__ void sym_cp_async16_v(double* sdst, const double* gsrc, int bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sym_saddr(sdst)), "l"(gsrc), "r"(bytes));
 }
-__device__ __forceinline__ void sym_cp_async16_full(double* sdst, const double* gsrc) {
+__device__ __forceinline__ void sym_cp_async16_vfull(double* sdst, const double* gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sym_saddr(sdst)), "l"(gsrc));
 }
 __device__ __forceinline__ void sym_mbar_init(unsigned long long* bar, unsigned count) {
@@ -113,34 +185,42 @@ __device__ __forceinline__ SymCopyPlan sym_copy_plan(long long ldk) {
 // Issue this thread's copies of tile (I, J) (top-left element `kt`) and of the
 // slices v_J, s_J into stage `dst`.  cp.async.cg reads through L2, so v may
 // have been written by other CTAs before the preceding grid barrier.
+template <bool kHint>
 __device__ __forceinline__ void sym_issue_tile(const double* __restrict__ kt, const SymCopyPlan& pl, long long n,
                                                long long I, long long J, const double* v, const double* s,
-                                               double* dst) {
+                                               double* dst, unsigned long long pol) {
     const int tid = threadIdx.x;
     const long long r_base = I * DCG_TB, c_base = J * DCG_TB;
     if (r_base + DCG_TB <= n) {   // J <= I: the column block is interior as well
 #pragma unroll
-        for (int u = 0; u < DCG_SYM_TILE_DOUBLES / 2 / DCG_NT; ++u)
-            sym_cp_async16_full(dst + pl.soff[u], kt + pl.koff[u]);
-        if (tid < 32) sym_cp_async16_full(dst + DCG_SYM_TILE_DOUBLES + 2 * tid, v + c_base + 2 * tid);
+        for (int u = 0; u < DCG_SYM_TILE_DOUBLES / 2 / DCG_NT; ++u) {
+            if constexpr (kHint) sym_cp_async16_full(dst + pl.soff[u], kt + pl.koff[u], pol);
+            else sym_cp_async16_vfull(dst + pl.soff[u], kt + pl.koff[u]);
+        }
+        if (tid < 32) sym_cp_async16_vfull(dst + DCG_SYM_TILE_DOUBLES + 2 * tid, v + c_base + 2 * tid);
         else if (tid < 64 && s)
-            sym_cp_async16_full(dst + DCG_SYM_TILE_DOUBLES + DCG_TB + 2 * (tid - 32), s + c_base + 2 * (tid - 32));
+            sym_cp_async16_vfull(dst + DCG_SYM_TILE_DOUBLES + DCG_TB + 2 * (tid - 32), s + c_base + 2 * (tid - 32));
         return;
     }
 #pragma unroll
     for (int u = 0; u < DCG_SYM_TILE_DOUBLES / 2 / DCG_NT; ++u) {
         const long long gr = r_base + pl.crow + 16 * u, gc = c_base + pl.c2;
         const int bytes = gr < n ? sym_chunk_bytes(gc, n) : 0;
-        sym_cp_async16(dst + pl.soff[u], bytes ? kt + pl.koff[u] : kt, bytes);
+        // chunks wholly beyond n are not copied: their stage slots keep earlier
+        // (finite) tile data, which only ever meets zero x entries
+        // (edge chunks use the plain form: a zero-filling cp.async with an L2
+        // cache hint faulted as an illegal instruction on sm_100a)
+        if (bytes == 16 && kHint) sym_cp_async16_full(dst + pl.soff[u], kt + pl.koff[u], pol);
+        else if (bytes) sym_cp_async16_v(dst + pl.soff[u], kt + pl.koff[u], bytes);
     }
     if (tid < 32) {
         const long long j = c_base + 2 * tid;
         const int bytes = sym_chunk_bytes(j, n);
-        sym_cp_async16(dst + DCG_SYM_TILE_DOUBLES + 2 * tid, bytes ? v + j : v, bytes);
+        sym_cp_async16_v(dst + DCG_SYM_TILE_DOUBLES + 2 * tid, bytes ? v + j : v, bytes);
     } else if (tid < 64 && s) {
         const long long j = c_base + 2 * (tid - 32);
         const int bytes = sym_chunk_bytes(j, n);
-        sym_cp_async16(dst + DCG_SYM_TILE_DOUBLES + DCG_TB + 2 * (tid - 32), bytes ? s + j : s, bytes);
+        sym_cp_async16_v(dst + DCG_SYM_TILE_DOUBLES + DCG_TB + 2 * (tid - 32), bytes ? s + j : s, bytes);
     }
 }
 
@@ -154,23 +234,27 @@ __device__ __forceinline__ double sym_xval(const double* v, const double* s, lon
 // The ring's mbarriers are initialised once per launch (re-initialising a
 // live mbarrier is undefined); every pass then continues the CTA's tile
 // sequence number `seq`, from which stage and phase parities follow.
-__device__ __forceinline__ void sym_ring_init(double* smem) {
+__device__ __forceinline__ void sym_ring_init(double* smem, long long n) {
     unsigned long long* full = reinterpret_cast<unsigned long long*>(
         smem + DCG_SYM_STAGES * DCG_SYM_STAGE_DOUBLES + 2 * DCG_NW * DCG_TB);
     unsigned long long* empty = full + DCG_SYM_STAGES;
+    // finite stage contents from the start (edge tiles leave slots uncopied)
+    for (int e = threadIdx.x; e < DCG_SYM_STAGES * DCG_SYM_STAGE_DOUBLES; e += blockDim.x) smem[e] = 0.0;
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int st = 0; st < DCG_SYM_STAGES; ++st) {
             sym_mbar_init(full + st, DCG_NT);     // one cp.async-arrival per thread per use
             sym_mbar_init(empty + st, DCG_NW);    // one arrival per warp per use
         }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    cta_sync();
+    sym_fill_range_table(sym_range_table(smem), n);
 }
 
 // Pass 1 over this CTA's tile range.  colpart/rowpart: ntt x 64 doubles.
 // `seq` (uniform per CTA) counts the tiles this CTA has pushed through the
 // ring in earlier passes of the same launch; it advances by the range length.
+template <bool kHint = true>
 __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long long ldk, long long n, const double* v,
                                           const double* s, double* colpart, double* rowpart, double* smem,
                                           unsigned int& seq) {
@@ -179,19 +263,17 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
     double* rowred = ring + DCG_SYM_STAGES * DCG_SYM_STAGE_DOUBLES;                       // 2 x NW x 64
     unsigned long long* full = reinterpret_cast<unsigned long long*>(rowred + 2 * DCG_NW * DCG_TB);
     unsigned long long* empty = full + DCG_SYM_STAGES;
-    const long long NT = sym_ntiles_side(n);
-    const long long ntt = NT * (NT + 1) / 2;
-    const long long t0 = sym_tile_begin(ntt, gridDim.x, blockIdx.x);
-    const long long t1 = sym_tile_begin(ntt, gridDim.x, blockIdx.x + 1);
+    const long long* tbl = sym_range_table(smem);
+    const long long t0 = tbl[blockIdx.x];
+    const long long t1 = tbl[blockIdx.x + 1];
     if (t0 >= t1) return;   // uniform per CTA
     const int ntiles = (int)(t1 - t0);
     const unsigned int q0 = seq;   // global sequence number of tile lt is q0 + lt
     seq += (unsigned int)ntiles;
-    long long I = (long long)((sqrt(8.0 * (double)t0 + 1.0) - 1.0) * 0.5);
-    while (sym_tile_row_base(I + 1) <= t0) ++I;
-    while (sym_tile_row_base(I) > t0) --I;
+    long long I = sym_tile_row(t0);
     long long J = t0 - sym_tile_row_base(I);
     const SymCopyPlan pl = sym_copy_plan(ldk);
+    const unsigned long long pol = sym_policy_evict_first();
     const long long row_stride = (long long)DCG_TB * ldk;
     // prologue: tiles 0 .. STAGES-2; issue cursor (iI, iJ, ip) follows
     long long iI = I, iJ = J;
@@ -202,7 +284,7 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
             const unsigned int q = q0 + st;
             const int stg = q % DCG_SYM_STAGES;
             if (q >= DCG_SYM_STAGES) sym_mbar_wait(empty + stg, ((q / DCG_SYM_STAGES) - 1) & 1);
-            sym_issue_tile(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES);
+            sym_issue_tile<kHint>(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES, pol);
             sym_mbar_cp_arrive(full + stg);
         }
         if (++iJ > iI) { ++iI; iJ = 0; ip = K + iI * row_stride; } else { ip += DCG_TB; }
@@ -225,7 +307,7 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
                 const unsigned int q = q0 + tn;
                 const int stg = q % DCG_SYM_STAGES;
                 if (q >= DCG_SYM_STAGES) sym_mbar_wait(empty + stg, ((q / DCG_SYM_STAGES) - 1) & 1);
-                sym_issue_tile(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES);
+                sym_issue_tile<kHint>(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES, pol);
                 sym_mbar_cp_arrive(full + stg);
             }
             if (++iJ > iI) { ++iI; iJ = 0; ip = K + iI * row_stride; } else { ip += DCG_TB; }
@@ -307,57 +389,69 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
     cta_sync();
 }
 
-// Pass 2: t_i for rows [r0, r1) from the partials; epi(i, t_i) runs on one
-// thread per row.  `red` needs 8 x 64 doubles of shared memory.
+// Pass 2: t_i for rows [q0, q1) (sym_row_begin partition) from the partials;
+// epi(i, t_i) runs on one thread per row.  `tbl` is the pass-1 range table,
+// `red` 512 doubles of shared scratch.  A round covers 32 * nwr consecutive
+// rows (lane = row, so a warp's loads of one tile partial are coalesced); the
+// 16 / nwr warps sharing a row slice each sum a strided subset of the column
+// partials with up to 16 independent loads in flight, then the subsets are
+// combined in a fixed order.
 template <class Epi>
-__device__ __forceinline__ void sym_pass2(long long n, const double* colpart, const double* rowpart, long long r0,
-                                          long long r1, double* red, Epi&& epi) {
-    const int tid = threadIdx.x;
-    const int r = tid & (DCG_TB - 1), g = tid >> 6;
+__device__ __forceinline__ void sym_pass2(long long n, const double* colpart, const double* rowpart, long long q0,
+                                          long long q1, const long long* tbl, double* red, Epi&& epi) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long NT = sym_ntiles_side(n);
-    const long long ntt = NT * (NT + 1) / 2;
-    const long long G = gridDim.x;
-    if (r0 >= r1) return;
-    for (long long I = r0 / DCG_TB; I * DCG_TB < r1; ++I) {
-        const long long i = I * DCG_TB + r;
-        const bool mine = (i >= r0 && i < r1);
+    const long long R = q1 - q0;
+    if (R <= 0) return;
+    const int nwr = (int)min((R + 31) / 32, (long long)DCG_NW);   // row warps per round
+    const int S = DCG_NW / nwr;                                    // warps per row slice
+    const int slice = warp / S, sub = warp % S;
+    const bool active = slice < nwr;                               // (16 % nwr leftovers idle)
+    const int G = gridDim.x;
+    for (long long rb = q0; rb < q1; rb += 32LL * nwr) {
+        const long long i = rb + 32LL * slice + lane;
         double acc = 0.0;
-        if (mine) {
-            // column parts from tiles (I', I), I' > I, strided over the 8 groups;
-            // eight independent predicated loads per round (one or two rounds in
-            // practice) instead of a dependent chain; fixed combination order
-            double a[8];
+        if (active && i < q1) {
+            const long long I = i / DCG_TB;
+            const int r = (int)(i - I * DCG_TB);
+            double a[16];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) a[q] = 0.0;
-            for (long long Ib = I + 1 + g; Ib < NT; Ib += 64) {
+            for (int q = 0; q < 16; ++q) a[q] = 0.0;
+            for (long long Ib = I + 1 + sub; Ib < NT; Ib += 16LL * S) {
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const long long Ip = Ib + 8 * q;
+                for (int q = 0; q < 16; ++q) {
+                    const long long Ip = Ib + (long long)q * S;
                     if (Ip < NT) a[q] += ld_cg(colpart + (sym_tile_row_base(Ip) + I) * DCG_TB + r);
                 }
             }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) a[q] += a[q + 8];
             acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-            if (g == 0) {
-                // row segments of tile row I: start at J = 0 and at every CTA range start inside the row
+            if (sub == 0) {
+                // row segments of tile row I: one starts at J = 0, one at every
+                // pass-1 range start inside the row (empty ranges counted once)
                 const long long base = sym_tile_row_base(I);
                 acc += ld_cg(rowpart + base * DCG_TB + r);
-                const long long b_lo = sym_tile_owner(ntt, G, base), b_hi = sym_tile_owner(ntt, G, base + I);
-                // (several CTAs share a start when there are more CTAs than tiles: count it once)
-                for (long long b = b_lo + 1; b <= b_hi; ++b) {
-                    const long long ts = sym_tile_begin(ntt, G, b);
-                    if (ts > sym_tile_begin(ntt, G, b - 1)) acc += ld_cg(rowpart + ts * DCG_TB + r);
+                int lo = 0, hi = G + 1;   // first b with tbl[b] > base
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (tbl[mid] > base) hi = mid; else lo = mid + 1;
                 }
+                for (int b = lo; b <= G && tbl[b] <= base + I; ++b)
+                    if (tbl[b] > tbl[b - 1]) acc += ld_cg(rowpart + tbl[b] * DCG_TB + r);
             }
         }
-        cta_sync();
-        red[g * DCG_TB + r] = acc;
-        cta_sync();
-        if (g == 0 && mine) {
-            double t = 0.0;
-#pragma unroll
-            for (int gg = 0; gg < 8; ++gg) t += red[gg * DCG_TB + r];
-            epi(i, t);
+        if (S > 1) {
+            red[tid] = acc;
+            cta_sync();
+            if (sub == 0 && active && i < q1) {
+                double t = acc;
+                for (int u = 1; u < S; ++u) t += red[(warp + u) * 32 + lane];
+                epi(i, t);
+            }
+            cta_sync();
+        } else if (active && i < q1) {
+            epi(i, acc);
         }
     }
-    cta_sync();
 }
