@@ -16,6 +16,8 @@
 #include "common.cuh"
 
 #define SD_NT 512
+// pencils up to this order keep all working matrices in shared memory (4 T^2 doubles)
+#define DCG_PENCIL_SMEM_T 80
 
 // ---------------------------------------------------------------------------
 // Cholesky with the reference's pivot rule (acc <= pivot_tol fails at j).
@@ -138,108 +140,156 @@ static __device__ void warp_solve_lower_trans(const double* L, int ldl, int n, c
 // Parallel-order Jacobi eigensolver on a symmetric T x T matrix A (row-major,
 // leading dimension T, typically shared memory); V receives eigenvectors as
 // columns (unsorted).  Returns 0, or the sweep budget on NoConvergence.
+//
+// Same method as linalg.sym_eigen / _core.jacobi_sweep (linalg.py:139-165,
+// _core.pyx:135-177): convergence test off(A) <= rtol ||A||_F before every
+// sweep, the skip rule |a_pp| + 100|a_pq| == |a_pp| (and for q) zeroes a_pq,
+// t = sgn(tau) / (|tau| + sqrt(1 + tau^2)), c = 1 / sqrt(1 + t^2), s = t c.
+// The rotations of a sweep are applied in the circle-method parallel order
+// (T/2 disjoint pairs per round) instead of the row-cyclic order, and the
+// rotation parameters come from hardware reciprocal / rsqrt approximations
+// refined by two Newton steps (working precision): the solver is a chain of
+// ~8 sweeps x (T - 1) dependent rounds, so each round's latency is what
+// counts.  Every thread updates at most a couple of 2 x 2 blocks per round
+// (a 32 x 16 grid over row pairs x column pairs), so the round is one short
+// dependent chain per thread.
 // ---------------------------------------------------------------------------
+#define JAC_NT 512   // == the pencil / eigen kernels' CTA size
+__device__ __forceinline__ void jac_sync() { cta_sync(); }
+__device__ __forceinline__ double fast_rcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = fma(r, fma(-x, r, 1.0), r);
+    r = fma(r, fma(-x, r, 1.0), r);
+    return r;
+}
+__device__ __forceinline__ double fast_rsqrt(double x) {
+    double r;
+    asm("rsqrt.approx.f64 %0, %1;" : "=d"(r) : "d"(x));
+    const double hx = 0.5 * x;
+    r = r * fma(-hx * r, r, 1.5);
+    r = r * fma(-hx * r, r, 1.5);
+    return r;
+}
+
 __device__ int cta_jacobi(double* A, double* V, int T, int max_sweeps, double rtol, double* red,
                           double* s_c, double* s_s, int* s_mode) {
     const int tid = threadIdx.x;
+    __shared__ int s_result;
     for (int e = tid; e < T * T; e += blockDim.x) V[e] = (e / T == e % T) ? 1.0 : 0.0;
-    // frob = sqrt(sum a^2) of the input; off = sqrt(sum offdiag^2)
+    // frob = sqrt(sum a^2) of the input
     double f2 = 0.0;
     for (int e = tid; e < T * T; e += blockDim.x) f2 = fma(A[e], A[e], f2);
     const double frob = sqrt(block_sum(f2, red));
     if (frob == 0.0) return 0;   // zeros and identity (linalg.py:153-154)
-    auto offdiag = [&]() {
-        double o2 = 0.0;
-        for (int e = tid; e < T * T; e += blockDim.x)
-            if (e / T != e % T) o2 = fma(A[e], A[e], o2);
-        return sqrt(block_sum(o2, red));
-    };
-    bool converged = offdiag() <= rtol * frob;
-    const int Te = T + (T & 1);
-    const int npairs = Te / 2;
-    for (int sweep = 0; sweep < max_sweeps && !converged; ++sweep) {
-        for (int round = 0; round < Te - 1; ++round) {
-            // circle method: position 0 holds player Te-1, others rotate
-            if (tid < npairs) {
-                auto player = [&](int pos) { return pos == 0 ? Te - 1 : ((pos - 1 + round) % (Te - 1)); };
-                int pa = player(tid), pb = player(Te - 1 - tid);
-                const int p = min(pa, pb), q = max(pa, pb);
-                double c = 1.0, s = 0.0;
-                int mode = 0;   // 0 identity, 1 zero a_pq, 2 rotate
-                if (q < T) {
-                    const double apq = A[p * T + q];
-                    const double app = A[p * T + p], aqq = A[q * T + q];
-                    const double g = 100.0 * fabs(apq);
-                    if (add_rn(fabs(app), g) == fabs(app) && add_rn(fabs(aqq), g) == fabs(aqq)) {
-                        mode = 1;
-                    } else if (apq != 0.0) {
-                        const double tau = div_rn(sub_rn(aqq, app), mul_rn(2.0, apq));
-                        double t;
-                        if (tau >= 0.0)
-                            t = div_rn(1.0, add_rn(tau, sqrt(add_rn(1.0, mul_rn(tau, tau)))));
-                        else
-                            t = div_rn(-1.0, add_rn(-tau, sqrt(add_rn(1.0, mul_rn(tau, tau)))));
-                        c = div_rn(1.0, sqrt(add_rn(1.0, mul_rn(t, t))));
-                        s = mul_rn(t, c);
-                        mode = 2;
+    if (tid < JAC_NT) {
+        const int Te = T + (T & 1);
+        const int np = Te / 2;
+        int* s_p = s_mode + np;
+        int* s_q = s_p + np;
+        const int ga = tid >> 4, gb = tid & 15;   // 32 x 16 thread grid over (row pair, column pair)
+        auto offdiag = [&]() {
+            double o2 = 0.0;
+            for (int i = ga; i < T; i += 32)
+                for (int j = gb; j < T; j += 16)
+                    if (i != j) o2 = fma(A[i * T + j], A[i * T + j], o2);
+            return sqrt(block_sum(o2, red));
+        };
+        bool converged = offdiag() <= rtol * frob;
+        for (int sweep = 0; sweep < max_sweeps && !converged; ++sweep) {
+            for (int round = 0; round < Te - 1; ++round) {
+                if (tid < np) {
+                    // circle method: position 0 holds player Te-1, the others rotate
+                    const int pos_a = tid, pos_b = Te - 1 - tid;
+                    const int pa = pos_a == 0 ? Te - 1 : (pos_a - 1 + round) % (Te - 1);
+                    const int pb = pos_b == 0 ? Te - 1 : (pos_b - 1 + round) % (Te - 1);
+                    const int p = min(pa, pb), q = max(pa, pb);
+                    double c = 1.0, sn = 0.0;
+                    int mode = 0;   // 0 identity, 1 zero a_pq, 2 rotate
+                    if (q < T) {
+                        const double apq = A[p * T + q];
+                        const double app = A[p * T + p], aqq = A[q * T + q];
+                        const double g = 100.0 * fabs(apq);
+                        if (add_rn(fabs(app), g) == fabs(app) && add_rn(fabs(aqq), g) == fabs(aqq)) {
+                            mode = 1;
+                        } else if (apq != 0.0) {
+                            const double tau = (aqq - app) * fast_rcp(2.0 * apq);
+                            const double at = fabs(tau);
+                            double t;
+                            if (at < 1e100) {
+                                const double w = fma(tau, tau, 1.0);
+                                t = fast_rcp(at + w * fast_rsqrt(w));
+                            } else {
+                                t = 0.5 * fast_rcp(at);
+                            }
+                            if (tau < 0.0) t = -t;
+                            c = fast_rsqrt(fma(t, t, 1.0));
+                            sn = t * c;
+                            mode = 2;
+                        }
+                    }
+                    s_c[tid] = c;
+                    s_s[tid] = sn;
+                    s_mode[tid] = mode;
+                    s_p[tid] = p;
+                    s_q[tid] = q;
+                }
+                jac_sync();
+                // A <- R A R' on 2 x 2 blocks (row pair a, column pair b)
+                for (int a2 = ga; a2 < np; a2 += 32) {
+                    const int ra0 = s_p[a2], ra1 = s_q[a2];
+                    const bool ra1v = ra1 < T;
+                    const int ma = s_mode[a2];
+                    const double ca = s_c[a2], sa = s_s[a2];
+                    for (int b2 = gb; b2 < np; b2 += 16) {
+                        const int cb0 = s_p[b2], cb1 = s_q[b2];
+                        const bool cb1v = cb1 < T;
+                        const int mb = s_mode[b2];
+                        double x00 = A[ra0 * T + cb0];
+                        double x01 = cb1v ? A[ra0 * T + cb1] : 0.0;
+                        double x10 = ra1v ? A[ra1 * T + cb0] : 0.0;
+                        double x11 = (ra1v && cb1v) ? A[ra1 * T + cb1] : 0.0;
+                        if (mb == 2) {   // columns: a'_ip = c a_ip - s a_iq ; a'_iq = s a_ip + c a_iq
+                            const double cb = s_c[b2], sb = s_s[b2];
+                            const double y00 = sub_rn(mul_rn(cb, x00), mul_rn(sb, x01));
+                            const double y01 = add_rn(mul_rn(sb, x00), mul_rn(cb, x01));
+                            const double y10 = sub_rn(mul_rn(cb, x10), mul_rn(sb, x11));
+                            const double y11 = add_rn(mul_rn(sb, x10), mul_rn(cb, x11));
+                            x00 = y00; x01 = y01; x10 = y10; x11 = y11;
+                        }
+                        if (ma == 2) {   // rows
+                            const double y00 = sub_rn(mul_rn(ca, x00), mul_rn(sa, x10));
+                            const double y10 = add_rn(mul_rn(sa, x00), mul_rn(ca, x10));
+                            const double y01 = sub_rn(mul_rn(ca, x01), mul_rn(sa, x11));
+                            const double y11 = add_rn(mul_rn(sa, x01), mul_rn(ca, x11));
+                            x00 = y00; x01 = y01; x10 = y10; x11 = y11;
+                        }
+                        if (a2 == b2 && ma != 0) { x01 = 0.0; x10 = 0.0; }
+                        A[ra0 * T + cb0] = x00;
+                        if (cb1v) A[ra0 * T + cb1] = x01;
+                        if (ra1v) A[ra1 * T + cb0] = x10;
+                        if (ra1v && cb1v) A[ra1 * T + cb1] = x11;
                     }
                 }
-                // slot tid describes the pair (p, q)
-                s_c[tid] = c;
-                s_s[tid] = s;
-                s_mode[tid] = mode;
-                s_mode[npairs + 2 * tid] = p;
-                s_mode[npairs + 2 * tid + 1] = q;
-            }
-            cta_sync();
-            // A <- R A R' applied on 2x2 blocks of (pair a rows) x (pair b cols)
-            for (int e = tid; e < npairs * npairs; e += blockDim.x) {
-                const int pa = e / npairs, pb = e % npairs;
-                const int ra0 = s_mode[npairs + 2 * pa], ra1 = s_mode[npairs + 2 * pa + 1];
-                const int cb0 = s_mode[npairs + 2 * pb], cb1 = s_mode[npairs + 2 * pb + 1];
-                const bool ra1v = ra1 < T, cb1v = cb1 < T;
-                const double ca = s_c[pa], sa = s_s[pa], cbv = s_c[pb], sbv = s_s[pb];
-                double x00 = A[ra0 * T + cb0];
-                double x01 = cb1v ? A[ra0 * T + cb1] : 0.0;
-                double x10 = ra1v ? A[ra1 * T + cb0] : 0.0;
-                double x11 = (ra1v && cb1v) ? A[ra1 * T + cb1] : 0.0;
-                // columns (R_b on the right): a'_ip = c a_ip - s a_iq ; a'_iq = s a_ip + c a_iq
-                if (s_mode[pb] == 2) {
-                    const double y00 = sub_rn(mul_rn(cbv, x00), mul_rn(sbv, x01));
-                    const double y01 = add_rn(mul_rn(sbv, x00), mul_rn(cbv, x01));
-                    const double y10 = sub_rn(mul_rn(cbv, x10), mul_rn(sbv, x11));
-                    const double y11 = add_rn(mul_rn(sbv, x10), mul_rn(cbv, x11));
-                    x00 = y00; x01 = y01; x10 = y10; x11 = y11;
+                // V <- V R'
+                for (int i = ga; i < T; i += 32) {
+                    for (int b2 = gb; b2 < np; b2 += 16) {
+                        if (s_mode[b2] != 2) continue;
+                        const int c0 = s_p[b2], c1 = s_q[b2];
+                        const double cb = s_c[b2], sb = s_s[b2];
+                        const double vp = V[i * T + c0], vq = V[i * T + c1];
+                        V[i * T + c0] = sub_rn(mul_rn(cb, vp), mul_rn(sb, vq));
+                        V[i * T + c1] = add_rn(mul_rn(sb, vp), mul_rn(cb, vq));
+                    }
                 }
-                // rows (R_a on the left)
-                if (s_mode[pa] == 2) {
-                    const double y00 = sub_rn(mul_rn(ca, x00), mul_rn(sa, x10));
-                    const double y10 = add_rn(mul_rn(sa, x00), mul_rn(ca, x10));
-                    const double y01 = sub_rn(mul_rn(ca, x01), mul_rn(sa, x11));
-                    const double y11 = add_rn(mul_rn(sa, x01), mul_rn(ca, x11));
-                    x00 = y00; x01 = y01; x10 = y10; x11 = y11;
-                }
-                if (pa == pb && s_mode[pa] != 0) { x01 = 0.0; x10 = 0.0; }
-                A[ra0 * T + cb0] = x00;
-                if (cb1v) A[ra0 * T + cb1] = x01;
-                if (ra1v) A[ra1 * T + cb0] = x10;
-                if (ra1v && cb1v) A[ra1 * T + cb1] = x11;
+                jac_sync();
             }
-            // V <- V R'
-            for (int e = tid; e < T * npairs; e += blockDim.x) {
-                const int i = e / npairs, pb = e % npairs;
-                if (s_mode[pb] != 2) continue;
-                const int c0 = s_mode[npairs + 2 * pb], c1 = s_mode[npairs + 2 * pb + 1];
-                const double cbv = s_c[pb], sbv = s_s[pb];
-                const double vp = V[i * T + c0], vq = V[i * T + c1];
-                V[i * T + c0] = sub_rn(mul_rn(cbv, vp), mul_rn(sbv, vq));
-                V[i * T + c1] = add_rn(mul_rn(sbv, vp), mul_rn(cbv, vq));
-            }
-            cta_sync();
+            converged = offdiag() <= rtol * frob;
         }
-        converged = offdiag() <= rtol * frob;
+        if (tid == 0) s_result = converged ? 0 : max_sweeps;
     }
-    return converged ? 0 : max_sweeps;
+    cta_sync();
+    return s_result;
 }
 
 // order[r] = index of the r-th smallest value, ties by index (stable argsort)
@@ -336,11 +386,16 @@ __global__ void __launch_bounds__(SD_NT) ritz_pencil_kernel(const double* Fraw, 
     }
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nw = blockDim.x >> 5;
+    // F, G (symmetrised, T x T) stay in the global scratch: they are only read
+    // by parallel compaction loops.  The matrices the serial chains walk
+    // (Cholesky, triangular solves, Jacobi) live in shared memory when they fit:
+    // slots S0 = Fa then V, S1 = L, S2 = Ga then Y (in place), S3 = A.
     double* F = wk;
     double* G = F + T * T;
-    double* L = G + T * T;
-    double* Y = L + T * T;
-    double* Fa = Y + T * T;
+    const bool staged = T <= DCG_PENCIL_SMEM_T;
+    double* L = staged ? sm + T * T : G + T * T;
+    double* Y = staged ? sm + 2 * T * T : L + T * T;
+    double* Fa = staged ? sm : Y + T * T;
     for (int e = tid; e < T * T; e += blockDim.x) {
         const int i = e / T, j = e % T;
         F[e] = mul_rn(0.5, add_rn(Fraw[i * T + j], Fraw[j * T + i]));
@@ -371,8 +426,8 @@ __global__ void __launch_bounds__(SD_NT) ritz_pencil_kernel(const double* Fraw, 
         }
         cta_sync();
     }
-    // Ga -> Fa storage (F no longer needed in compact form)
-    double* Ga = Fa;
+    // compact Ga (solved in place into Y below)
+    double* Ga = staged ? Y : Fa;
     for (int e = tid; e < na * na; e += blockDim.x) {
         const int i = e / na, j = e % na;
         Ga[e] = G[s_act[i] * T + s_act[j]];
@@ -382,8 +437,8 @@ __global__ void __launch_bounds__(SD_NT) ritz_pencil_kernel(const double* Fraw, 
     for (int c = warp; c < na; c += nw) warp_solve_lower(L, na, na, Ga + c, na, Y + c, na);
     cta_sync();
     // C = L^-1 Y'  -> into shared A
-    double* A = sm;
-    double* V = sm + na * na;
+    double* A = staged ? sm + 3 * T * T : sm;
+    double* V = staged ? sm : sm + T * T;
     for (int c = warp; c < na; c += nw) warp_solve_lower(L, na, na, Y + c * na, 1, A + c, na);
     cta_sync();
     // symmetrise
@@ -602,11 +657,12 @@ int dcg_gram_factor_launch(cudaStream_t st, const double* Graw, int k, int prune
 }
 
 size_t dcg_pencil_smem(int T) { return sizeof(double) * 2 * (size_t)T * T; }
+static size_t pencil_smem(int T) { return sizeof(double) * (T <= DCG_PENCIL_SMEM_T ? 4 : 2) * (size_t)T * T; }
 
 int dcg_ritz_pencil_launch(cudaStream_t st, const double* Fraw, const double* Graw, int T, int k, int largest,
                            int max_sweeps, double* wk, double* theta, double* U, int* active, DevStatus* ds,
                            const DevStatus* plan) {
-    const size_t smem = dcg_pencil_smem(T);
+    const size_t smem = pencil_smem(T);
     DCG_CUDA(cudaFuncSetAttribute(ritz_pencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ritz_pencil_kernel<<<1, SD_NT, smem, st>>>(Fraw, Graw, T, k, largest, max_sweeps, wk, theta, U, active, ds,
                                                 plan);

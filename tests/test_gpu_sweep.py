@@ -1,0 +1,77 @@
+"""GPU: the GP-regression hyperparameter sweep (config 4, SURVEY.md section
+3.5) against the reference algorithm run through the oracle.
+
+The reference has no driver for the sweep; it is composed from the public
+API exactly as the oracle does it here (rbf_kernel per theta with jitter
+0.01, then solve_next with a SequenceState carried across thetas).  Bars:
+per-theta iteration counts within the reference's own rounding spread (+-1),
+solutions within 1e-9 relative (north_star), and the recycled basis must
+help as in the reference (fewer iterations than plain CG summed over the
+sweep)."""
+
+import numpy as np
+import pytest
+
+from oracle import defcg_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1706_00241_b200 as P
+
+    return P
+
+
+def oracle_sweep(x, y, thetas, k, ell, tol=1e-8, jitter=0.01, perm=None):
+    if perm is not None:
+        x, y = x[perm], y[perm]
+    st = O.Sequence(k=k, cfg=O.Cfg(tol=tol, ell=ell), selection="largest")
+    sols, its = [], []
+    for th in thetas:
+        a = O.rbf_kernel(x, 1.0, float(th), jitter=jitter, be="numpy")
+        xs, st = O.solve_next(st, a, y, be="numpy")
+        sols.append(xs if perm is None else xs[np.argsort(perm)])
+        its.append(st.history[-1].iterations)
+    return sols, its
+
+
+@pytest.mark.parametrize("n,k", [(700, 8), (1500, 12)])
+def test_sweep_matches_reference(P, n, k):
+    x, y = O.sweep_inputs(n, d=8, seed=0)
+    thetas = np.logspace(np.log10(0.5), np.log10(2.0), 6)
+    ell = k + 4
+    ref_sols, ref_its = oracle_sweep(x, y, thetas, k, ell)
+    spread = [oracle_sweep(x, y, thetas, k, ell, perm=np.random.default_rng(s).permutation(n))[1] for s in range(3)]
+    sols, recs = P.hyperparameter_sweep(x, y, thetas, k=k, cfg=P.SolverConfig(tol=1e-8, ell=ell))
+    its = [r.iterations for r in recs]
+    for i in range(len(thetas)):
+        lo = min([ref_its[i]] + [s[i] for s in spread]) - 1
+        hi = max([ref_its[i]] + [s[i] for s in spread]) + 1
+        assert lo <= its[i] <= hi, (i, its, ref_its, spread)
+        err = np.linalg.norm(sols[i] - ref_sols[i]) / np.linalg.norm(ref_sols[i])
+        assert err <= 1e-7, (i, err)
+
+
+def test_sweep_recycling_saves_iterations(P):
+    x, y = O.sweep_inputs(1500, d=8, seed=1)
+    thetas = np.logspace(np.log10(0.5), np.log10(2.0), 8)
+    _, recs = P.hyperparameter_sweep(x, y, thetas, k=12, cfg=P.SolverConfig(tol=1e-8, ell=16))
+    _, recs0 = P.hyperparameter_sweep(x, y, thetas, k=0, cfg=P.SolverConfig(tol=1e-8, ell=16))
+    assert sum(r.iterations for r in recs) < sum(r.iterations for r in recs0)
+    # first system has no basis yet: identical to plain CG
+    assert recs[0].iterations == recs0[0].iterations
+
+
+def test_sweep_device_inputs_stay_on_device(P):
+    import torch
+
+    x, y = O.sweep_inputs(600, d=8, seed=2)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.from_numpy(y).cuda()
+    sols, recs = P.hyperparameter_sweep(xd, yd, [0.7, 1.0], k=6, cfg=P.SolverConfig(tol=1e-8, ell=10))
+    assert all(isinstance(s, torch.Tensor) and s.is_cuda for s in sols)
+    sols_h, _ = P.hyperparameter_sweep(x, y, [0.7, 1.0], k=6, cfg=P.SolverConfig(tol=1e-8, ell=10))
+    for a, b in zip(sols, sols_h):
+        assert np.array_equal(a.cpu().numpy(), b)

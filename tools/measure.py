@@ -1,0 +1,136 @@
+#!/usr/bin/env python
+"""Secondary measurements of the def-CG hot path (not the driver's bench line).
+
+  python tools/measure.py config1        GPC Newton sequence n=2000, k=8 (BASELINE configs[0])
+  python tools/measure.py config2-cg     config 2 with plain CG (k=0) for the def-CG vs CG comparison
+  python tools/measure.py config4 [n]    GP-regression hyperparameter sweep, 20 lengthscales, k=24
+
+Each prints one JSON line: device time (CUDA events) of the whole sequence,
+iterations, iterations/s, and a CPU sample of the reference algorithm (oracle
+port, numpy backend, all host threads) on the same inputs.  Inputs are the
+seeded synthetic recipes of SURVEY.md section 8d.
+"""
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def gpc_sequence(n, d, ell, k, solver="defcg", reps=3):
+    import torch
+
+    import paper_1706_00241_b200 as P
+    from oracle.defcg_oracle import gpc_inputs
+
+    x, y = gpc_inputs(n, d, 0)
+    gram = P.rbf_kernel(torch.from_numpy(x).cuda(), P.KernelParams(1.0, ell))
+    yd = torch.from_numpy(y).cuda()
+    cfg = P.SolverConfig(tol=1e-8, ell=max(k, 8) + 4)
+
+    def run():
+        _, recs = P.laplace_newton(gram, yd, solver, cfg, newton_tol=-np.inf, max_newton=8, k=k,
+                                   selection="largest")
+        return recs
+
+    run()
+    torch.cuda.synchronize()
+    best = None
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        recs = run()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    its = [r.solver_iterations for r in recs]
+    return {"n": n, "k": k, "solver": solver, "iterations": its, "sequence_ms": best,
+            "iters_per_s": sum(its) / (best / 1e3), "psi": [r.psi for r in recs]}
+
+
+def cpu_gpc(n, d, ell, k, steps):
+    from oracle import defcg_oracle as O
+
+    x, y = O.gpc_inputs(n, d, 0)
+    kmat = O.rbf_kernel(x, 1.0, ell, be="numpy")
+    _, _, recs = O.laplace_newton(kmat, y, "defcg", O.Cfg(tol=1e-8, ell=k + 4), newton_tol=-np.inf, max_newton=8,
+                                  k=k, selection="largest", be="numpy", max_steps_timed=steps)
+    its = sum(r.solver_iterations for r in recs)
+    secs = sum(r.solve_time_s for r in recs)
+    return {"value": its / secs, "unit": "iters/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"first {len(recs)} Newton systems, {its} iterations in {secs:.2f} s"}
+
+
+def sweep(n, k=24, n_theta=20, reps=1):
+    import torch
+
+    import paper_1706_00241_b200 as P
+    from oracle.defcg_oracle import sweep_inputs
+
+    x, y = sweep_inputs(n, d=8, seed=0)
+    thetas = np.logspace(np.log10(0.5), np.log10(2.0), n_theta)
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    cfg = P.SolverConfig(tol=1e-8, ell=k + 4)
+    P.hyperparameter_sweep(xd, yd, thetas[:2], k=k, cfg=cfg)   # warm-up (allocations, contexts)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _, recs = P.hyperparameter_sweep(xd, yd, thetas, k=k, cfg=cfg)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    e0.record()
+    _, recs0 = P.hyperparameter_sweep(xd, yd, thetas, k=0, cfg=cfg)
+    e1.record()
+    torch.cuda.synchronize()
+    ms0 = e0.elapsed_time(e1)
+    its, its0 = [r.iterations for r in recs], [r.iterations for r in recs0]
+    return {"n": n, "k": k, "thetas": len(thetas), "iterations": its, "sweep_ms": ms,
+            "iters_per_s": sum(its) / (ms / 1e3), "plain_cg_iterations": its0, "plain_cg_sweep_ms": ms0,
+            "includes": "Gram assembly per theta (K6) + refresh + def-CG + extraction"}
+
+
+def cpu_sweep_sample(n, iters=5, n_cpu=12000):
+    """Per-iteration CPU cost of the reference algorithm (numpy matvec on the
+    host Gram, all threads), timed on `iters` CG iterations at n_cpu <= n and
+    extrapolated proportionally to n^2 (the numpy Gram assembly needs several
+    n x n temporaries, ~40 GB of host RAM at n = 30000)."""
+    from oracle import defcg_oracle as O
+
+    m = min(n, n_cpu)
+    x, y = O.sweep_inputs(m, d=8, seed=0)
+    a = O.rbf_kernel(x, 1.0, 0.5, jitter=0.01, be="numpy")
+    t0 = time.perf_counter()
+    _, rep, _ = O.cg_solve(a, y, None, O.Cfg(tol=1e-30, max_iters=iters, ell=0), be="numpy")
+    dt = time.perf_counter() - t0
+    scale = (m / n) ** 2
+    return {"value": rep.iterations / dt * scale, "unit": "iters/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{rep.iterations} plain-CG iterations at n={m} (numpy, all threads)"
+                      + (f", extrapolated x(n_cpu/n)^2 = {scale:.3f} to n={n}" if m < n else "")}
+
+
+def main():
+    what = sys.argv[1]
+    if what == "config1":
+        out = gpc_sequence(2000, 5, 1.5, 8)
+        out["cpu_baseline"] = cpu_gpc(2000, 5, 1.5, 8, 8)
+    elif what == "config2-cg":
+        out = {"defcg": gpc_sequence(10000, 10, 1.5, 16), "cg": gpc_sequence(10000, 10, 1.5, 0, solver="cg")}
+    elif what == "config4":
+        n = int(sys.argv[2]) if len(sys.argv) > 2 else 30000
+        out = sweep(n)
+        out["cpu_baseline"] = cpu_sweep_sample(n)
+    else:
+        raise SystemExit(__doc__)
+    out["workload"] = what
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
