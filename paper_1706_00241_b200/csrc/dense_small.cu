@@ -185,14 +185,18 @@ __device__ int cta_jacobi(double* A, double* V, int T, int max_sweeps, double rt
     if (tid < JAC_NT) {
         const int Te = T + (T & 1);
         const int np = Te / 2;
-        int* s_p = s_mode + np;
-        int* s_q = s_p + np;
-        const int ga = tid >> 4, gb = tid & 15;   // 32 x 16 thread grid over (row pair, column pair)
+        // per-round pair table: (p, q, mode) and (c, s), one 16-byte record each
+        __shared__ int4 s_pi[DCG_MAX_T / 2 + 1];
+        __shared__ double2 s_cs[DCG_MAX_T / 2 + 1];
+        // fixed work assignment for the whole solve: block (ba, bb) of the
+        // np x np grid of 2 x 2 blocks, and V entries (row vi, pair vb)
+        const int nblk = np * np;
         auto offdiag = [&]() {
             double o2 = 0.0;
-            for (int i = ga; i < T; i += 32)
-                for (int j = gb; j < T; j += 16)
-                    if (i != j) o2 = fma(A[i * T + j], A[i * T + j], o2);
+            for (int e = tid; e < T * T; e += JAC_NT) {
+                const int i = e / T, j = e - (e / T) * T;
+                if (i != j) o2 = fma(A[e], A[e], o2);
+            }
             return sqrt(block_sum(o2, red));
         };
         bool converged = offdiag() <= rtol * frob;
@@ -200,9 +204,11 @@ __device__ int cta_jacobi(double* A, double* V, int T, int max_sweeps, double rt
             for (int round = 0; round < Te - 1; ++round) {
                 if (tid < np) {
                     // circle method: position 0 holds player Te-1, the others rotate
-                    const int pos_a = tid, pos_b = Te - 1 - tid;
-                    const int pa = pos_a == 0 ? Te - 1 : (pos_a - 1 + round) % (Te - 1);
-                    const int pb = pos_b == 0 ? Te - 1 : (pos_b - 1 + round) % (Te - 1);
+                    const int pos_b = Te - 1 - tid;
+                    int pa = tid == 0 ? Te - 1 : tid - 1 + round;
+                    if (tid != 0 && pa >= Te - 1) pa -= Te - 1;
+                    int pb = pos_b - 1 + round;
+                    if (pb >= Te - 1) pb -= Te - 1;
                     const int p = min(pa, pb), q = max(pa, pb);
                     double c = 1.0, sn = 0.0;
                     int mode = 0;   // 0 identity, 1 zero a_pq, 2 rotate
@@ -228,59 +234,49 @@ __device__ int cta_jacobi(double* A, double* V, int T, int max_sweeps, double rt
                             mode = 2;
                         }
                     }
-                    s_c[tid] = c;
-                    s_s[tid] = sn;
-                    s_mode[tid] = mode;
-                    s_p[tid] = p;
-                    s_q[tid] = q;
+                    s_pi[tid] = make_int4(p, q, mode, 0);
+                    s_cs[tid] = make_double2(c, sn);
                 }
                 jac_sync();
-                // A <- R A R' on 2 x 2 blocks (row pair a, column pair b)
-                for (int a2 = ga; a2 < np; a2 += 32) {
-                    const int ra0 = s_p[a2], ra1 = s_q[a2];
-                    const bool ra1v = ra1 < T;
-                    const int ma = s_mode[a2];
-                    const double ca = s_c[a2], sa = s_s[a2];
-                    for (int b2 = gb; b2 < np; b2 += 16) {
-                        const int cb0 = s_p[b2], cb1 = s_q[b2];
-                        const bool cb1v = cb1 < T;
-                        const int mb = s_mode[b2];
-                        double x00 = A[ra0 * T + cb0];
-                        double x01 = cb1v ? A[ra0 * T + cb1] : 0.0;
-                        double x10 = ra1v ? A[ra1 * T + cb0] : 0.0;
-                        double x11 = (ra1v && cb1v) ? A[ra1 * T + cb1] : 0.0;
-                        if (mb == 2) {   // columns: a'_ip = c a_ip - s a_iq ; a'_iq = s a_ip + c a_iq
-                            const double cb = s_c[b2], sb = s_s[b2];
-                            const double y00 = sub_rn(mul_rn(cb, x00), mul_rn(sb, x01));
-                            const double y01 = add_rn(mul_rn(sb, x00), mul_rn(cb, x01));
-                            const double y10 = sub_rn(mul_rn(cb, x10), mul_rn(sb, x11));
-                            const double y11 = add_rn(mul_rn(sb, x10), mul_rn(cb, x11));
-                            x00 = y00; x01 = y01; x10 = y10; x11 = y11;
-                        }
-                        if (ma == 2) {   // rows
-                            const double y00 = sub_rn(mul_rn(ca, x00), mul_rn(sa, x10));
-                            const double y10 = add_rn(mul_rn(sa, x00), mul_rn(ca, x10));
-                            const double y01 = sub_rn(mul_rn(ca, x01), mul_rn(sa, x11));
-                            const double y11 = add_rn(mul_rn(sa, x01), mul_rn(ca, x11));
-                            x00 = y00; x01 = y01; x10 = y10; x11 = y11;
-                        }
-                        if (a2 == b2 && ma != 0) { x01 = 0.0; x10 = 0.0; }
-                        A[ra0 * T + cb0] = x00;
-                        if (cb1v) A[ra0 * T + cb1] = x01;
-                        if (ra1v) A[ra1 * T + cb0] = x10;
-                        if (ra1v && cb1v) A[ra1 * T + cb1] = x11;
+                // A <- R A R' on the 2 x 2 block (row pair ba, column pair bb)
+                for (int blk = tid; blk < nblk; blk += JAC_NT) {
+                    const int ba = blk / np, bb = blk - (blk / np) * np;
+                    const int4 ia = s_pi[ba], ib = s_pi[bb];
+                    const double2 ra = s_cs[ba], rb = s_cs[bb];
+                    const bool ra1v = ia.y < T, cb1v = ib.y < T;
+                    double x00 = A[ia.x * T + ib.x];
+                    double x01 = cb1v ? A[ia.x * T + ib.y] : 0.0;
+                    double x10 = ra1v ? A[ia.y * T + ib.x] : 0.0;
+                    double x11 = (ra1v && cb1v) ? A[ia.y * T + ib.y] : 0.0;
+                    if (ib.z == 2) {   // columns: a'_ip = c a_ip - s a_iq ; a'_iq = s a_ip + c a_iq
+                        const double y00 = sub_rn(mul_rn(rb.x, x00), mul_rn(rb.y, x01));
+                        const double y01 = add_rn(mul_rn(rb.y, x00), mul_rn(rb.x, x01));
+                        const double y10 = sub_rn(mul_rn(rb.x, x10), mul_rn(rb.y, x11));
+                        const double y11 = add_rn(mul_rn(rb.y, x10), mul_rn(rb.x, x11));
+                        x00 = y00; x01 = y01; x10 = y10; x11 = y11;
                     }
+                    if (ia.z == 2) {   // rows
+                        const double y00 = sub_rn(mul_rn(ra.x, x00), mul_rn(ra.y, x10));
+                        const double y10 = add_rn(mul_rn(ra.y, x00), mul_rn(ra.x, x10));
+                        const double y01 = sub_rn(mul_rn(ra.x, x01), mul_rn(ra.y, x11));
+                        const double y11 = add_rn(mul_rn(ra.y, x01), mul_rn(ra.x, x11));
+                        x00 = y00; x01 = y01; x10 = y10; x11 = y11;
+                    }
+                    if (ba == bb && ia.z != 0) { x01 = 0.0; x10 = 0.0; }
+                    A[ia.x * T + ib.x] = x00;
+                    if (cb1v) A[ia.x * T + ib.y] = x01;
+                    if (ra1v) A[ia.y * T + ib.x] = x10;
+                    if (ra1v && cb1v) A[ia.y * T + ib.y] = x11;
                 }
-                // V <- V R'
-                for (int i = ga; i < T; i += 32) {
-                    for (int b2 = gb; b2 < np; b2 += 16) {
-                        if (s_mode[b2] != 2) continue;
-                        const int c0 = s_p[b2], c1 = s_q[b2];
-                        const double cb = s_c[b2], sb = s_s[b2];
-                        const double vp = V[i * T + c0], vq = V[i * T + c1];
-                        V[i * T + c0] = sub_rn(mul_rn(cb, vp), mul_rn(sb, vq));
-                        V[i * T + c1] = add_rn(mul_rn(sb, vp), mul_rn(cb, vq));
-                    }
+                // V <- V R' (row vi, pair vb)
+                for (int e = tid; e < T * np; e += JAC_NT) {
+                    const int vi = e / np, vb = e - (e / np) * np;
+                    const int4 ib = s_pi[vb];
+                    if (ib.z != 2) continue;
+                    const double2 rb = s_cs[vb];
+                    const double vp = V[vi * T + ib.x], vq = V[vi * T + ib.y];
+                    V[vi * T + ib.x] = sub_rn(mul_rn(rb.x, vp), mul_rn(rb.y, vq));
+                    V[vi * T + ib.y] = add_rn(mul_rn(rb.y, vp), mul_rn(rb.x, vq));
                 }
                 jac_sync();
             }
