@@ -245,6 +245,78 @@ DCG_API int dcg_gpc_newton_update(dcg_context* ctx, void* stream, const dcg_oper
                           const double* d_y, double* d_a, double* d_f, double* d_grad,
                           double* d_h, double* loglik, double* psi);
 
+/* ---- L5: row-sharded def-CG ------------------------------ *
+ * K is row-partitioned over R ranks (one process per GPU); a rank owns the
+ * slab rows [row0, row0 + rows) of K (op->kind = DCG_OP_DENSE, op->d_k = its
+ * first row) and the same rows of x, r, p, Ap, W, AW.  The iteration of
+ * solvers.py:131-204 becomes, per rank (collectives by the caller, e.g. NCCL):
+ *     all-gather p -> dcg_shard_apply_dot -> all-reduce(1)
+ *     -> dcg_shard_update -> all-reduce(1 + k) -> dcg_shard_direction
+ * Scalars never leave the device: every kernel reads a dcg_shard_state at
+ * entry and only the last CTA to finish writes it, so a kernel enqueued after
+ * convergence (done != 0) is a no-op and every rank enqueues the same
+ * collectives.  Reductions are fixed-order; with the all-reduced inputs being
+ * bit-identical on all ranks, every rank takes the same decisions.          */
+typedef struct dcg_shard_state {
+    double rr;            /* r'r of the current residual (global)              */
+    double norm_b;        /* ||b||                                             */
+    double rel;           /* sqrt(rr) / norm_b                                 */
+    double alpha, beta, d;
+    double tol;
+    long long it;         /* completed iterations                              */
+    long long max_iters;
+    long long done;       /* 1: converged / max_iters / breakdown / zero rhs   */
+    long long status;     /* DCG_OK or DCG_E_BREAKDOWN                         */
+    long long info;       /* breakdown iteration                               */
+    long long ell;        /* KrylovLog capacity                                */
+    long long pad[3];
+} dcg_shard_state;
+
+/* out = A_rows v (v: all n entries) for this rank's rows; part[0] = sum over
+ * the rank's rows of v_i out_i (p'Ap partial) when part != NULL.  No-op if
+ * state != NULL and state->done.                                              */
+DCG_API int dcg_shard_apply_dot(dcg_context* ctx, void* stream, const dcg_operator* op,
+                                const double* d_v, double* d_out, double* d_part,
+                                const dcg_shard_state* d_state);
+/* r = b - A_rows v (v full): r_prev (warm start), r_0, and the true-residual
+ * refresh (solvers.py:175-177; no-op if state != NULL and state->done).      */
+DCG_API int dcg_shard_residual(dcg_context* ctx, void* stream, const dcg_operator* op,
+                               const double* d_v, const double* d_b, double* d_r,
+                               const dcg_shard_state* d_state);
+/* part = [u'u, M' w] over the rank's rows (M: rows x k row-major; k may be 0). */
+DCG_API int dcg_shard_partials(dcg_context* ctx, void* stream, long long rows, int k,
+                               const double* d_u, const double* d_w, const double* d_m,
+                               double* d_part);
+/* Warm start (deflated_cg_solve, solvers.py:236-238) from the reduced
+ * [b'b, W' r_prev]: x0 = x_prev + W chol_solve(L, W'r_prev); initialises the
+ * state (norm_b, tol, max_iters, ell, it = 0).  k = 0: x0 = x_prev.           */
+DCG_API int dcg_shard_start(dcg_context* ctx, void* stream, long long rows, int k,
+                            const double* d_red, const double* d_chol, const double* d_w,
+                            const double* d_xprev, double* d_x0, dcg_shard_state* d_state,
+                            double tol, long long max_iters, long long ell);
+/* From the reduced [r0'r0, AW' r0]: mu_0, p_0 = r_0 - W mu_0 (or r_0), rel_0,
+ * history[0], log r_0 / p_0 / mu_0, done; zero rhs -> x = 0 (solvers.py:142-147). */
+DCG_API int dcg_shard_begin(dcg_context* ctx, void* stream, long long rows, int k,
+                            const double* d_red, const double* d_chol, const double* d_w,
+                            const double* d_r, double* d_p, double* d_x, dcg_shard_state* d_state,
+                            double* d_history, double* d_log_r, double* d_log_p, double* d_log_mu);
+/* mode 0: alpha = rr / d (d = reduced p'Ap; d <= 0 -> breakdown); x += alpha p;
+ *         r -= alpha Ap; part = [r'r, AW' r]; logs d, alpha, r_it.
+ * mode 1 (true-residual iteration): only the alpha / x / it / d, alpha part;
+ * mode 2 (after dcg_shard_residual): only part = [r'r, AW' r] and the r_it log. */
+DCG_API int dcg_shard_update(dcg_context* ctx, void* stream, int mode, long long rows, int k,
+                             const double* d_red_d, double* d_x, double* d_r, const double* d_p,
+                             const double* d_ap, const double* d_aw, double* d_part,
+                             dcg_shard_state* d_state, double* d_log_r, double* d_log_d,
+                             double* d_log_alpha, double* d_log_beta);
+/* beta = rr'/rr, mu = chol_solve(L, AW'r), p = beta p + r - W mu (k > 0) or
+ * r + beta p; rel, history[it], logs p_it / mu_it; done.                       */
+DCG_API int dcg_shard_direction(dcg_context* ctx, void* stream, long long rows, int k,
+                                const double* d_red, const double* d_chol, const double* d_w,
+                                const double* d_r, double* d_p, dcg_shard_state* d_state,
+                                double* d_history, double* d_log_p, double* d_log_mu,
+                                double* d_log_beta);
+
 #ifdef __cplusplus
 }
 #endif

@@ -175,7 +175,20 @@ SIGNATURES = {
     "dcg_gpc_derivs": [_P, _P, _LL, _P, _P, _P, _P, _PD],
     "dcg_gpc_newton_system": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P, _P, _P],
     "dcg_gpc_newton_update": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P, _P, _P, _P, _P, _PD, _PD],
+    # row-sharded def-CG (include/defcg_b200.h L5)
+    "dcg_shard_apply_dot": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P],
+    "dcg_shard_residual": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P],
+    "dcg_shard_partials": [_P, _P, _LL, ctypes.c_int, _P, _P, _P, _P],
+    "dcg_shard_start": [_P, _P, _LL, ctypes.c_int, _P, _P, _P, _P, _P, _P, _D, _LL, _LL],
+    "dcg_shard_begin": [_P, _P, _LL, ctypes.c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "dcg_shard_update": [_P, _P, ctypes.c_int, _LL, ctypes.c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "dcg_shard_direction": [_P, _P, _LL, ctypes.c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
 }
+
+# dcg_shard_state (include/defcg_b200.h): 7 doubles then 9 int64, 128 bytes
+SHARD_STATE_DOUBLES = 16
+SHARD_RR, SHARD_NORM_B, SHARD_REL, SHARD_ALPHA, SHARD_BETA, SHARD_D, SHARD_TOL = range(7)
+SHARD_IT, SHARD_MAX_ITERS, SHARD_DONE, SHARD_STATUS, SHARD_INFO, SHARD_ELL = range(7, 13)
 
 _lib = None
 _lock = threading.Lock()

@@ -1,0 +1,486 @@
+// Row-sharded def-CG building blocks (include/defcg_b200.h L5).
+//
+// One process per GPU owns a contiguous slab of K's rows and the same rows of
+// every n-vector.  The iteration of _run_loop (solvers.py:131-204) is split at
+// its two reductions; the caller runs the collectives (all-gather of p,
+// all-reduce of the p'Ap partial, all-reduce of [r'r, AW'r]) between these
+// kernels.  Scalars live in a device-resident dcg_shard_state: every kernel
+// reads it at entry, and only the last CTA to arrive (after every CTA has read
+// it) writes it, so kernels enqueued after convergence are no-ops and ranks
+// never diverge.  All reductions are fixed-order.
+#include "common.cuh"
+#include "gemv.cuh"
+
+#define SH_NT 512
+
+namespace {
+
+int shard_grid(const dcg_context* ctx, long long rows) {
+    long long g = (rows + SH_NT - 1) / SH_NT;
+    if (g > ctx->sm_count) g = ctx->sm_count;
+    return g < 1 ? 1 : (int)g;
+}
+int slot_stride(int k) { return ((1 + k) + 1) & ~1; }
+
+// workspace: G x ps CTA partials + a 16-byte arrival counter (zero between uses)
+struct ShardWs {
+    double* parts;
+    unsigned int* counter;
+};
+int shard_ws(dcg_context* ctx, cudaStream_t st, int G, int ps, ShardWs* w) {
+    const size_t bytes = al(sizeof(double) * (size_t)G * ps) + 256;
+    int rc = dcg_ws_reserve(ctx, bytes);
+    if (rc) return rc;
+    char* base = static_cast<char*>(ctx->ws);
+    w->parts = reinterpret_cast<double*>(base);
+    w->counter = reinterpret_cast<unsigned int*>(base + al(sizeof(double) * (size_t)G * ps));
+    // the workspace is shared with the other entry points: start from zero
+    DCG_CUDA(cudaMemsetAsync(w->counter, 0, 16, st));
+    return DCG_OK;
+}
+
+// Per-CTA partials over rows [r0, r1): slot 0 = sum_i u_i^2 (thread per row),
+// slot 1 + j = sum_i M[i][j] w_i ((row group, j) threads, coalesced rows of M).
+// Result in out[0..k] (shared), all threads call.
+__device__ void cta_row_partials(long long r0, long long r1, int k, const double* u, const double* w,
+                                 const double* M, double* out, double* s_scr, double* s_tmp) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double sq = 0.0;
+    if (u)
+        for (long long i = r0 + tid; i < r1; i += SH_NT) sq = add_rn(sq, mul_rn(u[i], u[i]));
+    int swk = 1;
+    while (swk < k) swk <<= 1;
+    double c = 0.0;
+    if (k > 0) {
+        const int j = tid & (swk - 1), grp = tid / swk, ngrp = SH_NT / swk;
+        if (j < k)
+            for (long long i = r0 + grp; i < r1; i += ngrp) c = fma(M[i * k + j], w[i], c);
+        if (swk < 32)
+            for (int o = swk; o < 32; o <<= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    sq = warp_sum(sq);
+    if (lane == 0) s_tmp[warp] = sq;
+    if (k > 0) {
+        if (swk <= 32) {
+            if (lane < swk) s_scr[warp * 32 + lane] = c;
+        } else {
+            s_scr[tid] = c;
+        }
+    }
+    cta_sync();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int q = 0; q < SH_NT / 32; ++q) t += s_tmp[q];
+        out[0] = t;
+    }
+    if (tid < k) {
+        double t = 0.0;
+        if (swk <= 32) {
+            for (int q = 0; q < SH_NT / 32; ++q) t += s_scr[q * 32 + tid];
+        } else {
+            for (int g = 0; g < SH_NT / swk; ++g) t += s_scr[g * swk + tid];
+        }
+        out[1 + tid] = t;
+    }
+    cta_sync();
+}
+
+// Publish this CTA's nslots values, then the last CTA to arrive sums all CTAs'
+// values in CTA order into out[0..nslots).  Returns true on the last CTA.
+__device__ bool grid_reduce_slots(const double* mine, int nslots, double* parts, int ps, unsigned int* counter,
+                                  double* out) {
+    for (int v = threadIdx.x; v < nslots; v += blockDim.x) parts[(long long)blockIdx.x * ps + v] = mine[v];
+    const bool last = cta_last_arrival(counter, gridDim.x);
+    if (last) {
+        for (int v = threadIdx.x; v < nslots; v += blockDim.x) {
+            double t = 0.0;
+            for (int b = 0; b < (int)gridDim.x; ++b) t += ld_cg(parts + (long long)b * ps + v);
+            out[v] = t;
+        }
+    }
+    return last;
+}
+
+// mu = L^-T L^-1 c by warp 0 (forward substitution in the reference order,
+// backward sweep as a wavefront), then a CTA barrier.  L in shared memory.
+__device__ void cta_chol_solve(const double* L, int k, const double* c, double* mu) {
+    if ((threadIdx.x >> 5) == 0) {
+        const int lane = threadIdx.x & 31;
+        const int i0 = lane, i1 = lane + 32;
+        double a0 = (i0 < k) ? c[i0] : 0.0;
+        double a1 = (i1 < k) ? c[i1] : 0.0;
+        for (int j = 0; j < k; ++j) {
+            const double accj = __shfl_sync(0xffffffffu, (j < 32) ? a0 : a1, j & 31);
+            const double yj = div_rn(accj, L[j * k + j]);
+            if (lane == (j & 31)) {
+                if (j < 32) a0 = yj; else a1 = yj;
+            }
+            if (i0 > j && i0 < k) a0 = sub_rn(a0, mul_rn(L[i0 * k + j], yj));
+            if (i1 > j && i1 < k) a1 = sub_rn(a1, mul_rn(L[i1 * k + j], yj));
+        }
+        for (int j = k - 1; j >= 0; --j) {
+            const double accj = __shfl_sync(0xffffffffu, (j < 32) ? a0 : a1, j & 31);
+            const double xj = div_rn(accj, L[j * k + j]);
+            if (lane == (j & 31)) {
+                if (j < 32) a0 = xj; else a1 = xj;
+            }
+            if (i0 < j) a0 = sub_rn(a0, mul_rn(L[j * k + i0], xj));
+            if (i1 < j && i1 < k) a1 = sub_rn(a1, mul_rn(L[j * k + i1], xj));
+        }
+        if (i0 < k) mu[i0] = a0;
+        if (i1 < k) mu[i1] = a1;
+    }
+    cta_sync();
+}
+
+__device__ __forceinline__ double row_dot(const double* M, long long i, int k, const double* v) {
+    double t = 0.0;
+    for (int j = 0; j < k; ++j) t = fma(M[i * k + j], v[j], t);
+    return t;
+}
+
+// ---- GEMV over the slab with two epilogues --------------------------------
+// mode 0: out_i = (A v)_i and a p'Ap partial; mode 1: out_i = b_i - (A v)_i.
+__global__ void __launch_bounds__(DCG_NT, 1)
+    shard_gemv_kernel(int mode, const double* __restrict__ K, long long ldk, long long n, long long rows,
+                      long long row0, const double* v, const double* s, double shift, const double* b, double* out,
+                      double* part, double* parts, int ps, unsigned int* counter, const dcg_shard_state* state) {
+    extern __shared__ __align__(16) double smem[];
+    if (state && state->done) return;
+    const long long r0 = part_begin(rows, gridDim.x, blockIdx.x), r1 = part_begin(rows, gridDim.x, blockIdx.x + 1);
+    const int xt = (int)min(n, (long long)DCG_QT) + 2;
+    double* s_x = smem;
+    double* s_red = smem + xt;
+    __shared__ double s_tmp[40];
+    __shared__ double s_out[2];
+    double dot = 0.0;
+    block_gemv<true>(K, ldk, n, v, s, r0, r1, s_x, s_red, [&](long long i, double t) {
+        const long long g = row0 + i;
+        const double vi = ld_cg(v + g);
+        const double ax = s ? add_rn(mul_rn(shift, vi), mul_rn(s[g], t)) : add_rn(mul_rn(shift, vi), t);
+        if (mode == 0) {
+            out[i] = ax;
+            dot = fma(vi, ax, dot);
+        } else {
+            out[i] = sub_rn(b[i], ax);
+        }
+    });
+    if (mode == 0 && part) {
+        dot = block_sum(dot, s_tmp);
+        if (threadIdx.x == 0) s_out[0] = dot;
+        cta_sync();
+        grid_reduce_slots(s_out, 1, parts, ps, counter, part);
+    }
+}
+
+size_t shard_gemv_smem(long long n) { return sizeof(double) * ((size_t)min(n, (long long)DCG_QT) + 2 + DCG_NW * DCG_RB); }
+
+__global__ void __launch_bounds__(SH_NT)
+    shard_partials_kernel(long long rows, int k, const double* u, const double* w, const double* M, double* part,
+                          double* parts, int ps, unsigned int* counter) {
+    __shared__ double s_scr[SH_NT];
+    __shared__ double s_tmp[40];
+    __shared__ double s_out[DCG_MAX_K + 2];
+    const long long r0 = part_begin(rows, gridDim.x, blockIdx.x), r1 = part_begin(rows, gridDim.x, blockIdx.x + 1);
+    cta_row_partials(r0, r1, k, u, w, M, s_out, s_scr, s_tmp);
+    grid_reduce_slots(s_out, 1 + k, parts, ps, counter, part);
+}
+
+__global__ void __launch_bounds__(SH_NT)
+    shard_start_kernel(long long rows, int k, const double* red, const double* Lg, const double* W,
+                       const double* xprev, double* x0, dcg_shard_state* state, double tol, long long max_iters,
+                       long long ell) {
+    __shared__ double s_L[DCG_MAX_K * DCG_MAX_K];
+    __shared__ double s_y[DCG_MAX_K];
+    const long long r0 = part_begin(rows, gridDim.x, blockIdx.x), r1 = part_begin(rows, gridDim.x, blockIdx.x + 1);
+    if (k > 0) {
+        for (int e = threadIdx.x; e < k * k; e += blockDim.x) s_L[e] = Lg[e];
+        cta_sync();
+        cta_chol_solve(s_L, k, red + 1, s_y);
+    }
+    for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x)
+        x0[i] = k > 0 ? add_rn(xprev[i], row_dot(W, i, k, s_y)) : xprev[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        state->rr = 0.0;
+        state->norm_b = sqrt(red[0]);
+        state->rel = 0.0;
+        state->alpha = state->beta = state->d = 0.0;
+        state->tol = tol;
+        state->it = 0;
+        state->max_iters = max_iters;
+        state->done = 0;
+        state->status = DCG_OK;
+        state->info = 0;
+        state->ell = ell;
+    }
+}
+
+__global__ void __launch_bounds__(SH_NT)
+    shard_begin_kernel(long long rows, int k, const double* red, const double* Lg, const double* W, const double* r,
+                       double* p, double* x, dcg_shard_state* state, double* history, double* log_r, double* log_p,
+                       double* log_mu, unsigned int* counter) {
+    __shared__ double s_L[DCG_MAX_K * DCG_MAX_K];
+    __shared__ double s_mu[DCG_MAX_K];
+    const long long r0 = part_begin(rows, gridDim.x, blockIdx.x), r1 = part_begin(rows, gridDim.x, blockIdx.x + 1);
+    const double norm_b = state->norm_b;
+    const long long ell = state->ell, max_iters = state->max_iters;
+    const double tol = state->tol;
+    const double rr = red[0];
+    bool zero = norm_b == 0.0;
+    const double rel = zero ? 0.0 : sqrt(rr) / norm_b;
+    const bool cont = !zero && rel > tol && 0 < max_iters;
+    if (zero) {
+        // solvers.py:142-147: x = zeros (not x0), history [0.0], log.r = [zeros]
+        for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+            x[i] = 0.0;
+            if (log_r) log_r[i] = 0.0;
+        }
+    } else {
+        if (k > 0) {
+            for (int e = threadIdx.x; e < k * k; e += blockDim.x) s_L[e] = Lg[e];
+            cta_sync();
+            cta_chol_solve(s_L, k, red + 1, s_mu);
+        }
+        for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+            const double ri = r[i];
+            const double pi = k > 0 ? sub_rn(ri, row_dot(W, i, k, s_mu)) : ri;
+            p[i] = pi;
+            if (log_r) log_r[i] = ri;
+            if (cont && ell > 0 && log_p) log_p[i] = pi;
+        }
+    }
+    if (cta_last_arrival(counter, gridDim.x) && threadIdx.x == 0) {
+        state->rr = rr;
+        state->rel = rel;
+        state->done = cont ? 0 : 1;
+        history[0] = rel;
+        if (cont && ell > 0 && k > 0 && log_mu)
+            for (int j = 0; j < k; ++j) log_mu[j] = s_mu[j];
+    }
+}
+
+__global__ void __launch_bounds__(SH_NT)
+    shard_update_kernel(int mode, long long rows, int k, const double* red_d, double* x, double* r, const double* p,
+                        const double* ap, const double* AW, double* part, dcg_shard_state* state, double* log_r,
+                        double* log_d, double* log_alpha, double* parts, int ps, unsigned int* counter) {
+    __shared__ double s_scr[SH_NT];
+    __shared__ double s_tmp[40];
+    __shared__ double s_out[DCG_MAX_K + 2];
+    if (state->done) return;
+    const long long r0 = part_begin(rows, gridDim.x, blockIdx.x), r1 = part_begin(rows, gridDim.x, blockIdx.x + 1);
+    const long long it = state->it, ell = state->ell;
+    const long long n_loc = rows;
+    if (mode != 2) {
+        const double d = red_d[0];
+        if (!(d > 0.0) && !(d != d)) {   // solvers.py:170-172: d <= 0 (NaN falls through, as in numpy)
+            if (cta_last_arrival(counter, gridDim.x) && threadIdx.x == 0) {
+                state->status = DCG_E_BREAKDOWN;
+                state->info = it;
+                state->done = 1;
+            }
+            return;
+        }
+        const double alpha = state->rr / d;
+        for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+            x[i] = add_rn(x[i], mul_rn(alpha, p[i]));
+            if (mode == 0) r[i] = sub_rn(r[i], mul_rn(alpha, ap[i]));
+        }
+        if (mode == 1) {
+            if (cta_last_arrival(counter, gridDim.x) && threadIdx.x == 0) {
+                state->alpha = alpha;
+                state->d = d;
+                state->it = it + 1;
+                if (it < ell) {
+                    log_d[it] = d;
+                    log_alpha[it] = alpha;
+                }
+            }
+            return;
+        }
+        cta_sync();
+        const bool log = log_r && it < ell;   // (it + 1) - 1 < ell
+        if (log)
+            for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) log_r[(it + 1) * n_loc + i] = r[i];
+        cta_row_partials(r0, r1, k, r, r, AW, s_out, s_scr, s_tmp);
+        if (grid_reduce_slots(s_out, 1 + k, parts, ps, counter, part) && threadIdx.x == 0) {
+            state->alpha = alpha;
+            state->d = d;
+            state->it = it + 1;
+            if (it < ell) {
+                log_d[it] = d;
+                log_alpha[it] = alpha;
+            }
+        }
+        return;
+    }
+    // mode 2: r was recomputed as b - A x; `it` already counts this iteration
+    const bool log = log_r && (it - 1) < ell;
+    if (log)
+        for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) log_r[it * n_loc + i] = r[i];
+    cta_row_partials(r0, r1, k, r, r, AW, s_out, s_scr, s_tmp);
+    grid_reduce_slots(s_out, 1 + k, parts, ps, counter, part);
+}
+
+__global__ void __launch_bounds__(SH_NT)
+    shard_direction_kernel(long long rows, int k, const double* red, const double* Lg, const double* W,
+                           const double* r, double* p, dcg_shard_state* state, double* history, double* log_p,
+                           double* log_mu, double* log_beta, unsigned int* counter) {
+    __shared__ double s_L[DCG_MAX_K * DCG_MAX_K];
+    __shared__ double s_mu[DCG_MAX_K];
+    if (state->done) return;
+    const long long r0 = part_begin(rows, gridDim.x, blockIdx.x), r1 = part_begin(rows, gridDim.x, blockIdx.x + 1);
+    const long long it = state->it, ell = state->ell, max_iters = state->max_iters;
+    const double rr_new = red[0];
+    const double beta = rr_new / state->rr;
+    const double rel = sqrt(rr_new) / state->norm_b;
+    const bool cont = (rel > state->tol) && (it < max_iters);
+    const bool log_pn = cont && it < ell && log_p;
+    if (k > 0) {
+        for (int e = threadIdx.x; e < k * k; e += blockDim.x) s_L[e] = Lg[e];
+        cta_sync();
+        cta_chol_solve(s_L, k, red + 1, s_mu);
+    }
+    for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        const double ri = r[i];
+        const double pi = k > 0 ? sub_rn(add_rn(mul_rn(beta, p[i]), ri), row_dot(W, i, k, s_mu))   // beta*p + r - W mu
+                                : add_rn(ri, mul_rn(beta, p[i]));                                  // r + beta*p
+        p[i] = pi;
+        if (log_pn) log_p[it * rows + i] = pi;
+    }
+    if (cta_last_arrival(counter, gridDim.x) && threadIdx.x == 0) {
+        history[it] = rel;
+        if (it - 1 < ell && log_beta) log_beta[it - 1] = beta;
+        if (log_pn && k > 0 && log_mu)
+            for (int j = 0; j < k; ++j) log_mu[it * k + j] = s_mu[j];
+        state->rr = rr_new;
+        state->beta = beta;
+        state->rel = rel;
+        state->done = cont ? 0 : 1;
+    }
+}
+
+int check_slab(const dcg_operator* op) {
+    if (!op || op->kind != DCG_OP_DENSE) return DCG_E_CONFIG;
+    if (op->n < 0 || op->row0 < 0 || op->rows < 0 || op->row0 + op->rows > op->n) return DCG_E_CONFIG;
+    if (op->ldk < op->n || (op->ldk & 1) || !aligned16(op->d_k)) return DCG_E_CONFIG;
+    return DCG_OK;
+}
+
+int launch_gemv(dcg_context* ctx, cudaStream_t st, int mode, const dcg_operator* op, const double* v,
+                const double* b, double* out, double* part, const dcg_shard_state* state) {
+    int rc = check_slab(op);
+    if (rc) return rc;
+    if (op->rows == 0) return DCG_OK;
+    long long G = ctx->sm_count;
+    if (G > op->rows) G = op->rows;
+    ShardWs w;
+    rc = shard_ws(ctx, st, (int)G, 2, &w);
+    if (rc) return rc;
+    const size_t smem = shard_gemv_smem(op->n);
+    DCG_CUDA(cudaFuncSetAttribute(shard_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    shard_gemv_kernel<<<(unsigned)G, DCG_NT, smem, st>>>(mode, op->d_k, op->ldk, op->n, op->rows, op->row0, v,
+                                                          op->d_s, op->shift, b, out, part, w.parts, 2, w.counter,
+                                                          state);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}
+
+}  // namespace
+
+extern "C" int dcg_shard_apply_dot(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_v,
+                                   double* d_out, double* d_part, const dcg_shard_state* d_state) {
+    if (!ctx || !d_v || !d_out) return DCG_E_CONFIG;
+    return launch_gemv(ctx, as_stream(stream), 0, op, d_v, nullptr, d_out, d_part, d_state);
+}
+
+extern "C" int dcg_shard_residual(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_v,
+                                  const double* d_b, double* d_r, const dcg_shard_state* d_state) {
+    if (!ctx || !d_v || !d_b || !d_r) return DCG_E_CONFIG;
+    return launch_gemv(ctx, as_stream(stream), 1, op, d_v, d_b, d_r, nullptr, d_state);
+}
+
+extern "C" int dcg_shard_partials(dcg_context* ctx, void* stream, long long rows, int k, const double* d_u,
+                                  const double* d_w, const double* d_m, double* d_part) {
+    if (!ctx || rows < 0 || k < 0 || !d_part || (k > 0 && (!d_w || !d_m))) return DCG_E_CONFIG;
+    if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
+    cudaStream_t st = as_stream(stream);
+    const int G = shard_grid(ctx, rows), ps = slot_stride(k);
+    ShardWs w;
+    int rc = shard_ws(ctx, st, G, ps, &w);
+    if (rc) return rc;
+    shard_partials_kernel<<<G, SH_NT, 0, st>>>(rows, k, d_u, d_w, d_m, d_part, w.parts, ps, w.counter);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}
+
+extern "C" int dcg_shard_start(dcg_context* ctx, void* stream, long long rows, int k, const double* d_red,
+                               const double* d_chol, const double* d_w, const double* d_xprev, double* d_x0,
+                               dcg_shard_state* d_state, double tol, long long max_iters, long long ell) {
+    if (!ctx || rows < 0 || k < 0 || !d_red || !d_xprev || !d_x0 || !d_state) return DCG_E_CONFIG;
+    if (k > 0 && (!d_chol || !d_w)) return DCG_E_CONFIG;
+    if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
+    cudaStream_t st = as_stream(stream);
+    shard_start_kernel<<<shard_grid(ctx, rows), SH_NT, 0, st>>>(rows, k, d_red, d_chol, d_w, d_xprev, d_x0, d_state,
+                                                                 tol, max_iters, ell);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}
+
+extern "C" int dcg_shard_begin(dcg_context* ctx, void* stream, long long rows, int k, const double* d_red,
+                               const double* d_chol, const double* d_w, const double* d_r, double* d_p, double* d_x,
+                               dcg_shard_state* d_state, double* d_history, double* d_log_r, double* d_log_p,
+                               double* d_log_mu) {
+    if (!ctx || rows < 0 || k < 0 || !d_red || !d_r || !d_p || !d_x || !d_state || !d_history) return DCG_E_CONFIG;
+    if (k > 0 && (!d_chol || !d_w)) return DCG_E_CONFIG;
+    if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
+    cudaStream_t st = as_stream(stream);
+    const int G = shard_grid(ctx, rows);
+    ShardWs w;
+    int rc = shard_ws(ctx, st, G, 2, &w);
+    if (rc) return rc;
+    shard_begin_kernel<<<G, SH_NT, 0, st>>>(rows, k, d_red, d_chol, d_w, d_r, d_p, d_x, d_state, d_history, d_log_r,
+                                            d_log_p, d_log_mu, w.counter);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}
+
+extern "C" int dcg_shard_update(dcg_context* ctx, void* stream, int mode, long long rows, int k,
+                                const double* d_red_d, double* d_x, double* d_r, const double* d_p,
+                                const double* d_ap, const double* d_aw, double* d_part, dcg_shard_state* d_state,
+                                double* d_log_r, double* d_log_d, double* d_log_alpha, double* d_log_beta) {
+    (void)d_log_beta;
+    if (!ctx || rows < 0 || k < 0 || mode < 0 || mode > 2 || !d_x || !d_r || !d_state) return DCG_E_CONFIG;
+    if (mode != 2 && (!d_red_d || !d_p)) return DCG_E_CONFIG;
+    if (mode == 0 && !d_ap) return DCG_E_CONFIG;
+    if (mode != 1 && !d_part) return DCG_E_CONFIG;
+    if (k > 0 && !d_aw) return DCG_E_CONFIG;
+    if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
+    if (d_log_r && (!d_log_d || !d_log_alpha)) return DCG_E_CONFIG;
+    cudaStream_t st = as_stream(stream);
+    const int G = shard_grid(ctx, rows), ps = slot_stride(k);
+    ShardWs w;
+    int rc = shard_ws(ctx, st, G, ps, &w);
+    if (rc) return rc;
+    shard_update_kernel<<<G, SH_NT, 0, st>>>(mode, rows, k, d_red_d, d_x, d_r, d_p, d_ap, d_aw, d_part, d_state,
+                                             d_log_r, d_log_d, d_log_alpha, w.parts, ps, w.counter);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}
+
+extern "C" int dcg_shard_direction(dcg_context* ctx, void* stream, long long rows, int k, const double* d_red,
+                                   const double* d_chol, const double* d_w, const double* d_r, double* d_p,
+                                   dcg_shard_state* d_state, double* d_history, double* d_log_p, double* d_log_mu,
+                                   double* d_log_beta) {
+    if (!ctx || rows < 0 || k < 0 || !d_red || !d_r || !d_p || !d_state || !d_history) return DCG_E_CONFIG;
+    if (k > 0 && (!d_chol || !d_w)) return DCG_E_CONFIG;
+    if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
+    cudaStream_t st = as_stream(stream);
+    const int G = shard_grid(ctx, rows);
+    ShardWs w;
+    int rc = shard_ws(ctx, st, G, 2, &w);
+    if (rc) return rc;
+    shard_direction_kernel<<<G, SH_NT, 0, st>>>(rows, k, d_red, d_chol, d_w, d_r, d_p, d_state, d_history, d_log_p,
+                                                d_log_mu, d_log_beta, w.counter);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}

@@ -1,0 +1,472 @@
+"""Row-sharded def-CG over R ranks, one process per GPU.
+
+K is partitioned into contiguous row slabs: rank r owns rows
+[r * ceil(n / R), ...) of K and the same rows of x, r, p, Ap (and of W, AW).
+With that uniform partition the padded all-gather buffer (R x ceil(n / R))
+holds the full vector in its first n entries, so no reordering is needed.
+
+One iteration of the reference's _run_loop (solvers.py:131-204) becomes
+
+    all-gather p                  (8 n / R bytes per rank)
+    dcg_shard_apply_dot           local GEMV over the slab + p'Ap partial
+    all-reduce(1)
+    dcg_shard_update              alpha, x, r, partials [r'r, AW'r]
+    all-reduce(1 + k)
+    dcg_shard_direction           beta, mu = chol_solve(L, AW'r), p, rel, done
+
+The scalars live in a device-resident dcg_shard_state.  Iterations are
+enqueued `poll` at a time and the host reads the done flag once per chunk;
+every rank enqueues the same kernels and collectives (kernels after
+convergence are no-ops), and the all-reduced values are bit-identical on all
+ranks, so all ranks stop together.
+
+The small recycling steps run redundantly on every rank, on all-gathered data
+(W, AW are n x k, the Krylov log (2m + 1) x n): refresh_basis's Gram
+factorisation with pruning (recycle.py:66-92) and harmonic_ritz_extract
+(recycle.py:95-159) use the single-GPU kernels, whose results are
+deterministic, so every rank holds the same basis.  Each rank keeps W / AW
+whole (n x k) and uses its rows.
+
+The collectives go through a `comm` object (TorchComm: torch.distributed with
+NCCL on GPUs; the CPU tests use gloo) and the local arithmetic through a
+`backend` (DeviceShardBackend: the C ABI, include/defcg_b200.h L5).  The host
+logic here is the same for both.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from . import _device as D
+from . import _native as N
+from .errors import BasisDeficient, BreakdownZeroCurvature
+from .solvers import SolveReport, SolverConfig, TERM_CONVERGED, TERM_MAX_ITERS
+
+# ---------------------------------------------------------------------------
+# partition and communication
+# ---------------------------------------------------------------------------
+
+
+def row_block(n: int, world: int) -> int:
+    return max(1, -(-n // world))
+
+
+def row_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """(row0, rows) of `rank` under the uniform ceil(n / world) partition."""
+    mb = row_block(n, world)
+    r0 = min(n, rank * mb)
+    return r0, max(0, min(n, r0 + mb) - r0)
+
+
+class SelfComm:
+    """world = 1: collectives are identities."""
+
+    rank, world = 0, 1
+
+    def allgather(self, local: torch.Tensor, full: torch.Tensor):
+        full[: local.shape[0]].copy_(local)
+
+    def allreduce(self, buf: torch.Tensor):
+        return buf
+
+
+class TorchComm:
+    """torch.distributed collectives (NCCL for CUDA tensors, gloo for CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self._pad = {}
+
+    def allgather(self, local: torch.Tensor, full: torch.Tensor):
+        """`full` holds world x mb entries per leading index (mb = the padded
+        block); `local` holds this rank's rows (may be shorter)."""
+        mb = full.shape[0] // self.world
+        if local.shape[0] == mb:
+            src = local
+        else:
+            key = (mb,) + tuple(local.shape[1:]) + (local.device.type,)
+            src = self._pad.get(key)
+            if src is None:
+                src = torch.zeros((mb,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+                self._pad[key] = src
+            src[: local.shape[0]].copy_(local)
+        src = src.contiguous()
+        try:
+            self.dist.all_gather_into_tensor(full, src, group=self.group)
+        except (RuntimeError, NotImplementedError):   # backends without the fused form
+            parts = list(full.view((self.world,) + tuple(src.shape)).unbind(0))
+            self.dist.all_gather(parts, src, group=self.group)
+
+    def allreduce(self, buf: torch.Tensor):
+        self.dist.all_reduce(buf, op=self.dist.ReduceOp.SUM, group=self.group)
+        return buf
+
+
+# ---------------------------------------------------------------------------
+# operator
+# ---------------------------------------------------------------------------
+
+
+class ShardedOperator:
+    """This rank's slab of A = shift I + S K S: rows [row0, row0 + rows) of K
+    (device, leading dimension ldk), the full scale vector s (n) or None."""
+
+    def __init__(self, kslab: torch.Tensor, n: int, ldk: int, row0: int, rows: int, s=None, shift: float = 0.0):
+        self.kslab, self.n, self.ldk, self.row0, self.rows = kslab, int(n), int(ldk), int(row0), int(rows)
+        self.s = s
+        self.shift = float(shift)
+
+    def scaled(self, s, shift: float) -> "ShardedOperator":
+        return ShardedOperator(self.kslab, self.n, self.ldk, self.row0, self.rows, s, shift)
+
+    def c_struct(self) -> N.COperator:
+        c = N.COperator()
+        c.kind = N.DCG_OP_DENSE
+        c.n = self.n
+        c.row0 = self.row0
+        c.rows = self.rows
+        c.d_k = self.kslab.data_ptr()
+        c.ldk = self.ldk
+        c.d_s = self.s.data_ptr() if self.s is not None else None
+        c.shift = self.shift
+        return c
+
+
+def sharded_rbf_kernel(x, params, jitter=None, comm=None) -> ShardedOperator:
+    """This rank's rows of the RBF Gram (gpc.py:82-98), built on device from
+    the replicated data X (n x d, a few MB) - Gram blocks never cross PCIe."""
+    comm = comm or SelfComm()
+    xd = D.to_dev(x, 2)
+    n, dim = xd.shape
+    var = params.signal_sd**2
+    jitter = 1e-8 * var if jitter is None else float(jitter)
+    if jitter < 0.0:
+        raise ValueError("jitter must be non-negative")
+    r0, rows = row_range(n, comm.world, comm.rank)
+    ld = D.padded_ld(n)
+    kslab = D.zeros(max(rows, 1), ld)
+    if rows:
+        N.check(N.lib().dcg_k_rbf_gram(D.ctx(), D.stream(), xd.data_ptr(), n, dim, var,
+                                       1.0 / (2.0 * params.lengthscale**2), jitter, kslab.data_ptr(), ld, r0, rows),
+                what="rbf_gram")
+    return ShardedOperator(kslab, n, ld, r0, rows)
+
+
+# ---------------------------------------------------------------------------
+# device backend (the C ABI)
+# ---------------------------------------------------------------------------
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+class DeviceShardBackend:
+    """Local arithmetic of one rank through the L5 entry points."""
+
+    def __init__(self, slot: int = 0):
+        self.slot = slot
+
+    def ctx(self):
+        return D.ctx(self.slot)
+
+    def stream(self):
+        return D.stream()
+
+    def empty(self, *shape):
+        return D.empty(*shape)
+
+    def zeros(self, *shape):
+        return D.zeros(*shape)
+
+    def new_state(self):
+        return D.zeros(N.SHARD_STATE_DOUBLES)
+
+    def read_state(self, st: torch.Tensor) -> dict:
+        h = st.cpu()
+        i = h.view(torch.int64)
+        return {"rr": float(h[N.SHARD_RR]), "norm_b": float(h[N.SHARD_NORM_B]), "rel": float(h[N.SHARD_REL]),
+                "it": int(i[N.SHARD_IT]), "done": int(i[N.SHARD_DONE]), "status": int(i[N.SHARD_STATUS]),
+                "info": int(i[N.SHARD_INFO])}
+
+    def residual(self, op, vfull, b, r, state=None):
+        cop = op.c_struct()
+        N.check(N.lib().dcg_shard_residual(self.ctx(), self.stream(), ctypes.byref(cop), _p(vfull), _p(b), _p(r),
+                                           _p(state)), what="shard_residual")
+
+    def apply_dot(self, op, vfull, out, part, state):
+        cop = op.c_struct()
+        N.check(N.lib().dcg_shard_apply_dot(self.ctx(), self.stream(), ctypes.byref(cop), _p(vfull), _p(out),
+                                            _p(part), _p(state)), what="shard_apply_dot")
+
+    def partials(self, rows, k, u, w, m, part):
+        N.check(N.lib().dcg_shard_partials(self.ctx(), self.stream(), rows, k, _p(u), _p(w), _p(m), _p(part)),
+                what="shard_partials")
+
+    def start(self, rows, k, red, chol, w, xprev, x0, state, tol, max_iters, ell):
+        N.check(N.lib().dcg_shard_start(self.ctx(), self.stream(), rows, k, _p(red), _p(chol), _p(w), _p(xprev),
+                                        _p(x0), _p(state), tol, max_iters, ell), what="shard_start")
+
+    def begin(self, rows, k, red, chol, w, r, p, x, state, hist, log):
+        N.check(N.lib().dcg_shard_begin(self.ctx(), self.stream(), rows, k, _p(red), _p(chol), _p(w), _p(r), _p(p),
+                                        _p(x), _p(state), _p(hist), _p(log.r), _p(log.p), _p(log.mu)),
+                what="shard_begin")
+
+    def update(self, mode, rows, k, red_d, x, r, p, ap, aw, part, state, log):
+        N.check(N.lib().dcg_shard_update(self.ctx(), self.stream(), mode, rows, k, _p(red_d), _p(x), _p(r), _p(p),
+                                         _p(ap), _p(aw), _p(part), _p(state), _p(log.r), _p(log.d), _p(log.alpha),
+                                         _p(log.beta)), what="shard_update")
+
+    def direction(self, rows, k, red, chol, w, r, p, state, hist, log):
+        N.check(N.lib().dcg_shard_direction(self.ctx(), self.stream(), rows, k, _p(red), _p(chol), _p(w), _p(r),
+                                            _p(p), _p(state), _p(hist), _p(log.p), _p(log.mu), _p(log.beta)),
+                what="shard_direction")
+
+
+# ---------------------------------------------------------------------------
+# solve
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class ShardLog:
+    """This rank's rows of the KrylovLog (solvers.py:54-72): p (ell x rows),
+    r ((ell + 1) x rows), d / alpha / beta (ell), mu (ell x k)."""
+
+    p: torch.Tensor
+    r: torch.Tensor
+    d: torch.Tensor
+    alpha: torch.Tensor
+    beta: torch.Tensor
+    mu: torch.Tensor | None
+    m: int = 0
+
+
+@dataclass
+class ShardBasis:
+    """RecycleBasis replicated on every rank: W, AW (n x k) and L (k x k)."""
+
+    w: torch.Tensor
+    aw: torch.Tensor
+    chol: torch.Tensor
+
+    @property
+    def k(self) -> int:
+        return int(self.w.shape[1])
+
+
+def _alloc_log(be, rows, ell, k):
+    cap = max(ell, 1)
+    return ShardLog(p=be.empty(cap, max(rows, 1)), r=be.empty(cap + 1, max(rows, 1)), d=be.empty(cap),
+                    alpha=be.empty(cap), beta=be.empty(cap), mu=be.empty(cap, max(k, 1)) if k else None)
+
+
+def sharded_solve(op: ShardedOperator, b_loc, x_prev_loc, basis: ShardBasis | None, cfg: SolverConfig | None = None,
+                  comm=None, backend=None, poll: int = 4):
+    """CG (basis None or k = 0, solvers.py:207-219) or deflated CG with the
+    warm-start correction (solvers.py:222-239) on this rank's rows.  Returns
+    (x_loc, SolveReport, ShardLog); every rank gets the same report."""
+    cfg = cfg or SolverConfig()
+    comm = comm or SelfComm()
+    be = backend or DeviceShardBackend()
+    t0 = time.perf_counter()
+    n, rows, r0 = op.n, op.rows, op.row0
+    k = basis.k if basis is not None else 0
+    mb = row_block(n, comm.world)
+    ell = int(cfg.ell)
+    max_iters = 10 * n if cfg.max_iters is None else int(cfg.max_iters)
+    every = int(cfg.recompute_residual_every or 0)
+
+    w_loc = basis.w[r0:r0 + rows] if k else None
+    aw_loc = basis.aw[r0:r0 + rows] if k else None
+    chol = basis.chol if k else None
+    full = be.empty(comm.world * mb)
+    x = be.empty(max(rows, 1))
+    r = be.empty(max(rows, 1))
+    p = be.empty(max(rows, 1))
+    ap = be.empty(max(rows, 1))
+    part1 = be.zeros(2)
+    part2 = be.zeros(2 + k)
+    state = be.new_state()
+    hist = be.zeros(max_iters + 1)
+    log = _alloc_log(be, rows, ell, k)
+
+    # ---- prologue: norm_b, warm start, r_0, mu_0, p_0 ----------------------
+    if k:
+        comm.allgather(x_prev_loc, full)
+        be.residual(op, full, b_loc, r)                    # r_prev = b - A x_prev
+        be.partials(rows, k, b_loc, r, w_loc, part2)       # [b'b, W' r_prev]
+    else:
+        be.partials(rows, 0, b_loc, None, None, part2)     # [b'b]
+    comm.allreduce(part2)
+    be.start(rows, k, part2, chol, w_loc, x_prev_loc, x, state, float(cfg.tol), max_iters, ell)
+    comm.allgather(x[:rows], full)
+    be.residual(op, full, b_loc, r)                        # r_0 = b - A x_0
+    be.partials(rows, k, r, r, aw_loc, part2)              # [r0'r0, AW' r0]
+    comm.allreduce(part2)
+    be.begin(rows, k, part2, chol, w_loc, r, p, x, state, hist, log)
+
+    # ---- iterations, `poll` per host check -----------------------------------
+    j = 0
+    while True:
+        st = be.read_state(state)
+        if st["done"]:
+            break
+        for _ in range(max(1, poll)):
+            j += 1
+            comm.allgather(p[:rows], full)
+            be.apply_dot(op, full, ap, part1, state)
+            comm.allreduce(part1)
+            if every > 0 and j % every == 0:               # true residual (solvers.py:175-177)
+                be.update(1, rows, k, part1, x, r, p, ap, aw_loc, part2, state, log)
+                comm.allgather(x[:rows], full)
+                be.residual(op, full, b_loc, r, state)
+                be.update(2, rows, k, None, x, r, p, ap, aw_loc, part2, state, log)
+            else:
+                be.update(0, rows, k, part1, x, r, p, ap, aw_loc, part2, state, log)
+            comm.allreduce(part2)
+            be.direction(rows, k, part2, chol, w_loc, r, p, state, hist, log)
+
+    if st["status"] == N.DCG_E_BREAKDOWN:
+        raise BreakdownZeroCurvature(st["info"])
+    its = st["it"]
+    log.m = min(its, ell)
+    history = hist[: its + 1].cpu().tolist()
+    conv = st["rel"] <= cfg.tol
+    rep = SolveReport(its, history, conv, time.perf_counter() - t0, TERM_CONVERGED if conv else TERM_MAX_ITERS)
+    return x[:rows], rep, log
+
+
+# ---------------------------------------------------------------------------
+# recycling on gathered data
+# ---------------------------------------------------------------------------
+
+
+def _gather_rows(comm, be, local: torch.Tensor, n: int) -> torch.Tensor:
+    """(rows x c) local row block -> (n x c) on every rank."""
+    mb = row_block(n, comm.world)
+    c = local.shape[1] if local.dim() == 2 else 1
+    full = be.empty(comm.world * mb, c) if local.dim() == 2 else be.empty(comm.world * mb)
+    comm.allgather(local, full)
+    return full[:n]
+
+
+def _gather_log(comm, be, log: ShardLog, n: int, rows: int):
+    """Full (n-row) KrylovLog buffers of the first m logged iterations."""
+    from .solvers import KrylovLog
+
+    m = log.m
+    cap = log.p.shape[0]
+    full = KrylovLog(n, cap, log.mu.shape[1] if log.mu is not None else 0)
+    mb = row_block(n, comm.world)
+    # gather (vectors x rows) blocks as rows x vectors so the row-block gather applies
+    pr = torch.cat([log.p[:m, :rows], log.r[: m + 1, :rows]], dim=0).t().contiguous()
+    g = be.empty(comm.world * mb, pr.shape[1])
+    comm.allgather(pr, g)
+    g = g[:n].t()
+    if m:
+        full._p[:m].copy_(g[:m])
+    full._r[: m + 1].copy_(g[m:])
+    full._s[0, :m].copy_(log.d[:m])
+    full._s[1, :m].copy_(log.alpha[:m])
+    full._s[2, :m].copy_(log.beta[:m])
+    if log.mu is not None and m:
+        full._mu[:m].copy_(log.mu[:m])
+    full.m = m
+    return full
+
+
+def sharded_refresh_basis(op: ShardedOperator, w_full: torch.Tensor, comm=None, backend=None) -> ShardBasis:
+    """refresh_basis (recycle.py:80-92) for the sharded operator: AW's rows by
+    the local slab product, all-gathered; W'AW factored with failing-pivot
+    pruning redundantly (and identically) on every rank."""
+    comm = comm or SelfComm()
+    be = backend or DeviceShardBackend()
+    n, k = w_full.shape
+    if k == 0:
+        return ShardBasis(w_full, w_full.clone(), be.empty(0, 0))
+    rows = op.rows
+    aw_loc = be.empty(max(rows, 1), k)
+    cop = op.c_struct()
+    if rows:
+        N.check(N.lib().dcg_op_apply_block(be.ctx(), be.stream(), ctypes.byref(cop), w_full.data_ptr(), k,
+                                           aw_loc.data_ptr()), what="refresh_basis")
+    aw = _gather_rows(comm, be, aw_loc[:rows], n).contiguous()
+    w = w_full.contiguous().clone()
+    chol = be.empty(k, k)
+    kout, info = ctypes.c_longlong(k), ctypes.c_longlong(0)
+    rc = N.lib().dcg_gram_factor(be.ctx(), be.stream(), w.data_ptr(), aw.data_ptr(), n, k, 1, chol.data_ptr(),
+                                 ctypes.byref(kout), ctypes.byref(info))
+    N.check(rc, info.value, "refresh_basis")
+    kk = int(kout.value)
+    return ShardBasis(w.view(-1)[: n * kk].view(n, kk), aw.view(-1)[: n * kk].view(n, kk),
+                      chol.view(-1)[: kk * kk].view(kk, kk))
+
+
+def sharded_extract(log: ShardLog, prev: ShardBasis | None, k: int, selection: str, n: int, rows: int, comm=None,
+                    backend=None) -> ShardBasis | None:
+    """harmonic_ritz_extract (recycle.py:95-159) on the gathered log, run
+    redundantly on every rank; returns W_next / AW_next (n x k, factor
+    computed at the next refresh) or raises BasisDeficient."""
+    from .recycle import RecycleBasis, _extract_dev
+
+    comm = comm or SelfComm()
+    be = backend or DeviceShardBackend()
+    flog = _gather_log(comm, be, log, n, rows)
+    pb = None
+    if prev is not None and prev.k:
+        pb = RecycleBasis.__new__(RecycleBasis)
+        pb.w_dev, pb.aw_dev, pb.chol_dev = prev.w, prev.aw, prev.chol
+    ext = _extract_dev(flog, pb, int(k), selection)
+    if ext.w_next.shape[1] == 0:
+        return None
+    w_next = ext.w_next if isinstance(ext.w_next, torch.Tensor) else D.to_dev(ext.w_next, 2)
+    aw_next = ext.aw_next if isinstance(ext.aw_next, torch.Tensor) else D.to_dev(ext.aw_next, 2)
+    return ShardBasis(w_next.contiguous(), aw_next.contiguous(), be.empty(0, 0))
+
+
+@dataclass
+class ShardSequenceState:
+    """SequenceState (recycle.py:49-63) for the sharded solver: the basis is
+    replicated (n x k), x_last holds this rank's rows."""
+
+    k: int
+    cfg: SolverConfig = field(default_factory=SolverConfig)
+    selection: str = "smallest"
+    basis: ShardBasis | None = None
+    x_last: torch.Tensor | None = None
+    history: list = field(default_factory=list)
+
+
+def sharded_solve_next(state: ShardSequenceState, op: ShardedOperator, b_loc, comm=None, backend=None):
+    """solve_next (recycle.py:162-203) on row shards: refresh (BasisDeficient
+    -> plain CG), solve, extraction (BasisDeficient -> no basis)."""
+    comm = comm or SelfComm()
+    be = backend or DeviceShardBackend()
+    rows = op.rows
+    x_prev = state.x_last if state.x_last is not None else be.zeros(max(rows, 1))
+    used = None
+    if state.basis is not None and state.basis.k > 0:
+        try:
+            used = sharded_refresh_basis(op, state.basis.w, comm, be)
+        except BasisDeficient:
+            used = None
+    x, rep, log = sharded_solve(op, b_loc, x_prev[:rows], used, state.cfg, comm, be)
+    nxt = None
+    if state.k > 0:
+        try:
+            nxt = sharded_extract(log, used, state.k, state.selection, op.n, rows, comm, be)
+        except BasisDeficient:
+            nxt = None
+    return x, replace(state, basis=nxt, x_last=x, history=state.history + [rep])

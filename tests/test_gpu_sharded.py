@@ -1,0 +1,181 @@
+"""GPU: the row-sharded def-CG kernels (csrc/shard.cu, include/defcg_b200.h L5)
+through the sharded driver (paper_1706_00241_b200/sharded.py).
+
+* world = 1: same answers as the single-GPU persistent solver;
+* two ranks in one process: each rank is a thread with its own library
+  context, the collectives are host-ordered copies on the one stream (the
+  kernels never wait on each other), checked against the reference (oracle);
+* a recycled sequence (refresh -> solve -> extraction on gathered data)
+  against the single-GPU solve_next."""
+
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import random_spd
+from oracle import defcg_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1706_00241_b200 as P
+
+    return P
+
+
+class ThreadComm:
+    """In-process collectives for `world` rank threads sharing one device."""
+
+    def __init__(self, shared, rank, world):
+        self.shared, self.rank, self.world = shared, rank, world
+
+    def _barrier(self):
+        self.shared["barrier"].wait()
+
+    def allgather(self, local, full):
+        mb = full.shape[0] // self.world
+        self.shared.setdefault("slots", {})
+        self._barrier()
+        self.shared["slots"][self.rank] = local.clone()
+        self._barrier()
+        for r in range(self.world):
+            src = self.shared["slots"][r]
+            full[r * mb: r * mb + src.shape[0]].copy_(src)
+        self._barrier()
+
+    def allreduce(self, buf):
+        self.shared.setdefault("red", {})
+        self._barrier()
+        self.shared["red"][self.rank] = buf.clone()
+        self._barrier()
+        acc = self.shared["red"][0].clone()
+        for r in range(1, self.world):
+            acc += self.shared["red"][r]
+        buf.copy_(acc)
+        self._barrier()
+        return buf
+
+
+def run_ranks(world, fn):
+    shared = {"barrier": threading.Barrier(world)}
+    out, errs = [None] * world, []
+
+    def body(rank):
+        try:
+            out[rank] = fn(rank, ThreadComm(shared, rank, world))
+        except BaseException as e:  # noqa: BLE001 - surfaced below
+            errs.append(e)
+            shared["barrier"].abort()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    return out
+
+
+def slab_op(a, world, rank, P):
+    from paper_1706_00241_b200 import _device as D
+    from paper_1706_00241_b200.sharded import ShardedOperator, row_range
+
+    n = a.shape[0]
+    r0, rows = row_range(n, world, rank)
+    ld = D.padded_ld(n)
+    slab = torch.zeros(max(rows, 1), ld, dtype=torch.float64, device="cuda")
+    slab[:rows, :n] = torch.from_numpy(a[r0:r0 + rows])
+    return ShardedOperator(slab, n, ld, r0, rows)
+
+
+def dev(v):
+    return torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).cuda()
+
+
+@pytest.mark.parametrize("k,every", [(0, 0), (5, 0), (5, 7)])
+def test_world1_matches_single_gpu_solver(P, rng, k, every):
+    from paper_1706_00241_b200.sharded import SelfComm, ShardBasis, sharded_solve
+
+    n = 300
+    a = random_spd(rng, n, kappa=100.0)   # converges well below n iterations
+    b = rng.standard_normal(n)
+    xprev = 0.1 * rng.standard_normal(n)
+    cfg = P.SolverConfig(tol=1e-10, ell=10, recompute_residual_every=every)
+    basis = P.refresh_basis(a, rng.standard_normal((n, k))) if k else None
+    if k:
+        x_ref, rep_ref, _ = P.deflated_cg_solve(a, b, xprev, basis, cfg)
+        sb = ShardBasis(basis.w_dev, basis.aw_dev, basis.chol_dev)
+    else:
+        x_ref, rep_ref, _ = P.cg_solve(a, b, xprev, cfg)
+        sb = None
+    x, rep, log = sharded_solve(slab_op(a, 1, 0, P), dev(b), dev(xprev), sb, cfg, SelfComm())
+    assert abs(rep.iterations - rep_ref.iterations) <= 1
+    xs = x.cpu().numpy()
+    assert np.linalg.norm(xs - x_ref) <= 1e-8 * np.linalg.norm(x_ref)
+    assert log.m == min(rep.iterations, 10)
+    assert abs(rep.residual_history[0] - rep_ref.residual_history[0]) <= 1e-12 * rep_ref.residual_history[0]
+
+
+@pytest.mark.parametrize("world,k,every", [(2, 0, 0), (2, 4, 0), (3, 4, 6)])
+def test_virtual_ranks_match_reference(P, rng, world, k, every):
+    from paper_1706_00241_b200.sharded import DeviceShardBackend, ShardBasis, sharded_solve
+
+    n = 257
+    a = random_spd(rng, n, kappa=100.0)
+    b = rng.standard_normal(n)
+    xprev = 0.1 * rng.standard_normal(n)
+    w = rng.standard_normal((n, k))
+    cfg = P.SolverConfig(tol=1e-10, ell=8, recompute_residual_every=every)
+    ocfg = O.Cfg(tol=1e-10, ell=8, recompute_residual_every=every)
+    if k:
+        ob = O.refresh_basis(a, w, be="numpy")
+        x_ref, rep_ref, _ = O.deflated_cg_solve(a, b, xprev, ob, ocfg, be="numpy")
+        aw = a @ w
+        g = w.T @ aw
+        sb = ShardBasis(dev(w), dev(aw), dev(np.linalg.cholesky(0.5 * (g + g.T))))
+    else:
+        x_ref, rep_ref, _ = O.cg_solve(a, b, xprev, ocfg, be="numpy")
+        sb = None
+
+    def rank_fn(rank, comm):
+        op = slab_op(a, world, rank, P)
+        r0, rows = op.row0, op.rows
+        x, rep, _ = sharded_solve(op, dev(b[r0:r0 + rows]), dev(xprev[r0:r0 + rows]), sb, cfg, comm,
+                                  DeviceShardBackend(slot=2 + rank), poll=3)
+        torch.cuda.synchronize()
+        return r0, x.cpu().numpy(), rep
+
+    outs = run_ranks(world, rank_fn)
+    x = np.zeros(n)
+    for r0, xl, _ in outs:
+        x[r0:r0 + xl.shape[0]] = xl
+    reps = [o[2] for o in outs]
+    assert all(r.iterations == reps[0].iterations for r in reps)          # ranks agree
+    assert all(r.residual_history == reps[0].residual_history for r in reps)
+    assert abs(reps[0].iterations - rep_ref.iterations) <= 1
+    assert np.linalg.norm(x - x_ref) <= 1e-8 * np.linalg.norm(x_ref)
+
+
+def test_sharded_sequence_matches_single_gpu(P, rng):
+    """solve_next over a drifting sequence A_i = A + i * 0.05 I: same
+    iteration counts (+-1) as the single-GPU sequence, solutions 1e-8."""
+    from paper_1706_00241_b200.sharded import SelfComm, ShardSequenceState, sharded_solve_next
+
+    n = 400
+    a0 = random_spd(rng, n, kappa=200.0)
+    bs = [rng.standard_normal(n) for _ in range(4)]
+    cfg = P.SolverConfig(tol=1e-9, ell=12)
+    st = P.SequenceState(k=6, cfg=cfg, selection="largest")
+    sst = ShardSequenceState(k=6, cfg=cfg, selection="largest")
+    for i, b in enumerate(bs):
+        a = a0 + 0.05 * i * np.eye(n)
+        x_ref, st = P.solve_next(st, a, b)
+        x, sst = sharded_solve_next(sst, slab_op(a, 1, 0, P), dev(b), SelfComm())
+        assert abs(sst.history[-1].iterations - st.history[-1].iterations) <= 1, (i, sst.history[-1].iterations,
+                                                                                    st.history[-1].iterations)
+        assert np.linalg.norm(x.cpu().numpy() - x_ref) <= 1e-8 * np.linalg.norm(x_ref)
