@@ -18,8 +18,12 @@ prescribes (X drawn first, then the noise vector).
   --impl reference = the reference's CPU algorithm (the oracle restatement,
             numpy backend, all host threads), one Newton system per step.
 
-Multi-GPU (torchrun, N > 1): every rank runs an independent replica of the
-workload (weak scaling); timing is the max over ranks.
+Multi-GPU (torchrun, N > 1): the same config-2 sequence with K row-sharded
+over the N ranks (paper_1706_00241_b200/sharded.py): every
+rank builds its Gram slab on device from the replicated X, each def-CG
+iteration all-gathers p and all-reduces the CG scalars and the k projection
+coefficients over NCCL.  Strong scaling (fixed total work); timing is the max
+over ranks.
 """
 
 from __future__ import annotations
@@ -387,12 +391,109 @@ def run_native(args, rank, world):
     return 0
 
 
+def run_native_sharded(args, rank, world):
+    """Config 2 with K row-sharded over `world` GPUs (one process per GPU)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1706_00241_b200 as P
+    from paper_1706_00241_b200 import _native
+    from paper_1706_00241_b200.sharded import TorchComm, sharded_laplace_newton, sharded_rbf_kernel
+
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    comm = TorchComm()
+    c = CONFIG2
+    n, k = args.n, c["k"]
+    x, y = inputs(n, c["d"])
+    cfg = P.SolverConfig(tol=c["tol"], ell=c["ell"])
+    params = P.KernelParams(1.0, c["lengthscale"])
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    op = sharded_rbf_kernel(xd, params, None, comm)
+
+    def sequence():
+        recs = sharded_laplace_newton(op, yd, None, cfg, newton_tol=-np.inf, max_newton=c["newton_steps"], k=k,
+                                      selection="largest", comm=comm)
+        return [r.solver_iterations for r in recs]
+
+    def barrier():
+        dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        sequence()
+    clocks = Clocks(dev)
+    barrier()
+    clocks.start()
+    launches0 = _native.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    total_its, its_list = 0, []
+    for _ in range(args.steps):
+        its_list = sequence()
+        total_its += sum(its_list)
+    ev1.record()
+    barrier()
+    launches = _native.launch_count() - launches0
+    clk = clocks.stop()
+    t = torch.tensor([ev0.elapsed_time(ev1)], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = total_its / (ms / 1e3)   # one sequence solved jointly: iterations counted once
+    # step-average bytes per GPU: the slab (8 n^2 / N) once per matvec-equivalent
+    mv = total_its + args.steps * 2 * c["newton_steps"]
+    achieved = (mv * 8.0 * n * n / world) / (ms / 1e3) / 1e9
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    roofline = {"kernel": "shard_gemv_kernel (row-slab GEMV) - step average incl. collectives", "bound": "hbm",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "bytes_model": "(iterations + 2 prologue matvecs per system) x 8 n^2 / N per GPU over the step"}
+
+    # e2e: pinned host X, y -> device, slab assembly, the sharded sequence, records back
+    xh, yh = torch.from_numpy(x).pin_memory(), torch.from_numpy(y).pin_memory()
+    e2e_steps = max(1, min(args.steps, 3))
+    barrier()
+    t0 = time.perf_counter()
+    e_its, d2h = 0, 0
+    for _ in range(e2e_steps):
+        xg, yg = xh.to("cuda", non_blocking=True), yh.to("cuda", non_blocking=True)
+        op2 = sharded_rbf_kernel(xg, params, None, comm)
+        recs = sharded_laplace_newton(op2, yg, None, cfg, newton_tol=-np.inf, max_newton=c["newton_steps"], k=k,
+                                      selection="largest", comm=comm)
+        e_its += sum(r.solver_iterations for r in recs)
+        d2h = sum(r.f.nbytes for r in recs) + sum(8 * len(r.residual_history) for r in recs)
+        del op2
+    torch.cuda.synchronize()
+    te = torch.tensor([time.perf_counter() - t0], device="cuda")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = {"value": e_its / float(te.item()), "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 8 + yh.numel() * 8),
+           "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
+           "includes": "H2D of X and y, per-rank Gram slab assembly, sharded 8-step Newton sequence, records D2H"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8d recipe)",
+        "config": workload(args) | {"parallelism": f"row-shards x{world} (NCCL all-gather p + all-reduce scalars)"},
+        "iterations_per_sequence": its_list, "sequence_ms": ms_per_step,
+        "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if world > 1 or os.environ.get("DCG_BENCH_SHARDED"):   # (env: exercise the sharded path at N = 1)
+        return run_native_sharded(args, rank, world)
     return run_native(args, rank, world)
 
 

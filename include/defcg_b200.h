@@ -239,11 +239,18 @@ DCG_API int dcg_gpc_newton_system(dcg_context* ctx, void* stream, const dcg_oper
                           const double* d_f, const double* d_grad, const double* d_h,
                           double* d_s, double* d_inner, double* d_b);
 /* a = inner - s x; f = K a; (loglik, grad, h)(f); psi = loglik - f'a / 2
- *                                                     gpc.py:186-209          */
+ *                                                     gpc.py:186-209
+ * For a row-slab kop (sharded): a for all n entries, f for the slab's rows
+ * only; loglik / psi untouched (gather f, then dcg_gpc_objective).          */
 DCG_API int dcg_gpc_newton_update(dcg_context* ctx, void* stream, const dcg_operator* kop,
                           const double* d_inner, const double* d_s, const double* d_x,
                           const double* d_y, double* d_a, double* d_f, double* d_grad,
                           double* d_h, double* loglik, double* psi);
+
+/* (loglik, grad, h)(f) and psi = loglik - f'a / 2 for full f, a (gpc.py:204-209) */
+DCG_API int dcg_gpc_objective(dcg_context* ctx, void* stream, long long n, const double* d_f,
+                              const double* d_y, const double* d_a, double* d_grad, double* d_h,
+                              double* loglik, double* psi);
 
 /* ---- L5: row-sharded def-CG ------------------------------ *
  * K is row-partitioned over R ranks (one process per GPU); a rank owns the

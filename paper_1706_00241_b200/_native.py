@@ -175,6 +175,7 @@ SIGNATURES = {
     "dcg_gpc_derivs": [_P, _P, _LL, _P, _P, _P, _P, _PD],
     "dcg_gpc_newton_system": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P, _P, _P],
     "dcg_gpc_newton_update": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P, _P, _P, _P, _P, _PD, _PD],
+    "dcg_gpc_objective": [_P, _P, _LL, _P, _P, _P, _P, _P, _PD, _PD],
     # row-sharded def-CG (include/defcg_b200.h L5)
     "dcg_shard_apply_dot": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P],
     "dcg_shard_residual": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P],

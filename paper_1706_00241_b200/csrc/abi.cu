@@ -574,6 +574,26 @@ extern "C" int dcg_gpc_derivs(dcg_context* ctx, void* stream, long long n, const
     return DCG_OK;
 }
 
+extern "C" int dcg_gpc_objective(dcg_context* ctx, void* stream, long long n, const double* d_f, const double* d_y,
+                                 const double* d_a, double* d_grad, double* d_h, double* loglik, double* psi) {
+    if (!ctx || n < 0 || !d_f || !d_y || !d_a) return DCG_E_CONFIG;
+    cudaStream_t st = as_stream(stream);
+    const size_t need = al(sizeof(double) * 2 * ctx->sm_count * 2) + al(sizeof(DevStatus));
+    int rc = dcg_ws_reserve(ctx, need);
+    if (rc) return rc;
+    Arena ar{static_cast<char*>(ctx->ws), 0};
+    double* part = ar.take<double>(4 * ctx->sm_count);
+    DevStatus* ds = ar.take<DevStatus>(1);
+    rc = dcg_derivs_launch(ctx, st, n, d_f, d_y, d_a, d_grad, d_h, part, ds);
+    if (rc) return rc;
+    DevStatus hs;
+    rc = dcg_read_status(ctx, st, ds, &hs);
+    if (rc) return rc;
+    if (loglik) *loglik = hs.value;
+    if (psi) *psi = hs.value2;
+    return DCG_OK;
+}
+
 extern "C" int dcg_gpc_newton_system(dcg_context* ctx, void* stream, const dcg_operator* kop, const double* d_f,
                                      const double* d_grad, const double* d_h, double* d_s, double* d_inner,
                                      double* d_b) {
@@ -596,9 +616,17 @@ extern "C" int dcg_gpc_newton_update(dcg_context* ctx, void* stream, const dcg_o
     if (!ctx) return DCG_E_CONFIG;
     int rc = check_dense_op(kop);
     if (rc) return rc;
-    if (kop->row0 != 0 || kop->rows != kop->n) return DCG_E_UNSUPPORTED;
     cudaStream_t st = as_stream(stream);
     const long long n = kop->n;
+    if (kop->row0 != 0 || kop->rows != kop->n) {
+        // row slab (sharded Newton loop): a over all n entries, f for this
+        // rank's rows only; the caller gathers f and calls dcg_gpc_objective
+        rc = dcg_ws_reserve(ctx, sizeof(double) * apply_k_scratch(kop) + 256);
+        if (rc) return rc;
+        rc = dcg_newton_a_launch(ctx, st, n, d_inner, d_s, d_x, d_a);
+        if (rc) return rc;
+        return apply_k(ctx, st, kop, d_a, nullptr, nullptr, 0.0, d_f, static_cast<double*>(ctx->ws));
+    }
     const size_t need = al(sizeof(double) * 2 * ctx->sm_count * 2) + al(sizeof(DevStatus)) +
                         al(sizeof(double) * apply_k_scratch(kop));
     rc = dcg_ws_reserve(ctx, need);

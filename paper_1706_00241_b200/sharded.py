@@ -470,3 +470,79 @@ def sharded_solve_next(state: ShardSequenceState, op: ShardedOperator, b_loc, co
         except BasisDeficient:
             nxt = None
     return x, replace(state, basis=nxt, x_last=x, history=state.history + [rep])
+
+
+# ---------------------------------------------------------------------------
+# GPC Laplace-Newton on row shards
+# ---------------------------------------------------------------------------
+
+
+def _allgather_vec(comm, be, local: torch.Tensor, n: int) -> torch.Tensor:
+    mb = row_block(n, comm.world)
+    full = be.empty(comm.world * mb)
+    comm.allgather(local, full)
+    return full[:n]
+
+
+def sharded_laplace_newton(x, y, params=None, cfg: SolverConfig | None = None, newton_tol=1.0, max_newton=30, k=8,
+                           selection="largest", comm=None, backend=None, jitter=None):
+    """laplace_newton(rbf_kernel(x, params), y, "defcg", ...) (gpc.py:212-291)
+    with K row-sharded over the ranks of `comm`: every rank builds its slab
+    from the replicated X, the n-vectors of the Newton glue (f, a, s, H f + g)
+    are replicated (O(n) work, computed identically on every rank), and each
+    system is solved by sharded_solve_next.  Returns the list of
+    NewtonRecord (f as numpy) - identical on every rank."""
+    from .errors import NoProgress
+    from .gpc import NewtonRecord
+
+    cfg = cfg or SolverConfig()
+    comm = comm or SelfComm()
+    be = backend or DeviceShardBackend()
+    # `x` is the data matrix (the slab is built here) or a prebuilt kernel slab
+    op = x if isinstance(x, ShardedOperator) else sharded_rbf_kernel(x, params, jitter, comm)
+    kop = op.c_struct()   # the kernel matrix itself (no scaling, no shift)
+    n, rows = op.n, op.rows
+    yd = D.to_dev(y, 1)
+    f = be.zeros(n)
+    a = be.zeros(n)
+    grad, h = be.empty(n), be.empty(n)
+    ll = ctypes.c_double(0.0)
+    N.check(N.lib().dcg_gpc_derivs(be.ctx(), be.stream(), n, f.data_ptr(), yd.data_ptr(), grad.data_ptr(),
+                                   h.data_ptr(), ctypes.byref(ll)), what="derivs")
+    psi_prev = float(ll.value)
+    state = ShardSequenceState(k=k, cfg=cfg, selection=selection)
+    records = []
+    for it in range(1, max_newton + 1):
+        s, inner, b_loc = be.empty(n), be.empty(n), be.empty(max(rows, 1))
+        N.check(N.lib().dcg_gpc_newton_system(be.ctx(), be.stream(), ctypes.byref(kop), f.data_ptr(), grad.data_ptr(),
+                                              h.data_ptr(), s.data_ptr(), inner.data_ptr(), b_loc.data_ptr()),
+                what="newton_system")
+        t0 = time.perf_counter()
+        x_loc, state = sharded_solve_next(state, op.scaled(s, 1.0), b_loc[:rows], comm, be)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        rep = state.history[-1]
+        x_full = _allgather_vec(comm, be, x_loc, n).contiguous()
+        f_loc = be.empty(max(rows, 1))
+        a = be.empty(n)
+        N.check(N.lib().dcg_gpc_newton_update(be.ctx(), be.stream(), ctypes.byref(kop), inner.data_ptr(),
+                                              s.data_ptr(), x_full.data_ptr(), yd.data_ptr(), a.data_ptr(),
+                                              f_loc.data_ptr(), grad.data_ptr(), h.data_ptr(), None, None),
+                what="newton_update")
+        f = _allgather_vec(comm, be, f_loc[:rows], n).contiguous()
+        ll, psi = ctypes.c_double(0.0), ctypes.c_double(0.0)
+        N.check(N.lib().dcg_gpc_objective(be.ctx(), be.stream(), n, f.data_ptr(), yd.data_ptr(), a.data_ptr(),
+                                          grad.data_ptr(), h.data_ptr(), ctypes.byref(ll), ctypes.byref(psi)),
+                what="objective")
+        psi = float(psi.value)
+        records.append(NewtonRecord(newton_iter=it, psi=psi, loglik=float(ll.value),
+                                    solver_iterations=rep.iterations, rel_residual=rep.residual_history[-1],
+                                    solve_time_s=dt, residual_history=list(rep.residual_history), f=f.clone()))
+        if psi < psi_prev - 1e-6:
+            raise NoProgress(f"objective fell from {psi_prev:.9g} to {psi:.9g} at iteration {it}")
+        if psi - psi_prev < newton_tol:
+            break
+        psi_prev = psi
+    for r in records:
+        r.f = r.f.cpu().numpy()
+    return records

@@ -179,3 +179,22 @@ def test_sharded_sequence_matches_single_gpu(P, rng):
         assert abs(sst.history[-1].iterations - st.history[-1].iterations) <= 1, (i, sst.history[-1].iterations,
                                                                                     st.history[-1].iterations)
         assert np.linalg.norm(x.cpu().numpy() - x_ref) <= 1e-8 * np.linalg.norm(x_ref)
+
+
+def test_sharded_laplace_newton_world1_matches_gpc(P):
+    """The sharded GPC Newton driver at world = 1 against laplace_newton on
+    the config-1 inputs: iteration counts +-1 per step, psi within 1e-8."""
+    from paper_1706_00241_b200.sharded import SelfComm, sharded_laplace_newton
+
+    x, y = O.gpc_inputs(2000, 5, 0)
+    cfg = P.SolverConfig(tol=1e-8, ell=12)
+    gram = P.rbf_kernel(x, P.KernelParams(1.0, 1.5))
+    _, recs = P.laplace_newton(gram, y, "defcg", cfg, newton_tol=-np.inf, max_newton=6, k=8, selection="largest")
+    srecs = sharded_laplace_newton(x, y, P.KernelParams(1.0, 1.5), cfg, newton_tol=-np.inf, max_newton=6, k=8,
+                                   selection="largest", comm=SelfComm())
+    assert len(srecs) == len(recs)
+    for a, b in zip(srecs, recs):
+        assert abs(a.solver_iterations - b.solver_iterations) <= 1, ([r.solver_iterations for r in srecs],
+                                                                     [r.solver_iterations for r in recs])
+        assert abs(a.psi - b.psi) <= 1e-8 * abs(b.psi)
+    assert np.linalg.norm(srecs[-1].f - recs[-1].f) <= 1e-6 * np.linalg.norm(recs[-1].f)
