@@ -61,6 +61,7 @@ enum dcg_status {
 
 #define DCG_MAX_K 64            /* deflation basis columns handled by the fused kernels */
 #define DCG_MAX_T 112           /* harmonic pencil order k_prev + m handled on device   */
+#define DCG_RBF_MAX_DIM 64      /* point dimension of the matrix-free RBF operator      */
 
 /* ---- operator: A = shift * I + diag(s) * K * diag(s) --------------------- */
 /* The reference always materialises A (gpc.py:178 builds K * outer(s,s) + I).
@@ -69,6 +70,9 @@ enum dcg_status {
  * locally stored row slab for row-sharded operators (rows == n on one GPU). */
 /* DCG_OP_DENSE_SYM: same dense storage, K exactly symmetric and unsharded: the
  * GEMV streams only the lower triangle (64 x 64 tiles), half the bytes.     */
+/* DCG_OP_RBF: matrix-free RBF Gram (config 5): K is regenerated from the
+ * points d_x on every product (never stored); elements are computed exactly
+ * as dcg_k_rbf_gram computes them.                                           */
 enum dcg_op_kind { DCG_OP_DENSE = 0, DCG_OP_RBF = 1, DCG_OP_DENSE_SYM = 2 };
 
 typedef struct dcg_operator {

@@ -336,8 +336,15 @@ extern "C" int dcg_gen_sym_eigen(dcg_context* ctx, void* stream, const double* d
 // ---------------------------------------------------------------------------
 // L2: operator application
 // ---------------------------------------------------------------------------
+int dcg_rbf_mf_check(const dcg_operator* op);
+int dcg_rbf_mf_apply(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, const double* v, const double* s_in,
+                     const double* s_out, double shift, double* y);
+int dcg_rbf_mf_block(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, const double* X, int k,
+                     const double* s_in, const double* s_out, double shift, double* Y);
+
 static int check_dense_op(const dcg_operator* op) {
     if (!op) return DCG_E_CONFIG;
+    if (op->kind == DCG_OP_RBF) return dcg_rbf_mf_check(op);
     if (op->kind != DCG_OP_DENSE && op->kind != DCG_OP_DENSE_SYM) return DCG_E_UNSUPPORTED;
     if (op->n < 0 || op->row0 < 0 || op->rows < 0 || op->row0 + op->rows > op->n) return DCG_E_CONFIG;
     if (op->ldk < op->n || (op->ldk & 1) || !aligned16(op->d_k)) return DCG_E_CONFIG;
@@ -352,6 +359,7 @@ static size_t apply_k_scratch(const dcg_operator* op) {
 }
 static int apply_k(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, const double* v, const double* s_in,
                    const double* s_out, double shift, double* y, double* scratch) {
+    if (op->kind == DCG_OP_RBF) return dcg_rbf_mf_apply(ctx, st, op, v, s_in, s_out, shift, y);
     // the lower-triangle strategy stages 16-byte slices of v and s_in
     if (op->kind == DCG_OP_DENSE_SYM && aligned16(v) && aligned16(s_in))
         return dcg_sym_apply(ctx, st, op->d_k, op->ldk, op->n, v, s_in, s_out, shift, y, scratch);
@@ -376,6 +384,9 @@ extern "C" int dcg_op_apply_block(dcg_context* ctx, void* stream, const dcg_oper
     if (rc) return rc;
     if (k == 0) return DCG_OK;
     if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
+    if (op->kind == DCG_OP_RBF)
+        return dcg_rbf_mf_block(ctx, as_stream(stream), op, d_x, (int)k, op->d_s,
+                                op->d_s ? op->d_s + op->row0 : nullptr, op->shift, d_y);
     rc = dcg_ws_reserve(ctx, sizeof(double) * dcg_block_apply_scratch_doubles(op->n, op->rows, (int)k) + 256);
     if (rc) return rc;
     const double* s_out = op->d_s ? op->d_s + op->row0 : nullptr;
@@ -485,7 +496,11 @@ extern "C" int dcg_refresh_basis(dcg_context* ctx, void* stream, const dcg_opera
     double* aw = ar.take<double>(n * k);
     int* active = ar.take<int>(DCG_MAX_K);
     double* scratch = ar.take<double>(dcg_block_apply_scratch_doubles(n, n, (int)k));
-    rc = dcg_block_apply(ctx, st, op->d_k, op->ldk, n, n, d_w, (int)k, op->d_s, op->d_s, op->shift, d_w, aw, scratch);
+    if (op->kind == DCG_OP_RBF)
+        rc = dcg_rbf_mf_block(ctx, st, op, d_w, (int)k, op->d_s, op->d_s, op->shift, aw);
+    else
+        rc = dcg_block_apply(ctx, st, op->d_k, op->ldk, n, n, d_w, (int)k, op->d_s, op->d_s, op->shift, d_w, aw,
+                             scratch);
     if (rc) return rc;
     long long kk = k;
     rc = gram_core(ctx, st, d_w, aw, n, (int)k, 1, d_chol, active, &kk, info, ar);

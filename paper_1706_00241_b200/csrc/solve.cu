@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "gemv.cuh"
 #include "symgemv.cuh"
+#include "rbfmf.cuh"
 
 #include <stdio.h>
 #include <stdlib.h>
@@ -61,6 +62,7 @@ struct SolveArgs {
     DevStatus* st;
     unsigned int* bar;  // grid barrier arrival counter (zeroed per launch)
     unsigned long long* timers;   // optional per-phase ns accumulators (CTA 0, thread 0)
+    RbfParams rbf;                // matrix-free operator (STRAT_RBF)
 };
 
 // mu = L^-T L^-1 c for the k x k row-major lower factor of W'AW in shared
@@ -157,12 +159,17 @@ __device__ __forceinline__ void reduce_partials(const double* partials, int G, i
     cta_sync();
 }
 
+// GEMV strategies of the persistent kernel
+enum { STRAT_ROWS = 0, STRAT_SYM = 1, STRAT_RBF = 2 };
+
 // Shared-memory doubles of the GEMV region for each strategy.
-__host__ __device__ __forceinline__ long long gemv_region_doubles(bool sym, long long n) {
-    return sym ? sym_smem_doubles() : (min(n, (long long)DCG_QT) + 2 + DCG_NW * DCG_RB);
+__host__ __device__ __forceinline__ long long gemv_region_doubles(int strat, long long n, int dim) {
+    if (strat == STRAT_SYM) return sym_smem_doubles();
+    if (strat == STRAT_RBF) return rbf_mf_smem_doubles(dim);
+    return min(n, (long long)DCG_QT) + 2 + DCG_NW * DCG_RB;
 }
 
-template <bool SYM>
+template <int STRAT>
 __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
 #define GSYNC() dcg_grid_barrier(a.bar, gridDim.x)
     // Phase timers (DCG_PHASE_TIMERS): CTA 0 / thread 0 attributes the time since
@@ -183,7 +190,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int xt = (int)min(n, (long long)DCG_QT) + 2;
     double* s_g = smem;                                  // GEMV region (strategy dependent)
-    double* s_L = s_g + gemv_region_doubles(SYM, n);     // k*k
+    double* s_L = s_g + gemv_region_doubles(STRAT, n, a.rbf.dim);   // k*k
     double* s_rd = s_L + k * k;                          // DCG_MAX_K  1 / L_jj
     double* s_c = s_rd + DCG_MAX_K;                      // 1 + DCG_MAX_K reduced slots
     double* s_mu = s_c + DCG_MAX_K + 2;                  // DCG_MAX_K
@@ -203,15 +210,22 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     // (sym_row_begin), not the vector-phase rows [r0, r1); pass-2 outputs are
     // therefore read by other CTAs after a grid barrier, through L2.
     long long q0 = r0, q1 = r1;
-    if constexpr (SYM) {
+    if constexpr (STRAT == STRAT_SYM) {
         sym_ring_init(s_g, n);
         q0 = sym_row_begin(n, G, blockIdx.x);
         q1 = sym_row_begin(n, G, blockIdx.x + 1);
     }
     // t = K (s (.) v) for the own rows [r0, r1); epi(i, t_i) per row.  The
     // symmetric strategy contains one extra grid barrier between its passes.
+    // The matrix-free strategy computes whole 64-row chunks (c = b, b + G, ...),
+    // again read by other CTAs only after a grid barrier.
     auto gemv = [&](const double* v, auto&& epi) {
-        if constexpr (SYM) {
+        if constexpr (STRAT == STRAT_RBF) {
+            const long long nchunks = (n + MF_TB - 1) / MF_TB;
+            for (long long c = blockIdx.x; c < nchunks; c += G)
+                rbf_rows_gemv(a.rbf, c * MF_TB, min(n, (c + 1) * MF_TB), v, s, s_g, epi);
+            PHASE(0);
+        } else if constexpr (STRAT == STRAT_SYM) {
             PHASE(15);
             unsigned long long tc0 = 0;
             if (a.timers && threadIdx.x == 0) tc0 = globaltimer_ns();
@@ -310,7 +324,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
                                 : add_rn(mul_rn(shift, a.x0[i]), t);
             a.r[i] = sub_rn(a.b[i], ax);
         });
-        if constexpr (SYM) GSYNC(); else cta_sync();
+        if constexpr (STRAT != STRAT_ROWS) GSYNC(); else cta_sync();
         // slot0 = b'b, slots 1.. = W' r_prev
         own_partials([&](long long i) { return a.b[i]; }, a.r, a.W, a.partials);
     } else {
@@ -350,7 +364,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         const double ax = s ? add_rn(mul_rn(shift, xi), mul_rn(s[i], t)) : add_rn(mul_rn(shift, xi), t);
         a.r[i] = sub_rn(a.b[i], ax);
     });
-    if constexpr (SYM) GSYNC(); else cta_sync();
+    if constexpr (STRAT != STRAT_ROWS) GSYNC(); else cta_sync();
     own_partials([&](long long i) { return ld_cg(a.r + i); }, a.r, deflate ? a.AW : nullptr, a.partials);
     GSYNC();
     reduce_partials(a.partials, G, a.ps, nslots, s_c, s_scr);
@@ -417,7 +431,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
                 const double ax = s ? add_rn(mul_rn(shift, xi), mul_rn(s[i], t)) : add_rn(mul_rn(shift, xi), t);
                 a.r[i] = sub_rn(a.b[i], ax);
             });
-            if constexpr (SYM) GSYNC();
+            if constexpr (STRAT != STRAT_ROWS) GSYNC();
         } else {
             for (long long i = r0 + tid; i < r1; i += blockDim.x)
                 a.r[i] = sub_rn(ld_cg(a.r + i), mul_rn(alpha, ld_cg(a.ap + i)));
@@ -477,9 +491,9 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
 
 }  // namespace
 
-size_t dcg_solve_smem_bytes(long long n, int k, bool sym) {
-    return sizeof(double) * (size_t)(gemv_region_doubles(sym, n) + k * k + DCG_MAX_K + DCG_MAX_K + 2 + DCG_MAX_K +
-                                     64 + DCG_NT);
+size_t dcg_solve_smem_bytes(long long n, int k, int strat, int dim) {
+    return sizeof(double) * (size_t)(gemv_region_doubles(strat, n, dim) + k * k + DCG_MAX_K + DCG_MAX_K + 2 +
+                                     DCG_MAX_K + 64 + DCG_NT);
 }
 
 extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_b,
@@ -489,10 +503,16 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
     if (!ctx || !op || !cfg || !d_b || !d_x0 || !d_x || !d_history) return DCG_E_CONFIG;
     if (info) *info = 0;
     const long long n = op->n;
-    if (op->kind != DCG_OP_DENSE && op->kind != DCG_OP_DENSE_SYM) return DCG_E_UNSUPPORTED;
+    if (op->kind != DCG_OP_DENSE && op->kind != DCG_OP_DENSE_SYM && op->kind != DCG_OP_RBF) return DCG_E_UNSUPPORTED;
     const bool sym = op->kind == DCG_OP_DENSE_SYM && ((reinterpret_cast<uintptr_t>(d_x0) | reinterpret_cast<uintptr_t>(op->d_s)) & 15) == 0;
+    const int strat = op->kind == DCG_OP_RBF ? STRAT_RBF : (sym ? STRAT_SYM : STRAT_ROWS);
     if (op->row0 != 0 || op->rows != n) return DCG_E_UNSUPPORTED;   // sharded solves: host loop
-    if (op->ldk < n || (op->ldk & 1) || (reinterpret_cast<uintptr_t>(op->d_k) & 15)) return DCG_E_CONFIG;
+    if (strat == STRAT_RBF) {
+        if (!op->d_x || op->dim < 1) return DCG_E_CONFIG;
+        if (op->dim > DCG_RBF_MAX_DIM) return DCG_E_UNSUPPORTED;
+    } else if (op->ldk < n || (op->ldk & 1) || (reinterpret_cast<uintptr_t>(op->d_k) & 15)) {
+        return DCG_E_CONFIG;
+    }
     if (!(cfg->tol > 0.0) || cfg->ell < 0 || cfg->recompute_residual_every < 0) return DCG_E_CONFIG;
     const int k = basis ? (int)basis->k : 0;
     if (k < 0) return DCG_E_CONFIG;
@@ -551,8 +571,16 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
     }
 
     cudaStream_t st = as_stream(stream);
-    const size_t smem = dcg_solve_smem_bytes(n, k, sym);
-    const void* kfn = sym ? (const void*)dcg_solve_kernel<true> : (const void*)dcg_solve_kernel<false>;
+    const size_t smem = dcg_solve_smem_bytes(n, k, strat, (int)op->dim);
+    const void* kfn = strat == STRAT_RBF ? (const void*)dcg_solve_kernel<STRAT_RBF>
+                      : strat == STRAT_SYM ? (const void*)dcg_solve_kernel<STRAT_SYM>
+                                           : (const void*)dcg_solve_kernel<STRAT_ROWS>;
+    a.rbf.X = op->d_x;
+    a.rbf.n = n;
+    a.rbf.dim = strat == STRAT_RBF ? (int)op->dim : 0;
+    a.rbf.var = op->var;
+    a.rbf.inv2 = op->inv_two_ell2;
+    a.rbf.diag = op->diag;
     DCG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     DCG_CUDA(cudaMemsetAsync(a.st, 0, sizeof(DevStatus), st));
     a.bar = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(a.st) + 128);   // inside the st line

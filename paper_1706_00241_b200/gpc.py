@@ -29,7 +29,7 @@ import torch
 from . import _device as D
 from . import _native as N
 from .errors import InvalidLabel, NoProgress, NotPositiveDefinite, StateInconsistent
-from .operators import DenseOperator, as_operator
+from .operators import DenseOperator, RbfOperator, as_operator
 from .recycle import SELECT_LARGEST, SequenceState, solve_next
 from .solvers import SolverConfig, _solve_dev
 
@@ -87,10 +87,12 @@ class NewtonRecord:
     f: object
 
 
-def rbf_kernel(x, params, jitter=None):
+def rbf_kernel(x, params, jitter=None, matrix_free=False):
     """Dense RBF Gram matrix built on device (gpc.py:82-98, _core.pyx:97-114).
 
-    Returns a DenseOperator holding K in HBM."""
+    Returns a DenseOperator holding K in HBM, or with ``matrix_free`` an
+    RbfOperator that regenerates K from X on every product (config 5: the
+    Gram would not fit)."""
     xd = D.to_dev(x, 2)
     if not bool(torch.isfinite(xd).all()):
         raise ValueError("data matrix contains non-finite entries")
@@ -101,6 +103,8 @@ def rbf_kernel(x, params, jitter=None):
         raise ValueError("jitter must be non-negative")
     inv_two_ell2 = 1.0 / (2.0 * params.lengthscale**2)
     n, dim = xd.shape
+    if matrix_free:
+        return RbfOperator(xd.contiguous(), var, inv_two_ell2, var + float(jitter))
     ld = D.padded_ld(n)
     kbuf = D.zeros(n, ld) if ld != n else D.empty(n, ld)
     if n:

@@ -166,6 +166,64 @@ class DenseOperator:
         return D.out_like(y, other)
 
 
+class RbfOperator(DenseOperator):
+    """Matrix-free A = shift I + S K S with the RBF kernel K regenerated from
+    the points X on every product (kernel K7, config 5; csrc/rbfmf.cuh): K_ij
+    = var * exp(-||x_i - x_j||^2 * inv_two_ell2), K_ii = diag = var + jitter,
+    elements bit-identical to the stored Gram of rbf_kernel (gpc.py:82-98).
+    Nothing of size n^2 is ever allocated."""
+
+    def __init__(self, x: torch.Tensor, var: float, inv_two_ell2: float, diag: float, s=None, shift: float = 0.0):
+        n = int(x.shape[0])
+        super().__init__(None, n, n, s, shift, 0, n, "rows")
+        self.x = x
+        self.var, self.inv_two_ell2, self.diag = float(var), float(inv_two_ell2), float(diag)
+
+    def scaled(self, s, shift: float) -> "RbfOperator":
+        s_dev = None if s is None else D.to_dev(s, 1)
+        return RbfOperator(self.x, self.var, self.inv_two_ell2, self.diag, s_dev, shift)
+
+    def with_strategy(self, strategy: str) -> "RbfOperator":
+        return self
+
+    def kernel_view(self) -> "RbfOperator":
+        return RbfOperator(self.x, self.var, self.inv_two_ell2, self.diag, None, 0.0)
+
+    def require_symmetric(self, rtol: float = SYMMETRY_RTOL) -> "RbfOperator":
+        return self   # exactly symmetric by construction
+
+    def c_struct(self) -> N.COperator:
+        op = N.COperator()
+        op.kind = N.DCG_OP_RBF
+        op.n = self.n
+        op.row0 = 0
+        op.rows = self.n
+        op.d_k = None
+        op.ldk = 0
+        op.d_x = self.x.data_ptr() if self.n else None
+        op.dim = int(self.x.shape[1])
+        op.var = self.var
+        op.inv_two_ell2 = self.inv_two_ell2
+        op.diag = self.diag
+        op.d_s = None if self.s is None else self.s.data_ptr()
+        op.shift = self.shift
+        return op
+
+    def dense_dev(self) -> torch.Tensor:
+        """Explicit A (tests / small problems only): the stored-Gram builder."""
+        n, dim = self.x.shape
+        k = D.empty(n, n)
+        if n:
+            N.check(N.lib().dcg_k_rbf_gram(D.ctx(), D.stream(), self.x.data_ptr(), n, dim, self.var,
+                                           self.inv_two_ell2, self.diag - self.var, k.data_ptr(), n, 0, n),
+                    what="rbf_gram")
+        if self.s is not None:
+            k = k * self.s[:, None] * self.s[None, :]
+        if self.shift:
+            k += self.shift * torch.eye(n, dtype=k.dtype, device=k.device)
+        return k
+
+
 def as_operator(a) -> DenseOperator:
     """Operator for any accepted matrix argument (validates raw matrices once)."""
     if isinstance(a, DenseOperator):

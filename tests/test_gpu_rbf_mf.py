@@ -1,0 +1,91 @@
+"""GPU: the matrix-free RBF operator (K7, config 5; csrc/rbfmf.cuh) against the
+stored Gram of the same points.  The elements are generated exactly as the
+stored builder generates them (_core.pyx:97-114 order), so products agree to
+the summation-order level and solves / Newton trajectories agree with the
+stored-Gram path (which is itself checked against the reference)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import defcg_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1706_00241_b200 as P
+
+    return P
+
+
+def pair(P, n, d, ell, seed=0, jitter=None):
+    rng = np.random.default_rng(seed)
+    x = torch.from_numpy(rng.standard_normal((n, d))).cuda()
+    kp = P.KernelParams(1.3, ell)
+    return P.rbf_kernel(x, kp, jitter), P.rbf_kernel(x, kp, jitter, matrix_free=True), rng
+
+
+@pytest.mark.parametrize("n,d", [(1, 3), (65, 5), (1000, 10), (3001, 16)])
+def test_matvec_matches_stored(P, n, d):
+    stored, mf, rng = pair(P, n, d, 1.5)
+    v = torch.from_numpy(rng.standard_normal(n)).cuda()
+    s = torch.from_numpy(rng.uniform(0.1, 0.5, n)).cuda()
+    for a_st, a_mf in ((stored, mf), (stored.scaled(s, 1.0), mf.scaled(s, 1.0))):
+        y_st = a_st.kernel_view().with_strategy("rows").scaled(a_st.s, a_st.shift).matvec_dev(v)
+        y_mf = a_mf.matvec_dev(v)
+        err = float(torch.linalg.norm(y_mf - y_st) / torch.linalg.norm(y_st))
+        assert err <= 1e-13, err
+
+
+def test_elements_bit_identical(P):
+    stored, mf, _ = pair(P, 300, 7, 0.9)
+    assert torch.equal(mf.dense_dev(), stored.kbuf[:300, :300])
+
+
+@pytest.mark.parametrize("k", [3, 16, 21])
+def test_block_product_matches_stored(P, k):
+    stored, mf, rng = pair(P, 1500, 8, 1.2)
+    s = torch.from_numpy(rng.uniform(0.1, 0.5, 1500)).cuda()
+    w = torch.from_numpy(rng.standard_normal((1500, k))).cuda()
+    y_st = stored.scaled(s, 1.0).apply_block_dev(w)
+    y_mf = mf.scaled(s, 1.0).apply_block_dev(w)
+    assert float(torch.linalg.norm(y_mf - y_st) / torch.linalg.norm(y_st)) <= 1e-13
+
+
+@pytest.mark.parametrize("k", [0, 6])
+def test_solve_matches_stored(P, k):
+    # the Newton-system shape A = I + S K S (well conditioned: counts are not rounding-driven)
+    stored, mf, rng = pair(P, 2000, 6, 1.5)
+    s = torch.from_numpy(rng.uniform(0.2, 0.5, 2000)).cuda()
+    stored, mf = stored.scaled(s, 1.0), mf.scaled(s, 1.0)
+    b = rng.standard_normal(2000)
+    cfg = P.SolverConfig(tol=1e-10, ell=10)
+    if k:
+        w = rng.standard_normal((2000, k))
+        bs, bm = P.refresh_basis(stored, w), P.refresh_basis(mf, w)
+        assert np.allclose(bm.gram_chol, bs.gram_chol, rtol=1e-12, atol=1e-12)
+        x_s, r_s, _ = P.deflated_cg_solve(stored, b, np.zeros(2000), bs, cfg)
+        x_m, r_m, _ = P.deflated_cg_solve(mf, b, np.zeros(2000), bm, cfg)
+    else:
+        x_s, r_s, _ = P.cg_solve(stored, b, None, cfg)
+        x_m, r_m, _ = P.cg_solve(mf, b, None, cfg)
+    assert abs(r_m.iterations - r_s.iterations) <= 1
+    assert np.linalg.norm(x_m - x_s) <= 1e-9 * np.linalg.norm(x_s)
+
+
+def test_gpc_trajectory_matrix_free_matches_stored(P):
+    """Config-1 inputs: the Newton trajectory with K never stored equals the
+    stored-Gram trajectory (iterations +-1, psi 1e-8)."""
+    x, y = O.gpc_inputs(2000, 5, 0)
+    cfg = P.SolverConfig(tol=1e-8, ell=12)
+    kp = P.KernelParams(1.0, 1.5)
+    _, rs = P.laplace_newton(P.rbf_kernel(x, kp), y, "defcg", cfg, newton_tol=-np.inf, max_newton=6, k=8,
+                             selection="largest")
+    _, rm = P.laplace_newton(P.rbf_kernel(x, kp, matrix_free=True), y, "defcg", cfg, newton_tol=-np.inf,
+                             max_newton=6, k=8, selection="largest")
+    for a, b in zip(rm, rs):
+        assert abs(a.solver_iterations - b.solver_iterations) <= 1, ([r.solver_iterations for r in rm],
+                                                                     [r.solver_iterations for r in rs])
+        assert abs(a.psi - b.psi) <= 1e-8 * abs(b.psi)
