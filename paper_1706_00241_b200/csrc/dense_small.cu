@@ -18,6 +18,8 @@
 #define SD_NT 512
 // pencils up to this order keep all working matrices in shared memory (4 T^2 doubles)
 #define DCG_PENCIL_SMEM_T 80
+// the pencil runs one warp per Jacobi pair: 32 warps cover T <= 64
+#define PENCIL_NT 1024
 
 // ---------------------------------------------------------------------------
 // Cholesky with the reference's pivot rule (acc <= pivot_tol fails at j).
@@ -26,22 +28,26 @@
 // ---------------------------------------------------------------------------
 __device__ int cta_cholesky(const double* A, int lda, int n, double pivot_tol, double* L, int ldl,
                             double* s_scal) {
-    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-        const int i = e / n, j = e % n;
-        if (j > i) L[i * ldl + j] = 0.0;
+    // Right-looking in place in L: after column t is final, every trailing
+    // element (i, c), t < c <= i, subtracts L_it L_ct.  Each element therefore
+    // sees its subtractions in ascending t, rounded separately - the same
+    // arithmetic as the reference's left-looking dot products
+    // (_core.pyx:47-66) - but a column costs three CTA barriers and one
+    // parallel trailing update instead of a serial diagonal chain.
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    for (int e = tid; e < n * n; e += blockDim.x) {
+        const int i = e / n, c = e - (e / n) * n;
+        L[i * ldl + c] = (c <= i) ? A[i * lda + c] : 0.0;
     }
     cta_sync();
     for (int j = 0; j < n; ++j) {
-        if (threadIdx.x == 0) {
-            double acc = A[j * lda + j];
-            for (int t = 0; t < j; ++t) acc = sub_rn(acc, mul_rn(L[j * ldl + t], L[j * ldl + t]));
+        if (tid == 0) {
+            const double acc = L[j * ldl + j];
             if (acc <= pivot_tol) {
                 s_scal[0] = 1.0;
             } else {
                 s_scal[0] = 0.0;
-                const double ljj = sqrt(acc);
-                s_scal[1] = ljj;
-                L[j * ldl + j] = ljj;
+                L[j * ldl + j] = sqrt(acc);
             }
         }
         cta_sync();
@@ -49,11 +55,13 @@ __device__ int cta_cholesky(const double* A, int lda, int n, double pivot_tol, d
             cta_sync();
             return j;
         }
-        const double ljj = s_scal[1];
-        for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) {
-            double acc = A[i * lda + j];
-            for (int t = 0; t < j; ++t) acc = sub_rn(acc, mul_rn(L[i * ldl + t], L[j * ldl + t]));
-            L[i * ldl + j] = div_rn(acc, ljj);
+        const double ljj = L[j * ldl + j];
+        for (int i = j + 1 + tid; i < n; i += blockDim.x) L[i * ldl + j] = div_rn(L[i * ldl + j], ljj);
+        cta_sync();
+        for (int i = j + 1 + warp; i < n; i += nw) {
+            const double lij = L[i * ldl + j];
+            for (int c = j + 1 + lane; c <= i; c += 32)
+                L[i * ldl + c] = sub_rn(L[i * ldl + c], mul_rn(lij, L[c * ldl + j]));
         }
         cta_sync();
     }
@@ -170,6 +178,135 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
     r = r * fma(-hx * r, r, 1.5);
     r = r * fma(-hx * r, r, 1.5);
     return r;
+}
+
+// Rotation (c, s, mode) of the pair in circle slot `slot` for `round` from
+// the current matrix: mode 0 identity (padding player), 1 zero a_pq (skip
+// rule), 2 rotate.  Deterministic: every thread that needs a slot's rotation
+// computes the same bits.
+__device__ __forceinline__ void jac_rotation(const double* A, int T, int Te, int slot, int round, int& p, int& q,
+                                             int& mode, double& c, double& sn) {
+    int pa = slot == 0 ? Te - 1 : slot - 1 + round;
+    if (slot != 0 && pa >= Te - 1) pa -= Te - 1;
+    int pb = Te - 2 - slot + round;
+    if (pb >= Te - 1) pb -= Te - 1;
+    p = min(pa, pb);
+    q = max(pa, pb);
+    c = 1.0;
+    sn = 0.0;
+    mode = 0;
+    if (q >= T) return;
+    const double apq = A[p * T + q];
+    const double app = A[p * T + p], aqq = A[q * T + q];
+    const double g = 100.0 * fabs(apq);
+    if (add_rn(fabs(app), g) == fabs(app) && add_rn(fabs(aqq), g) == fabs(aqq)) {
+        mode = 1;
+    } else if (apq != 0.0) {
+        const double tau = (aqq - app) * fast_rcp(2.0 * apq);
+        const double at = fabs(tau);
+        double t;
+        if (at < 1e100) {
+            const double w = fma(tau, tau, 1.0);
+            t = fast_rcp(at + w * fast_rsqrt(w));
+        } else {
+            t = 0.5 * fast_rcp(at);
+        }
+        if (tau < 0.0) t = -t;
+        c = fast_rsqrt(fma(t, t, 1.0));
+        sn = t * c;
+        mode = 2;
+    }
+}
+
+// Double-buffered variant: a round reads A (current) and writes Anext, every
+// thread recomputing the rotations of its own row and column pairs, so a
+// round needs one CTA barrier instead of two and no rotation broadcast.
+// Same rotations, same order of application as cta_jacobi; the result is
+// left in A.  `Anext` holds T * T doubles of shared memory.
+__device__ int cta_jacobi2(double* A, double* Anext, double* V, int T, int max_sweeps, double rtol, double* red) {
+    const int tid = threadIdx.x;
+    __shared__ int s_result2;
+    for (int e = tid; e < T * T; e += blockDim.x) V[e] = (e / T == e % T) ? 1.0 : 0.0;
+    double f2 = 0.0;
+    for (int e = tid; e < T * T; e += blockDim.x) f2 = fma(A[e], A[e], f2);
+    const double frob = sqrt(block_sum(f2, red));
+    if (frob == 0.0) return 0;   // zeros and identity (linalg.py:153-154)
+    const int Te = T + (T & 1);
+    const int np = Te / 2;
+    const int nblk = np * np;
+    double* cur = A;
+    double* nxt = Anext;
+    auto offdiag = [&]() {
+        double o2 = 0.0;
+        for (int e = tid; e < T * T; e += blockDim.x) {
+            const int i = e / T, j = e - (e / T) * T;
+            if (i != j) o2 = fma(cur[e], cur[e], o2);
+        }
+        return sqrt(block_sum(o2, red));
+    };
+    bool converged = offdiag() <= rtol * frob;
+    for (int sweep = 0; sweep < max_sweeps && !converged; ++sweep) {
+        for (int round = 0; round < Te - 1; ++round) {
+            for (int blk = tid; blk < nblk; blk += blockDim.x) {
+                const int ba = blk / np, bb = blk - (blk / np) * np;
+                int pa0, pa1, ma, pb0, pb1, mb;
+                double ca, sa, cb, sb;
+                jac_rotation(cur, T, Te, ba, round, pa0, pa1, ma, ca, sa);
+                if (bb == ba) {
+                    pb0 = pa0; pb1 = pa1; mb = ma; cb = ca; sb = sa;
+                } else {
+                    jac_rotation(cur, T, Te, bb, round, pb0, pb1, mb, cb, sb);
+                }
+                const bool ra1v = pa1 < T, cb1v = pb1 < T;
+                double x00 = cur[pa0 * T + pb0];
+                double x01 = cb1v ? cur[pa0 * T + pb1] : 0.0;
+                double x10 = ra1v ? cur[pa1 * T + pb0] : 0.0;
+                double x11 = (ra1v && cb1v) ? cur[pa1 * T + pb1] : 0.0;
+                if (mb == 2) {
+                    const double y00 = sub_rn(mul_rn(cb, x00), mul_rn(sb, x01));
+                    const double y01 = add_rn(mul_rn(sb, x00), mul_rn(cb, x01));
+                    const double y10 = sub_rn(mul_rn(cb, x10), mul_rn(sb, x11));
+                    const double y11 = add_rn(mul_rn(sb, x10), mul_rn(cb, x11));
+                    x00 = y00; x01 = y01; x10 = y10; x11 = y11;
+                }
+                if (ma == 2) {
+                    const double y00 = sub_rn(mul_rn(ca, x00), mul_rn(sa, x10));
+                    const double y10 = add_rn(mul_rn(sa, x00), mul_rn(ca, x10));
+                    const double y01 = sub_rn(mul_rn(ca, x01), mul_rn(sa, x11));
+                    const double y11 = add_rn(mul_rn(sa, x01), mul_rn(ca, x11));
+                    x00 = y00; x01 = y01; x10 = y10; x11 = y11;
+                }
+                if (ba == bb && ma != 0) { x01 = 0.0; x10 = 0.0; }
+                nxt[pa0 * T + pb0] = x00;
+                if (cb1v) nxt[pa0 * T + pb1] = x01;
+                if (ra1v) nxt[pa1 * T + pb0] = x10;
+                if (ra1v && cb1v) nxt[pa1 * T + pb1] = x11;
+                // V <- V R' for pair bb on rows ba and ba + np (in place: each
+                // (row, pair) belongs to exactly one block thread)
+                if (mb == 2) {
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int vi = ba + u * np;
+                        if (vi < T) {
+                            const double vp = V[vi * T + pb0], vq = V[vi * T + pb1];
+                            V[vi * T + pb0] = sub_rn(mul_rn(cb, vp), mul_rn(sb, vq));
+                            V[vi * T + pb1] = add_rn(mul_rn(sb, vp), mul_rn(cb, vq));
+                        }
+                    }
+                }
+            }
+            cta_sync();
+            double* t = cur;
+            cur = nxt;
+            nxt = t;
+        }
+        converged = offdiag() <= rtol * frob;
+    }
+    if (cur != A)
+        for (int e = tid; e < T * T; e += blockDim.x) A[e] = cur[e];
+    if (tid == 0) s_result2 = converged ? 0 : max_sweeps;
+    cta_sync();
+    return s_result2;
 }
 
 __device__ int cta_jacobi(double* A, double* V, int T, int max_sweeps, double rtol, double* red,
@@ -355,6 +492,113 @@ __global__ void __launch_bounds__(SD_NT) gram_factor_kernel(const double* Graw, 
     }
 }
 
+// ---------------------------------------------------------------------------
+// One-sided (Hestenes) Jacobi for C = L^-1 G L^-T without forming C.
+// With G = R R' (lower R) and X = (L^-1 R)', X'X = C; rotating pairs of X's
+// columns with the rotation two-sided Jacobi would apply to C (computed from
+// the pair's 2 x 2 Gram [x_p'x_p x_p'x_q; x_p'x_q x_q'x_q], same skip rule,
+// same formulas) orthogonalises the columns: theta_c = ||x_c||^2, V holds the
+// accumulated rotations.  A pair belongs to one warp (lanes own rows lane and
+// lane + 32): the rotation never leaves the warp, so a round is one CTA
+// barrier.  Convergence: off(X'X) <= rtol ||C||_F before every sweep
+// (linalg.py:156-163).  X: column c at X + c * n (T <= 64); Vc column-major.
+// ---------------------------------------------------------------------------
+__device__ int cta_jacobi_onesided(double* X, double* Vc, int n, int max_sweeps, double rtol, double* red) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    __shared__ int s_res1;
+    for (int e = tid; e < n * n; e += blockDim.x) Vc[e] = (e / n == e - (e / n) * n) ? 1.0 : 0.0;
+    const int i0 = lane, i1 = lane + 32;
+    auto gram = [&](double* frob2) {
+        // off^2 = sum_{p != q} (x_p'x_q)^2 ; frob^2 = sum_{p,q} (x_p'x_q)^2.
+        // Warp per p, lanes over q >= p, each dot sequential over the rows.
+        double off2 = 0.0, all2 = 0.0;
+        for (int p = warp; p < n; p += nw) {
+            const double* xp = X + p * n;
+            for (int q = p + lane; q < n; q += 32) {
+                const double* xq = X + q * n;
+                double d = 0.0;
+                for (int i = 0; i < n; ++i) d = fma(xp[i], xq[i], d);
+                if (q == p) {
+                    all2 = fma(d, d, all2);
+                } else {
+                    off2 = fma(2.0 * d, d, off2);
+                    all2 = fma(2.0 * d, d, all2);
+                }
+            }
+        }
+        off2 = block_sum(off2, red);
+        all2 = block_sum(all2, red);
+        if (frob2) *frob2 = all2;
+        return sqrt(off2);
+    };
+    double frob2 = 0.0;
+    double off = gram(&frob2);
+    const double frob = sqrt(frob2);
+    if (frob == 0.0) return 0;
+    bool converged = off <= rtol * frob;
+    const int Te = n + (n & 1), np = Te / 2;
+    for (int sweep = 0; sweep < max_sweeps && !converged; ++sweep) {
+        for (int round = 0; round < Te - 1; ++round) {
+            // each pair's warp forms the pair's 2 x 2 Gram, computes the
+            // rotation (redundantly on its lanes: no broadcast) and rotates
+            for (int slot = warp; slot < np; slot += nw) {
+                int pa = slot == 0 ? Te - 1 : slot - 1 + round;
+                if (slot != 0 && pa >= Te - 1) pa -= Te - 1;
+                int pb = Te - 2 - slot + round;
+                if (pb >= Te - 1) pb -= Te - 1;
+                const int p = min(pa, pb), q = max(pa, pb);
+                if (q >= n) continue;
+                const double xp0 = i0 < n ? X[p * n + i0] : 0.0, xp1 = i1 < n ? X[p * n + i1] : 0.0;
+                const double xq0 = i0 < n ? X[q * n + i0] : 0.0, xq1 = i1 < n ? X[q * n + i1] : 0.0;
+                double app = fma(xp1, xp1, xp0 * xp0);
+                double aqq = fma(xq1, xq1, xq0 * xq0);
+                double apq = fma(xp1, xq1, xp0 * xq0);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    app += __shfl_xor_sync(0xffffffffu, app, o);
+                    aqq += __shfl_xor_sync(0xffffffffu, aqq, o);
+                    apq += __shfl_xor_sync(0xffffffffu, apq, o);
+                }
+                const double g = 100.0 * fabs(apq);
+                if (add_rn(fabs(app), g) == fabs(app) && add_rn(fabs(aqq), g) == fabs(aqq)) continue;
+                if (apq == 0.0) continue;
+                const double tau = (aqq - app) * fast_rcp(2.0 * apq);
+                const double at = fabs(tau);
+                double t;
+                if (at < 1e100) {
+                    const double w = fma(tau, tau, 1.0);
+                    t = fast_rcp(at + w * fast_rsqrt(w));
+                } else {
+                    t = 0.5 * fast_rcp(at);
+                }
+                if (tau < 0.0) t = -t;
+                const double c = fast_rsqrt(fma(t, t, 1.0));
+                const double sn = t * c;
+                if (i0 < n) {
+                    X[p * n + i0] = sub_rn(mul_rn(c, xp0), mul_rn(sn, xq0));
+                    X[q * n + i0] = add_rn(mul_rn(sn, xp0), mul_rn(c, xq0));
+                    const double vp = Vc[p * n + i0], vq = Vc[q * n + i0];
+                    Vc[p * n + i0] = sub_rn(mul_rn(c, vp), mul_rn(sn, vq));
+                    Vc[q * n + i0] = add_rn(mul_rn(sn, vp), mul_rn(c, vq));
+                }
+                if (i1 < n) {
+                    X[p * n + i1] = sub_rn(mul_rn(c, xp1), mul_rn(sn, xq1));
+                    X[q * n + i1] = add_rn(mul_rn(sn, xp1), mul_rn(c, xq1));
+                    const double vp = Vc[p * n + i1], vq = Vc[q * n + i1];
+                    Vc[p * n + i1] = sub_rn(mul_rn(c, vp), mul_rn(sn, vq));
+                    Vc[q * n + i1] = add_rn(mul_rn(sn, vp), mul_rn(c, vq));
+                }
+            }
+            cta_sync();
+        }
+        off = gram(nullptr);
+        converged = off <= rtol * frob;
+    }
+    if (tid == 0) s_res1 = converged ? 0 : max_sweeps;
+    cta_sync();
+    return s_res1;
+}
+
 // ===========================================================================
 // Harmonic pencil: symmetrise F, G; prune F's failing-pivot columns; solve
 // G u = theta F u (gen_sym_eigen, linalg.py:168-191); select k values.
@@ -364,7 +608,7 @@ __global__ void __launch_bounds__(SD_NT) gram_factor_kernel(const double* Graw, 
 // `plan` (when non-null) carries the pencil order T (= count) decided on the
 // device by the extraction's zero-column scan, and its status: the kernel does
 // nothing unless that status is DCG_OK, so the pipeline needs no host sync.
-__global__ void __launch_bounds__(SD_NT) ritz_pencil_kernel(const double* Fraw, const double* Graw, int T,
+__global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fraw, const double* Graw, int T,
                                                             int k, int largest, int max_sweeps,
                                                             double* wk, double* theta, double* U,
                                                             int* active, DevStatus* st, const DevStatus* plan) {
@@ -422,6 +666,51 @@ __global__ void __launch_bounds__(SD_NT) ritz_pencil_kernel(const double* Fraw, 
         }
         cta_sync();
     }
+    double* A = staged ? sm + 3 * T * T : sm;
+    double* V = staged ? sm : sm + T * T;
+    bool onesided = false;
+    if (staged && na <= 64) {
+        // G (compact) -> S0, R = chol(G) -> S2, X = (L^-1 R)' in place in S2
+        for (int e = tid; e < na * na; e += blockDim.x) {
+            const int i = e / na, j = e % na;
+            Fa[e] = G[s_act[i] * T + s_act[j]];
+        }
+        cta_sync();
+        if (cta_cholesky(Fa, na, na, 0.0, Y, na, s_scal) < 0) {
+            onesided = true;
+            // B = L^-1 R, right-looking over rows (lower triangular B, row-major = X column-major)
+            for (int j = 0; j < na; ++j) {
+                for (int c = tid; c <= j; c += blockDim.x) Y[j * na + c] = div_rn(Y[j * na + c], L[j * na + j]);
+                cta_sync();
+                for (int i = j + 1 + warp; i < na; i += nw) {
+                    const double lij = L[i * na + j];
+                    for (int c = lane; c <= j; c += 32) Y[i * na + c] = sub_rn(Y[i * na + c], mul_rn(lij, Y[j * na + c]));
+                }
+                cta_sync();
+            }
+        }
+        cta_sync();
+    }
+    int nc;
+    if (onesided) {
+        // Vc (column-major) in S3; afterwards theta on the diagonal of A := S2 and V row-major in S0
+        double* Vc = A;
+        nc = cta_jacobi_onesided(Y, Vc, na, max_sweeps, 1e-14, red);
+        if (nc == 0) {
+            for (int c = warp; c < na; c += nw) {
+                const double x0 = lane < na ? Y[c * na + lane] : 0.0, x1 = lane + 32 < na ? Y[c * na + lane + 32] : 0.0;
+                const double th = warp_sum(fma(x1, x1, x0 * x0));
+                __syncwarp();
+                if (lane == 0) Y[c * na + c] = th;
+            }
+            for (int e = tid; e < na * na; e += blockDim.x) {
+                const int i = e / na, c = e % na;
+                V[i * na + c] = Vc[c * na + i];
+            }
+            cta_sync();
+            A = Y;
+        }
+    } else {
     // compact Ga (solved in place into Y below)
     double* Ga = staged ? Y : Fa;
     for (int e = tid; e < na * na; e += blockDim.x) {
@@ -433,8 +722,6 @@ __global__ void __launch_bounds__(SD_NT) ritz_pencil_kernel(const double* Fraw, 
     for (int c = warp; c < na; c += nw) warp_solve_lower(L, na, na, Ga + c, na, Y + c, na);
     cta_sync();
     // C = L^-1 Y'  -> into shared A
-    double* A = staged ? sm + 3 * T * T : sm;
-    double* V = staged ? sm : sm + T * T;
     for (int c = warp; c < na; c += nw) warp_solve_lower(L, na, na, Y + c * na, 1, A + c, na);
     cta_sync();
     // symmetrise
@@ -447,7 +734,10 @@ __global__ void __launch_bounds__(SD_NT) ritz_pencil_kernel(const double* Fraw, 
         }
     }
     cta_sync();
-    const int nc = cta_jacobi(A, V, na, max_sweeps, 1e-14, red, s_c, s_s, s_mode);
+    // staged: the Ga / Y slot (S2) is free again and double-buffers the Jacobi
+    nc = staged ? cta_jacobi2(A, Y, V, na, max_sweeps, 1e-14, red)
+                : cta_jacobi(A, V, na, max_sweeps, 1e-14, red, s_c, s_s, s_mode);
+    }
     if (nc) {
         if (tid == 0) { st->status = DCG_E_NO_CONVERGENCE; st->info = nc; st->count = na; }
         return;
@@ -660,7 +950,7 @@ int dcg_ritz_pencil_launch(cudaStream_t st, const double* Fraw, const double* Gr
                            const DevStatus* plan) {
     const size_t smem = pencil_smem(T);
     DCG_CUDA(cudaFuncSetAttribute(ritz_pencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    ritz_pencil_kernel<<<1, SD_NT, smem, st>>>(Fraw, Graw, T, k, largest, max_sweeps, wk, theta, U, active, ds,
+    ritz_pencil_kernel<<<1, PENCIL_NT, smem, st>>>(Fraw, Graw, T, k, largest, max_sweeps, wk, theta, U, active, ds,
                                                 plan);
     DCG_LAUNCHED();
     return DCG_OK;

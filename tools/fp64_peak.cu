@@ -1,0 +1,60 @@
+// FP64 FMA peak of this GPU (DFMA pipe), for the matrix-free operator's
+// roofline: every thread runs 8 independent FMA chains, 148 x 8 CTAs of 256
+// threads, timed with CUDA events after a warm-up.  Prints one JSON line.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/_build/fp64_peak tools/fp64_peak.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void dfma_kernel(double* out, int iters, double a, double b) {
+    double c[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) c[u] = threadIdx.x * 1e-3 + u;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c[u] = fma(c[u], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += c[u];
+    if (s == 12345.678) out[0] = s;   // keep the chains alive
+}
+
+__global__ void exp_kernel(double* out, int iters, double a) {
+    double s = threadIdx.x * 1e-6;
+    double t = 0.0;
+    for (int i = 0; i < iters; ++i) {
+        t += exp(-s);
+        s = fma(s, a, 1e-9);
+    }
+    if (t == 12345.678) out[0] = t;
+}
+
+int main() {
+    int dev = 0, sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    double* d;
+    cudaMalloc(&d, 8);
+    const int blocks = sms * 8, threads = 256, iters = 1 << 16;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    dfma_kernel<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
+    cudaEventRecord(e0);
+    dfma_kernel<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double flops = 2.0 * 8.0 * iters * (double)blocks * threads;
+    exp_kernel<<<blocks, threads>>>(d, iters / 8, 0.9999);
+    cudaEventRecord(e0);
+    exp_kernel<<<blocks, threads>>>(d, iters / 8, 0.9999);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms2 = 0.f;
+    cudaEventElapsedTime(&ms2, e0, e1);
+    const double exps = (double)(iters / 8) * blocks * threads;
+    printf("{\"fp64_fma_tflops\": %.3f, \"fp64_exp_per_s\": %.4g, \"sms\": %d, \"dfma_ms\": %.3f, \"exp_ms\": %.3f}\n",
+           flops / (ms * 1e-3) / 1e12, exps / (ms2 * 1e-3), sms, ms, ms2);
+    return 0;
+}

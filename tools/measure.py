@@ -4,6 +4,7 @@
   python tools/measure.py config1        GPC Newton sequence n=2000, k=8 (BASELINE configs[0])
   python tools/measure.py config2-cg     config 2 with plain CG (k=0) for the def-CG vs CG comparison
   python tools/measure.py config4 [n]    GP-regression hyperparameter sweep, 20 lengthscales, k=24
+  python tools/measure.py config5 [n]    matrix-free RBF operator (K7), d=16, ell=3, k=32 (1 GPU)
 
 Each prints one JSON line: device time (CUDA events) of the whole sequence,
 iterations, iterations/s, and a CPU sample of the reference algorithm (oracle
@@ -115,6 +116,42 @@ def cpu_sweep_sample(n, iters=5, n_cpu=12000):
                       + (f", extrapolated x(n_cpu/n)^2 = {scale:.3f} to n={n}" if m < n else "")}
 
 
+def config5(n, d=16, ell=3.0, k=32, iters=20):
+    """Matrix-free RBF operator (K7) at n points: device time of one product
+    (CUDA events), FLOP_alg per product n^2 (2d + 4) (exp
+    counted separately), and a def-CG solve of the first GPC Newton system
+    with a random k-column basis (iterations, time per iteration)."""
+    import torch
+
+    import paper_1706_00241_b200 as P
+    from oracle.defcg_oracle import gpc_inputs
+
+    rng = np.random.default_rng(0)
+    x = torch.from_numpy(rng.standard_normal((n, d))).cuda()
+    op = P.rbf_kernel(x, P.KernelParams(1.0, ell), matrix_free=True)
+    v = torch.from_numpy(rng.standard_normal(n)).cuda()
+    y = op.matvec_dev(v)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(3):
+        op.matvec_dev(v, out=y)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 3
+    flop = float(n) * n * (2 * d + 4)
+    s = torch.from_numpy(rng.uniform(0.2, 0.5, n)).cuda()
+    a = op.scaled(s, 1.0)
+    b = torch.from_numpy(rng.standard_normal(n)).cuda()
+    cfg = P.SolverConfig(tol=1e-8, ell=k + 4, max_iters=iters)
+    basis = P.refresh_basis(a, torch.from_numpy(rng.standard_normal((n, k))).cuda())
+    _, rep, _ = P.deflated_cg_solve(a, b, torch.zeros(n, dtype=torch.float64, device="cuda"), basis, cfg)
+    return {"n": n, "d": d, "matvec_ms": ms, "flop_alg_per_matvec": flop, "achieved_tflops": flop / (ms / 1e3) / 1e12,
+            "exp_per_s": float(n) * n / (ms / 1e3), "solve_iterations": rep.iterations,
+            "solve_ms_per_iteration": rep.device_ms / (rep.iterations + 2),
+            "note": "row-owned matrix-free GEMV: every pair evaluated twice (no symmetric halving yet)"}
+
+
 def main():
     what = sys.argv[1]
     if what == "config1":
@@ -126,6 +163,9 @@ def main():
         n = int(sys.argv[2]) if len(sys.argv) > 2 else 30000
         out = sweep(n)
         out["cpu_baseline"] = cpu_sweep_sample(n)
+    elif what == "config5":
+        n = int(sys.argv[2]) if len(sys.argv) > 2 else 50000
+        out = config5(n)
     else:
         raise SystemExit(__doc__)
     out["workload"] = what
