@@ -417,11 +417,21 @@ __device__ __forceinline__ void sym_pass2(long long n, const double* colpart, co
             double a[16];
 #pragma unroll
             for (int q = 0; q < 16; ++q) a[q] = 0.0;
-            for (long long Ib = I + 1 + sub; Ib < NT; Ib += 16LL * S) {
+            // tiles (Ip, I), Ip = I + 1 + sub + S u: base(Ip + S) - base(Ip) =
+            // S Ip + S (S + 1) / 2, so the next partial is one pointer add away
+            // (the 64-bit row-base products dominated this loop otherwise)
+            const int NTi = (int)NT;
+            int Ip = (int)I + 1 + sub;
+            const double* ptr = colpart + (sym_tile_row_base(Ip) + I) * DCG_TB + r;
+            const long long sstep = (long long)S * (S + 1) / 2;
+            while (Ip < NTi) {
 #pragma unroll
                 for (int q = 0; q < 16; ++q) {
-                    const long long Ip = Ib + (long long)q * S;
-                    if (Ip < NT) a[q] += ld_cg(colpart + (sym_tile_row_base(Ip) + I) * DCG_TB + r);
+                    if (Ip < NTi) {
+                        a[q] += ld_cg(ptr);
+                        ptr += ((long long)S * Ip + sstep) * DCG_TB;
+                        Ip += S;
+                    }
                 }
             }
 #pragma unroll
