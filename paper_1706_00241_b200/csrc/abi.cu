@@ -338,7 +338,8 @@ extern "C" int dcg_gen_sym_eigen(dcg_context* ctx, void* stream, const double* d
 // ---------------------------------------------------------------------------
 int dcg_rbf_mf_check(const dcg_operator* op);
 int dcg_rbf_mf_apply(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, const double* v, const double* s_in,
-                     const double* s_out, double shift, double* y);
+                     const double* s_out, double shift, double* y, double* scratch);
+size_t dcg_rbf_mf_scratch_doubles(const dcg_operator* op);
 int dcg_rbf_mf_block(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, const double* X, int k,
                      const double* s_in, const double* s_out, double shift, double* Y);
 
@@ -355,11 +356,12 @@ static int check_dense_op(const dcg_operator* op) {
 // y = shift v + s_out (.) K (s_in (.) v) over the operator's storage strategy;
 // `scratch` holds apply_k_scratch(op) doubles (workspace reserved by the caller).
 static size_t apply_k_scratch(const dcg_operator* op) {
+    if (op->kind == DCG_OP_RBF) return dcg_rbf_mf_scratch_doubles(op);
     return op->kind == DCG_OP_DENSE_SYM ? dcg_sym_apply_scratch_doubles(op->n) : 0;
 }
 static int apply_k(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, const double* v, const double* s_in,
                    const double* s_out, double shift, double* y, double* scratch) {
-    if (op->kind == DCG_OP_RBF) return dcg_rbf_mf_apply(ctx, st, op, v, s_in, s_out, shift, y);
+    if (op->kind == DCG_OP_RBF) return dcg_rbf_mf_apply(ctx, st, op, v, s_in, s_out, shift, y, scratch);
     // the lower-triangle strategy stages 16-byte slices of v and s_in
     if (op->kind == DCG_OP_DENSE_SYM && aligned16(v) && aligned16(s_in))
         return dcg_sym_apply(ctx, st, op->d_k, op->ldk, op->n, v, s_in, s_out, shift, y, scratch);

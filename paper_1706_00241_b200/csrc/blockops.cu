@@ -97,6 +97,14 @@ int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, long long 
     return DCG_OK;
 }
 
+// pass 2 alone (the matrix-free operator's symmetric pass 1 produces the same partials)
+int dcg_sym_pass2_launch(cudaStream_t st, int G, long long n, const double* colpart, const double* rowpart,
+                         const double* v, const double* s_out, double shift, double* y) {
+    sym_pass2_kernel<<<G, DCG_NT, 0, st>>>(n, colpart, rowpart, v, s_out, shift, y);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}
+
 // =============================================================================
 // K3: Y(rows x k) = K(rows x n) V(n x k) with mma.sync.m8n8k4 FP64.
 // CTA = 8 warps = 64 rows x all k columns; blockIdx.y splits the inner

@@ -49,6 +49,8 @@ __global__ void __launch_bounds__(DCG_NT, 1)
     double* xjt = xit + p.dim * MF_TB;
     double* vj = xjt + p.dim * MF_TB;            // 64 x MF_KC
     double* red = vj + MF_TB * MF_KC;            // NW x 64
+    double* nI = red + DCG_NW * MF_TB;           // 64 row norms of the I chunk
+    double* nJ = nI + MF_TB;                     // 64 row norms of the J tile
     const long long nchunks = (rows + MF_TB - 1) / MF_TB;
     for (long long c = blockIdx.x; c < nchunks; c += gridDim.x) {
         const long long i0 = row0 + c * MF_TB, r1 = min(row0 + rows, i0 + MF_TB);
@@ -56,6 +58,8 @@ __global__ void __launch_bounds__(DCG_NT, 1)
             const int kc = min(MF_KC, k - c0);
             cta_sync();
             rbf_stage_rows(p, i0, r1, xit);
+            cta_sync();
+            rbf_stage_norms(p, xit, nI);
             double acc[2][MF_KC];
 #pragma unroll
             for (int r = 0; r < 2; ++r)
@@ -75,8 +79,10 @@ __global__ void __launch_bounds__(DCG_NT, 1)
                     vj[jr * MF_KC + q] = vv;
                 }
                 cta_sync();
+                rbf_stage_norms(p, xjt, nJ);
+                cta_sync();
                 double kv[2][4];
-                rbf_tile_values(p, xit, xjt, i0, j0, r1, kv);
+                rbf_tile_values(p, xit, xjt, i0, j0, r1, kv, nI, nJ);
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc) {
                     const double* vr = vj + (4 * warp + cc) * MF_KC;
@@ -108,6 +114,13 @@ __global__ void __launch_bounds__(DCG_NT, 1)
     }
 }
 
+__global__ void __launch_bounds__(DCG_NT, 1)
+    rbf_sym_pass1_kernel(RbfParams p, const double* v, const double* s_in, double* colpart, double* rowpart) {
+    extern __shared__ __align__(16) double smem[];
+    rbf_sym_init(smem, p);
+    rbf_sym_pass1(p, v, s_in, colpart, rowpart, smem);
+}
+
 int grid_for(const dcg_context* ctx, long long rows) {
     long long nchunks = (rows + MF_TB - 1) / MF_TB;
     if (nchunks > ctx->sm_count) nchunks = ctx->sm_count;
@@ -126,11 +139,31 @@ int dcg_rbf_mf_check(const dcg_operator* op) {
 
 size_t dcg_rbf_mf_smem(int dim) { return sizeof(double) * (size_t)rbf_mf_smem_doubles(dim); }
 
+int dcg_sym_pass2_launch(cudaStream_t st, int G, long long n, const double* colpart, const double* rowpart,
+                         const double* v, const double* s_out, double shift, double* y);
+size_t dcg_sym_apply_scratch_doubles(long long n);
+
+size_t dcg_rbf_mf_scratch_doubles(const dcg_operator* op) {
+    return (op->row0 == 0 && op->rows == op->n) ? dcg_sym_apply_scratch_doubles(op->n) : 0;
+}
+
 int dcg_rbf_mf_apply(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, const double* v, const double* s_in,
-                     const double* s_out, double shift, double* y) {
+                     const double* s_out, double shift, double* y, double* scratch) {
     int rc = dcg_rbf_mf_check(op);
     if (rc) return rc;
     if (op->rows == 0) return DCG_OK;
+    if (scratch && op->row0 == 0 && op->rows == op->n) {
+        // unsharded: symmetric half-evaluation + the stored strategy's pass 2
+        const long long n = op->n;
+        const int G = ctx->sm_count < DCG_SYM_MAX_CTAS ? ctx->sm_count : DCG_SYM_MAX_CTAS;
+        const size_t smem = sizeof(double) * (size_t)rbf_sym_smem_doubles((int)op->dim);
+        DCG_CUDA(cudaFuncSetAttribute(rbf_sym_pass1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        double* colpart = scratch;
+        double* rowpart = scratch + sym_ntiles(n) * DCG_TB;
+        rbf_sym_pass1_kernel<<<G, DCG_NT, smem, st>>>(params_of(op), v, s_in, colpart, rowpart);
+        DCG_LAUNCHED();
+        return dcg_sym_pass2_launch(st, G, n, colpart, rowpart, v, s_out, shift, y);
+    }
     const size_t smem = dcg_rbf_mf_smem((int)op->dim);
     DCG_CUDA(cudaFuncSetAttribute(rbf_mf_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     rbf_mf_gemv_kernel<<<grid_for(ctx, op->rows), DCG_NT, smem, st>>>(params_of(op), op->row0, op->rows, v, s_in,
@@ -144,7 +177,7 @@ int dcg_rbf_mf_block(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, 
     int rc = dcg_rbf_mf_check(op);
     if (rc) return rc;
     if (op->rows == 0 || k <= 0) return DCG_OK;
-    const size_t smem = sizeof(double) * (size_t)(2LL * op->dim * MF_TB + MF_TB * MF_KC + DCG_NW * MF_TB);
+    const size_t smem = sizeof(double) * (size_t)(2LL * op->dim * MF_TB + MF_TB * MF_KC + DCG_NW * MF_TB + 2 * MF_TB);
     DCG_CUDA(cudaFuncSetAttribute(rbf_mf_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     rbf_mf_block_kernel<<<grid_for(ctx, op->rows), DCG_NT, smem, st>>>(params_of(op), op->row0, op->rows, X, k, s_in,
                                                                        s_out, shift, Y);

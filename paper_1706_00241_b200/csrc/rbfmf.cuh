@@ -22,7 +22,7 @@
 
 // shared memory (doubles) of rbf_rows_gemv for data dimension `dim`
 __host__ __device__ __forceinline__ long long rbf_mf_smem_doubles(int dim) {
-    return 2LL * dim * MF_TB + MF_TB + DCG_NW * MF_TB;
+    return 2LL * dim * MF_TB + MF_TB + DCG_NW * MF_TB + 2 * MF_TB;
 }
 
 struct RbfParams {
@@ -33,28 +33,57 @@ struct RbfParams {
 };
 
 // the 8 kernel values of this thread in tile (rows gi0 + {2l, 2l+1}, cols gj0 + 4w + {0..3});
-// xit: dim x 64 (rows of the I chunk), xjt: dim x 64 (J tile); out-of-range -> 0
+// xit: dim x 64 (rows of the I chunk), xjt: dim x 64 (J tile); out-of-range -> 0.
+// With row norms nI / nJ (64 each) the squared distance is formed as
+// |x_i|^2 + |x_j|^2 - 2 x_i.x_j (one FMA per coordinate instead of a rounded
+// sub / mul / add; the cancellation error is ~eps |x|^2 absolute in the
+// exponent, ~1e-16 relative in K); with nI == nullptr it is the stored
+// builder's exact difference form (bit-identical elements).
 __device__ __forceinline__ void rbf_tile_values(const RbfParams& p, const double* xit, const double* xjt,
-                                                long long gi0, long long gj0, long long row_end, double k[2][4]) {
+                                                long long gi0, long long gj0, long long row_end, double k[2][4],
+                                                const double* nI = nullptr, const double* nJ = nullptr) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double acc[2][4];
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-    for (int t = 0; t < p.dim; ++t) {
-        const double2 xi = *reinterpret_cast<const double2*>(xit + t * MF_TB + 2 * lane);
-        const double2 xa = *reinterpret_cast<const double2*>(xjt + t * MF_TB + 4 * warp);
-        const double2 xb = *reinterpret_cast<const double2*>(xjt + t * MF_TB + 4 * warp + 2);
-        const double xr[2] = {xi.x, xi.y};
-        const double xc[4] = {xa.x, xa.y, xb.x, xb.y};
+    if (nI) {
+        for (int t = 0; t < p.dim; ++t) {
+            const double2 xi = *reinterpret_cast<const double2*>(xit + t * MF_TB + 2 * lane);
+            const double2 xa = *reinterpret_cast<const double2*>(xjt + t * MF_TB + 4 * warp);
+            const double2 xb = *reinterpret_cast<const double2*>(xjt + t * MF_TB + 4 * warp + 2);
+            const double xr[2] = {xi.x, xi.y};
+            const double xc[4] = {xa.x, xa.y, xb.x, xb.y};
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[r][c] = fma(xr[r], xc[c], acc[r][c]);
+        }
+        const double2 ni = *reinterpret_cast<const double2*>(nI + 2 * lane);
+        const double2 na = *reinterpret_cast<const double2*>(nJ + 4 * warp);
+        const double2 nb = *reinterpret_cast<const double2*>(nJ + 4 * warp + 2);
+        const double nr[2] = {ni.x, ni.y};
+        const double nc[4] = {na.x, na.y, nb.x, nb.y};
 #pragma unroll
         for (int r = 0; r < 2; ++r)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const double diff = sub_rn(xr[r], xc[c]);
-                acc[r][c] = add_rn(acc[r][c], mul_rn(diff, diff));
-            }
+            for (int c = 0; c < 4; ++c) acc[r][c] = fmax(0.0, fma(-2.0, acc[r][c], nr[r] + nc[c]));
+    } else {
+        for (int t = 0; t < p.dim; ++t) {
+            const double2 xi = *reinterpret_cast<const double2*>(xit + t * MF_TB + 2 * lane);
+            const double2 xa = *reinterpret_cast<const double2*>(xjt + t * MF_TB + 4 * warp);
+            const double2 xb = *reinterpret_cast<const double2*>(xjt + t * MF_TB + 4 * warp + 2);
+            const double xr[2] = {xi.x, xi.y};
+            const double xc[4] = {xa.x, xa.y, xb.x, xb.y};
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const double diff = sub_rn(xr[r], xc[c]);
+                    acc[r][c] = add_rn(acc[r][c], mul_rn(diff, diff));
+                }
+        }
     }
 #pragma unroll
     for (int r = 0; r < 2; ++r)
@@ -78,6 +107,15 @@ __device__ __forceinline__ void rbf_stage_rows(const RbfParams& p, long long g0,
     }
 }
 
+// squared norms of the staged rows (dim x 64 transposed) into nrm[64], fixed order
+__device__ __forceinline__ void rbf_stage_norms(const RbfParams& p, const double* xt, double* nrm) {
+    if (threadIdx.x < MF_TB) {
+        double a = 0.0;
+        for (int t = 0; t < p.dim; ++t) a = fma(xt[t * MF_TB + threadIdx.x], xt[t * MF_TB + threadIdx.x], a);
+        nrm[threadIdx.x] = a;
+    }
+}
+
 // t_i = sum_j K_ij (s_j v_j) for rows [r0, r1) (global indices); epi(i, t_i)
 // on one thread per row.  `smem` holds rbf_mf_smem_doubles(dim).  All CTA
 // threads call (contains CTA barriers).
@@ -89,13 +127,19 @@ __device__ void rbf_rows_gemv(const RbfParams& p, long long r0, long long r1, co
     double* xjt = xit + p.dim * MF_TB;
     double* vj = xjt + p.dim * MF_TB;
     double* red = vj + MF_TB;
+    double* nI = red + DCG_NW * MF_TB;
+    double* nJ = nI + MF_TB;
     for (long long i0 = r0; i0 < r1; i0 += MF_TB) {
         cta_sync();
         rbf_stage_rows(p, i0, r1, xit);
+        cta_sync();
+        rbf_stage_norms(p, xit, nI);
         double row[2] = {0.0, 0.0};
         for (long long j0 = 0; j0 < p.n; j0 += MF_TB) {
             cta_sync();
             rbf_stage_rows(p, j0, p.n, xjt);
+            cta_sync();
+            rbf_stage_norms(p, xjt, nJ);
             if (tid < MF_TB) {
                 const long long j = j0 + tid;
                 double vv = 0.0;
@@ -107,7 +151,7 @@ __device__ void rbf_rows_gemv(const RbfParams& p, long long r0, long long r1, co
             }
             cta_sync();
             double k[2][4];
-            rbf_tile_values(p, xit, xjt, i0, j0, r1, k);
+            rbf_tile_values(p, xit, xjt, i0, j0, r1, k, nI, nJ);
             const double2 va = *reinterpret_cast<const double2*>(vj + 4 * warp);
             const double2 vb = *reinterpret_cast<const double2*>(vj + 4 * warp + 2);
 #pragma unroll
@@ -127,6 +171,121 @@ __device__ void rbf_rows_gemv(const RbfParams& p, long long r0, long long r1, co
 #pragma unroll 4
             for (int w = 0; w < DCG_NW; ++w) t += red[w * MF_TB + tid];
             epi(i0 + tid, t);
+        }
+    }
+    cta_sync();
+}
+
+// ---------------------------------------------------------------------------
+// Symmetric half-evaluation (unsharded operators): each lower-triangle tile
+// (I, J <= I) is generated once and serves both its row sums (rows of I) and
+// its column sums (rows of J), exactly like the stored strategy's pass 1
+// (symgemv.cuh) - same tile partition, same partial layout, so pass 2 is
+// sym_pass2.  Half the exp / distance work of the row-owned form.
+// ---------------------------------------------------------------------------
+#include "symgemv.cuh"
+
+// staging region (>= 512 doubles: pass 2 reuses it as its reduction scratch)
+__host__ __device__ __forceinline__ long long rbf_sym_xregion(int dim) {
+    const long long x = 2LL * dim * MF_TB;
+    return x < DCG_NT ? DCG_NT : x;
+}
+__host__ __device__ __forceinline__ long long rbf_sym_smem_doubles(int dim) {
+    return rbf_sym_xregion(dim) + 3 * MF_TB + 2 * DCG_NW * DCG_TB + (DCG_SYM_MAX_CTAS + 1) + 2;
+}
+__device__ __forceinline__ long long* rbf_sym_table(double* smem, int dim) {
+    return reinterpret_cast<long long*>(smem + rbf_sym_xregion(dim) + 3 * MF_TB + 2 * DCG_NW * DCG_TB);
+}
+__device__ __forceinline__ void rbf_sym_init(double* smem, const RbfParams& p) {
+    sym_fill_range_table(rbf_sym_table(smem, p.dim), p.n);
+}
+
+static __device__ void rbf_sym_pass1(const RbfParams& p, const double* v, const double* s, double* colpart,
+                              double* rowpart, double* smem) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long n = p.n;
+    double* xit = smem;
+    double* xjt = xit + p.dim * MF_TB;
+    double* vj = smem + rbf_sym_xregion(p.dim);
+    double* nI = vj + MF_TB;
+    double* nJ = nI + MF_TB;
+    double* rowred = nJ + MF_TB;
+    const long long* tbl = rbf_sym_table(smem, p.dim);
+    const long long t0 = tbl[blockIdx.x], t1 = tbl[blockIdx.x + 1];
+    if (t0 >= t1) return;
+    const int ntiles = (int)(t1 - t0);
+    long long I = sym_tile_row(t0);
+    long long J = t0 - sym_tile_row_base(I);
+    long long staged_I = -1, norms_I = -1;
+    double xI0 = 0.0, xI1 = 0.0;
+    double row0 = 0.0, row1 = 0.0;
+    long long seg_start = t0;
+    int flush = 0;
+    for (int lt = 0; lt < ntiles; ++lt) {
+        cta_sync();   // the previous tile's reads of xit / xjt / vj are done
+        if (I != staged_I) {
+            rbf_stage_rows(p, I * MF_TB, n, xit);
+            staged_I = I;
+            xI0 = sym_xval(v, s, I * MF_TB + 2 * lane, n);
+            xI1 = sym_xval(v, s, I * MF_TB + 2 * lane + 1, n);
+        }
+        rbf_stage_rows(p, J * MF_TB, n, xjt);
+        if (tid < MF_TB) vj[tid] = sym_xval(v, s, J * MF_TB + tid, n);
+        cta_sync();
+        rbf_stage_norms(p, xjt, nJ);
+        if (I != norms_I) {
+            rbf_stage_norms(p, xit, nI);
+            norms_I = I;
+        }
+        cta_sync();
+        double k[2][4];
+        rbf_tile_values(p, xit, xjt, I * MF_TB, J * MF_TB, n, k, nI, nJ);
+        const double x0 = vj[4 * warp], x1 = vj[4 * warp + 1], x2 = vj[4 * warp + 2], x3 = vj[4 * warp + 3];
+        row0 = fma(k[0][0], x0, row0);
+        row0 = fma(k[0][1], x1, row0);
+        row0 = fma(k[0][2], x2, row0);
+        row0 = fma(k[0][3], x3, row0);
+        row1 = fma(k[1][0], x0, row1);
+        row1 = fma(k[1][1], x1, row1);
+        row1 = fma(k[1][2], x2, row1);
+        row1 = fma(k[1][3], x3, row1);
+        if (J < I) {
+            // column sums over the tile's 64 rows: warp reduce-scatter of 4 values
+            const double c0 = fma(k[1][0], xI1, k[0][0] * xI0);
+            const double c1 = fma(k[1][1], xI1, k[0][1] * xI0);
+            const double c2 = fma(k[1][2], xI1, k[0][2] * xI0);
+            const double c3 = fma(k[1][3], xI1, k[0][3] * xI0);
+            const bool hi16 = lane & 16;
+            const double r0 = __shfl_xor_sync(0xffffffffu, hi16 ? c0 : c2, 16);
+            const double r1 = __shfl_xor_sync(0xffffffffu, hi16 ? c1 : c3, 16);
+            const double k0 = (hi16 ? c2 : c0) + r0;
+            const double k1 = (hi16 ? c3 : c1) + r1;
+            const bool hi8 = lane & 8;
+            const double r2 = __shfl_xor_sync(0xffffffffu, hi8 ? k0 : k1, 8);
+            double cv = (hi8 ? k1 : k0) + r2;
+            cv += __shfl_xor_sync(0xffffffffu, cv, 4);
+            cv += __shfl_xor_sync(0xffffffffu, cv, 2);
+            cv += __shfl_xor_sync(0xffffffffu, cv, 1);
+            if ((lane & 7) == 0) colpart[(t0 + lt) * DCG_TB + 4 * warp + 2 * (lane >> 4) + ((lane >> 3) & 1)] = cv;
+        }
+        if (J == I || lt + 1 == ntiles) {   // end of a tile-row segment
+            double* rr = rowred + (flush & 1) * DCG_NW * DCG_TB;
+            rr[warp * DCG_TB + 2 * lane] = row0;
+            rr[warp * DCG_TB + 2 * lane + 1] = row1;
+            cta_sync();
+            if (tid < DCG_TB) {
+                double a = 0.0;
+#pragma unroll
+                for (int w = 0; w < DCG_NW; ++w) a += rr[w * DCG_TB + tid];
+                rowpart[seg_start * DCG_TB + tid] = a;
+            }
+            row0 = row1 = 0.0;
+            seg_start = t0 + lt + 1;
+            ++flush;
+        }
+        if (++J > I) {
+            ++I;
+            J = 0;
         }
     }
     cta_sync();

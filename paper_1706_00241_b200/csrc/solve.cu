@@ -165,7 +165,7 @@ enum { STRAT_ROWS = 0, STRAT_SYM = 1, STRAT_RBF = 2 };
 // Shared-memory doubles of the GEMV region for each strategy.
 __host__ __device__ __forceinline__ long long gemv_region_doubles(int strat, long long n, int dim) {
     if (strat == STRAT_SYM) return sym_smem_doubles();
-    if (strat == STRAT_RBF) return rbf_mf_smem_doubles(dim);
+    if (strat == STRAT_RBF) return rbf_sym_smem_doubles(dim);
     return min(n, (long long)DCG_QT) + 2 + DCG_NW * DCG_RB;
 }
 
@@ -215,16 +215,24 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         q0 = sym_row_begin(n, G, blockIdx.x);
         q1 = sym_row_begin(n, G, blockIdx.x + 1);
     }
+    if constexpr (STRAT == STRAT_RBF) {
+        rbf_sym_init(s_g, a.rbf);
+        q0 = sym_row_begin(n, G, blockIdx.x);
+        q1 = sym_row_begin(n, G, blockIdx.x + 1);
+    }
     // t = K (s (.) v) for the own rows [r0, r1); epi(i, t_i) per row.  The
     // symmetric strategy contains one extra grid barrier between its passes.
     // The matrix-free strategy computes whole 64-row chunks (c = b, b + G, ...),
     // again read by other CTAs only after a grid barrier.
     auto gemv = [&](const double* v, auto&& epi) {
         if constexpr (STRAT == STRAT_RBF) {
-            const long long nchunks = (n + MF_TB - 1) / MF_TB;
-            for (long long c = blockIdx.x; c < nchunks; c += G)
-                rbf_rows_gemv(a.rbf, c * MF_TB, min(n, (c + 1) * MF_TB), v, s, s_g, epi);
+            // symmetric half-evaluation of the regenerated tiles + the shared pass 2
+            rbf_sym_pass1(a.rbf, v, s, a.colpart, a.rowpart, s_g);
             PHASE(0);
+            GSYNC();
+            PHASE(1);
+            sym_pass2(n, a.colpart, a.rowpart, q0, q1, rbf_sym_table(s_g, a.rbf.dim), s_g, epi);
+            PHASE(2);
         } else if constexpr (STRAT == STRAT_SYM) {
             PHASE(15);
             unsigned long long tc0 = 0;
@@ -527,7 +535,7 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
     const int G = ctx->solve_blocks;
     const int ps = ((1 + k) + 1) & ~1;
     const size_t vec = sizeof(double) * (size_t)((n + 31) & ~31LL);
-    const size_t tiles = sym ? (size_t)sym_ntiles(n) : 0;
+    const size_t tiles = (strat != STRAT_ROWS) ? (size_t)sym_ntiles(n) : 0;
     const size_t need = 3 * vec + 2 * sizeof(double) * (size_t)G * ps + 1024 + 2 * sizeof(double) * tiles * DCG_TB;
     int rc = dcg_ws_reserve(ctx, need);
     if (rc) return rc;

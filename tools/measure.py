@@ -149,7 +149,7 @@ def config5(n, d=16, ell=3.0, k=32, iters=20):
     return {"n": n, "d": d, "matvec_ms": ms, "flop_alg_per_matvec": flop, "achieved_tflops": flop / (ms / 1e3) / 1e12,
             "exp_per_s": float(n) * n / (ms / 1e3), "solve_iterations": rep.iterations,
             "solve_ms_per_iteration": rep.device_ms / (rep.iterations + 2),
-            "note": "row-owned matrix-free GEMV: every pair evaluated twice (no symmetric halving yet)"}
+            "note": "symmetric half-evaluation (each pair once), dot-product distance form"}
 
 
 def main():
