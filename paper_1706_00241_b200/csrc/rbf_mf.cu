@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(DCG_NT, 1)
                 rbf_stage_norms(p, xjt, nJ);
                 cta_sync();
                 double kv[2][4];
-                rbf_tile_values(p, xit, xjt, i0, j0, r1, kv, nI, nJ);
+                rbf_tile_values<true>(p, xit, xjt, i0, j0, r1, kv, nI, nJ);
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc) {
                     const double* vr = vj + (4 * warp + cc) * MF_KC;

@@ -20,6 +20,35 @@
 
 #define MF_TB 64
 
+// exp(x) for x <= 0 without branches (the kernel argument -|d|^2 / (2 l^2)):
+// k = rint(x log2 e), r = x - k ln 2 (two-part ln 2), |r| <= ln2 / 2; degree-13
+// Taylor polynomial (truncation r^14 / 14! < 5e-18) in Horner form, scaled by
+// adding k to the exponent field; x < -708 returns 0.  A few ulp; ~25 FP64
+// instructions against the general-purpose exp's range checks and branches.
+__device__ __forceinline__ double rbf_exp_neg(double x) {
+    const bool under = x < -708.0;
+    x = fmax(x, -708.0);
+    const double kf = rint(x * 1.4426950408889634074);
+    double r = fma(kf, -6.93147180369123816490e-01, x);
+    r = fma(kf, -1.90821492927058770002e-10, r);
+    double p = 1.6059043836821614599e-10;            // 1/13!
+    p = fma(p, r, 2.0876756987868098979e-09);        // 1/12!
+    p = fma(p, r, 2.5052108385441718775e-08);        // 1/11!
+    p = fma(p, r, 2.7557319223985890653e-07);        // 1/10!
+    p = fma(p, r, 2.7557319223985890653e-06);        // 1/9!
+    p = fma(p, r, 2.4801587301587301587e-05);        // 1/8!
+    p = fma(p, r, 1.9841269841269841270e-04);        // 1/7!
+    p = fma(p, r, 1.3888888888888888889e-03);        // 1/6!
+    p = fma(p, r, 8.3333333333333333333e-03);        // 1/5!
+    p = fma(p, r, 4.1666666666666666667e-02);        // 1/4!
+    p = fma(p, r, 1.6666666666666666667e-01);        // 1/3!
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
+    const long long bits = __double_as_longlong(p) + ((long long)(int)kf << 52);
+    return under ? 0.0 : __longlong_as_double(bits);
+}
+
 // shared memory (doubles) of rbf_rows_gemv for data dimension `dim`
 __host__ __device__ __forceinline__ long long rbf_mf_smem_doubles(int dim) {
     return 2LL * dim * MF_TB + MF_TB + DCG_NW * MF_TB + 2 * MF_TB;
@@ -34,11 +63,12 @@ struct RbfParams {
 
 // the 8 kernel values of this thread in tile (rows gi0 + {2l, 2l+1}, cols gj0 + 4w + {0..3});
 // xit: dim x 64 (rows of the I chunk), xjt: dim x 64 (J tile); out-of-range -> 0.
-// With row norms nI / nJ (64 each) the squared distance is formed as
-// |x_i|^2 + |x_j|^2 - 2 x_i.x_j (one FMA per coordinate instead of a rounded
-// sub / mul / add; the cancellation error is ~eps |x|^2 absolute in the
-// exponent, ~1e-16 relative in K); with nI == nullptr it is the stored
-// builder's exact difference form (bit-identical elements).
+// FAST: the squared distance as |x_i|^2 + |x_j|^2 - 2 x_i.x_j from the staged
+// row norms nI / nJ (one FMA per coordinate; the cancellation error is ~eps
+// |x|^2 absolute in the exponent, ~1e-16 relative in K) and the branch-free
+// exponential; otherwise the stored builder's exact difference form
+// (bit-identical elements).
+template <bool FAST>
 __device__ __forceinline__ void rbf_tile_values(const RbfParams& p, const double* xit, const double* xjt,
                                                 long long gi0, long long gj0, long long row_end, double k[2][4],
                                                 const double* nI = nullptr, const double* nJ = nullptr) {
@@ -48,18 +78,28 @@ __device__ __forceinline__ void rbf_tile_values(const RbfParams& p, const double
     for (int r = 0; r < 2; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-    if (nI) {
-        for (int t = 0; t < p.dim; ++t) {
-            const double2 xi = *reinterpret_cast<const double2*>(xit + t * MF_TB + 2 * lane);
-            const double2 xa = *reinterpret_cast<const double2*>(xjt + t * MF_TB + 4 * warp);
-            const double2 xb = *reinterpret_cast<const double2*>(xjt + t * MF_TB + 4 * warp + 2);
-            const double xr[2] = {xi.x, xi.y};
-            const double xc[4] = {xa.x, xa.y, xb.x, xb.y};
+    const double* pi = xit + 2 * lane;
+    const double* pj = xjt + 4 * warp;
+#pragma unroll 4
+    for (int t = 0; t < p.dim; ++t, pi += MF_TB, pj += MF_TB) {
+        const double2 xi = *reinterpret_cast<const double2*>(pi);
+        const double2 xa = *reinterpret_cast<const double2*>(pj);
+        const double2 xb = *reinterpret_cast<const double2*>(pj + 2);
+        const double xr[2] = {xi.x, xi.y};
+        const double xc[4] = {xa.x, xa.y, xb.x, xb.y};
 #pragma unroll
-            for (int r = 0; r < 2; ++r)
+        for (int r = 0; r < 2; ++r)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) acc[r][c] = fma(xr[r], xc[c], acc[r][c]);
-        }
+            for (int c = 0; c < 4; ++c) {
+                if constexpr (FAST) {
+                    acc[r][c] = fma(xr[r], xc[c], acc[r][c]);
+                } else {
+                    const double diff = sub_rn(xr[r], xc[c]);
+                    acc[r][c] = add_rn(acc[r][c], mul_rn(diff, diff));
+                }
+            }
+    }
+    if constexpr (FAST) {
         const double2 ni = *reinterpret_cast<const double2*>(nI + 2 * lane);
         const double2 na = *reinterpret_cast<const double2*>(nJ + 4 * warp);
         const double2 nb = *reinterpret_cast<const double2*>(nJ + 4 * warp + 2);
@@ -69,31 +109,17 @@ __device__ __forceinline__ void rbf_tile_values(const RbfParams& p, const double
         for (int r = 0; r < 2; ++r)
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[r][c] = fmax(0.0, fma(-2.0, acc[r][c], nr[r] + nc[c]));
-    } else {
-        for (int t = 0; t < p.dim; ++t) {
-            const double2 xi = *reinterpret_cast<const double2*>(xit + t * MF_TB + 2 * lane);
-            const double2 xa = *reinterpret_cast<const double2*>(xjt + t * MF_TB + 4 * warp);
-            const double2 xb = *reinterpret_cast<const double2*>(xjt + t * MF_TB + 4 * warp + 2);
-            const double xr[2] = {xi.x, xi.y};
-            const double xc[4] = {xa.x, xa.y, xb.x, xb.y};
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const double diff = sub_rn(xr[r], xc[c]);
-                    acc[r][c] = add_rn(acc[r][c], mul_rn(diff, diff));
-                }
-        }
     }
+    const long long gib = gi0 + 2 * lane, gjb = gj0 + 4 * warp;
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            const long long gi = gi0 + 2 * lane + r, gj = gj0 + 4 * warp + c;
             double v;
-            if (gi >= row_end || gj >= p.n) v = 0.0;
-            else if (gi == gj) v = p.diag;
+            if constexpr (FAST) v = p.var * rbf_exp_neg(-acc[r][c] * p.inv2);
             else v = mul_rn(p.var, exp(mul_rn(-acc[r][c], p.inv2)));
+            v = (gib + r == gjb + c) ? p.diag : v;
+            v = (gib + r < row_end && gjb + c < p.n) ? v : 0.0;
             k[r][c] = v;
         }
 }
@@ -151,7 +177,7 @@ __device__ void rbf_rows_gemv(const RbfParams& p, long long r0, long long r1, co
             }
             cta_sync();
             double k[2][4];
-            rbf_tile_values(p, xit, xjt, i0, j0, r1, k, nI, nJ);
+            rbf_tile_values<true>(p, xit, xjt, i0, j0, r1, k, nI, nJ);
             const double2 va = *reinterpret_cast<const double2*>(vj + 4 * warp);
             const double2 vb = *reinterpret_cast<const double2*>(vj + 4 * warp + 2);
 #pragma unroll
@@ -221,6 +247,28 @@ static __device__ void rbf_sym_pass1(const RbfParams& p, const double* v, const 
     double row0 = 0.0, row1 = 0.0;
     long long seg_start = t0;
     int flush = 0;
+    // Register prefetch of the next tile's X_J and v'_J: issued before the
+    // current tile's arithmetic, stored to shared memory after the next
+    // barrier, so the L2 round trip overlaps the FP64 work.
+    constexpr int PF = (DCG_RBF_MAX_DIM * MF_TB + DCG_NT - 1) / DCG_NT;
+    double pf[PF];
+    double pfv = 0.0;
+    const int nel = p.dim * MF_TB;
+    auto prefetch = [&](long long Jn) {
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            const int e = tid + u * DCG_NT;
+            double val = 0.0;
+            if (e < nel) {
+                const int r = e / p.dim, t = e - (e / p.dim) * p.dim;
+                const long long g = Jn * MF_TB + r;
+                if (g < n) val = __ldg(p.X + g * p.dim + t);
+            }
+            pf[u] = val;
+        }
+        if (tid < MF_TB) pfv = sym_xval(v, s, Jn * MF_TB + tid, n);
+    };
+    prefetch(J);
     for (int lt = 0; lt < ntiles; ++lt) {
         cta_sync();   // the previous tile's reads of xit / xjt / vj are done
         if (I != staged_I) {
@@ -229,8 +277,15 @@ static __device__ void rbf_sym_pass1(const RbfParams& p, const double* v, const 
             xI0 = sym_xval(v, s, I * MF_TB + 2 * lane, n);
             xI1 = sym_xval(v, s, I * MF_TB + 2 * lane + 1, n);
         }
-        rbf_stage_rows(p, J * MF_TB, n, xjt);
-        if (tid < MF_TB) vj[tid] = sym_xval(v, s, J * MF_TB + tid, n);
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            const int e = tid + u * DCG_NT;
+            if (e < nel) {
+                const int r = e / p.dim, t = e - (e / p.dim) * p.dim;
+                xjt[t * MF_TB + r] = pf[u];
+            }
+        }
+        if (tid < MF_TB) vj[tid] = pfv;
         cta_sync();
         rbf_stage_norms(p, xjt, nJ);
         if (I != norms_I) {
@@ -238,8 +293,9 @@ static __device__ void rbf_sym_pass1(const RbfParams& p, const double* v, const 
             norms_I = I;
         }
         cta_sync();
+        if (lt + 1 < ntiles) prefetch(J + 1 > I ? 0 : J + 1);
         double k[2][4];
-        rbf_tile_values(p, xit, xjt, I * MF_TB, J * MF_TB, n, k, nI, nJ);
+        rbf_tile_values<true>(p, xit, xjt, I * MF_TB, J * MF_TB, n, k, nI, nJ);
         const double x0 = vj[4 * warp], x1 = vj[4 * warp + 1], x2 = vj[4 * warp + 2], x3 = vj[4 * warp + 3];
         row0 = fma(k[0][0], x0, row0);
         row0 = fma(k[0][1], x1, row0);
