@@ -64,14 +64,14 @@ __global__ void __launch_bounds__(DCG_NT, 1)
 }
 
 __global__ void __launch_bounds__(DCG_NT, 1)
-    sym_pass2_kernel(long long n, const double* colpart, const double* rowpart, const double* v,
+    sym_pass2_kernel(long long n, int R, const double* colpart, const double* rowpart, const double* v,
                      const double* s_out, double shift, double* y) {
-    __shared__ long long tbl[DCG_SYM_MAX_CTAS + 1];
+    __shared__ long long tbl[2 * DCG_SYM_MAX_CTAS + 1];
     __shared__ double red[DCG_NT];
-    sym_fill_range_table(tbl, n);
+    sym_fill_range_table(tbl, n, R);
     const long long q0 = sym_row_begin(n, gridDim.x, blockIdx.x);
     const long long q1 = sym_row_begin(n, gridDim.x, blockIdx.x + 1);
-    sym_pass2(n, colpart, rowpart, q0, q1, tbl, red, [&](long long i, double t) {
+    sym_pass2(n, colpart, rowpart, q0, q1, tbl, R, red, [&](long long i, double t) {
         double val = s_out ? mul_rn(s_out[i], t) : t;
         if (shift != 0.0) val = add_rn(mul_rn(shift, v[i]), val);
         y[i] = val;
@@ -92,15 +92,16 @@ int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, long long 
     const int G = ctx->sm_count < DCG_SYM_MAX_CTAS ? ctx->sm_count : DCG_SYM_MAX_CTAS;
     sym_pass1_kernel<<<G, DCG_NT, smem, st>>>(K, ldk, n, v, s_in, colpart, rowpart);
     DCG_LAUNCHED();
-    sym_pass2_kernel<<<G, DCG_NT, 0, st>>>(n, colpart, rowpart, v, s_out, shift, y);
+    sym_pass2_kernel<<<G, DCG_NT, 0, st>>>(n, G, colpart, rowpart, v, s_out, shift, y);
     DCG_LAUNCHED();
     return DCG_OK;
 }
 
 // pass 2 alone (the matrix-free operator's symmetric pass 1 produces the same partials)
-int dcg_sym_pass2_launch(cudaStream_t st, int G, long long n, const double* colpart, const double* rowpart,
+// (R = pass-1 ranges: G x teams)
+int dcg_sym_pass2_launch(cudaStream_t st, int G, int R, long long n, const double* colpart, const double* rowpart,
                          const double* v, const double* s_out, double shift, double* y) {
-    sym_pass2_kernel<<<G, DCG_NT, 0, st>>>(n, colpart, rowpart, v, s_out, shift, y);
+    sym_pass2_kernel<<<G, DCG_NT, 0, st>>>(n, R, colpart, rowpart, v, s_out, shift, y);
     DCG_LAUNCHED();
     return DCG_OK;
 }

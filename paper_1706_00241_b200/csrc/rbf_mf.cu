@@ -6,6 +6,7 @@
 // whole 64-row chunks.
 #include "common.cuh"
 #include "rbfmf.cuh"
+#include "rbfmma.cuh"
 
 #define MF_KC 16   // columns of X per pass of the multi-vector kernel
 
@@ -115,10 +116,10 @@ __global__ void __launch_bounds__(DCG_NT, 1)
 }
 
 __global__ void __launch_bounds__(DCG_NT, 1)
-    rbf_sym_pass1_kernel(RbfParams p, const double* v, const double* s_in, double* colpart, double* rowpart) {
-    extern __shared__ __align__(16) double smem[];
-    rbf_sym_init(smem, p);
-    rbf_sym_pass1(p, v, s_in, colpart, rowpart, smem);
+    rbf_mma_pass1_kernel(RbfMma p, const double* v, const double* s_in, double* colpart, double* rowpart) {
+    extern __shared__ __align__(128) double smem[];
+    rm_init(smem, p);
+    rbf_mma_pass1(p, v, s_in, colpart, rowpart, smem);
 }
 
 int grid_for(const dcg_context* ctx, long long rows) {
@@ -139,12 +140,45 @@ int dcg_rbf_mf_check(const dcg_operator* op) {
 
 size_t dcg_rbf_mf_smem(int dim) { return sizeof(double) * (size_t)rbf_mf_smem_doubles(dim); }
 
-int dcg_sym_pass2_launch(cudaStream_t st, int G, long long n, const double* colpart, const double* rowpart,
+int dcg_sym_pass2_launch(cudaStream_t st, int G, int R, long long n, const double* colpart, const double* rowpart,
                          const double* v, const double* s_out, double shift, double* y);
 size_t dcg_sym_apply_scratch_doubles(long long n);
 
+// operands of the tensor-pipe pass 1 (rbfmma.cuh): fragment-major x~ and b
+size_t dcg_rbf_mma_operand_doubles(long long n, int dim) {
+    return (size_t)rm_npad(n) * rm_dpad(dim) + (size_t)rm_npad(n);
+}
+
+// teams per 512-thread CTA that fit next to `other_bytes` of shared memory
+int dcg_rbf_mma_teams(const dcg_context* ctx, int dim, size_t other_bytes) {
+    return sizeof(double) * (size_t)rm_smem_doubles(dim, 2) + other_bytes <= ctx->smem_optin ? 2 : 1;
+}
+
+RbfMma dcg_rbf_mma_params(const dcg_operator* op, double* operands, int nteam) {
+    RbfMma p;
+    p.X = op->d_x;
+    p.n = op->n;
+    p.dim = (int)op->dim;
+    p.dp = rm_dpad(p.dim);
+    p.xf = operands;
+    p.xb = operands + rm_npad(op->n) * p.dp;
+    p.var = op->var;
+    p.inv2 = op->inv_two_ell2;
+    p.diag = op->diag / op->var;
+    p.nteam = nteam;
+    return p;
+}
+
+int dcg_rbf_mma_prep(const dcg_context* ctx, cudaStream_t st, const RbfMma& p) {
+    rbf_prep_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(p);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}
+
 size_t dcg_rbf_mf_scratch_doubles(const dcg_operator* op) {
-    return (op->row0 == 0 && op->rows == op->n) ? dcg_sym_apply_scratch_doubles(op->n) : 0;
+    return (op->row0 == 0 && op->rows == op->n)
+               ? dcg_sym_apply_scratch_doubles(op->n) + dcg_rbf_mma_operand_doubles(op->n, (int)op->dim) + 32
+               : 0;
 }
 
 int dcg_rbf_mf_apply(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, const double* v, const double* s_in,
@@ -153,16 +187,23 @@ int dcg_rbf_mf_apply(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, 
     if (rc) return rc;
     if (op->rows == 0) return DCG_OK;
     if (scratch && op->row0 == 0 && op->rows == op->n) {
-        // unsharded: symmetric half-evaluation + the stored strategy's pass 2
+        // unsharded: symmetric half-evaluation on the FP64 tensor pipe + the
+        // stored strategy's pass 2
         const long long n = op->n;
         const int G = ctx->sm_count < DCG_SYM_MAX_CTAS ? ctx->sm_count : DCG_SYM_MAX_CTAS;
-        const size_t smem = sizeof(double) * (size_t)rbf_sym_smem_doubles((int)op->dim);
-        DCG_CUDA(cudaFuncSetAttribute(rbf_sym_pass1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const int nteam = dcg_rbf_mma_teams(ctx, (int)op->dim, 0);
+        const size_t smem = sizeof(double) * (size_t)rm_smem_doubles((int)op->dim, nteam);
+        DCG_CUDA(cudaFuncSetAttribute(rbf_mma_pass1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         double* colpart = scratch;
         double* rowpart = scratch + sym_ntiles(n) * DCG_TB;
-        rbf_sym_pass1_kernel<<<G, DCG_NT, smem, st>>>(params_of(op), v, s_in, colpart, rowpart);
+        double* operands = reinterpret_cast<double*>(
+            (reinterpret_cast<uintptr_t>(rowpart + sym_ntiles(n) * DCG_TB) + 255) & ~uintptr_t(255));
+        const RbfMma p = dcg_rbf_mma_params(op, operands, nteam);
+        rc = dcg_rbf_mma_prep(ctx, st, p);
+        if (rc) return rc;
+        rbf_mma_pass1_kernel<<<G, DCG_NT, smem, st>>>(p, v, s_in, colpart, rowpart);
         DCG_LAUNCHED();
-        return dcg_sym_pass2_launch(st, G, n, colpart, rowpart, v, s_out, shift, y);
+        return dcg_sym_pass2_launch(st, G, G * nteam, n, colpart, rowpart, v, s_out, shift, y);
     }
     const size_t smem = dcg_rbf_mf_smem((int)op->dim);
     DCG_CUDA(cudaFuncSetAttribute(rbf_mf_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

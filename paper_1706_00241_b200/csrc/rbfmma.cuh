@@ -1,0 +1,357 @@
+// Matrix-free RBF operator, symmetric pass 1 on the FP64 tensor pipe
+// (kernel K7 of SURVEY.md section 2; config 5).
+//
+//   K_ij = var exp(-|x_i - x_j|^2 / (2 l^2))  (i != j),   K_ii = var + jitter
+//
+// is regenerated tile by tile in every product.  Per element the exponent is
+//   e_ij = b_i + b_j + x~_i . x~_j,   b_i = -|x_i|^2 / (2 l^2),   x~ = x sqrt(2 / (2 l^2))
+// The signal variance is folded into the vector: K v' = E (var v') with
+// E_ij = exp(e_ij) and E_ii = (var + jitter) / var.
+// (the |x_i|^2 + |x_j|^2 - 2 x_i.x_j form; the cancellation error is ~eps |x|^2
+// absolute in the exponent, ~1e-16 relative in K), so the d-term contraction is
+// an (64 x d) x (d x 64) matrix product per tile: mma.sync.m8n8k4.f64 (DMMA),
+// whose accumulators start at b_i + b_j.  DMMA and DFMA share the FP64 pipe
+// (tools/fp64_peak.cu: 37 vs 34 TFLOP/s, a DMMA+DFMA mix takes the sum of the
+// two times), so the contraction still costs d FMAs per element; what DMMA
+// removes is the issue and operand-load overhead of the FMA form.
+// The exponential is table-based: e = k ln2 / 64 + r, |r| <= ln2 / 128,
+//   exp(e) = 2^(k >> 6) * T[k & 63] * (1 + p(r)),   T[j] = 2^(j / 64),
+// with p the degree-5 Taylor polynomial of expm1 (truncation < 3.5e-17), k from
+// the 1.5 * 2^52 rounding trick: ~11 FP64 instructions per element.  With the
+// two accumulations (row sums and column sums) an element costs ~d + 15 FP64
+// pipe operations, against ~130 issued instructions of the FMA-form kernel.
+//
+// Work decomposition: the lower-triangle 64 x 64 tile sequence of the stored
+// strategy (symgemv.cuh) is split into ranges per *team* -- 8 warps (256
+// threads) -- so a 512-thread CTA runs two independent teams with their own
+// named barriers.  Warp w of a team owns the tile's columns 8w..8w+7 and all
+// 64 rows: 8 DMMA accumulator tiles, 16 elements per lane.  Operands arrive
+// by TMA-style bulk copies (cp.async.bulk + mbarrier complete_tx) from a
+// fragment-major copy of x~ (rbf_prep_kernel), so a lane's A / B fragments of
+// two k-steps are one conflict-free 16-byte shared load; the next J tile is
+// in flight while the current one is computed.  Partials use exactly the
+// stored strategy's layout (colpart per tile, rowpart per tile-row segment),
+// so sym_pass2 reduces them (with the team range table).
+#pragma once
+#include "common.cuh"
+#include "symgemv.cuh"
+
+#define RM_TB 64                 // tile side
+#define RM_TW 8                  // warps per team
+#define RM_TT (RM_TW * 32)       // threads per team
+#define RM_MAX_TEAMS (DCG_NT / RM_TT)
+
+// fragment-major operand layout (per 64-row tile, dp = dim padded to 8):
+// element (row 8 rb + r, coordinate 8 ch + 4 e + q) at ((rb * nch + ch) * 32 + 4 r + q) * 2 + e
+__host__ __device__ __forceinline__ int rm_dpad(int dim) { return (dim + 7) & ~7; }
+__host__ __device__ __forceinline__ long long rm_npad(long long n) { return (n + RM_TB - 1) / RM_TB * RM_TB; }
+__host__ __device__ __forceinline__ long long rm_frag_index(long long i, int t, int dp) {
+    const long long T = i / RM_TB;
+    const int il = (int)(i - T * RM_TB), rb = il >> 3, r = il & 7;
+    const int ch = t >> 3, e = (t >> 2) & 1, q = t & 3;
+    return T * RM_TB * dp + ((long long)(rb * (dp >> 3) + ch) * 32 + 4 * r + q) * 2 + e;
+}
+
+struct RbfMma {
+    const double* X;     // n x dim row-major (the operator's points)
+    double* xf;          // npad x dp fragment-major x~ (prep output)
+    double* xb;          // npad: b_i (0 beyond n)
+    long long n;
+    int dim, dp;
+    double var, inv2, diag;   // diag = (var + jitter) / var (the E_ii above)
+    int nteam;           // teams per CTA (1 or 2)
+};
+
+// xf / xb from X (one launch per product or solve; X is read once)
+static __global__ void rbf_prep_kernel(RbfMma p) {
+    const long long npad = rm_npad(p.n);
+    const double sc = sqrt(2.0 * p.inv2);
+    const long long total = npad * p.dp;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long i = e / p.dp;
+        const int t = (int)(e - i * p.dp);
+        const double v = (i < p.n && t < p.dim) ? mul_rn(__ldg(p.X + i * p.dim + t), sc) : 0.0;
+        p.xf[rm_frag_index(i, t, p.dp)] = v;
+    }
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < npad;
+         i += (long long)gridDim.x * blockDim.x) {
+        double a = 0.0;
+        if (i < p.n)
+            for (int t = 0; t < p.dim; ++t) {
+                const double x = __ldg(p.X + i * p.dim + t);
+                a = fma(x, x, a);
+            }
+        p.xb[i] = -a * p.inv2;
+    }
+}
+
+// ---- shared-memory layout ----------------------------------------------------
+// CTA header (doubles): exp table (64), mbarriers (4 per team), team sequence
+// words, range table (RM_MAX_TEAMS x 255 + 1 longs); then per team: XI frags
+// (64 dp), XJ frags x2, I pairs {b, v'} (128), J pairs x2 (256), row-flush
+// buffer (8 x 64).
+#define RM_HDR 592
+__host__ __device__ __forceinline__ long long rm_team_doubles(int dp) { return 3LL * RM_TB * dp + 128 + 256 + RM_TW * RM_TB; }
+__host__ __device__ __forceinline__ long long rm_smem_doubles(int dim, int nteam) {
+    return RM_HDR + nteam * rm_team_doubles(rm_dpad(dim));
+}
+struct RmTeamSmem {
+    double* xi;
+    double* xj;      // 2 buffers of 64 dp
+    double* pi;      // 64 x {b, v'}
+    double* pj;      // 2 x 64 x {b, v'}
+    double* red;     // 8 x 64
+};
+__device__ __forceinline__ RmTeamSmem rm_team_smem(double* smem, int dp, int team) {
+    RmTeamSmem t;
+    double* b = smem + RM_HDR + team * rm_team_doubles(dp);
+    t.xi = b;
+    t.xj = b + RM_TB * dp;
+    t.pi = b + 3 * RM_TB * dp;
+    t.pj = t.pi + 128;
+    t.red = t.pj + 256;
+    return t;
+}
+__device__ __forceinline__ double* rm_tab(double* smem) { return smem; }
+__device__ __forceinline__ unsigned long long* rm_bars(double* smem, int team) {
+    return reinterpret_cast<unsigned long long*>(smem + 64) + 4 * team;
+}
+__device__ __forceinline__ unsigned* rm_seq(double* smem, int team) {
+    return reinterpret_cast<unsigned*>(smem + 64 + 4 * RM_MAX_TEAMS) + 2 * team;
+}
+__device__ __forceinline__ long long* rm_table(double* smem) {
+    return reinterpret_cast<long long*>(smem + 64 + 4 * RM_MAX_TEAMS + RM_MAX_TEAMS);
+}
+static_assert(64 + 4 * RM_MAX_TEAMS + RM_MAX_TEAMS + RM_MAX_TEAMS * DCG_SYM_MAX_CTAS + 1 <= RM_HDR, "rbfmma header");
+// the pass-2 reduction scratch (512 doubles, generic-proxy only): team 0's flush buffer
+__device__ __forceinline__ double* rm_pass2_scratch(double* smem, int dp) { return rm_team_smem(smem, dp, 0).red; }
+
+// ---- primitives --------------------------------------------------------------
+__device__ __forceinline__ void rm_team_sync(int team) {
+    asm volatile("barrier.sync %0, %1;" ::"r"(1 + team), "r"(RM_TT) : "memory");
+}
+__device__ __forceinline__ void rm_dmma(double& c0, double& c1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+__device__ __forceinline__ unsigned rm_saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void rm_bar_init(unsigned long long* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(rm_saddr(bar)));
+}
+// one elected thread: expect `bytes` on `bar` and start the bulk copy gsrc -> sdst
+__device__ __forceinline__ void rm_bulk_load(double* sdst, const double* gsrc, unsigned bytes, unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(rm_saddr(bar)), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(rm_saddr(sdst)),
+        "l"(gsrc), "r"(bytes), "r"(rm_saddr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void rm_bar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "RM_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra RM_WAIT;\n"
+        "}\n" ::"r"(rm_saddr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// exp(x) for x >= -700 (clamped: e^-700 ~ 1e-304 stands in for smaller values,
+// and keeps every intermediate normal), table T in shared memory.  k = rint(64 x / ln 2) via the 1.5 * 2^52 shift, r = x - k
+// ln2/64 with a two-part constant (both FMAs exact to ~1e-19), expm1(r) by its
+// degree-5 Taylor polynomial, result T[k & 63] (1 + expm1 r) scaled by
+// 2^(k >> 6) in the exponent field.  ~1 ulp.
+__device__ __forceinline__ double rm_exp(double x, const double* tab) {
+    x = fmax(x, -700.0);
+    const double t = fma(x, 92.33248261689366, 6755399441055744.0);
+    const double kf = t - 6755399441055744.0;
+    double r = fma(kf, -0.010830424696249145, x);
+    r = fma(kf, -3.623510646634843e-19, r);
+    const int ki = __double2loint(t);
+    double q = fma(r, 8.3333333333333333e-03, 4.1666666666666667e-02);
+    q = fma(q, r, 1.6666666666666667e-01);
+    q = fma(q, r, 0.5);
+    const double r2 = r * r;
+    const double pm = fma(q, r2, r);
+    const double tj = tab[ki & 63];
+    const double res = fma(tj, pm, tj);
+    return __hiloint2double(__double2hiint(res) + (ki >> 6) * 1048576, __double2loint(res));
+}
+
+// Once per launch (all CTA threads): exp table, mbarriers, team range table.
+// Ends with a CTA barrier.
+__device__ __forceinline__ void rm_init(double* smem, const RbfMma& p) {
+    double* tab = rm_tab(smem);
+    if (threadIdx.x < 64) tab[threadIdx.x] = exp2((double)threadIdx.x / 64.0);
+    if (threadIdx.x < (unsigned)RM_MAX_TEAMS) {
+        unsigned long long* b = rm_bars(smem, threadIdx.x);
+        rm_bar_init(b);
+        rm_bar_init(b + 1);
+        rm_bar_init(b + 2);
+        unsigned* sq = rm_seq(smem, threadIdx.x);
+        sq[0] = sq[1] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    long long* tbl = rm_table(smem);
+    const int R = gridDim.x * p.nteam;
+    for (int b = threadIdx.x; b <= R; b += blockDim.x) tbl[b] = sym_tile_begin(p.n, R, b);
+    cta_sync();
+}
+
+__device__ __forceinline__ double2 rm_pair(const RbfMma& p, const double* v, const double* s, long long j) {
+    if (j >= p.n) return make_double2(0.0, 0.0);
+    const double vv = ld_cg(v + j);
+    return make_double2(__ldg(p.xb + j), mul_rn(p.var, s ? mul_rn(__ldg(s + j), vv) : vv));
+}
+
+// Pass 1 of t = K (s (.) v): colpart / rowpart as in sym_pass1.  All CTA
+// threads call; teams >= p.nteam idle.  No CTA barrier inside (team barriers only).
+static __device__ void rbf_mma_pass1(const RbfMma& p, const double* v, const double* s, double* colpart, double* rowpart,
+                              double* smem) {
+    const int team = threadIdx.x / RM_TT;
+    if (team >= p.nteam) return;
+    const int tt = threadIdx.x - team * RM_TT, lane = tt & 31, w = tt >> 5;
+    const int dp = p.dp, nch = dp >> 3;
+    const long long n = p.n;
+    const RmTeamSmem S = rm_team_smem(smem, dp, team);
+    const double* tab = rm_tab(smem);
+    unsigned long long* bars = rm_bars(smem, team);   // [0], [1]: XJ buffers, [2]: XI
+    unsigned* seq = rm_seq(smem, team);
+    const long long* tbl = rm_table(smem);
+    const int range = blockIdx.x * p.nteam + team;
+    const long long t0 = tbl[range], t1 = tbl[range + 1];
+    if (t0 >= t1) return;
+    const int ntiles = (int)(t1 - t0);
+    const unsigned tile_bytes = (unsigned)(RM_TB * dp * sizeof(double));
+    unsigned jseq = seq[0], iseq = seq[1];
+    long long I = sym_tile_row(t0);
+    long long J = t0 - sym_tile_row_base(I);
+    const int r = lane >> 2, q = lane & 3;
+
+    // prologue: XI(I), XJ(J) in flight; I / J pairs
+    rm_team_sync(team);   // previous pass's readers of these buffers are done
+    if (tt == 0) {
+        rm_bulk_load(S.xi, p.xf + I * RM_TB * dp, tile_bytes, bars + 2);
+        rm_bulk_load(S.xj + (jseq & 1) * RM_TB * dp, p.xf + J * RM_TB * dp, tile_bytes, bars + (jseq & 1));
+    }
+    if (tt < RM_TB) {
+        reinterpret_cast<double2*>(S.pi)[tt] = rm_pair(p, v, s, I * RM_TB + tt);
+        reinterpret_cast<double2*>(S.pj + (jseq & 1) * 128)[tt] = rm_pair(p, v, s, J * RM_TB + tt);
+    }
+    rm_bar_wait(bars + 2, iseq & 1);
+    ++iseq;
+    rm_team_sync(team);
+
+    double rowp[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) rowp[u] = 0.0;
+    long long seg_start = t0;
+    for (int lt = 0; lt < ntiles; ++lt) {
+        const int buf = jseq & 1;
+        // next tile: bulk copy into the other buffer (free: everyone passed the
+        // barrier that ended the previous tile) and its pairs into registers
+        long long In = I, Jn = J + 1;
+        if (Jn > In) { ++In; Jn = 0; }
+        const bool more = lt + 1 < ntiles;
+        double2 pn = make_double2(0.0, 0.0);
+        if (more) {
+            if (tt == 0) rm_bulk_load(S.xj + (buf ^ 1) * RM_TB * dp, p.xf + Jn * RM_TB * dp, tile_bytes, bars + (buf ^ 1));
+            if (tt < RM_TB) pn = rm_pair(p, v, s, Jn * RM_TB + tt);
+        }
+        rm_bar_wait(bars + buf, (jseq >> 1) & 1);
+        ++jseq;
+
+        // ---- the tile: 8 accumulator blocks (rows 8 rb + r, cols 8 w + 2 q + e)
+        const double* xj = S.xj + buf * RM_TB * dp;
+        const double2* pj2 = reinterpret_cast<const double2*>(S.pj + buf * 128);
+        const double2* pi2 = reinterpret_cast<const double2*>(S.pi);
+        const double2 pJ0 = pj2[8 * w + 2 * q], pJ1 = pj2[8 * w + 2 * q + 1];
+        double c[8][2];
+#pragma unroll
+        for (int rb = 0; rb < 8; ++rb) {
+            const double bI = S.pi[2 * (8 * rb + r)];
+            c[rb][0] = bI + pJ0.x;
+            c[rb][1] = bI + pJ1.x;
+        }
+        for (int ch = 0; ch < nch; ++ch) {
+            const double2 bf = reinterpret_cast<const double2*>(xj)[(w * nch + ch) * 32 + lane];
+#pragma unroll
+            for (int rb = 0; rb < 8; ++rb) {
+                const double2 af = reinterpret_cast<const double2*>(S.xi)[(rb * nch + ch) * 32 + lane];
+                rm_dmma(c[rb][0], c[rb][1], af.x, bf.x);
+                rm_dmma(c[rb][0], c[rb][1], af.y, bf.y);
+            }
+        }
+        double col0 = 0.0, col1 = 0.0;
+        const bool diag_tile = (J == I);
+#pragma unroll
+        for (int rb = 0; rb < 8; ++rb) {
+            double k0 = rm_exp(c[rb][0], tab);
+            double k1 = rm_exp(c[rb][1], tab);
+            if (diag_tile && rb == w) {
+                if (r == 2 * q) k0 = p.diag;
+                if (r == 2 * q + 1) k1 = p.diag;
+            }
+            rowp[rb] = fma(k0, pJ0.y, rowp[rb]);
+            rowp[rb] = fma(k1, pJ1.y, rowp[rb]);
+            const double vI = S.pi[2 * (8 * rb + r) + 1];
+            col0 = fma(k0, vI, col0);
+            col1 = fma(k1, vI, col1);
+        }
+        if (!diag_tile) {
+            // column sums over the 64 rows: the 8 lanes of equal q (xor 4, 8, 16)
+            const bool hi = lane & 16;
+            double cv = (hi ? col1 : col0) + __shfl_xor_sync(0xffffffffu, hi ? col0 : col1, 16);
+            cv += __shfl_xor_sync(0xffffffffu, cv, 8);
+            cv += __shfl_xor_sync(0xffffffffu, cv, 4);
+            if ((lane & 12) == 0) colpart[(t0 + lt) * RM_TB + 8 * w + 2 * q + (hi ? 1 : 0)] = cv;
+        }
+        const bool seg_end = diag_tile || !more;
+        if (seg_end) {
+            // rows 8 rb + r: the quad's lanes (xor 1, 2), then the 8 warps in a fixed order
+            const bool h2 = lane & 2;
+            double s4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                s4[u] = (h2 ? rowp[u + 4] : rowp[u]) + __shfl_xor_sync(0xffffffffu, h2 ? rowp[u] : rowp[u + 4], 2);
+            const bool h1 = lane & 1;
+            double s2[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+                s2[u] = (h1 ? s4[u + 2] : s4[u]) + __shfl_xor_sync(0xffffffffu, h1 ? s4[u] : s4[u + 2], 1);
+            // lane holds rows 8 (4 h2 + 2 h1 + u) + r, u = 0, 1
+#pragma unroll
+            for (int u = 0; u < 2; ++u) S.red[w * RM_TB + 8 * (4 * h2 + 2 * h1 + u) + r] = s2[u];
+            rm_team_sync(team);
+            if (tt < RM_TB) {
+                double a = 0.0;
+#pragma unroll
+                for (int u = 0; u < RM_TW; ++u) a += S.red[u * RM_TB + tt];
+                rowpart[seg_start * RM_TB + tt] = a;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) rowp[u] = 0.0;
+            seg_start = t0 + lt + 1;
+        }
+        if (more && tt < RM_TB) reinterpret_cast<double2*>(S.pj + (buf ^ 1) * 128)[tt] = pn;
+        rm_team_sync(team);   // tile done: buffers of this tile and the flush buffer are free
+        if (more && In != I) {
+            // new tile row: restage XI and the I pairs
+            if (tt == 0) rm_bulk_load(S.xi, p.xf + In * RM_TB * dp, tile_bytes, bars + 2);
+            if (tt < RM_TB) reinterpret_cast<double2*>(S.pi)[tt] = rm_pair(p, v, s, In * RM_TB + tt);
+            rm_bar_wait(bars + 2, iseq & 1);
+            ++iseq;
+            rm_team_sync(team);
+        }
+        I = In;
+        J = Jn;
+    }
+    if (tt == 0) {
+        seq[0] = jseq;
+        seq[1] = iseq;
+    }
+}

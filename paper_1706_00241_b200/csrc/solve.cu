@@ -17,10 +17,11 @@
 #include "common.cuh"
 #include "gemv.cuh"
 #include "symgemv.cuh"
-#include "rbfmf.cuh"
+#include "rbfmma.cuh"
 
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 namespace cg = cooperative_groups;
 
@@ -62,7 +63,7 @@ struct SolveArgs {
     DevStatus* st;
     unsigned int* bar;  // grid barrier arrival counter (zeroed per launch)
     unsigned long long* timers;   // optional per-phase ns accumulators (CTA 0, thread 0)
-    RbfParams rbf;                // matrix-free operator (STRAT_RBF)
+    RbfMma rbf;                   // matrix-free operator (STRAT_RBF)
 };
 
 // mu = L^-T L^-1 c for the k x k row-major lower factor of W'AW in shared
@@ -163,9 +164,9 @@ __device__ __forceinline__ void reduce_partials(const double* partials, int G, i
 enum { STRAT_ROWS = 0, STRAT_SYM = 1, STRAT_RBF = 2 };
 
 // Shared-memory doubles of the GEMV region for each strategy.
-__host__ __device__ __forceinline__ long long gemv_region_doubles(int strat, long long n, int dim) {
+__host__ __device__ __forceinline__ long long gemv_region_doubles(int strat, long long n, int dim, int nteam) {
     if (strat == STRAT_SYM) return sym_smem_doubles();
-    if (strat == STRAT_RBF) return rbf_sym_smem_doubles(dim);
+    if (strat == STRAT_RBF) return rm_smem_doubles(dim, nteam);
     return min(n, (long long)DCG_QT) + 2 + DCG_NW * DCG_RB;
 }
 
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int xt = (int)min(n, (long long)DCG_QT) + 2;
     double* s_g = smem;                                  // GEMV region (strategy dependent)
-    double* s_L = s_g + gemv_region_doubles(STRAT, n, a.rbf.dim);   // k*k
+    double* s_L = s_g + gemv_region_doubles(STRAT, n, a.rbf.dim, a.rbf.nteam);   // k*k
     double* s_rd = s_L + k * k;                          // DCG_MAX_K  1 / L_jj
     double* s_c = s_rd + DCG_MAX_K;                      // 1 + DCG_MAX_K reduced slots
     double* s_mu = s_c + DCG_MAX_K + 2;                  // DCG_MAX_K
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         q1 = sym_row_begin(n, G, blockIdx.x + 1);
     }
     if constexpr (STRAT == STRAT_RBF) {
-        rbf_sym_init(s_g, a.rbf);
+        rm_init(s_g, a.rbf);
         q0 = sym_row_begin(n, G, blockIdx.x);
         q1 = sym_row_begin(n, G, blockIdx.x + 1);
     }
@@ -226,12 +227,14 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     // again read by other CTAs only after a grid barrier.
     auto gemv = [&](const double* v, auto&& epi) {
         if constexpr (STRAT == STRAT_RBF) {
-            // symmetric half-evaluation of the regenerated tiles + the shared pass 2
-            rbf_sym_pass1(a.rbf, v, s, a.colpart, a.rowpart, s_g);
+            // symmetric half-evaluation of the regenerated tiles (FP64 tensor
+            // pipe, rbfmma.cuh) + the shared pass 2 over the team ranges
+            rbf_mma_pass1(a.rbf, v, s, a.colpart, a.rowpart, s_g);
             PHASE(0);
             GSYNC();
             PHASE(1);
-            sym_pass2(n, a.colpart, a.rowpart, q0, q1, rbf_sym_table(s_g, a.rbf.dim), s_g, epi);
+            sym_pass2(n, a.colpart, a.rowpart, q0, q1, rm_table(s_g), G * a.rbf.nteam,
+                      rm_pass2_scratch(s_g, a.rbf.dp), epi);
             PHASE(2);
         } else if constexpr (STRAT == STRAT_SYM) {
             PHASE(15);
@@ -243,7 +246,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
             GSYNC();
             PHASE(1);
             if (a.timers && threadIdx.x == 0) tc0 = globaltimer_ns();
-            sym_pass2(n, a.colpart, a.rowpart, q0, q1, sym_range_table(s_g), s_g, epi);
+            sym_pass2(n, a.colpart, a.rowpart, q0, q1, sym_range_table(s_g), G, s_g, epi);
             if (a.timers && threadIdx.x == 0) a.timers[16 + gridDim.x + blockIdx.x] += globaltimer_ns() - tc0;
             PHASE(2);
         } else {
@@ -499,10 +502,15 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
 
 }  // namespace
 
-size_t dcg_solve_smem_bytes(long long n, int k, int strat, int dim) {
-    return sizeof(double) * (size_t)(gemv_region_doubles(strat, n, dim) + k * k + DCG_MAX_K + DCG_MAX_K + 2 +
+size_t dcg_solve_smem_bytes(long long n, int k, int strat, int dim, int nteam) {
+    return sizeof(double) * (size_t)(gemv_region_doubles(strat, n, dim, nteam) + k * k + DCG_MAX_K + DCG_MAX_K + 2 +
                                      DCG_MAX_K + 64 + DCG_NT);
 }
+
+size_t dcg_rbf_mma_operand_doubles(long long n, int dim);
+int dcg_rbf_mma_teams(const dcg_context* ctx, int dim, size_t other_bytes);
+RbfMma dcg_rbf_mma_params(const dcg_operator* op, double* operands, int nteam);
+int dcg_rbf_mma_prep(const dcg_context* ctx, cudaStream_t st, const RbfMma& p);
 
 extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_b,
                          const double* d_x0, const dcg_basis* basis, const dcg_solver_config* cfg,
@@ -536,7 +544,9 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
     const int ps = ((1 + k) + 1) & ~1;
     const size_t vec = sizeof(double) * (size_t)((n + 31) & ~31LL);
     const size_t tiles = (strat != STRAT_ROWS) ? (size_t)sym_ntiles(n) : 0;
-    const size_t need = 3 * vec + 2 * sizeof(double) * (size_t)G * ps + 1024 + 2 * sizeof(double) * tiles * DCG_TB;
+    const size_t operands = strat == STRAT_RBF ? sizeof(double) * dcg_rbf_mma_operand_doubles(n, (int)op->dim) + 256 : 0;
+    const size_t need = 3 * vec + 2 * sizeof(double) * (size_t)G * ps + 1024 + 2 * sizeof(double) * tiles * DCG_TB +
+                        operands;
     int rc = dcg_ws_reserve(ctx, need);
     if (rc) return rc;
     char* w = static_cast<char*>(ctx->ws);
@@ -579,16 +589,22 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
     }
 
     cudaStream_t st = as_stream(stream);
-    const size_t smem = dcg_solve_smem_bytes(n, k, strat, (int)op->dim);
+    const int nteam = strat == STRAT_RBF ? dcg_rbf_mma_teams(ctx, (int)op->dim,
+                                                             dcg_solve_smem_bytes(n, k, strat, (int)op->dim, 0))
+                                         : 1;
+    const size_t smem = dcg_solve_smem_bytes(n, k, strat, (int)op->dim, nteam);
     const void* kfn = strat == STRAT_RBF ? (const void*)dcg_solve_kernel<STRAT_RBF>
                       : strat == STRAT_SYM ? (const void*)dcg_solve_kernel<STRAT_SYM>
                                            : (const void*)dcg_solve_kernel<STRAT_ROWS>;
-    a.rbf.X = op->d_x;
-    a.rbf.n = n;
-    a.rbf.dim = strat == STRAT_RBF ? (int)op->dim : 0;
-    a.rbf.var = op->var;
-    a.rbf.inv2 = op->inv_two_ell2;
-    a.rbf.diag = op->diag;
+    if (strat == STRAT_RBF) {
+        double* opnd = reinterpret_cast<double*>(
+            (reinterpret_cast<uintptr_t>(a.rowpart + tiles * DCG_TB) + 255) & ~uintptr_t(255));
+        a.rbf = dcg_rbf_mma_params(op, opnd, nteam);
+        rc = dcg_rbf_mma_prep(ctx, st, a.rbf);
+        if (rc) return rc;
+    } else {
+        memset(&a.rbf, 0, sizeof(a.rbf));
+    }
     DCG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     DCG_CUDA(cudaMemsetAsync(a.st, 0, sizeof(DevStatus), st));
     a.bar = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(a.st) + 128);   // inside the st line

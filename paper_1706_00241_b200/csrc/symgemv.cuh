@@ -111,8 +111,9 @@ __device__ __forceinline__ long long* sym_range_table(double* smem) {
                                         2 * DCG_SYM_STAGES + 2);
 }
 // tbl[b] = first tile of CTA b, b = 0..G (all threads call; ends with a barrier)
-__device__ __forceinline__ void sym_fill_range_table(long long* tbl, long long n) {
-    for (int b = threadIdx.x; b <= (int)gridDim.x; b += blockDim.x) tbl[b] = sym_tile_begin(n, gridDim.x, b);
+__device__ __forceinline__ void sym_fill_range_table(long long* tbl, long long n, int R = -1) {
+    if (R < 0) R = gridDim.x;
+    for (int b = threadIdx.x; b <= R; b += blockDim.x) tbl[b] = sym_tile_begin(n, R, b);
     cta_sync();
 }
 
@@ -390,7 +391,8 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
 }
 
 // Pass 2: t_i for rows [q0, q1) (sym_row_begin partition) from the partials;
-// epi(i, t_i) runs on one thread per row.  `tbl` is the pass-1 range table,
+// epi(i, t_i) runs on one thread per row.  `tbl` is the pass-1 range table of
+// `nranges` ranges (one per CTA, or per team of the matrix-free pass 1),
 // `red` 512 doubles of shared scratch.  A round covers 32 * nwr consecutive
 // rows (lane = row, so a warp's loads of one tile partial are coalesced); the
 // 16 / nwr warps sharing a row slice each sum a strided subset of the column
@@ -398,7 +400,7 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
 // combined in a fixed order.
 template <class Epi>
 __device__ __forceinline__ void sym_pass2(long long n, const double* colpart, const double* rowpart, long long q0,
-                                          long long q1, const long long* tbl, double* red, Epi&& epi) {
+                                          long long q1, const long long* tbl, int nranges, double* red, Epi&& epi) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long NT = sym_ntiles_side(n);
     const long long R = q1 - q0;
@@ -407,7 +409,7 @@ __device__ __forceinline__ void sym_pass2(long long n, const double* colpart, co
     const int S = DCG_NW / nwr;                                    // warps per row slice
     const int slice = warp / S, sub = warp % S;
     const bool active = slice < nwr;                               // (16 % nwr leftovers idle)
-    const int G = gridDim.x;
+    const int G = nranges;
     for (long long rb = q0; rb < q1; rb += 32LL * nwr) {
         const long long i = rb + 32LL * slice + lane;
         double acc = 0.0;
