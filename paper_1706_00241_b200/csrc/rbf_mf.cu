@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(DCG_NT, 1)
 
 __global__ void __launch_bounds__(DCG_NT, 1)
     rbf_mma_pass1_kernel(RbfMma p, const double* v, const double* s_in, double* colpart, double* rowpart) {
-    extern __shared__ __align__(128) double smem[];
+    extern __shared__ __align__(16) double smem[];
     rm_init(smem, p);
     rbf_mma_pass1(p, v, s_in, colpart, rowpart, smem);
 }
@@ -146,7 +146,7 @@ size_t dcg_sym_apply_scratch_doubles(long long n);
 
 // operands of the tensor-pipe pass 1 (rbfmma.cuh): fragment-major x~ and b
 size_t dcg_rbf_mma_operand_doubles(long long n, int dim) {
-    return (size_t)rm_npad(n) * rm_dpad(dim) + (size_t)rm_npad(n);
+    return (size_t)rm_npad(n) * rm_dpad(dim) + (size_t)rm_npad(n) + 2;
 }
 
 // teams per 512-thread CTA that fit next to `other_bytes` of shared memory
@@ -170,6 +170,7 @@ RbfMma dcg_rbf_mma_params(const dcg_operator* op, double* operands, int nteam) {
 }
 
 int dcg_rbf_mma_prep(const dcg_context* ctx, cudaStream_t st, const RbfMma& p) {
+    DCG_CUDA(cudaMemsetAsync(p.xb + rm_npad(p.n), 0, sizeof(double), st));
     rbf_prep_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(p);
     DCG_LAUNCHED();
     return DCG_OK;

@@ -14,10 +14,12 @@
 // (tools/fp64_peak.cu: 37 vs 34 TFLOP/s, a DMMA+DFMA mix takes the sum of the
 // two times), so the contraction still costs d FMAs per element; what DMMA
 // removes is the issue and operand-load overhead of the FMA form.
-// The exponential is table-based: e = k ln2 / 64 + r, |r| <= ln2 / 128,
-//   exp(e) = 2^(k >> 6) * T[k & 63] * (1 + p(r)),   T[j] = 2^(j / 64),
-// with p the degree-5 Taylor polynomial of expm1 (truncation < 3.5e-17), k from
-// the 1.5 * 2^52 rounding trick: ~11 FP64 instructions per element.  With the
+// The exponential is table-based: e = k ln2 / 256 + r, |r| <= ln2 / 512,
+//   exp(e) = 2^(k >> 8) * T[k & 255] * (1 + p(r)),   T[j] = 2^(j / 256),
+// with p the degree-4 Taylor polynomial of expm1 (truncation < 3.8e-17), k from
+// the 1.5 * 2^52 rounding trick: 9 FP64 instructions per element.  The clamp
+// that keeps intermediates normal (e >= -700) is compiled only into the path
+// taken when the data's largest norm allows an exponent below -690.  With the
 // two accumulations (row sums and column sums) an element costs ~d + 15 FP64
 // pipe operations, against ~130 issued instructions of the FMA-form kernel.
 //
@@ -55,7 +57,7 @@ __host__ __device__ __forceinline__ long long rm_frag_index(long long i, int t, 
 struct RbfMma {
     const double* X;     // n x dim row-major (the operator's points)
     double* xf;          // npad x dp fragment-major x~ (prep output)
-    double* xb;          // npad: b_i (0 beyond n)
+    double* xb;          // npad: b_i (0 beyond n); xb[npad] = max |x_i|^2 (bits, atomicMax)
     long long n;
     int dim, dp;
     double var, inv2, diag;   // diag = (var + jitter) / var (the E_ii above)
@@ -83,6 +85,8 @@ static __global__ void rbf_prep_kernel(RbfMma p) {
                 a = fma(x, x, a);
             }
         p.xb[i] = -a * p.inv2;
+        // nonnegative doubles order like their bit patterns: a deterministic max
+        atomicMax(reinterpret_cast<unsigned long long*>(p.xb + npad), (unsigned long long)__double_as_longlong(a));
     }
 }
 
@@ -91,7 +95,8 @@ static __global__ void rbf_prep_kernel(RbfMma p) {
 // words, range table (RM_MAX_TEAMS x 255 + 1 longs); then per team: XI frags
 // (64 dp), XJ frags x2, I pairs {b, v'} (128), J pairs x2 (256), row-flush
 // buffer (8 x 64).
-#define RM_HDR 592
+#define RM_TAB 256
+#define RM_HDR 784
 __host__ __device__ __forceinline__ long long rm_team_doubles(int dp) { return 3LL * RM_TB * dp + 128 + 256 + RM_TW * RM_TB; }
 __host__ __device__ __forceinline__ long long rm_smem_doubles(int dim, int nteam) {
     return RM_HDR + nteam * rm_team_doubles(rm_dpad(dim));
@@ -115,15 +120,15 @@ __device__ __forceinline__ RmTeamSmem rm_team_smem(double* smem, int dp, int tea
 }
 __device__ __forceinline__ double* rm_tab(double* smem) { return smem; }
 __device__ __forceinline__ unsigned long long* rm_bars(double* smem, int team) {
-    return reinterpret_cast<unsigned long long*>(smem + 64) + 4 * team;
+    return reinterpret_cast<unsigned long long*>(smem + RM_TAB) + 4 * team;
 }
 __device__ __forceinline__ unsigned* rm_seq(double* smem, int team) {
-    return reinterpret_cast<unsigned*>(smem + 64 + 4 * RM_MAX_TEAMS) + 2 * team;
+    return reinterpret_cast<unsigned*>(smem + RM_TAB + 4 * RM_MAX_TEAMS) + 2 * team;
 }
 __device__ __forceinline__ long long* rm_table(double* smem) {
-    return reinterpret_cast<long long*>(smem + 64 + 4 * RM_MAX_TEAMS + RM_MAX_TEAMS);
+    return reinterpret_cast<long long*>(smem + RM_TAB + 4 * RM_MAX_TEAMS + RM_MAX_TEAMS);
 }
-static_assert(64 + 4 * RM_MAX_TEAMS + RM_MAX_TEAMS + RM_MAX_TEAMS * DCG_SYM_MAX_CTAS + 1 <= RM_HDR, "rbfmma header");
+static_assert(RM_TAB + 4 * RM_MAX_TEAMS + RM_MAX_TEAMS + RM_MAX_TEAMS * DCG_SYM_MAX_CTAS + 1 <= RM_HDR, "rbfmma header");
 // the pass-2 reduction scratch (512 doubles, generic-proxy only): team 0's flush buffer
 __device__ __forceinline__ double* rm_pass2_scratch(double* smem, int dp) { return rm_team_smem(smem, dp, 0).red; }
 
@@ -160,33 +165,34 @@ __device__ __forceinline__ void rm_bar_wait(unsigned long long* bar, unsigned pa
         : "memory");
 }
 
-// exp(x) for x >= -700 (clamped: e^-700 ~ 1e-304 stands in for smaller values,
-// and keeps every intermediate normal), table T in shared memory.  k = rint(64 x / ln 2) via the 1.5 * 2^52 shift, r = x - k
-// ln2/64 with a two-part constant (both FMAs exact to ~1e-19), expm1(r) by its
-// degree-5 Taylor polynomial, result T[k & 63] (1 + expm1 r) scaled by
-// 2^(k >> 6) in the exponent field.  ~1 ulp.
+// exp(x), table T in shared memory: k = rint(256 x / ln 2) via the 1.5 * 2^52
+// shift, r = x - k ln2/256 with a two-part constant, expm1(r) by its degree-4
+// Taylor polynomial, result T[k & 255] (1 + expm1 r) scaled by 2^(k >> 8) in
+// the exponent field; ~1 ulp.  The exponent-field scaling needs a normal
+// result: CLAMP bounds x below by -700 (e^-700 ~ 1e-304 then stands in for
+// smaller values), compiled only into the path for data that can reach it.
+template <bool CLAMP>
 __device__ __forceinline__ double rm_exp(double x, const double* tab) {
-    x = fmax(x, -700.0);
-    const double t = fma(x, 92.33248261689366, 6755399441055744.0);
+    if constexpr (CLAMP) x = fmax(x, -700.0);
+    const double t = fma(x, 369.3299304675746, 6755399441055744.0);
     const double kf = t - 6755399441055744.0;
-    double r = fma(kf, -0.010830424696249145, x);
-    r = fma(kf, -3.623510646634843e-19, r);
+    double r = fma(kf, -0.0027076061740622863, x);
+    r = fma(kf, -9.058776616587108e-20, r);
     const int ki = __double2loint(t);
-    double q = fma(r, 8.3333333333333333e-03, 4.1666666666666667e-02);
-    q = fma(q, r, 1.6666666666666667e-01);
+    double q = fma(r, 4.1666666666666667e-02, 1.6666666666666667e-01);
     q = fma(q, r, 0.5);
     const double r2 = r * r;
     const double pm = fma(q, r2, r);
-    const double tj = tab[ki & 63];
+    const double tj = tab[ki & 255];
     const double res = fma(tj, pm, tj);
-    return __hiloint2double(__double2hiint(res) + (ki >> 6) * 1048576, __double2loint(res));
+    return __hiloint2double(__double2hiint(res) + (ki >> 8) * 1048576, __double2loint(res));
 }
 
 // Once per launch (all CTA threads): exp table, mbarriers, team range table.
 // Ends with a CTA barrier.
 __device__ __forceinline__ void rm_init(double* smem, const RbfMma& p) {
     double* tab = rm_tab(smem);
-    if (threadIdx.x < 64) tab[threadIdx.x] = exp2((double)threadIdx.x / 64.0);
+    for (int j = threadIdx.x; j < RM_TAB; j += blockDim.x) tab[j] = exp2((double)j / RM_TAB);
     if (threadIdx.x < (unsigned)RM_MAX_TEAMS) {
         unsigned long long* b = rm_bars(smem, threadIdx.x);
         rm_bar_init(b);
@@ -206,6 +212,55 @@ __device__ __forceinline__ double2 rm_pair(const RbfMma& p, const double* v, con
     if (j >= p.n) return make_double2(0.0, 0.0);
     const double vv = ld_cg(v + j);
     return make_double2(__ldg(p.xb + j), mul_rn(p.var, s ? mul_rn(__ldg(s + j), vv) : vv));
+}
+
+// One tile for warp w: E values of rows 8 rb + r, columns 8 w + 2 q + {0, 1};
+// row sums into rowp[rb], column sums over the warp's rows into col0 / col1.
+// DMMAs are issued in an order where consecutive ones use different
+// accumulators (4 blocks per half), so the dependent k-steps do not stall.
+template <bool DIAG, bool CLAMP>
+__device__ __forceinline__ void rm_tile(const RmTeamSmem& S, const double* xj, int nch, int w, int lane, double2 pJ0,
+                                        double2 pJ1, const double* tab, double diag, double rowp[8], double& col0,
+                                        double& col1) {
+    const int r = lane >> 2, q = lane & 3;
+    double c[8][2];
+#pragma unroll
+    for (int rb = 0; rb < 8; ++rb) {
+        const double bI = S.pi[2 * (8 * rb + r)];
+        c[rb][0] = bI + pJ0.x;
+        c[rb][1] = bI + pJ1.x;
+    }
+    const double2* xi2 = reinterpret_cast<const double2*>(S.xi);
+    const double2* xj2 = reinterpret_cast<const double2*>(xj);
+    for (int ch = 0; ch < nch; ++ch) {
+        const double2 bf = xj2[(w * nch + ch) * 32 + lane];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            double2 af[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) af[u] = xi2[((4 * h + u) * nch + ch) * 32 + lane];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) rm_dmma(c[4 * h + u][0], c[4 * h + u][1], af[u].x, bf.x);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) rm_dmma(c[4 * h + u][0], c[4 * h + u][1], af[u].y, bf.y);
+        }
+    }
+#pragma unroll
+    for (int rb = 0; rb < 8; ++rb) {
+        double k0 = rm_exp<CLAMP>(c[rb][0], tab);
+        double k1 = rm_exp<CLAMP>(c[rb][1], tab);
+        if constexpr (DIAG) {
+            if (rb == w) {
+                if (r == 2 * q) k0 = diag;
+                if (r == 2 * q + 1) k1 = diag;
+            }
+        }
+        rowp[rb] = fma(k0, pJ0.y, rowp[rb]);
+        rowp[rb] = fma(k1, pJ1.y, rowp[rb]);
+        const double vI = S.pi[2 * (8 * rb + r) + 1];
+        col0 = fma(k0, vI, col0);
+        col1 = fma(k1, vI, col1);
+    }
 }
 
 // Pass 1 of t = K (s (.) v): colpart / rowpart as in sym_pass1.  All CTA
@@ -231,6 +286,9 @@ static __device__ void rbf_mma_pass1(const RbfMma& p, const double* v, const dou
     long long I = sym_tile_row(t0);
     long long J = t0 - sym_tile_row_base(I);
     const int r = lane >> 2, q = lane & 3;
+    // the exponent can only reach -690 if 4 max|x|^2 / (2 l^2) can
+    const double maxn2 = ld_cg(p.xb + rm_npad(n));   // written by rbf_prep_kernel
+    const bool clamp = !(4.0 * maxn2 * p.inv2 <= 690.0);
 
     // prologue: XI(I), XJ(J) in flight; I / J pairs
     rm_team_sync(team);   // previous pass's readers of these buffers are done
@@ -268,39 +326,15 @@ static __device__ void rbf_mma_pass1(const RbfMma& p, const double* v, const dou
         // ---- the tile: 8 accumulator blocks (rows 8 rb + r, cols 8 w + 2 q + e)
         const double* xj = S.xj + buf * RM_TB * dp;
         const double2* pj2 = reinterpret_cast<const double2*>(S.pj + buf * 128);
-        const double2* pi2 = reinterpret_cast<const double2*>(S.pi);
         const double2 pJ0 = pj2[8 * w + 2 * q], pJ1 = pj2[8 * w + 2 * q + 1];
-        double c[8][2];
-#pragma unroll
-        for (int rb = 0; rb < 8; ++rb) {
-            const double bI = S.pi[2 * (8 * rb + r)];
-            c[rb][0] = bI + pJ0.x;
-            c[rb][1] = bI + pJ1.x;
-        }
-        for (int ch = 0; ch < nch; ++ch) {
-            const double2 bf = reinterpret_cast<const double2*>(xj)[(w * nch + ch) * 32 + lane];
-#pragma unroll
-            for (int rb = 0; rb < 8; ++rb) {
-                const double2 af = reinterpret_cast<const double2*>(S.xi)[(rb * nch + ch) * 32 + lane];
-                rm_dmma(c[rb][0], c[rb][1], af.x, bf.x);
-                rm_dmma(c[rb][0], c[rb][1], af.y, bf.y);
-            }
-        }
-        double col0 = 0.0, col1 = 0.0;
         const bool diag_tile = (J == I);
-#pragma unroll
-        for (int rb = 0; rb < 8; ++rb) {
-            double k0 = rm_exp(c[rb][0], tab);
-            double k1 = rm_exp(c[rb][1], tab);
-            if (diag_tile && rb == w) {
-                if (r == 2 * q) k0 = p.diag;
-                if (r == 2 * q + 1) k1 = p.diag;
-            }
-            rowp[rb] = fma(k0, pJ0.y, rowp[rb]);
-            rowp[rb] = fma(k1, pJ1.y, rowp[rb]);
-            const double vI = S.pi[2 * (8 * rb + r) + 1];
-            col0 = fma(k0, vI, col0);
-            col1 = fma(k1, vI, col1);
+        double col0 = 0.0, col1 = 0.0;
+        if (diag_tile) {
+            if (clamp) rm_tile<true, true>(S, xj, nch, w, lane, pJ0, pJ1, tab, p.diag, rowp, col0, col1);
+            else rm_tile<true, false>(S, xj, nch, w, lane, pJ0, pJ1, tab, p.diag, rowp, col0, col1);
+        } else {
+            if (clamp) rm_tile<false, true>(S, xj, nch, w, lane, pJ0, pJ1, tab, p.diag, rowp, col0, col1);
+            else rm_tile<false, false>(S, xj, nch, w, lane, pJ0, pJ1, tab, p.diag, rowp, col0, col1);
         }
         if (!diag_tile) {
             // column sums over the 64 rows: the 8 lanes of equal q (xor 4, 8, 16)
