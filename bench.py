@@ -270,6 +270,23 @@ def run_native(args, rank, world):
     P.solvers._solve_dev = traced
     P.recycle._solve_dev = traced
     P.gpc._solve_dev = traced
+    # the def-CG Newton loop runs pipelined (recycle.solve_next_async): the
+    # per-solve numbers come from the finished job (kernel device time, its,
+    # basis columns actually used)
+    orig_finish = P.recycle._AsyncSolve.finish
+
+    def traced_finish(job, *args, **kw):
+        x_, st_ = orig_finish(job, *args, **kw)
+        rep = st_.history[-1]
+        kk, its = job.log.k, rep.iterations
+        cfg_ = job.cfg
+        mv = (2 if kk else 1) + its + (its // cfg_.recompute_residual_every if cfg_.recompute_residual_every else 0)
+        solve_ms.append(rep.device_ms)
+        solve_its.append((its, kk))
+        solve_mv.append(mv)
+        return x_, st_
+
+    P.recycle._AsyncSolve.finish = traced_finish
 
     def sequence():
         _, recs = P.laplace_newton(gram, yd, "defcg", cfg, newton_tol=-np.inf, max_newton=c["newton_steps"], k=k,
@@ -341,6 +358,7 @@ def run_native(args, rank, world):
     P.solvers._solve_dev = orig
     P.recycle._solve_dev = orig
     P.gpc._solve_dev = orig
+    P.recycle._AsyncSolve.finish = orig_finish
     xh = torch.from_numpy(x).pin_memory()
     yh = torch.from_numpy(y).pin_memory()
     e2e_steps = max(1, min(args.steps, 3))

@@ -209,6 +209,24 @@ DCG_API int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op, co
               const double* d_x0, const dcg_basis* basis, const dcg_solver_config* cfg,
               double* d_x, dcg_krylov_log* log, double* d_history,
               dcg_solve_info* out, long long* info);
+/* Enqueue-only dcg_solve: no host synchronisation.  d_kuse (optional device
+ * int64): basis columns in use (<= basis->k, 0 = plain CG), as written by
+ * dcg_refresh_basis_async.  d_status (64 bytes on the device) receives
+ * {int32 status, int32 columns used, int64 info, int64 iterations, int64
+ * stored log entries, f64 rel residual, f64 norm_b} in stream order.  The
+ * log's mu rows keep the stride basis->k.                                  */
+DCG_API int dcg_solve_async(dcg_context* ctx, void* stream, const dcg_operator* op,
+                            const double* d_b, const double* d_x0, const dcg_basis* basis,
+                            const dcg_solver_config* cfg, double* d_x, dcg_krylov_log* log,
+                            double* d_history, const long long* d_kuse, void* d_status);
+/* Enqueue-only refresh_basis: surviving column count to *d_kout (device
+ * int64; 0 when nothing survives -- BasisDeficient -- or when d_valid, the
+ * result block of the extraction that produced d_w, reports a failure).
+ * Outputs compacted to d_kout columns; d_w_out / d_aw_out hold n x k.       */
+DCG_API int dcg_refresh_basis_async(dcg_context* ctx, void* stream, const dcg_operator* op,
+                                    const double* d_w, long long k, const long long* d_valid,
+                                    double* d_w_out, double* d_aw_out, double* d_chol,
+                                    long long* d_kout);
 /* v - AW (W'AW)^-1 W' v                              solvers.py:242-256       */
 DCG_API int dcg_deflation_project(dcg_context* ctx, void* stream, long long n,
                           const dcg_basis* basis, const double* d_v, double* d_out);
@@ -234,6 +252,17 @@ DCG_API int dcg_ritz_extract_async(dcg_context* ctx, void* stream, long long n,
                                    double* d_z, double* d_w_next, double* d_aw_next,
                                    long long* d_result);
 
+/* Device-driven form, enqueued behind dcg_solve_async without waiting for it:
+ * the stored log length and the basis columns that solve used are read from
+ * its status block (d_solve_status); prev->k is the basis' column capacity
+ * (columns compacted, stride = columns used), log->ell the log capacity.
+ * d_result as for dcg_ritz_extract_async (BasisDeficient when k > T).      */
+DCG_API int dcg_ritz_extract_dev(dcg_context* ctx, void* stream, long long n,
+                                 const dcg_krylov_log* log, const void* d_solve_status,
+                                 const dcg_basis* prev, long long k, int selection,
+                                 double* d_theta, double* d_w_next, double* d_aw_next,
+                                 long long* d_result);
+
 /* ---- L4: GPC Laplace-Newton glue (gpc.py) -------------------------------- */
 /* loglik, grad, h of the logistic likelihood          gpc.py:126-157          */
 DCG_API int dcg_gpc_derivs(dcg_context* ctx, void* stream, long long n, const double* d_f,
@@ -251,6 +280,12 @@ DCG_API int dcg_gpc_newton_update(dcg_context* ctx, void* stream, const dcg_oper
                           const double* d_y, double* d_a, double* d_f, double* d_grad,
                           double* d_h, double* loglik, double* psi);
 
+/* Enqueue-only newton_update for a full operator: (loglik, psi) are written
+ * to d_llpsi (2 doubles on the device) in stream order.                     */
+DCG_API int dcg_gpc_newton_update_async(dcg_context* ctx, void* stream, const dcg_operator* kop,
+                                        const double* d_inner, const double* d_s, const double* d_x,
+                                        const double* d_y, double* d_a, double* d_f, double* d_grad,
+                                        double* d_h, double* d_llpsi);
 /* (loglik, grad, h)(f) and psi = loglik - f'a / 2 for full f, a (gpc.py:204-209) */
 DCG_API int dcg_gpc_objective(dcg_context* ctx, void* stream, long long n, const double* d_f,
                               const double* d_y, const double* d_a, double* d_grad, double* d_h,

@@ -36,6 +36,20 @@ def side_stream() -> torch.cuda.Stream:
     return s
 
 
+_copy_streams: dict[int, torch.cuda.Stream] = {}
+
+
+def copy_stream() -> torch.cuda.Stream:
+    """Per-device stream for small device-to-host result copies that must not
+    queue behind either compute stream."""
+    d = device()
+    s = _copy_streams.get(d.index)
+    if s is None:
+        s = torch.cuda.Stream(device=d)
+        _copy_streams[d.index] = s
+    return s
+
+
 def stream() -> int:
     return torch.cuda.current_stream(device()).cuda_stream
 

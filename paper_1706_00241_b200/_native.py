@@ -138,6 +138,21 @@ SIGNATURES = {
         ctypes.POINTER(CSolveInfo),
         _PLL,
     ],
+    "dcg_solve_async": [
+        _P,
+        _P,
+        ctypes.POINTER(COperator),
+        _P,
+        _P,
+        ctypes.POINTER(CBasis),
+        ctypes.POINTER(CSolverConfig),
+        _P,
+        ctypes.POINTER(CKrylovLog),
+        _P,
+        _P,
+        _P,
+    ],
+    "dcg_refresh_basis_async": [_P, _P, ctypes.POINTER(COperator), _P, _LL, _P, _P, _P, _P, _P],
     "dcg_deflation_project": [_P, _P, _LL, ctypes.POINTER(CBasis), _P, _P],
     "dcg_ritz_extract": [
         _P,
@@ -172,10 +187,25 @@ SIGNATURES = {
         _P,
         _P,
     ],
+    "dcg_ritz_extract_dev": [
+        _P,
+        _P,
+        _LL,
+        ctypes.POINTER(CKrylovLog),
+        _P,
+        ctypes.POINTER(CBasis),
+        _LL,
+        ctypes.c_int,
+        _P,
+        _P,
+        _P,
+        _P,
+    ],
     "dcg_gpc_derivs": [_P, _P, _LL, _P, _P, _P, _P, _PD],
     "dcg_gpc_newton_system": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P, _P, _P],
     "dcg_gpc_newton_update": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P, _P, _P, _P, _P, _PD, _PD],
     "dcg_gpc_objective": [_P, _P, _LL, _P, _P, _P, _P, _P, _PD, _PD],
+    "dcg_gpc_newton_update_async": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P, _P, _P, _P, _P, _P],
     # row-sharded def-CG (include/defcg_b200.h L5)
     "dcg_shard_apply_dot": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P],
     "dcg_shard_residual": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P],

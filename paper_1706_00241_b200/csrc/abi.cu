@@ -1,3 +1,4 @@
+#include <stddef.h>
 // C ABI entry points (include/defcg_b200.h): context, workspace, the L0
 // kernel twins, operator application, basis refresh / Gram factorisation,
 // harmonic-Ritz extraction, eigensolvers and the GPC glue.  Each entry point
@@ -520,6 +521,78 @@ extern "C" int dcg_refresh_basis(dcg_context* ctx, void* stream, const dcg_opera
     return DCG_OK;
 }
 
+// Device-side end of an asynchronous refresh: the surviving column count
+// (0 when the extraction that produced W failed -- its result block says so --
+// or when pruning empties the basis: recycle.py:178-179 then solves with
+// plain CG), the gathered W / AW columns and the compact factor.
+__global__ void refresh_finish_kernel(const DevStatus* ds, const long long* d_valid, const int* active, int k,
+                                      long long n, const double* W, const double* AW, const double* Lc,
+                                      double* w_out, double* aw_out, double* chol_out, long long* kout) {
+    const bool ok = ds->status == DCG_OK && (!d_valid || d_valid[0] == DCG_OK);
+    const int kk = ok ? (int)ds->count : 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *kout = kk;
+    if (kk == 0) return;
+    const long long total = n * kk;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long i = e / kk;
+        const int c = active[(int)(e - i * kk)];
+        w_out[e] = W[i * k + c];
+        aw_out[e] = AW[i * k + c];
+    }
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)kk * kk;
+         e += (long long)gridDim.x * blockDim.x)
+        chol_out[e] = Lc[e];
+}
+
+// refresh_basis without host synchronisation: the column count stays on the
+// device (*d_kout), for dcg_solve_async's d_kuse.  d_valid (optional) is the
+// result block of the extraction that produced d_w.
+extern "C" int dcg_refresh_basis_async(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_w,
+                                       long long k, const long long* d_valid, double* d_w_out, double* d_aw_out,
+                                       double* d_chol, long long* d_kout) {
+    if (!ctx || k < 0 || !d_kout) return DCG_E_CONFIG;
+    int rc = check_dense_op(op);
+    if (rc) return rc;
+    if (op->row0 != 0 || op->rows != op->n) return DCG_E_UNSUPPORTED;
+    cudaStream_t st = as_stream(stream);
+    if (k == 0) {
+        DCG_CUDA(cudaMemsetAsync(d_kout, 0, sizeof(long long), st));
+        return DCG_OK;
+    }
+    if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
+    const long long n = op->n;
+    const size_t nk = sizeof(double) * n * k;
+    const size_t need = al(sizeof(double) * dcg_block_apply_scratch_doubles(n, n, (int)k)) + al(nk) +
+                        gram_scratch_bytes(ctx, (int)k);
+    rc = dcg_ws_reserve(ctx, need);
+    if (rc) return rc;
+    Arena ar{static_cast<char*>(ctx->ws), 0};
+    double* aw = ar.take<double>(n * k);
+    int* active = ar.take<int>(DCG_MAX_K);
+    double* scratch = ar.take<double>(dcg_block_apply_scratch_doubles(n, n, (int)k));
+    if (op->kind == DCG_OP_RBF)
+        rc = dcg_rbf_mf_block(ctx, st, op, d_w, (int)k, op->d_s, op->d_s, op->shift, aw);
+    else
+        rc = dcg_block_apply(ctx, st, op->d_k, op->ldk, n, n, d_w, (int)k, op->d_s, op->d_s, op->shift, d_w, aw,
+                             scratch);
+    if (rc) return rc;
+    double* graw = ar.take<double>((size_t)k * k);
+    double* gsym = ar.take<double>((size_t)k * k);
+    double* lwork = ar.take<double>((size_t)2 * k * k);
+    double* parts = ar.take<double>(dcg_xty_scratch_doubles(ctx, (int)k, (int)k));
+    DevStatus* ds = ar.take<DevStatus>(1);
+    DCG_CUDA(cudaMemsetAsync(ds, 0, sizeof(DevStatus), st));
+    rc = dcg_xty(ctx, st, d_w, (int)k, aw, (int)k, n, (int)k, (int)k, graw, parts);
+    if (rc) return rc;
+    rc = dcg_gram_factor_launch(st, graw, (int)k, 1, gsym, lwork, active, ds);
+    if (rc) return rc;
+    refresh_finish_kernel<<<ctx->sm_count * 2, 256, 0, st>>>(ds, d_valid, active, (int)k, n, d_w, aw, lwork, d_w_out,
+                                                             d_aw_out, d_chol, d_kout);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}
+
 // P_W v = v - AW (W'AW)^-1 W' v   (solvers.py:242-256)
 __global__ void project_kernel(long long n, int k, const double* L, const double* c, const double* v,
                                const double* AW, double* out) {
@@ -625,6 +698,37 @@ extern "C" int dcg_gpc_newton_system(dcg_context* ctx, void* stream, const dcg_o
     if (rc) return rc;
     // b = s (.) (K inner): K's own scaling/shift are ignored here (K is the kernel matrix)
     return apply_k(ctx, st, kop, d_inner, nullptr, d_s + kop->row0, 0.0, d_b, static_cast<double*>(ctx->ws));
+}
+
+// gpc newton_update without host synchronisation: (loglik, psi) go to d_llpsi
+// (2 doubles on the device).  Full (unsharded) operators only.
+extern "C" int dcg_gpc_newton_update_async(dcg_context* ctx, void* stream, const dcg_operator* kop,
+                                           const double* d_inner, const double* d_s, const double* d_x,
+                                           const double* d_y, double* d_a, double* d_f, double* d_grad, double* d_h,
+                                           double* d_llpsi) {
+    if (!ctx || !d_llpsi) return DCG_E_CONFIG;
+    int rc = check_dense_op(kop);
+    if (rc) return rc;
+    if (kop->row0 != 0 || kop->rows != kop->n) return DCG_E_UNSUPPORTED;
+    cudaStream_t st = as_stream(stream);
+    const long long n = kop->n;
+    const size_t need = al(sizeof(double) * 2 * ctx->sm_count * 2) + al(sizeof(DevStatus)) +
+                        al(sizeof(double) * apply_k_scratch(kop));
+    rc = dcg_ws_reserve(ctx, need);
+    if (rc) return rc;
+    Arena ar{static_cast<char*>(ctx->ws), 0};
+    double* part = ar.take<double>(4 * ctx->sm_count);
+    DevStatus* ds = ar.take<DevStatus>(1);
+    double* scratch = ar.take<double>(apply_k_scratch(kop));
+    rc = dcg_newton_a_launch(ctx, st, n, d_inner, d_s, d_x, d_a);
+    if (rc) return rc;
+    rc = apply_k(ctx, st, kop, d_a, nullptr, nullptr, 0.0, d_f, scratch);
+    if (rc) return rc;
+    rc = dcg_derivs_launch(ctx, st, n, d_f, d_y, d_a, d_grad, d_h, part, ds);
+    if (rc) return rc;
+    static_assert(offsetof(DevStatus, value2) == offsetof(DevStatus, value) + sizeof(double), "DevStatus layout");
+    DCG_CUDA(cudaMemcpyAsync(d_llpsi, &ds->value, 2 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return DCG_OK;
 }
 
 extern "C" int dcg_gpc_newton_update(dcg_context* ctx, void* stream, const dcg_operator* kop, const double* d_inner,

@@ -84,12 +84,20 @@ size_t dcg_sym_apply_scratch_doubles(long long n) { return 2 * (size_t)sym_ntile
 int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, long long ldk, long long n, const double* v,
                   const double* s_in, const double* s_out, double shift, double* y, double* scratch) {
     if (n <= 0) return DCG_OK;
-    const size_t smem = sizeof(double) * (size_t)sym_smem_doubles();
+    // One SM is left to the single-CTA Ritz pencil that the def-CG sequence
+    // runs concurrently on the side stream (the K-products of the Newton
+    // update overlap it): the pass-1 CTAs ask for the whole opt-in shared
+    // memory, so none of them can share the pencil's SM, and they are one
+    // fewer than the SMs.  A CTA sharing the pencil's SM had stretched both
+    // (pencil 220 -> 360 us, pass 1 73 -> 117 us).
+    size_t smem = sizeof(double) * (size_t)sym_smem_doubles();
+    if (ctx->smem_optin > smem) smem = ctx->smem_optin;
     DCG_CUDA(cudaFuncSetAttribute(sym_pass1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const long long ntt = sym_ntiles(n);
     double* colpart = scratch;
     double* rowpart = scratch + ntt * DCG_TB;
-    const int G = ctx->sm_count < DCG_SYM_MAX_CTAS ? ctx->sm_count : DCG_SYM_MAX_CTAS;
+    const int navail = ctx->sm_count > 1 ? ctx->sm_count - 1 : 1;
+    const int G = navail < DCG_SYM_MAX_CTAS ? navail : DCG_SYM_MAX_CTAS;
     sym_pass1_kernel<<<G, DCG_NT, smem, st>>>(K, ldk, n, v, s_in, colpart, rowpart);
     DCG_LAUNCHED();
     sym_pass2_kernel<<<G, DCG_NT, 0, st>>>(n, G, colpart, rowpart, v, s_out, shift, y);

@@ -503,6 +503,13 @@ __global__ void __launch_bounds__(SD_NT) gram_factor_kernel(const double* Graw, 
 // barrier.  Convergence: off(X'X) <= rtol ||C||_F before every sweep
 // (linalg.py:156-163).  X: column c at X + c * n (T <= 64); Vc column-major.
 // ---------------------------------------------------------------------------
+// developer diagnostics of the Ritz pencil (dcg_debug_pencil_profile):
+// globaltimer stamps of its phases and the one-sided Jacobi sweep count
+__device__ unsigned long long g_pencil_prof[16];
+__device__ __forceinline__ void pencil_stamp(int i) {
+    if (threadIdx.x == 0) g_pencil_prof[i] = globaltimer_ns();
+}
+
 __device__ int cta_jacobi_onesided(double* X, double* Vc, int n, int max_sweeps, double rtol, double* red) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     __shared__ int s_res1;
@@ -537,7 +544,9 @@ __device__ int cta_jacobi_onesided(double* X, double* Vc, int n, int max_sweeps,
     if (frob == 0.0) return 0;
     bool converged = off <= rtol * frob;
     const int Te = n + (n & 1), np = Te / 2;
+    int sweeps_done = 0;
     for (int sweep = 0; sweep < max_sweeps && !converged; ++sweep) {
+        ++sweeps_done;
         for (int round = 0; round < Te - 1; ++round) {
             // each pair's warp forms the pair's 2 x 2 Gram, computes the
             // rotation (redundantly on its lanes: no broadcast) and rotates
@@ -595,6 +604,7 @@ __device__ int cta_jacobi_onesided(double* X, double* Vc, int n, int max_sweeps,
         converged = off <= rtol * frob;
     }
     if (tid == 0) s_res1 = converged ? 0 : max_sweeps;
+    if (tid == 0) g_pencil_prof[7] = sweeps_done;
     cta_sync();
     return s_res1;
 }
@@ -624,6 +634,9 @@ __global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fr
         if (plan->status != DCG_OK) return;
         T = (int)plan->count;
     }
+    pencil_stamp(0);
+    if (threadIdx.x == 0)
+        for (int i = 8; i < 14; ++i) g_pencil_prof[i] = 0;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nw = blockDim.x >> 5;
     // F, G (symmetrised, T x T) stay in the global scratch: they are only read
@@ -666,6 +679,7 @@ __global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fr
         }
         cta_sync();
     }
+    pencil_stamp(1);
     double* A = staged ? sm + 3 * T * T : sm;
     double* V = staged ? sm : sm + T * T;
     bool onesided = false;
@@ -695,7 +709,9 @@ __global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fr
     if (onesided) {
         // Vc (column-major) in S3; afterwards theta on the diagonal of A := S2 and V row-major in S0
         double* Vc = A;
+        pencil_stamp(2);
         nc = cta_jacobi_onesided(Y, Vc, na, max_sweeps, 1e-14, red);
+        pencil_stamp(3);
         if (nc == 0) {
             for (int c = warp; c < na; c += nw) {
                 const double x0 = lane < na ? Y[c * na + lane] : 0.0, x1 = lane + 32 < na ? Y[c * na + lane + 32] : 0.0;
@@ -758,6 +774,15 @@ __global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fr
     }
     if (tid < na) active[tid] = s_act[tid];
     if (tid == 0) { st->status = DCG_OK; st->count = na; }
+    pencil_stamp(4);
+    if (tid == 0) g_pencil_prof[6] = na;
+}
+
+extern "C" __attribute__((visibility("default"))) int dcg_debug_pencil_profile(long long* out8) {
+    unsigned long long h[16];
+    if (cudaMemcpyFromSymbol(h, g_pencil_prof, sizeof(h)) != cudaSuccess) return DCG_E_CUDA;
+    for (int i = 0; i < 16; ++i) out8[i] = (long long)h[i];
+    return DCG_OK;
 }
 
 // ===========================================================================
@@ -943,7 +968,12 @@ int dcg_gram_factor_launch(cudaStream_t st, const double* Graw, int k, int prune
 }
 
 size_t dcg_pencil_smem(int T) { return sizeof(double) * 2 * (size_t)T * T; }
-static size_t pencil_smem(int T) { return sizeof(double) * (T <= DCG_PENCIL_SMEM_T ? 4 : 2) * (size_t)T * T; }
+// for any pencil order up to T (the device-driven extraction knows only a bound)
+static size_t pencil_smem(int T) {
+    const size_t staged = 4 * (size_t)(T < DCG_PENCIL_SMEM_T ? T : DCG_PENCIL_SMEM_T) * (T < DCG_PENCIL_SMEM_T ? T : DCG_PENCIL_SMEM_T);
+    const size_t plain = 2 * (size_t)T * T;
+    return sizeof(double) * (staged > plain ? staged : plain);
+}
 
 int dcg_ritz_pencil_launch(cudaStream_t st, const double* Fraw, const double* Graw, int T, int k, int largest,
                            int max_sweeps, double* wk, double* theta, double* U, int* active, DevStatus* ds,

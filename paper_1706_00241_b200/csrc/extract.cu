@@ -29,8 +29,26 @@ __global__ void __launch_bounds__(EX_NT)
     zgather_kernel(long long n, int kp, const double* __restrict__ Wp, const double* __restrict__ AWp, int m,
                    const double* __restrict__ P, const double* __restrict__ R, const double* __restrict__ alpha,
                    int k, double* Zraw, double* AZraw, double* part, unsigned int* counter, double* norms, int* keep,
-                   DevStatus* plan) {
+                   DevStatus* plan, const DevStatus* solve_st) {
     extern __shared__ double sm[];
+    if (solve_st) {
+        // device-driven form: the finished solve's status block gives the
+        // basis columns it used (pad) and the stored log length (aux)
+        const bool bad = solve_st->status != DCG_OK;
+        kp = (int)solve_st->pad;
+        m = (int)solve_st->aux;
+        if (bad || k > kp + m) {
+            // recycle.py:104-108 (k > T: BasisDeficient(T)); a failed solve
+            // leaves nothing to extract (its error surfaces from the solve)
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                plan->status = bad ? solve_st->status : DCG_E_BASIS_DEFICIENT;
+                plan->info = kp + m;
+                plan->count = kp + m;
+                plan->aux = kp + m;
+            }
+            return;
+        }
+    }
     const int T = kp + m;
     double* zt = sm;                   // EX_ROWS x T
     double* azt = sm + EX_ROWS * T;    // EX_ROWS x T
@@ -78,6 +96,7 @@ __global__ void __launch_bounds__(EX_NT)
             if (norms[c] > 0.0) keep[t++] = c;
         plan->count = t;
         plan->info = t;
+        plan->aux = T;   // column stride of Zraw / AZraw
         plan->status = (t < k) ? DCG_E_BASIS_DEFICIENT : DCG_OK;   // recycle.py:131-132
     }
 }
@@ -85,11 +104,12 @@ __global__ void __launch_bounds__(EX_NT)
 // ---------------------------------------------------------------------------- E2
 #define FG_PPT 8
 __global__ void __launch_bounds__(EX_NT)
-    zscale_fg_kernel(long long n, int T, const double* __restrict__ Zraw, const double* __restrict__ AZraw,
+    zscale_fg_kernel(long long n, const double* __restrict__ Zraw, const double* __restrict__ AZraw,
                      const double* __restrict__ norms, const int* __restrict__ keep, const DevStatus* plan, double* Zs,
                      double* AZs, double* part) {
     if (plan->status != DCG_OK) return;
     extern __shared__ double sm[];
+    const int T = (int)plan->aux;
     const int Tk = (int)plan->count;
     const int npairs = 2 * Tk * Tk;
     const int p0 = blockIdx.y * (EX_NT * FG_PPT);
@@ -271,28 +291,14 @@ static size_t extract_ws_bytes(dcg_context* ctx, long long n, int T, int k) {
            3 * al(sizeof(DevStatus)) + 2 * al(sizeof(unsigned int) * 4) + 8192;
 }
 
-// Enqueue the extraction; `d_result` (3 x int64 on the device) receives
-// status, info, t_out when the stream reaches the end.  Host-checkable
-// argument errors return immediately.
-extern "C" int dcg_ritz_extract_async(dcg_context* ctx, void* stream, long long n, const dcg_krylov_log* log,
-                                      long long m, const dcg_basis* prev, long long k, int selection, double* d_theta,
-                                      double* d_u, double* d_z, double* d_w_next, double* d_aw_next,
-                                      long long* d_result) {
-    if (!ctx || n < 0 || m < 0 || k < 0 || !d_result) return DCG_E_CONFIG;
-    if (selection != DCG_SELECT_SMALLEST && selection != DCG_SELECT_LARGEST) return DCG_E_CONFIG;
-    const long long kp = prev ? prev->k : 0;
-    const long long T = kp + m;
-    cudaStream_t st = as_stream(stream);
-    if (k > T || k == 0) {
-        // decided on the host (recycle.py:104-108 / k == 0): write the result block
-        long long h[3] = {k > T ? (long long)DCG_E_BASIS_DEFICIENT : (long long)DCG_OK, T, T};
-        DCG_CUDA(cudaMemcpyAsync(d_result, h, sizeof(h), cudaMemcpyHostToDevice, st));
-        DCG_CUDA(cudaStreamSynchronize(st));   // h is a stack buffer
-        return DCG_OK;
-    }
+// Enqueue the pipeline.  T is the column count (host-known), or with
+// solve_st the upper bound k_prev_max + ell (the actual k_prev and m are read
+// from the solve's status block on the device).
+static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const dcg_krylov_log* log, long long m,
+                           long long kp, long long T, const DevStatus* solve_st, const double* Wp, const double* AWp,
+                           long long k, int selection, double* d_theta, double* d_u, double* d_z, double* d_w_next,
+                           double* d_aw_next, long long* d_result) {
     if (k > DCG_MAX_K || T > DCG_MAX_T) return DCG_E_UNSUPPORTED;
-    if (m > 0 && (!log || log->ell < m || !log->d_p || !log->d_r || !log->d_alpha)) return DCG_E_CONFIG;
-    if (kp > 0 && (!prev->d_w || !prev->d_aw)) return DCG_E_CONFIG;
     int rc = dcg_ws_reserve(ctx, extract_ws_bytes(ctx, n, (int)T, (int)k));
     if (rc) return rc;
     const int G = ctx->sm_count;
@@ -318,22 +324,20 @@ extern "C" int dcg_ritz_extract_async(dcg_context* ctx, void* stream, long long 
     unsigned int* counters = ar.take<unsigned int>(4);
     DCG_CUDA(cudaMemsetAsync(plan, 0, al(sizeof(DevStatus)) * 2, st));
     DCG_CUDA(cudaMemsetAsync(counters, 0, 16, st));
-    const double* Wp = kp ? prev->d_w : nullptr;
-    const double* AWp = kp ? prev->d_aw : nullptr;
-    const double* P = m ? log->d_p : nullptr;
-    const double* R = m ? log->d_r : nullptr;
-    const double* alpha = m ? log->d_alpha : nullptr;
+    const double* P = log ? log->d_p : nullptr;
+    const double* R = log ? log->d_r : nullptr;
+    const double* alpha = log ? log->d_alpha : nullptr;
 
     int nb = G;
     if (n < (long long)nb * EX_ROWS) nb = (int)max(1LL, (n + EX_ROWS - 1) / EX_ROWS);
     const size_t sm1 = sizeof(double) * 2 * EX_ROWS * T;
     DCG_CUDA(cudaFuncSetAttribute(zgather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
     zgather_kernel<<<nb, EX_NT, sm1, st>>>(n, (int)kp, Wp, AWp, (int)m, P, R, alpha, (int)k, Zraw, AZraw, part,
-                                           counters, norms, keep, plan);
+                                           counters, norms, keep, plan, solve_st);
     DCG_LAUNCHED();
     const int gy = (int)((2 * T * T + EX_NT * FG_PPT - 1) / (EX_NT * FG_PPT));
     DCG_CUDA(cudaFuncSetAttribute(zscale_fg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
-    zscale_fg_kernel<<<dim3(nb, gy), EX_NT, sm1, st>>>(n, (int)T, Zraw, AZraw, norms, keep, plan, Zs, AZs, fgpart);
+    zscale_fg_kernel<<<dim3(nb, gy), EX_NT, sm1, st>>>(n, Zraw, AZraw, norms, keep, plan, Zs, AZs, fgpart);
     DCG_LAUNCHED();
     const int warps = (int)(2 * T * T);
     fg_reduce_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>(fgpart, nb, plan, Fraw, Graw);
@@ -347,11 +351,65 @@ extern "C" int dcg_ritz_extract_async(dcg_context* ctx, void* stream, long long 
     DCG_LAUNCHED();
     const size_t sm6 = sizeof(double) * (size_t)T * k;
     DCG_CUDA(cudaFuncSetAttribute(wnext_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm6));
-    wnext_kernel<<<G * 2, EX_NT, sm6, st>>>(n, (int)k, Zs, AZs, plan, pencil, Uexp, active, d_w_next, d_aw_next, d_z,
-                                            d_result);
+    wnext_kernel<<<G * 2, EX_NT, sm6, st>>>(n, (int)k, Zs, AZs, plan, pencil, Uexp, active, d_w_next, d_aw_next,
+                                            d_z, d_result);
     DCG_LAUNCHED();
     if (d_u) DCG_CUDA(cudaMemcpyAsync(d_u, U, sizeof(double) * T * k, cudaMemcpyDeviceToDevice, st));
     return DCG_OK;
+}
+
+// Enqueue the extraction; `d_result` (3 x int64 on the device) receives
+// status, info, t_out when the stream reaches the end.  Host-checkable
+// argument errors return immediately.
+extern "C" int dcg_ritz_extract_async(dcg_context* ctx, void* stream, long long n, const dcg_krylov_log* log,
+                                      long long m, const dcg_basis* prev, long long k, int selection, double* d_theta,
+                                      double* d_u, double* d_z, double* d_w_next, double* d_aw_next,
+                                      long long* d_result) {
+    if (!ctx || n < 0 || m < 0 || k < 0 || !d_result) return DCG_E_CONFIG;
+    if (selection != DCG_SELECT_SMALLEST && selection != DCG_SELECT_LARGEST) return DCG_E_CONFIG;
+    const long long kp = prev ? prev->k : 0;
+    const long long T = kp + m;
+    cudaStream_t st = as_stream(stream);
+    if (k > T || k == 0) {
+        // decided on the host (recycle.py:104-108 / k == 0): write the result block
+        long long h[3] = {k > T ? (long long)DCG_E_BASIS_DEFICIENT : (long long)DCG_OK, T, T};
+        DCG_CUDA(cudaMemcpyAsync(d_result, h, sizeof(h), cudaMemcpyHostToDevice, st));
+        DCG_CUDA(cudaStreamSynchronize(st));   // h is a stack buffer
+        return DCG_OK;
+    }
+    if (k > DCG_MAX_K || T > DCG_MAX_T) return DCG_E_UNSUPPORTED;
+    if (m > 0 && (!log || log->ell < m || !log->d_p || !log->d_r || !log->d_alpha)) return DCG_E_CONFIG;
+    if (kp > 0 && (!prev->d_w || !prev->d_aw)) return DCG_E_CONFIG;
+    return extract_enqueue(ctx, st, n, m ? log : nullptr, m, kp, T, nullptr, kp ? prev->d_w : nullptr,
+                           kp ? prev->d_aw : nullptr, k, selection, d_theta, d_u, d_z, d_w_next, d_aw_next, d_result);
+}
+
+// Device-driven form, enqueued right behind dcg_solve_async without waiting
+// for it: the stored log length m and the basis columns the solve used are
+// read from its status block (d_solve_status, the 64-byte block
+// dcg_solve_async wrote); prev->k is the basis' column capacity (its columns
+// compacted, stride = columns used), log->ell the log capacity.
+extern "C" int dcg_ritz_extract_dev(dcg_context* ctx, void* stream, long long n, const dcg_krylov_log* log,
+                                    const void* d_solve_status, const dcg_basis* prev, long long k, int selection,
+                                    double* d_theta, double* d_w_next, double* d_aw_next, long long* d_result) {
+    if (!ctx || n < 0 || k < 1 || !d_result || !d_solve_status || !log) return DCG_E_CONFIG;
+    if (selection != DCG_SELECT_SMALLEST && selection != DCG_SELECT_LARGEST) return DCG_E_CONFIG;
+    const long long kmax = prev ? prev->k : 0;
+    const long long T = kmax + log->ell;
+    if (kmax > 0 && (!prev->d_w || !prev->d_aw)) return DCG_E_CONFIG;
+    if (log->ell > 0 && (!log->d_p || !log->d_r || !log->d_alpha)) return DCG_E_CONFIG;
+    if (T < 1) {
+        // nothing can ever be extracted: BasisDeficient(0) (k >= 1 > T)
+        DCG_CUDA(cudaMemsetAsync(d_result, 0, 3 * sizeof(long long), as_stream(stream)));
+        long long* r0 = d_result;
+        const long long code = DCG_E_BASIS_DEFICIENT;
+        DCG_CUDA(cudaMemcpyAsync(r0, &code, sizeof(code), cudaMemcpyHostToDevice, as_stream(stream)));
+        DCG_CUDA(cudaStreamSynchronize(as_stream(stream)));
+        return DCG_OK;
+    }
+    return extract_enqueue(ctx, as_stream(stream), n, log, 0, 0, T, static_cast<const DevStatus*>(d_solve_status),
+                           kmax ? prev->d_w : nullptr, kmax ? prev->d_aw : nullptr, k, selection, d_theta, nullptr,
+                           nullptr, d_w_next, d_aw_next, d_result);
 }
 
 // Synchronous form: enqueue, wait, and map the outcome to a status.

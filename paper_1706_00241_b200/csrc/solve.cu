@@ -37,7 +37,8 @@ struct SolveArgs {
     const double* b;
     const double* x0;
     double* x;
-    int k;
+    int k;                 // basis columns (the layout / maximum)
+    const long long* kdev; // optional: columns in use, read on the device (<= k; 0 = plain CG)
     const double* W;
     const double* AW;
     const double* L;
@@ -186,13 +187,16 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     } while (0)
     extern __shared__ __align__(16) double smem[];
     const long long n = a.n;
-    const int k = a.k;
+    // columns in use: the host's k, or the device-side count an asynchronous
+    // refresh left (W / AW / L are then compacted to that many columns)
+    const int kmax = a.k;
+    const int k = a.kdev ? (int)min((long long)kmax, max(0LL, *a.kdev)) : kmax;
     const int G = gridDim.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int xt = (int)min(n, (long long)DCG_QT) + 2;
     double* s_g = smem;                                  // GEMV region (strategy dependent)
     double* s_L = s_g + gemv_region_doubles(STRAT, n, a.rbf.dim, a.rbf.nteam);   // k*k
-    double* s_rd = s_L + k * k;                          // DCG_MAX_K  1 / L_jj
+    double* s_rd = s_L + kmax * kmax;                    // DCG_MAX_K  1 / L_jj
     double* s_c = s_rd + DCG_MAX_K;                      // 1 + DCG_MAX_K reduced slots
     double* s_mu = s_c + DCG_MAX_K + 2;                  // DCG_MAX_K
     double* s_tmp = s_mu + DCG_MAX_K;                    // 64 scratch
@@ -353,6 +357,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         if (blockIdx.x == 0 && tid == 0) {
             a.history[0] = 0.0;
             a.st->status = DCG_OK;
+            a.st->pad = k;
             a.st->info = 0;
             a.st->count = 0;   // iterations
             a.st->aux = 0;     // stored
@@ -395,7 +400,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     }
     if (blockIdx.x == 0) {
         if (tid == 0) a.history[0] = rel;
-        if (deflate && cont && it < ell && tid < k) a.logMu[tid] = s_mu[tid];
+        if (deflate && cont && it < ell && tid < k) a.logMu[tid] = s_mu[tid];   // stride kmax
     }
     GSYNC();
 
@@ -425,6 +430,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         if (d <= 0.0) {   // solvers.py:170-172 (NaN falls through, as in numpy)
             if (blockIdx.x == 0 && tid == 0) {
                 a.st->status = DCG_E_BREAKDOWN;
+                a.st->pad = k;
                 a.st->info = it;
                 a.st->count = it;
             }
@@ -484,7 +490,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
             a.p[i] = pi;
             if (log_p) a.logP[it * n + i] = pi;
         }
-        if (log_p && deflate && blockIdx.x == 0 && tid < k) a.logMu[it * k + tid] = s_mu[tid];
+        if (log_p && deflate && blockIdx.x == 0 && tid < k) a.logMu[it * kmax + tid] = s_mu[tid];
         rr = rr_new;
         PHASE(11);
         GSYNC();
@@ -492,6 +498,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     }
     if (blockIdx.x == 0 && tid == 0) {
         a.st->status = DCG_OK;
+        a.st->pad = k;
         a.st->info = 0;
         a.st->count = it;
         a.st->aux = (it < ell) ? it : ell;
@@ -512,10 +519,10 @@ int dcg_rbf_mma_teams(const dcg_context* ctx, int dim, size_t other_bytes);
 RbfMma dcg_rbf_mma_params(const dcg_operator* op, double* operands, int nteam);
 int dcg_rbf_mma_prep(const dcg_context* ctx, cudaStream_t st, const RbfMma& p);
 
-extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_b,
-                         const double* d_x0, const dcg_basis* basis, const dcg_solver_config* cfg,
-                         double* d_x, dcg_krylov_log* log, double* d_history, dcg_solve_info* out,
-                         long long* info) {
+static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_b,
+                      const double* d_x0, const dcg_basis* basis, const dcg_solver_config* cfg, double* d_x,
+                      dcg_krylov_log* log, double* d_history, dcg_solve_info* out, long long* info,
+                      const long long* d_kuse, void* d_status) {
     if (!ctx || !op || !cfg || !d_b || !d_x0 || !d_x || !d_history) return DCG_E_CONFIG;
     if (info) *info = 0;
     const long long n = op->n;
@@ -560,6 +567,7 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
     a.x0 = d_x0;
     a.x = d_x;
     a.k = k;
+    a.kdev = k ? d_kuse : nullptr;
     a.W = k ? basis->d_w : nullptr;
     a.AW = k ? basis->d_aw : nullptr;
     a.L = k ? basis->d_chol : nullptr;
@@ -623,6 +631,12 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
     DCG_CUDA(cudaEventRecord(ctx->ev0, st));
     DCG_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(DCG_NT), args, smem, st));
     dcg_count_launch();
+    if (d_status) {
+        // asynchronous form: the status block (and the column count used, in
+        // its `pad` word) is copied out in stream order; nothing waits here
+        DCG_CUDA(cudaMemcpyAsync(d_status, a.st, sizeof(DevStatus), cudaMemcpyDeviceToDevice, st));
+        return DCG_OK;
+    }
     DCG_CUDA(cudaEventRecord(ctx->ev1, st));
     rc = dcg_host_reserve(ctx, sizeof(DevStatus));
     if (rc) return rc;
@@ -679,4 +693,25 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
         out->device_ms = ms;
     }
     return DCG_OK;
+}
+
+extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_b,
+                         const double* d_x0, const dcg_basis* basis, const dcg_solver_config* cfg,
+                         double* d_x, dcg_krylov_log* log, double* d_history, dcg_solve_info* out,
+                         long long* info) {
+    return solve_impl(ctx, stream, op, d_b, d_x0, basis, cfg, d_x, log, d_history, out, info, nullptr, nullptr);
+}
+
+// Enqueue-only form (no host synchronisation).  d_kuse (optional, device):
+// the basis columns in use, as left by dcg_refresh_basis_async; the basis'
+// k is the layout maximum.  d_status (64 bytes, device) receives the status
+// block: int32 status, int32 columns used, int64 info, int64 iterations,
+// int64 stored log entries, f64 relative residual, f64 norm_b.
+extern "C" int dcg_solve_async(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_b,
+                               const double* d_x0, const dcg_basis* basis, const dcg_solver_config* cfg,
+                               double* d_x, dcg_krylov_log* log, double* d_history, const long long* d_kuse,
+                               void* d_status) {
+    if (!d_status) return DCG_E_CONFIG;
+    return solve_impl(ctx, stream, op, d_b, d_x0, basis, cfg, d_x, log, d_history, nullptr, nullptr, d_kuse,
+                      d_status);
 }

@@ -30,7 +30,7 @@ from . import _device as D
 from . import _native as N
 from .errors import InvalidLabel, NoProgress, NotPositiveDefinite, StateInconsistent
 from .operators import DenseOperator, RbfOperator, as_operator
-from .recycle import SELECT_LARGEST, SequenceState, solve_next
+from .recycle import SELECT_LARGEST, SequenceState, _pinned, _pinned_pool, solve_next, solve_next_async
 from .solvers import SolverConfig, _solve_dev
 
 SOLVER_CHOLESKY = "cholesky"
@@ -192,6 +192,75 @@ def _update_dev(state, inner, s, x):
     return new, float(psi.value)
 
 
+class _PendingObjective:
+    """(loglik, psi) of an enqueued newton update: copied to pinned host memory
+    right behind the derivative kernels, read on demand."""
+
+    def __init__(self, llpsi):
+        self.host = _pinned(2)
+        self.host.view(torch.float64)[:2].copy_(llpsi, non_blocking=True)
+        self.event = torch.cuda.Event()
+        self.event.record()
+
+    def get(self):
+        self.event.synchronize()
+        ll, psi = (float(v) for v in self.host.view(torch.float64)[:2].tolist())
+        _pinned_pool.append(self.host)
+        return ll, psi
+
+
+def _update_dev_async(state, inner, s, x):
+    """_update_dev without the host read: returns (new state with loglik
+    pending, _PendingObjective)."""
+    op = state.k_matrix
+    n = op.n
+    a, f, g, h = D.empty(n), D.empty(n), D.empty(n), D.empty(n)
+    llpsi = D.empty(2)
+    kop = op.kernel_view().c_struct()
+    N.check(N.lib().dcg_gpc_newton_update_async(D.ctx(), D.stream(), ctypes.byref(kop), inner.data_ptr(),
+                                                s.data_ptr(), x.data_ptr(), state.y.data_ptr(), a.data_ptr(),
+                                                f.data_ptr(), g.data_ptr(), h.data_ptr(), llpsi.data_ptr()),
+            what="newton_update_async")
+    new = GpcState(f=f, y=state.y, k_matrix=op, a=a, loglik=float("nan"), grad_loglik=g, h=h)
+    return new, _PendingObjective(llpsi)
+
+
+def _laplace_newton_pipelined(state, psi_prev, cfg, newton_tol, max_newton, k, selection):
+    """The def-CG Newton loop with every host synchronisation off the device's
+    critical path.  Per step the main stream runs refresh -> solve -> newton
+    update -> next system back to back while the extraction of the next basis
+    runs on the side stream; the host waits only for the solve status (to
+    enqueue the extraction with its sizes) and for psi (the reference's
+    NoProgress / newton_tol checks, gpc.py:272-290), both already complete or
+    about to be.  The next system is formed before psi is checked; when the
+    loop stops it is simply dropped."""
+    records = []
+    seq = SequenceState(k=k, cfg=cfg, selection=selection)
+    system = build_newton_system(state)
+    for it in range(1, max_newton + 1):
+        t0 = time.perf_counter()
+        x, job = solve_next_async(seq, system.a_matrix, system.b)
+        new_state, objective = _update_dev_async(state, system.inner, system.sqrt_h, x)
+        next_system = build_newton_system(new_state) if it < max_newton else None
+        x, seq = job.finish()
+        dt = time.perf_counter() - t0
+        report = seq.history[-1]
+        loglik, psi = objective.get()
+        new_state.loglik = loglik
+        state = new_state
+        records.append(NewtonRecord(newton_iter=it, psi=psi, loglik=loglik, solver_iterations=report.iterations,
+                                    rel_residual=report.residual_history[-1], solve_time_s=dt,
+                                    residual_history=list(report.residual_history), f=state.f))
+        if psi < psi_prev - 1e-6:
+            raise NoProgress(f"objective fell from {psi_prev:.9g} to {psi:.9g} at iteration {it}")
+        if psi - psi_prev < newton_tol:
+            break
+        psi_prev = psi
+        system = next_system
+    _ = seq.basis   # join a pending extraction (surfaces its errors here)
+    return state, records
+
+
 def newton_update(state, x):
     """a_new = (H f + grad) - H^1/2 x, f_new = K a_new (gpc.py:186-201)."""
     xd = D.to_dev(x, 1)
@@ -223,6 +292,13 @@ def laplace_newton(k_matrix, y, solver=SOLVER_CHOLESKY, cfg=None, newton_tol=1.0
     n = state.y.shape[0]
     psi_prev = state.loglik   # f = a = 0: psi = loglik, ||f - K a|| = 0 (gpc.py:239)
     records = []
+    if solver == SOLVER_DEFCG:
+        state, records = _laplace_newton_pipelined(state, psi_prev, cfg, newton_tol, max_newton, k, selection)
+        if records:
+            stacked = torch.stack([r.f for r in records]).cpu().numpy()
+            for r, row in zip(records, stacked):
+                r.f = row
+        return state, records
     seq = SequenceState(k=k, cfg=cfg, selection=selection)
     x_prev = D.zeros(n)
 

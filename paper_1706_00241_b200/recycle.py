@@ -28,7 +28,7 @@ from . import _device as D
 from . import _native as N
 from .errors import BasisDeficient, DimensionMismatch
 from .operators import as_operator
-from .solvers import KrylovLog, RecycleBasis, SolverConfig, _solve_dev
+from .solvers import TERM_CONVERGED, TERM_MAX_ITERS, KrylovLog, RecycleBasis, SolveReport, SolverConfig, _solve_dev
 
 SELECT_SMALLEST = "smallest"
 SELECT_LARGEST = "largest"
@@ -167,8 +167,11 @@ def _extract_dev(log: KrylovLog, prev: RecycleBasis | None, k: int, selection: s
                           selection)
 
 
-def _extract_async(log: KrylovLog, prev: RecycleBasis | None, k: int, selection: str) -> "_PendingBasis | None":
-    """Enqueue the extraction on the side stream (own context and workspace)."""
+def _extract_async(log: KrylovLog, prev: RecycleBasis | None, k: int, selection: str,
+                   after: "torch.cuda.Event | None" = None) -> "_PendingBasis | None":
+    """Enqueue the extraction on the side stream (own context and workspace).
+    The side stream waits for `after` (the solve) if given, else for
+    everything enqueued on the main stream so far."""
     m = log.stored_iterations
     kp = prev.k if prev is not None else 0
     if k > kp + m:
@@ -176,7 +179,10 @@ def _extract_async(log: KrylovLog, prev: RecycleBasis | None, k: int, selection:
     n = log.n
     main = torch.cuda.current_stream()
     side = D.side_stream()
-    side.wait_stream(main)
+    if after is not None:
+        side.wait_event(after)
+    else:
+        side.wait_stream(main)
     theta = D.empty(k)
     w_next, aw_next = D.empty(n, k), D.empty(n, k)
     result = torch.zeros(4, dtype=torch.int64, device=D.device())
@@ -193,6 +199,152 @@ def _extract_async(log: KrylovLog, prev: RecycleBasis | None, k: int, selection:
         event = torch.cuda.Event()
         event.record(side)
     return _PendingBasis(event, result, w_next, aw_next, (log, prev, theta))
+
+
+# ---------------------------------------------------------------------------
+# Pipelined sequence step (no host synchronisation between the extraction,
+# the refresh and the solve).  solve_next's semantics are kept: the refresh
+# uses the previous basis' W against the new operator, a BasisDeficient
+# refresh (or a failed extraction) runs plain CG -- decided on the device:
+# dcg_refresh_basis_async leaves the surviving column count in HBM and the
+# solve kernel reads it -- and the next extraction uses the basis actually
+# used.  The caller can enqueue independent work (the Newton update and the
+# next system) between solve_next_async and finish().
+# ---------------------------------------------------------------------------
+_STATUS_WORDS = 8   # the 64-byte status block of dcg_solve_async
+
+
+_pinned_pool: list = []
+
+
+def _pinned(nwords):
+    for i, t in enumerate(_pinned_pool):
+        if t.numel() >= nwords:
+            return _pinned_pool.pop(i)
+    return torch.empty(max(nwords, 64), dtype=torch.int64, pin_memory=True)
+
+
+_HIST_PREFIX = 1024   # residual-history entries copied back eagerly
+
+
+class _AsyncSolve:
+    """A refresh + solve (+ the next extraction) in flight.  The status block
+    and a prefix of the residual history come back on the copy stream as soon
+    as the solve ends, whatever the compute streams do next."""
+
+    def __init__(self, state, x, log, hist, status, basis, event, t0, cfg, pending):
+        self.state, self.x, self.log, self.hist, self.status = state, x, log, hist, status
+        self.basis, self.event, self.t0, self.cfg, self.pending = basis, event, t0, cfg, pending
+        self.ev_end = torch.cuda.Event(enable_timing=True)
+        self.ev_end.record()
+        cs = D.copy_stream()
+        cs.wait_event(self.ev_end)
+        self.host = _pinned(_STATUS_WORDS + _HIST_PREFIX)
+        npre = min(_HIST_PREFIX, hist.shape[0])
+        with torch.cuda.stream(cs):
+            self.host[:_STATUS_WORDS].copy_(status, non_blocking=True)
+            self.host[_STATUS_WORDS:_STATUS_WORDS + npre].view(torch.float64).copy_(hist[:npre], non_blocking=True)
+            self.done = torch.cuda.Event()
+            self.done.record(cs)
+
+    def finish(self):
+        """Wait for the solve and build its report.  Returns (x, new SequenceState)."""
+        self.done.synchronize()
+        words = self.host[:_STATUS_WORDS].numpy().copy()
+        status = int(np.int32(words[0] & 0xFFFFFFFF))
+        kused = int(words[0] >> 32)
+        info = int(words[1])
+        if status != N.DCG_OK:
+            _pinned_pool.append(self.host)
+            N.check(status, info, "solve")
+        its, m = int(words[2]), int(words[3])
+        rel = float(words[4:5].view(np.float64)[0])
+        if its + 1 <= _HIST_PREFIX:
+            history = self.host[_STATUS_WORDS:_STATUS_WORDS + its + 1].view(torch.float64).tolist()
+        else:
+            history = self.hist[: its + 1].cpu().tolist()
+        _pinned_pool.append(self.host)
+        conv = rel <= self.cfg.tol
+        ms = self.event.elapsed_time(self.ev_end)
+        rep = SolveReport(its, history, conv, time.perf_counter() - self.t0,
+                          TERM_CONVERGED if conv else TERM_MAX_ITERS, float(ms))
+        self.log.m, self.log.k = m, kused
+        st = self.state
+        return self.x, replace(st, basis=self.pending, x_last=self.x, history=st.history + [rep])
+
+
+def solve_next_async(state, a, b):
+    """Enqueue refresh + solve of the next system of a sequence and the
+    extraction of the basis after it (device data only, nothing waits).
+    Returns (x, job); job.finish() completes the report and the new state."""
+    op = as_operator(a)
+    bd = D.to_dev(b, 1)
+    n = bd.shape[0]
+    if op.n != n:
+        raise DimensionMismatch(f"system shapes {op.shape}, {tuple(bd.shape)}")
+    if state.selection not in (SELECT_SMALLEST, SELECT_LARGEST):
+        raise ValueError(f"unknown selection {state.selection!r}")
+    x_prev = D.zeros(n) if state.x_last is None else D.to_dev(state.x_last, 1)
+    t0 = time.perf_counter()
+    main = torch.cuda.current_stream()
+    pending = object.__getattribute__(state, "basis")
+    w_src, valid = None, None
+    if isinstance(pending, _PendingBasis):
+        main.wait_event(pending.event)
+        pending.keep_alive = None   # main-stream work is now ordered after the extraction
+        w_src, valid = pending.w_next, pending.result
+    elif pending is not None and pending.k > 0:
+        w_src = pending.w_dev
+    kmax = 0 if w_src is None else int(w_src.shape[1])
+    cb, kdev, bufs = None, None, None
+    if kmax:
+        w_out, aw_out, chol = D.empty(n, kmax), D.empty(n, kmax), D.empty(kmax, kmax)
+        kdev = torch.empty(1, dtype=torch.int64, device=D.device())
+        N.check(N.lib().dcg_refresh_basis_async(D.ctx(), D.stream(), ctypes.byref(op.c_struct()), w_src.data_ptr(),
+                                                kmax, valid.data_ptr() if valid is not None else None,
+                                                w_out.data_ptr(), aw_out.data_ptr(), chol.data_ptr(),
+                                                kdev.data_ptr()), what="refresh_basis_async")
+        cb = N.CBasis()
+        cb.k, cb.d_w, cb.d_aw, cb.d_chol = kmax, w_out.data_ptr(), aw_out.data_ptr(), chol.data_ptr()
+        bufs = (w_out, aw_out, chol, kdev, w_src)
+    cfg = state.cfg
+    log = KrylovLog(n, cfg.ell, kmax)
+    max_iters = 10 * n if cfg.max_iters is None else cfg.max_iters
+    hist = D.empty(max_iters + 1)
+    x = D.empty(n)
+    status = torch.empty(_STATUS_WORDS, dtype=torch.int64, device=D.device())
+    clog = log.c_struct()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    N.check(N.lib().dcg_solve_async(D.ctx(), D.stream(), ctypes.byref(op.c_struct()), bd.data_ptr(),
+                                    x_prev.data_ptr(), ctypes.byref(cb) if cb is not None else None,
+                                    ctypes.byref(cfg.c_struct()), x.data_ptr(), ctypes.byref(clog),
+                                    hist.data_ptr(), kdev.data_ptr() if kdev is not None else None,
+                                    status.data_ptr()), what="solve_async")
+    nxt = None
+    if state.k > 0:
+        # the next basis: extracted on the side stream straight behind the solve
+        # (its sizes come from the solve's status block on the device)
+        solved = torch.cuda.Event()
+        solved.record()
+        side = D.side_stream()
+        side.wait_event(solved)
+        k = state.k
+        theta = D.empty(k)
+        w_next, aw_next = D.empty(n, k), D.empty(n, k)
+        result = torch.empty(4, dtype=torch.int64, device=D.device())
+        with torch.cuda.stream(side):
+            rc = N.lib().dcg_ritz_extract_dev(D.ctx(1), side.cuda_stream, n, ctypes.byref(clog), status.data_ptr(),
+                                              ctypes.byref(cb) if cb is not None else None, k,
+                                              N.DCG_SELECT_LARGEST if state.selection == SELECT_LARGEST
+                                              else N.DCG_SELECT_SMALLEST,
+                                              theta.data_ptr(), w_next.data_ptr(), aw_next.data_ptr(),
+                                              result.data_ptr())
+            N.check(rc, 0, "ritz_extract_dev")
+            event = torch.cuda.Event()
+            event.record(side)
+        nxt = _PendingBasis(event, result, w_next, aw_next, (log, bufs, theta, status))
+    return x, _AsyncSolve(state, x, log, hist, status, bufs, ev0, t0, cfg, nxt)
 
 
 def harmonic_ritz_extract(log, prev_basis, k, selection=SELECT_SMALLEST):
