@@ -256,12 +256,16 @@ DCG_API int dcg_ritz_extract_async(dcg_context* ctx, void* stream, long long n,
  * the stored log length and the basis columns that solve used are read from
  * its status block (d_solve_status); prev->k is the basis' column capacity
  * (columns compacted, stride = columns used), log->ell the log capacity.
- * d_result as for dcg_ritz_extract_async (BasisDeficient when k > T).      */
+ * d_result as for dcg_ritz_extract_async (BasisDeficient when k > T).
+ * stage 0 enqueues everything; stage 1 only the device-wide column work
+ * (Z / AZ gather, normalisation, F and G), stage 2 the single-CTA pencil and
+ * the W_next tail -- the two halves may go to different streams (the caller
+ * orders stage 2 after stage 1) and must get identical arguments.          */
 DCG_API int dcg_ritz_extract_dev(dcg_context* ctx, void* stream, long long n,
                                  const dcg_krylov_log* log, const void* d_solve_status,
                                  const dcg_basis* prev, long long k, int selection,
                                  double* d_theta, double* d_w_next, double* d_aw_next,
-                                 long long* d_result);
+                                 long long* d_result, int stage);
 
 /* ---- L4: GPC Laplace-Newton glue (gpc.py) -------------------------------- */
 /* loglik, grad, h of the logistic likelihood          gpc.py:126-157          */

@@ -200,6 +200,7 @@ SIGNATURES = {
         _P,
         _P,
         _P,
+        ctypes.c_int,
     ],
     "dcg_gpc_derivs": [_P, _P, _LL, _P, _P, _P, _P, _PD],
     "dcg_gpc_newton_system": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P, _P, _P],

@@ -6,6 +6,7 @@
 //                                                              recycle.py:71,133-136)
 //   gemm_lr_kernel   C = A B with the reference's i-k-j order (K4, Z.U; _core.pyx:31-44)
 #include "common.cuh"
+#include <algorithm>
 #include "gemv.cuh"
 #include "symgemv.cuh"
 

@@ -294,10 +294,14 @@ static size_t extract_ws_bytes(dcg_context* ctx, long long n, int T, int k) {
 // Enqueue the pipeline.  T is the column count (host-known), or with
 // solve_st the upper bound k_prev_max + ell (the actual k_prev and m are read
 // from the solve's status block on the device).
+// stage: 0 = the whole pipeline; 1 = E1-E3 (the SM-wide column work, run on
+// the main stream ahead of the Newton update); 2 = E4-E6 (the single-CTA
+// pencil and the tail, on the side stream).  Stages share the context's
+// workspace layout, so they must be enqueued with identical arguments.
 static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const dcg_krylov_log* log, long long m,
                            long long kp, long long T, const DevStatus* solve_st, const double* Wp, const double* AWp,
                            long long k, int selection, double* d_theta, double* d_u, double* d_z, double* d_w_next,
-                           double* d_aw_next, long long* d_result) {
+                           double* d_aw_next, long long* d_result, int stage = 0) {
     if (k > DCG_MAX_K || T > DCG_MAX_T) return DCG_E_UNSUPPORTED;
     int rc = dcg_ws_reserve(ctx, extract_ws_bytes(ctx, n, (int)T, (int)k));
     if (rc) return rc;
@@ -322,8 +326,6 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
     DevStatus* plan = ar.take<DevStatus>(1);
     DevStatus* pencil = ar.take<DevStatus>(1);
     unsigned int* counters = ar.take<unsigned int>(4);
-    DCG_CUDA(cudaMemsetAsync(plan, 0, al(sizeof(DevStatus)) * 2, st));
-    DCG_CUDA(cudaMemsetAsync(counters, 0, 16, st));
     const double* P = log ? log->d_p : nullptr;
     const double* R = log ? log->d_r : nullptr;
     const double* alpha = log ? log->d_alpha : nullptr;
@@ -331,6 +333,9 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
     int nb = G;
     if (n < (long long)nb * EX_ROWS) nb = (int)max(1LL, (n + EX_ROWS - 1) / EX_ROWS);
     const size_t sm1 = sizeof(double) * 2 * EX_ROWS * T;
+    if (stage != 2) {
+    DCG_CUDA(cudaMemsetAsync(plan, 0, al(sizeof(DevStatus)) * 2, st));
+    DCG_CUDA(cudaMemsetAsync(counters, 0, 16, st));
     DCG_CUDA(cudaFuncSetAttribute(zgather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
     zgather_kernel<<<nb, EX_NT, sm1, st>>>(n, (int)kp, Wp, AWp, (int)m, P, R, alpha, (int)k, Zraw, AZraw, part,
                                            counters, norms, keep, plan, solve_st);
@@ -342,6 +347,8 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
     const int warps = (int)(2 * T * T);
     fg_reduce_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>(fgpart, nb, plan, Fraw, Graw);
     DCG_LAUNCHED();
+    }
+    if (stage == 1) return DCG_OK;
     rc = dcg_ritz_pencil_launch(st, Fraw, Graw, (int)T, (int)k, selection == DCG_SELECT_LARGEST, 60, wk, d_theta, U,
                                 active, pencil, plan);
     if (rc) return rc;
@@ -391,7 +398,9 @@ extern "C" int dcg_ritz_extract_async(dcg_context* ctx, void* stream, long long 
 // compacted, stride = columns used), log->ell the log capacity.
 extern "C" int dcg_ritz_extract_dev(dcg_context* ctx, void* stream, long long n, const dcg_krylov_log* log,
                                     const void* d_solve_status, const dcg_basis* prev, long long k, int selection,
-                                    double* d_theta, double* d_w_next, double* d_aw_next, long long* d_result) {
+                                    double* d_theta, double* d_w_next, double* d_aw_next, long long* d_result,
+                                    int stage) {
+    if (stage < 0 || stage > 2) return DCG_E_CONFIG;
     if (!ctx || n < 0 || k < 1 || !d_result || !d_solve_status || !log) return DCG_E_CONFIG;
     if (selection != DCG_SELECT_SMALLEST && selection != DCG_SELECT_LARGEST) return DCG_E_CONFIG;
     const long long kmax = prev ? prev->k : 0;
@@ -399,6 +408,7 @@ extern "C" int dcg_ritz_extract_dev(dcg_context* ctx, void* stream, long long n,
     if (kmax > 0 && (!prev->d_w || !prev->d_aw)) return DCG_E_CONFIG;
     if (log->ell > 0 && (!log->d_p || !log->d_r || !log->d_alpha)) return DCG_E_CONFIG;
     if (T < 1) {
+        if (stage == 1) return DCG_OK;
         // nothing can ever be extracted: BasisDeficient(0) (k >= 1 > T)
         DCG_CUDA(cudaMemsetAsync(d_result, 0, 3 * sizeof(long long), as_stream(stream)));
         long long* r0 = d_result;
@@ -409,7 +419,7 @@ extern "C" int dcg_ritz_extract_dev(dcg_context* ctx, void* stream, long long n,
     }
     return extract_enqueue(ctx, as_stream(stream), n, log, 0, 0, T, static_cast<const DevStatus*>(d_solve_status),
                            kmax ? prev->d_w : nullptr, kmax ? prev->d_aw : nullptr, k, selection, d_theta, nullptr,
-                           nullptr, d_w_next, d_aw_next, d_result);
+                           nullptr, d_w_next, d_aw_next, d_result, stage);
 }
 
 // Synchronous form: enqueue, wait, and map the outcome to a status.

@@ -232,11 +232,10 @@ class _AsyncSolve:
     and a prefix of the residual history come back on the copy stream as soon
     as the solve ends, whatever the compute streams do next."""
 
-    def __init__(self, state, x, log, hist, status, basis, event, t0, cfg, pending):
+    def __init__(self, state, x, log, hist, status, basis, event, ev_end, t0, cfg, pending):
         self.state, self.x, self.log, self.hist, self.status = state, x, log, hist, status
         self.basis, self.event, self.t0, self.cfg, self.pending = basis, event, t0, cfg, pending
-        self.ev_end = torch.cuda.Event(enable_timing=True)
-        self.ev_end.record()
+        self.ev_end = ev_end
         cs = D.copy_stream()
         cs.wait_event(self.ev_end)
         self.host = _pinned(_STATUS_WORDS + _HIST_PREFIX)
@@ -321,30 +320,33 @@ def solve_next_async(state, a, b):
                                     ctypes.byref(cfg.c_struct()), x.data_ptr(), ctypes.byref(clog),
                                     hist.data_ptr(), kdev.data_ptr() if kdev is not None else None,
                                     status.data_ptr()), what="solve_async")
+    ev_end = torch.cuda.Event(enable_timing=True)
+    ev_end.record()
     nxt = None
     if state.k > 0:
-        # the next basis: extracted on the side stream straight behind the solve
-        # (its sizes come from the solve's status block on the device)
-        solved = torch.cuda.Event()
-        solved.record()
-        side = D.side_stream()
-        side.wait_event(solved)
+        # The next basis, extracted straight behind the solve (its sizes come
+        # from the solve's status block on the device): the SM-wide column work
+        # (Z / AZ, F, G) on the main stream, then the single-CTA pencil and
+        # the tail on the side stream, overlapping the caller's next work
+        # (the Newton update's K-products leave the pencil an SM of its own).
         k = state.k
         theta = D.empty(k)
         w_next, aw_next = D.empty(n, k), D.empty(n, k)
         result = torch.empty(4, dtype=torch.int64, device=D.device())
+        sel = N.DCG_SELECT_LARGEST if state.selection == SELECT_LARGEST else N.DCG_SELECT_SMALLEST
+        args = (D.ctx(1), None, n, ctypes.byref(clog), status.data_ptr(), ctypes.byref(cb) if cb is not None else None,
+                k, sel, theta.data_ptr(), w_next.data_ptr(), aw_next.data_ptr(), result.data_ptr())
+        N.check(N.lib().dcg_ritz_extract_dev(*args[:1], main.cuda_stream, *args[2:], 1), 0, "ritz_extract_dev")
+        gathered = torch.cuda.Event()
+        gathered.record()
+        side = D.side_stream()
+        side.wait_event(gathered)
         with torch.cuda.stream(side):
-            rc = N.lib().dcg_ritz_extract_dev(D.ctx(1), side.cuda_stream, n, ctypes.byref(clog), status.data_ptr(),
-                                              ctypes.byref(cb) if cb is not None else None, k,
-                                              N.DCG_SELECT_LARGEST if state.selection == SELECT_LARGEST
-                                              else N.DCG_SELECT_SMALLEST,
-                                              theta.data_ptr(), w_next.data_ptr(), aw_next.data_ptr(),
-                                              result.data_ptr())
-            N.check(rc, 0, "ritz_extract_dev")
+            N.check(N.lib().dcg_ritz_extract_dev(*args[:1], side.cuda_stream, *args[2:], 2), 0, "ritz_extract_dev")
             event = torch.cuda.Event()
             event.record(side)
         nxt = _PendingBasis(event, result, w_next, aw_next, (log, bufs, theta, status))
-    return x, _AsyncSolve(state, x, log, hist, status, bufs, ev0, t0, cfg, nxt)
+    return x, _AsyncSolve(state, x, log, hist, status, bufs, ev0, ev_end, t0, cfg, nxt)
 
 
 def harmonic_ritz_extract(log, prev_basis, k, selection=SELECT_SMALLEST):
