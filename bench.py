@@ -354,6 +354,29 @@ def run_native(args, rank, world):
         "bytes_model": "per launch: matvec-equivalents x 8 n(n+1)/2 (unique Gram entries) + 8 n (2k + 10) per iteration",
     }
 
+    # ---- the stored-Gram matvec on its own (north_star: matvec HBM GB/s) -----
+    # y = K v through the public operator (symmetric lower-triangle GEMV,
+    # sym_pass1 + sym_pass2), the K-product of the Newton update / system.
+    kview = gram.kernel_view()
+    vprobe = torch.randn(n, dtype=torch.float64, device="cuda")
+    yprobe = kview.matvec_dev(vprobe)
+    for _ in range(3):
+        kview.matvec_dev(vprobe, out=yprobe)
+    reps = 20
+    m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    m0.record()
+    for _ in range(reps):
+        kview.matvec_dev(vprobe, out=yprobe)
+    m1.record()
+    torch.cuda.synchronize()
+    mv_ms = m0.elapsed_time(m1) / reps
+    mv_bytes = gram_bytes + 3 * 8 * n
+    matvec = {"kernel": "sym_pass1_kernel + sym_pass2_kernel (K v, stored symmetric Gram, lower-triangle tiles)",
+              "bound": "hbm", "achieved": mv_bytes / (mv_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+              "frac": mv_bytes / (mv_ms / 1e3) / 1e9 / peak, "us_per_product": mv_ms * 1e3,
+              "bytes_model": "8 n(n+1)/2 unique Gram entries + 3 x 8 n vector bytes per product"}
+
     # ---- e2e through the public API from pinned host buffers ----------------
     P.solvers._solve_dev = orig
     P.recycle._solve_dev = orig
@@ -396,7 +419,7 @@ def run_native(args, rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8d recipe)",
         "config": workload(args) | {"parallelism": "replicas" if world > 1 else "single-gpu"},
         "iterations_per_sequence": its_lists[-1], "sequence_ms": ms_per_step,
-        "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+        "roofline": roofline, "matvec_roofline": matvec, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, sample = cpu_baseline(n, args.cpu_sample_steps)
@@ -495,7 +518,7 @@ def run_native_sharded(args, rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8d recipe)",
         "config": workload(args) | {"parallelism": f"row-shards x{world} (NCCL all-gather p + all-reduce scalars)"},
         "iterations_per_sequence": its_list, "sequence_ms": ms_per_step,
-        "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+        "roofline": roofline, "matvec_roofline": matvec, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

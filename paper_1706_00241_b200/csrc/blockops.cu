@@ -64,6 +64,26 @@ __global__ void __launch_bounds__(DCG_NT, 1)
     sym_pass1<false>(K, ldk, n, v, s_in, colpart, rowpart, smem, seq);
 }
 
+// Both passes in one cooperative launch (grid barrier between them): no
+// second launch, and pass 2's partial reads follow pass 1 without a gap.
+__global__ void __launch_bounds__(DCG_NT, 1)
+    sym_apply_coop_kernel(const double* __restrict__ K, long long ldk, long long n, const double* v,
+                          const double* s_in, const double* s_out, double shift, double* colpart, double* rowpart,
+                          double* y, unsigned int* bar) {
+    extern __shared__ __align__(16) double smem[];
+    sym_ring_init(smem, n);
+    unsigned int seq = 0;
+    sym_pass1<false>(K, ldk, n, v, s_in, colpart, rowpart, smem, seq);
+    dcg_grid_barrier(bar, gridDim.x);
+    const long long q0 = sym_row_begin(n, gridDim.x, blockIdx.x);
+    const long long q1 = sym_row_begin(n, gridDim.x, blockIdx.x + 1);
+    sym_pass2(n, colpart, rowpart, q0, q1, sym_range_table(smem), gridDim.x, smem, [&](long long i, double t) {
+        double val = s_out ? mul_rn(s_out[i], t) : t;
+        if (shift != 0.0) val = add_rn(mul_rn(shift, v[i]), val);
+        y[i] = val;
+    });
+}
+
 __global__ void __launch_bounds__(DCG_NT, 1)
     sym_pass2_kernel(long long n, int R, const double* colpart, const double* rowpart, const double* v,
                      const double* s_out, double shift, double* y) {
@@ -79,7 +99,7 @@ __global__ void __launch_bounds__(DCG_NT, 1)
     });
 }
 
-size_t dcg_sym_apply_scratch_doubles(long long n) { return 2 * (size_t)sym_ntiles(n) * DCG_TB; }
+size_t dcg_sym_apply_scratch_doubles(long long n) { return 2 * (size_t)sym_ntiles(n) * DCG_TB + 32; }
 
 // y = shift v + s_out (.) K (s_in (.) v) with K exactly symmetric (n x n, unsharded).
 int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, long long ldk, long long n, const double* v,
@@ -99,10 +119,14 @@ int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, long long 
     double* rowpart = scratch + ntt * DCG_TB;
     const int navail = ctx->sm_count > 1 ? ctx->sm_count - 1 : 1;
     const int G = navail < DCG_SYM_MAX_CTAS ? navail : DCG_SYM_MAX_CTAS;
-    sym_pass1_kernel<<<G, DCG_NT, smem, st>>>(K, ldk, n, v, s_in, colpart, rowpart);
-    DCG_LAUNCHED();
-    sym_pass2_kernel<<<G, DCG_NT, 0, st>>>(n, G, colpart, rowpart, v, s_out, shift, y);
-    DCG_LAUNCHED();
+    // one cooperative launch: pass 1, grid barrier, pass 2 (barrier word after the partials)
+    unsigned int* bar = reinterpret_cast<unsigned int*>(rowpart + ntt * DCG_TB);
+    DCG_CUDA(cudaFuncSetAttribute(sym_apply_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DCG_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), st));
+    void* args[] = {(void*)&K, (void*)&ldk, (void*)&n, (void*)&v, (void*)&s_in, (void*)&s_out, (void*)&shift,
+                    (void*)&colpart, (void*)&rowpart, (void*)&y, (void*)&bar};
+    DCG_CUDA(cudaLaunchCooperativeKernel((const void*)sym_apply_coop_kernel, dim3(G), dim3(DCG_NT), args, smem, st));
+    dcg_count_launch();
     return DCG_OK;
 }
 
