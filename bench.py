@@ -261,7 +261,10 @@ def run_native(args, rank, world):
         its = rep.iterations
         # matvec-equivalents streamed by the solve kernel: prologue (1, or 2 with
         # the warm-start correction), one per iteration, true-residual refreshes
-        mv = (2 if kk else 1) + its + (its // cfg_.recompute_residual_every if cfg_.recompute_residual_every else 0)
+        # prologue products: r_prev = b - A x_prev (unless computed ahead of the
+        # launch: job.hoisted) and r0 = b - A x0
+        warm_mv = 1 if (kk and not getattr(job, "hoisted", False)) else 0
+        mv = 1 + warm_mv + its + (its // cfg_.recompute_residual_every if cfg_.recompute_residual_every else 0)
         solve_ms.append(rep.device_ms)
         solve_its.append((its, kk))
         solve_mv.append(mv)
@@ -280,7 +283,10 @@ def run_native(args, rank, world):
         rep = st_.history[-1]
         kk, its = job.log.k, rep.iterations
         cfg_ = job.cfg
-        mv = (2 if kk else 1) + its + (its // cfg_.recompute_residual_every if cfg_.recompute_residual_every else 0)
+        # prologue products: r_prev = b - A x_prev (unless computed ahead of the
+        # launch: job.hoisted) and r0 = b - A x0
+        warm_mv = 1 if (kk and not getattr(job, "hoisted", False)) else 0
+        mv = 1 + warm_mv + its + (its // cfg_.recompute_residual_every if cfg_.recompute_residual_every else 0)
         solve_ms.append(rep.device_ms)
         solve_its.append((its, kk))
         solve_mv.append(mv)

@@ -214,11 +214,13 @@ DCG_API int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op, co
  * dcg_refresh_basis_async.  d_status (64 bytes on the device) receives
  * {int32 status, int32 columns used, int64 info, int64 iterations, int64
  * stored log entries, f64 rel residual, f64 norm_b} in stream order.  The
- * log's mu rows keep the stride basis->k.                                  */
+ * log's mu rows keep the stride basis->k.  d_ax0 (optional): A x0 already
+ * computed (the warm-start correction's first product, solvers.py:237).     */
 DCG_API int dcg_solve_async(dcg_context* ctx, void* stream, const dcg_operator* op,
                             const double* d_b, const double* d_x0, const dcg_basis* basis,
                             const dcg_solver_config* cfg, double* d_x, dcg_krylov_log* log,
-                            double* d_history, const long long* d_kuse, void* d_status);
+                            double* d_history, const long long* d_kuse, void* d_status,
+                            const double* d_ax0);
 /* Enqueue-only refresh_basis: surviving column count to *d_kout (device
  * int64; 0 when nothing survives -- BasisDeficient -- or when d_valid, the
  * result block of the extraction that produced d_w, reports a failure).

@@ -151,6 +151,7 @@ SIGNATURES = {
         _P,
         _P,
         _P,
+        _P,
     ],
     "dcg_refresh_basis_async": [_P, _P, ctypes.POINTER(COperator), _P, _LL, _P, _P, _P, _P, _P],
     "dcg_deflation_project": [_P, _P, _LL, ctypes.POINTER(CBasis), _P, _P],

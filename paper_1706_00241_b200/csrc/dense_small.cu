@@ -510,7 +510,8 @@ __device__ __forceinline__ void pencil_stamp(int i) {
     if (threadIdx.x == 0) g_pencil_prof[i] = globaltimer_ns();
 }
 
-__device__ int cta_jacobi_onesided(double* X, double* Vc, int n, int max_sweeps, double rtol, double* red) {
+__device__ __forceinline__ int cta_jacobi_onesided(double* X, double* Vc, int n, int max_sweeps, double rtol,
+                                                   double* red) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     __shared__ int s_res1;
     for (int e = tid; e < n * n; e += blockDim.x) Vc[e] = (e / n == e - (e / n) * n) ? 1.0 : 0.0;
@@ -559,6 +560,9 @@ __device__ int cta_jacobi_onesided(double* X, double* Vc, int n, int max_sweeps,
                 if (q >= n) continue;
                 const double xp0 = i0 < n ? X[p * n + i0] : 0.0, xp1 = i1 < n ? X[p * n + i1] : 0.0;
                 const double xq0 = i0 < n ? X[q * n + i0] : 0.0, xq1 = i1 < n ? X[q * n + i1] : 0.0;
+                // V rows loaded with X's, ahead of the rotation chain
+                const double vp0 = i0 < n ? Vc[p * n + i0] : 0.0, vq0 = i0 < n ? Vc[q * n + i0] : 0.0;
+                const double vp1 = i1 < n ? Vc[p * n + i1] : 0.0, vq1 = i1 < n ? Vc[q * n + i1] : 0.0;
                 double app = fma(xp1, xp1, xp0 * xp0);
                 double aqq = fma(xq1, xq1, xq0 * xq0);
                 double apq = fma(xp1, xq1, xp0 * xq0);
@@ -586,16 +590,14 @@ __device__ int cta_jacobi_onesided(double* X, double* Vc, int n, int max_sweeps,
                 if (i0 < n) {
                     X[p * n + i0] = sub_rn(mul_rn(c, xp0), mul_rn(sn, xq0));
                     X[q * n + i0] = add_rn(mul_rn(sn, xp0), mul_rn(c, xq0));
-                    const double vp = Vc[p * n + i0], vq = Vc[q * n + i0];
-                    Vc[p * n + i0] = sub_rn(mul_rn(c, vp), mul_rn(sn, vq));
-                    Vc[q * n + i0] = add_rn(mul_rn(sn, vp), mul_rn(c, vq));
+                    Vc[p * n + i0] = sub_rn(mul_rn(c, vp0), mul_rn(sn, vq0));
+                    Vc[q * n + i0] = add_rn(mul_rn(sn, vp0), mul_rn(c, vq0));
                 }
                 if (i1 < n) {
                     X[p * n + i1] = sub_rn(mul_rn(c, xp1), mul_rn(sn, xq1));
                     X[q * n + i1] = add_rn(mul_rn(sn, xp1), mul_rn(c, xq1));
-                    const double vp = Vc[p * n + i1], vq = Vc[q * n + i1];
-                    Vc[p * n + i1] = sub_rn(mul_rn(c, vp), mul_rn(sn, vq));
-                    Vc[q * n + i1] = add_rn(mul_rn(sn, vp), mul_rn(c, vq));
+                    Vc[p * n + i1] = sub_rn(mul_rn(c, vp1), mul_rn(sn, vq1));
+                    Vc[q * n + i1] = add_rn(mul_rn(sn, vp1), mul_rn(c, vq1));
                 }
             }
             cta_sync();
@@ -710,7 +712,9 @@ __global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fr
         // Vc (column-major) in S3; afterwards theta on the diagonal of A := S2 and V row-major in S0
         double* Vc = A;
         pencil_stamp(2);
-        nc = cta_jacobi_onesided(Y, Vc, na, max_sweeps, 1e-14, red);
+        // staged: X is S2 and Vc is S3 -- pointers formed from `sm` here so the
+        // (inlined) rounds use shared-memory instructions, not generic ones
+        nc = cta_jacobi_onesided(sm + 2 * T * T, sm + 3 * T * T, na, max_sweeps, 1e-14, red);
         pencil_stamp(3);
         if (nc == 0) {
             for (int c = warp; c < na; c += nw) {

@@ -36,6 +36,7 @@ struct SolveArgs {
     double shift;
     const double* b;
     const double* x0;
+    const double* ax0;     // optional: A x0 computed ahead of the launch (warm start)
     double* x;
     int k;                 // basis columns (the layout / maximum)
     const long long* kdev; // optional: columns in use, read on the device (<= k; 0 = plain CG)
@@ -334,12 +335,19 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     // ---------------- prologue: norm_b and the warm-start correction ----------
     // deflated_cg_solve: r_prev = b - A x_prev ; x0 = x_prev + W chol_solve(L, W' r_prev)
     if (a.warm && deflate) {
-        gemv(a.x0, [&](long long i, double t) {
-            const double ax = s ? add_rn(mul_rn(shift, a.x0[i]), mul_rn(s[i], t))
-                                : add_rn(mul_rn(shift, a.x0[i]), t);
-            a.r[i] = sub_rn(a.b[i], ax);
-        });
-        if constexpr (STRAT != STRAT_ROWS) GSYNC(); else cta_sync();
+        if (a.ax0) {
+            // A x_prev came from a product enqueued before the launch (it
+            // overlaps the Ritz pencil in the pipelined Newton step)
+            for (long long i = r0 + tid; i < r1; i += DCG_NT) a.r[i] = sub_rn(a.b[i], ld_cg(a.ax0 + i));
+            cta_sync();
+        } else {
+            gemv(a.x0, [&](long long i, double t) {
+                const double ax = s ? add_rn(mul_rn(shift, a.x0[i]), mul_rn(s[i], t))
+                                    : add_rn(mul_rn(shift, a.x0[i]), t);
+                a.r[i] = sub_rn(a.b[i], ax);
+            });
+            if constexpr (STRAT != STRAT_ROWS) GSYNC(); else cta_sync();
+        }
         // slot0 = b'b, slots 1.. = W' r_prev
         own_partials([&](long long i) { return a.b[i]; }, a.r, a.W, a.partials);
     } else {
@@ -522,7 +530,7 @@ int dcg_rbf_mma_prep(const dcg_context* ctx, cudaStream_t st, const RbfMma& p);
 static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_b,
                       const double* d_x0, const dcg_basis* basis, const dcg_solver_config* cfg, double* d_x,
                       dcg_krylov_log* log, double* d_history, dcg_solve_info* out, long long* info,
-                      const long long* d_kuse, void* d_status) {
+                      const long long* d_kuse, void* d_status, const double* d_ax0 = nullptr) {
     if (!ctx || !op || !cfg || !d_b || !d_x0 || !d_x || !d_history) return DCG_E_CONFIG;
     if (info) *info = 0;
     const long long n = op->n;
@@ -565,6 +573,7 @@ static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, co
     a.shift = op->shift;
     a.b = d_b;
     a.x0 = d_x0;
+    a.ax0 = d_ax0;
     a.x = d_x;
     a.k = k;
     a.kdev = k ? d_kuse : nullptr;
@@ -706,12 +715,13 @@ extern "C" int dcg_solve(dcg_context* ctx, void* stream, const dcg_operator* op,
 // the basis columns in use, as left by dcg_refresh_basis_async; the basis'
 // k is the layout maximum.  d_status (64 bytes, device) receives the status
 // block: int32 status, int32 columns used, int64 info, int64 iterations,
-// int64 stored log entries, f64 relative residual, f64 norm_b.
+// int64 stored log entries, f64 relative residual, f64 norm_b.  d_ax0
+// (optional): A x0, computed ahead (the warm-start correction's first product).
 extern "C" int dcg_solve_async(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_b,
                                const double* d_x0, const dcg_basis* basis, const dcg_solver_config* cfg,
                                double* d_x, dcg_krylov_log* log, double* d_history, const long long* d_kuse,
-                               void* d_status) {
+                               void* d_status, const double* d_ax0) {
     if (!d_status) return DCG_E_CONFIG;
     return solve_impl(ctx, stream, op, d_b, d_x0, basis, cfg, d_x, log, d_history, nullptr, nullptr, d_kuse,
-                      d_status);
+                      d_status, d_ax0);
 }

@@ -287,8 +287,11 @@ def solve_next_async(state, a, b):
     t0 = time.perf_counter()
     main = torch.cuda.current_stream()
     pending = object.__getattribute__(state, "basis")
-    w_src, valid = None, None
+    w_src, valid, ax0 = None, None, None
     if isinstance(pending, _PendingBasis):
+        # the warm start's first product A x_prev needs no basis: it runs
+        # while the extraction of the basis is still going on
+        ax0 = op.matvec_dev(x_prev)
         main.wait_event(pending.event)
         pending.keep_alive = None   # main-stream work is now ordered after the extraction
         w_src, valid = pending.w_next, pending.result
@@ -319,7 +322,8 @@ def solve_next_async(state, a, b):
                                     x_prev.data_ptr(), ctypes.byref(cb) if cb is not None else None,
                                     ctypes.byref(cfg.c_struct()), x.data_ptr(), ctypes.byref(clog),
                                     hist.data_ptr(), kdev.data_ptr() if kdev is not None else None,
-                                    status.data_ptr()), what="solve_async")
+                                    status.data_ptr(), ax0.data_ptr() if (ax0 is not None and kmax) else None),
+            what="solve_async")
     ev_end = torch.cuda.Event(enable_timing=True)
     ev_end.record()
     nxt = None
@@ -346,7 +350,9 @@ def solve_next_async(state, a, b):
             event = torch.cuda.Event()
             event.record(side)
         nxt = _PendingBasis(event, result, w_next, aw_next, (log, bufs, theta, status))
-    return x, _AsyncSolve(state, x, log, hist, status, bufs, ev0, ev_end, t0, cfg, nxt)
+    job = _AsyncSolve(state, x, log, hist, status, bufs, ev0, ev_end, t0, cfg, nxt)
+    job.hoisted = ax0 is not None and kmax > 0   # the solve kernel skips its first product
+    return x, job
 
 
 def harmonic_ritz_extract(log, prev_basis, k, selection=SELECT_SMALLEST):
