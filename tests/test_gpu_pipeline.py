@@ -1,0 +1,127 @@
+"""GPU: the pipelined sequence step (recycle.solve_next_async + job.finish,
+used by the def-CG Newton loop) against the synchronous solve_next, which is
+itself checked against the reference (test_gpu_recycle.py).
+
+The pipelined path moves three host decisions onto the device: the refresh's
+surviving column count (the solve kernel reads it), the extraction's sizes
+(read from the solve's status block) and BasisDeficient (a column count of 0,
+i.e. plain CG, recycle.py:178-179, 194-195).  These tests pin each of them to
+the synchronous semantics on identical inputs."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1706_00241_b200 as P
+
+    return P
+
+
+def gpc_like_sequence(P, n, steps, seed=0):
+    """A = I + S_t K S_t with K an RBF Gram and slowly varying s_t (the
+    Laplace-Newton system shape), b_t random."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((n, 5))
+    gram = P.rbf_kernel(x, P.KernelParams(1.0, 1.5))
+    s0 = rng.uniform(0.2, 0.5, n)
+    systems = []
+    for t in range(steps):
+        s = torch.from_numpy(s0 * (1.0 + 0.05 * t * rng.uniform(-1, 1, n))).cuda()
+        b = torch.from_numpy(rng.standard_normal(n)).cuda()
+        systems.append((gram.scaled(s, 1.0), b))
+    return systems
+
+
+def run_sync(P, systems, k, cfg):
+    st = P.SequenceState(k=k, cfg=cfg, selection="largest")
+    xs, its = [], []
+    for a, b in systems:
+        x, st = P.solve_next(st, a, b)
+        xs.append(x.clone())
+        its.append(st.history[-1].iterations)
+    return xs, its
+
+
+def run_pipelined(P, systems, k, cfg):
+    st = P.SequenceState(k=k, cfg=cfg, selection="largest")
+    xs, its = [], []
+    for a, b in systems:
+        _, job = P.recycle.solve_next_async(st, a, b)
+        x, st = job.finish()
+        xs.append(x.clone())
+        its.append(st.history[-1].iterations)
+    _ = st.basis
+    return xs, its
+
+
+@pytest.mark.parametrize("n,k,ell", [(800, 8, 12), (1500, 16, 20)])
+def test_pipelined_sequence_matches_sync(P, n, k, ell):
+    systems = gpc_like_sequence(P, n, 6)
+    cfg = P.SolverConfig(tol=1e-8, ell=ell)
+    xs_s, its_s = run_sync(P, systems, k, cfg)
+    xs_p, its_p = run_pipelined(P, systems, k, cfg)
+    assert all(abs(a - b) <= 1 for a, b in zip(its_s, its_p)), (its_s, its_p)
+    for a, b in zip(xs_s, xs_p):
+        assert float(torch.linalg.norm(a - b) / torch.linalg.norm(a)) <= 1e-9
+    # recycling engaged after the first system (fewer iterations than plain CG)
+    assert its_p[-1] < its_p[0]
+
+
+def test_pipelined_first_solve_is_plain_cg_bitwise(P):
+    """No basis yet: the pipelined first solve is exactly cg_solve (k = 0 path)."""
+    systems = gpc_like_sequence(P, 600, 1)
+    cfg = P.SolverConfig(tol=1e-8, ell=10)
+    a, b = systems[0]
+    x_ref, rep_ref, _ = P.cg_solve(a, b, torch.zeros_like(b), cfg)
+    st = P.SequenceState(k=6, cfg=cfg, selection="largest")
+    _, job = P.recycle.solve_next_async(st, a, b)
+    x, st = job.finish()
+    assert torch.equal(x, x_ref)
+    assert st.history[-1].residual_history == rep_ref.residual_history
+
+
+def test_failed_extraction_means_plain_cg(P):
+    """An extraction that reports BasisDeficient (device result block) makes
+    the pipelined refresh leave 0 columns: the next solve is plain CG from
+    the previous solution, exactly as solve_next after a swallowed
+    BasisDeficient (recycle.py:194-195)."""
+    systems = gpc_like_sequence(P, 700, 2)
+    cfg = P.SolverConfig(tol=1e-8, ell=12)
+    st = P.SequenceState(k=8, cfg=cfg, selection="largest")
+    _, job = P.recycle.solve_next_async(st, *systems[0])
+    x0, st = job.finish()
+    pending = object.__getattribute__(st, "basis")
+    pending.event.synchronize()
+    pending.result[0] = P._native.DCG_E_BASIS_DEFICIENT   # as the device would have written it
+    _, job = P.recycle.solve_next_async(st, *systems[1])
+    x1, st1 = job.finish()
+    assert job.log.k == 0
+    x_ref, rep_ref, _ = P.cg_solve(systems[1][0], systems[1][1], x0, cfg)
+    assert torch.equal(x1, x_ref)
+    assert st1.history[-1].iterations == rep_ref.iterations
+
+
+def test_deficient_extraction_on_device(P):
+    """k > k_prev + m (a solve that stops after fewer than k iterations with no
+    previous basis): the device-side check yields BasisDeficient, the next
+    solve runs plain CG -- the same outcome the synchronous path reaches."""
+    n = 400
+    rng = np.random.default_rng(3)
+    d = np.linspace(1.0, 2.0, n)
+    a = torch.diag(torch.from_numpy(d)).cuda()
+    b = torch.from_numpy(rng.standard_normal(n)).cuda()
+    cfg = P.SolverConfig(tol=1e-3, ell=20)
+    st = P.SequenceState(k=16, cfg=cfg, selection="largest")
+    _, job = P.recycle.solve_next_async(st, a, b)
+    _, st = job.finish()
+    its = st.history[-1].iterations
+    assert its < 16
+    assert st.basis is None   # resolves the device result: BasisDeficient, swallowed
+    ss = P.SequenceState(k=16, cfg=cfg, selection="largest")
+    _, ss = P.solve_next(ss, a, b)
+    assert ss.basis is None
