@@ -383,6 +383,33 @@ def run_native(args, rank, world):
               "frac": mv_bytes / (mv_ms / 1e3) / 1e9 / peak, "us_per_product": mv_ms * 1e3,
               "bytes_model": "8 n(n+1)/2 unique Gram entries + 3 x 8 n vector bytes per product"}
 
+    # ---- the same product inside the persistent solve (phase timers) --------
+    # One plain-CG solve of the first Newton system with DCG_PHASE_TIMERS=1:
+    # pass 1 + its grid barrier + pass 2 (with the Ap epilogue) per product,
+    # as CTA 0 sees them (developer timers: one globaltimer read per phase).
+    matvec_in_solve = None
+    try:
+        import ctypes as _ct
+
+        st0 = P.gpc.make_state(gram, yd)
+        sys0 = P.gpc.build_newton_system(st0)
+        os.environ["DCG_PHASE_TIMERS"] = "1"
+        _, rep0, _ = P.cg_solve(sys0.a_matrix, sys0.b, torch.zeros(n, dtype=torch.float64, device="cuda"), cfg)
+        os.environ.pop("DCG_PHASE_TIMERS", None)
+        tm = (_ct.c_ulonglong * 16)()
+        if _native.lib().dcg_debug_phase_timers(tm) == 0:
+            products = rep0.iterations + 1
+            ns = (tm[0] + tm[1] + tm[2]) / products
+            gbs = mv_bytes / (ns * 1e-9) / 1e9
+            matvec_in_solve = {"kernel": "dcg_solve_kernel<SYM> pass 1 + grid barrier + pass 2 (Ap epilogue)",
+                               "bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                               "us_per_product": ns / 1e3, "products": products,
+                               "how": "CTA-0 phase timers (globaltimer) over one plain-CG solve of the first "
+                                      "Newton system"}
+    except Exception as exc:   # diagnostic only
+        os.environ.pop("DCG_PHASE_TIMERS", None)
+        matvec_in_solve = {"error": repr(exc)[:200]}
+
     # ---- e2e through the public API from pinned host buffers ----------------
     P.solvers._solve_dev = orig
     P.recycle._solve_dev = orig
@@ -425,7 +452,7 @@ def run_native(args, rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8d recipe)",
         "config": workload(args) | {"parallelism": "replicas" if world > 1 else "single-gpu"},
         "iterations_per_sequence": its_lists[-1], "sequence_ms": ms_per_step,
-        "roofline": roofline, "matvec_roofline": matvec, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+        "roofline": roofline, "matvec_roofline": matvec, "matvec_in_solve": matvec_in_solve, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, sample = cpu_baseline(n, args.cpu_sample_steps)
@@ -524,7 +551,7 @@ def run_native_sharded(args, rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8d recipe)",
         "config": workload(args) | {"parallelism": f"row-shards x{world} (NCCL all-gather p + all-reduce scalars)"},
         "iterations_per_sequence": its_list, "sequence_ms": ms_per_step,
-        "roofline": roofline, "matvec_roofline": matvec, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+        "roofline": roofline, "matvec_roofline": matvec, "matvec_in_solve": matvec_in_solve, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

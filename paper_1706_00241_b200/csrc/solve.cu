@@ -527,6 +527,18 @@ int dcg_rbf_mma_teams(const dcg_context* ctx, int dim, size_t other_bytes);
 RbfMma dcg_rbf_mma_params(const dcg_operator* op, double* operands, int nteam);
 int dcg_rbf_mma_prep(const dcg_context* ctx, cudaStream_t st, const RbfMma& p);
 
+// per-phase device timers of the last dcg_solve run with DCG_PHASE_TIMERS set
+static unsigned long long* g_phase_timers = nullptr;
+
+// Developer diagnostic: the 16 phase accumulators (ns, CTA 0) of the last
+// solve run with DCG_PHASE_TIMERS=1 (slot order as printed on stderr: pass1,
+// gsync_mv, pass2+epi, ...).  DCG_E_CONFIG if none was recorded.
+extern "C" __attribute__((visibility("default"))) int dcg_debug_phase_timers(unsigned long long* out16) {
+    if (!g_phase_timers || !out16) return DCG_E_CONFIG;
+    DCG_CUDA(cudaMemcpy(out16, g_phase_timers, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    return DCG_OK;
+}
+
 static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_b,
                       const double* d_x0, const dcg_basis* basis, const dcg_solver_config* cfg, double* d_x,
                       dcg_krylov_log* log, double* d_history, dcg_solve_info* out, long long* info,
@@ -628,7 +640,7 @@ static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, co
     DCG_CUDA(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned int), st));
     // DCG_PHASE_TIMERS=1: per-phase device time of CTA 0 printed per solve
     // (developer diagnostic; costs one predicated branch per phase otherwise).
-    static unsigned long long* d_timers = nullptr;
+    unsigned long long*& d_timers = g_phase_timers;
     const bool timers = getenv("DCG_PHASE_TIMERS") != nullptr;
     a.timers = nullptr;
     if (timers) {
