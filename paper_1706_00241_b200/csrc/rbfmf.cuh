@@ -202,147 +202,7 @@ __device__ void rbf_rows_gemv(const RbfParams& p, long long r0, long long r1, co
     cta_sync();
 }
 
-// ---------------------------------------------------------------------------
-// Symmetric half-evaluation (unsharded operators): each lower-triangle tile
-// (I, J <= I) is generated once and serves both its row sums (rows of I) and
-// its column sums (rows of J), exactly like the stored strategy's pass 1
-// (symgemv.cuh) - same tile partition, same partial layout, so pass 2 is
-// sym_pass2.  Half the exp / distance work of the row-owned form.
-// ---------------------------------------------------------------------------
-#include "symgemv.cuh"
-
-// staging region (>= 512 doubles: pass 2 reuses it as its reduction scratch)
-__host__ __device__ __forceinline__ long long rbf_sym_xregion(int dim) {
-    const long long x = 2LL * dim * MF_TB;
-    return x < DCG_NT ? DCG_NT : x;
-}
-__host__ __device__ __forceinline__ long long rbf_sym_smem_doubles(int dim) {
-    return rbf_sym_xregion(dim) + 3 * MF_TB + 2 * DCG_NW * DCG_TB + (DCG_SYM_MAX_CTAS + 1) + 2;
-}
-__device__ __forceinline__ long long* rbf_sym_table(double* smem, int dim) {
-    return reinterpret_cast<long long*>(smem + rbf_sym_xregion(dim) + 3 * MF_TB + 2 * DCG_NW * DCG_TB);
-}
-__device__ __forceinline__ void rbf_sym_init(double* smem, const RbfParams& p) {
-    sym_fill_range_table(rbf_sym_table(smem, p.dim), p.n);
-}
-
-static __device__ void rbf_sym_pass1(const RbfParams& p, const double* v, const double* s, double* colpart,
-                              double* rowpart, double* smem) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const long long n = p.n;
-    double* xit = smem;
-    double* xjt = xit + p.dim * MF_TB;
-    double* vj = smem + rbf_sym_xregion(p.dim);
-    double* nI = vj + MF_TB;
-    double* nJ = nI + MF_TB;
-    double* rowred = nJ + MF_TB;
-    const long long* tbl = rbf_sym_table(smem, p.dim);
-    const long long t0 = tbl[blockIdx.x], t1 = tbl[blockIdx.x + 1];
-    if (t0 >= t1) return;
-    const int ntiles = (int)(t1 - t0);
-    long long I = sym_tile_row(t0);
-    long long J = t0 - sym_tile_row_base(I);
-    long long staged_I = -1, norms_I = -1;
-    double xI0 = 0.0, xI1 = 0.0;
-    double row0 = 0.0, row1 = 0.0;
-    long long seg_start = t0;
-    int flush = 0;
-    // Register prefetch of the next tile's X_J and v'_J: issued before the
-    // current tile's arithmetic, stored to shared memory after the next
-    // barrier, so the L2 round trip overlaps the FP64 work.
-    constexpr int PF = (DCG_RBF_MAX_DIM * MF_TB + DCG_NT - 1) / DCG_NT;
-    double pf[PF];
-    double pfv = 0.0;
-    const int nel = p.dim * MF_TB;
-    auto prefetch = [&](long long Jn) {
-#pragma unroll
-        for (int u = 0; u < PF; ++u) {
-            const int e = tid + u * DCG_NT;
-            double val = 0.0;
-            if (e < nel) {
-                const int r = e / p.dim, t = e - (e / p.dim) * p.dim;
-                const long long g = Jn * MF_TB + r;
-                if (g < n) val = __ldg(p.X + g * p.dim + t);
-            }
-            pf[u] = val;
-        }
-        if (tid < MF_TB) pfv = sym_xval(v, s, Jn * MF_TB + tid, n);
-    };
-    prefetch(J);
-    for (int lt = 0; lt < ntiles; ++lt) {
-        cta_sync();   // the previous tile's reads of xit / xjt / vj are done
-        if (I != staged_I) {
-            rbf_stage_rows(p, I * MF_TB, n, xit);
-            staged_I = I;
-            xI0 = sym_xval(v, s, I * MF_TB + 2 * lane, n);
-            xI1 = sym_xval(v, s, I * MF_TB + 2 * lane + 1, n);
-        }
-#pragma unroll
-        for (int u = 0; u < PF; ++u) {
-            const int e = tid + u * DCG_NT;
-            if (e < nel) {
-                const int r = e / p.dim, t = e - (e / p.dim) * p.dim;
-                xjt[t * MF_TB + r] = pf[u];
-            }
-        }
-        if (tid < MF_TB) vj[tid] = pfv;
-        cta_sync();
-        rbf_stage_norms(p, xjt, nJ);
-        if (I != norms_I) {
-            rbf_stage_norms(p, xit, nI);
-            norms_I = I;
-        }
-        cta_sync();
-        if (lt + 1 < ntiles) prefetch(J + 1 > I ? 0 : J + 1);
-        double k[2][4];
-        rbf_tile_values<true>(p, xit, xjt, I * MF_TB, J * MF_TB, n, k, nI, nJ);
-        const double x0 = vj[4 * warp], x1 = vj[4 * warp + 1], x2 = vj[4 * warp + 2], x3 = vj[4 * warp + 3];
-        row0 = fma(k[0][0], x0, row0);
-        row0 = fma(k[0][1], x1, row0);
-        row0 = fma(k[0][2], x2, row0);
-        row0 = fma(k[0][3], x3, row0);
-        row1 = fma(k[1][0], x0, row1);
-        row1 = fma(k[1][1], x1, row1);
-        row1 = fma(k[1][2], x2, row1);
-        row1 = fma(k[1][3], x3, row1);
-        if (J < I) {
-            // column sums over the tile's 64 rows: warp reduce-scatter of 4 values
-            const double c0 = fma(k[1][0], xI1, k[0][0] * xI0);
-            const double c1 = fma(k[1][1], xI1, k[0][1] * xI0);
-            const double c2 = fma(k[1][2], xI1, k[0][2] * xI0);
-            const double c3 = fma(k[1][3], xI1, k[0][3] * xI0);
-            const bool hi16 = lane & 16;
-            const double r0 = __shfl_xor_sync(0xffffffffu, hi16 ? c0 : c2, 16);
-            const double r1 = __shfl_xor_sync(0xffffffffu, hi16 ? c1 : c3, 16);
-            const double k0 = (hi16 ? c2 : c0) + r0;
-            const double k1 = (hi16 ? c3 : c1) + r1;
-            const bool hi8 = lane & 8;
-            const double r2 = __shfl_xor_sync(0xffffffffu, hi8 ? k0 : k1, 8);
-            double cv = (hi8 ? k1 : k0) + r2;
-            cv += __shfl_xor_sync(0xffffffffu, cv, 4);
-            cv += __shfl_xor_sync(0xffffffffu, cv, 2);
-            cv += __shfl_xor_sync(0xffffffffu, cv, 1);
-            if ((lane & 7) == 0) colpart[(t0 + lt) * DCG_TB + 4 * warp + 2 * (lane >> 4) + ((lane >> 3) & 1)] = cv;
-        }
-        if (J == I || lt + 1 == ntiles) {   // end of a tile-row segment
-            double* rr = rowred + (flush & 1) * DCG_NW * DCG_TB;
-            rr[warp * DCG_TB + 2 * lane] = row0;
-            rr[warp * DCG_TB + 2 * lane + 1] = row1;
-            cta_sync();
-            if (tid < DCG_TB) {
-                double a = 0.0;
-#pragma unroll
-                for (int w = 0; w < DCG_NW; ++w) a += rr[w * DCG_TB + tid];
-                rowpart[seg_start * DCG_TB + tid] = a;
-            }
-            row0 = row1 = 0.0;
-            seg_start = t0 + lt + 1;
-            ++flush;
-        }
-        if (++J > I) {
-            ++I;
-            J = 0;
-        }
-    }
-    cta_sync();
-}
+// The unsharded operator's symmetric half-evaluation (each lower-triangle
+// tile generated once, serving its row and column sums) runs on the FP64
+// tensor pipe: rbfmma.cuh.  The row-owned form above serves row slabs
+// (sharded operators) and the multi-vector product.

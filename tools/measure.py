@@ -4,6 +4,7 @@
   python tools/measure.py config1        GPC Newton sequence n=2000, k=8 (BASELINE configs[0])
   python tools/measure.py config2-cg     config 2 with plain CG (k=0) for the def-CG vs CG comparison
   python tools/measure.py config4 [n]    GP-regression hyperparameter sweep, 20 lengthscales, k=24
+  python tools/measure.py config3 [n]    GPC Newton sequence n=50000, d=8, ell=2, k=32, stored Gram (20 GB), 1 GPU
   python tools/measure.py config5 [n]    matrix-free RBF operator (K7), d=16, ell=3, k=32 (1 GPU)
 
 Each prints one JSON line: device time (CUDA events) of the whole sequence,
@@ -23,7 +24,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 
-def gpc_sequence(n, d, ell, k, solver="defcg", reps=3):
+def gpc_sequence(n, d, ell, k, solver="defcg", reps=3, ell_log=None):
     import torch
 
     import paper_1706_00241_b200 as P
@@ -32,7 +33,7 @@ def gpc_sequence(n, d, ell, k, solver="defcg", reps=3):
     x, y = gpc_inputs(n, d, 0)
     gram = P.rbf_kernel(torch.from_numpy(x).cuda(), P.KernelParams(1.0, ell))
     yd = torch.from_numpy(y).cuda()
-    cfg = P.SolverConfig(tol=1e-8, ell=max(k, 8) + 4)
+    cfg = P.SolverConfig(tol=1e-8, ell=ell_log if ell_log is not None else max(k, 8) + 4)
 
     def run():
         _, recs = P.laplace_newton(gram, yd, solver, cfg, newton_tol=-np.inf, max_newton=8, k=k,
@@ -163,6 +164,13 @@ def main():
         n = int(sys.argv[2]) if len(sys.argv) > 2 else 30000
         out = sweep(n)
         out["cpu_baseline"] = cpu_sweep_sample(n)
+    elif what == "config3":
+        n = int(sys.argv[2]) if len(sys.argv) > 2 else 50000
+        out = gpc_sequence(n, 8, 2.0, 32, reps=1, ell_log=36)
+        out["gram_bytes"] = 8 * n * n
+        out["note"] = "BASELINE configs[2] at one GPU (the 1-GPU point of its 1/2/4/8 scaling); stored Gram in HBM"
+        out["cpu_baseline"] = cpu_sweep_sample(n, n_cpu=12000)
+        out["cpu_baseline"]["sample"] += " (plain-CG iteration cost on the host at n_cpu, scaled to n)"
     elif what == "config5":
         n = int(sys.argv[2]) if len(sys.argv) > 2 else 50000
         out = config5(n)
