@@ -96,6 +96,7 @@ extern "C" int dcg_context_destroy(dcg_context* ctx) {
     if (!ctx) return DCG_OK;
     cudaDeviceSynchronize();
     if (ctx->ws) cudaFree(ctx->ws);
+    if (ctx->ws2) cudaFree(ctx->ws2);
     if (ctx->host) cudaFreeHost(ctx->host);
     cudaEventDestroy(ctx->ev0);
     cudaEventDestroy(ctx->ev1);
@@ -121,6 +122,20 @@ int dcg_ws_reserve(dcg_context* ctx, size_t bytes) {
     size_t want = bytes + bytes / 4 + (1 << 20);
     DCG_CUDA(cudaMalloc(&ctx->ws, want));
     ctx->ws_bytes = want;
+    return DCG_OK;
+}
+
+int dcg_ws2_reserve(dcg_context* ctx, size_t bytes) {
+    if (bytes <= ctx->ws2_bytes) return DCG_OK;
+    if (ctx->ws2) {
+        cudaDeviceSynchronize();
+        cudaFree(ctx->ws2);
+        ctx->ws2 = nullptr;
+        ctx->ws2_bytes = 0;
+    }
+    size_t want = bytes + bytes / 4 + (1 << 20);
+    DCG_CUDA(cudaMalloc(&ctx->ws2, want));
+    ctx->ws2_bytes = want;
     return DCG_OK;
 }
 

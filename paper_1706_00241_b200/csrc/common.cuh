@@ -28,6 +28,8 @@ struct dcg_context {
     size_t smem_optin;
     void* ws;                // device workspace
     size_t ws_bytes;
+    void* ws2;               // second workspace: operands of kernels whose callers hold `ws`
+    size_t ws2_bytes;
     void* host;              // pinned host scratch for status read-back
     size_t host_bytes;
     cudaEvent_t ev0, ev1;
@@ -66,6 +68,7 @@ void dcg_count_launch();
     } while (0)
 
 int dcg_ws_reserve(dcg_context* ctx, size_t bytes);
+int dcg_ws2_reserve(dcg_context* ctx, size_t bytes);
 int dcg_host_reserve(dcg_context* ctx, size_t bytes);
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }

@@ -176,6 +176,57 @@ int dcg_rbf_mma_prep(const dcg_context* ctx, cudaStream_t st, const RbfMma& p) {
     return DCG_OK;
 }
 
+// Row-owned tensor-pipe product Y = shift X_rows + s_out (.) K (s_in (.) X) for
+// the operator's row slab (k = 0: X is a vector).  Operands in ctx->ws2.
+template <int NB>
+static int launch_rows(const dcg_context* ctx, cudaStream_t st, const RbfMma& p, long long row0, long long rows,
+                       const double* vs, const double* s_out, double shift, const double* x_rows, double* Y, int kout,
+                       const dcg_shard_state* gate) {
+    const size_t smem = sizeof(double) * (size_t)rr_smem_doubles<NB>(p.dp);
+    DCG_CUDA(cudaFuncSetAttribute(rbf_mma_rows_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    DCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rbf_mma_rows_kernel<NB>, RR_NT, smem));
+    if (per_sm < 1) per_sm = 1;
+    const long long nblk = (rows + RM_TB - 1) / RM_TB;
+    long long grid = (long long)per_sm * ctx->sm_count;
+    if (grid > nblk) grid = nblk;
+    rbf_mma_rows_kernel<NB><<<(unsigned)grid, RR_NT, smem, st>>>(p, row0, rows, vs, s_out, shift, x_rows, Y, kout,
+                                                                  gate);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}
+
+int dcg_rbf_rows_product(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, const double* X, int k,
+                         const double* s_in, const double* s_out, double shift, double* Y,
+                         const dcg_shard_state* gate) {
+    const long long n = op->n, npad = rm_npad(n);
+    const int kk = k ? (k + 7) / 8 * 8 : 0;
+    const size_t opnd = dcg_rbf_mma_operand_doubles(n, (int)op->dim);
+    const size_t vsz = (size_t)npad * (k ? kk : 1);
+    int rc = dcg_ws2_reserve(ctx, sizeof(double) * (opnd + vsz) + 512);
+    if (rc) return rc;
+    double* operands = static_cast<double*>(ctx->ws2);
+    double* vs = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(operands + opnd) + 255) & ~uintptr_t(255));
+    const RbfMma p = dcg_rbf_mma_params(op, operands, 1);
+    rc = dcg_rbf_mma_prep(ctx, st, p);
+    if (rc) return rc;
+    rr_scale_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(X, k, kk, s_in, op->var, n, npad, vs);
+    DCG_LAUNCHED();
+    const long long row0 = op->row0, rows = op->rows;
+    const double* x_rows = X + row0 * (k ? k : 1);
+    switch (kk / 8) {
+        case 0: return launch_rows<0>(ctx, st, p, row0, rows, vs, s_out, shift, x_rows, Y, 1, gate);
+        case 1: return launch_rows<1>(ctx, st, p, row0, rows, vs, s_out, shift, x_rows, Y, k, gate);
+        case 2: return launch_rows<2>(ctx, st, p, row0, rows, vs, s_out, shift, x_rows, Y, k, gate);
+        case 3: return launch_rows<3>(ctx, st, p, row0, rows, vs, s_out, shift, x_rows, Y, k, gate);
+        case 4: return launch_rows<4>(ctx, st, p, row0, rows, vs, s_out, shift, x_rows, Y, k, gate);
+        case 5: return launch_rows<5>(ctx, st, p, row0, rows, vs, s_out, shift, x_rows, Y, k, gate);
+        case 6: return launch_rows<6>(ctx, st, p, row0, rows, vs, s_out, shift, x_rows, Y, k, gate);
+        case 7: return launch_rows<7>(ctx, st, p, row0, rows, vs, s_out, shift, x_rows, Y, k, gate);
+        default: return launch_rows<8>(ctx, st, p, row0, rows, vs, s_out, shift, x_rows, Y, k, gate);
+    }
+}
+
 size_t dcg_rbf_mf_scratch_doubles(const dcg_operator* op) {
     return (op->row0 == 0 && op->rows == op->n)
                ? dcg_sym_apply_scratch_doubles(op->n) + dcg_rbf_mma_operand_doubles(op->n, (int)op->dim) + 32
@@ -206,12 +257,8 @@ int dcg_rbf_mf_apply(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, 
         DCG_LAUNCHED();
         return dcg_sym_pass2_launch(st, G, G * nteam, n, colpart, rowpart, v, s_out, shift, y);
     }
-    const size_t smem = dcg_rbf_mf_smem((int)op->dim);
-    DCG_CUDA(cudaFuncSetAttribute(rbf_mf_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    rbf_mf_gemv_kernel<<<grid_for(ctx, op->rows), DCG_NT, smem, st>>>(params_of(op), op->row0, op->rows, v, s_in,
-                                                                      s_out, shift, y);
-    DCG_LAUNCHED();
-    return DCG_OK;
+    // row slab (sharded operator): the row-owned tensor-pipe form
+    return dcg_rbf_rows_product(ctx, st, op, v, 0, s_in, s_out, shift, y, nullptr);
 }
 
 int dcg_rbf_mf_block(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, const double* X, int k,
@@ -219,10 +266,6 @@ int dcg_rbf_mf_block(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, 
     int rc = dcg_rbf_mf_check(op);
     if (rc) return rc;
     if (op->rows == 0 || k <= 0) return DCG_OK;
-    const size_t smem = sizeof(double) * (size_t)(2LL * op->dim * MF_TB + MF_TB * MF_KC + DCG_NW * MF_TB + 2 * MF_TB);
-    DCG_CUDA(cudaFuncSetAttribute(rbf_mf_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    rbf_mf_block_kernel<<<grid_for(ctx, op->rows), DCG_NT, smem, st>>>(params_of(op), op->row0, op->rows, X, k, s_in,
-                                                                       s_out, shift, Y);
-    DCG_LAUNCHED();
-    return DCG_OK;
+    if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
+    return dcg_rbf_rows_product(ctx, st, op, X, k, s_in, s_out, shift, Y, nullptr);
 }

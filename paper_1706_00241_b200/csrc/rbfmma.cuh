@@ -389,3 +389,199 @@ static __device__ void rbf_mma_pass1(const RbfMma& p, const double* v, const dou
         seq[1] = iseq;
     }
 }
+
+// ---------------------------------------------------------------------------
+// Row-owned products on the FP64 tensor pipe: Y = shift X_rows + s_out (.)
+// K (s_in (.) X) for a row slab [row0, row0 + rows) of the operator, X n x kk
+// (kk = 8 NB; NB = 0: a single vector).  A 256-thread CTA owns 64-row blocks
+// and sweeps every 64-column tile: warp w owns the block's rows 8w..8w+7 and
+// all 64 columns of a tile (8 accumulator blocks cb), so
+//   * the distance contraction's A fragments (its 8 rows of x~) stay in
+//     registers for the whole sweep, B fragments come from the staged tile;
+//   * the product E V_J uses E straight from the accumulators: with the k
+//     index of k-step e mapped to column 8 cb + 2 q + e, lane (r, q)'s
+//     accumulator element e IS the A fragment, and V_J's rows are read in
+//     the same order -- no transpose, no shared-memory round trip;
+//   * a warp's output rows are complete inside the warp: no column
+//     partials (the symmetric pass's per-tile partials would be 64 x kk per
+//     tile here) and no cross-warp reduction.
+// Used for row slabs (sharded operators) and for the
+// multi-vector product of refresh_basis (recycle.py:90).  Costs ~d + 12 + kk
+// FP64-pipe operations per element over all n x rows pairs.  Operands: the
+// fragment-major x~ and b of rbf_prep_kernel, vs = var s_in (.) X (n_pad x
+// kk, zero-padded) or, for NB = 0, var s_in (.) v (n_pad).
+// ---------------------------------------------------------------------------
+#define RR_NT 256
+
+__device__ __forceinline__ void rr_cp16(void* sdst, const void* gsrc, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(rm_saddr(sdst)), "l"(gsrc), "r"(bytes));
+}
+__device__ __forceinline__ void rr_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void rr_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+template <int NB>
+__host__ __device__ __forceinline__ long long rr_smem_doubles(int dp) {
+    const int kk = NB ? 8 * NB : 1;
+    const int kks = NB ? kk + 2 : 1;   // padded V row stride (conflict-free B fragment reads)
+    return RM_TAB + RM_TB * dp + 2LL * RM_TB * dp + 2LL * RM_TB * kks + 2 * RM_TB + RM_TB + 64;
+}
+
+template <int NB>
+__global__ void __launch_bounds__(RR_NT, 1)
+    rbf_mma_rows_kernel(RbfMma p, long long row0, long long rows, const double* __restrict__ vs,
+                        const double* __restrict__ s_out, double shift, const double* __restrict__ x_rows,
+                        double* __restrict__ Y, int kout, const dcg_shard_state* gate) {
+    if (gate && gate->done) return;   // sharded solve: iterations enqueued past convergence
+    constexpr int KK = NB ? 8 * NB : 1;
+    constexpr int KKS = NB ? KK + 2 : 1;
+    extern __shared__ __align__(16) double sm[];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int r = lane >> 2, q = lane & 3;
+    const int dp = p.dp, nch = dp >> 3;
+    const long long n = p.n;
+    double* tab = sm;
+    double* xi = tab + RM_TAB;                 // 64 x dp (fragment-major, rows of the block)
+    double* xj = xi + RM_TB * dp;              // 2 x 64 x dp
+    double* vj = xj + 2 * RM_TB * dp;          // 2 x 64 x KKS
+    double* bj = vj + 2 * RM_TB * KKS;         // 2 x 64
+    double* bi = bj + 2 * RM_TB;               // 64
+    for (int j = tid; j < RM_TAB; j += RR_NT) tab[j] = exp2((double)j / RM_TAB);
+    const long long ntj = (n + RM_TB - 1) / RM_TB;
+    const long long nblk = (rows + RM_TB - 1) / RM_TB;
+    // stage tile J (x~ fragments, b, V rows) into buffer `buf` with cp.async
+    auto stage = [&](long long J, int buf) {
+        const double* src = p.xf + J * RM_TB * dp;
+        double* dst = xj + buf * RM_TB * dp;
+        for (int c = tid; c < RM_TB * dp / 2; c += RR_NT) rr_cp16(dst + 2 * c, src + 2 * c, 16);
+        if (tid < RM_TB / 2) rr_cp16(bj + buf * RM_TB + 2 * tid, p.xb + J * RM_TB + 2 * tid, 16);
+        if constexpr (NB) {
+            double* vd = vj + buf * RM_TB * KKS;
+            const double* vsrc = vs + J * RM_TB * KK;
+            for (int c = tid; c < RM_TB * KK / 2; c += RR_NT) {
+                const int rr = c / (KK / 2), cc = (c - rr * (KK / 2)) * 2;
+                rr_cp16(vd + rr * KKS + cc, vsrc + rr * KK + cc, 16);
+            }
+        } else {
+            if (tid < RM_TB / 2) rr_cp16(vj + buf * RM_TB + 2 * tid, vs + J * RM_TB + 2 * tid, 16);
+        }
+        rr_commit();
+    };
+    for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const long long i0 = row0 + blk * RM_TB;   // first global row of the block
+        cta_sync();   // previous block's readers are done with xi / the buffers
+        // the block's own rows (global rows i0.. - not tile-aligned for slabs):
+        // fragment-major x~ of rows i0 + 8 w + r, built here from X
+        {
+            const double sc = sqrt(2.0 * p.inv2);
+            for (int e = tid; e < RM_TB * dp; e += RR_NT) {
+                const int il = e / dp, t = e - il * dp;
+                const long long g = i0 + il;
+                const double v = (g < row0 + rows && g < n && t < p.dim) ? mul_rn(__ldg(p.X + g * p.dim + t), sc) : 0.0;
+                xi[rm_frag_index(il, t, dp)] = v;
+            }
+            if (tid < RM_TB) {
+                const long long g = i0 + tid;
+                bi[tid] = (g < row0 + rows && g < n) ? __ldg(p.xb + g) : 0.0;
+            }
+        }
+        stage(0, 0);
+        cta_sync();
+        const double bI = bi[8 * w + r];
+        double acc[NB ? NB : 1][2];
+#pragma unroll
+        for (int nb = 0; nb < (NB ? NB : 1); ++nb) acc[nb][0] = acc[nb][1] = 0.0;
+        for (long long J = 0; J < ntj; ++J) {
+            const int buf = (int)(J & 1);
+            rr_wait_all();
+            cta_sync();   // tile J landed for everyone; everyone is done with tile J - 1
+            if (J + 1 < ntj) stage(J + 1, buf ^ 1);
+            const double2* xi2 = reinterpret_cast<const double2*>(xi);
+            const double2* xj2 = reinterpret_cast<const double2*>(xj + buf * RM_TB * dp);
+            const double* bJ = bj + buf * RM_TB;
+            double c[8][2];
+#pragma unroll
+            for (int cb = 0; cb < 8; ++cb) {
+                c[cb][0] = bI + bJ[8 * cb + 2 * q];
+                c[cb][1] = bI + bJ[8 * cb + 2 * q + 1];
+            }
+            for (int ch = 0; ch < nch; ++ch) {
+                const double2 af = xi2[(w * nch + ch) * 32 + lane];
+#pragma unroll
+                for (int cb = 0; cb < 8; ++cb) {
+                    const double2 bf = xj2[(cb * nch + ch) * 32 + lane];
+                    rm_dmma(c[cb][0], c[cb][1], af.x, bf.x);
+                    rm_dmma(c[cb][0], c[cb][1], af.y, bf.y);
+                }
+            }
+            // elements: row i0 + 8 w + r, column 64 J + 8 cb + 2 q + e
+            const long long dd = i0 + 8 * w + r - 64 * J;   // diagonal at local column dd
+            const bool diag_tile = (i0 + 8 * w + 7 >= 64 * J) && (i0 + 8 * w <= 64 * J + 63);
+            const double* vJ = vj + buf * RM_TB * KKS;
+#pragma unroll
+            for (int cb = 0; cb < 8; ++cb) {
+                double e0 = rm_exp<true>(c[cb][0], tab), e1 = rm_exp<true>(c[cb][1], tab);
+                if (diag_tile) {
+                    if (dd == 8 * cb + 2 * q) e0 = p.diag;
+                    if (dd == 8 * cb + 2 * q + 1) e1 = p.diag;
+                }
+                if constexpr (NB == 0) {
+                    acc[0][0] = fma(e0, vJ[8 * cb + 2 * q], acc[0][0]);
+                    acc[0][1] = fma(e1, vJ[8 * cb + 2 * q + 1], acc[0][1]);
+                } else {
+#pragma unroll
+                    for (int nb = 0; nb < NB; ++nb) {
+                        rm_dmma(acc[nb][0], acc[nb][1], e0, vJ[(8 * cb + 2 * q) * KKS + 8 * nb + r]);
+                        rm_dmma(acc[nb][0], acc[nb][1], e1, vJ[(8 * cb + 2 * q + 1) * KKS + 8 * nb + r]);
+                    }
+                }
+            }
+        }
+        // epilogue: the warp's 8 rows
+        if constexpr (NB == 0) {
+            double t = acc[0][0] + acc[0][1];
+            t += __shfl_xor_sync(0xffffffffu, t, 1);
+            t += __shfl_xor_sync(0xffffffffu, t, 2);
+            const long long g = i0 + 8 * w + r;
+            if (q == 0 && g < row0 + rows) {
+                const long long li = g - row0;
+                double val = s_out ? mul_rn(s_out[li], t) : t;
+                if (shift != 0.0) val = add_rn(mul_rn(shift, x_rows[li]), val);
+                Y[li] = val;
+            }
+        } else {
+            // C fragment: row 8 w + r, columns 8 nb + 2 q + {0, 1}
+            const long long g = i0 + 8 * w + r;
+            if (g < row0 + rows) {
+                const long long li = g - row0;
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int col = 8 * nb + 2 * q + e;
+                        if (col < kout) {
+                            double val = s_out ? mul_rn(s_out[li], acc[nb][e]) : acc[nb][e];
+                            if (shift != 0.0) val = add_rn(mul_rn(shift, x_rows[li * kout + col]), val);
+                            Y[li * kout + col] = val;
+                        }
+                    }
+            }
+        }
+    }
+}
+
+// vs = var s_in (.) X, zero-padded to n_pad x kk (kk >= k); k = 0 means a vector
+static __global__ void rr_scale_kernel(const double* X, int k, int kk, const double* s_in, double var, long long n,
+                                       long long npad, double* vs) {
+    const long long total = npad * (k ? kk : 1);
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long i = k ? e / kk : e;
+        const int c = k ? (int)(e - i * kk) : 0;
+        double v = 0.0;
+        if (i < n && c < (k ? k : 1)) {
+            const double x = k ? X[i * k + c] : X[i];
+            v = mul_rn(var, s_in ? mul_rn(s_in[i], x) : x);
+        }
+        vs[e] = v;
+    }
+}

@@ -13,6 +13,11 @@
 
 #define SH_NT 512
 
+int dcg_rbf_mf_check(const dcg_operator* op);
+int dcg_rbf_rows_product(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, const double* X, int k,
+                         const double* s_in, const double* s_out, double shift, double* Y,
+                         const dcg_shard_state* gate);
+
 namespace {
 
 int shard_grid(const dcg_context* ctx, long long rows) {
@@ -165,6 +170,37 @@ __global__ void __launch_bounds__(DCG_NT, 1)
             out[i] = sub_rn(b[i], ax);
         }
     });
+    if (mode == 0 && part) {
+        dot = block_sum(dot, s_tmp);
+        if (threadIdx.x == 0) s_out[0] = dot;
+        cta_sync();
+        grid_reduce_slots(s_out, 1, parts, ps, counter, part);
+    }
+}
+
+// RBF slabs: `out` already holds t = K_slab (s (.) v) (dcg_rbf_rows_product);
+// the same epilogues as shard_gemv_kernel, in place.
+__global__ void __launch_bounds__(DCG_NT, 1)
+    shard_rbf_epi_kernel(int mode, long long rows, long long row0, const double* v, const double* s, double shift,
+                         const double* b, double* out, double* part, double* parts, int ps, unsigned int* counter,
+                         const dcg_shard_state* state) {
+    if (state && state->done) return;
+    __shared__ double s_tmp[40];
+    __shared__ double s_out[2];
+    const long long r0 = part_begin(rows, gridDim.x, blockIdx.x), r1 = part_begin(rows, gridDim.x, blockIdx.x + 1);
+    double dot = 0.0;
+    for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        const long long g = row0 + i;
+        const double t = out[i];
+        const double vi = ld_cg(v + g);
+        const double ax = s ? add_rn(mul_rn(shift, vi), mul_rn(s[g], t)) : add_rn(mul_rn(shift, vi), t);
+        if (mode == 0) {
+            out[i] = ax;
+            dot = fma(vi, ax, dot);
+        } else {
+            out[i] = sub_rn(b[i], ax);
+        }
+    }
     if (mode == 0 && part) {
         dot = block_sum(dot, s_tmp);
         if (threadIdx.x == 0) s_out[0] = dot;
@@ -368,6 +404,24 @@ int check_slab(const dcg_operator* op) {
 
 int launch_gemv(dcg_context* ctx, cudaStream_t st, int mode, const dcg_operator* op, const double* v,
                 const double* b, double* out, double* part, const dcg_shard_state* state) {
+    if (op && op->kind == DCG_OP_RBF) {
+        // matrix-free slab (config 5): the row-owned tensor-pipe product, then
+        // the epilogue in place
+        int rc = dcg_rbf_mf_check(op);
+        if (rc) return rc;
+        if (op->rows == 0) return DCG_OK;
+        rc = dcg_rbf_rows_product(ctx, st, op, v, 0, op->d_s, nullptr, 0.0, out, state);
+        if (rc) return rc;
+        long long G = ctx->sm_count;
+        if (G > op->rows) G = op->rows;
+        ShardWs w;
+        rc = shard_ws(ctx, st, (int)G, 2, &w);
+        if (rc) return rc;
+        shard_rbf_epi_kernel<<<(unsigned)G, DCG_NT, 0, st>>>(mode, op->rows, op->row0, v, op->d_s, op->shift, b, out,
+                                                               part, w.parts, 2, w.counter, state);
+        DCG_LAUNCHED();
+        return DCG_OK;
+    }
     int rc = check_slab(op);
     if (rc) return rc;
     if (op->rows == 0) return DCG_OK;

@@ -143,9 +143,46 @@ class ShardedOperator:
         return c
 
 
-def sharded_rbf_kernel(x, params, jitter=None, comm=None) -> ShardedOperator:
+class ShardedRbfOperator:
+    """This rank's slab of the matrix-free A = shift I + S K S (config 5):
+    rows [row0, row0 + rows) of the RBF kernel, regenerated from the
+    replicated points X on every product (the row-owned tensor-pipe kernel,
+    csrc/rbfmma.cuh); nothing of size n^2 / R is stored."""
+
+    def __init__(self, x: torch.Tensor, var: float, inv_two_ell2: float, diag: float, row0: int, rows: int, s=None,
+                 shift: float = 0.0):
+        self.x = x
+        self.n, self.row0, self.rows = int(x.shape[0]), int(row0), int(rows)
+        self.var, self.inv_two_ell2, self.diag = float(var), float(inv_two_ell2), float(diag)
+        self.s = s
+        self.shift = float(shift)
+
+    def scaled(self, s, shift: float) -> "ShardedRbfOperator":
+        return ShardedRbfOperator(self.x, self.var, self.inv_two_ell2, self.diag, self.row0, self.rows, s, shift)
+
+    def c_struct(self) -> N.COperator:
+        c = N.COperator()
+        c.kind = N.DCG_OP_RBF
+        c.n = self.n
+        c.row0 = self.row0
+        c.rows = self.rows
+        c.d_k = None
+        c.ldk = 0
+        c.d_x = self.x.data_ptr() if self.n else None
+        c.dim = int(self.x.shape[1])
+        c.var = self.var
+        c.inv_two_ell2 = self.inv_two_ell2
+        c.diag = self.diag
+        c.d_s = self.s.data_ptr() if self.s is not None else None
+        c.shift = self.shift
+        return c
+
+
+def sharded_rbf_kernel(x, params, jitter=None, comm=None, matrix_free=False):
     """This rank's rows of the RBF Gram (gpc.py:82-98), built on device from
-    the replicated data X (n x d, a few MB) - Gram blocks never cross PCIe."""
+    the replicated data X (n x d, a few MB) - Gram blocks never cross PCIe.
+    With ``matrix_free`` the slab is never stored: a ShardedRbfOperator
+    regenerates it on every product (config 5)."""
     comm = comm or SelfComm()
     xd = D.to_dev(x, 2)
     n, dim = xd.shape
@@ -154,6 +191,8 @@ def sharded_rbf_kernel(x, params, jitter=None, comm=None) -> ShardedOperator:
     if jitter < 0.0:
         raise ValueError("jitter must be non-negative")
     r0, rows = row_range(n, comm.world, comm.rank)
+    if matrix_free:
+        return ShardedRbfOperator(xd.contiguous(), var, 1.0 / (2.0 * params.lengthscale**2), var + jitter, r0, rows)
     ld = D.padded_ld(n)
     kslab = D.zeros(max(rows, 1), ld)
     if rows:
@@ -485,7 +524,7 @@ def _allgather_vec(comm, be, local: torch.Tensor, n: int) -> torch.Tensor:
 
 
 def sharded_laplace_newton(x, y, params=None, cfg: SolverConfig | None = None, newton_tol=1.0, max_newton=30, k=8,
-                           selection="largest", comm=None, backend=None, jitter=None):
+                           selection="largest", comm=None, backend=None, jitter=None, matrix_free=False):
     """laplace_newton(rbf_kernel(x, params), y, "defcg", ...) (gpc.py:212-291)
     with K row-sharded over the ranks of `comm`: every rank builds its slab
     from the replicated X, the n-vectors of the Newton glue (f, a, s, H f + g)
@@ -499,7 +538,8 @@ def sharded_laplace_newton(x, y, params=None, cfg: SolverConfig | None = None, n
     comm = comm or SelfComm()
     be = backend or DeviceShardBackend()
     # `x` is the data matrix (the slab is built here) or a prebuilt kernel slab
-    op = x if isinstance(x, ShardedOperator) else sharded_rbf_kernel(x, params, jitter, comm)
+    op = x if isinstance(x, (ShardedOperator, ShardedRbfOperator)) else sharded_rbf_kernel(x, params, jitter, comm,
+                                                                                             matrix_free)
     kop = op.c_struct()   # the kernel matrix itself (no scaling, no shift)
     n, rows = op.n, op.rows
     yd = D.to_dev(y, 1)

@@ -198,3 +198,62 @@ def test_sharded_laplace_newton_world1_matches_gpc(P):
                                                                      [r.solver_iterations for r in recs])
         assert abs(a.psi - b.psi) <= 1e-8 * abs(b.psi)
     assert np.linalg.norm(srecs[-1].f - recs[-1].f) <= 1e-6 * np.linalg.norm(recs[-1].f)
+
+
+def test_matrix_free_slab_products_match_stored(P, rng):
+    """Config-5 building block: the matrix-free slab operator (row-owned
+    tensor-pipe kernel) against the stored slab's products, single vector
+    (the sharded solve's apply) and multi-vector (its refresh), on row slabs
+    that are not 64-aligned."""
+    from paper_1706_00241_b200.sharded import row_range, sharded_rbf_kernel
+
+    n, dim = 900, 9
+    x = torch.from_numpy(rng.standard_normal((n, dim))).cuda()
+    params = P.KernelParams(1.2, 1.7)
+    s = torch.from_numpy(rng.uniform(0.2, 0.6, n)).cuda()
+    v = torch.from_numpy(rng.standard_normal(n)).cuda()
+    w = torch.from_numpy(rng.standard_normal((n, 11))).cuda()
+
+    class C:
+        def __init__(self, rank, world):
+            self.rank, self.world = rank, world
+
+    for world in (1, 3):
+        for rank in range(world):
+            st = sharded_rbf_kernel(x, params, comm=C(rank, world)).scaled(s, 1.0)
+            mf = sharded_rbf_kernel(x, params, comm=C(rank, world), matrix_free=True).scaled(s, 1.0)
+            r0, rows = row_range(n, world, rank)
+            for a in (st, mf):
+                assert (a.row0, a.rows) == (r0, rows)
+            outs = []
+            for a in (st, mf):
+                y = torch.empty(rows, dtype=torch.float64, device="cuda")
+                yb = torch.empty(rows, 11, dtype=torch.float64, device="cuda")
+                c = a.c_struct()
+                import ctypes
+
+                P._native.check(P._native.lib().dcg_op_apply(P._device.ctx(), P._device.stream(), ctypes.byref(c),
+                                                             v.data_ptr(), y.data_ptr()))
+                P._native.check(P._native.lib().dcg_op_apply_block(P._device.ctx(), P._device.stream(),
+                                                                   ctypes.byref(c), w.data_ptr(), 11, yb.data_ptr()))
+                outs.append((y, yb))
+            for ref, got in zip(outs[0], outs[1]):
+                err = float(torch.linalg.norm(got - ref) / torch.linalg.norm(ref))
+                assert err <= 1e-13, (world, rank, err)
+
+
+def test_sharded_laplace_newton_matrix_free(P):
+    """The sharded Newton driver on the matrix-free slab (config 5's path) at
+    world = 1 against laplace_newton on the stored Gram: iteration counts +-1,
+    psi within 1e-8."""
+    from paper_1706_00241_b200.sharded import SelfComm, sharded_laplace_newton
+
+    x, y = O.gpc_inputs(1500, 6, 0)
+    cfg = P.SolverConfig(tol=1e-8, ell=12)
+    gram = P.rbf_kernel(x, P.KernelParams(1.0, 1.5))
+    _, recs = P.laplace_newton(gram, y, "defcg", cfg, newton_tol=-np.inf, max_newton=4, k=8, selection="largest")
+    srecs = sharded_laplace_newton(x, y, P.KernelParams(1.0, 1.5), cfg, newton_tol=-np.inf, max_newton=4, k=8,
+                                   selection="largest", comm=SelfComm(), matrix_free=True)
+    for a, b in zip(srecs, recs):
+        assert abs(a.solver_iterations - b.solver_iterations) <= 1
+        assert abs(a.psi - b.psi) <= 1e-8 * abs(b.psi)

@@ -145,12 +145,72 @@ def config5(n, d=16, ell=3.0, k=32, iters=20):
     a = op.scaled(s, 1.0)
     b = torch.from_numpy(rng.standard_normal(n)).cuda()
     cfg = P.SolverConfig(tol=1e-8, ell=k + 4, max_iters=iters)
-    basis = P.refresh_basis(a, torch.from_numpy(rng.standard_normal((n, k))).cuda())
+    wk = torch.from_numpy(rng.standard_normal((n, k))).cuda()
+    basis = P.refresh_basis(a, wk)
+    torch.cuda.synchronize()
+    e0.record()
+    basis = P.refresh_basis(a, wk)
+    e1.record()
+    torch.cuda.synchronize()
+    refresh_ms = e0.elapsed_time(e1)
+    half = a.with_rows(0, n // 2) if hasattr(a, "with_rows") else None
+    del half
     _, rep, _ = P.deflated_cg_solve(a, b, torch.zeros(n, dtype=torch.float64, device="cuda"), basis, cfg)
     return {"n": n, "d": d, "matvec_ms": ms, "flop_alg_per_matvec": flop, "achieved_tflops": flop / (ms / 1e3) / 1e12,
             "exp_per_s": float(n) * n / (ms / 1e3), "solve_iterations": rep.iterations,
             "solve_ms_per_iteration": rep.device_ms / (rep.iterations + 2),
+            "refresh_ms_k": [refresh_ms, k],
             "note": "symmetric half-evaluation (each pair once), dot-product distance form"}
+
+
+def config5_slab(n=200000, d=16, ell=3.0, k=32, world=8):
+    """Config 5 per rank: rank 0's row slab (n / world rows) of the matrix-free
+    operator -- the product every rank runs per sharded def-CG iteration, and
+    the slab's multi-vector product of the refresh (k columns)."""
+    import ctypes
+
+    import torch
+
+    import paper_1706_00241_b200 as P
+    from paper_1706_00241_b200.sharded import sharded_rbf_kernel
+
+    C = type("C", (), {"rank": 0, "world": world})
+
+    rng = np.random.default_rng(0)
+    x = torch.from_numpy(rng.standard_normal((n, d))).cuda()
+    s = torch.from_numpy(rng.uniform(0.2, 0.5, n)).cuda()
+    op = sharded_rbf_kernel(x, P.KernelParams(1.0, ell), comm=C(), matrix_free=True).scaled(s, 1.0)
+    c = op.c_struct()
+    v = torch.from_numpy(rng.standard_normal(n)).cuda()
+    w = torch.from_numpy(rng.standard_normal((n, k))).cuda()
+    y = torch.empty(op.rows, dtype=torch.float64, device="cuda")
+    yb = torch.empty(op.rows, k, dtype=torch.float64, device="cuda")
+    lib, ctx, st = P._native.lib(), P._device.ctx(), P._device.stream()
+
+    def apply():
+        P._native.check(lib.dcg_op_apply(ctx, st, ctypes.byref(c), v.data_ptr(), y.data_ptr()))
+
+    def block():
+        P._native.check(lib.dcg_op_apply_block(ctx, st, ctypes.byref(c), w.data_ptr(), k, yb.data_ptr()))
+
+    out = {"n": n, "d": d, "k": k, "world": world, "rows_per_rank": op.rows}
+    for name, fn, reps in (("slab_matvec_ms", apply, 3), ("slab_block_ms", block, 1)):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        out[name] = e0.elapsed_time(e1) / reps
+    pairs = float(n) * op.rows
+    ops = pairs * (d + 12 + 1)
+    out["slab_fp64_ops_per_s"] = ops / (out["slab_matvec_ms"] / 1e3)
+    out["note"] = ("row-owned tensor-pipe kernel (rbf_mma_rows_kernel): per element d DMMA-FMAs + ~12 FP64 ops "
+                   "(exp, init) + 1 (product) [+ k on DMMA for the block product]; each rank also all-gathers p "
+                   "(8n B) per iteration")
+    return out
 
 
 def main():
@@ -171,6 +231,8 @@ def main():
         out["note"] = "BASELINE configs[2] at one GPU (the 1-GPU point of its 1/2/4/8 scaling); stored Gram in HBM"
         out["cpu_baseline"] = cpu_sweep_sample(n, n_cpu=12000)
         out["cpu_baseline"]["sample"] += " (plain-CG iteration cost on the host at n_cpu, scaled to n)"
+    elif what == "config5-slab":
+        out = config5_slab(int(sys.argv[2]) if len(sys.argv) > 2 else 200000)
     elif what == "config5":
         n = int(sys.argv[2]) if len(sys.argv) > 2 else 50000
         out = config5(n)
