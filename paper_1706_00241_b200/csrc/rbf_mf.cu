@@ -1,119 +1,13 @@
-// Standalone matrix-free RBF products (K7, rbfmf.cuh): the operator apply
+// Standalone matrix-free RBF products (K7, rbfmma.cuh): the operator apply
 // y = shift v + s_out (.) K (s_in (.) v) and the multi-vector form
 // Y = shift X_rows + s_out (.) K (s_in (.) X) used by refresh_basis
 // (recycle.py:90: A W with A the Newton matrix).  Rows [row0, row0 + rows) of
 // the operator (row slabs for the sharded solver); work is distributed in
 // whole 64-row chunks.
 #include "common.cuh"
-#include "rbfmf.cuh"
 #include "rbfmma.cuh"
 
-#define MF_KC 16   // columns of X per pass of the multi-vector kernel
-
 namespace {
-
-RbfParams params_of(const dcg_operator* op) {
-    RbfParams p;
-    p.X = op->d_x;
-    p.n = op->n;
-    p.dim = (int)op->dim;
-    p.var = op->var;
-    p.inv2 = op->inv_two_ell2;
-    p.diag = op->diag;
-    return p;
-}
-
-__global__ void __launch_bounds__(DCG_NT, 1)
-    rbf_mf_gemv_kernel(RbfParams p, long long row0, long long rows, const double* v, const double* s_in,
-                       const double* s_out, double shift, double* y) {
-    extern __shared__ __align__(16) double smem[];
-    const long long nchunks = (rows + MF_TB - 1) / MF_TB;
-    for (long long c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        const long long r0 = row0 + c * MF_TB, r1 = min(row0 + rows, r0 + MF_TB);
-        rbf_rows_gemv(p, r0, r1, v, s_in, smem, [&](long long i, double t) {
-            const long long li = i - row0;
-            double val = s_out ? mul_rn(s_out[li], t) : t;
-            if (shift != 0.0) val = add_rn(mul_rn(shift, v[i]), val);
-            y[li] = val;
-        });
-    }
-}
-
-// Y(rows x k) over chunks of MF_KC columns: each K tile is generated once per
-// column chunk and applied to the chunk's columns.
-__global__ void __launch_bounds__(DCG_NT, 1)
-    rbf_mf_block_kernel(RbfParams p, long long row0, long long rows, const double* X, int k, const double* s_in,
-                        const double* s_out, double shift, double* Y) {
-    extern __shared__ __align__(16) double smem[];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double* xit = smem;
-    double* xjt = xit + p.dim * MF_TB;
-    double* vj = xjt + p.dim * MF_TB;            // 64 x MF_KC
-    double* red = vj + MF_TB * MF_KC;            // NW x 64
-    double* nI = red + DCG_NW * MF_TB;           // 64 row norms of the I chunk
-    double* nJ = nI + MF_TB;                     // 64 row norms of the J tile
-    const long long nchunks = (rows + MF_TB - 1) / MF_TB;
-    for (long long c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        const long long i0 = row0 + c * MF_TB, r1 = min(row0 + rows, i0 + MF_TB);
-        for (int c0 = 0; c0 < k; c0 += MF_KC) {
-            const int kc = min(MF_KC, k - c0);
-            cta_sync();
-            rbf_stage_rows(p, i0, r1, xit);
-            cta_sync();
-            rbf_stage_norms(p, xit, nI);
-            double acc[2][MF_KC];
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-#pragma unroll
-                for (int q = 0; q < MF_KC; ++q) acc[r][q] = 0.0;
-            for (long long j0 = 0; j0 < p.n; j0 += MF_TB) {
-                cta_sync();
-                rbf_stage_rows(p, j0, p.n, xjt);
-                for (int e = tid; e < MF_TB * MF_KC; e += blockDim.x) {
-                    const int jr = e / MF_KC, q = e - (e / MF_KC) * MF_KC;
-                    const long long j = j0 + jr;
-                    double vv = 0.0;
-                    if (j < p.n && q < kc) {
-                        vv = __ldg(X + j * k + c0 + q);
-                        if (s_in) vv = mul_rn(__ldg(s_in + j), vv);
-                    }
-                    vj[jr * MF_KC + q] = vv;
-                }
-                cta_sync();
-                rbf_stage_norms(p, xjt, nJ);
-                cta_sync();
-                double kv[2][4];
-                rbf_tile_values<true>(p, xit, xjt, i0, j0, r1, kv, nI, nJ);
-#pragma unroll
-                for (int cc = 0; cc < 4; ++cc) {
-                    const double* vr = vj + (4 * warp + cc) * MF_KC;
-#pragma unroll
-                    for (int q = 0; q < MF_KC; ++q) {
-                        acc[0][q] = fma(kv[0][cc], vr[q], acc[0][q]);
-                        acc[1][q] = fma(kv[1][cc], vr[q], acc[1][q]);
-                    }
-                }
-            }
-            // combine the warps' column groups per output column, fixed order
-            for (int q = 0; q < kc; ++q) {
-                cta_sync();
-                red[warp * MF_TB + 2 * lane] = acc[0][q];
-                red[warp * MF_TB + 2 * lane + 1] = acc[1][q];
-                cta_sync();
-                if (tid < MF_TB && i0 + tid < r1) {
-                    double t = 0.0;
-#pragma unroll 4
-                    for (int w = 0; w < DCG_NW; ++w) t += red[w * MF_TB + tid];
-                    const long long li = i0 + tid - row0;
-                    const long long g = i0 + tid;
-                    double val = s_out ? mul_rn(s_out[li], t) : t;
-                    if (shift != 0.0) val = add_rn(mul_rn(shift, X[g * k + c0 + q]), val);
-                    Y[li * k + c0 + q] = val;
-                }
-            }
-        }
-    }
-}
 
 __global__ void __launch_bounds__(DCG_NT, 1)
     rbf_mma_pass1_kernel(RbfMma p, const double* v, const double* s_in, double* colpart, double* rowpart) {
@@ -122,11 +16,6 @@ __global__ void __launch_bounds__(DCG_NT, 1)
     rbf_mma_pass1(p, v, s_in, colpart, rowpart, smem);
 }
 
-int grid_for(const dcg_context* ctx, long long rows) {
-    long long nchunks = (rows + MF_TB - 1) / MF_TB;
-    if (nchunks > ctx->sm_count) nchunks = ctx->sm_count;
-    return nchunks < 1 ? 1 : (int)nchunks;
-}
 
 }  // namespace
 
@@ -138,7 +27,6 @@ int dcg_rbf_mf_check(const dcg_operator* op) {
     return DCG_OK;
 }
 
-size_t dcg_rbf_mf_smem(int dim) { return sizeof(double) * (size_t)rbf_mf_smem_doubles(dim); }
 
 int dcg_sym_pass2_launch(cudaStream_t st, int G, int R, long long n, const double* colpart, const double* rowpart,
                          const double* v, const double* s_out, double shift, double* y);

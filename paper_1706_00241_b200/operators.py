@@ -168,9 +168,11 @@ class DenseOperator:
 
 class RbfOperator(DenseOperator):
     """Matrix-free A = shift I + S K S with the RBF kernel K regenerated from
-    the points X on every product (kernel K7, config 5; csrc/rbfmf.cuh): K_ij
-    = var * exp(-||x_i - x_j||^2 * inv_two_ell2), K_ii = diag = var + jitter,
-    elements bit-identical to the stored Gram of rbf_kernel (gpc.py:82-98).
+    the points X on every product (kernel K7, config 5; csrc/rbfmma.cuh): K_ij
+    = var * exp(-||x_i - x_j||^2 * inv_two_ell2), K_ii = diag = var + jitter;
+    the distance is formed as |x_i|^2 + |x_j|^2 - 2 x_i.x_j on the FP64 tensor
+    pipe and the exponential from a table, so elements agree with the stored
+    Gram of rbf_kernel (gpc.py:82-98) to ~1e-16 relative.
     Nothing of size n^2 is ever allocated."""
 
     def __init__(self, x: torch.Tensor, var: float, inv_two_ell2: float, diag: float, s=None, shift: float = 0.0):
