@@ -369,6 +369,23 @@ DCG_API int dcg_shard_direction(dcg_context* ctx, void* stream, long long rows, 
                                 double* d_history, double* d_log_p, double* d_log_mu,
                                 double* d_log_beta);
 
+/* ---- L5b: sharded matrix-free products in the symmetric form (config 5) -- *
+ * Rank `rank` of `world` evaluates an equal-cost share of the lower-triangle
+ * 64 x 64 tiles of K (each pair once) for the full vector d_v (n, gathered)
+ * and writes its partial t = (K (s (.) v)) share to d_t (all n rows, zero
+ * where it has no tiles); the caller all-reduces d_t over the ranks and runs
+ * dcg_shard_epilogue.  op: the rank's RBF slab (d_s, shift, row0/rows used by
+ * the epilogue only).  Work per rank: n^2 / (2 world) pairs, against n^2 /
+ * world for the row-slab dcg_shard_apply_dot.                              */
+DCG_API int dcg_shard_rbf_sym_partial(dcg_context* ctx, void* stream, const dcg_operator* op,
+                                      int rank, int world, const double* d_v, double* d_t,
+                                      const dcg_shard_state* d_state);
+/* mode 0: d_out = (A v) on the slab rows and d_part = its p'Ap partial;
+ * mode 1: d_out = b - (A v) -- from the all-reduced t = K (s (.) v) (full).  */
+DCG_API int dcg_shard_epilogue(dcg_context* ctx, void* stream, int mode, const dcg_operator* op,
+                               const double* d_v, const double* d_b, const double* d_t,
+                               double* d_out, double* d_part, const dcg_shard_state* d_state);
+
 #ifdef __cplusplus
 }
 #endif

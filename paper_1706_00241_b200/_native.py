@@ -210,6 +210,8 @@ SIGNATURES = {
     "dcg_gpc_newton_update_async": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P, _P, _P, _P, _P, _P],
     # row-sharded def-CG (include/defcg_b200.h L5)
     "dcg_shard_apply_dot": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P],
+    "dcg_shard_rbf_sym_partial": [_P, _P, ctypes.POINTER(COperator), ctypes.c_int, ctypes.c_int, _P, _P, _P],
+    "dcg_shard_epilogue": [_P, _P, ctypes.c_int, ctypes.POINTER(COperator), _P, _P, _P, _P, _P, _P],
     "dcg_shard_residual": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P],
     "dcg_shard_partials": [_P, _P, _LL, ctypes.c_int, _P, _P, _P, _P],
     "dcg_shard_start": [_P, _P, _LL, ctypes.c_int, _P, _P, _P, _P, _P, _P, _D, _LL, _LL],

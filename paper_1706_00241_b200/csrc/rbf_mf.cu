@@ -54,6 +54,8 @@ RbfMma dcg_rbf_mma_params(const dcg_operator* op, double* operands, int nteam) {
     p.inv2 = op->inv_two_ell2;
     p.diag = op->diag / op->var;
     p.nteam = nteam;
+    p.t_lo = 0;
+    p.t_hi = sym_ntiles(op->n);
     return p;
 }
 
@@ -157,3 +159,106 @@ int dcg_rbf_mf_block(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, 
     if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
     return dcg_rbf_rows_product(ctx, st, op, X, k, s_in, s_out, shift, Y, nullptr);
 }
+
+namespace {
+
+// A rank's share [t_lo, t_hi) of the lower-triangle tiles: pass 1 with the
+// team table exported (block 0) for the local pass 2.  colpart / rowpart are
+// indexed relative to t_lo.
+__global__ void __launch_bounds__(DCG_NT, 1)
+    rbf_mma_pass1_share_kernel(RbfMma p, const double* v, const double* s_in, double* colpart, double* rowpart,
+                               long long* tbl_out, const dcg_shard_state* gate) {
+    if (gate && gate->done) return;
+    extern __shared__ __align__(16) double smem[];
+    rm_init(smem, p);
+    const int R = gridDim.x * p.nteam;
+    if (blockIdx.x == 0)
+        for (int b = threadIdx.x; b <= R; b += blockDim.x) tbl_out[b] = rm_table(smem)[b];
+    rbf_mma_pass1(p, v, s_in, colpart - p.t_lo * RM_TB, rowpart - p.t_lo * RM_TB, smem);
+}
+
+// t_i (all n rows) from this share's partials: column partials of the tiles
+// (I', I), I' > I, inside [t_lo, t_hi), and the row segments of tile row I
+// that start inside it (at J = 0 or at a team range start).  Rows without
+// contributions get 0.  One thread per row; consecutive rows read
+// consecutive partial entries.
+__global__ void sym_pass2_share_kernel(long long n, long long t_lo, long long t_hi, const long long* tbl, int R,
+                                       const double* colpart, const double* rowpart, double* t,
+                                       const dcg_shard_state* gate) {
+    if (gate && gate->done) return;
+    const long long NT = sym_ntiles_side(n);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long I = i / RM_TB;
+        const int rl = (int)(i - I * RM_TB);
+        double acc = 0.0;
+        // column partials: tile id base(I') + I in [t_lo, t_hi), I' > I
+        long long Ip = I + 1;
+        if (t_lo > I) {
+            const long long need = t_lo - I;   // base(I') >= need
+            long long c = sym_tile_row(need);
+            if (sym_tile_row_base(c) < need) ++c;
+            if (c > Ip) Ip = c;
+        }
+        for (; Ip < NT; ++Ip) {
+            const long long id = sym_tile_row_base(Ip) + I;
+            if (id >= t_hi) break;
+            acc += ld_cg(colpart + (id - t_lo) * RM_TB + rl);
+        }
+        // row segments of tile row I
+        const long long base = sym_tile_row_base(I);
+        if (base >= t_lo && base < t_hi) acc += ld_cg(rowpart + (base - t_lo) * RM_TB + rl);
+        for (int b = 0; b < R; ++b) {   // team range starts inside the row (tbl[0] = t_lo may be one)
+            const long long st = tbl[b];
+            if (st > base && st <= base + I && st < t_hi && (b == 0 || st > tbl[b - 1]))
+                acc += ld_cg(rowpart + (st - t_lo) * RM_TB + rl);
+        }
+        t[i] = acc;
+    }
+}
+
+}  // namespace
+
+// Sharded matrix-free K (s (.) v), symmetric form: rank `rank` of `world`
+// evaluates an equal-cost share of the lower-triangle tiles (each pair once,
+// as in the unsharded operator) and writes its partial t (all n rows) to d_t;
+// the sum over ranks (an all-reduce) is K (s (.) v).  Half the pairs of the
+// row-slab form; the exchange is one n-vector all-reduce per product.
+extern "C" int dcg_shard_rbf_sym_partial(dcg_context* ctx, void* stream, const dcg_operator* op, int rank, int world,
+                                         const double* d_v, double* d_t, const dcg_shard_state* d_state) {
+    if (!ctx || !d_v || !d_t || world < 1 || rank < 0 || rank >= world) return DCG_E_CONFIG;
+    int rc = dcg_rbf_mf_check(op);
+    if (rc) return rc;
+    const long long n = op->n;
+    if (n == 0) return DCG_OK;
+    cudaStream_t st = as_stream(stream);
+    const long long ntt = sym_ntiles(n);
+    const long long t_lo = sym_tile_begin(n, world, rank), t_hi = sym_tile_begin(n, world, rank + 1);
+    const long long nloc = t_hi - t_lo;
+    const int G = ctx->sm_count < DCG_SYM_MAX_CTAS ? ctx->sm_count : DCG_SYM_MAX_CTAS;
+    const int nteam = dcg_rbf_mma_teams(ctx, (int)op->dim, 0);
+    const size_t opnd = dcg_rbf_mma_operand_doubles(n, (int)op->dim);
+    const size_t need = sizeof(double) * (opnd + 2 * (size_t)(nloc > 0 ? nloc : 1) * RM_TB) +
+                        sizeof(long long) * (2 * DCG_SYM_MAX_CTAS + 2) + 1024;
+    rc = dcg_ws2_reserve(ctx, need);
+    if (rc) return rc;
+    double* operands = static_cast<double*>(ctx->ws2);
+    double* colpart = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(operands + opnd) + 255) & ~uintptr_t(255));
+    double* rowpart = colpart + (nloc > 0 ? nloc : 1) * RM_TB;
+    long long* tbl = reinterpret_cast<long long*>(rowpart + (nloc > 0 ? nloc : 1) * RM_TB);
+    RbfMma p = dcg_rbf_mma_params(op, operands, nteam);
+    p.t_lo = t_lo;
+    p.t_hi = t_hi;
+    (void)ntt;
+    rc = dcg_rbf_mma_prep(ctx, st, p);
+    if (rc) return rc;
+    const size_t smem = sizeof(double) * (size_t)rm_smem_doubles((int)op->dim, nteam);
+    DCG_CUDA(cudaFuncSetAttribute(rbf_mma_pass1_share_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    rbf_mma_pass1_share_kernel<<<G, DCG_NT, smem, st>>>(p, d_v, op->d_s, colpart, rowpart, tbl, d_state);
+    DCG_LAUNCHED();
+    sym_pass2_share_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(n, t_lo, t_hi, tbl, G * nteam, colpart, rowpart, d_t,
+                                                              d_state);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}
+

@@ -62,6 +62,7 @@ struct RbfMma {
     int dim, dp;
     double var, inv2, diag;   // diag = (var + jitter) / var (the E_ii above)
     int nteam;           // teams per CTA (1 or 2)
+    long long t_lo, t_hi;   // lower-triangle tiles covered by this launch (a rank's share when sharded)
 };
 
 // xf / xb from X (one launch per product or solve; X is read once)
@@ -204,7 +205,7 @@ __device__ __forceinline__ void rm_init(double* smem, const RbfMma& p) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     long long* tbl = rm_table(smem);
     const int R = gridDim.x * p.nteam;
-    for (int b = threadIdx.x; b <= R; b += blockDim.x) tbl[b] = sym_tile_begin(p.n, R, b);
+    for (int b = threadIdx.x; b <= R; b += blockDim.x) tbl[b] = sym_tile_begin_range(p.n, p.t_lo, p.t_hi, R, b);
     cta_sync();
 }
 

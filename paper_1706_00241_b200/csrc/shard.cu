@@ -182,8 +182,8 @@ __global__ void __launch_bounds__(DCG_NT, 1)
 // the same epilogues as shard_gemv_kernel, in place.
 __global__ void __launch_bounds__(DCG_NT, 1)
     shard_rbf_epi_kernel(int mode, long long rows, long long row0, const double* v, const double* s, double shift,
-                         const double* b, double* out, double* part, double* parts, int ps, unsigned int* counter,
-                         const dcg_shard_state* state) {
+                         const double* b, const double* t_rows, double* out, double* part, double* parts, int ps,
+                         unsigned int* counter, const dcg_shard_state* state) {
     if (state && state->done) return;
     __shared__ double s_tmp[40];
     __shared__ double s_out[2];
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(DCG_NT, 1)
     double dot = 0.0;
     for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
         const long long g = row0 + i;
-        const double t = out[i];
+        const double t = t_rows ? ld_cg(t_rows + i) : out[i];
         const double vi = ld_cg(v + g);
         const double ax = s ? add_rn(mul_rn(shift, vi), mul_rn(s[g], t)) : add_rn(mul_rn(shift, vi), t);
         if (mode == 0) {
@@ -417,8 +417,8 @@ int launch_gemv(dcg_context* ctx, cudaStream_t st, int mode, const dcg_operator*
         ShardWs w;
         rc = shard_ws(ctx, st, (int)G, 2, &w);
         if (rc) return rc;
-        shard_rbf_epi_kernel<<<(unsigned)G, DCG_NT, 0, st>>>(mode, op->rows, op->row0, v, op->d_s, op->shift, b, out,
-                                                               part, w.parts, 2, w.counter, state);
+        shard_rbf_epi_kernel<<<(unsigned)G, DCG_NT, 0, st>>>(mode, op->rows, op->row0, v, op->d_s, op->shift, b,
+                                                               nullptr, out, part, w.parts, 2, w.counter, state);
         DCG_LAUNCHED();
         return DCG_OK;
     }
@@ -451,6 +451,27 @@ extern "C" int dcg_shard_residual(dcg_context* ctx, void* stream, const dcg_oper
                                   const double* d_b, double* d_r, const dcg_shard_state* d_state) {
     if (!ctx || !d_v || !d_b || !d_r) return DCG_E_CONFIG;
     return launch_gemv(ctx, as_stream(stream), 1, op, d_v, d_b, d_r, nullptr, d_state);
+}
+
+// The slab epilogue of a product whose K (s (.) v) arrived by an all-reduce
+// (dcg_shard_rbf_sym_partial): mode 0 out = (A v) rows + the p'Ap partial,
+// mode 1 out = b - (A v) rows.  d_t is the full-length reduced vector.
+extern "C" int dcg_shard_epilogue(dcg_context* ctx, void* stream, int mode, const dcg_operator* op, const double* d_v,
+                                  const double* d_b, const double* d_t, double* d_out, double* d_part,
+                                  const dcg_shard_state* d_state) {
+    if (!ctx || !op || !d_v || !d_t || !d_out || (mode != 0 && mode != 1) || (mode == 1 && !d_b)) return DCG_E_CONFIG;
+    if (op->rows == 0) return DCG_OK;
+    cudaStream_t st = as_stream(stream);
+    long long G = ctx->sm_count;
+    if (G > op->rows) G = op->rows;
+    ShardWs w;
+    int rc = shard_ws(ctx, st, (int)G, 2, &w);
+    if (rc) return rc;
+    shard_rbf_epi_kernel<<<(unsigned)G, DCG_NT, 0, st>>>(mode, op->rows, op->row0, d_v, op->d_s, op->shift, d_b,
+                                                           d_t + op->row0, d_out, mode == 0 ? d_part : nullptr, w.parts,
+                                                           2, w.counter, d_state);
+    DCG_LAUNCHED();
+    return DCG_OK;
 }
 
 extern "C" int dcg_shard_partials(dcg_context* ctx, void* stream, long long rows, int k, const double* d_u,

@@ -99,6 +99,22 @@ __host__ __device__ __forceinline__ long long sym_row_begin(long long n, long lo
     return lo;
 }
 
+// first tile of part b of R over the tile sub-range [t_lo, t_hi) (equal cost;
+// t_lo = 0, t_hi = all tiles reproduces sym_tile_begin)
+__host__ __device__ __forceinline__ long long sym_tile_begin_range(long long n, long long t_lo, long long t_hi,
+                                                                   long long R, long long b) {
+    if (b <= 0) return t_lo;
+    if (b >= R) return t_hi;
+    const long long c0 = sym_cost4(t_lo, n), c1 = sym_cost4(t_hi, n);
+    const long long goal = c0 + (b * (c1 - c0) + R - 1) / R;
+    long long lo = t_lo, hi = t_hi;
+    while (lo < hi) {
+        const long long mid = (lo + hi) / 2;
+        if (sym_cost4(mid, n) >= goal) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
 #define DCG_SYM_MAX_CTAS 255
 // Shared memory the two passes need (doubles): ring, 2 x 16 x 64 row-flush
 // buffers, 2 x STAGES mbarriers, the table of G + 1 pass-1 range starts.

@@ -150,15 +150,20 @@ class ShardedRbfOperator:
     csrc/rbfmma.cuh); nothing of size n^2 / R is stored."""
 
     def __init__(self, x: torch.Tensor, var: float, inv_two_ell2: float, diag: float, row0: int, rows: int, s=None,
-                 shift: float = 0.0):
+                 shift: float = 0.0, rank: int = 0, world: int = 1, symmetric: bool = True):
         self.x = x
         self.n, self.row0, self.rows = int(x.shape[0]), int(row0), int(rows)
         self.var, self.inv_two_ell2, self.diag = float(var), float(inv_two_ell2), float(diag)
         self.s = s
         self.shift = float(shift)
+        # symmetric: the solve's products evaluate this rank's share of the
+        # lower-triangle tiles and all-reduce an n-vector (half the pairs of
+        # the row slab); otherwise the row slab is evaluated in full
+        self.rank, self.world, self.symmetric = int(rank), int(world), bool(symmetric)
 
     def scaled(self, s, shift: float) -> "ShardedRbfOperator":
-        return ShardedRbfOperator(self.x, self.var, self.inv_two_ell2, self.diag, self.row0, self.rows, s, shift)
+        return ShardedRbfOperator(self.x, self.var, self.inv_two_ell2, self.diag, self.row0, self.rows, s, shift,
+                                  self.rank, self.world, self.symmetric)
 
     def c_struct(self) -> N.COperator:
         c = N.COperator()
@@ -192,7 +197,8 @@ def sharded_rbf_kernel(x, params, jitter=None, comm=None, matrix_free=False):
         raise ValueError("jitter must be non-negative")
     r0, rows = row_range(n, comm.world, comm.rank)
     if matrix_free:
-        return ShardedRbfOperator(xd.contiguous(), var, 1.0 / (2.0 * params.lengthscale**2), var + jitter, r0, rows)
+        return ShardedRbfOperator(xd.contiguous(), var, 1.0 / (2.0 * params.lengthscale**2), var + jitter, r0, rows,
+                                  rank=comm.rank, world=comm.world)
     ld = D.padded_ld(n)
     kslab = D.zeros(max(rows, 1), ld)
     if rows:
@@ -248,6 +254,16 @@ class DeviceShardBackend:
         cop = op.c_struct()
         N.check(N.lib().dcg_shard_apply_dot(self.ctx(), self.stream(), ctypes.byref(cop), _p(vfull), _p(out),
                                             _p(part), _p(state)), what="shard_apply_dot")
+
+    def sym_partial(self, op, vfull, t, state=None):
+        cop = op.c_struct()
+        N.check(N.lib().dcg_shard_rbf_sym_partial(self.ctx(), self.stream(), ctypes.byref(cop), op.rank, op.world,
+                                                  _p(vfull), _p(t), _p(state)), what="shard_rbf_sym_partial")
+
+    def epilogue(self, mode, op, vfull, b, t, out, part, state=None):
+        cop = op.c_struct()
+        N.check(N.lib().dcg_shard_epilogue(self.ctx(), self.stream(), mode, ctypes.byref(cop), _p(vfull), _p(b), _p(t),
+                                           _p(out), _p(part), _p(state)), what="shard_epilogue")
 
     def partials(self, rows, k, u, w, m, part):
         N.check(N.lib().dcg_shard_partials(self.ctx(), self.stream(), rows, k, _p(u), _p(w), _p(m), _p(part)),
@@ -341,17 +357,38 @@ def sharded_solve(op: ShardedOperator, b_loc, x_prev_loc, basis: ShardBasis | No
     hist = be.zeros(max_iters + 1)
     log = _alloc_log(be, rows, ell, k)
 
+    # products: the row slab, or (symmetric matrix-free operators) this rank's
+    # share of the lower-triangle tiles + an all-reduce of K (s (.) v)
+    sym = getattr(op, "symmetric", False)
+    tfull = be.empty(comm.world * mb) if sym else None
+
+    def residual(bvec, out, st=None):
+        if sym:
+            be.sym_partial(op, full, tfull, st)
+            comm.allreduce(tfull)
+            be.epilogue(1, op, full, bvec, tfull, out, None, st)
+        else:
+            be.residual(op, full, bvec, out, st)
+
+    def apply_dot(out, part, st):
+        if sym:
+            be.sym_partial(op, full, tfull, st)
+            comm.allreduce(tfull)
+            be.epilogue(0, op, full, None, tfull, out, part, st)
+        else:
+            be.apply_dot(op, full, out, part, st)
+
     # ---- prologue: norm_b, warm start, r_0, mu_0, p_0 ----------------------
     if k:
         comm.allgather(x_prev_loc, full)
-        be.residual(op, full, b_loc, r)                    # r_prev = b - A x_prev
+        residual(b_loc, r)                                 # r_prev = b - A x_prev
         be.partials(rows, k, b_loc, r, w_loc, part2)       # [b'b, W' r_prev]
     else:
         be.partials(rows, 0, b_loc, None, None, part2)     # [b'b]
     comm.allreduce(part2)
     be.start(rows, k, part2, chol, w_loc, x_prev_loc, x, state, float(cfg.tol), max_iters, ell)
     comm.allgather(x[:rows], full)
-    be.residual(op, full, b_loc, r)                        # r_0 = b - A x_0
+    residual(b_loc, r)                                     # r_0 = b - A x_0
     be.partials(rows, k, r, r, aw_loc, part2)              # [r0'r0, AW' r0]
     comm.allreduce(part2)
     be.begin(rows, k, part2, chol, w_loc, r, p, x, state, hist, log)
@@ -365,12 +402,12 @@ def sharded_solve(op: ShardedOperator, b_loc, x_prev_loc, basis: ShardBasis | No
         for _ in range(max(1, poll)):
             j += 1
             comm.allgather(p[:rows], full)
-            be.apply_dot(op, full, ap, part1, state)
+            apply_dot(ap, part1, state)
             comm.allreduce(part1)
             if every > 0 and j % every == 0:               # true residual (solvers.py:175-177)
                 be.update(1, rows, k, part1, x, r, p, ap, aw_loc, part2, state, log)
                 comm.allgather(x[:rows], full)
-                be.residual(op, full, b_loc, r, state)
+                residual(b_loc, r, state)
                 be.update(2, rows, k, None, x, r, p, ap, aw_loc, part2, state, log)
             else:
                 be.update(0, rows, k, part1, x, r, p, ap, aw_loc, part2, state, log)

@@ -257,3 +257,47 @@ def test_sharded_laplace_newton_matrix_free(P):
     for a, b in zip(srecs, recs):
         assert abs(a.solver_iterations - b.solver_iterations) <= 1
         assert abs(a.psi - b.psi) <= 1e-8 * abs(b.psi)
+
+
+@pytest.mark.parametrize("world,k", [(1, 0), (2, 0), (3, 5)])
+def test_symmetric_matrix_free_virtual_ranks(P, rng, world, k):
+    """Config 5's sharded product in the symmetric form: each rank evaluates
+    its share of the lower-triangle tiles of the regenerated K and the ranks
+    all-reduce K (s (.) p).  Against the single-GPU solve on the stored Gram
+    of the same points: same iterations (+-1), solutions 1e-9."""
+    from paper_1706_00241_b200.sharded import DeviceShardBackend, ShardBasis, sharded_rbf_kernel, sharded_solve
+
+    n, dim = 700, 5
+    x = rng.standard_normal((n, dim))
+    params = P.KernelParams(1.0, 1.4)
+    s = rng.uniform(0.2, 0.5, n)
+    b = rng.standard_normal(n)
+    xprev = 0.05 * rng.standard_normal(n)
+    cfg = P.SolverConfig(tol=1e-10, ell=8)
+    a_st = P.rbf_kernel(x, params).scaled(dev(s), 1.0)
+    if k:
+        w = rng.standard_normal((n, k))
+        basis = P.refresh_basis(a_st, w)
+        x_ref, rep_ref, _ = P.deflated_cg_solve(a_st, b, xprev, basis, cfg)
+        sb = ShardBasis(basis.w_dev, basis.aw_dev, basis.chol_dev.contiguous())
+    else:
+        x_ref, rep_ref, _ = P.cg_solve(a_st, b, xprev, cfg)
+        sb = None
+
+    def rank_fn(rank, comm):
+        op = sharded_rbf_kernel(dev(x), params, comm=comm, matrix_free=True).scaled(dev(s), 1.0)
+        assert op.symmetric
+        r0, rows = op.row0, op.rows
+        xl, rep, _ = sharded_solve(op, dev(b[r0:r0 + rows]), dev(xprev[r0:r0 + rows]), sb, cfg, comm,
+                                   DeviceShardBackend(slot=2 + rank), poll=3)
+        torch.cuda.synchronize()
+        return r0, xl.cpu().numpy(), rep
+
+    outs = run_ranks(world, rank_fn)
+    xs = np.zeros(n)
+    for r0, xl, _ in outs:
+        xs[r0:r0 + xl.shape[0]] = xl
+    reps = [o[2] for o in outs]
+    assert all(r.iterations == reps[0].iterations for r in reps)
+    assert abs(reps[0].iterations - rep_ref.iterations) <= 1, (reps[0].iterations, rep_ref.iterations)
+    assert np.linalg.norm(xs - x_ref) <= 1e-9 * np.linalg.norm(x_ref)

@@ -193,8 +193,18 @@ def config5_slab(n=200000, d=16, ell=3.0, k=32, world=8):
     def block():
         P._native.check(lib.dcg_op_apply_block(ctx, st, ctypes.byref(c), w.data_ptr(), k, yb.data_ptr()))
 
+    t = torch.empty(n, dtype=torch.float64, device="cuda")
+
+    def sym_share(rank):
+        def fn():
+            P._native.check(lib.dcg_shard_rbf_sym_partial(ctx, st, ctypes.byref(c), rank, world, v.data_ptr(),
+                                                          t.data_ptr(), None))
+        return fn
+
     out = {"n": n, "d": d, "k": k, "world": world, "rows_per_rank": op.rows}
-    for name, fn, reps in (("slab_matvec_ms", apply, 3), ("slab_block_ms", block, 1)):
+    for name, fn, reps in (("slab_matvec_ms", apply, 3), ("slab_block_ms", block, 1),
+                           ("sym_share_rank0_ms", sym_share(0), 3), (f"sym_share_rank{world - 1}_ms",
+                                                                      sym_share(world - 1), 3)):
         fn()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -207,7 +217,10 @@ def config5_slab(n=200000, d=16, ell=3.0, k=32, world=8):
     pairs = float(n) * op.rows
     ops = pairs * (d + 12 + 1)
     out["slab_fp64_ops_per_s"] = ops / (out["slab_matvec_ms"] / 1e3)
-    out["note"] = ("row-owned tensor-pipe kernel (rbf_mma_rows_kernel): per element d DMMA-FMAs + ~12 FP64 ops "
+    out["sym_allreduce_bytes"] = 8 * n
+    out["note"] = ("sym_share: this rank's share of the lower-triangle tiles (each pair once) + local pass 2, "
+                   "followed by an all-reduce of 8n bytes; slab_*: "
+                   "row-owned tensor-pipe kernel (rbf_mma_rows_kernel): per element d DMMA-FMAs + ~12 FP64 ops "
                    "(exp, init) + 1 (product) [+ k on DMMA for the block product]; each rank also all-gathers p "
                    "(8n B) per iteration")
     return out
