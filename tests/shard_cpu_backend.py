@@ -143,3 +143,103 @@ class CpuShardBackend:
             log.beta[it - 1] = beta
         state[N.SHARD_RR], state[N.SHARD_BETA], state[N.SHARD_REL] = rr_new, beta, rel
         i[N.SHARD_DONE] = 0 if cont else 1
+
+
+# ---- symmetric sharded products (dcg_shard_rbf_sym_partial / dcg_shard_epilogue)
+# The tile-share partition restated from csrc/symgemv.cuh (sym_cost4,
+# sym_tile_begin): same integer arithmetic, so the CPU ranks cover exactly the
+# tiles the CUDA ranks would.
+TB = 64
+
+
+def _side(n):
+    return (n + TB - 1) // TB
+
+
+def _row_base(i):
+    return i * (i + 1) // 2
+
+
+def _tile_row(t):
+    i = int(((8 * t + 1) ** 0.5 - 1) * 0.5)
+    while _row_base(i + 1) <= t:
+        i += 1
+    while _row_base(i) > t:
+        i -= 1
+    return i
+
+
+def _cost4(t, n):
+    nt = _side(n)
+    last = _row_base(nt - 1) if n % TB else _row_base(nt)
+    return 4 * t + max(t - last, 0) + 4 * _tile_row(t)
+
+
+def tile_begin(n, parts, b):
+    nt = _side(n)
+    ntt = nt * (nt + 1) // 2
+    if b <= 0:
+        return 0
+    if b >= parts:
+        return ntt
+    goal = (b * _cost4(ntt, n) + parts - 1) // parts
+    lo, hi = 0, ntt
+    while lo < hi:
+        mid = (lo + hi) // 2
+        if _cost4(mid, n) >= goal:
+            hi = mid
+        else:
+            lo = mid + 1
+    return lo
+
+
+class CpuSymOperator:
+    """A dense symmetric K standing in for the matrix-free operator's values:
+    this rank's slab rows for the epilogue, its tile share for the product."""
+
+    symmetric = True
+
+    def __init__(self, kfull, row0, rows, rank, world, s=None, shift=0.0):
+        self.kfull, self.n = kfull, int(kfull.shape[0])
+        self.row0, self.rows, self.rank, self.world = int(row0), int(rows), int(rank), int(world)
+        self.s, self.shift = s, float(shift)
+
+    def scaled(self, s, shift):
+        return CpuSymOperator(self.kfull, self.row0, self.rows, self.rank, self.world, s, shift)
+
+
+def _sym_partial(self, op, vfull, t, state=None):
+    if self._done(state):
+        return
+    n = op.n
+    v = vfull[:n]
+    sv = op.s * v if op.s is not None else v
+    t[:n] = 0.0
+    t_lo, t_hi = tile_begin(n, op.world, op.rank), tile_begin(n, op.world, op.rank + 1)
+    for tid in range(t_lo, t_hi):
+        i = _tile_row(tid)
+        j = tid - _row_base(i)
+        ri, rj = slice(i * TB, min(n, i * TB + TB)), slice(j * TB, min(n, j * TB + TB))
+        blk = op.kfull[ri, rj]
+        t[ri] += blk @ sv[rj]
+        if j < i:
+            t[rj] += blk.t() @ sv[ri]
+
+
+def _epilogue(self, mode, op, vfull, b, t, out, part, state=None):
+    if self._done(state):
+        return
+    r0, rows = op.row0, op.rows
+    tr = t[r0:r0 + rows]
+    if op.s is not None:
+        tr = op.s[r0:r0 + rows] * tr
+    ax = op.shift * vfull[r0:r0 + rows] + tr
+    if mode == 0:
+        out[:rows] = ax
+        part[0] = torch.dot(vfull[r0:r0 + rows], ax)
+    else:
+        out[:rows] = b[:rows] - ax
+
+
+CpuShardBackend.sym_partial = _sym_partial
+CpuShardBackend.epilogue = _epilogue

@@ -127,6 +127,70 @@ def test_sharded_solver_world2_matches_reference():
             assert its == max_iters
 
 
+def _sym_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from shard_cpu_backend import CpuShardBackend, CpuSymOperator
+
+        from paper_1706_00241_b200 import SolverConfig
+        from paper_1706_00241_b200.sharded import TorchComm, row_range, sharded_solve
+
+        comm, be = TorchComm(), CpuShardBackend()
+        results = []
+        for seed, n in ((7, 150), (8, 200)):
+            a, b, xprev, _ = _case(seed, n, 0, 50.0)
+            t = lambda v: torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64))
+            r0, rows = row_range(n, world, rank)
+            op = CpuSymOperator(t(a), r0, rows, rank, world)
+            x, rep, _ = sharded_solve(op, t(b[r0:r0 + rows]), t(xprev[r0:r0 + rows]), None,
+                                      SolverConfig(tol=1e-10, ell=6, recompute_residual_every=9), comm, be, poll=2)
+            parts = [torch.zeros(-(-n // world), dtype=torch.float64) for _ in range(world)]
+            pad = torch.zeros(-(-n // world), dtype=torch.float64)
+            pad[:rows] = x
+            dist.all_gather(parts, pad)
+            results.append((torch.cat(parts)[:n].numpy(), rep.iterations))
+        if rank == 0:
+            out.put(results)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_symmetric_sharded_products_world2():
+    """The symmetric sharded product path (each rank a share of the
+    lower-triangle tiles, an all-reduce of K (s (.) p), the slab epilogue)
+    through sharded_solve over gloo, world 2, against the reference CG; the
+    true-residual path uses the same product."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sym_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for (seed, n), (x, its) in zip(((7, 150), (8, 200)), results):
+        a, b, xprev, _ = _case(seed, n, 0, 50.0)
+        xr, rep, _ = O.cg_solve(a, b, xprev, O.Cfg(tol=1e-10, ell=6, recompute_residual_every=9), be="numpy")
+        assert abs(its - rep.iterations) <= 1, (n, its, rep.iterations)
+        assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
+
+
+def test_tile_share_partition_matches_device_rule():
+    """The CPU restatement of the tile-share partition covers every tile once."""
+    from shard_cpu_backend import _side, tile_begin
+
+    for n in (1, 63, 64, 150, 1000, 5000):
+        ntt = _side(n) * (_side(n) + 1) // 2
+        for world in (1, 2, 3, 8):
+            cuts = [tile_begin(n, world, b) for b in range(world + 1)]
+            assert cuts[0] == 0 and cuts[-1] == ntt
+            assert all(c0 <= c1 for c0, c1 in zip(cuts, cuts[1:]))
+
+
 def test_row_partition_covers_rows():
     from paper_1706_00241_b200.sharded import row_block, row_range
 
