@@ -180,6 +180,10 @@ __global__ void fg_reduce_kernel(const double* part, int nparts, const DevStatus
 
 // ---------------------------------------------------------------------------- E5
 // ||Zs u_j||^2 partials for the selected vectors; the last CTA scales U.
+// Rows are staged EX_ROWS at a time into shared memory with coalesced loads
+// (a lane's dependent FMA chain over the Tk columns then reads shared memory:
+// with the global loads inside the chain, in-order issue serialised one L2
+// round trip per column -- 1.3 ms per call at n = 50k, T = 68).
 __global__ void __launch_bounds__(EX_NT)
     uscale_kernel(long long n, int k, const double* __restrict__ Zs, const DevStatus* plan, const DevStatus* pencil,
                   double* U, const int* active, double* Uexp, double* part, unsigned int* counter) {
@@ -187,23 +191,29 @@ __global__ void __launch_bounds__(EX_NT)
     extern __shared__ double sm[];
     const int Tk = (int)plan->count, na = (int)pencil->count;
     double* ue = sm;                       // Tk x k
-    double* wp = sm + Tk * k;              // 8 warps x 64
+    double* wp = ue + Tk * k;              // 8 warps x 64
+    double* zr = wp + 8 * 64;              // EX_ROWS x Tk staged rows
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int e = tid; e < Tk * k; e += EX_NT) ue[e] = 0.0;
     cta_sync();
     for (int e = tid; e < na * k; e += EX_NT) ue[active[e / k] * k + e % k] = U[e];
-    cta_sync();
     const long long r0 = part_begin(n, gridDim.x, blockIdx.x), r1 = part_begin(n, gridDim.x, blockIdx.x + 1);
     double s0 = 0.0, s1 = 0.0;   // lanes own columns lane, lane + 32
-    for (long long i = r0 + warp; i < r1; i += EX_NT / 32) {
-        double v0 = 0.0, v1 = 0.0;
-        for (int c = 0; c < Tk; ++c) {
-            const double z = Zs[i * Tk + c];
-            if (lane < k) v0 = fma(z, ue[c * k + lane], v0);
-            if (lane + 32 < k) v1 = fma(z, ue[c * k + lane + 32], v1);
+    for (long long i0 = r0; i0 < r1; i0 += EX_ROWS) {
+        const int nr = (int)min((long long)EX_ROWS, r1 - i0);
+        cta_sync();
+        for (int e = tid; e < nr * Tk; e += EX_NT) zr[e] = Zs[i0 * Tk + e];
+        cta_sync();
+        for (int rr = warp; rr < nr; rr += EX_NT / 32) {
+            const double* z = zr + rr * Tk;
+            double v0 = 0.0, v1 = 0.0;
+            for (int c = 0; c < Tk; ++c) {
+                if (lane < k) v0 = fma(z[c], ue[c * k + lane], v0);
+                if (lane + 32 < k) v1 = fma(z[c], ue[c * k + lane + 32], v1);
+            }
+            s0 = fma(v0, v0, s0);
+            s1 = fma(v1, v1, s1);
         }
-        s0 = fma(v0, v0, s0);
-        s1 = fma(v1, v1, s1);
     }
     wp[warp * 64 + lane] = s0;
     wp[warp * 64 + lane + 32] = s1;
@@ -236,6 +246,9 @@ __global__ void __launch_bounds__(EX_NT)
 // ---------------------------------------------------------------------------- E6
 // W_next = Zs U, AW_next = AZs U with the reference's accumulation order
 // (_core.gemm i-k-j, recycle.py:157-158); z output = the surviving columns.
+// A CTA takes EX_ROWS rows at a time: Zs / AZs rows staged coalesced into
+// shared memory, then every thread runs (EX_ROWS k / EX_NT) independent
+// column chains from there.
 __global__ void __launch_bounds__(EX_NT)
     wnext_kernel(long long n, int k, const double* __restrict__ Zs, const double* __restrict__ AZs,
                  const DevStatus* plan, const DevStatus* pencil, const double* __restrict__ Uexp, const int* active,
@@ -256,21 +269,33 @@ __global__ void __launch_bounds__(EX_NT)
     if (!ok) return;
     extern __shared__ double sm[];
     const int Tk = (int)plan->count, na = (int)pencil->count;
-    double* ue = sm;   // Tk x k
+    double* ue = sm;                   // Tk x k
+    double* zr = ue + Tk * k;          // EX_ROWS x Tk
+    double* ar = zr + EX_ROWS * Tk;    // EX_ROWS x Tk
     for (int e = threadIdx.x; e < Tk * k; e += EX_NT) ue[e] = Uexp[e];
-    cta_sync();
-    const long long total = n * k;
-    for (long long e = blockIdx.x * (long long)EX_NT + threadIdx.x; e < total; e += (long long)gridDim.x * EX_NT) {
-        const long long i = e / k;
-        const int j = (int)(e % k);
-        double a = 0.0, b = 0.0;
-        for (int c = 0; c < Tk; ++c) {
-            const double u = ue[c * k + j];
-            a = add_rn(a, mul_rn(Zs[i * Tk + c], u));
-            b = add_rn(b, mul_rn(AZs[i * Tk + c], u));
+    const long long nblk = (n + EX_ROWS - 1) / EX_ROWS;
+    for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const long long i0 = blk * EX_ROWS;
+        const int nr = (int)min((long long)EX_ROWS, n - i0);
+        cta_sync();
+        for (int e = threadIdx.x; e < nr * Tk; e += EX_NT) {
+            zr[e] = Zs[i0 * Tk + e];
+            ar[e] = AZs[i0 * Tk + e];
         }
-        w_next[e] = a;
-        aw_next[e] = b;
+        cta_sync();
+        for (int e = threadIdx.x; e < nr * k; e += EX_NT) {
+            const int rr = e / k, j = e - (e / k) * k;
+            const double* z = zr + rr * Tk;
+            const double* az = ar + rr * Tk;
+            double a = 0.0, b = 0.0;
+            for (int c = 0; c < Tk; ++c) {
+                const double u = ue[c * k + j];
+                a = add_rn(a, mul_rn(z[c], u));
+                b = add_rn(b, mul_rn(az[c], u));
+            }
+            w_next[(i0 + rr) * k + j] = a;
+            aw_next[(i0 + rr) * k + j] = b;
+        }
     }
     if (z_out) {
         const long long tz = n * na;
@@ -352,11 +377,11 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
     rc = dcg_ritz_pencil_launch(st, Fraw, Graw, (int)T, (int)k, selection == DCG_SELECT_LARGEST, 60, wk, d_theta, U,
                                 active, pencil, plan);
     if (rc) return rc;
-    const size_t sm5 = sizeof(double) * ((size_t)T * k + 8 * 64);
+    const size_t sm5 = sizeof(double) * ((size_t)T * k + 8 * 64 + (size_t)EX_ROWS * T);
     DCG_CUDA(cudaFuncSetAttribute(uscale_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm5));
     uscale_kernel<<<nb, EX_NT, sm5, st>>>(n, (int)k, Zs, plan, pencil, U, active, Uexp, upart, counters + 1);
     DCG_LAUNCHED();
-    const size_t sm6 = sizeof(double) * (size_t)T * k;
+    const size_t sm6 = sizeof(double) * ((size_t)T * k + 2 * (size_t)EX_ROWS * T);
     DCG_CUDA(cudaFuncSetAttribute(wnext_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm6));
     wnext_kernel<<<G * 2, EX_NT, sm6, st>>>(n, (int)k, Zs, AZs, plan, pencil, Uexp, active, d_w_next, d_aw_next,
                                             d_z, d_result);

@@ -27,15 +27,17 @@ def main():
 
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 10000
     out = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/timeline.json"
-    x, y = gpc_inputs(n, 10, 0)
-    gram = P.rbf_kernel(torch.from_numpy(x).cuda(), P.KernelParams(1.0, 1.5))
+    # config 2 (n = 10k: d 10, l 1.5, k 16) or config 3 (n = 50k: d 8, l 2, k 32)
+    d, ell, k = (8, 2.0, 32) if n >= 50000 else (10, 1.5, 16)
+    x, y = gpc_inputs(n, d, 0)
+    gram = P.rbf_kernel(torch.from_numpy(x).cuda(), P.KernelParams(1.0, ell))
     yd = torch.from_numpy(y).cuda()
-    cfg = P.SolverConfig(tol=1e-8, ell=20)
+    cfg = P.SolverConfig(tol=1e-8, ell=k + 4)
 
     def run():
-        return P.laplace_newton(gram, yd, "defcg", cfg, newton_tol=-np.inf, max_newton=8, k=16, selection="largest")
+        return P.laplace_newton(gram, yd, "defcg", cfg, newton_tol=-np.inf, max_newton=8, k=k, selection="largest")
 
-    for _ in range(3):
+    for _ in range(1 if n >= 50000 else 3):
         run()
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
