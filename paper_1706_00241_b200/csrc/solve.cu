@@ -538,6 +538,12 @@ extern "C" __attribute__((visibility("default"))) int dcg_debug_phase_timers(uns
     DCG_CUDA(cudaMemcpy(out16, g_phase_timers, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     return DCG_OK;
 }
+// ... and the per-CTA pass-1 / pass-2 accumulators (slots 16 .. 16 + 2 G)
+extern "C" __attribute__((visibility("default"))) int dcg_debug_phase_timers_all(unsigned long long* out, int nslots) {
+    if (!g_phase_timers || !out || nslots < 0 || nslots > 1024) return DCG_E_CONFIG;
+    DCG_CUDA(cudaMemcpy(out, g_phase_timers, (size_t)nslots * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    return DCG_OK;
+}
 
 static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, const double* d_b,
                       const double* d_x0, const dcg_basis* basis, const dcg_solver_config* cfg, double* d_x,
