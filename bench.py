@@ -551,7 +551,7 @@ def run_native_sharded(args, rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8d recipe)",
         "config": workload(args) | {"parallelism": f"row-shards x{world} (NCCL all-gather p + all-reduce scalars)"},
         "iterations_per_sequence": its_list, "sequence_ms": ms_per_step,
-        "roofline": roofline, "matvec_roofline": matvec, "matvec_in_solve": matvec_in_solve, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+        "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
