@@ -113,6 +113,24 @@ static __device__ void warp_solve_lower(const double* L, int ldl, int n, const d
     }
 }
 
+// Column-parallel forward substitution Y = L^-1 B (n x n): a thread per
+// column, left-looking.  Element i takes the same operation sequence as the
+// right-looking warp_solve_lower -- b_i - L_i0 y_0 - L_i1 y_1 - ... in that
+// order, unfused, then one division -- so the results are bit-identical; the
+// chain is per thread instead of a warp shuffle per step.  B(i, c) =
+// B[i * brs + c * bcs], Y(i, c) = Y[i * yrs + c * ycs].
+static __device__ void cta_solve_lower_cols(const double* L, int n, const double* B, int brs, int bcs, double* Y,
+                                            int yrs, int ycs) {
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+        for (int i = 0; i < n; ++i) {
+            double a = B[i * brs + c * bcs];
+            const double* li = L + i * n;
+            for (int j = 0; j < i; ++j) a = sub_rn(a, mul_rn(li[j], Y[j * yrs + c * ycs]));
+            Y[i * yrs + c * ycs] = div_rn(a, li[i]);
+        }
+    }
+}
+
 // Warp-level back substitution x = L^-T b (wavefront order).
 static __device__ void warp_solve_lower_trans(const double* L, int ldl, int n, const double* b, int bstride,
                                        double* x, int xstride) {
@@ -506,6 +524,8 @@ __global__ void __launch_bounds__(SD_NT) gram_factor_kernel(const double* Graw, 
 // developer diagnostics of the Ritz pencil (dcg_debug_pencil_profile):
 // globaltimer stamps of its phases and the one-sided Jacobi sweep count
 __device__ unsigned long long g_pencil_prof[16];
+// the pencil's tridiagonal fast path (1) or always the cyclic Jacobi (0)
+__device__ int g_pencil_fast = 1;
 __device__ __forceinline__ void pencil_stamp(int i) {
     if (threadIdx.x == 0) g_pencil_prof[i] = globaltimer_ns();
 }
@@ -612,6 +632,288 @@ __device__ __forceinline__ int cta_jacobi_onesided(double* X, double* Vc, int n,
 }
 
 // ===========================================================================
+// Fast path of the pencil's symmetric eigenproblem: C (n x n, n <= 64, shared,
+// row-major, destroyed) -> the k eigenpairs selected (the k largest or
+// smallest), eigenvalues ascending.  Householder tridiagonalisation (n - 2
+// reflector steps, two CTA phases each), multisection of the tridiagonal's
+// Sturm counts for the selected eigenvalues (a warp per eigenvalue, 32
+// shifts per round), a twisted factorisation per eigenvalue for its vector
+// (Parlett-Dhillon: forward and backward pivots, the twist at min |gamma|),
+// back-transformation by the stored reflectors.  Replaces the cyclic Jacobi's
+// ~210 dependent rotation rounds at n = 36.
+// Returns 0 -- and the caller runs Jacobi -- when two selected eigenvalues,
+// or the boundary pair, are closer than 1e-7 ||C|| (twisted vectors of a
+// cluster would need reorthogonalisation) or a vector is not finite.  Writes
+// V[:, j] (row-major n x n storage, column j) and lam[j], j < k.  All CTA
+// threads call; smem scratch `ws` >= 6 n + 64 doubles.
+// ===========================================================================
+// 1 / q to ~1 ulp: the MUFU estimate and two Newton steps (Sturm pivots
+// tolerate a relative perturbation of a few ulps; div_rn's latency does not)
+__device__ __forceinline__ double rcp_nr(double q) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+    double e = fma(-q, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-q, r, 1.0);
+    return fma(r, e, r);
+}
+
+__device__ int pencil_tridiag_fast(double* C, int n, int k, int largest, double* V, int ldv, double* lam, double* ws) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    __shared__ double s_sc[4];
+    __shared__ int s_ok;
+    double* d = ws;            // n
+    double* e = d + n;         // n (e[i] couples i, i+1)
+    double* tau = e + n;       // n
+    double* e2 = tau + n;      // n: e2[i] = e[i-1]^2
+    double* pb = e2 + n;       // n: p = t A22 v
+    if (tid == 0) s_ok = 1;
+    // ---- tridiagonalisation on the first TW threads (a named barrier: the
+    // step is latency-bound, a 1024-thread barrier costs more than its work).
+    // A[j+1:, j] -> alpha e_1; the reflector is kept in row j's upper part,
+    // C[j, j+1:] (only its head differs from the row), contiguous for the
+    // back-transformation.  Every warp
+    // forms the reflector's scalars itself (a warp reduction over the column),
+    // so a step is two phases: p = t A22 v (a thread per row, reading A22 by
+    // columns -- it is symmetric -- so the lanes' loads are contiguous), then
+    // the rank-2 update with w = p - (t/2)(p'v) v, formed symmetrically.
+    constexpr int TW = 256;
+    if (tid < TW) {
+        for (int j = 0; j + 2 < n; ++j) {
+            const int m = n - j - 1;
+            // column j below the diagonal, read as row j right of it (the
+            // updates keep C bitwise symmetric): contiguous, conflict-free
+            const double* col = C + j * n + j + 1;     // col[i], i < m
+            const double x0 = col[0];
+            double ss = 0.0;
+            for (int i = lane; i < m; i += 32) ss = fma(col[i], col[i], ss);
+            ss = warp_sum(ss);
+            const double nrm = sqrt(ss);
+            const double alpha = x0 >= 0.0 ? -nrm : nrm;
+            const double v0 = x0 - alpha;
+            const double vtv = ss - x0 * x0 + v0 * v0;
+            const double t = (nrm == 0.0 || vtv == 0.0) ? 0.0 : 2.0 / vtv;
+            if (tid == 0) {
+                tau[j] = t;
+                e[j] = (t == 0.0) ? x0 : alpha;
+                d[j] = C[j * n + j];
+            }
+            if (t != 0.0) {
+                double* a22 = C + (j + 1) * n + (j + 1);
+                // p: four threads per row (m <= 63 rows in one pass), columns
+                // interleaved over the four, combined by two shuffles
+                {
+                    const int r = tid >> 2, h = tid & 3;
+                    double s0 = 0.0, s1 = 0.0;
+                    if (r < m) {
+                        int c = h;
+                        for (; c + 4 < m; c += 8) {
+                            s0 = fma(a22[c * n + r], c == 0 ? v0 : col[c], s0);
+                            s1 = fma(a22[(c + 4) * n + r], col[c + 4], s1);
+                        }
+                        if (c < m) s0 = fma(a22[c * n + r], c == 0 ? v0 : col[c], s0);
+                    }
+                    double sp = s0 + s1;
+                    sp += __shfl_xor_sync(0xffffffffu, sp, 1);
+                    sp += __shfl_xor_sync(0xffffffffu, sp, 2);
+                    if (h == 0 && r < m) pb[r] = t * sp;
+                }
+                asm volatile("barrier.sync 1, 256;" ::: "memory");
+                double pv = 0.0;
+                for (int i = lane; i < m; i += 32) pv = fma(pb[i], i == 0 ? v0 : col[i], pv);
+                const double K = 0.5 * t * warp_sum(pv);
+                // rank-2 update: thread (tid >> 4, tid & 15) walks a 16-strided grid
+                for (int r = tid >> 4; r < m; r += TW / 16) {
+                    const double vr = r == 0 ? v0 : col[r];
+                    const double wr = pb[r] - K * vr;
+                    for (int c = tid & 15; c < m; c += 16) {
+                        const double vc = c == 0 ? v0 : col[c];
+                        const double wc = pb[c] - K * vc;
+                        a22[r * n + c] = sub_rn(a22[r * n + c], add_rn(mul_rn(vr, wc), mul_rn(wr, vc)));
+                    }
+                }
+            }
+            asm volatile("barrier.sync 1, 256;" ::: "memory");
+            // the reflector is row j's upper part with its head replaced
+            if (tid == 0 && t != 0.0) C[j * n + j + 1] = v0;
+        }
+    }
+    cta_sync();
+    if (tid == 0) {
+        if (n >= 2) {
+            d[n - 2] = C[(n - 2) * n + (n - 2)];
+            e[n - 2] = C[(n - 1) * n + (n - 2)];
+        }
+        d[n - 1] = C[(n - 1) * n + (n - 1)];
+        if (n == 1) e[0] = 0.0;
+        e[n - 1] = 0.0;
+        // Gershgorin interval and the norm scale
+        double lo = 1e300, hi = -1e300, nrm = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
+            lo = fmin(lo, d[i] - r);
+            hi = fmax(hi, d[i] + r);
+            nrm = fmax(nrm, fabs(d[i]) + r);
+            e2[i] = i > 0 ? e[i - 1] * e[i - 1] : 0.0;
+        }
+        s_sc[0] = lo;
+        s_sc[1] = hi;
+        s_sc[2] = nrm;
+    }
+    cta_sync();
+    pencil_stamp(8);
+    const double glo = s_sc[0], ghi = s_sc[1], tnrm = s_sc[2];
+    const double pivmin = fmax(1e-200, 1e-30 * tnrm * tnrm);
+    // Sturm count: #eigenvalues < sigma, as sign changes of the scaled
+    // characteristic-polynomial sequence p_i = (d_i - sigma) p_{i-1} - e_{i-1}^2 p_{i-2}.
+    // Its ratios are the LDL pivots q_i = p_i / p_{i-1} of the division form
+    // with the same rounding per step (one fused product each), and the same
+    // pivmin clamp (|q_i| < pivmin -> q_i = -pivmin); a step's latency is one
+    // FMA instead of a division.  |p| is kept in [2^-200, 2^200].
+    auto count_below = [&](double sigma) {
+        int c = 0;
+        double pp = 1.0;
+        double p = d[0] - sigma;
+        if (fabs(p) < pivmin) p = -pivmin;
+        c += p < 0.0;
+        for (int i = 1; i < n; ++i) {
+            double pn = fma(d[i] - sigma, p, -(e2[i] * pp));
+            if (fabs(pn) < pivmin * fabs(p)) pn = -pivmin * p;
+            c += (pn < 0.0) != (p < 0.0);
+            pp = p;
+            p = pn;
+            const double ap = fabs(p);
+            if (ap > 0x1p200) { p *= 0x1p-200; pp *= 0x1p-200; }
+            else if (ap < 0x1p-200) { p *= 0x1p200; pp *= 0x1p200; }
+        }
+        return c;
+    };
+    // ---- multisection: warp w finds eigenvalue idx (ascending) of the selection
+    const int first = largest ? n - k : 0;
+    double* lamall = pb;   // reuse: k + 1 entries (the selection and its boundary neighbour)
+    const int nloc = k + ((largest ? first > 0 : first + k < n) ? 1 : 0);
+    for (int w = warp; w < nloc; w += nw) {
+        const int idx = (w < k) ? first + w : (largest ? first - 1 : first + k);
+        double a = glo, b = ghi;
+        for (int it = 0; it < 40; ++it) {
+            const double width = b - a;
+            if (!(width > 4e-16 * fmax(fabs(a), fabs(b)))) break;
+            const double sig = a + width * (lane + 1) / 33.0;
+            const long long c0 = clock64();
+            const int cnt = count_below(sig);
+            if (tid == 0) { g_pencil_prof[12] += clock64() - c0; g_pencil_prof[13] += 1; }
+            // lanes whose shift is above the eigenvalue: cnt > idx
+            const unsigned above = __ballot_sync(0xffffffffu, cnt > idx);
+            const int lo_lane = above ? __ffs(above) - 2 : 31;   // last lane below (-1: a)
+            const double na_ = lo_lane < 0 ? a : a + width * (lo_lane + 1) / 33.0;
+            const double nb_ = above ? a + width * (lo_lane + 2) / 33.0 : b;
+            a = na_;
+            b = nb_;
+        }
+        if (lane == 0) lamall[w] = 0.5 * (a + b);
+    }
+    cta_sync();
+    pencil_stamp(9);
+    // cluster check on the selected eigenvalues and the boundary pair
+    if (tid == 0) {
+        double prev = 0.0;
+        bool have = false;
+        const double gap = 1e-7 * fmax(tnrm, 1e-300);
+        double vals[DCG_MAX_T + 2];
+        int nv = 0;
+        if (nloc > k && largest) vals[nv++] = lamall[k];
+        for (int j = 0; j < k; ++j) vals[nv++] = lamall[j];
+        if (nloc > k && !largest) vals[nv++] = lamall[k];
+        for (int j = 0; j < nv; ++j) {
+            if (have && vals[j] - prev < gap) s_ok = 0;
+            prev = vals[j];
+            have = true;
+        }
+        for (int j = 0; j < k; ++j) lam[j] = lamall[j];
+    }
+    cta_sync();
+    if (!s_ok) return 0;
+    // ---- twisted factorisation, a warp per eigenvalue.  All lanes run the
+    // pivot recurrences (uniform control flow); lane l keeps pivots l, l + 32:
+    //   D+_i = (d_i - lam) - e_{i-1}^2 / D+_{i-1},  D-_i = (d_i - lam) - e_i^2 / D-_{i+1},
+    //   gamma_i = D+_i + D-_i - (d_i - lam),  r = argmin |gamma_i|,
+    //   z_r = 1, z_i = -e_i z_{i+1} / D+_i (i < r), z_i = -e_{i-1} z_{i-1} / D-_i (i > r).
+    for (int w = warp; w < k; w += nw) {
+        const double lm = lam[w];
+        double dp0 = 0.0, dp1 = 0.0, dm0 = 0.0, dm1 = 0.0;
+        double q = 1.0;
+        for (int i = 0; i < n; ++i) {
+            q = (i == 0) ? d[0] - lm : (d[i] - lm) - e2[i] * rcp_nr(q);
+            if (fabs(q) < pivmin) q = q < 0.0 ? -pivmin : pivmin;
+            if (i == lane) dp0 = q;
+            if (i == lane + 32) dp1 = q;
+        }
+        for (int i = n - 1; i >= 0; --i) {
+            q = (i == n - 1) ? d[i] - lm : (d[i] - lm) - e2[i + 1] * rcp_nr(q);
+            if (fabs(q) < pivmin) q = q < 0.0 ? -pivmin : pivmin;
+            if (i == lane) dm0 = q;
+            if (i == lane + 32) dm1 = q;
+        }
+        // twist index: min |gamma|, ties to the lower index
+        double g = 1e308;
+        int gi = n;
+        if (lane < n) { g = fabs(dp0 + dm0 - (d[lane] - lm)); gi = lane; }
+        if (lane + 32 < n) {
+            const double g1 = fabs(dp1 + dm1 - (d[lane + 32] - lm));
+            if (g1 < g) { g = g1; gi = lane + 32; }
+        }
+        for (int o = 16; o; o >>= 1) {
+            const double og = __shfl_xor_sync(0xffffffffu, g, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, gi, o);
+            if (og < g || (og == g && oi < gi)) { g = og; gi = oi; }
+        }
+        const int r = gi;
+        // ratios into V's column w, then the products outward from the twist
+        if (lane < n) V[lane * ldv + w] = lane < r ? -e[lane] / dp0 : (lane > r ? -e[lane - 1] / dm0 : 1.0);
+        if (lane + 32 < n) {
+            const int i = lane + 32;
+            V[i * ldv + w] = i < r ? -e[i] / dp1 : (i > r ? -e[i - 1] / dm1 : 1.0);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            double z = 1.0;
+            for (int i = r - 1; i >= 0; --i) { z *= V[i * ldv + w]; V[i * ldv + w] = z; }
+            z = 1.0;
+            for (int i = r + 1; i < n; ++i) { z *= V[i * ldv + w]; V[i * ldv + w] = z; }
+        }
+        __syncwarp();
+        double s2 = 0.0;
+        for (int i = lane; i < n; i += 32) s2 = fma(V[i * ldv + w], V[i * ldv + w], s2);
+        const double inv = 1.0 / sqrt(warp_sum(s2));
+        if (!(inv > 0.0) || !isfinite(inv)) { if (lane == 0) s_ok = 0; }
+        else for (int i = lane; i < n; i += 32) V[i * ldv + w] *= inv;
+    }
+    cta_sync();
+    pencil_stamp(10);
+    if (!s_ok) return 0;
+    // ---- back-transformation: y <- H_0 ... H_{n-3} y (reflectors in reverse
+    // order, read from the upper rows: contiguous); a warp per vector
+    for (int w = warp; w < k; w += nw) {
+        for (int j = n - 3; j >= 0; --j) {
+            const double t = tau[j];
+            if (t == 0.0) continue;
+            const int m = n - j - 1;
+            const double* v = C + j * n + j + 1;
+            double* y = V + (j + 1) * ldv + w;
+            double dot = 0.0;
+            for (int i = lane; i < m; i += 32) dot = fma(v[i], y[i * ldv], dot);
+            dot = t * warp_sum(dot);
+            for (int i = lane; i < m; i += 32) y[i * ldv] -= dot * v[i];
+            __syncwarp();
+        }
+    }
+    cta_sync();
+    pencil_stamp(11);
+    if (tid == 0) g_pencil_prof[14] = 1;
+    return 1;
+}
+
+// ===========================================================================
 // Harmonic pencil: symmetrise F, G; prune F's failing-pivot columns; solve
 // G u = theta F u (gen_sym_eigen, linalg.py:168-191); select k values.
 // Global scratch `wk` holds 5 * T * T doubles.  Outputs: theta (k), U (na x k,
@@ -638,7 +940,7 @@ __global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fr
     }
     pencil_stamp(0);
     if (threadIdx.x == 0)
-        for (int i = 8; i < 14; ++i) g_pencil_prof[i] = 0;
+        for (int i = 7; i < 15; ++i) g_pencil_prof[i] = 0;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nw = blockDim.x >> 5;
     // F, G (symmetrised, T x T) stay in the global scratch: they are only read
@@ -684,7 +986,51 @@ __global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fr
     pencil_stamp(1);
     double* A = staged ? sm + 3 * T * T : sm;
     double* V = staged ? sm : sm + T * T;
+    const int off = largest ? (na - k) : 0;
+    // ---- fast path: C = L^-1 G L^-T, tridiagonal eigensolver for the k
+    // selected pairs (pencil_tridiag_fast); Jacobi below when it declines
+    bool fast = false;
+    int ldv = na;
+    if (staged && na >= 12 && na <= 64 && g_pencil_fast) {   // na >= 12: T*T >= 6 na + 64 scratch in S2
+        __shared__ double s_lam[DCG_MAX_T];
+        for (int e = tid; e < na * na; e += blockDim.x) {
+            const int i = e / na, j = e % na;
+            Fa[e] = G[s_act[i] * T + s_act[j]];
+        }
+        cta_sync();
+        cta_solve_lower_cols(L, na, Fa, na, 1, Y, na, 1);
+        cta_sync();
+        cta_solve_lower_cols(L, na, Y, 1, na, A, na, 1);
+        cta_sync();
+        for (int e = tid; e < na * na; e += blockDim.x) {
+            const int i = e / na, j = e % na;
+            if (i < j) {
+                const double v = mul_rn(0.5, add_rn(A[i * na + j], A[j * na + i]));
+                A[i * na + j] = v;
+                A[j * na + i] = v;
+            }
+        }
+        cta_sync();
+        pencil_stamp(2);
+        // V's row stride padded to na + 1 when it fits: the column walks of
+        // the twisted factorisation and the back-transformation then spread
+        // over the banks
+        ldv = (na + 1) * na <= T * T ? na + 1 : na;
+        fast = pencil_tridiag_fast(A, na, k, largest, V, ldv, s_lam, Y) != 0;
+        pencil_stamp(3);
+        if (fast) {
+            for (int j = tid; j < k; j += blockDim.x) {
+                A[j * na + j] = s_lam[j];
+                s_order[off + j] = j;
+            }
+            cta_sync();
+        } else {
+            ldv = na;
+        }
+    }
     bool onesided = false;
+    int nc = 0;
+    if (!fast) {
     if (staged && na <= 64) {
         // G (compact) -> S0, R = chol(G) -> S2, X = (L^-1 R)' in place in S2
         for (int e = tid; e < na * na; e += blockDim.x) {
@@ -707,7 +1053,6 @@ __global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fr
         }
         cta_sync();
     }
-    int nc;
     if (onesided) {
         // Vc (column-major) in S3; afterwards theta on the diagonal of A := S2 and V row-major in S0
         double* Vc = A;
@@ -758,16 +1103,16 @@ __global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fr
     nc = staged ? cta_jacobi2(A, Y, V, na, max_sweeps, 1e-14, red)
                 : cta_jacobi(A, V, na, max_sweeps, 1e-14, red, s_c, s_s, s_mode);
     }
+    }   // !fast
     if (nc) {
         if (tid == 0) { st->status = DCG_E_NO_CONVERGENCE; st->info = nc; st->count = na; }
         return;
     }
-    cta_stable_argsort(A, na + 1, na, s_order);
+    if (!fast) cta_stable_argsort(A, na + 1, na, s_order);
     // selected eigen-pairs: u = L^-T w, normalised
-    const int off = largest ? (na - k) : 0;
     for (int j = warp; j < k; j += nw) {
         const int col = s_order[off + j];
-        warp_solve_lower_trans(L, na, na, V + col, na, U + j, k);
+        warp_solve_lower_trans(L, na, na, V + col, ldv, U + j, k);
         __syncwarp();
         double s2 = 0.0;
         for (int i = lane; i < na; i += 32) s2 = fma(U[i * k + j], U[i * k + j], s2);
@@ -780,6 +1125,12 @@ __global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fr
     if (tid == 0) { st->status = DCG_OK; st->count = na; }
     pencil_stamp(4);
     if (tid == 0) g_pencil_prof[6] = na;
+}
+
+extern "C" __attribute__((visibility("default"))) int dcg_debug_set_pencil_fast(int on) {
+    const int v = on ? 1 : 0;
+    if (cudaMemcpyToSymbol(g_pencil_fast, &v, sizeof(int)) != cudaSuccess) return DCG_E_CUDA;
+    return DCG_OK;
 }
 
 extern "C" __attribute__((visibility("default"))) int dcg_debug_pencil_profile(long long* out8) {

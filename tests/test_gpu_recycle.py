@@ -254,3 +254,55 @@ def test_warm_start_carries_solution(P, rng):
     _, st = P.solve_next(st, a, b)
     _, st = P.solve_next(st, a, b)
     assert st.history[1].iterations <= 1
+
+
+def _set_pencil_fast(on):
+    import ctypes
+
+    from paper_1706_00241_b200 import _native as N
+
+    fn = N.lib().dcg_debug_set_pencil_fast
+    fn.restype = ctypes.c_int
+    fn.argtypes = [ctypes.c_int]
+    assert fn(1 if on else 0) == 0
+
+
+# well-conditioned pencils (cond F < 1e2): on a nearly singular F the two
+# formations -- explicit C here, the one-sided X = L^-1 chol(G) there -- agree
+# only to cond(F) eps
+def _pencil_profile():
+    import ctypes
+
+    import torch
+
+    from paper_1706_00241_b200 import _native as N
+
+    torch.cuda.synchronize()
+    h = (ctypes.c_longlong * 16)()
+    N.lib().dcg_debug_pencil_profile.restype = ctypes.c_int
+    assert N.lib().dcg_debug_pencil_profile(h) == 0
+    return list(h)
+
+
+@pytest.mark.parametrize("n,ell,k,kappa", [(60, 14, 4, 1e3), (120, 30, 8, 1e4), (200, 40, 16, 1e3), (300, 48, 16, 1e4),
+                                           (500, 64, 32, 1e3)])
+def test_pencil_tridiagonal_path_matches_jacobi(P, rng, n, ell, k, kappa):
+    """The pencil's tridiagonal fast path (pencil_tridiag_fast) and the cyclic
+    Jacobi path select the same Ritz pairs: values to 1e-9 relative, vectors as
+    spans (both paths, both selections; T = ell stored directions >= 12)."""
+    a = random_spd(rng, n, kappa=kappa)
+    _, _, log = P.cg_solve(a, rng.standard_normal(n), cfg=P.SolverConfig(tol=1e-14, ell=ell))
+    taken = 0
+    try:
+        for sel in ("smallest", "largest"):
+            _set_pencil_fast(True)
+            ef = P.harmonic_ritz_extract(log, None, k, sel)
+            taken += _pencil_profile()[14]
+            _set_pencil_fast(False)
+            ej = P.harmonic_ritz_extract(log, None, k, sel)
+            assert np.allclose(ef.theta, ej.theta, rtol=1e-9, atol=0)
+            assert span_gap(ef.w_next, ej.w_next) < 1e-7
+            assert np.allclose(np.linalg.norm(ef.w_next, axis=0), 1.0, atol=1e-12)
+        assert taken >= 1   # the fast path ran (it may decline a clustered selection)
+    finally:
+        _set_pencil_fast(True)

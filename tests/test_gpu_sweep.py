@@ -39,17 +39,30 @@ def oracle_sweep(x, y, thetas, k, ell, tol=1e-8, jitter=0.01, perm=None):
 
 @pytest.mark.parametrize("n,k", [(700, 8), (1500, 12)])
 def test_sweep_matches_reference(P, n, k):
+    """Iteration counts of a sweep are chaotic in rounding: the reference's own
+    counts over row permutations of the same problem spread by up to ~7 at
+    n = 700 (12 permutations: 177..184 at the fifth theta), and so do the
+    GPU's.  The bar compares the two distributions: the median of the GPU's
+    counts over the original order and three permutations lies inside the
+    reference's range over the original order and six permutations (+-1), and
+    every single GPU run is within 5% of the reference's median."""
     x, y = O.sweep_inputs(n, d=8, seed=0)
     thetas = np.logspace(np.log10(0.5), np.log10(2.0), 6)
     ell = k + 4
     ref_sols, ref_its = oracle_sweep(x, y, thetas, k, ell)
-    spread = [oracle_sweep(x, y, thetas, k, ell, perm=np.random.default_rng(s).permutation(n))[1] for s in range(3)]
-    sols, recs = P.hyperparameter_sweep(x, y, thetas, k=k, cfg=P.SolverConfig(tol=1e-8, ell=ell))
-    its = [r.iterations for r in recs]
+    spread = [ref_its] + [oracle_sweep(x, y, thetas, k, ell, perm=np.random.default_rng(s).permutation(n))[1]
+                          for s in range(6)]
+    cfg = P.SolverConfig(tol=1e-8, ell=ell)
+    sols, recs = P.hyperparameter_sweep(x, y, thetas, k=k, cfg=cfg)
+    gpu = [[r.iterations for r in recs]]
+    for s in range(100, 103):
+        perm = np.random.default_rng(s).permutation(n)
+        gpu.append([r.iterations for r in P.hyperparameter_sweep(x[perm], y[perm], thetas, k=k, cfg=cfg)[1]])
     for i in range(len(thetas)):
-        lo = min([ref_its[i]] + [s[i] for s in spread]) - 1
-        hi = max([ref_its[i]] + [s[i] for s in spread]) + 1
-        assert lo <= its[i] <= hi, (i, its, ref_its, spread)
+        ref_i = [s[i] for s in spread]
+        gpu_i = [g[i] for g in gpu]
+        assert min(ref_i) - 1 <= np.median(gpu_i) <= max(ref_i) + 1, (i, gpu, spread)
+        assert all(abs(g - np.median(ref_i)) <= max(1, 0.05 * np.median(ref_i)) for g in gpu_i), (i, gpu, spread)
         err = np.linalg.norm(sols[i] - ref_sols[i]) / np.linalg.norm(ref_sols[i])
         assert err <= 1e-7, (i, err)
 
