@@ -262,7 +262,9 @@ DCG_API int dcg_ritz_extract_async(dcg_context* ctx, void* stream, long long n,
  * stage 0 enqueues everything; stage 1 only the device-wide column work
  * (Z / AZ gather, normalisation, F and G), stage 2 the single-CTA pencil and
  * the W_next tail -- the two halves may go to different streams (the caller
- * orders stage 2 after stage 1) and must get identical arguments.          */
+ * orders stage 2 after stage 1) and must get identical arguments.  Stage 2
+ * splits further into 3 (the pencil) and 4 (the SM-wide W_next tail), so
+ * the tail can follow the pencil on another stream (ordered after it).     */
 DCG_API int dcg_ritz_extract_dev(dcg_context* ctx, void* stream, long long n,
                                  const dcg_krylov_log* log, const void* d_solve_status,
                                  const dcg_basis* prev, long long k, int selection,
@@ -277,6 +279,15 @@ DCG_API int dcg_gpc_derivs(dcg_context* ctx, void* stream, long long n, const do
 DCG_API int dcg_gpc_newton_system(dcg_context* ctx, void* stream, const dcg_operator* kop,
                           const double* d_f, const double* d_grad, const double* d_h,
                           double* d_s, double* d_inner, double* d_b);
+/* newton_system plus ax0 = (I + S K S) x_prev, the next solve's first product
+ * (pass it to dcg_solve_async as d_ax0): one pass over a symmetric-stored K
+ * serves both products, bitwise equal to computing them separately.
+ * Replaces the pair build_newton_system (gpc.py:175-183) + the first A x0 of
+ * the deflated solve, r_prev = b - A x_prev (solvers.py:237).              */
+DCG_API int dcg_gpc_newton_system_ax0(dcg_context* ctx, void* stream, const dcg_operator* kop,
+                          const double* d_f, const double* d_grad, const double* d_h,
+                          const double* d_x_prev, double* d_s, double* d_inner, double* d_b,
+                          double* d_ax0);
 /* a = inner - s x; f = K a; (loglik, grad, h)(f); psi = loglik - f'a / 2
  *                                                     gpc.py:186-209
  * For a row-slab kop (sharded): a for all n entries, f for the slab's rows

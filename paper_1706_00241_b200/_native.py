@@ -205,6 +205,7 @@ SIGNATURES = {
     ],
     "dcg_gpc_derivs": [_P, _P, _LL, _P, _P, _P, _P, _PD],
     "dcg_gpc_newton_system": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P, _P, _P],
+    "dcg_gpc_newton_system_ax0": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P, _P, _P, _P, _P],
     "dcg_gpc_newton_update": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P, _P, _P, _P, _P, _PD, _PD],
     "dcg_gpc_objective": [_P, _P, _LL, _P, _P, _P, _P, _P, _PD, _PD],
     "dcg_gpc_newton_update_async": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P, _P, _P, _P, _P, _P],

@@ -21,6 +21,12 @@ extern "C" long long dcg_launch_count(void) { return g_launches.load(std::memory
 int dcg_gemv_launch(dcg_context*, cudaStream_t, const double*, long long, long long, long long, const double*,
                     const double*, const double*, double, const double*, double*);
 size_t dcg_sym_apply_scratch_doubles(long long n);
+size_t dcg_sym_apply2_scratch_doubles(long long n);
+int dcg_sym_apply2(dcg_context*, cudaStream_t, const double*, long long, long long, const double*, const double*,
+                   const double*, const double*, const double*, const double*, double, double, double*, double*,
+                   double*);
+int dcg_newton_prep2_launch(dcg_context*, cudaStream_t, long long, const double*, const double*, const double*,
+                            const double*, double*, double*, double*);
 int dcg_sym_apply(dcg_context*, cudaStream_t, const double*, long long, long long, const double*, const double*,
                   const double*, double, double*, double*);
 size_t dcg_block_apply_scratch_doubles(long long n, long long rows, int k);
@@ -713,6 +719,39 @@ extern "C" int dcg_gpc_newton_system(dcg_context* ctx, void* stream, const dcg_o
     if (rc) return rc;
     // b = s (.) (K inner): K's own scaling/shift are ignored here (K is the kernel matrix)
     return apply_k(ctx, st, kop, d_inner, nullptr, d_s + kop->row0, 0.0, d_b, static_cast<double*>(ctx->ws));
+}
+
+// newton_system plus the next solve's first product, ax0 = A x_prev with
+// A = I + S K S of the new system, from ONE pass over K's lower triangle when
+// K is stored symmetric (sym_pass1<NV = 2>): b and ax0 are bitwise the results
+// of the two separate products (newton_system's K inner, the operator's
+// A x_prev), one K read fewer per Newton step.  Other operators: two products.
+extern "C" int dcg_gpc_newton_system_ax0(dcg_context* ctx, void* stream, const dcg_operator* kop, const double* d_f,
+                                         const double* d_grad, const double* d_h, const double* d_x_prev,
+                                         double* d_s, double* d_inner, double* d_b, double* d_ax0) {
+    if (!ctx || !d_x_prev || !d_ax0) return DCG_E_CONFIG;
+    int rc = check_dense_op(kop);
+    if (rc) return rc;
+    cudaStream_t st = as_stream(stream);
+    const long long n = kop->n;
+    const bool fused = kop->kind == DCG_OP_DENSE_SYM && kop->row0 == 0 && kop->rows == n && aligned16(d_inner);
+    const size_t scr = fused ? dcg_sym_apply2_scratch_doubles(n) : apply_k_scratch(kop);
+    rc = dcg_ws_reserve(ctx, al(sizeof(double) * (size_t)n) + sizeof(double) * scr + 256);
+    if (rc) return rc;
+    Arena ar{static_cast<char*>(ctx->ws), 0};
+    double* xs = ar.take<double>(n);
+    double* scratch = ar.take<double>(scr);
+    if (!fused) {
+        rc = dcg_newton_prep_launch(ctx, st, n, d_f, d_grad, d_h, d_s, d_inner);
+        if (rc) return rc;
+        rc = apply_k(ctx, st, kop, d_inner, nullptr, d_s + kop->row0, 0.0, d_b, scratch);
+        if (rc) return rc;
+        return apply_k(ctx, st, kop, d_x_prev, d_s, d_s + kop->row0, 1.0, d_ax0, scratch);
+    }
+    rc = dcg_newton_prep2_launch(ctx, st, n, d_f, d_grad, d_h, d_x_prev, d_s, d_inner, xs);
+    if (rc) return rc;
+    return dcg_sym_apply2(ctx, st, kop->d_k, kop->ldk, n, d_inner, xs, nullptr, d_x_prev, d_s, d_s, 0.0, 1.0, d_b,
+                          d_ax0, scratch);
 }
 
 // gpc newton_update without host synchronisation: (loglik, psi) go to d_llpsi

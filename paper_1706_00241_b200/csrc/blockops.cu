@@ -130,6 +130,63 @@ int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, long long 
     return DCG_OK;
 }
 
+// Two products over one pass of K's lower triangle (sym_pass1<NV = 2>):
+//   y1 = shift1 v1 + s_out1 (.) K x1,   y2 = shift2 v2 + s_out2 (.) K x2
+// x1, x2 are the (already input-scaled) operands, v1, v2 the shift vectors.
+// Same tile partition, partial layout and pass-2 order as two dcg_sym_apply
+// calls with (v, s_in) such that x = s_in (.) v: bitwise the same results.
+__global__ void __launch_bounds__(DCG_NT, 1)
+    sym_apply2_coop_kernel(const double* __restrict__ K, long long ldk, long long n, const double* x1,
+                           const double* x2, const double* v1, const double* v2, const double* s_out1,
+                           const double* s_out2, double shift1, double shift2, double* colpart, double* rowpart,
+                           long long part2, double* y1, double* y2, unsigned int* bar) {
+    extern __shared__ __align__(16) double smem[];
+    sym_ring_init(smem, n);
+    unsigned int seq = 0;
+    sym_pass1<false, 2>(K, ldk, n, x1, nullptr, colpart, rowpart, smem, seq, x2, part2);
+    dcg_grid_barrier(bar, gridDim.x);
+    const long long q0 = sym_row_begin(n, gridDim.x, blockIdx.x);
+    const long long q1 = sym_row_begin(n, gridDim.x, blockIdx.x + 1);
+    sym_pass2(n, colpart, rowpart, q0, q1, sym_range_table(smem), gridDim.x, smem, [&](long long i, double t) {
+        double val = s_out1 ? mul_rn(s_out1[i], t) : t;
+        if (shift1 != 0.0) val = add_rn(mul_rn(shift1, v1[i]), val);
+        y1[i] = val;
+    });
+    sym_pass2(n, colpart + part2, rowpart + part2, q0, q1, sym_range_table(smem), gridDim.x, smem,
+              [&](long long i, double t) {
+                  double val = s_out2 ? mul_rn(s_out2[i], t) : t;
+                  if (shift2 != 0.0) val = add_rn(mul_rn(shift2, v2[i]), val);
+                  y2[i] = val;
+              });
+}
+
+size_t dcg_sym_apply2_scratch_doubles(long long n) { return 4 * (size_t)sym_ntiles(n) * DCG_TB + 32; }
+
+int dcg_sym_apply2(dcg_context* ctx, cudaStream_t st, const double* K, long long ldk, long long n, const double* x1,
+                   const double* x2, const double* v1, const double* v2, const double* s_out1, const double* s_out2,
+                   double shift1, double shift2, double* y1, double* y2, double* scratch) {
+    if (n <= 0) return DCG_OK;
+    size_t smem = sizeof(double) * (size_t)sym_smem_doubles();
+    if (ctx->smem_optin > smem) smem = ctx->smem_optin;
+    const long long ntt = sym_ntiles(n);
+    double* colpart = scratch;
+    double* rowpart = scratch + ntt * DCG_TB;
+    const long long part2 = 2 * ntt * DCG_TB;
+    // the CTA count of dcg_sym_apply (same partition -> same partials)
+    const int navail = ctx->sm_count > 1 ? ctx->sm_count - 1 : 1;
+    const int G = navail < DCG_SYM_MAX_CTAS ? navail : DCG_SYM_MAX_CTAS;
+    unsigned int* bar = reinterpret_cast<unsigned int*>(scratch + 4 * ntt * DCG_TB);
+    DCG_CUDA(cudaFuncSetAttribute(sym_apply2_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DCG_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), st));
+    void* args[] = {(void*)&K,      (void*)&ldk,    (void*)&n,      (void*)&x1,      (void*)&x2,
+                    (void*)&v1,     (void*)&v2,     (void*)&s_out1, (void*)&s_out2,  (void*)&shift1,
+                    (void*)&shift2, (void*)&colpart, (void*)&rowpart, (void*)&part2, (void*)&y1,
+                    (void*)&y2,     (void*)&bar};
+    DCG_CUDA(cudaLaunchCooperativeKernel((const void*)sym_apply2_coop_kernel, dim3(G), dim3(DCG_NT), args, smem, st));
+    dcg_count_launch();
+    return DCG_OK;
+}
+
 // pass 2 alone (the matrix-free operator's symmetric pass 1 produces the same partials)
 // (R = pass-1 ranges: G x teams)
 int dcg_sym_pass2_launch(cudaStream_t st, int G, int R, long long n, const double* colpart, const double* rowpart,

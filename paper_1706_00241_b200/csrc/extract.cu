@@ -102,7 +102,13 @@ __global__ void __launch_bounds__(EX_NT)
 }
 
 // ---------------------------------------------------------------------------- E2
-#define FG_PPT 8
+// Register-blocked: thread (ta, tb) of a 16 x 16 grid owns F / G entries
+// (a, b') with a = ta + 16 i, b' = tb + 16 j (b' < Tk: F[a][b'], else
+// G[a][b' - Tk]), i < 4, j < 8 -- per staged row 12 shared loads feed up to
+// 32 FMAs.  Each entry still accumulates over this CTA's rows in row order
+// (fg_reduce then sums the CTAs in a fixed order), as before.
+#define FG_BI 4
+#define FG_BJ 8
 __global__ void __launch_bounds__(EX_NT)
     zscale_fg_kernel(long long n, const double* __restrict__ Zraw, const double* __restrict__ AZraw,
                      const double* __restrict__ norms, const int* __restrict__ keep, const DevStatus* plan, double* Zs,
@@ -112,25 +118,21 @@ __global__ void __launch_bounds__(EX_NT)
     const int T = (int)plan->aux;
     const int Tk = (int)plan->count;
     const int npairs = 2 * Tk * Tk;
-    const int p0 = blockIdx.y * (EX_NT * FG_PPT);
-    if (p0 >= npairs) return;
-    double* zs = sm;                    // EX_ROWS x Tk
-    double* azs = sm + EX_ROWS * T;     // EX_ROWS x Tk
+    // staged rows: [zs | azs] per row, 2 Tk wide, so b' indexes one array
+    double* za = sm;                    // EX_ROWS x 2 Tk
     const int tid = threadIdx.x;
+    // blockIdx.y picks the 64 x 128 region of the (a, b') grid (one region for Tk <= 64)
+    const int nbj = (2 * Tk + 16 * FG_BJ - 1) / (16 * FG_BJ);
+    const int a0 = (blockIdx.y / nbj) * 16 * FG_BI, b0 = (blockIdx.y % nbj) * 16 * FG_BJ;
+    if (a0 >= Tk) return;
+    const int ta = a0 + (tid >> 4), tb = b0 + (tid & 15);
     const long long r0 = part_begin(n, gridDim.x, blockIdx.x), r1 = part_begin(n, gridDim.x, blockIdx.x + 1);
-    double acc[FG_PPT];
-    int pa[FG_PPT], pb[FG_PPT];
-    bool pg[FG_PPT];
+    double acc[FG_BI][FG_BJ];
 #pragma unroll
-    for (int u = 0; u < FG_PPT; ++u) {
-        acc[u] = 0.0;
-        int e = p0 + u * EX_NT + tid;
-        pg[u] = e >= Tk * Tk;            // G entries follow the F entries
-        if (pg[u]) e -= Tk * Tk;
-        const bool valid = p0 + u * EX_NT + tid < npairs;
-        pa[u] = valid ? e / Tk : -1;
-        pb[u] = valid ? e % Tk : 0;
-    }
+    for (int i = 0; i < FG_BI; ++i)
+#pragma unroll
+        for (int j = 0; j < FG_BJ; ++j) acc[i][j] = 0.0;
+    const int W = 2 * Tk;
     for (long long i0 = r0; i0 < r1; i0 += EX_ROWS) {
         const int nr = (int)min((long long)EX_ROWS, r1 - i0);
         cta_sync();
@@ -140,8 +142,8 @@ __global__ void __launch_bounds__(EX_NT)
             const double nv = norms[c];
             const double zv = div_rn(Zraw[(i0 + r) * T + c], nv);
             const double av = div_rn(AZraw[(i0 + r) * T + c], nv);
-            zs[r * Tk + cc] = zv;
-            azs[r * Tk + cc] = av;
+            za[r * W + cc] = zv;
+            za[r * W + Tk + cc] = av;
             if (blockIdx.y == 0) {
                 Zs[(i0 + r) * Tk + cc] = zv;
                 AZs[(i0 + r) * Tk + cc] = av;
@@ -149,15 +151,35 @@ __global__ void __launch_bounds__(EX_NT)
         }
         cta_sync();
         for (int r = 0; r < nr; ++r) {
+            const double* row = za + r * W;
+            double av[FG_BI], bv[FG_BJ];
 #pragma unroll
-            for (int u = 0; u < FG_PPT; ++u)
-                if (pa[u] >= 0) acc[u] = fma(azs[r * Tk + pa[u]], pg[u] ? azs[r * Tk + pb[u]] : zs[r * Tk + pb[u]], acc[u]);
+            for (int i = 0; i < FG_BI; ++i) {
+                const int a = ta + 16 * i;
+                av[i] = a < Tk ? row[Tk + a] : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < FG_BJ; ++j) {
+                const int b = tb + 16 * j;
+                bv[j] = b < W ? row[b] : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < FG_BI; ++i)
+#pragma unroll
+                for (int j = 0; j < FG_BJ; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
         }
     }
+    double* out = part + (long long)blockIdx.x * npairs;
 #pragma unroll
-    for (int u = 0; u < FG_PPT; ++u) {
-        const int e = p0 + u * EX_NT + tid;
-        if (e < npairs) part[(long long)blockIdx.x * npairs + e] = acc[u];
+    for (int i = 0; i < FG_BI; ++i) {
+        const int a = ta + 16 * i;
+        if (a >= Tk) continue;
+#pragma unroll
+        for (int j = 0; j < FG_BJ; ++j) {
+            const int b = tb + 16 * j;
+            if (b < Tk) out[a * Tk + b] = acc[i][j];
+            else if (b < W) out[Tk * Tk + a * Tk + (b - Tk)] = acc[i][j];
+        }
     }
 }
 
@@ -183,7 +205,9 @@ __global__ void fg_reduce_kernel(const double* part, int nparts, const DevStatus
 // Rows are staged EX_ROWS at a time into shared memory with coalesced loads
 // (a lane's dependent FMA chain over the Tk columns then reads shared memory:
 // with the global loads inside the chain, in-order issue serialised one L2
-// round trip per column -- 1.3 ms per call at n = 50k, T = 68).
+// round trip per column -- 1.3 ms per call at n = 50k, T = 68).  A 16 x 16
+// thread grid (two rows x up to four columns per thread per staged block)
+// keeps every thread busy; with a warp per row only k of 32 lanes worked.
 __global__ void __launch_bounds__(EX_NT)
     uscale_kernel(long long n, int k, const double* __restrict__ Zs, const DevStatus* plan, const DevStatus* pencil,
                   double* U, const int* active, double* Uexp, double* part, unsigned int* counter) {
@@ -191,36 +215,40 @@ __global__ void __launch_bounds__(EX_NT)
     extern __shared__ double sm[];
     const int Tk = (int)plan->count, na = (int)pencil->count;
     double* ue = sm;                       // Tk x k
-    double* wp = ue + Tk * k;              // 8 warps x 64
-    double* zr = wp + 8 * 64;              // EX_ROWS x Tk staged rows
+    double* wp = ue + Tk * k;              // 16 row slots x 64
+    double* zr = wp + 16 * 64;             // EX_ROWS x Tk staged rows
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int e = tid; e < Tk * k; e += EX_NT) ue[e] = 0.0;
     cta_sync();
     for (int e = tid; e < na * k; e += EX_NT) ue[active[e / k] * k + e % k] = U[e];
     const long long r0 = part_begin(n, gridDim.x, blockIdx.x), r1 = part_begin(n, gridDim.x, blockIdx.x + 1);
-    double s0 = 0.0, s1 = 0.0;   // lanes own columns lane, lane + 32
+    // thread (rs, jg): rows rs, rs + 16 of a staged block, columns jg + 16 q
+    const int rs = tid >> 4, jg = tid & 15;
+    double sq[4] = {0.0, 0.0, 0.0, 0.0};
     for (long long i0 = r0; i0 < r1; i0 += EX_ROWS) {
         const int nr = (int)min((long long)EX_ROWS, r1 - i0);
         cta_sync();
         for (int e = tid; e < nr * Tk; e += EX_NT) zr[e] = Zs[i0 * Tk + e];
         cta_sync();
-        for (int rr = warp; rr < nr; rr += EX_NT / 32) {
+        for (int rr = rs; rr < nr; rr += 16) {
             const double* z = zr + rr * Tk;
-            double v0 = 0.0, v1 = 0.0;
+            double v[4] = {0.0, 0.0, 0.0, 0.0};
             for (int c = 0; c < Tk; ++c) {
-                if (lane < k) v0 = fma(z[c], ue[c * k + lane], v0);
-                if (lane + 32 < k) v1 = fma(z[c], ue[c * k + lane + 32], v1);
+                const double zc = z[c];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (jg + 16 * q < k) v[q] = fma(zc, ue[c * k + jg + 16 * q], v[q]);
             }
-            s0 = fma(v0, v0, s0);
-            s1 = fma(v1, v1, s1);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) sq[q] = fma(v[q], v[q], sq[q]);
         }
     }
-    wp[warp * 64 + lane] = s0;
-    wp[warp * 64 + lane + 32] = s1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) wp[rs * 64 + jg + 16 * q] = sq[q];
     cta_sync();
     if (tid < k) {
         double s = 0.0;
-        for (int w = 0; w < EX_NT / 32; ++w) s += wp[w * 64 + tid];
+        for (int w = 0; w < 16; ++w) s += wp[w * 64 + tid];
         part[(long long)blockIdx.x * k + tid] = s;
     }
     if (!cta_last_arrival(counter, gridDim.x)) return;
@@ -308,8 +336,6 @@ __global__ void __launch_bounds__(EX_NT)
 static size_t extract_ws_bytes(dcg_context* ctx, long long n, int T, int k) {
     const int G = ctx->sm_count;
     const size_t nT = (size_t)n * T;
-    const int gy = (2 * T * T + EX_NT * FG_PPT - 1) / (EX_NT * FG_PPT);
-    (void)gy;
     return 4 * al(sizeof(double) * nT) + al(sizeof(double) * (size_t)G * T) + al(sizeof(double) * T) +
            2 * al(sizeof(int) * T) + 2 * al(sizeof(double) * T * T) + al(sizeof(double) * (size_t)G * 2 * T * T) +
            al(sizeof(double) * 5 * T * T) + 2 * al(sizeof(double) * T * k) + al(sizeof(double) * (size_t)G * k) +
@@ -321,7 +347,10 @@ static size_t extract_ws_bytes(dcg_context* ctx, long long n, int T, int k) {
 // from the solve's status block on the device).
 // stage: 0 = the whole pipeline; 1 = E1-E3 (the SM-wide column work, run on
 // the main stream ahead of the Newton update); 2 = E4-E6 (the single-CTA
-// pencil and the tail, on the side stream).  Stages share the context's
+// pencil and the tail, on the side stream); 3 = E4 alone and 4 = E5-E6 alone
+// (the pencil on the side stream, its SM-wide tail on the main stream once
+// the pencil is done: on the side stream the tail only gets the SMs the main
+// stream's products leave).  Stages share the context's
 // workspace layout, so they must be enqueued with identical arguments.
 static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const dcg_krylov_log* log, long long m,
                            long long kp, long long T, const DevStatus* solve_st, const double* Wp, const double* AWp,
@@ -358,14 +387,15 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
     int nb = G;
     if (n < (long long)nb * EX_ROWS) nb = (int)max(1LL, (n + EX_ROWS - 1) / EX_ROWS);
     const size_t sm1 = sizeof(double) * 2 * EX_ROWS * T;
-    if (stage != 2) {
+    if (stage == 0 || stage == 1) {
     DCG_CUDA(cudaMemsetAsync(plan, 0, al(sizeof(DevStatus)) * 2, st));
     DCG_CUDA(cudaMemsetAsync(counters, 0, 16, st));
     DCG_CUDA(cudaFuncSetAttribute(zgather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
     zgather_kernel<<<nb, EX_NT, sm1, st>>>(n, (int)kp, Wp, AWp, (int)m, P, R, alpha, (int)k, Zraw, AZraw, part,
                                            counters, norms, keep, plan, solve_st);
     DCG_LAUNCHED();
-    const int gy = (int)((2 * T * T + EX_NT * FG_PPT - 1) / (EX_NT * FG_PPT));
+    // regions of 64 x 128 (a, b') entries; Tk <= T decides on the device which are live
+    const int gy = (int)(((T + 16 * FG_BI - 1) / (16 * FG_BI)) * ((2 * T + 16 * FG_BJ - 1) / (16 * FG_BJ)));
     DCG_CUDA(cudaFuncSetAttribute(zscale_fg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
     zscale_fg_kernel<<<dim3(nb, gy), EX_NT, sm1, st>>>(n, Zraw, AZraw, norms, keep, plan, Zs, AZs, fgpart);
     DCG_LAUNCHED();
@@ -374,10 +404,13 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
     DCG_LAUNCHED();
     }
     if (stage == 1) return DCG_OK;
-    rc = dcg_ritz_pencil_launch(st, Fraw, Graw, (int)T, (int)k, selection == DCG_SELECT_LARGEST, 60, wk, d_theta, U,
-                                active, pencil, plan);
-    if (rc) return rc;
-    const size_t sm5 = sizeof(double) * ((size_t)T * k + 8 * 64 + (size_t)EX_ROWS * T);
+    if (stage != 4) {
+        rc = dcg_ritz_pencil_launch(st, Fraw, Graw, (int)T, (int)k, selection == DCG_SELECT_LARGEST, 60, wk, d_theta,
+                                    U, active, pencil, plan);
+        if (rc) return rc;
+    }
+    if (stage == 3) return DCG_OK;
+    const size_t sm5 = sizeof(double) * ((size_t)T * k + 16 * 64 + (size_t)EX_ROWS * T);
     DCG_CUDA(cudaFuncSetAttribute(uscale_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm5));
     uscale_kernel<<<nb, EX_NT, sm5, st>>>(n, (int)k, Zs, plan, pencil, U, active, Uexp, upart, counters + 1);
     DCG_LAUNCHED();
@@ -425,7 +458,7 @@ extern "C" int dcg_ritz_extract_dev(dcg_context* ctx, void* stream, long long n,
                                     const void* d_solve_status, const dcg_basis* prev, long long k, int selection,
                                     double* d_theta, double* d_w_next, double* d_aw_next, long long* d_result,
                                     int stage) {
-    if (stage < 0 || stage > 2) return DCG_E_CONFIG;
+    if (stage < 0 || stage > 4) return DCG_E_CONFIG;
     if (!ctx || n < 0 || k < 1 || !d_result || !d_solve_status || !log) return DCG_E_CONFIG;
     if (selection != DCG_SELECT_SMALLEST && selection != DCG_SELECT_LARGEST) return DCG_E_CONFIG;
     const long long kmax = prev ? prev->k : 0;
@@ -433,7 +466,7 @@ extern "C" int dcg_ritz_extract_dev(dcg_context* ctx, void* stream, long long n,
     if (kmax > 0 && (!prev->d_w || !prev->d_aw)) return DCG_E_CONFIG;
     if (log->ell > 0 && (!log->d_p || !log->d_r || !log->d_alpha)) return DCG_E_CONFIG;
     if (T < 1) {
-        if (stage == 1) return DCG_OK;
+        if (stage == 1 || stage == 3) return DCG_OK;
         // nothing can ever be extracted: BasisDeficient(0) (k >= 1 > T)
         DCG_CUDA(cudaMemsetAsync(d_result, 0, 3 * sizeof(long long), as_stream(stream)));
         long long* r0 = d_result;

@@ -135,6 +135,19 @@ __global__ void newton_prep_kernel(long long n, const double* f, const double* g
     }
 }
 
+// newton_prep plus xs = s (.) x_prev, the operand of the next solve's first
+// product A x_prev (formed as the symmetric product stages it: s_j * x_j)
+__global__ void newton_prep2_kernel(long long n, const double* f, const double* grad, const double* h,
+                                    const double* x, double* s, double* inner, double* xs) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double si = sqrt(h[i]);
+        s[i] = si;
+        inner[i] = add_rn(mul_rn(h[i], f[i]), grad[i]);
+        xs[i] = mul_rn(si, x[i]);
+    }
+}
+
 // a = inner - s x   (gpc.py:190)
 __global__ void newton_a_kernel(long long n, const double* inner, const double* s, const double* x, double* a) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -156,6 +169,13 @@ int dcg_derivs_launch(dcg_context* ctx, cudaStream_t st, long long n, const doub
 int dcg_newton_prep_launch(dcg_context* ctx, cudaStream_t st, long long n, const double* f, const double* grad,
                            const double* h, double* s, double* inner) {
     newton_prep_kernel<<<ctx->sm_count * 2, 256, 0, st>>>(n, f, grad, h, s, inner);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}
+
+int dcg_newton_prep2_launch(dcg_context* ctx, cudaStream_t st, long long n, const double* f, const double* grad,
+                            const double* h, const double* x, double* s, double* inner, double* xs) {
+    newton_prep2_kernel<<<ctx->sm_count * 2, 256, 0, st>>>(n, f, grad, h, x, s, inner, xs);
     DCG_LAUNCHED();
     return DCG_OK;
 }

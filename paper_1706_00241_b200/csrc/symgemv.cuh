@@ -271,10 +271,16 @@ __device__ __forceinline__ void sym_ring_init(double* smem, long long n) {
 // Pass 1 over this CTA's tile range.  colpart/rowpart: ntt x 64 doubles.
 // `seq` (uniform per CTA) counts the tiles this CTA has pushed through the
 // ring in earlier passes of the same launch; it advances by the range length.
-template <bool kHint = true>
+// NV = 2: a second vector v2 rides in the stage's s slot (both vectors
+// unscaled, s == nullptr) and its partials go to colpart / rowpart + part2 --
+// every tile read from HBM serves two products, each with exactly the
+// operation sequence of its NV = 1 pass.
+template <bool kHint = true, int NV = 1>
 __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long long ldk, long long n, const double* v,
                                           const double* s, double* colpart, double* rowpart, double* smem,
-                                          unsigned int& seq) {
+                                          unsigned int& seq, const double* v2 = nullptr, long long part2 = 0) {
+    static_assert(NV == 1 || NV == 2, "one or two vectors");
+    if constexpr (NV == 2) s = v2;   // the s slot of every stage carries v2
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double* ring = smem;
     double* rowred = ring + DCG_SYM_STAGES * DCG_SYM_STAGE_DOUBLES;                       // 2 x NW x 64
@@ -311,9 +317,14 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
     const int o00 = (2 * lane) * DCG_TB + 2 * ((2 * warp) ^ key);
     const int o01 = (2 * lane) * DCG_TB + 2 * ((2 * warp + 1) ^ key);
     const int o10 = o00 + DCG_TB, o11 = o01 + DCG_TB;
-    double xI0 = sym_xval(v, s, I * DCG_TB + 2 * lane, n);
-    double xI1 = sym_xval(v, s, I * DCG_TB + 2 * lane + 1, n);
-    double row0 = 0.0, row1 = 0.0;
+    double xI0 = sym_xval(v, NV == 2 ? nullptr : s, I * DCG_TB + 2 * lane, n);
+    double xI1 = sym_xval(v, NV == 2 ? nullptr : s, I * DCG_TB + 2 * lane + 1, n);
+    double yI0 = 0.0, yI1 = 0.0;
+    if constexpr (NV == 2) {
+        yI0 = sym_xval(v2, nullptr, I * DCG_TB + 2 * lane, n);
+        yI1 = sym_xval(v2, nullptr, I * DCG_TB + 2 * lane + 1, n);
+    }
+    double row0 = 0.0, row1 = 0.0, rowb0 = 0.0, rowb1 = 0.0;
     long long seg_start = t0;
     int flush = 0;
     for (int lt = 0; lt < ntiles; ++lt) {
@@ -341,7 +352,15 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
         const double2 v0 = *reinterpret_cast<const double2*>(tile + DCG_SYM_TILE_DOUBLES + 4 * warp);
         const double2 v1 = *reinterpret_cast<const double2*>(tile + DCG_SYM_TILE_DOUBLES + 4 * warp + 2);
         double x0 = v0.x, x1 = v0.y, x2 = v1.x, x3 = v1.y;
-        if (s) {
+        double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
+        if constexpr (NV == 2) {
+            const double2 s0 = *reinterpret_cast<const double2*>(tile + DCG_SYM_TILE_DOUBLES + DCG_TB + 4 * warp);
+            const double2 s1 = *reinterpret_cast<const double2*>(tile + DCG_SYM_TILE_DOUBLES + DCG_TB + 4 * warp + 2);
+            y0 = s0.x;
+            y1 = s0.y;
+            y2 = s1.x;
+            y3 = s1.y;
+        } else if (s) {
             const double2 s0 = *reinterpret_cast<const double2*>(tile + DCG_SYM_TILE_DOUBLES + DCG_TB + 4 * warp);
             const double2 s1 = *reinterpret_cast<const double2*>(tile + DCG_SYM_TILE_DOUBLES + DCG_TB + 4 * warp + 2);
             x0 = mul_rn(s0.x, x0);
@@ -359,36 +378,70 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
         row1 = fma(b0.y, x1, row1);
         row1 = fma(b1.x, x2, row1);
         row1 = fma(b1.y, x3, row1);
+        if constexpr (NV == 2) {
+            rowb0 = fma(a0.x, y0, rowb0);
+            rowb0 = fma(a0.y, y1, rowb0);
+            rowb0 = fma(a1.x, y2, rowb0);
+            rowb0 = fma(a1.y, y3, rowb0);
+            rowb1 = fma(b0.x, y0, rowb1);
+            rowb1 = fma(b0.y, y1, rowb1);
+            rowb1 = fma(b1.x, y2, rowb1);
+            rowb1 = fma(b1.y, y3, rowb1);
+        }
         if (J < I) {
             // column sums over the tile's 64 rows: warp reduce-scatter of 4 values
-            double c0 = fma(b0.x, xI1, a0.x * xI0);
-            double c1 = fma(b0.y, xI1, a0.y * xI0);
-            double c2 = fma(b1.x, xI1, a1.x * xI0);
-            double c3 = fma(b1.y, xI1, a1.y * xI0);
-            const bool hi16 = lane & 16;
-            const double r0 = __shfl_xor_sync(0xffffffffu, hi16 ? c0 : c2, 16);
-            const double r1 = __shfl_xor_sync(0xffffffffu, hi16 ? c1 : c3, 16);
-            double k0 = (hi16 ? c2 : c0) + r0;   // columns {0,1} (lanes < 16) or {2,3}
-            double k1 = (hi16 ? c3 : c1) + r1;
-            const bool hi8 = lane & 8;
-            const double r2 = __shfl_xor_sync(0xffffffffu, hi8 ? k0 : k1, 8);
-            double cv = (hi8 ? k1 : k0) + r2;    // column 2*hi16 + hi8
-            cv += __shfl_xor_sync(0xffffffffu, cv, 4);
-            cv += __shfl_xor_sync(0xffffffffu, cv, 2);
-            cv += __shfl_xor_sync(0xffffffffu, cv, 1);
-            if ((lane & 7) == 0) colpart[(t0 + lt) * DCG_TB + 4 * warp + 2 * (lane >> 4) + ((lane >> 3) & 1)] = cv;
+            auto colsum = [&](double zI0, double zI1, double* cp) {
+                double c0 = fma(b0.x, zI1, a0.x * zI0);
+                double c1 = fma(b0.y, zI1, a0.y * zI0);
+                double c2 = fma(b1.x, zI1, a1.x * zI0);
+                double c3 = fma(b1.y, zI1, a1.y * zI0);
+                const bool hi16 = lane & 16;
+                const double r0 = __shfl_xor_sync(0xffffffffu, hi16 ? c0 : c2, 16);
+                const double r1 = __shfl_xor_sync(0xffffffffu, hi16 ? c1 : c3, 16);
+                double k0 = (hi16 ? c2 : c0) + r0;   // columns {0,1} (lanes < 16) or {2,3}
+                double k1 = (hi16 ? c3 : c1) + r1;
+                const bool hi8 = lane & 8;
+                const double r2 = __shfl_xor_sync(0xffffffffu, hi8 ? k0 : k1, 8);
+                double cv = (hi8 ? k1 : k0) + r2;    // column 2*hi16 + hi8
+                cv += __shfl_xor_sync(0xffffffffu, cv, 4);
+                cv += __shfl_xor_sync(0xffffffffu, cv, 2);
+                cv += __shfl_xor_sync(0xffffffffu, cv, 1);
+                if ((lane & 7) == 0) cp[(t0 + lt) * DCG_TB + 4 * warp + 2 * (lane >> 4) + ((lane >> 3) & 1)] = cv;
+            };
+            colsum(xI0, xI1, colpart);
+            if constexpr (NV == 2) colsum(yI0, yI1, colpart + part2);
         }
         // end of a tile-row segment: diagonal tile reached or last tile of the range
         if (J == I || lt + 1 == ntiles) {
-            double* rr = rowred + (flush & 1) * DCG_NW * DCG_TB;
-            rr[warp * DCG_TB + 2 * lane] = row0;
-            rr[warp * DCG_TB + 2 * lane + 1] = row1;
-            cta_sync();
-            if (tid < DCG_TB) {
-                double a = 0.0;
+            if constexpr (NV == 1) {
+                double* rr = rowred + (flush & 1) * DCG_NW * DCG_TB;
+                rr[warp * DCG_TB + 2 * lane] = row0;
+                rr[warp * DCG_TB + 2 * lane + 1] = row1;
+                cta_sync();
+                if (tid < DCG_TB) {
+                    double a = 0.0;
 #pragma unroll
-                for (int w = 0; w < DCG_NW; ++w) a += rr[w * DCG_TB + tid];
-                rowpart[seg_start * DCG_TB + tid] = a;
+                    for (int w = 0; w < DCG_NW; ++w) a += rr[w * DCG_TB + tid];
+                    rowpart[seg_start * DCG_TB + tid] = a;
+                }
+            } else {
+                // both halves of the flush buffer in use: a second barrier
+                // instead of the alternation
+                double* rr = rowred + (tid >= DCG_TB ? DCG_NW * DCG_TB : 0);
+                rowred[warp * DCG_TB + 2 * lane] = row0;
+                rowred[warp * DCG_TB + 2 * lane + 1] = row1;
+                rowred[DCG_NW * DCG_TB + warp * DCG_TB + 2 * lane] = rowb0;
+                rowred[DCG_NW * DCG_TB + warp * DCG_TB + 2 * lane + 1] = rowb1;
+                cta_sync();
+                if (tid < 2 * DCG_TB) {
+                    const int c = tid & (DCG_TB - 1);
+                    double a = 0.0;
+#pragma unroll
+                    for (int w = 0; w < DCG_NW; ++w) a += rr[w * DCG_TB + c];
+                    (tid >= DCG_TB ? rowpart + part2 : rowpart)[seg_start * DCG_TB + c] = a;
+                }
+                cta_sync();
+                rowb0 = rowb1 = 0.0;
             }
             row0 = row1 = 0.0;
             seg_start = t0 + lt + 1;
@@ -398,8 +451,12 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
             ++I;
             J = 0;
             if (lt + 1 < ntiles) {
-                xI0 = sym_xval(v, s, I * DCG_TB + 2 * lane, n);
-                xI1 = sym_xval(v, s, I * DCG_TB + 2 * lane + 1, n);
+                xI0 = sym_xval(v, NV == 2 ? nullptr : s, I * DCG_TB + 2 * lane, n);
+                xI1 = sym_xval(v, NV == 2 ? nullptr : s, I * DCG_TB + 2 * lane + 1, n);
+                if constexpr (NV == 2) {
+                    yI0 = sym_xval(v2, nullptr, I * DCG_TB + 2 * lane, n);
+                    yI1 = sym_xval(v2, nullptr, I * DCG_TB + 2 * lane + 1, n);
+                }
             }
         }
     }

@@ -71,6 +71,8 @@ class NewtonSystem:
     b: torch.Tensor
     sqrt_h: torch.Tensor
     inner: torch.Tensor | None = None
+    ax0: torch.Tensor | None = None      # a_matrix @ x_prev, when built with x_prev
+    x_prev: torch.Tensor | None = None
 
 
 @dataclass
@@ -167,12 +169,22 @@ def make_state(k_matrix, y, f=None):
     return GpcState(f=fd, y=yd, k_matrix=op, a=ad, loglik=ll, grad_loglik=g, h=h)
 
 
-def build_newton_system(state):
-    """A = I + H^1/2 K H^1/2 (implicit) and b = H^1/2 K (H f + grad) (gpc.py:175-183)."""
+def build_newton_system(state, x_prev=None):
+    """A = I + H^1/2 K H^1/2 (implicit) and b = H^1/2 K (H f + grad) (gpc.py:175-183).
+
+    With ``x_prev`` (a device vector) also ax0 = A x_prev, the first product of
+    the next warm-started solve, from the same pass over K."""
     op = state.k_matrix
     n = op.n
     s, inner, b = D.empty(n), D.empty(n), D.empty(n)
     kop = op.kernel_view().c_struct()
+    if x_prev is not None:
+        ax0 = D.empty(n)
+        N.check(N.lib().dcg_gpc_newton_system_ax0(D.ctx(), D.stream(), ctypes.byref(kop), state.f.data_ptr(),
+                                                  state.grad_loglik.data_ptr(), state.h.data_ptr(),
+                                                  x_prev.data_ptr(), s.data_ptr(), inner.data_ptr(), b.data_ptr(),
+                                                  ax0.data_ptr()), what="newton_system_ax0")
+        return NewtonSystem(a_matrix=op.scaled(s, 1.0), b=b, sqrt_h=s, inner=inner, ax0=ax0, x_prev=x_prev)
     N.check(N.lib().dcg_gpc_newton_system(D.ctx(), D.stream(), ctypes.byref(kop), state.f.data_ptr(),
                                           state.grad_loglik.data_ptr(), state.h.data_ptr(), s.data_ptr(),
                                           inner.data_ptr(), b.data_ptr()), what="newton_system")
@@ -239,9 +251,10 @@ def _laplace_newton_pipelined(state, psi_prev, cfg, newton_tol, max_newton, k, s
     system = build_newton_system(state)
     for it in range(1, max_newton + 1):
         t0 = time.perf_counter()
-        x, job = solve_next_async(seq, system.a_matrix, system.b)
+        x, job = solve_next_async(seq, system.a_matrix, system.b, ax0=system.ax0, ax0_of=system.x_prev)
         new_state, objective = _update_dev_async(state, system.inner, system.sqrt_h, x)
-        next_system = build_newton_system(new_state) if it < max_newton else None
+        # the next system and its solve's first product A_next x in one K pass
+        next_system = build_newton_system(new_state, x_prev=x) if it < max_newton else None
         x, seq = job.finish()
         dt = time.perf_counter() - t0
         report = seq.history[-1]

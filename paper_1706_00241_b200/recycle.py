@@ -60,15 +60,26 @@ class _PendingBasis:
     basis (ok), None (BasisDeficient, swallowed as in recycle.py:194-195) or
     the reference's exception (e.g. NoConvergence)."""
 
-    def __init__(self, event, result, w_next, aw_next, keep_alive):
+    def __init__(self, event, result, w_next, aw_next, keep_alive, tail=None):
         self.event = event
         self.result = result
         self.w_next = w_next
         self.aw_next = aw_next
         self.keep_alive = keep_alive   # inputs the side stream reads
+        self.tail = tail               # enqueues the extraction's last stage on a given stream
+
+    def join(self, stream):
+        """Order `stream` after the extraction: wait for the side stream's
+        event, then enqueue the extraction's tail (if split off) on `stream`."""
+        stream.wait_event(self.event)
+        if self.tail is not None:
+            tail, self.tail = self.tail, None
+            tail(stream)
+            self.event = torch.cuda.Event()
+            self.event.record(stream)
 
     def resolve(self):
-        torch.cuda.current_stream().wait_event(self.event)
+        self.join(torch.cuda.current_stream())
         self.event.synchronize()
         status, info = (int(v) for v in self.result[:2].cpu().tolist())
         self.keep_alive = None
@@ -272,10 +283,13 @@ class _AsyncSolve:
         return self.x, replace(st, basis=self.pending, x_last=self.x, history=st.history + [rep])
 
 
-def solve_next_async(state, a, b):
+def solve_next_async(state, a, b, ax0=None, ax0_of=None):
     """Enqueue refresh + solve of the next system of a sequence and the
     extraction of the basis after it (device data only, nothing waits).
-    Returns (x, job); job.finish() completes the report and the new state."""
+    Returns (x, job); job.finish() completes the report and the new state.
+    ``ax0`` = a @ ax0_of, precomputed by the caller (gpc's fused system
+    build), stands in for the warm start's first product when ``ax0_of`` is
+    the sequence's last solution."""
     op = as_operator(a)
     bd = D.to_dev(b, 1)
     n = bd.shape[0]
@@ -287,12 +301,15 @@ def solve_next_async(state, a, b):
     t0 = time.perf_counter()
     main = torch.cuda.current_stream()
     pending = object.__getattribute__(state, "basis")
-    w_src, valid, ax0 = None, None, None
+    w_src, valid = None, None
+    if not isinstance(pending, _PendingBasis):
+        ax0 = None
     if isinstance(pending, _PendingBasis):
         # the warm start's first product A x_prev needs no basis: it runs
         # while the extraction of the basis is still going on
-        ax0 = op.matvec_dev(x_prev)
-        main.wait_event(pending.event)
+        if ax0 is None or ax0_of is None or ax0_of is not state.x_last:
+            ax0 = op.matvec_dev(x_prev)
+        pending.join(main)
         pending.keep_alive = None   # main-stream work is now ordered after the extraction
         w_src, valid = pending.w_next, pending.result
     elif pending is not None and pending.k > 0:
@@ -346,10 +363,16 @@ def solve_next_async(state, a, b):
         side = D.side_stream()
         side.wait_event(gathered)
         with torch.cuda.stream(side):
-            N.check(N.lib().dcg_ritz_extract_dev(*args[:1], side.cuda_stream, *args[2:], 2), 0, "ritz_extract_dev")
+            N.check(N.lib().dcg_ritz_extract_dev(*args[:1], side.cuda_stream, *args[2:], 3), 0, "ritz_extract_dev")
             event = torch.cuda.Event()
             event.record(side)
-        nxt = _PendingBasis(event, result, w_next, aw_next, (log, bufs, theta, status))
+
+        def tail(stream, args=args):
+            # uscale + wnext: SM-wide, so they run on the joining stream (the
+            # main one) rather than in the SMs the side stream is left
+            N.check(N.lib().dcg_ritz_extract_dev(*args[:1], stream.cuda_stream, *args[2:], 4), 0, "ritz_extract_dev")
+
+        nxt = _PendingBasis(event, result, w_next, aw_next, (log, bufs, theta, status), tail)
     job = _AsyncSolve(state, x, log, hist, status, bufs, ev0, ev_end, t0, cfg, nxt)
     job.hoisted = ax0 is not None and kmax > 0   # the solve kernel skips its first product
     return x, job

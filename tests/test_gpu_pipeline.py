@@ -96,6 +96,7 @@ def test_failed_extraction_means_plain_cg(P):
     _, job = P.recycle.solve_next_async(st, *systems[0])
     x0, st = job.finish()
     pending = object.__getattribute__(st, "basis")
+    pending.join(torch.cuda.current_stream())
     pending.event.synchronize()
     pending.result[0] = P._native.DCG_E_BASIS_DEFICIENT   # as the device would have written it
     _, job = P.recycle.solve_next_async(st, *systems[1])
@@ -125,3 +126,34 @@ def test_deficient_extraction_on_device(P):
     ss = P.SequenceState(k=16, cfg=cfg, selection="largest")
     _, ss = P.solve_next(ss, a, b)
     assert ss.basis is None
+
+
+@pytest.mark.parametrize("n", [300, 1000, 2113])
+def test_fused_newton_system_matches_separate_products(P, n):
+    """dcg_gpc_newton_system_ax0 (b and ax0 = A x_prev from one pass over a
+    symmetric-stored K, sym_pass1<NV = 2>) equals newton_system followed by
+    the operator's own A x_prev bitwise: same tile partition, same partial
+    layout, same pass-2 order."""
+    from paper_1706_00241_b200 import gpc as G
+
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, 4))
+    gram = P.rbf_kernel(x, P.KernelParams(1.0, 1.3))
+    y = np.where(rng.standard_normal(n) > 0, 1.0, -1.0)
+    state = G.make_state(gram, torch.from_numpy(y).cuda())
+    state.f = torch.from_numpy(rng.standard_normal(n)).cuda()
+    state.grad_loglik = torch.from_numpy(rng.standard_normal(n)).cuda()
+    state.h = torch.from_numpy(rng.uniform(0.05, 0.25, n)).cuda()
+    x_prev = torch.from_numpy(rng.standard_normal(n)).cuda()
+    fused = G.build_newton_system(state, x_prev=x_prev)
+    plain = G.build_newton_system(state)
+    ax0 = plain.a_matrix.matvec_dev(x_prev)
+    torch.cuda.synchronize()
+    assert torch.equal(fused.sqrt_h, plain.sqrt_h) and torch.equal(fused.inner, plain.inner)
+    assert torch.equal(fused.b, plain.b)
+    assert torch.equal(fused.ax0, ax0)
+    # and against fp64 torch on the dense Gram
+    kd = gram.dense_dev()[:n, :n]
+    s = plain.sqrt_h
+    assert torch.allclose(fused.ax0, x_prev + s * (kd @ (s * x_prev)), rtol=1e-12, atol=1e-11)
+    assert torch.allclose(fused.b, s * (kd @ plain.inner), rtol=1e-12, atol=1e-11)

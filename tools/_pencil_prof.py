@@ -11,6 +11,7 @@ orig = recycle._AsyncSolve.finish
 def fin(job):
     out = orig(job)
     if job.pending is not None:
+        job.pending.join(torch.cuda.current_stream())
         job.pending.event.synchronize()
         h = (ctypes.c_longlong * 16)()
         N.lib().dcg_debug_pencil_profile.restype = ctypes.c_int
