@@ -198,13 +198,13 @@ int dcg_sym_pass2_launch(cudaStream_t st, int G, int R, long long n, const doubl
 
 // =============================================================================
 // K3: Y(rows x k) = K(rows x n) V(n x k) with mma.sync.m8n8k4 FP64.
-// CTA = 8 warps = 64 rows x all k columns; blockIdx.y splits the inner
+// CTA = 8 warps = 128 rows x all k columns; blockIdx.y splits the inner
 // dimension (partials reduced in a fixed order by yscale_reduce_kernel).
 // Operand tiles are staged with cp.async double buffering; the inner index is
 // permuted inside each 8-chunk (thread loads a 16-byte pair for two MMAs),
 // which leaves every dot product unchanged.
 // =============================================================================
-#define GM_BM 64
+#define GM_BM 128                // 8 warps x 16 rows: each B fragment feeds two row tiles
 #define GM_BK 32
 #define GM_SA (GM_BK + 4)        // A row stride (doubles): conflict-free 16 B fragment loads
 
@@ -270,9 +270,11 @@ __global__ void __launch_bounds__(256)
         }
     };
 
-    double acc[NTILE][2];
+    double acc[2][NTILE][2];
 #pragma unroll
-    for (int j = 0; j < NTILE; ++j) acc[j][0] = acc[j][1] = 0.0;
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int j = 0; j < NTILE; ++j) acc[h][j][0] = acc[h][j][1] = 0.0;
 
     if (ntiles > 0) {
         load_tile(0, cbeg);
@@ -288,29 +290,36 @@ __global__ void __launch_bounds__(256)
             cp_async_wait<0>();
         }
         cta_sync();
-        const double* a = sA + buf * GM_BM * GM_SA + (warp * 8 + g) * GM_SA;
+        const double* a = sA + buf * GM_BM * GM_SA + (warp * 16 + g) * GM_SA;
         const double* bsm = sB + buf * GM_BK * SB;
 #pragma unroll
         for (int kk = 0; kk < GM_BK / 8; ++kk) {
-            const double2 av = *reinterpret_cast<const double2*>(a + kk * 8 + 2 * t);
+            const double2 av0 = *reinterpret_cast<const double2*>(a + kk * 8 + 2 * t);
+            const double2 av1 = *reinterpret_cast<const double2*>(a + 8 * GM_SA + kk * 8 + 2 * t);
             const double* b0 = bsm + (kk * 8 + 2 * t) * SB + g;
 #pragma unroll
             for (int j = 0; j < NTILE; ++j) {
-                dmma(acc[j][0], acc[j][1], av.x, b0[j * 8]);
-                dmma(acc[j][0], acc[j][1], av.y, b0[SB + j * 8]);
+                const double bx = b0[j * 8], by = b0[SB + j * 8];
+                dmma(acc[0][j][0], acc[0][j][1], av0.x, bx);
+                dmma(acc[1][j][0], acc[1][j][1], av1.x, bx);
+                dmma(acc[0][j][0], acc[0][j][1], av0.y, by);
+                dmma(acc[1][j][0], acc[1][j][1], av1.y, by);
             }
         }
         cta_sync();
     }
-    // D fragment: row = g, cols 2t, 2t+1 of each n-tile
-    const long long r = row0 + warp * 8 + g;
-    if (r < rows) {
-        double* out = P + ((long long)blockIdx.y * rows + r) * kcols;
+    // D fragment: row = g, cols 2t, 2t+1 of each n-tile (two row tiles per warp)
 #pragma unroll
-        for (int j = 0; j < NTILE; ++j) {
-            const int c = j * 8 + 2 * t;
-            if (c < kcols) out[c] = acc[j][0];
-            if (c + 1 < kcols) out[c + 1] = acc[j][1];
+    for (int h = 0; h < 2; ++h) {
+        const long long r = row0 + warp * 16 + 8 * h + g;
+        if (r < rows) {
+            double* out = P + ((long long)blockIdx.y * rows + r) * kcols;
+#pragma unroll
+            for (int j = 0; j < NTILE; ++j) {
+                const int c = j * 8 + 2 * t;
+                if (c < kcols) out[c] = acc[h][j][0];
+                if (c + 1 < kcols) out[c + 1] = acc[h][j][1];
+            }
         }
     }
 }
