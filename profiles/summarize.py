@@ -2,6 +2,7 @@
 
   python profiles/summarize.py launches <launches.csv>            -> per-kernel table
   python profiles/summarize.py full <report.ncu-rep>              -> key metrics of the captured launch
+  python profiles/summarize.py fullall <report.ncu-rep>           -> the same for every captured launch
   python profiles/summarize.py traffic <report.ncu-rep> n mv k its -> solve_kernel_dram.json payload
 """
 import collections
@@ -61,6 +62,20 @@ def full(rep):
     return "\n".join(out)
 
 
+def fullall(rep):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(txt)))
+    h, u = r[0], r[1]
+    out = []
+    for v in r[2:]:
+        out.append("== " + v[h.index("Kernel Name")].split("(")[0])
+        for k in KEYS:
+            if k in h:
+                i = h.index(k)
+                out.append(f"{k:70s} {v[i]:>16s} {u[i]}")
+    return "\n".join(out)
+
+
 def traffic(rep, n, mv, k, its):
     h, u, v = raw(rep)
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -75,4 +90,4 @@ def traffic(rep, n, mv, k, its):
 
 if __name__ == "__main__":
     mode = sys.argv[1]
-    print({"launches": launches, "full": full, "traffic": traffic}[mode](*sys.argv[2:]))
+    print({"launches": launches, "full": full, "fullall": fullall, "traffic": traffic}[mode](*sys.argv[2:]))
