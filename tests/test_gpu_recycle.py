@@ -306,3 +306,27 @@ def test_pencil_tridiagonal_path_matches_jacobi(P, rng, n, ell, k, kappa):
         assert taken >= 1   # the fast path ran (it may decline a clustered selection)
     finally:
         _set_pencil_fast(True)
+
+
+def test_pencil_fast_path_declines_a_cluster(P):
+    """A selected double eigenvalue (two exact eigenvectors of the same value
+    carried in the previous basis): the tridiagonal fast path must decline
+    (twisted-factorisation vectors of a cluster are not orthogonal) and the
+    Jacobi path answers -- both copies of the value, their span exactly."""
+    n = 80
+    ev = np.arange(1.0, n + 1.0)
+    ev[5] = ev[4]                      # eigenvalue 5 twice (coordinates 4 and 5)
+    a = np.diag(ev)
+    prev = P.refresh_basis(a, np.eye(n)[:, [4, 5]])
+    rng = np.random.default_rng(3)
+    b = rng.standard_normal(n)
+    b[[4, 5]] = 0.0
+    _, _, log = P.deflated_cg_solve(a, b, np.zeros(n), prev, P.SolverConfig(tol=1e-14, ell=16))
+    assert prev.k + log.stored_iterations >= 12
+    _set_pencil_fast(True)
+    ext = P.harmonic_ritz_extract(log, prev, 6, "smallest")
+    assert _pencil_profile()[14] == 0          # declined
+    assert np.sum(np.abs(ext.theta - 5.0) < 1e-8) == 2
+    e45 = np.eye(n)[:, [4, 5]]
+    proj = ext.w_next @ np.linalg.pinv(ext.w_next)
+    assert np.linalg.norm(proj @ e45 - e45) < 1e-8
