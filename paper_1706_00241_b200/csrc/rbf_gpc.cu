@@ -22,6 +22,11 @@ __global__ void __launch_bounds__(256)
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
     const long long i0 = (long long)blockIdx.y * RBF_T;        // local row tile
     const long long j0 = (long long)blockIdx.x * RBF_T;
+    // whole square Gram: evaluate the tiles on and below the diagonal only
+    // and store each off-diagonal tile a second time, transposed -- the
+    // mirrored value is the directly evaluated one bit for bit (see above)
+    const bool mirror = gram && row0 == 0 && rows == nc;
+    if (mirror && blockIdx.x > blockIdx.y) return;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (long long t0 = 0; t0 < dim; t0 += RBF_T) {
         const int tn = (int)min((long long)RBF_T, dim - t0);
@@ -43,16 +48,26 @@ __global__ void __launch_bounds__(256)
         cta_sync();
     }
     const long long j = j0 + tx;
-    if (j >= nc) return;
+    double vals[4];
 #pragma unroll
     for (int rr = 0; rr < 4; ++rr) {
         const long long li = i0 + ty + 8 * rr;
-        if (li >= rows) continue;
         const long long gi = row0 + li;
         double val;
         if (gram && gi == j) val = add_rn(var, jitter);
         else val = mul_rn(var, exp(mul_rn(-acc[rr], inv2l2)));
-        out[li * ldo + j] = val;
+        vals[rr] = val;
+        if (j < nc && li < rows) out[li * ldo + j] = val;
+    }
+    if (!mirror || blockIdx.x == blockIdx.y) return;
+    // transposed copy through shared memory (sr is free again): coalesced rows
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) sr[ty + 8 * rr][tx] = vals[rr];
+    cta_sync();
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+        const long long orow = j0 + ty + 8 * rr, ocol = i0 + tx;   // K[j][i] = K[i][j]
+        if (orow < nc && ocol < rows) out[orow * ldo + ocol] = sr[tx][ty + 8 * rr];
     }
 }
 
