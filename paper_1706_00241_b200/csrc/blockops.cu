@@ -334,6 +334,22 @@ __global__ void rowscale_kernel(const double* X, const double* s, long long n, i
     }
 }
 
+// V (n x kk, kk >= k) = s (.) X with zero padding columns (s may be null)
+__global__ void pad_scale_kernel(const double* X, int k, const double* s, long long n, int kk, double* V) {
+    const long long total = n * kk;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long i = e / kk;
+        const int c = (int)(e - i * kk);
+        double v = 0.0;
+        if (c < k) {
+            v = X[i * k + c];
+            if (s) v = mul_rn(s[i], v);
+        }
+        V[e] = v;
+    }
+}
+
 // Y[i][j] = shift X[i][j] + s_out[i] * sum_split P[split][i][j]   (fixed split order)
 __global__ void yscale_reduce_kernel(const double* P, int splits, long long rows, int k,
                                      const double* X_rows, const double* s_out, double shift,
@@ -397,30 +413,27 @@ int dcg_block_apply(dcg_context* ctx, cudaStream_t st, const double* K, long lon
     int rc = DCG_OK;
     double* V = scratch;
     double* P = V + n * kk;
-    // V = s_in (.) X, padded to an even column count
-    if (kk != k || s_in) {
-        DCG_CUDA(cudaMemsetAsync(V, 0, vbytes, st));
-        // scatter into padded layout via a 2D copy, then scale in place
-        DCG_CUDA(cudaMemcpy2DAsync(V, sizeof(double) * kk, X, sizeof(double) * k, sizeof(double) * k, n,
-                                   cudaMemcpyDeviceToDevice, st));
-        if (s_in) {
-            rowscale_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(V, s_in, n, kk, V);
-            DCG_LAUNCHED();
-        }
+    (void)vbytes;
+    // V = s_in (.) X, padded to an even column count, in one pass (X itself
+    // when it needs neither: V is only read)
+    const double* Vin = V;
+    if (kk != k || s_in || (reinterpret_cast<uintptr_t>(X) & 15)) {
+        pad_scale_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(X, k, s_in, n, kk, V);
+        DCG_LAUNCHED();
     } else {
-        DCG_CUDA(cudaMemcpyAsync(V, X, vbytes, cudaMemcpyDeviceToDevice, st));
+        Vin = X;
     }
     int splits = 1;
     const int ntile = (kk + 7) / 8;
     switch (ntile) {
-        case 1: rc = launch_dmma<1>(ctx, st, K, ldk, rows, n, V, kk, P, splits); break;
-        case 2: rc = launch_dmma<2>(ctx, st, K, ldk, rows, n, V, kk, P, splits); break;
-        case 3: rc = launch_dmma<3>(ctx, st, K, ldk, rows, n, V, kk, P, splits); break;
-        case 4: rc = launch_dmma<4>(ctx, st, K, ldk, rows, n, V, kk, P, splits); break;
-        case 5: rc = launch_dmma<5>(ctx, st, K, ldk, rows, n, V, kk, P, splits); break;
-        case 6: rc = launch_dmma<6>(ctx, st, K, ldk, rows, n, V, kk, P, splits); break;
-        case 7: rc = launch_dmma<7>(ctx, st, K, ldk, rows, n, V, kk, P, splits); break;
-        default: rc = launch_dmma<8>(ctx, st, K, ldk, rows, n, V, kk, P, splits); break;
+        case 1: rc = launch_dmma<1>(ctx, st, K, ldk, rows, n, Vin, kk, P, splits); break;
+        case 2: rc = launch_dmma<2>(ctx, st, K, ldk, rows, n, Vin, kk, P, splits); break;
+        case 3: rc = launch_dmma<3>(ctx, st, K, ldk, rows, n, Vin, kk, P, splits); break;
+        case 4: rc = launch_dmma<4>(ctx, st, K, ldk, rows, n, Vin, kk, P, splits); break;
+        case 5: rc = launch_dmma<5>(ctx, st, K, ldk, rows, n, Vin, kk, P, splits); break;
+        case 6: rc = launch_dmma<6>(ctx, st, K, ldk, rows, n, Vin, kk, P, splits); break;
+        case 7: rc = launch_dmma<7>(ctx, st, K, ldk, rows, n, Vin, kk, P, splits); break;
+        default: rc = launch_dmma<8>(ctx, st, K, ldk, rows, n, Vin, kk, P, splits); break;
     }
     if (rc) return rc;
     if (kk == k) {
