@@ -498,10 +498,20 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Partials summed in CTA order; eight loads are issued ahead of their adds
+// (same order, same result: the loop had paid one L2 round trip per partial)
 __global__ void reduce_parts_kernel(const double* part, int nparts, int m, double* out) {
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
         double acc = 0.0;
-        for (int b = 0; b < nparts; ++b) acc += part[(long long)b * m + e];
+        int b = 0;
+        for (; b + 8 <= nparts; b += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = ld_cg(part + (long long)(b + u) * m + e);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc += v[u];
+        }
+        for (; b < nparts; ++b) acc += ld_cg(part + (long long)b * m + e);
         out[e] = acc;
     }
 }
