@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(DCG_NT, 1)
     dcg_grid_barrier(bar, gridDim.x);
     const long long q0 = sym_row_begin(n, gridDim.x, blockIdx.x);
     const long long q1 = sym_row_begin(n, gridDim.x, blockIdx.x + 1);
-    sym_pass2(n, colpart, rowpart, q0, q1, sym_range_table(smem), gridDim.x, smem, [&](long long i, double t) {
+    sym_pass2<true>(n, colpart, rowpart, q0, q1, sym_range_table(smem), gridDim.x, smem, [&](long long i, double t) {
         double val = s_out ? mul_rn(s_out[i], t) : t;
         if (shift != 0.0) val = add_rn(mul_rn(shift, v[i]), val);
         y[i] = val;
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(DCG_NT, 1)
     sym_fill_range_table(tbl, n, R);
     const long long q0 = sym_row_begin(n, gridDim.x, blockIdx.x);
     const long long q1 = sym_row_begin(n, gridDim.x, blockIdx.x + 1);
-    sym_pass2(n, colpart, rowpart, q0, q1, tbl, R, red, [&](long long i, double t) {
+    sym_pass2<true>(n, colpart, rowpart, q0, q1, tbl, R, red, [&](long long i, double t) {
         double val = s_out ? mul_rn(s_out[i], t) : t;
         if (shift != 0.0) val = add_rn(mul_rn(shift, v[i]), val);
         y[i] = val;
@@ -147,12 +147,12 @@ __global__ void __launch_bounds__(DCG_NT, 1)
     dcg_grid_barrier(bar, gridDim.x);
     const long long q0 = sym_row_begin(n, gridDim.x, blockIdx.x);
     const long long q1 = sym_row_begin(n, gridDim.x, blockIdx.x + 1);
-    sym_pass2(n, colpart, rowpart, q0, q1, sym_range_table(smem), gridDim.x, smem, [&](long long i, double t) {
+    sym_pass2<true>(n, colpart, rowpart, q0, q1, sym_range_table(smem), gridDim.x, smem, [&](long long i, double t) {
         double val = s_out1 ? mul_rn(s_out1[i], t) : t;
         if (shift1 != 0.0) val = add_rn(mul_rn(shift1, v1[i]), val);
         y1[i] = val;
     });
-    sym_pass2(n, colpart + part2, rowpart + part2, q0, q1, sym_range_table(smem), gridDim.x, smem,
+    sym_pass2<true>(n, colpart + part2, rowpart + part2, q0, q1, sym_range_table(smem), gridDim.x, smem,
               [&](long long i, double t) {
                   double val = s_out2 ? mul_rn(s_out2[i], t) : t;
                   if (shift2 != 0.0) val = add_rn(mul_rn(shift2, v2[i]), val);

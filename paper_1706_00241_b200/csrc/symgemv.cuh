@@ -471,7 +471,11 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
 // 16 / nwr warps sharing a row slice each sum a strided subset of the column
 // partials with up to 16 independent loads in flight, then the subsets are
 // combined in a fixed order.
-template <class Epi>
+// DEEP: two rounds of 16 partial loads in flight before their adds (the
+// standalone products; inside the persistent solve kernel, whose pass 1
+// shares the register budget, one round measured faster).  a[q] takes its
+// partials in the same sequence either way: bitwise the same sums.
+template <bool DEEP = false, class Epi>
 __device__ __forceinline__ void sym_pass2(long long n, const double* colpart, const double* rowpart, long long q0,
                                           long long q1, const long long* tbl, int nranges, double* red, Epi&& epi) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -499,15 +503,33 @@ __device__ __forceinline__ void sym_pass2(long long n, const double* colpart, co
             int Ip = (int)I + 1 + sub;
             const double* ptr = colpart + (sym_tile_row_base(Ip) + I) * DCG_TB + r;
             const long long sstep = (long long)S * (S + 1) / 2;
-            while (Ip < NTi) {
+            if constexpr (!DEEP) {
+                while (Ip < NTi) {
 #pragma unroll
-                for (int q = 0; q < 16; ++q) {
+                    for (int q = 0; q < 16; ++q) {
+                        if (Ip < NTi) {
+                            a[q] += ld_cg(ptr);
+                            ptr += ((long long)S * Ip + sstep) * DCG_TB;
+                            Ip += S;
+                        }
+                    }
+                }
+            }
+            while (DEEP && Ip < NTi) {
+                double v[32];
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    v[q] = 0.0;
                     if (Ip < NTi) {
-                        a[q] += ld_cg(ptr);
+                        v[q] = ld_cg(ptr);
                         ptr += ((long long)S * Ip + sstep) * DCG_TB;
                         Ip += S;
                     }
                 }
+#pragma unroll
+                for (int q = 0; q < 16; ++q) a[q] += v[q];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) a[q] += v[16 + q];
             }
 #pragma unroll
             for (int q = 0; q < 8; ++q) a[q] += a[q + 8];
