@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
             GSYNC();
             PHASE(1);
             if (a.timers && threadIdx.x == 0) tc0 = globaltimer_ns();
-            sym_pass2(n, a.colpart, a.rowpart, q0, q1, sym_range_table(s_g), G, s_g, epi);
+            sym_pass2<true>(n, a.colpart, a.rowpart, q0, q1, sym_range_table(s_g), G, s_g, epi);
             if (a.timers && threadIdx.x == 0) a.timers[16 + gridDim.x + blockIdx.x] += globaltimer_ns() - tc0;
             PHASE(2);
         } else {

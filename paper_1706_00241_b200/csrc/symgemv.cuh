@@ -81,11 +81,17 @@ __host__ __device__ __forceinline__ long long sym_tile_begin(long long n, long l
 
 // ---- pass-2 partition: rows weighted by their partial count -------------------
 // Row i of tile row I reads NT - 1 - I column partials, ~1 row-segment partial
-// and runs the epilogue: weight NT + 3 - I.  W(i) = weight of rows [0, i).
+// and runs the epilogue: weight NT + F - I.  W(i) = weight of rows [0, i).
+// F = DCG_SYM_ROW_FIXED prices a row's fixed cost (its row-segment partials,
+// the epilogue's loads and store) in partial loads: with F = 3 the last CTA,
+// all cheap rows, took 5.5 us against a 3.6 us mean (n = 10k).
+#ifndef DCG_SYM_ROW_FIXED
+#define DCG_SYM_ROW_FIXED 12
+#endif
 __host__ __device__ __forceinline__ long long sym_row_work(long long i, long long n) {
-    const long long NT = sym_ntiles_side(n);
+    const long long NT = sym_ntiles_side(n) + DCG_SYM_ROW_FIXED;
     const long long I = i / DCG_TB;
-    return DCG_TB * (I * (NT + 3) - I * (I - 1) / 2) + (i - I * DCG_TB) * (NT + 3 - I);
+    return DCG_TB * (I * NT - I * (I - 1) / 2) + (i - I * DCG_TB) * (NT - I);
 }
 __host__ __device__ __forceinline__ long long sym_row_begin(long long n, long long G, long long b) {
     if (b <= 0) return 0;
