@@ -11,14 +11,19 @@
 // Newton right-hand side and update, psi) with deterministic reductions.
 #include "common.cuh"
 
-#define RBF_T 32
+#define RBF_T 64     // tile edge (rows and columns per CTA)
+#define RBF_D 32     // dimensions staged per round
 
+// A CTA evaluates a 64 x 64 tile, 16 entries per thread (columns tx, tx + 32;
+// rows ty + 8 rr): the staging and barriers of a tile are shared by four
+// times the entries of a 32 x 32 tile.
 __global__ void __launch_bounds__(256)
     rbf_tile_kernel(const double* __restrict__ xr, long long nr_total, const double* __restrict__ xc,
                     long long nc, long long dim, double var, double inv2l2, double jitter, int gram,
                     long long row0, long long rows, double* out, long long ldo) {
-    __shared__ double sr[RBF_T][RBF_T + 1];
-    __shared__ double sc[RBF_T][RBF_T + 1];
+    __shared__ double sbuf[2 * RBF_T * (RBF_D + 1)];
+    double (*sr)[RBF_D + 1] = reinterpret_cast<double (*)[RBF_D + 1]>(sbuf);
+    double (*sc)[RBF_D + 1] = reinterpret_cast<double (*)[RBF_D + 1]>(sbuf + RBF_T * (RBF_D + 1));
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
     const long long i0 = (long long)blockIdx.y * RBF_T;        // local row tile
     const long long j0 = (long long)blockIdx.x * RBF_T;
@@ -27,47 +32,62 @@ __global__ void __launch_bounds__(256)
     // mirrored value is the directly evaluated one bit for bit (see above)
     const bool mirror = gram && row0 == 0 && rows == nc;
     if (mirror && blockIdx.x > blockIdx.y) return;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (long long t0 = 0; t0 < dim; t0 += RBF_T) {
-        const int tn = (int)min((long long)RBF_T, dim - t0);
-        for (int e = threadIdx.x; e < RBF_T * RBF_T; e += 256) {
-            const int r = e / RBF_T, t = e % RBF_T;
+    double acc[8][2];
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) acc[rr][0] = acc[rr][1] = 0.0;
+    for (long long t0 = 0; t0 < dim; t0 += RBF_D) {
+        const int tn = (int)min((long long)RBF_D, dim - t0);
+        for (int e = threadIdx.x; e < RBF_T * RBF_D; e += 256) {
+            const int r = e / RBF_D, t = e % RBF_D;
             const long long gi = row0 + i0 + r, gj = j0 + r;
             sr[r][t] = (t < tn && i0 + r < rows) ? xr[gi * dim + t0 + t] : 0.0;
             sc[r][t] = (t < tn && gj < nc) ? xc[gj * dim + t0 + t] : 0.0;
         }
         cta_sync();
+        for (int t = 0; t < tn; ++t) {
+            const double c0 = sc[tx][t], c1 = sc[tx + 32][t];
 #pragma unroll
-        for (int rr = 0; rr < 4; ++rr) {
-            const int r = ty + 8 * rr;
-            for (int t = 0; t < tn; ++t) {
-                const double diff = sub_rn(sr[r][t], sc[tx][t]);
-                acc[rr] = add_rn(acc[rr], mul_rn(diff, diff));
+            for (int rr = 0; rr < 8; ++rr) {
+                const double rv = sr[ty + 8 * rr][t];
+                const double d0 = sub_rn(rv, c0), d1 = sub_rn(rv, c1);
+                acc[rr][0] = add_rn(acc[rr][0], mul_rn(d0, d0));
+                acc[rr][1] = add_rn(acc[rr][1], mul_rn(d1, d1));
             }
         }
         cta_sync();
     }
-    const long long j = j0 + tx;
-    double vals[4];
+    double vals[8][2];
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
+    for (int rr = 0; rr < 8; ++rr) {
         const long long li = i0 + ty + 8 * rr;
         const long long gi = row0 + li;
-        double val;
-        if (gram && gi == j) val = add_rn(var, jitter);
-        else val = mul_rn(var, exp(mul_rn(-acc[rr], inv2l2)));
-        vals[rr] = val;
-        if (j < nc && li < rows) out[li * ldo + j] = val;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const long long j = j0 + tx + 32 * h;
+            double val;
+            if (gram && gi == j) val = add_rn(var, jitter);
+            else val = mul_rn(var, exp(mul_rn(-acc[rr][h], inv2l2)));
+            vals[rr][h] = val;
+            if (j < nc && li < rows) out[li * ldo + j] = val;
+        }
     }
     if (!mirror || blockIdx.x == blockIdx.y) return;
-    // transposed copy through shared memory (sr is free again): coalesced rows
+    // transposed copy through shared memory (the staging buffer is free
+    // again): rows of the mirror tile stored coalesced
+    double (*tt)[RBF_T + 1] = reinterpret_cast<double (*)[RBF_T + 1]>(sbuf);
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr) sr[ty + 8 * rr][tx] = vals[rr];
+    for (int rr = 0; rr < 8; ++rr) {
+        tt[ty + 8 * rr][tx] = vals[rr][0];
+        tt[ty + 8 * rr][tx + 32] = vals[rr][1];
+    }
     cta_sync();
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
-        const long long orow = j0 + ty + 8 * rr, ocol = i0 + tx;   // K[j][i] = K[i][j]
-        if (orow < nc && ocol < rows) out[orow * ldo + ocol] = sr[tx][ty + 8 * rr];
+    for (int rr = 0; rr < 8; ++rr) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const long long orow = j0 + ty + 8 * rr, ocol = i0 + tx + 32 * h;   // K[j][i] = K[i][j]
+            if (orow < nc && ocol < rows) out[orow * ldo + ocol] = tt[tx + 32 * h][ty + 8 * rr];
+        }
     }
 }
 
