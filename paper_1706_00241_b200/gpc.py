@@ -108,7 +108,9 @@ def rbf_kernel(x, params, jitter=None, matrix_free=False):
     if matrix_free:
         return RbfOperator(xd.contiguous(), var, inv_two_ell2, var + float(jitter))
     ld = D.padded_ld(n)
-    kbuf = D.zeros(n, ld) if ld != n else D.empty(n, ld)
+    kbuf = D.empty(n, ld)
+    if ld != n:
+        kbuf[:, n:].zero_()   # only the row-pitch padding (the kernel writes every entry of K)
     if n:
         N.check(N.lib().dcg_k_rbf_gram(D.ctx(), D.stream(), xd.data_ptr(), n, dim, var, inv_two_ell2, float(jitter),
                                        kbuf.data_ptr(), ld, 0, n), what="rbf_gram")
