@@ -25,11 +25,43 @@ size_t dcg_pencil_smem(int T);
 #define EX_ROWS 32
 
 // ---------------------------------------------------------------------------- E1
-__global__ void __launch_bounds__(EX_NT)
-    zgather_kernel(long long n, int kp, const double* __restrict__ Wp, const double* __restrict__ AWp, int m,
-                   const double* __restrict__ P, const double* __restrict__ R, const double* __restrict__ alpha,
-                   int k, double* Zraw, double* AZraw, double* part, unsigned int* counter, double* norms, int* keep,
-                   DevStatus* plan, const DevStatus* solve_st) {
+// Column norms from the per-CTA partials (one warp per column, CTA order),
+// the keep list of non-zero columns and the plan.  Results in shared memory
+// (s_norm, s_keep, *s_t); `norms` (when non-null), keep and plan in global.
+__device__ void zgather_finish(int T, int k, const double* part, double* s_norm, int* s_keep, int* s_t,
+                               double* norms, int* keep, DevStatus* plan) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int c = warp; c < T; c += EX_NT / 32) {
+        double s = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) s += ld_cg(part + (long long)b * T + c);
+        s = warp_sum(s);
+        if (lane == 0) {
+            s_norm[c] = sqrt(s);
+            if (norms) norms[c] = s_norm[c];
+        }
+    }
+    cta_sync();
+    if (tid == 0) {
+        int t = 0;
+        for (int c = 0; c < T; ++c)
+            if (s_norm[c] > 0.0) s_keep[t++] = c;
+        *s_t = t;
+        if (norms) {
+            for (int c = 0; c < t; ++c) keep[c] = s_keep[c];
+            plan->count = t;
+            plan->info = t;
+            plan->aux = T;   // column stride of Zraw / AZraw
+            plan->status = (t < k) ? DCG_E_BASIS_DEFICIENT : DCG_OK;   // recycle.py:131-132
+        }
+    }
+    cta_sync();
+}
+
+__device__ void zgather_body(long long n, int kp, const double* __restrict__ Wp, const double* __restrict__ AWp,
+                             int m, const double* __restrict__ P, const double* __restrict__ R,
+                             const double* __restrict__ alpha, int k, double* Zraw, double* AZraw, double* part,
+                             unsigned int* counter, double* norms, int* keep, DevStatus* plan,
+                             const DevStatus* solve_st, bool coop, double* s_norm, int* s_keep, int* s_t) {
     extern __shared__ double sm[];
     if (solve_st) {
         // device-driven form: the finished solve's status block gives the
@@ -46,6 +78,8 @@ __global__ void __launch_bounds__(EX_NT)
                 plan->count = kp + m;
                 plan->aux = kp + m;
             }
+            if (threadIdx.x == 0) *s_t = -1;   // nothing to scale (uniform over the grid)
+            cta_sync();
             return;
         }
     }
@@ -80,25 +114,29 @@ __global__ void __launch_bounds__(EX_NT)
         cta_sync();
     }
     if (tid < T) part[(long long)blockIdx.x * T + tid] = acc;
+    if (coop) {
+        // fused stage: every CTA forms the norms and the keep list itself
+        // after a grid barrier (same partial order: same values); CTA 0
+        // publishes them with the plan
+        dcg_grid_barrier(counter + 2, gridDim.x);
+        zgather_finish(T, k, part, s_norm, s_keep, s_t, blockIdx.x == 0 ? norms : nullptr, keep, plan);
+        return;
+    }
     if (!cta_last_arrival(counter, gridDim.x)) return;
     // last CTA: norms (one warp per column), keep list, plan
-    const int lane = tid & 31, warp = tid >> 5;
-    for (int c = warp; c < T; c += EX_NT / 32) {
-        double s = 0.0;
-        for (int b = lane; b < (int)gridDim.x; b += 32) s += ld_cg(part + (long long)b * T + c);
-        s = warp_sum(s);
-        if (lane == 0) norms[c] = sqrt(s);
-    }
-    cta_sync();
-    if (tid == 0) {
-        int t = 0;
-        for (int c = 0; c < T; ++c)
-            if (norms[c] > 0.0) keep[t++] = c;
-        plan->count = t;
-        plan->info = t;
-        plan->aux = T;   // column stride of Zraw / AZraw
-        plan->status = (t < k) ? DCG_E_BASIS_DEFICIENT : DCG_OK;   // recycle.py:131-132
-    }
+    zgather_finish(T, k, part, s_norm, s_keep, s_t, norms, keep, plan);
+}
+
+__global__ void __launch_bounds__(EX_NT)
+    zgather_kernel(long long n, int kp, const double* __restrict__ Wp, const double* __restrict__ AWp, int m,
+                   const double* __restrict__ P, const double* __restrict__ R, const double* __restrict__ alpha,
+                   int k, double* Zraw, double* AZraw, double* part, unsigned int* counter, double* norms, int* keep,
+                   DevStatus* plan, const DevStatus* solve_st) {
+    __shared__ double s_norm[DCG_MAX_T];
+    __shared__ int s_keep[DCG_MAX_T];
+    __shared__ int s_t;
+    zgather_body(n, kp, Wp, AWp, m, P, R, alpha, k, Zraw, AZraw, part, counter, norms, keep, plan, solve_st, false,
+                 s_norm, s_keep, &s_t);
 }
 
 // ---------------------------------------------------------------------------- E2
@@ -109,21 +147,17 @@ __global__ void __launch_bounds__(EX_NT)
 // (fg_reduce then sums the CTAs in a fixed order), as before.
 #define FG_BI 4
 #define FG_BJ 8
-__global__ void __launch_bounds__(EX_NT)
-    zscale_fg_kernel(long long n, const double* __restrict__ Zraw, const double* __restrict__ AZraw,
-                     const double* __restrict__ norms, const int* __restrict__ keep, const DevStatus* plan, double* Zs,
-                     double* AZs, double* part) {
-    if (plan->status != DCG_OK) return;
+__device__ void zscale_fg_body(long long n, const double* __restrict__ Zraw, const double* __restrict__ AZraw,
+                               const double* norms, const int* keep, int T, int Tk, int region, double* Zs,
+                               double* AZs, double* part) {
     extern __shared__ double sm[];
-    const int T = (int)plan->aux;
-    const int Tk = (int)plan->count;
     const int npairs = 2 * Tk * Tk;
     // staged rows: [zs | azs] per row, 2 Tk wide, so b' indexes one array
     double* za = sm;                    // EX_ROWS x 2 Tk
     const int tid = threadIdx.x;
     // blockIdx.y picks the 64 x 128 region of the (a, b') grid (one region for Tk <= 64)
     const int nbj = (2 * Tk + 16 * FG_BJ - 1) / (16 * FG_BJ);
-    const int a0 = (blockIdx.y / nbj) * 16 * FG_BI, b0 = (blockIdx.y % nbj) * 16 * FG_BJ;
+    const int a0 = (region / nbj) * 16 * FG_BI, b0 = (region % nbj) * 16 * FG_BJ;
     if (a0 >= Tk) return;
     const int ta = a0 + (tid >> 4), tb = b0 + (tid & 15);
     const long long r0 = part_begin(n, gridDim.x, blockIdx.x), r1 = part_begin(n, gridDim.x, blockIdx.x + 1);
@@ -144,7 +178,7 @@ __global__ void __launch_bounds__(EX_NT)
             const double av = div_rn(AZraw[(i0 + r) * T + c], nv);
             za[r * W + cc] = zv;
             za[r * W + Tk + cc] = av;
-            if (blockIdx.y == 0) {
+            if (region == 0) {
                 Zs[(i0 + r) * Tk + cc] = zv;
                 AZs[(i0 + r) * Tk + cc] = av;
             }
@@ -180,6 +214,38 @@ __global__ void __launch_bounds__(EX_NT)
             if (b < Tk) out[a * Tk + b] = acc[i][j];
             else if (b < W) out[Tk * Tk + a * Tk + (b - Tk)] = acc[i][j];
         }
+    }
+}
+
+__global__ void __launch_bounds__(EX_NT)
+    zscale_fg_kernel(long long n, const double* __restrict__ Zraw, const double* __restrict__ AZraw,
+                     const double* __restrict__ norms, const int* __restrict__ keep, const DevStatus* plan, double* Zs,
+                     double* AZs, double* part) {
+    if (plan->status != DCG_OK) return;
+    zscale_fg_body(n, Zraw, AZraw, norms, keep, (int)plan->aux, (int)plan->count, blockIdx.y, Zs, AZs, part);
+}
+
+// E1 + E2 as one cooperative launch (the norms after a grid barrier instead
+// of a last-CTA pass and a second launch): same row partition, same partial
+// orders, so the same Zs, AZs and F / G partials.  The F / G regions run one
+// after the other in each CTA.
+__global__ void __launch_bounds__(EX_NT)
+    zstage1_coop_kernel(long long n, int kp, const double* __restrict__ Wp, const double* __restrict__ AWp, int m,
+                        const double* __restrict__ P, const double* __restrict__ R, const double* __restrict__ alpha,
+                        int k, double* Zraw, double* AZraw, double* part, unsigned int* counter, double* norms,
+                        int* keep, DevStatus* plan, const DevStatus* solve_st, int nregions, double* Zs, double* AZs,
+                        double* fgpart) {
+    __shared__ double s_norm[DCG_MAX_T];
+    __shared__ int s_keep[DCG_MAX_T];
+    __shared__ int s_t;
+    zgather_body(n, kp, Wp, AWp, m, P, R, alpha, k, Zraw, AZraw, part, counter, norms, keep, plan, solve_st, true,
+                 s_norm, s_keep, &s_t);
+    const int t = s_t;
+    if (t < 0 || t < k) return;   // failed / deficient: uniform over the grid
+    const int T = solve_st ? (int)(solve_st->pad + solve_st->aux) : kp + m;
+    for (int y = 0; y < nregions; ++y) {
+        zscale_fg_body(n, Zraw, AZraw, s_norm, s_keep, T, t, y, Zs, AZs, fgpart);
+        cta_sync();
     }
 }
 
@@ -390,15 +456,29 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
     if (stage == 0 || stage == 1) {
     DCG_CUDA(cudaMemsetAsync(plan, 0, al(sizeof(DevStatus)) * 2, st));
     DCG_CUDA(cudaMemsetAsync(counters, 0, 16, st));
-    DCG_CUDA(cudaFuncSetAttribute(zgather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
-    zgather_kernel<<<nb, EX_NT, sm1, st>>>(n, (int)kp, Wp, AWp, (int)m, P, R, alpha, (int)k, Zraw, AZraw, part,
-                                           counters, norms, keep, plan, solve_st);
-    DCG_LAUNCHED();
     // regions of 64 x 128 (a, b') entries; Tk <= T decides on the device which are live
-    const int gy = (int)(((T + 16 * FG_BI - 1) / (16 * FG_BI)) * ((2 * T + 16 * FG_BJ - 1) / (16 * FG_BJ)));
-    DCG_CUDA(cudaFuncSetAttribute(zscale_fg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
-    zscale_fg_kernel<<<dim3(nb, gy), EX_NT, sm1, st>>>(n, Zraw, AZraw, norms, keep, plan, Zs, AZs, fgpart);
-    DCG_LAUNCHED();
+    int gy = (int)(((T + 16 * FG_BI - 1) / (16 * FG_BI)) * ((2 * T + 16 * FG_BJ - 1) / (16 * FG_BJ)));
+    // one cooperative launch when the grid is co-resident (it is: nb <= SMs)
+    int per_sm = 0;
+    DCG_CUDA(cudaFuncSetAttribute(zstage1_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+    DCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, zstage1_coop_kernel, EX_NT, sm1));
+    if ((long long)per_sm * G >= nb) {
+        int ikp = (int)kp, im = (int)m, ik = (int)k;
+        void* args[] = {(void*)&n,    (void*)&ikp,   (void*)&Wp,     (void*)&AWp,   (void*)&im,      (void*)&P,
+                        (void*)&R,    (void*)&alpha, (void*)&ik,     (void*)&Zraw,  (void*)&AZraw,   (void*)&part,
+                        (void*)&counters, (void*)&norms, (void*)&keep, (void*)&plan, (void*)&solve_st, (void*)&gy,
+                        (void*)&Zs,   (void*)&AZs,   (void*)&fgpart};
+        DCG_CUDA(cudaLaunchCooperativeKernel((const void*)zstage1_coop_kernel, dim3(nb), dim3(EX_NT), args, sm1, st));
+        dcg_count_launch();
+    } else {
+        DCG_CUDA(cudaFuncSetAttribute(zgather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+        zgather_kernel<<<nb, EX_NT, sm1, st>>>(n, (int)kp, Wp, AWp, (int)m, P, R, alpha, (int)k, Zraw, AZraw, part,
+                                               counters, norms, keep, plan, solve_st);
+        DCG_LAUNCHED();
+        DCG_CUDA(cudaFuncSetAttribute(zscale_fg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+        zscale_fg_kernel<<<dim3(nb, gy), EX_NT, sm1, st>>>(n, Zraw, AZraw, norms, keep, plan, Zs, AZs, fgpart);
+        DCG_LAUNCHED();
+    }
     const int warps = (int)(2 * T * T);
     fg_reduce_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>(fgpart, nb, plan, Fraw, Graw);
     DCG_LAUNCHED();
