@@ -208,13 +208,20 @@ def _update_dev(state, inner, s, x):
 
 class _PendingObjective:
     """(loglik, psi) of an enqueued newton update: copied to pinned host memory
-    right behind the derivative kernels, read on demand."""
+    on the copy stream right behind the derivative kernels (off the main
+    stream, which goes on with the next system), read on demand."""
 
     def __init__(self, llpsi):
         self.host = _pinned(2)
-        self.host.view(torch.float64)[:2].copy_(llpsi, non_blocking=True)
-        self.event = torch.cuda.Event()
-        self.event.record()
+        ready = torch.cuda.Event()
+        ready.record()
+        cs = D.copy_stream()
+        cs.wait_event(ready)
+        with torch.cuda.stream(cs):
+            self.host.view(torch.float64)[:2].copy_(llpsi, non_blocking=True)
+            self.event = torch.cuda.Event()
+            self.event.record(cs)
+        llpsi.record_stream(cs)
 
     def get(self):
         self.event.synchronize()
