@@ -128,8 +128,9 @@ def test_deficient_extraction_on_device(P):
     assert ss.basis is None
 
 
-@pytest.mark.parametrize("n", [300, 1000, 2113])
-def test_fused_newton_system_matches_separate_products(P, n):
+@pytest.mark.parametrize("strategy", ["sym", "rows"])
+@pytest.mark.parametrize("n", [300, 1000, 2113, 4500])
+def test_fused_newton_system_matches_separate_products(P, n, strategy):
     """dcg_gpc_newton_system_ax0 (b and ax0 = A x_prev from one pass over a
     symmetric-stored K, sym_pass1<NV = 2>) equals newton_system followed by
     the operator's own A x_prev bitwise: same tile partition, same partial
@@ -138,7 +139,7 @@ def test_fused_newton_system_matches_separate_products(P, n):
 
     rng = np.random.default_rng(n)
     x = rng.standard_normal((n, 4))
-    gram = P.rbf_kernel(x, P.KernelParams(1.0, 1.3))
+    gram = P.rbf_kernel(x, P.KernelParams(1.0, 1.3)).with_strategy(strategy)   # "sym": the fused pass
     y = np.where(rng.standard_normal(n) > 0, 1.0, -1.0)
     state = G.make_state(gram, torch.from_numpy(y).cuda())
     state.f = torch.from_numpy(rng.standard_normal(n)).cuda()
