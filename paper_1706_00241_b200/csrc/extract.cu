@@ -398,6 +398,115 @@ __global__ void __launch_bounds__(EX_NT)
     }
 }
 
+// E5 + E6 as one cooperative launch: the ||Zs u_j|| partials, a grid barrier,
+// every CTA forms the scales from the partials (warp per column, CTA order:
+// the values of uscale's last CTA) and scales its shared copy of U, then
+// W_next / AW_next for its row blocks (each element as in wnext).  No U
+// round trip through global memory, one launch instead of two.
+__global__ void __launch_bounds__(EX_NT)
+    tail_coop_kernel(long long n, int k, const double* __restrict__ Zs, const double* __restrict__ AZs,
+                     const DevStatus* plan, const DevStatus* pencil, double* U, const int* active, double* part,
+                     unsigned int* bar, double* w_next, double* aw_next, long long* result) {
+    const bool ok = plan->status == DCG_OK && pencil->status == DCG_OK;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (plan->status != DCG_OK) {
+            result[0] = plan->status;
+            result[1] = plan->info;
+            result[2] = plan->count;
+        } else {
+            result[0] = pencil->status;
+            result[1] = pencil->info;
+            result[2] = pencil->count;
+        }
+    }
+    if (!ok) return;
+    extern __shared__ double sm[];
+    const int Tk = (int)plan->count, na = (int)pencil->count;
+    double* ue = sm;                       // Tk x k (unscaled, then scaled)
+    double* wp = ue + Tk * k;              // 16 row slots x 64
+    double* zr = wp + 16 * 64;             // EX_ROWS x Tk
+    double* ar = zr + EX_ROWS * Tk;        // EX_ROWS x Tk
+    __shared__ double scale[DCG_MAX_K];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < Tk * k; e += EX_NT) ue[e] = 0.0;
+    cta_sync();
+    for (int e = tid; e < na * k; e += EX_NT) ue[active[e / k] * k + e % k] = U[e];
+    // ---- E5: partial column norms (uscale's thread grid and order)
+    const long long r0 = part_begin(n, gridDim.x, blockIdx.x), r1 = part_begin(n, gridDim.x, blockIdx.x + 1);
+    const int rs = tid >> 4, jg = tid & 15;
+    double sq[4] = {0.0, 0.0, 0.0, 0.0};
+    for (long long i0 = r0; i0 < r1; i0 += EX_ROWS) {
+        const int nr = (int)min((long long)EX_ROWS, r1 - i0);
+        cta_sync();
+        for (int e = tid; e < nr * Tk; e += EX_NT) zr[e] = Zs[i0 * Tk + e];
+        cta_sync();
+        for (int rr = rs; rr < nr; rr += 16) {
+            const double* z = zr + rr * Tk;
+            double v[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int c = 0; c < Tk; ++c) {
+                const double zc = z[c];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (jg + 16 * q < k) v[q] = fma(zc, ue[c * k + jg + 16 * q], v[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) sq[q] = fma(v[q], v[q], sq[q]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) wp[rs * 64 + jg + 16 * q] = sq[q];
+    cta_sync();
+    if (tid < k) {
+        double sacc = 0.0;
+        for (int w = 0; w < 16; ++w) sacc += wp[w * 64 + tid];
+        part[(long long)blockIdx.x * k + tid] = sacc;
+    }
+    dcg_grid_barrier(bar, gridDim.x);
+    for (int j = warp; j < k; j += EX_NT / 32) {
+        double sacc = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) sacc += ld_cg(part + (long long)b * k + j);
+        sacc = warp_sum(sacc);
+        if (lane == 0) scale[j] = sqrt(sacc);
+    }
+    cta_sync();
+    // u[:, j] /= ||Z u_j|| when positive (recycle.py:150-153), in shared memory;
+    // CTA 0 also leaves the scaled U in global memory (the caller's copy)
+    for (int e = tid; e < na * k; e += EX_NT) {
+        const double sc = scale[e % k];
+        const double u = sc > 0.0 ? div_rn(U[e], sc) : U[e];
+        ue[active[e / k] * k + e % k] = u;
+    }
+    cta_sync();
+    dcg_grid_barrier(bar, gridDim.x);   // every CTA has read the unscaled U
+    if (blockIdx.x == 0)
+        for (int e = tid; e < na * k; e += EX_NT) U[e] = ue[active[e / k] * k + e % k];
+    // ---- E6: W_next = Zs U, AW_next = AZs U (wnext's element order)
+    const long long nblk = (n + EX_ROWS - 1) / EX_ROWS;
+    for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const long long i0 = blk * EX_ROWS;
+        const int nr = (int)min((long long)EX_ROWS, n - i0);
+        cta_sync();
+        for (int e = tid; e < nr * Tk; e += EX_NT) {
+            zr[e] = Zs[i0 * Tk + e];
+            ar[e] = AZs[i0 * Tk + e];
+        }
+        cta_sync();
+        for (int e = tid; e < nr * k; e += EX_NT) {
+            const int rr = e / k, j = e - (e / k) * k;
+            const double* z = zr + rr * Tk;
+            const double* az = ar + rr * Tk;
+            double a = 0.0, b = 0.0;
+            for (int c = 0; c < Tk; ++c) {
+                const double u = ue[c * k + j];
+                a = add_rn(a, mul_rn(z[c], u));
+                b = add_rn(b, mul_rn(az[c], u));
+            }
+            w_next[(i0 + rr) * k + j] = a;
+            aw_next[(i0 + rr) * k + j] = b;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------- launch
 static size_t extract_ws_bytes(dcg_context* ctx, long long n, int T, int k) {
     const int G = ctx->sm_count;
@@ -490,6 +599,25 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
         if (rc) return rc;
     }
     if (stage == 3) return DCG_OK;
+    // the cooperative tail (no z_out requested: the device-driven pipeline)
+    if (!d_z) {
+        const size_t smt = sizeof(double) * ((size_t)T * k + 16 * 64 + 2 * (size_t)EX_ROWS * T);
+        int per_sm = 0;
+        DCG_CUDA(cudaFuncSetAttribute(tail_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smt));
+        DCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tail_coop_kernel, EX_NT, smt));
+        if ((long long)per_sm * G >= nb) {
+            DCG_CUDA(cudaMemsetAsync(counters + 3, 0, sizeof(unsigned int), st));
+            int ik = (int)k;
+            unsigned int* bar = counters + 3;
+            void* args[] = {(void*)&n,      (void*)&ik,     (void*)&Zs,      (void*)&AZs,      (void*)&plan,
+                            (void*)&pencil, (void*)&U,      (void*)&active,  (void*)&upart,    (void*)&bar,
+                            (void*)&d_w_next, (void*)&d_aw_next, (void*)&d_result};
+            DCG_CUDA(cudaLaunchCooperativeKernel((const void*)tail_coop_kernel, dim3(nb), dim3(EX_NT), args, smt, st));
+            dcg_count_launch();
+            if (d_u) DCG_CUDA(cudaMemcpyAsync(d_u, U, sizeof(double) * T * k, cudaMemcpyDeviceToDevice, st));
+            return DCG_OK;
+        }
+    }
     const size_t sm5 = sizeof(double) * ((size_t)T * k + 16 * 64 + (size_t)EX_ROWS * T);
     DCG_CUDA(cudaFuncSetAttribute(uscale_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm5));
     uscale_kernel<<<nb, EX_NT, sm5, st>>>(n, (int)k, Zs, plan, pencil, U, active, Uexp, upart, counters + 1);
