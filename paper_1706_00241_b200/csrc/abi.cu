@@ -51,7 +51,7 @@ int dcg_k_jacobi_sweep_launch(cudaStream_t, double*, double*, int, DevStatus*);
 int dcg_rbf_launch(cudaStream_t, const double*, long long, const double*, long long, long long, double, double,
                    double, int, long long, long long, double*, long long);
 int dcg_derivs_launch(dcg_context*, cudaStream_t, long long, const double*, const double*, const double*, double*,
-                      double*, double*, DevStatus*);
+                      double*, double*, DevStatus*, double* llpsi = nullptr);
 int dcg_newton_prep_launch(dcg_context*, cudaStream_t, long long, const double*, const double*, const double*,
                            double*, double*);
 int dcg_newton_a_launch(dcg_context*, cudaStream_t, long long, const double*, const double*, const double*,
@@ -778,11 +778,8 @@ extern "C" int dcg_gpc_newton_update_async(dcg_context* ctx, void* stream, const
     if (rc) return rc;
     rc = apply_k(ctx, st, kop, d_a, nullptr, nullptr, 0.0, d_f, scratch);
     if (rc) return rc;
-    rc = dcg_derivs_launch(ctx, st, n, d_f, d_y, d_a, d_grad, d_h, part, ds);
-    if (rc) return rc;
-    static_assert(offsetof(DevStatus, value2) == offsetof(DevStatus, value) + sizeof(double), "DevStatus layout");
-    DCG_CUDA(cudaMemcpyAsync(d_llpsi, &ds->value, 2 * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    return DCG_OK;
+    // the finalize kernel writes (loglik, psi) to d_llpsi itself
+    return dcg_derivs_launch(ctx, st, n, d_f, d_y, d_a, d_grad, d_h, part, ds, d_llpsi);
 }
 
 extern "C" int dcg_gpc_newton_update(dcg_context* ctx, void* stream, const dcg_operator* kop, const double* d_inner,

@@ -143,7 +143,7 @@ __global__ void derivs_kernel(long long n, const double* f, const double* y, con
     }
 }
 
-__global__ void derivs_finalize_kernel(const double* part, int nb, DevStatus* st) {
+__global__ void derivs_finalize_kernel(const double* part, int nb, DevStatus* st, double* llpsi) {
     __shared__ double red[40];
     double ll = 0.0, fa = 0.0;
     for (int b = threadIdx.x; b < nb; b += blockDim.x) {
@@ -157,6 +157,10 @@ __global__ void derivs_finalize_kernel(const double* part, int nb, DevStatus* st
         st->status = DCG_OK;
         st->value = loglik;
         st->value2 = sub_rn(loglik, mul_rn(0.5, fa));   // psi = loglik - f'a/2 (gpc.py:209)
+        if (llpsi) {
+            llpsi[0] = st->value;
+            llpsi[1] = st->value2;
+        }
     }
 }
 
@@ -191,12 +195,12 @@ __global__ void newton_a_kernel(long long n, const double* inner, const double* 
 }
 
 int dcg_derivs_launch(dcg_context* ctx, cudaStream_t st, long long n, const double* f, const double* y,
-                      const double* a, double* grad, double* h, double* part, DevStatus* ds) {
+                      const double* a, double* grad, double* h, double* part, DevStatus* ds, double* llpsi) {
     int nb = ctx->sm_count * 2;
     if ((long long)nb * 256 > n) nb = (int)max(1LL, (n + 255) / 256);
     derivs_kernel<<<nb, 256, 0, st>>>(n, f, y, a, grad, h, part);
     DCG_LAUNCHED();
-    derivs_finalize_kernel<<<1, 256, 0, st>>>(part, nb, ds);
+    derivs_finalize_kernel<<<1, 256, 0, st>>>(part, nb, ds, llpsi);
     DCG_LAUNCHED();
     return DCG_OK;
 }
