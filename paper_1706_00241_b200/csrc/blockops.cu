@@ -372,13 +372,16 @@ static int launch_dmma(dcg_context* ctx, cudaStream_t st, const double* K, long 
                        int& splits_out) {
     constexpr int KP = NTILE * 8;
     const size_t smem = sizeof(double) * (size_t)(2 * GM_BM * GM_SA + 2 * GM_BK * (KP + 4));
-    DCG_CUDA(cudaFuncSetAttribute(dmma_gemm_kernel<NTILE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    int per_sm = 0;
-    DCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmma_gemm_kernel<NTILE>, 256, smem));
-    if (per_sm < 1) per_sm = 1;
+    // attribute and occupancy once per instantiation (one device per
+    // process): these host calls sat between the refresh's launches
+    static int per_sm = 0;
+    if (per_sm == 0) {
+        DCG_CUDA(cudaFuncSetAttribute(dmma_gemm_kernel<NTILE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        DCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmma_gemm_kernel<NTILE>, 256, smem));
+    }
     const long long row_tiles = (rows + GM_BM - 1) / GM_BM;
-    const long long target = 2LL * per_sm * ctx->sm_count;          // ~2 waves
+    const long long target = 2LL * (per_sm < 1 ? 1 : per_sm) * ctx->sm_count;   // ~2 waves
     long long splits = (target + row_tiles - 1) / row_tiles;
     const long long max_splits = (n + GM_BK - 1) / GM_BK;
     if (splits > max_splits) splits = max_splits;

@@ -309,17 +309,24 @@ def solve_next_async(state, a, b, ax0=None, ax0_of=None):
         # while the extraction of the basis is still going on
         if ax0 is None or ax0_of is None or ax0_of is not state.x_last:
             ax0 = op.matvec_dev(x_prev)
-        pending.join(main)
-        pending.keep_alive = None   # main-stream work is now ordered after the extraction
+        # (joined right before the refresh launch below: the host-side set-up
+        # of the refresh then overlaps the device's work instead of idling it)
         w_src, valid = pending.w_next, pending.result
     elif pending is not None and pending.k > 0:
         w_src = pending.w_dev
     kmax = 0 if w_src is None else int(w_src.shape[1])
     cb, kdev, bufs = None, None, None
+    if isinstance(pending, _PendingBasis) and not kmax:
+        pending.join(main)
+        pending.keep_alive = None
     if kmax:
         w_out, aw_out, chol = D.empty(n, kmax), D.empty(n, kmax), D.empty(kmax, kmax)
         kdev = torch.empty(1, dtype=torch.int64, device=D.device())
-        N.check(N.lib().dcg_refresh_basis_async(D.ctx(), D.stream(), ctypes.byref(op.c_struct()), w_src.data_ptr(),
+        cop = op.c_struct()
+        if isinstance(pending, _PendingBasis):
+            pending.join(main)
+            pending.keep_alive = None   # main-stream work is now ordered after the extraction
+        N.check(N.lib().dcg_refresh_basis_async(D.ctx(), D.stream(), ctypes.byref(cop), w_src.data_ptr(),
                                                 kmax, valid.data_ptr() if valid is not None else None,
                                                 w_out.data_ptr(), aw_out.data_ptr(), chol.data_ptr(),
                                                 kdev.data_ptr()), what="refresh_basis_async")
