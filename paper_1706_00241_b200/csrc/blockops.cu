@@ -121,7 +121,7 @@ int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, long long 
     const int G = navail < DCG_SYM_MAX_CTAS ? navail : DCG_SYM_MAX_CTAS;
     // one cooperative launch: pass 1, grid barrier, pass 2 (barrier word after the partials)
     unsigned int* bar = reinterpret_cast<unsigned int*>(rowpart + ntt * DCG_TB);
-    DCG_CUDA(cudaFuncSetAttribute(sym_apply_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DCG_SMEM_ATTR(sym_apply_coop_kernel, smem);
     DCG_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), st));
     void* args[] = {(void*)&K, (void*)&ldk, (void*)&n, (void*)&v, (void*)&s_in, (void*)&s_out, (void*)&shift,
                     (void*)&colpart, (void*)&rowpart, (void*)&y, (void*)&bar};
@@ -176,7 +176,7 @@ int dcg_sym_apply2(dcg_context* ctx, cudaStream_t st, const double* K, long long
     const int navail = ctx->sm_count > 1 ? ctx->sm_count - 1 : 1;
     const int G = navail < DCG_SYM_MAX_CTAS ? navail : DCG_SYM_MAX_CTAS;
     unsigned int* bar = reinterpret_cast<unsigned int*>(scratch + 4 * ntt * DCG_TB);
-    DCG_CUDA(cudaFuncSetAttribute(sym_apply2_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DCG_SMEM_ATTR(sym_apply2_coop_kernel, smem);
     DCG_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), st));
     void* args[] = {(void*)&K,      (void*)&ldk,    (void*)&n,      (void*)&x1,      (void*)&x2,
                     (void*)&v1,     (void*)&v2,     (void*)&s_out1, (void*)&s_out2,  (void*)&shift1,
@@ -528,7 +528,7 @@ int dcg_xty(dcg_context* ctx, cudaStream_t st, const double* X, long long ldx, c
     const int pq = p * q;
     dim3 grid(nb, (pq + 256 * XTY_PPT - 1) / (256 * XTY_PPT));
     const size_t smem = sizeof(double) * XTY_ROWS * (size_t)(p + q);
-    DCG_CUDA(cudaFuncSetAttribute(xty_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DCG_SMEM_ATTR(xty_kernel, smem);
     xty_kernel<<<grid, 256, smem, st>>>(X, ldx, Y, ldy, n, p, q, scratch_parts);
     DCG_LAUNCHED();
     reduce_parts_kernel<<<(pq + 255) / 256, 256, 0, st>>>(scratch_parts, nb, pq, C);

@@ -73,6 +73,18 @@ int dcg_host_reserve(dcg_context* ctx, size_t bytes);
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Raise a kernel's dynamic shared-memory limit only when a launch needs more
+// than any earlier one at this call site (one device per process): the
+// attribute call otherwise sat on the host between back-to-back launches.
+#define DCG_SMEM_ATTR(kern, bytes)                                                                     \
+    do {                                                                                               \
+        static long long dcg_smem_set_ = -1;                                                           \
+        if ((long long)(bytes) > dcg_smem_set_) {                                                      \
+            DCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes))); \
+            dcg_smem_set_ = (long long)(bytes);                                                        \
+        }                                                                                              \
+    } while (0)
+
 // ---- CTA barrier ---------------------------------------------------------------
 // __syncthreads() is the *aligned* bar.sync: it assumes every warp arrives
 // converged.  Independent thread scheduling does not guarantee reconvergence

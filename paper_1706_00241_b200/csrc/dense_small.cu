@@ -1334,7 +1334,7 @@ int dcg_ritz_pencil_launch(cudaStream_t st, const double* Fraw, const double* Gr
                            int max_sweeps, double* wk, double* theta, double* U, int* active, DevStatus* ds,
                            const DevStatus* plan) {
     const size_t smem = pencil_smem(T);
-    DCG_CUDA(cudaFuncSetAttribute(ritz_pencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DCG_SMEM_ATTR(ritz_pencil_kernel, smem);
     ritz_pencil_kernel<<<1, PENCIL_NT, smem, st>>>(Fraw, Graw, T, k, largest, max_sweeps, wk, theta, U, active, ds,
                                                 plan);
     DCG_LAUNCHED();

@@ -569,8 +569,16 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
     int gy = (int)(((T + 16 * FG_BI - 1) / (16 * FG_BI)) * ((2 * T + 16 * FG_BJ - 1) / (16 * FG_BJ)));
     // one cooperative launch when the grid is co-resident (it is: nb <= SMs)
     int per_sm = 0;
-    DCG_CUDA(cudaFuncSetAttribute(zstage1_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
-    DCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, zstage1_coop_kernel, EX_NT, sm1));
+    DCG_SMEM_ATTR(zstage1_coop_kernel, sm1);
+    {
+        static size_t occ_bytes = 0;
+        static int occ = 0;
+        if (occ_bytes != sm1) {
+            DCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, zstage1_coop_kernel, EX_NT, sm1));
+            occ_bytes = sm1;
+        }
+        per_sm = occ;
+    }
     if ((long long)per_sm * G >= nb) {
         int ikp = (int)kp, im = (int)m, ik = (int)k;
         void* args[] = {(void*)&n,    (void*)&ikp,   (void*)&Wp,     (void*)&AWp,   (void*)&im,      (void*)&P,
@@ -603,8 +611,16 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
     if (!d_z) {
         const size_t smt = sizeof(double) * ((size_t)T * k + 16 * 64 + 2 * (size_t)EX_ROWS * T);
         int per_sm = 0;
-        DCG_CUDA(cudaFuncSetAttribute(tail_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smt));
-        DCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tail_coop_kernel, EX_NT, smt));
+        DCG_SMEM_ATTR(tail_coop_kernel, smt);
+        {
+            static size_t occ_bytes = 0;
+            static int occ = 0;
+            if (occ_bytes != smt) {
+                DCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tail_coop_kernel, EX_NT, smt));
+                occ_bytes = smt;
+            }
+            per_sm = occ;
+        }
         if ((long long)per_sm * G >= nb) {
             DCG_CUDA(cudaMemsetAsync(counters + 3, 0, sizeof(unsigned int), st));
             int ik = (int)k;
