@@ -43,9 +43,13 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-CONFIG2 = dict(n=10_000, d=10, lengthscale=1.5, k=16, ell=20, tol=1e-8, newton_steps=8)
-METRIC = "def-CG iters/sec (config 2: GPC Laplace-Newton sequence, n=10000, k=16, fp64)"
+from paper_1706_00241_b200.workloads import CONFIGS, gpc_inputs  # noqa: E402
+
 UNIT = "iters/s"
+
+
+def metric_name(cfgno, n, k):
+    return f"def-CG iters/sec (config {cfgno}: GPC Laplace-Newton sequence, n={n}, k={k}, fp64)"
 
 
 def parse():
@@ -54,27 +58,44 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--n", type=int, default=CONFIG2["n"])
+    ap.add_argument("--config", type=int, default=None, choices=[2, 3],
+                    help="BASELINE config (default: 2 at one GPU, 3 -- the sharded config -- under torchrun)")
+    ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cg", action="store_true", help="skip the plain-CG comparison sequence")
     ap.add_argument("--cpu-sample-steps", type=int, default=2)
-    return ap.parse_args()
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if args.config is None:
+        args.config = 3 if (world > 1 or os.environ.get("DCG_BENCH_SHARDED")) else 2
+    if args.n is None:
+        args.n = CONFIGS[args.config]["n"]
+    return args
+
+
+def config_of(args):
+    return dict(CONFIGS[args.config], n=args.n)
 
 
 def inputs(n, d, seed=0):
-    from oracle.defcg_oracle import gpc_inputs
-
     return gpc_inputs(n, d, seed)
 
 
-def workload(args):
-    c = dict(CONFIG2)
-    c["n"] = args.n
+def parallelism(world):
+    if world > 1 or os.environ.get("DCG_BENCH_SHARDED"):
+        return f"row-shards x{world} (NCCL all-gather p + all-reduce scalars)"
+    return "single-gpu"
+
+
+def workload(args, world=1):
+    c = config_of(args)
     return {
-        "workload": f"config2 GPC Laplace-Newton def-CG sequence n={c['n']} d={c['d']} "
+        "workload": f"config{args.config} GPC Laplace-Newton def-CG sequence n={c['n']} d={c['d']} "
                     f"ell={c['lengthscale']} k={c['k']} ell_log={c['ell']} tol={c['tol']} steps={c['newton_steps']}",
         "n": c["n"], "d": c["d"], "k": c["k"], "ell_log": c["ell"], "tol": c["tol"],
         "newton_steps": c["newton_steps"], "selection": "largest", "seed": 0,
         "l2": "inputs larger than L2 (8 n^2 B Gram = %.0f MB > 126 MB)" % (8 * c["n"] ** 2 / 1e6),
+        "parallelism": parallelism(world),
     }
 
 
@@ -135,22 +156,33 @@ class Clocks:
 # ----------------------------------------------------------------------------
 # CPU baseline: the oracle restatement of the reference (numpy backend)
 # ----------------------------------------------------------------------------
-def cpu_baseline(n, steps):
+CPU_SAMPLE_N = 12_000   # largest n whose host run stays within the bounded CPU sample
+
+
+def cpu_baseline(args, steps):
     """Time the reference algorithm on the host: the first `steps` Newton
     systems of the config (solve_time_s as the reference measures it,
-    gpc.py:246-268).  Returns (iters/s, cores, sample description)."""
+    gpc.py:246-268).  Above CPU_SAMPLE_N the same recipe runs at
+    CPU_SAMPLE_N points and the per-iteration cost is scaled by n^2 (the
+    bytes of one product), labelled "extrapolated".
+    Returns (iters/s, cores, sample description)."""
     from oracle import defcg_oracle as O
 
-    c = CONFIG2
-    x, y = inputs(n, c["d"])
+    c = config_of(args)
+    n_run = min(args.n, CPU_SAMPLE_N)
+    x, y = inputs(n_run, c["d"])
     kmat = O.rbf_kernel(x, 1.0, c["lengthscale"], be="numpy")
     _, _, recs = O.laplace_newton(kmat, y, "defcg", O.Cfg(tol=c["tol"], ell=c["ell"]), newton_tol=-np.inf,
                                   max_newton=c["newton_steps"], k=c["k"], selection="largest", be="numpy",
                                   max_steps_timed=steps)
     its = sum(r.solver_iterations for r in recs)
     secs = sum(r.solve_time_s for r in recs)
-    return its / secs, os.cpu_count(), (f"first {len(recs)} Newton systems of the config (oracle restatement of "
-                                        f"defcg, numpy backend, {its} def-CG iterations in {secs:.2f} s)")
+    scale = (n_run / args.n) ** 2
+    desc = (f"first {len(recs)} Newton systems of the config (oracle restatement of defcg, numpy backend, "
+            f"{its} def-CG iterations in {secs:.2f} s)")
+    if n_run != args.n:
+        desc += f" at n={n_run}, per-iteration cost extrapolated x (n/{n_run})^2 to n={args.n}"
+    return its / secs * scale, os.cpu_count(), desc
 
 
 # ----------------------------------------------------------------------------
@@ -161,8 +193,14 @@ def run_reference(args, rank, world):
         return 0
     from oracle import defcg_oracle as O
 
-    c = CONFIG2
+    c = config_of(args)
     n = args.n
+    if n > CPU_SAMPLE_N:
+        # the reference's host run cannot hold the full config (~4 x 8 n^2 B
+        # peak): the same recipe at CPU_SAMPLE_N points, per-iteration cost
+        # scaled by n^2 (labelled in the sample description)
+        n = CPU_SAMPLE_N
+    scale = (n / args.n) ** 2
     x, y = inputs(n, c["d"])
     kmat = O.rbf_kernel(x, 1.0, c["lengthscale"], be="numpy")
     cfg = O.Cfg(tol=c["tol"], ell=c["ell"])
@@ -201,15 +239,19 @@ def run_reference(args, rank, world):
         i, dt = one_step()
         its += i
         secs += dt
-    value = its / secs if secs > 0 else 0.0
+    value = its / secs * scale if secs > 0 else 0.0
+    sample = (f"{args.steps} Newton systems streamed through the oracle restatement of defcg.recycle.solve_next "
+              f"(numpy backend, all host threads); {its} iterations")
+    if n != args.n:
+        sample += f" at n={n}, per-iteration cost extrapolated x (n/{n})^2 to n={args.n}"
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(args.steps, 1),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload(args),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                         "sample": f"{args.steps} Newton systems streamed through the oracle restatement of "
-                                   f"defcg.recycle.solve_next (numpy backend, all host threads); {its} iterations"},
+        "impl": "reference", "metric": metric_name(args.config, args.n, c["k"]), "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / scale / max(args.steps, 1),
+        "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8d recipe)",
+        "config": workload(args, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -242,7 +284,7 @@ def run_native(args, rank, world):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-    c = CONFIG2
+    c = config_of(args)
     n, k = args.n, c["k"]
     x, y = inputs(n, c["d"])
     cfg = P.SolverConfig(tol=c["tol"], ell=c["ell"])
@@ -252,29 +294,8 @@ def run_native(args, rank, world):
     torch.cuda.synchronize()
 
     solve_ms, solve_its, solve_mv = [], [], []
-    orig = P.solvers._solve_dev
-
-    def traced(op, b, x0, basis, cfg_, t0):
-        out = orig(op, b, x0, basis, cfg_, t0)
-        rep = out[1]
-        kk = basis.k if basis is not None else 0
-        its = rep.iterations
-        # matvec-equivalents streamed by the solve kernel: prologue (1, or 2 with
-        # the warm-start correction), one per iteration, true-residual refreshes
-        # prologue products: r_prev = b - A x_prev (unless computed ahead of the
-        # launch: job.hoisted) and r0 = b - A x0
-        warm_mv = 1 if (kk and not getattr(job, "hoisted", False)) else 0
-        mv = 1 + warm_mv + its + (its // cfg_.recompute_residual_every if cfg_.recompute_residual_every else 0)
-        solve_ms.append(rep.device_ms)
-        solve_its.append((its, kk))
-        solve_mv.append(mv)
-        return out
-
-    P.solvers._solve_dev = traced
-    P.recycle._solve_dev = traced
-    P.gpc._solve_dev = traced
-    # the def-CG Newton loop runs pipelined (recycle.solve_next_async): the
-    # per-solve numbers come from the finished job (kernel device time, its,
+    # the Newton loop runs pipelined (recycle.solve_next_async): the per-solve
+    # numbers come from the finished job (kernel device time, iterations,
     # basis columns actually used)
     orig_finish = P.recycle._AsyncSolve.finish
 
@@ -283,10 +304,10 @@ def run_native(args, rank, world):
         rep = st_.history[-1]
         kk, its = job.log.k, rep.iterations
         cfg_ = job.cfg
-        # prologue products: r_prev = b - A x_prev (unless computed ahead of the
-        # launch: job.hoisted) and r0 = b - A x0
-        warm_mv = 1 if (kk and not getattr(job, "hoisted", False)) else 0
-        mv = 1 + warm_mv + its + (its // cfg_.recompute_residual_every if cfg_.recompute_residual_every else 0)
+        # prologue products: A x_prev (unless computed ahead of the launch:
+        # job.hoisted) and, with a basis, r0 = b - A x0 at the corrected x0
+        mv = (0 if job.hoisted else 1) + (1 if kk else 0) + its + \
+            (its // cfg_.recompute_residual_every if cfg_.recompute_residual_every else 0)
         solve_ms.append(rep.device_ms)
         solve_its.append((its, kk))
         solve_mv.append(mv)
@@ -294,8 +315,8 @@ def run_native(args, rank, world):
 
     P.recycle._AsyncSolve.finish = traced_finish
 
-    def sequence():
-        _, recs = P.laplace_newton(gram, yd, "defcg", cfg, newton_tol=-np.inf, max_newton=c["newton_steps"], k=k,
+    def sequence(solver="defcg"):
+        _, recs = P.laplace_newton(gram, yd, solver, cfg, newton_tol=-np.inf, max_newton=c["newton_steps"], k=k,
                                    selection="largest")
         return sum(r.solver_iterations for r in recs), recs
 
@@ -330,6 +351,33 @@ def run_native(args, rank, world):
         ms = float(t.item())
     ms_per_step = ms / args.steps
     value = world * total_its / (ms / 1e3)
+
+    # ---- plain CG on the same pipelined device path (the config's "def-CG vs
+    # plain CG iteration counts and time"; gpc.py solver="cg" = cg_solve warm
+    # started at the previous solution), timed the same way, after the line's
+    # own timed region
+    P.recycle._AsyncSolve.finish = orig_finish
+    cg = None
+    if not args.no_cg:
+        for _ in range(min(args.warmup, 2)):
+            sequence("cg")
+        barrier()
+        cg_steps = max(1, min(args.steps, 10))
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        cg_its = 0
+        for _ in range(cg_steps):
+            i_, recs_cg = sequence("cg")
+            cg_its += i_
+        c1.record()
+        barrier()
+        cg_ms = c0.elapsed_time(c1) / cg_steps
+        cg = {"sequence_ms": cg_ms, "iterations_per_sequence": [r.solver_iterations for r in recs_cg],
+              "iters_per_s": cg_its / cg_steps / (cg_ms / 1e3), "steps": cg_steps,
+              "defcg_time_saving": 1.0 - ms_per_step / cg_ms,
+              "defcg_iteration_saving": 1.0 - (total_its / args.steps) / (cg_its / cg_steps),
+              "how": "laplace_newton(..., solver='cg') on the same device-resident Gram and pipelined path, "
+                     "CUDA events over the sequences"}
 
     # ---- roofline of the dominant kernel (the persistent solve kernel) -------
     import json as _json
@@ -411,10 +459,6 @@ def run_native(args, rank, world):
         matvec_in_solve = {"error": repr(exc)[:200]}
 
     # ---- e2e through the public API from pinned host buffers ----------------
-    P.solvers._solve_dev = orig
-    P.recycle._solve_dev = orig
-    P.gpc._solve_dev = orig
-    P.recycle._AsyncSolve.finish = orig_finish
     xh = torch.from_numpy(x).pin_memory()
     yh = torch.from_numpy(y).pin_memory()
     e2e_steps = max(1, min(args.steps, 3))
@@ -447,15 +491,16 @@ def run_native(args, rank, world):
            "includes": "H2D of X and y, on-device Gram assembly, 8-step Newton sequence, records D2H"}
 
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8d recipe)",
-        "config": workload(args) | {"parallelism": "replicas" if world > 1 else "single-gpu"},
-        "iterations_per_sequence": its_lists[-1], "sequence_ms": ms_per_step,
-        "roofline": roofline, "matvec_roofline": matvec, "matvec_in_solve": matvec_in_solve, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+        "metric": metric_name(args.config, n, k), "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8d recipe)",
+        "config": workload(args, world),
+        "iterations_per_sequence": its_lists[-1], "sequence_ms": ms_per_step, "plain_cg": cg,
+        "roofline": roofline, "matvec_roofline": matvec, "matvec_in_solve": matvec_in_solve, "e2e": e2e,
+        "gpu_launches": int(launches), "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, cores, sample = cpu_baseline(n, args.cpu_sample_steps)
+        v, cores, sample = cpu_baseline(args, args.cpu_sample_steps)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -466,7 +511,8 @@ def run_native(args, rank, world):
 
 
 def run_native_sharded(args, rank, world):
-    """Config 2 with K row-sharded over `world` GPUs (one process per GPU)."""
+    """A GPC config (default: config 3) with K row-sharded over `world` GPUs
+    (one process per GPU)."""
     import torch
     import torch.distributed as dist
 
@@ -478,7 +524,7 @@ def run_native_sharded(args, rank, world):
     torch.cuda.set_device(dev)
     dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     comm = TorchComm()
-    c = CONFIG2
+    c = config_of(args)
     n, k = args.n, c["k"]
     x, y = inputs(n, c["d"])
     cfg = P.SolverConfig(tol=c["tol"], ell=c["ell"])
@@ -546,10 +592,10 @@ def run_native_sharded(args, rank, world):
            "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
            "includes": "H2D of X and y, per-rank Gram slab assembly, sharded 8-step Newton sequence, records D2H"}
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8d recipe)",
-        "config": workload(args) | {"parallelism": f"row-shards x{world} (NCCL all-gather p + all-reduce scalars)"},
+        "metric": metric_name(args.config, n, k), "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8d recipe)",
+        "config": workload(args, world),
         "iterations_per_sequence": its_list, "sequence_ms": ms_per_step,
         "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
     }

@@ -14,6 +14,11 @@
 
 thread_local cudaError_t dcg_last_cuda_error = cudaSuccess;
 static std::atomic<long long> g_launches{0};
+
+std::mutex& dcg_setup_mutex() {
+    static std::mutex m;
+    return m;
+}
 void dcg_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 extern "C" long long dcg_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
@@ -104,6 +109,7 @@ extern "C" int dcg_context_destroy(dcg_context* ctx) {
     if (ctx->ws) cudaFree(ctx->ws);
     if (ctx->ws2) cudaFree(ctx->ws2);
     if (ctx->host) cudaFreeHost(ctx->host);
+    if (ctx->d_res) cudaFree(ctx->d_res);
     cudaEventDestroy(ctx->ev0);
     cudaEventDestroy(ctx->ev1);
     delete ctx;
@@ -148,6 +154,7 @@ int dcg_ws2_reserve(dcg_context* ctx, size_t bytes) {
 int dcg_host_reserve(dcg_context* ctx, size_t bytes) {
     if (bytes <= ctx->host_bytes) return DCG_OK;
     if (ctx->host) cudaFreeHost(ctx->host);
+    if (ctx->d_res) cudaFree(ctx->d_res);
     ctx->host = nullptr;
     DCG_CUDA(cudaMallocHost(&ctx->host, bytes + 4096));
     ctx->host_bytes = bytes + 4096;

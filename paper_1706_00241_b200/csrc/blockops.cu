@@ -372,14 +372,13 @@ static int launch_dmma(dcg_context* ctx, cudaStream_t st, const double* K, long 
                        int& splits_out) {
     constexpr int KP = NTILE * 8;
     const size_t smem = sizeof(double) * (size_t)(2 * GM_BM * GM_SA + 2 * GM_BK * (KP + 4));
-    // attribute and occupancy once per instantiation (one device per
-    // process): these host calls sat between the refresh's launches
-    static int per_sm = 0;
-    if (per_sm == 0) {
-        DCG_CUDA(cudaFuncSetAttribute(dmma_gemm_kernel<NTILE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-        DCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmma_gemm_kernel<NTILE>, 256, smem));
-    }
+    // attribute and occupancy once per instantiation and device: these host
+    // calls sat between the refresh's launches
+    static std::atomic<long long> occ_cache[DCG_MAX_DEVICES];
+    int per_sm = 0;
+    DCG_SMEM_ATTR(dmma_gemm_kernel<NTILE>, smem);
+    int rc_ = dcg_occupancy_cached(occ_cache, (const void*)dmma_gemm_kernel<NTILE>, 256, smem, &per_sm);
+    if (rc_) return rc_;
     const long long row_tiles = (rows + GM_BM - 1) / GM_BM;
     const long long target = 2LL * (per_sm < 1 ? 1 : per_sm) * ctx->sm_count;   // ~2 waves
     long long splits = (target + row_tiles - 1) / row_tiles;

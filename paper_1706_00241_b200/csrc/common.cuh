@@ -13,6 +13,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <mutex>
+
 #include "../../include/defcg_b200.h"
 
 #define DCG_NT 512                      // threads of the persistent / GEMV CTAs
@@ -33,6 +36,7 @@ struct dcg_context {
     void* host;              // pinned host scratch for status read-back
     size_t host_bytes;
     cudaEvent_t ev0, ev1;
+    long long* d_res;        // result block of the synchronous Ritz extraction
 };
 
 // ---- status plumbing --------------------------------------------------------
@@ -73,17 +77,50 @@ int dcg_host_reserve(dcg_context* ctx, size_t bytes);
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// Raise a kernel's dynamic shared-memory limit only when a launch needs more
-// than any earlier one at this call site (one device per process): the
-// attribute call otherwise sat on the host between back-to-back launches.
-#define DCG_SMEM_ATTR(kern, bytes)                                                                     \
-    do {                                                                                               \
-        static long long dcg_smem_set_ = -1;                                                           \
-        if ((long long)(bytes) > dcg_smem_set_) {                                                      \
-            DCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes))); \
-            dcg_smem_set_ = (long long)(bytes);                                                        \
-        }                                                                                              \
+// Launch set-up cached per call site AND per device: function attributes are
+// per device, and contexts on different devices may be driven from different
+// host threads, so the caches are indexed by the current device and updated
+// under a process-wide mutex (the fast path is one atomic load).
+#define DCG_MAX_DEVICES 64
+static inline int dcg_current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d & (DCG_MAX_DEVICES - 1);
+}
+std::mutex& dcg_setup_mutex();
+
+// Raise a kernel's dynamic shared-memory limit only when a launch on this
+// device needs more than any earlier one at this call site: the attribute call
+// otherwise sat on the host between back-to-back launches.
+#define DCG_SMEM_ATTR(kern, bytes)                                                                         \
+    do {                                                                                                   \
+        static std::atomic<long long> dcg_smem_set_[DCG_MAX_DEVICES];                                      \
+        const int dev_ = dcg_current_device();                                                             \
+        if ((long long)(bytes) > dcg_smem_set_[dev_].load(std::memory_order_acquire)) {                    \
+            std::lock_guard<std::mutex> lock_(dcg_setup_mutex());                                          \
+            if ((long long)(bytes) > dcg_smem_set_[dev_].load(std::memory_order_relaxed)) {                \
+                DCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes))); \
+                dcg_smem_set_[dev_].store((long long)(bytes), std::memory_order_release);                 \
+            }                                                                                              \
+        }                                                                                                  \
     } while (0)
+
+// Occupancy (CTAs per SM) of `kern` at `smem` bytes, cached per device in
+// `cache` (one slot per device: smem << 16 | occupancy + 1).
+static inline int dcg_occupancy_cached(std::atomic<long long>* cache, const void* kern, int threads, size_t smem,
+                                       int* out) {
+    const int dev = dcg_current_device();
+    const long long v = cache[dev].load(std::memory_order_acquire);
+    if (v && (v >> 16) == (long long)smem) {
+        *out = (int)(v & 0xFFFF) - 1;
+        return DCG_OK;
+    }
+    int occ = 0;
+    DCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+    cache[dev].store(((long long)smem << 16) | (long long)(occ + 1), std::memory_order_release);
+    *out = occ;
+    return DCG_OK;
+}
 
 // ---- CTA barrier ---------------------------------------------------------------
 // __syncthreads() is the *aligned* bar.sync: it assumes every warp arrives

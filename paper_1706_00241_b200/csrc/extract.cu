@@ -571,13 +571,9 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
     int per_sm = 0;
     DCG_SMEM_ATTR(zstage1_coop_kernel, sm1);
     {
-        static size_t occ_bytes = 0;
-        static int occ = 0;
-        if (occ_bytes != sm1) {
-            DCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, zstage1_coop_kernel, EX_NT, sm1));
-            occ_bytes = sm1;
-        }
-        per_sm = occ;
+        static std::atomic<long long> occ_cache[DCG_MAX_DEVICES];
+        rc = dcg_occupancy_cached(occ_cache, (const void*)zstage1_coop_kernel, EX_NT, sm1, &per_sm);
+        if (rc) return rc;
     }
     if ((long long)per_sm * G >= nb) {
         int ikp = (int)kp, im = (int)m, ik = (int)k;
@@ -613,13 +609,9 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
         int per_sm = 0;
         DCG_SMEM_ATTR(tail_coop_kernel, smt);
         {
-            static size_t occ_bytes = 0;
-            static int occ = 0;
-            if (occ_bytes != smt) {
-                DCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tail_coop_kernel, EX_NT, smt));
-                occ_bytes = smt;
-            }
-            per_sm = occ;
+            static std::atomic<long long> occ_cache[DCG_MAX_DEVICES];
+            rc = dcg_occupancy_cached(occ_cache, (const void*)tail_coop_kernel, EX_NT, smt, &per_sm);
+            if (rc) return rc;
         }
         if ((long long)per_sm * G >= nb) {
             DCG_CUDA(cudaMemsetAsync(counters + 3, 0, sizeof(unsigned int), st));
@@ -715,9 +707,9 @@ extern "C" int dcg_ritz_extract(dcg_context* ctx, void* stream, long long n, con
     cudaStream_t st = as_stream(stream);
     int rc = dcg_host_reserve(ctx, 64);
     if (rc) return rc;
-    // the result block lives at the end of a small dedicated allocation
-    static thread_local long long* d_res = nullptr;
-    if (!d_res) DCG_CUDA(cudaMalloc(&d_res, 64));
+    // the result block: a small allocation owned by the context (its device)
+    if (!ctx->d_res) DCG_CUDA(cudaMalloc(&ctx->d_res, 64));
+    long long* d_res = ctx->d_res;
     rc = dcg_ritz_extract_async(ctx, stream, n, log, m, prev, k, selection, d_theta, d_u, d_z, d_w_next, d_aw_next,
                                 d_res);
     if (rc) return rc;

@@ -36,7 +36,7 @@ struct SolveArgs {
     double shift;
     const double* b;
     const double* x0;
-    const double* ax0;     // optional: A x0 computed ahead of the launch (warm start)
+    const double* ax0;     // optional: A x0 computed ahead of the launch (x0 as passed, before any deflation correction)
     double* x;
     int k;                 // basis columns (the layout / maximum)
     const long long* kdev; // optional: columns in use, read on the device (<= k; 0 = plain CG)
@@ -383,12 +383,19 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     GSYNC();
 
     // ---------------- r0 = b - A x0 ; mu ; p0 ------------------------------------
-    gemv(a.x, [&](long long i, double t) {
-        const double xi = ld_cg(a.x + i);
-        const double ax = s ? add_rn(mul_rn(shift, xi), mul_rn(s[i], t)) : add_rn(mul_rn(shift, xi), t);
-        a.r[i] = sub_rn(a.b[i], ax);
-    });
-    if constexpr (STRAT != STRAT_ROWS) GSYNC(); else cta_sync();
+    if (a.ax0 && !(a.warm && deflate)) {
+        // plain CG warm-started at x0 = x_prev (cg_solve, solvers.py:207-219):
+        // A x0 is the product computed ahead of the launch
+        for (long long i = r0 + tid; i < r1; i += DCG_NT) a.r[i] = sub_rn(a.b[i], ld_cg(a.ax0 + i));
+        cta_sync();
+    } else {
+        gemv(a.x, [&](long long i, double t) {
+            const double xi = ld_cg(a.x + i);
+            const double ax = s ? add_rn(mul_rn(shift, xi), mul_rn(s[i], t)) : add_rn(mul_rn(shift, xi), t);
+            a.r[i] = sub_rn(a.b[i], ax);
+        });
+        if constexpr (STRAT != STRAT_ROWS) GSYNC(); else cta_sync();
+    }
     own_partials([&](long long i) { return ld_cg(a.r + i); }, a.r, deflate ? a.AW : nullptr, a.partials);
     GSYNC();
     reduce_partials(a.partials, G, a.ps, nslots, s_c, s_scr);

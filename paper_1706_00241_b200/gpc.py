@@ -150,11 +150,28 @@ def likelihood_derivs(f, y):
 def _dense_cholesky_solve(op: DenseOperator, b: torch.Tensor) -> torch.Tensor:
     """Direct solve of the (materialised) SPD system — the reference's
     "cholesky" solver column (gpc.py:247-255) via cuSOLVER potrf."""
+    return torch.cholesky_solve(b[:, None], _dense_cholesky_factor(op))[:, 0]
+
+
+def _dense_cholesky_factor(op: DenseOperator) -> torch.Tensor:
+    """cholesky_factor(A) with the reference's pivot semantics (linalg.py:74-92,
+    _core.pyx:47-66): a pivot d_j = a_jj - sum_k L_jk^2 at or below
+    1e-14 * max(max diag, 0) raises NotPositiveDefinite(j).  potrf stops only
+    at a non-positive pivot and otherwise stores L_jj = sqrt(d_j), so the
+    failing index is the first j with L_jj^2 <= tol before potrf's own stop."""
     a = op.dense_dev()
+    n = a.shape[0]
+    if n == 0:
+        return a
+    tol = 1e-14 * max(float(a.diagonal().max()), 0.0)
     low, info = torch.linalg.cholesky_ex(a)
-    if int(info) != 0:
-        raise NotPositiveDefinite(int(info) - 1)
-    return torch.cholesky_solve(b[:, None], low)[:, 0]
+    stop = int(info) - 1 if int(info) > 0 else n       # potrf's failing column (or n)
+    piv = low.diagonal()[:stop]
+    bad = torch.nonzero(piv * piv <= tol)
+    fail = int(bad[0, 0]) if bad.numel() else (stop if stop < n else -1)
+    if fail >= 0:
+        raise NotPositiveDefinite(fail)
+    return low
 
 
 def make_state(k_matrix, y, f=None):
@@ -314,8 +331,11 @@ def laplace_newton(k_matrix, y, solver=SOLVER_CHOLESKY, cfg=None, newton_tol=1.0
     n = state.y.shape[0]
     psi_prev = state.loglik   # f = a = 0: psi = loglik, ||f - K a|| = 0 (gpc.py:239)
     records = []
-    if solver == SOLVER_DEFCG:
-        state, records = _laplace_newton_pipelined(state, psi_prev, cfg, newton_tol, max_newton, k, selection)
+    if solver in (SOLVER_DEFCG, SOLVER_CG):
+        # plain CG is solve_next with no basis (k = 0): cg_solve(A, b, x_prev)
+        # exactly as gpc.py:256-261, on the same pipelined device path
+        state, records = _laplace_newton_pipelined(state, psi_prev, cfg, newton_tol, max_newton,
+                                                   k if solver == SOLVER_DEFCG else 0, selection)
         if records:
             stacked = torch.stack([r.f for r in records]).cpu().numpy()
             for r, row in zip(records, stacked):
@@ -335,19 +355,6 @@ def laplace_newton(k_matrix, y, solver=SOLVER_CHOLESKY, cfg=None, newton_tol=1.0
             solver_iterations, history = None, []
             norm_b = float(torch.linalg.norm(system.b))
             rel_residual = float(torch.linalg.norm(resid)) / norm_b if norm_b > 0.0 else 0.0
-        elif solver == SOLVER_CG:
-            x, report, _ = _solve_dev(system.a_matrix, system.b, x_prev, None, cfg, t0)
-            dt = time.perf_counter() - t0
-            solver_iterations, history = report.iterations, report.residual_history
-            rel_residual = history[-1]
-        else:
-            # the next basis is extracted on a side stream while the Newton
-            # update and the next system are formed here
-            x, seq = solve_next(seq, system.a_matrix, system.b, defer_extraction=True)
-            dt = time.perf_counter() - t0
-            report = seq.history[-1]
-            solver_iterations, history = report.iterations, report.residual_history
-            rel_residual = history[-1]
 
         state, psi = _update_dev(state, system.inner, system.sqrt_h, x)
         records.append(NewtonRecord(newton_iter=it, psi=psi, loglik=state.loglik,

@@ -70,14 +70,24 @@ class DenseOperator:
         op = cls(kbuf, a.shape[0], ld)
         if check_symmetric:
             op.require_symmetric(rtol)
-            # make K exactly symmetric (its lower triangle mirrored): the change is
-            # within the 1e-12 * max|A| the check admits, and it makes the
-            # lower-triangle ("sym") and full-row products the same operator.
-            n = op.n
-            if n > 1:
-                low = torch.tril(kbuf[:, :n])
-                kbuf[:, :n] = low + torch.tril(low, -1).T
+            # The input is never modified (solvers.py:149 semantics).  The
+            # lower-triangle ("sym") products read each stored entry for both
+            # K_ij and K_ji, so they are the caller's operator only when the
+            # matrix is EXACTLY symmetric (every rbf_kernel Gram is); a matrix
+            # that is symmetric only within the tolerance streams full rows,
+            # exactly as the reference's row-wise matvec does (_core.pyx:16-28).
+            if op.n > 1 and not op.is_exactly_symmetric():
+                op.strategy = "rows"
         return op
+
+    def is_exactly_symmetric(self) -> bool:
+        """max|K - K^T| == 0 (one n^2 pass on the device)."""
+        if self.n == 0:
+            return True
+        ok = ctypes.c_int()
+        N.check(N.lib().dcg_check_symmetric(D.ctx(), D.stream(), self.kbuf.data_ptr(), self.n, self.ldk, 0.0,
+                                            ctypes.byref(ok)), what="check_symmetric")
+        return bool(ok.value)
 
     def require_symmetric(self, rtol: float = SYMMETRY_RTOL) -> "DenseOperator":
         if self.n == 0:

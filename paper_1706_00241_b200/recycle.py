@@ -199,6 +199,7 @@ def _extract_async(log: KrylovLog, prev: RecycleBasis | None, k: int, selection:
     result = torch.zeros(4, dtype=torch.int64, device=D.device())
     clog = log.c_struct()
     cprev = prev.c_struct() if kp else None
+    _slot1_owner[D.device().index] = None   # the slot-1 workspace now holds this extraction's data
     with torch.cuda.stream(side):
         rc = N.lib().dcg_ritz_extract_async(D.ctx(1), side.cuda_stream, n, ctypes.byref(clog), m,
                                             ctypes.byref(cprev) if cprev is not None else None, k,
@@ -224,6 +225,10 @@ def _extract_async(log: KrylovLog, prev: RecycleBasis | None, k: int, selection:
 # ---------------------------------------------------------------------------
 _STATUS_WORDS = 8   # the 64-byte status block of dcg_solve_async
 
+# Per device: the pending extraction whose intermediates the slot-1 context
+# workspace currently holds (its split-off tail reads them at join time).
+_slot1_owner: dict = {}
+
 
 _pinned_pool: list = []
 
@@ -243,17 +248,24 @@ class _AsyncSolve:
     and a prefix of the residual history come back on the copy stream as soon
     as the solve ends, whatever the compute streams do next."""
 
-    def __init__(self, state, x, log, hist, status, basis, event, ev_end, t0, cfg, pending):
+    def __init__(self, state, x, log, hist, status, basis, event, ev_end, t0, cfg, pending, consumed=None):
         self.state, self.x, self.log, self.hist, self.status = state, x, log, hist, status
         self.basis, self.event, self.t0, self.cfg, self.pending = basis, event, t0, cfg, pending
         self.ev_end = ev_end
+        # `consumed`: the result block of the extraction whose basis this solve
+        # was handed (device side, a failed one degraded it to plain CG); read
+        # back with the status so anything but BasisDeficient is raised
+        self.consumed = consumed
         cs = D.copy_stream()
         cs.wait_event(self.ev_end)
-        self.host = _pinned(_STATUS_WORDS + _HIST_PREFIX)
+        self.host = _pinned(_STATUS_WORDS + _HIST_PREFIX + 2)
         npre = min(_HIST_PREFIX, hist.shape[0])
         with torch.cuda.stream(cs):
             self.host[:_STATUS_WORDS].copy_(status, non_blocking=True)
             self.host[_STATUS_WORDS:_STATUS_WORDS + npre].view(torch.float64).copy_(hist[:npre], non_blocking=True)
+            if consumed is not None:
+                self.host[_STATUS_WORDS + _HIST_PREFIX:_STATUS_WORDS + _HIST_PREFIX + 2].copy_(consumed[:2],
+                                                                                            non_blocking=True)
             self.done = torch.cuda.Event()
             self.done.record(cs)
 
@@ -261,6 +273,14 @@ class _AsyncSolve:
         """Wait for the solve and build its report.  Returns (x, new SequenceState)."""
         self.done.synchronize()
         words = self.host[:_STATUS_WORDS].numpy().copy()
+        if self.consumed is not None:
+            # recycle.py:194-195 swallows only BasisDeficient; any other failure
+            # of the extraction (e.g. NoConvergence of the pencil) propagates
+            xst, xinfo = (int(v) for v in self.host[_STATUS_WORDS + _HIST_PREFIX:
+                                                    _STATUS_WORDS + _HIST_PREFIX + 2].tolist())
+            if xst not in (N.DCG_OK, N.DCG_E_BASIS_DEFICIENT):
+                _pinned_pool.append(self.host)
+                N.check(xst, xinfo, "ritz_extract")
         status = int(np.int32(words[0] & 0xFFFFFFFF))
         kused = int(words[0] >> 32)
         info = int(words[1])
@@ -302,12 +322,12 @@ def solve_next_async(state, a, b, ax0=None, ax0_of=None):
     main = torch.cuda.current_stream()
     pending = object.__getattribute__(state, "basis")
     w_src, valid = None, None
-    if not isinstance(pending, _PendingBasis):
+    if ax0 is not None and (ax0_of is None or ax0_of is not state.x_last):
         ax0 = None
     if isinstance(pending, _PendingBasis):
         # the warm start's first product A x_prev needs no basis: it runs
         # while the extraction of the basis is still going on
-        if ax0 is None or ax0_of is None or ax0_of is not state.x_last:
+        if ax0 is None:
             ax0 = op.matvec_dev(x_prev)
         # (joined right before the refresh launch below: the host-side set-up
         # of the refresh then overlaps the device's work instead of idling it)
@@ -346,7 +366,7 @@ def solve_next_async(state, a, b, ax0=None, ax0_of=None):
                                     x_prev.data_ptr(), ctypes.byref(cb) if cb is not None else None,
                                     ctypes.byref(cfg.c_struct()), x.data_ptr(), ctypes.byref(clog),
                                     hist.data_ptr(), kdev.data_ptr() if kdev is not None else None,
-                                    status.data_ptr(), ax0.data_ptr() if (ax0 is not None and kmax) else None),
+                                    status.data_ptr(), ax0.data_ptr() if ax0 is not None else None),
             what="solve_async")
     ev_end = torch.cuda.Event(enable_timing=True)
     ev_end.record()
@@ -374,14 +394,25 @@ def solve_next_async(state, a, b, ax0=None, ax0_of=None):
             event = torch.cuda.Event()
             event.record(side)
 
-        def tail(stream, args=args):
+        def tail(stream, args=args, dev=D.device().index):
             # uscale + wnext: SM-wide, so they run on the joining stream (the
-            # main one) rather than in the SMs the side stream is left
-            N.check(N.lib().dcg_ritz_extract_dev(*args[:1], stream.cuda_stream, *args[2:], 4), 0, "ritz_extract_dev")
+            # main one) rather than in the SMs the side stream is left.  They
+            # read stages 1-3's intermediates from the slot-1 workspace; if
+            # another extraction was enqueued there since (an interleaved
+            # sequence), the whole extraction is re-run from its inputs (the
+            # log, the basis used, the solve's status block: kept alive) on
+            # the joining stream in the slot-0 workspace, with the same values.
+            if _slot1_owner.get(dev) is nxt:
+                N.check(N.lib().dcg_ritz_extract_dev(*args[:1], stream.cuda_stream, *args[2:], 4), 0,
+                        "ritz_extract_dev")
+            else:
+                N.check(N.lib().dcg_ritz_extract_dev(D.ctx(0), stream.cuda_stream, *args[2:], 0), 0,
+                        "ritz_extract_dev")
 
         nxt = _PendingBasis(event, result, w_next, aw_next, (log, bufs, theta, status), tail)
-    job = _AsyncSolve(state, x, log, hist, status, bufs, ev0, ev_end, t0, cfg, nxt)
-    job.hoisted = ax0 is not None and kmax > 0   # the solve kernel skips its first product
+        _slot1_owner[D.device().index] = nxt
+    job = _AsyncSolve(state, x, log, hist, status, bufs, ev0, ev_end, t0, cfg, nxt, consumed=valid)
+    job.hoisted = ax0 is not None   # A x_prev came from outside: the solve kernel skips that product
     return x, job
 
 

@@ -85,6 +85,42 @@ def test_cholesky_solver_matches(P):
     assert abs(recs_c[-1].psi - recs_d[-1].psi) <= 1e-8 * abs(recs_c[-1].psi)
 
 
+def test_cholesky_column_vs_oracle(P):
+    """The direct-solver column (gpc.py:247-255) against the oracle's own
+    Cholesky path on the same inputs: the whole Newton trajectory."""
+    x, y = O.gpc_inputs(400, 4)
+    gram = P.rbf_kernel(x, P.KernelParams(1.0, 1.2))
+    _, recs = P.laplace_newton(gram, y, "cholesky", newton_tol=-np.inf, max_newton=6)
+    _, _, ref = O.laplace_newton(O.rbf_kernel(x, 1.0, 1.2), y, "cholesky", newton_tol=-np.inf, max_newton=6)
+    assert len(recs) == len(ref)
+    for a, b in zip(recs, ref):
+        assert a.solver_iterations is None and b.solver_iterations is None
+        assert abs(a.psi - b.psi) <= 1e-12 * abs(b.psi)
+        assert np.linalg.norm(a.f - b.f) <= 1e-11 * np.linalg.norm(b.f)
+        assert a.rel_residual <= 1e-13 and b.rel_residual <= 1e-13
+
+
+def test_cholesky_pivot_tolerance_semantics(P):
+    """linalg.py:74-92: a pivot at or below 1e-14 * max diag raises
+    NotPositiveDefinite with the reference's failing index, including pivots
+    that are small but positive (cuSOLVER's potrf alone would accept them)."""
+    from paper_1706_00241_b200.gpc import _dense_cholesky_factor
+
+    rng = np.random.default_rng(5)
+    for n, r in [(60, 23), (200, 150)]:
+        b = rng.standard_normal((n, r))
+        a = b @ b.T + 1e-17 * np.eye(n)      # pivot r ~ 1e-17 * scale: tiny, possibly positive
+        a = 0.5 * (a + a.T)
+        with pytest.raises(O.ONotPositiveDefinite) as ref:
+            O.chol_factor(a)
+        with pytest.raises(P.NotPositiveDefinite) as got:
+            _dense_cholesky_factor(P.operators.DenseOperator.from_matrix(a))
+        assert got.value.pivot_index == ref.value.pivot_index == r
+    spd = O.rbf_kernel(rng.standard_normal((300, 3)), 1.0, 1.0)
+    low = _dense_cholesky_factor(P.operators.DenseOperator.from_matrix(spd)).cpu().numpy()
+    assert np.allclose(low @ low.T, spd, rtol=0, atol=1e-13)
+
+
 def test_likelihood_derivs(P, rng):
     f = np.array([0.0, 800.0, -800.0, 3.0, -3.0])
     y = np.array([1.0, -1.0, 1.0, 1.0, -1.0])

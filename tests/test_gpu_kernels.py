@@ -135,3 +135,28 @@ def test_require_symmetric(P):
     big[7, 250] += 1e-6
     with pytest.raises(ValueError):
         linalg.require_symmetric(big)
+
+
+def test_raw_matrix_never_mutated(P, rng):
+    """A torch fp64 CUDA input whose row pitch needs no padding (n % 32 == 0)
+    is used in place by the operator: it must come back bit-identical, also
+    when it is symmetric only within the tolerance (that operator then streams
+    full rows, the reference's own matvec)."""
+    import torch
+
+    n = 1024
+    a = rng.standard_normal((n, n))
+    a = a @ a.T / n + np.eye(n)
+    a_pert = a + np.triu(1e-15 * rng.standard_normal((n, n)), 1)     # asymmetric within 1e-12 max|A|
+    for mat in (a, a_pert):
+        t = torch.from_numpy(mat.copy()).cuda()
+        before = t.clone()
+        b = rng.standard_normal(n)
+        x, rep, _ = P.cg_solve(t, torch.from_numpy(b).cuda(), None, P.SolverConfig(tol=1e-10))
+        assert torch.equal(t, before)
+        xo, repo, _ = O.cg_solve(mat, b, None, O.Cfg(tol=1e-10))
+        assert abs(rep.iterations - repo.iterations) <= 1
+        assert np.linalg.norm(x.cpu().numpy() - xo) <= 1e-8 * np.linalg.norm(xo)
+    op = P.operators.DenseOperator.from_matrix(torch.from_numpy(a_pert).cuda())
+    assert op.strategy == "rows"
+    assert P.operators.DenseOperator.from_matrix(torch.from_numpy(a).cuda()).strategy != "rows"
