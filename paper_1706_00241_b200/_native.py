@@ -8,6 +8,7 @@ benchmark can never pass on a silent CPU path.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -21,7 +22,10 @@ from .errors import (
     NotPositiveDefinite,
 )
 
-LIB_PATH = Path(__file__).resolve().with_name("libdefcg_b200.so")
+# DCG_LIB_PATH: a developer build of the same library (e.g. a variant with
+# different compile-time tuning, ``python -m paper_1706_00241_b200.build
+# --variant DIR -DNAME=VALUE``); the in-tree build otherwise.
+LIB_PATH = Path(os.environ.get("DCG_LIB_PATH") or Path(__file__).resolve().with_name("libdefcg_b200.so"))
 
 DCG_OK = 0
 DCG_E_DIMENSION = 1

@@ -58,16 +58,21 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, out_dir: Path | None = None,
+          defines: tuple = ()) -> Path:
+    """Compile csrc/*.cu and link the library (in-tree, or a tuning variant
+    with extra -D defines into out_dir)."""
     headers = list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
     srcs = sources()
-    OBJ.mkdir(exist_ok=True)
+    obj_dir = OBJ if out_dir is None else Path(out_dir) / "_build"
+    lib = LIB if out_dir is None else Path(out_dir) / LIB.name
+    obj_dir.mkdir(parents=True, exist_ok=True)
     cc = nvcc()
 
     def compile_one(src: Path) -> Path:
-        obj = OBJ / (src.stem + ".o")
+        obj = obj_dir / (src.stem + ".o")
         if force or _stale(obj, [src] + headers):
-            cmd = [cc, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+            cmd = [cc, *NVCC_FLAGS, *defines, "-c", str(src), "-o", str(obj)]
             if verbose:
                 print(" ".join(cmd), flush=True)
             res = subprocess.run(cmd, capture_output=True, text=True)
@@ -77,16 +82,21 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(compile_one, srcs))
-    if force or _stale(LIB, objs):
-        cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs)]
+    if force or _stale(lib, objs):
+        cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(lib), *map(str, objs)]
         if verbose:
             print(" ".join(cmd), flush=True)
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    out = build(force="--force" in sys.argv, verbose=True)
+    args = sys.argv[1:]
+    out_dir = None
+    if "--variant" in args:
+        out_dir = Path(args[args.index("--variant") + 1])
+    out = build(force="--force" in args, verbose=True, out_dir=out_dir,
+                defines=tuple(a for a in args if a.startswith("-D")))
     print(out)

@@ -29,6 +29,7 @@ namespace cg = cooperative_groups;
 namespace {
 
 struct SolveArgs {
+    int pin_q;             // L2-resident slice of the triangle (symgemv.cuh sym_pinned)
     const double* K;
     long long ldk;
     long long n;
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
             PHASE(15);
             unsigned long long tc0 = 0;
             if (a.timers && threadIdx.x == 0) tc0 = globaltimer_ns();
-            sym_pass1(K, a.ldk, n, v, s, a.colpart, a.rowpart, s_g, ring_seq);
+            sym_pass1(K, a.ldk, n, v, s, a.colpart, a.rowpart, s_g, ring_seq, a.pin_q);
             if (a.timers && threadIdx.x == 0) a.timers[16 + blockIdx.x] += globaltimer_ns() - tc0;
             PHASE(0);
             GSYNC();
@@ -591,6 +592,8 @@ static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, co
     if (rc) return rc;
     char* w = static_cast<char*>(ctx->ws);
     SolveArgs a;
+    memset(&a, 0, sizeof(a));
+    a.pin_q = strat == STRAT_SYM ? dcg_l2_pin_q(n) : 0;
     a.K = op->d_k;
     a.ldk = op->ldk;
     a.n = n;

@@ -143,10 +143,20 @@ __device__ __forceinline__ void sym_fill_range_table(long long* tbl, long long n
 __device__ __forceinline__ unsigned sym_saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 // K is streamed once per product and is far larger than L2: its lines are
 // marked evict-first so they do not push out the vectors and the tile
-// partials pass 2 reads back.
-// (the 64-bit L2 cache-policy encoding of createpolicy.fractional.L2::evict_first
-// with fraction 1.0, as a constant so it is materialised in uniform registers)
-__device__ __forceinline__ unsigned long long sym_policy_evict_first() { return 0x12F0000000000000ull; }
+// partials pass 2 reads back -- except a fixed subset of the lower-triangle
+// tiles, tile t with (t mod 32) < pin_q (the same subset in every kernel that
+// streams K this way, so every CTA partition keeps its share), which is loaded
+// evict-last and stays resident in the 126 MB L2 across products.  pin_q = 0
+// streams everything from HBM (dcg_l2_pin_q sizes it).
+__device__ __forceinline__ bool sym_pinned(long long t, int pin_q) { return (int)(t & 31) < pin_q; }
+__device__ __forceinline__ unsigned long long sym_policy(bool evict_last) {
+    unsigned long long pol;
+    if (evict_last)
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ void sym_cp_async16_full(double* sdst, const double* gsrc, unsigned long long pol) {
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sym_saddr(sdst)), "l"(gsrc),
                  "l"(pol));
@@ -284,7 +294,8 @@ __device__ __forceinline__ void sym_ring_init(double* smem, long long n) {
 template <bool kHint = true, int NV = 1>
 __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long long ldk, long long n, const double* v,
                                           const double* s, double* colpart, double* rowpart, double* smem,
-                                          unsigned int& seq, const double* v2 = nullptr, long long part2 = 0) {
+                                          unsigned int& seq, int pin_q = 0, const double* v2 = nullptr,
+                                          long long part2 = 0) {
     static_assert(NV == 1 || NV == 2, "one or two vectors");
     if constexpr (NV == 2) s = v2;   // the s slot of every stage carries v2
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -302,7 +313,7 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
     long long I = sym_tile_row(t0);
     long long J = t0 - sym_tile_row_base(I);
     const SymCopyPlan pl = sym_copy_plan(ldk);
-    const unsigned long long pol = sym_policy_evict_first();
+    const unsigned long long pol_first = sym_policy(false), pol_last = sym_policy(true);
     const long long row_stride = (long long)DCG_TB * ldk;
     // prologue: tiles 0 .. STAGES-2; issue cursor (iI, iJ, ip) follows
     long long iI = I, iJ = J;
@@ -313,7 +324,8 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
             const unsigned int q = q0 + st;
             const int stg = q % DCG_SYM_STAGES;
             if (q >= DCG_SYM_STAGES) sym_mbar_wait(empty + stg, ((q / DCG_SYM_STAGES) - 1) & 1);
-            sym_issue_tile<kHint>(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES, pol);
+            sym_issue_tile<kHint>(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES,
+                                  sym_pinned(t0 + st, pin_q) ? pol_last : pol_first);
             sym_mbar_cp_arrive(full + stg);
         }
         if (++iJ > iI) { ++iI; iJ = 0; ip = K + iI * row_stride; } else { ip += DCG_TB; }
@@ -341,7 +353,8 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
                 const unsigned int q = q0 + tn;
                 const int stg = q % DCG_SYM_STAGES;
                 if (q >= DCG_SYM_STAGES) sym_mbar_wait(empty + stg, ((q / DCG_SYM_STAGES) - 1) & 1);
-                sym_issue_tile<kHint>(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES, pol);
+                sym_issue_tile<kHint>(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES,
+                                      sym_pinned(t0 + tn, pin_q) ? pol_last : pol_first);
                 sym_mbar_cp_arrive(full + stg);
             }
             if (++iJ > iI) { ++iI; iJ = 0; ip = K + iI * row_stride; } else { ip += DCG_TB; }
