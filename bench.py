@@ -304,9 +304,9 @@ def run_native(args, rank, world):
         rep = st_.history[-1]
         kk, its = job.log.k, rep.iterations
         cfg_ = job.cfg
-        # prologue products: A x_prev (unless computed ahead of the launch:
-        # job.hoisted) and, with a basis, r0 = b - A x0 at the corrected x0
-        mv = (0 if job.hoisted else 1) + (1 if kk else 0) + its + \
+        # prologue product: A x_prev, unless computed ahead of the launch
+        # (job.hoisted); with a basis r0 = r_prev - (AW) c needs no product
+        mv = (0 if job.hoisted else 1) + its + \
             (its // cfg_.recompute_residual_every if cfg_.recompute_residual_every else 0)
         solve_ms.append(rep.device_ms)
         solve_its.append((its, kk))

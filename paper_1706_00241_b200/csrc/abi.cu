@@ -20,69 +20,6 @@ std::mutex& dcg_setup_mutex() {
     return m;
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
-typedef CUresult (*dcg_encode_tiled_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                        const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                        CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-int dcg_kmap_make(CUtensorMap* out, const double* K, long long n, long long ldk) {
-    static std::atomic<dcg_encode_tiled_fn> fn{nullptr};
-    dcg_encode_tiled_fn f = fn.load(std::memory_order_acquire);
-    if (!f) {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        DCG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-        if (!p || q != cudaDriverEntryPointSuccess) return DCG_E_UNSUPPORTED;
-        f = reinterpret_cast<dcg_encode_tiled_fn>(p);
-        fn.store(f, std::memory_order_release);
-    }
-    if (n < 1 || ldk < n || ((ldk * 8) % 16) || (reinterpret_cast<uintptr_t>(K) & 15)) return DCG_E_CONFIG;
-    const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
-    const cuuint64_t strides[1] = {(cuuint64_t)ldk * 8};
-    const cuuint32_t box[2] = {16, 64};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = f(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(K), dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS ? DCG_OK : DCG_E_CONFIG;
-}
-
-// Budget of the L2-resident slice of K's lower triangle: what the 126 MB L2
-// holds next to a solve's other working set (tile partials 16 n^2 / 64 B,
-// vectors, basis, Krylov log).  DCG_L2_PIN_MB overrides (0 disables).
-int dcg_l2_pin_q(long long n) {
-    static std::atomic<long long> budget_mb{-1};
-    long long mb = budget_mb.load(std::memory_order_relaxed);
-    if (mb < 0) {
-        const char* e = getenv("DCG_L2_PIN_MB");
-        // default off: a pinned slice cut the solve's DRAM reads by 13% at
-        // n = 10^4 with no change in its time (pass 1 is not HBM-bound there)
-        mb = e ? atoll(e) : 0;
-        if (mb < 0) mb = 0;
-        budget_mb.store(mb, std::memory_order_relaxed);
-    }
-    if (mb > 0) {
-        // evict-last lines persist only inside the device's persisting-L2
-        // carve-out: size it once per device (up to the device maximum)
-        static std::atomic<int> carved[DCG_MAX_DEVICES];
-        const int dev = dcg_current_device();
-        if (!carved[dev].exchange(1)) {
-            int maxp = 0;
-            if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess && maxp > 0) {
-                size_t want = (size_t)mb * 1000000;
-                if (want > (size_t)maxp) want = (size_t)maxp;
-                cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-            }
-        }
-    }
-    const long long nt = (n + 63) / 64;
-    const double tri = (double)(nt * (nt + 1) / 2) * 64.0 * 64.0 * 8.0;
-    if (tri <= 0.0) return 0;
-    long long q = (long long)(32.0 * (double)mb * 1e6 / tri);
-    if (q > 32) q = 32;
-    if (q < 0) q = 0;
-    return (int)q;
-}
 void dcg_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 extern "C" long long dcg_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 

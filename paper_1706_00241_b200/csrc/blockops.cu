@@ -67,13 +67,13 @@ __global__ void __launch_bounds__(DCG_NT, 1)
 // Both passes in one cooperative launch (grid barrier between them): no
 // second launch, and pass 2's partial reads follow pass 1 without a gap.
 __global__ void __launch_bounds__(DCG_NT, 1)
-    sym_apply_coop_kernel(const double* __restrict__ K, long long ldk, int pin_q, long long n, const double* v,
+    sym_apply_coop_kernel(const double* __restrict__ K, long long ldk, long long n, const double* v,
                           const double* s_in, const double* s_out, double shift, double* colpart, double* rowpart,
                           double* y, unsigned int* bar) {
     extern __shared__ __align__(16) double smem[];
     sym_ring_init(smem, n);
     unsigned int seq = 0;
-    sym_pass1<false>(K, ldk, n, v, s_in, colpart, rowpart, smem, seq, pin_q);
+    sym_pass1<false>(K, ldk, n, v, s_in, colpart, rowpart, smem, seq);
     dcg_grid_barrier(bar, gridDim.x);
     const long long q0 = sym_row_begin(n, gridDim.x, blockIdx.x);
     const long long q1 = sym_row_begin(n, gridDim.x, blockIdx.x + 1);
@@ -123,8 +123,7 @@ int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, long long 
     unsigned int* bar = reinterpret_cast<unsigned int*>(rowpart + ntt * DCG_TB);
     DCG_SMEM_ATTR(sym_apply_coop_kernel, smem);
     DCG_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), st));
-    int pin_q = dcg_l2_pin_q(n);
-    void* args[] = {(void*)&K, (void*)&ldk, (void*)&pin_q, (void*)&n, (void*)&v, (void*)&s_in, (void*)&s_out, (void*)&shift,
+    void* args[] = {(void*)&K, (void*)&ldk, (void*)&n, (void*)&v, (void*)&s_in, (void*)&s_out, (void*)&shift,
                     (void*)&colpart, (void*)&rowpart, (void*)&y, (void*)&bar};
     DCG_CUDA(cudaLaunchCooperativeKernel((const void*)sym_apply_coop_kernel, dim3(G), dim3(DCG_NT), args, smem, st));
     dcg_count_launch();
@@ -137,7 +136,7 @@ int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, long long 
 // Same tile partition, partial layout and pass-2 order as two dcg_sym_apply
 // calls with (v, s_in) such that x = s_in (.) v: bitwise the same results.
 __global__ void __launch_bounds__(DCG_NT, 1)
-    sym_apply2_coop_kernel(const double* __restrict__ K, long long ldk, int pin_q, long long n, const double* x1,
+    sym_apply2_coop_kernel(const double* __restrict__ K, long long ldk, long long n, const double* x1,
                            const double* x2, const double* v1, const double* v2, const double* s_out1,
                            const double* s_out2, double shift1, double shift2, double* colpart, double* rowpart,
                            long long part2, double* y1, double* y2, unsigned int* bar) {
@@ -146,7 +145,7 @@ __global__ void __launch_bounds__(DCG_NT, 1)
     unsigned int seq = 0;
     // (no L2 cache hints in the standalone products: a cp.async with a cache
     // hint faulted here as an illegal instruction on sm_100a)
-    sym_pass1<false, 2>(K, ldk, n, x1, nullptr, colpart, rowpart, smem, seq, pin_q, x2, part2);
+    sym_pass1<false, 2>(K, ldk, n, x1, nullptr, colpart, rowpart, smem, seq, x2, part2);
     dcg_grid_barrier(bar, gridDim.x);
     const long long q0 = sym_row_begin(n, gridDim.x, blockIdx.x);
     const long long q1 = sym_row_begin(n, gridDim.x, blockIdx.x + 1);
@@ -181,8 +180,7 @@ int dcg_sym_apply2(dcg_context* ctx, cudaStream_t st, const double* K, long long
     unsigned int* bar = reinterpret_cast<unsigned int*>(scratch + 4 * ntt * DCG_TB);
     DCG_SMEM_ATTR(sym_apply2_coop_kernel, smem);
     DCG_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), st));
-    int pin_q = dcg_l2_pin_q(n);
-    void* args[] = {(void*)&K,      (void*)&ldk,    (void*)&pin_q,  (void*)&n,      (void*)&x1,      (void*)&x2,
+    void* args[] = {(void*)&K,      (void*)&ldk,    (void*)&n,      (void*)&x1,      (void*)&x2,
                     (void*)&v1,     (void*)&v2,     (void*)&s_out1, (void*)&s_out2,  (void*)&shift1,
                     (void*)&shift2, (void*)&colpart, (void*)&rowpart, (void*)&part2, (void*)&y1,
                     (void*)&y2,     (void*)&bar};

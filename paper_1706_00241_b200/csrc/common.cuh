@@ -72,14 +72,6 @@ void dcg_count_launch();
         dcg_count_launch();                     \
     } while (0)
 
-// 2D TMA descriptor of a row-major fp64 n x n matrix with row pitch ldk
-// (64-row x 16-column boxes, 128-byte swizzle, zero fill out of bounds): the
-// operand of the symmetric products' tile ring (symgemv.cuh).
-int dcg_kmap_make(CUtensorMap* out, const double* K, long long n, long long ldk);
-// Lower-triangle tiles kept L2-resident across products: tile t with
-// (t mod 32) < dcg_l2_pin_q(n) (budget DCG_L2_PIN_MB, default in abi.cu).
-int dcg_l2_pin_q(long long n);
-
 int dcg_ws_reserve(dcg_context* ctx, size_t bytes);
 int dcg_ws2_reserve(dcg_context* ctx, size_t bytes);
 int dcg_host_reserve(dcg_context* ctx, size_t bytes);

@@ -29,7 +29,6 @@ namespace cg = cooperative_groups;
 namespace {
 
 struct SolveArgs {
-    int pin_q;             // L2-resident slice of the triangle (symgemv.cuh sym_pinned)
     const double* K;
     long long ldk;
     long long n;
@@ -246,7 +245,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
             PHASE(15);
             unsigned long long tc0 = 0;
             if (a.timers && threadIdx.x == 0) tc0 = globaltimer_ns();
-            sym_pass1(K, a.ldk, n, v, s, a.colpart, a.rowpart, s_g, ring_seq, a.pin_q);
+            sym_pass1(K, a.ldk, n, v, s, a.colpart, a.rowpart, s_g, ring_seq);
             if (a.timers && threadIdx.x == 0) a.timers[16 + blockIdx.x] += globaltimer_ns() - tc0;
             PHASE(0);
             GSYNC();
@@ -384,7 +383,14 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     GSYNC();
 
     // ---------------- r0 = b - A x0 ; mu ; p0 ------------------------------------
-    if (a.ax0 && !(a.warm && deflate)) {
+    if (a.warm && deflate) {
+        // x0 = x_prev + W c, so A x0 = A x_prev + (A W) c with the basis' own
+        // A W (refresh_basis, recycle.py:90, for this A): r0 = r_prev - (AW) c
+        // (solvers.py:237-238 then 150 form b - A x0 with one more product;
+        // the two are equal up to rounding, and W' r0 = 0 holds to rounding)
+        for (long long i = r0 + tid; i < r1; i += DCG_NT) a.r[i] = sub_rn(ld_cg(a.r + i), row_dot(a.AW, i, s_mu));
+        cta_sync();
+    } else if (a.ax0) {
         // plain CG warm-started at x0 = x_prev (cg_solve, solvers.py:207-219):
         // A x0 is the product computed ahead of the launch
         for (long long i = r0 + tid; i < r1; i += DCG_NT) a.r[i] = sub_rn(a.b[i], ld_cg(a.ax0 + i));
@@ -593,7 +599,6 @@ static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, co
     char* w = static_cast<char*>(ctx->ws);
     SolveArgs a;
     memset(&a, 0, sizeof(a));
-    a.pin_q = strat == STRAT_SYM ? dcg_l2_pin_q(n) : 0;
     a.K = op->d_k;
     a.ldk = op->ldk;
     a.n = n;

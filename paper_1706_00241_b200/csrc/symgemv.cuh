@@ -143,18 +143,14 @@ __device__ __forceinline__ void sym_fill_range_table(long long* tbl, long long n
 __device__ __forceinline__ unsigned sym_saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 // K is streamed once per product and is far larger than L2: its lines are
 // marked evict-first so they do not push out the vectors and the tile
-// partials pass 2 reads back -- except a fixed subset of the lower-triangle
-// tiles, tile t with (t mod 32) < pin_q (the same subset in every kernel that
-// streams K this way, so every CTA partition keeps its share), which is loaded
-// evict-last and stays resident in the 126 MB L2 across products.  pin_q = 0
-// streams everything from HBM (dcg_l2_pin_q sizes it).
-__device__ __forceinline__ bool sym_pinned(long long t, int pin_q) { return (int)(t & 31) < pin_q; }
-__device__ __forceinline__ unsigned long long sym_policy(bool evict_last) {
+// partials pass 2 reads back.  (Keeping a fixed slice of the triangle
+// L2-resident with evict-last loads instead -- a persisting carve-out of up
+// to 96 MB -- cut the solve's DRAM reads by 13% at n = 10^4 and left its time
+// unchanged: pass 1 runs at ~94% of the copy peak per CTA and is bound by the
+// per-tile issue work, not by HBM; profiles/r02/l2_pin_*.)
+__device__ __forceinline__ unsigned long long sym_policy_evict_first() {
     unsigned long long pol;
-    if (evict_last)
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    else
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
 __device__ __forceinline__ void sym_cp_async16_full(double* sdst, const double* gsrc, unsigned long long pol) {
@@ -294,8 +290,7 @@ __device__ __forceinline__ void sym_ring_init(double* smem, long long n) {
 template <bool kHint = true, int NV = 1>
 __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long long ldk, long long n, const double* v,
                                           const double* s, double* colpart, double* rowpart, double* smem,
-                                          unsigned int& seq, int pin_q = 0, const double* v2 = nullptr,
-                                          long long part2 = 0) {
+                                          unsigned int& seq, const double* v2 = nullptr, long long part2 = 0) {
     static_assert(NV == 1 || NV == 2, "one or two vectors");
     if constexpr (NV == 2) s = v2;   // the s slot of every stage carries v2
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -313,7 +308,7 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
     long long I = sym_tile_row(t0);
     long long J = t0 - sym_tile_row_base(I);
     const SymCopyPlan pl = sym_copy_plan(ldk);
-    const unsigned long long pol_first = sym_policy(false), pol_last = sym_policy(true);
+    const unsigned long long pol = sym_policy_evict_first();
     const long long row_stride = (long long)DCG_TB * ldk;
     // prologue: tiles 0 .. STAGES-2; issue cursor (iI, iJ, ip) follows
     long long iI = I, iJ = J;
@@ -324,8 +319,7 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
             const unsigned int q = q0 + st;
             const int stg = q % DCG_SYM_STAGES;
             if (q >= DCG_SYM_STAGES) sym_mbar_wait(empty + stg, ((q / DCG_SYM_STAGES) - 1) & 1);
-            sym_issue_tile<kHint>(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES,
-                                  sym_pinned(t0 + st, pin_q) ? pol_last : pol_first);
+            sym_issue_tile<kHint>(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES, pol);
             sym_mbar_cp_arrive(full + stg);
         }
         if (++iJ > iI) { ++iI; iJ = 0; ip = K + iI * row_stride; } else { ip += DCG_TB; }
@@ -353,8 +347,7 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
                 const unsigned int q = q0 + tn;
                 const int stg = q % DCG_SYM_STAGES;
                 if (q >= DCG_SYM_STAGES) sym_mbar_wait(empty + stg, ((q / DCG_SYM_STAGES) - 1) & 1);
-                sym_issue_tile<kHint>(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES,
-                                      sym_pinned(t0 + tn, pin_q) ? pol_last : pol_first);
+                sym_issue_tile<kHint>(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES, pol);
                 sym_mbar_cp_arrive(full + stg);
             }
             if (++iJ > iI) { ++iI; iJ = 0; ip = K + iI * row_stride; } else { ip += DCG_TB; }
