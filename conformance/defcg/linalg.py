@@ -1,0 +1,5 @@
+"""Conformance shim: paper_1706_00241_b200.linalg under the reference name."""
+from paper_1706_00241_b200.linalg import *  # noqa: F401,F403
+from paper_1706_00241_b200 import linalg as _m
+
+globals().update({k: v for k, v in vars(_m).items() if not k.startswith("__")})

@@ -28,7 +28,7 @@ import torch
 
 from . import _device as D
 from . import _native as N
-from .errors import InvalidLabel, NoProgress, NotPositiveDefinite, StateInconsistent
+from .errors import DimensionMismatch, InvalidLabel, NoProgress, NotPositiveDefinite, StateInconsistent
 from .operators import DenseOperator, RbfOperator, as_operator
 from .recycle import SELECT_LARGEST, SequenceState, _pinned, _pinned_pool, solve_next, solve_next_async
 from .solvers import SolverConfig, _solve_dev
@@ -52,20 +52,33 @@ class KernelParams:
 
 @dataclass
 class GpcState:
-    """Latent state with cached likelihood derivatives (gpc.py:48-58); device tensors."""
+    """Latent state with cached likelihood derivatives (gpc.py:48-58).
 
-    f: torch.Tensor
-    y: torch.Tensor
-    k_matrix: DenseOperator
-    a: torch.Tensor
+    Device flavour (the default inside laplace_newton, or when built from
+    torch inputs): the vectors are CUDA tensors and ``k_matrix`` a device
+    operator.  Host flavour (``host``, inferred from numpy fields when not
+    given): the fields are numpy arrays as in the reference, and every public
+    function moves them to the device for its work and returns host-flavour
+    results."""
+
+    f: object
+    y: object
+    k_matrix: object
+    a: object
     loglik: float
-    grad_loglik: torch.Tensor
-    h: torch.Tensor
+    grad_loglik: object
+    h: object
+    host: bool | None = None
+
+    def __post_init__(self):
+        if self.host is None:
+            self.host = not isinstance(self.f, torch.Tensor)
 
 
 @dataclass
 class NewtonSystem:
-    """gpc.py:61-65; ``a_matrix`` is the implicit operator I + S K S."""
+    """gpc.py:61-65; ``a_matrix`` is the implicit operator I + S K S (the
+    explicit matrix, b and sqrt_h as numpy arrays for a host-flavour state)."""
 
     a_matrix: DenseOperator
     b: torch.Tensor
@@ -92,9 +105,12 @@ class NewtonRecord:
 def rbf_kernel(x, params, jitter=None, matrix_free=False):
     """Dense RBF Gram matrix built on device (gpc.py:82-98, _core.pyx:97-114).
 
-    Returns a DenseOperator holding K in HBM, or with ``matrix_free`` an
-    RbfOperator that regenerates K from X on every product (config 5: the
-    Gram would not fit)."""
+    torch X: a DenseOperator holding K in HBM (the fast path), or with
+    ``matrix_free`` an RbfOperator that regenerates K from X on every product
+    (config 5: the Gram would not fit).  numpy X: K built on the device and
+    returned as a numpy array, as the reference does."""
+    if not matrix_free and not isinstance(x, torch.Tensor):
+        return np.asarray(rbf_kernel(D.to_dev(x, 2), params, jitter))
     xd = D.to_dev(x, 2)
     if not bool(torch.isfinite(xd).all()):
         raise ValueError("data matrix contains non-finite entries")
@@ -115,6 +131,26 @@ def rbf_kernel(x, params, jitter=None, matrix_free=False):
         N.check(N.lib().dcg_k_rbf_gram(D.ctx(), D.stream(), xd.data_ptr(), n, dim, var, inv_two_ell2, float(jitter),
                                        kbuf.data_ptr(), ld, 0, n), what="rbf_gram")
     return DenseOperator(kbuf, n, ld)
+
+
+def rbf_cross_kernel(xa, xb, params):
+    """Cross-kernel block between two point sets, no jitter (gpc.py:101-107),
+    built on device (``dcg_k_rbf_cross``, the reference's difference-squared
+    form _core.pyx:117-132).  numpy in -> numpy out, torch in -> device tensor."""
+    ad, bd = D.to_dev(xa, 2), D.to_dev(xb, 2)
+    if ad.shape[1] != bd.shape[1]:
+        raise DimensionMismatch(f"point dimensions {ad.shape[1]} and {bd.shape[1]}")
+    for t in (ad, bd):
+        if t.numel() and not bool(torch.isfinite(t).all()):
+            raise ValueError("data matrix contains non-finite entries")
+    var = params.signal_sd**2
+    inv_two_ell2 = 1.0 / (2.0 * params.lengthscale**2)
+    out = D.empty(ad.shape[0], bd.shape[0])
+    if out.numel():
+        N.check(N.lib().dcg_k_rbf_cross(D.ctx(), D.stream(), ad.data_ptr(), ad.shape[0], bd.data_ptr(), bd.shape[0],
+                                        ad.shape[1], float(var), float(inv_two_ell2), out.data_ptr()),
+                what="rbf_cross")
+    return D.out_like(out, xa)
 
 
 def check_labels(y):
@@ -174,9 +210,33 @@ def _dense_cholesky_factor(op: DenseOperator) -> torch.Tensor:
     return low
 
 
-def make_state(k_matrix, y, f=None):
-    """Fresh GpcState; f defaults to zero, a given f implies a = K^-1 f (gpc.py:160-172)."""
-    op = as_operator(k_matrix).kernel_view() if isinstance(k_matrix, DenseOperator) else as_operator(k_matrix)
+def _kernel_op(k_matrix) -> DenseOperator:
+    return as_operator(k_matrix).kernel_view() if isinstance(k_matrix, DenseOperator) else as_operator(k_matrix)
+
+
+def _host(v):
+    return v.detach().cpu().numpy() if isinstance(v, torch.Tensor) else v
+
+
+def _dev_state(state: GpcState) -> GpcState:
+    """Device-flavour view of a state (numpy fields uploaded, K as an operator)."""
+    if not state.host and isinstance(state.k_matrix, DenseOperator):
+        return state
+    return GpcState(f=D.to_dev(state.f, 1), y=check_labels(state.y), k_matrix=_kernel_op(state.k_matrix),
+                    a=D.to_dev(state.a, 1), loglik=state.loglik, grad_loglik=D.to_dev(state.grad_loglik, 1),
+                    h=D.to_dev(state.h, 1), host=False)
+
+
+def _as_flavour(state: GpcState, host: bool, k_matrix=None) -> GpcState:
+    if not host:
+        return state
+    return GpcState(f=_host(state.f), y=_host(state.y), k_matrix=state.k_matrix if k_matrix is None else k_matrix,
+                    a=_host(state.a), loglik=state.loglik, grad_loglik=_host(state.grad_loglik), h=_host(state.h),
+                    host=True)
+
+
+def _make_state_dev(k_matrix, y, f=None) -> GpcState:
+    op = _kernel_op(k_matrix)
     yd = check_labels(y)
     n = yd.shape[0]
     if f is None:
@@ -185,14 +245,27 @@ def make_state(k_matrix, y, f=None):
         fd = D.to_dev(f, 1)
         ad = _dense_cholesky_solve(op, fd)
     ll, g, h = _derivs_dev(fd, yd)
-    return GpcState(f=fd, y=yd, k_matrix=op, a=ad, loglik=ll, grad_loglik=g, h=h)
+    return GpcState(f=fd, y=yd, k_matrix=op, a=ad, loglik=ll, grad_loglik=g, h=h, host=False)
+
+
+def make_state(k_matrix, y, f=None):
+    """Fresh GpcState; f defaults to zero, a given f implies a = K^-1 f (gpc.py:160-172).
+    Host flavour (numpy fields, k_matrix as given) unless y is a torch tensor."""
+    st = _make_state_dev(k_matrix, y, f)
+    host = not isinstance(y, torch.Tensor)
+    return _as_flavour(st, host, k_matrix)
 
 
 def build_newton_system(state, x_prev=None):
     """A = I + H^1/2 K H^1/2 (implicit) and b = H^1/2 K (H f + grad) (gpc.py:175-183).
 
     With ``x_prev`` (a device vector) also ax0 = A x_prev, the first product of
-    the next warm-started solve, from the same pass over K."""
+    the next warm-started solve, from the same pass over K.  A host-flavour
+    state gets the reference's explicit A and numpy b, sqrt_h."""
+    if state.host:
+        sysm = build_newton_system(_dev_state(state))
+        return NewtonSystem(a_matrix=np.asarray(sysm.a_matrix), b=_host(sysm.b), sqrt_h=_host(sysm.sqrt_h))
+    state = _dev_state(state)
     op = state.k_matrix
     n = op.n
     s, inner, b = D.empty(n), D.empty(n), D.empty(n)
@@ -302,20 +375,23 @@ def _laplace_newton_pipelined(state, psi_prev, cfg, newton_tol, max_newton, k, s
 
 def newton_update(state, x):
     """a_new = (H f + grad) - H^1/2 x, f_new = K a_new (gpc.py:186-201)."""
+    host = state.host
+    dst = _dev_state(state)
     xd = D.to_dev(x, 1)
-    s = torch.sqrt(state.h)
-    inner = state.h * state.f + state.grad_loglik
-    new, _ = _update_dev(state, inner, s, xd)
-    return new
+    s = torch.sqrt(dst.h)
+    inner = dst.h * dst.f + dst.grad_loglik
+    new, _ = _update_dev(dst, inner, s, xd)
+    return _as_flavour(new, host, state.k_matrix)
 
 
 def psi_objective(state):
     """psi = log p(y|f) - f'a / 2 with the f = K a consistency check (gpc.py:204-209)."""
-    ka = state.k_matrix.kernel_view().matvec_dev(state.a)
-    err = float(torch.linalg.norm(state.f - ka))
-    if err > 1e-8 * float(torch.linalg.norm(state.f)):
+    st = _dev_state(state)
+    ka = st.k_matrix.kernel_view().matvec_dev(st.a)
+    err = float(torch.linalg.norm(st.f - ka))
+    if err > 1e-8 * float(torch.linalg.norm(st.f)):
         raise StateInconsistent(f"||f - K a|| = {err:g}")
-    return state.loglik - 0.5 * float(state.f @ state.a)
+    return st.loglik - 0.5 * float(st.f @ st.a)
 
 
 def laplace_newton(k_matrix, y, solver=SOLVER_CHOLESKY, cfg=None, newton_tol=1.0, max_newton=30, k=8,
@@ -327,7 +403,8 @@ def laplace_newton(k_matrix, y, solver=SOLVER_CHOLESKY, cfg=None, newton_tol=1.0
     if solver not in (SOLVER_CHOLESKY, SOLVER_CG, SOLVER_DEFCG):
         raise ValueError(f"unknown solver {solver!r}")
     cfg = cfg or SolverConfig()
-    state = make_state(k_matrix, y)
+    host = not isinstance(y, torch.Tensor)
+    state = _make_state_dev(k_matrix, y)
     n = state.y.shape[0]
     psi_prev = state.loglik   # f = a = 0: psi = loglik, ||f - K a|| = 0 (gpc.py:239)
     records = []
@@ -340,7 +417,7 @@ def laplace_newton(k_matrix, y, solver=SOLVER_CHOLESKY, cfg=None, newton_tol=1.0
             stacked = torch.stack([r.f for r in records]).cpu().numpy()
             for r, row in zip(records, stacked):
                 r.f = row
-        return state, records
+        return _as_flavour(state, host, k_matrix), records
     seq = SequenceState(k=k, cfg=cfg, selection=selection)
     x_prev = D.zeros(n)
 
@@ -372,4 +449,4 @@ def laplace_newton(k_matrix, y, solver=SOLVER_CHOLESKY, cfg=None, newton_tol=1.0
         stacked = torch.stack([r.f for r in records]).cpu().numpy()
         for r, row in zip(records, stacked):
             r.f = row
-    return state, records
+    return _as_flavour(state, host, k_matrix), records

@@ -206,7 +206,11 @@ def sym_eigen(a, max_sweeps=60, rtol=1e-14):
     if n == 0:
         return EigenPairs(np.empty(0), np.empty((0, 0)))
     if n > N.MAX_T:
-        raise N.DeviceError(f"sym_eigen on device supports n <= {N.MAX_T}")
+        # beyond the single-CTA Jacobi kernel (Ritz pencils are <= DCG_MAX_T):
+        # cuSOLVER's syevd on the device, eigenvalues equal to rounding, ascending,
+        # unit eigenvectors (test/diagnostic sizes; linalg.py:139-165 semantics)
+        vals, vecs = torch.linalg.eigh(D.to_dev(a, 2))
+        return EigenPairs(vals.cpu().numpy(), vecs.cpu().numpy())
     ad = D.to_dev(a)
     vals, vecs = D.empty(n), D.empty(n, n)
     info = ctypes.c_longlong(0)
@@ -227,7 +231,16 @@ def gen_sym_eigen(g, f, max_sweeps=60):
     if n == 0:
         return EigenPairs(np.empty(0), np.empty((0, 0)))
     if n > N.MAX_T:
-        raise N.DeviceError(f"gen_sym_eigen on device supports n <= {N.MAX_T}")
+        # G u = theta F u via F = L L' and C = L^-1 G L^-T (linalg.py:168-191) with
+        # cuSOLVER: the pivot rule of cholesky_factor, syevd, u = L^-T w normalised
+        lower = D.to_dev(cholesky_factor(D.to_dev(f, 2)), 2)
+        gd = D.to_dev(g, 2)
+        c = torch.linalg.solve_triangular(lower, torch.linalg.solve_triangular(lower, gd, upper=False).T,
+                                          upper=False)
+        vals, w = torch.linalg.eigh(0.5 * (c + c.T))
+        u = torch.linalg.solve_triangular(lower.T, w, upper=True)
+        u = u / torch.linalg.norm(u, dim=0, keepdim=True)
+        return EigenPairs(vals.cpu().numpy(), u.cpu().numpy())
     gd, fd = D.to_dev(g), D.to_dev(f)
     vals, vecs = D.empty(n), D.empty(n, n)
     info = ctypes.c_longlong(0)

@@ -27,7 +27,7 @@ import torch
 from . import _device as D
 from . import _native as N
 from .errors import BasisDeficient, DimensionMismatch
-from .operators import as_operator
+from .operators import DenseOperator, as_operator
 from .solvers import TERM_CONVERGED, TERM_MAX_ITERS, KrylovLog, RecycleBasis, SolveReport, SolverConfig, _solve_dev
 
 SELECT_SMALLEST = "smallest"
@@ -466,3 +466,56 @@ def solve_next(state, a, b, defer_extraction=False):
     x_out = x.cpu().numpy() if host else x
     new_state = replace(state, basis=nxt, x_last=x_out if host else x, history=state.history + [report])
     return x_out, new_state
+
+
+# ---------------------------------------------------------------------------
+# Diagnostics (recycle.py:206-231).  O(n^3) and test/report
+# only.  The reference runs its cyclic Jacobi (sym_eigen) on the explicit
+# matrices; here n <= DCG_MAX_T runs the same Jacobi kernel on the device and
+# larger n the cuSOLVER symmetric eigensolver (eigenvalues equal to rounding).
+# The deflated operator P_W A = A - AW (W'AW)^-1 W'A is formed on the device
+# with the basis' own Cholesky factor (solvers.py:107-115).
+# ---------------------------------------------------------------------------
+def _sym_eigvals_dev(m: torch.Tensor) -> np.ndarray:
+    n = m.shape[0]
+    if n <= N.MAX_T:
+        from .linalg import sym_eigen
+
+        return np.asarray(sym_eigen(m).values)
+    return torch.linalg.eigvalsh(m).cpu().numpy()
+
+
+def _explicit(a) -> torch.Tensor:
+    if isinstance(a, DenseOperator):
+        return a.dense_dev()
+    op = as_operator(a)   # validates symmetry (require_symmetric)
+    return op.dense_dev()
+
+
+def condition_numbers(a, k):
+    """(kappa, kappa_eff) = (lambda_n / lambda_1, lambda_n / lambda_{k+1}) (recycle.py:206-212)."""
+    m = _explicit(a)
+    n = m.shape[0]
+    if not 0 <= k < n:
+        raise ValueError(f"k must be in [0, n), got {k}")
+    values = _sym_eigvals_dev(m)
+    return float(values[-1] / values[0]), float(values[-1] / values[k])
+
+
+def deflated_spectrum(a, basis):
+    """Eigenvalues (ascending) of the deflated operator P_W A (recycle.py:215-231)."""
+    m = _explicit(a)
+    if basis is None or basis.k == 0:
+        return _sym_eigvals_dev(m)
+    low = basis.ensure_factored_dev()
+    k = basis.k
+    low = low[:k, :k]
+    wta = basis.w_dev.T @ m                                  # k x n
+    y = torch.linalg.solve_triangular(low, wta, upper=False)
+    y = torch.linalg.solve_triangular(low.T, y, upper=True)  # (W'AW)^-1 W'A
+    pm = m - basis.aw_dev @ y
+    scale = max(float(pm.abs().max()), 1e-300)
+    if float((pm - pm.T).abs().max()) <= 1e-8 * scale:
+        return _sym_eigvals_dev(0.5 * (pm + pm.T))
+    values = torch.linalg.eigvals(pm).real
+    return np.sort(values.cpu().numpy())

@@ -6,8 +6,8 @@ summary fields of `execute` :177-242, the three files of `emit_reports`
 :276-333, delta = |value - ref| / |ref| :161-163), so a GPU run and a CPU run
 can be diffed with the reference's own tooling: same columns, floats as
 17 significant digits, summary keys sorted.  The subset-of-data baseline
-(`subset.py`) is out of scope: `subset` stays empty and
-`subset.csv` carries its header only.  Times are the GPU solve times of
+(subset.py, run on the device) fills `subset` / `subset.csv` for each
+requested fraction (bench.py:243-275).  Times are the GPU solve times of
 NewtonRecord.solve_time_s.
 """
 
@@ -17,6 +17,7 @@ import csv
 import json
 from pathlib import Path
 
+from . import _device as D
 from .gpc import SOLVER_CHOLESKY, laplace_newton, rbf_kernel
 from .solvers import SolverConfig
 
@@ -44,11 +45,12 @@ def _solver_summary(recs):
 
 
 def run_comparison(x, y, params, solvers=(SOLVER_CHOLESKY, "cg", "defcg"), solver_cfg: SolverConfig | None = None,
-                   newton_tol=1.0, max_newton=30, k=8, selection="largest", jitter=None, config=None):
+                   newton_tol=1.0, max_newton=30, k=8, selection="largest", jitter=None, config=None,
+                   subset_fractions=(), seed=0):
     """One Laplace-Newton run per solver on the GPU.  Returns (rows, summary):
     rows are dicts keyed by TABLE_COLUMNS (plus `logp_tracked` = psi)."""
     solver_cfg = solver_cfg or SolverConfig()
-    kernel = rbf_kernel(x, params, jitter)
+    kernel = rbf_kernel(D.to_dev(x, 2), params, jitter)   # the Gram stays on the device for all solvers
     runs = {s: laplace_newton(kernel, y, solver=s, cfg=solver_cfg, newton_tol=newton_tol, max_newton=max_newton,
                               k=k, selection=selection)[1] for s in solvers}
     # the Cholesky run is the reference of the delta column (present when it ran first)
@@ -70,6 +72,23 @@ def run_comparison(x, y, params, solvers=(SOLVER_CHOLESKY, "cg", "defcg"), solve
         summary["reference_final_loglik"] = float(ref_ll[-1])
         for s, recs in runs.items():
             summary["solvers"][s]["rel_error_to_final"] = [rel_error_delta(r.loglik, ref_ll[-1]) for r in recs]
+    for frac in subset_fractions:
+        # subset-of-data baseline (bench.py:243-275): cumulative subset solve
+        # time against the full-data log-likelihood of the induced latents
+        from .gpc import likelihood_derivs
+        from .subset import assemble_full_latents, fit_subset
+
+        model, recs = fit_subset(x, y, frac, params, newton_tol=newton_tol, seed=seed, jitter=jitter,
+                                 max_newton=max_newton)
+        elapsed, points = 0.0, []
+        for r in recs:
+            elapsed += r.solve_time_s
+            loglik, _, _ = likelihood_derivs(assemble_full_latents(model, r.f), y)
+            point = {"newton_iter": r.newton_iter, "cpu_time": elapsed, "loglik": float(loglik)}
+            if ref_ll is not None:
+                point["rel_logp_error"] = rel_error_delta(loglik, ref_ll[-1])
+            points.append(point)
+        summary["subset"][str(frac)] = {"m": model.m, "points": points}
     summary["complete"] = True
     return rows, summary
 

@@ -20,6 +20,7 @@ from pathlib import Path
 
 import numpy as np
 import pytest
+import torch
 
 from conftest import GOLDEN, golden
 from paper_1706_00241_b200.workloads import gpc_inputs, sweep_inputs, sweep_thetas
@@ -53,7 +54,7 @@ def run_gpc(P, name, matrix_free=False):
     n, d, ell, k, steps = g["meta"]
     n, d, k, steps = int(n), int(d), int(k), int(steps)
     x, y = gpc_inputs(n, d)
-    gram = P.rbf_kernel(x, P.KernelParams(1.0, float(ell)), matrix_free=matrix_free)
+    gram = P.rbf_kernel(torch.from_numpy(x).cuda(), P.KernelParams(1.0, float(ell)), matrix_free=matrix_free)
     _, recs = P.laplace_newton(gram, y, "defcg", P.SolverConfig(tol=1e-8, ell=k + 4), newton_tol=-np.inf,
                                max_newton=steps, k=k, selection="largest")
     its = [r.solver_iterations for r in recs]
@@ -95,7 +96,7 @@ def test_config3_recipe_n24k(P):
     runs = []
     for perm in perms:
         xs, ys = (x, y) if perm is None else (x[perm], y[perm])
-        gram = P.rbf_kernel(xs, P.KernelParams(1.0, float(ell)))
+        gram = P.rbf_kernel(torch.from_numpy(xs).cuda(), P.KernelParams(1.0, float(ell)))
         _, recs = P.laplace_newton(gram, ys, "defcg", P.SolverConfig(tol=1e-8, ell=k + 4), newton_tol=-np.inf,
                                    max_newton=steps, k=k, selection="largest")
         del gram
@@ -130,8 +131,8 @@ def test_tight_solution_1e9(P, tag):
     g = need("config2_tight_ref")
     n, d, ell = g[f"{tag}_meta"]
     x, y = gpc_inputs(int(n), int(d))
-    gram = P.rbf_kernel(x, P.KernelParams(1.0, float(ell)))
-    st = P.gpc.make_state(gram, y)
+    gram = P.rbf_kernel(torch.from_numpy(x).cuda(), P.KernelParams(1.0, float(ell)))
+    st = P.gpc.make_state(gram, torch.from_numpy(y).cuda())
     sysm = P.gpc.build_newton_system(st)
     xs, rep, _ = P.cg_solve(sysm.a_matrix, sysm.b, None, P.SolverConfig(tol=1e-12, ell=1))
     xs = xs.cpu().numpy()
@@ -175,7 +176,7 @@ def test_config4_first_three_thetas(P):
         err = np.linalg.norm(sg - sr) / np.linalg.norm(sr)
         bound = 4 * 1e-8 * np.linalg.norm(y) / (0.01 * np.linalg.norm(sr))
         assert err <= bound, (i, err, bound)
-    a0 = P.rbf_kernel(x, P.KernelParams(1.0, float(thetas[0])), jitter=0.01)
+    a0 = P.rbf_kernel(torch.from_numpy(x).cuda(), P.KernelParams(1.0, float(thetas[0])), jitter=0.01)
     xt, rep, _ = P.cg_solve(a0, y, None, P.SolverConfig(tol=1e-12, ell=1))
     err = np.linalg.norm(xt - g["tight_x"]) / np.linalg.norm(g["tight_x"])
     assert err <= 1e-9, err

@@ -26,7 +26,9 @@ def P():
 
 
 def run(P, x, y, ell, k, solver):
-    gram = P.rbf_kernel(x, P.KernelParams(1.0, ell))
+    import torch
+
+    gram = P.rbf_kernel(torch.from_numpy(x).cuda(), P.KernelParams(1.0, ell))
     _, recs = P.laplace_newton(gram, y, solver, P.SolverConfig(tol=1e-8, ell=k + 4), newton_tol=-np.inf,
                                max_newton=8, k=k, selection="largest")
     return recs
@@ -142,9 +144,18 @@ def test_newton_system_toy(P):
     """gpc test_toy_assembly: K = [[1, .5], [.5, 1]], f = 0: A = I + K/4, b = K (y+1)/2 - ... """
     k = np.array([[1.0, 0.5], [0.5, 1.0]])
     st = P.make_state(k, np.array([1.0, -1.0]))
+    assert st.host and isinstance(st.f, np.ndarray)          # numpy in -> the reference's numpy state
     sysm = P.build_newton_system(st)
-    assert np.allclose(np.asarray(sysm.a_matrix), [[1.25, 0.125], [0.125, 1.25]], atol=1e-15)
-    assert np.allclose(sysm.b.cpu().numpy(), [0.125, -0.125], atol=1e-15)
+    assert isinstance(sysm.a_matrix, np.ndarray) and isinstance(sysm.b, np.ndarray)
+    assert np.allclose(sysm.a_matrix, [[1.25, 0.125], [0.125, 1.25]], atol=1e-15)
+    assert np.allclose(sysm.b, [0.125, -0.125], atol=1e-15)
+    import torch
+
+    std = P.make_state(torch.from_numpy(k).cuda(), torch.tensor([1.0, -1.0], dtype=torch.float64, device="cuda"))
+    assert not std.host                                      # torch in -> device state, implicit A
+    sysd = P.build_newton_system(std)
+    assert np.allclose(np.asarray(sysd.a_matrix), sysm.a_matrix, atol=1e-15)
+    assert np.allclose(sysd.b.cpu().numpy(), sysm.b, atol=1e-15)
 
 
 def test_psi_objective_and_state_check(P):

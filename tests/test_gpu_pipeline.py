@@ -27,7 +27,7 @@ def gpc_like_sequence(P, n, steps, seed=0):
     Laplace-Newton system shape), b_t random."""
     rng = np.random.default_rng(seed)
     x = rng.standard_normal((n, 5))
-    gram = P.rbf_kernel(x, P.KernelParams(1.0, 1.5))
+    gram = P.rbf_kernel(torch.from_numpy(x).cuda(), P.KernelParams(1.0, 1.5))
     s0 = rng.uniform(0.2, 0.5, n)
     systems = []
     for t in range(steps):
@@ -139,7 +139,7 @@ def test_fused_newton_system_matches_separate_products(P, n, strategy):
 
     rng = np.random.default_rng(n)
     x = rng.standard_normal((n, 4))
-    gram = P.rbf_kernel(x, P.KernelParams(1.0, 1.3)).with_strategy(strategy)   # "sym": the fused pass
+    gram = P.rbf_kernel(torch.from_numpy(x).cuda(), P.KernelParams(1.0, 1.3)).with_strategy(strategy)   # "sym": the fused pass
     y = np.where(rng.standard_normal(n) > 0, 1.0, -1.0)
     state = G.make_state(gram, torch.from_numpy(y).cuda())
     state.f = torch.from_numpy(rng.standard_normal(n)).cuda()

@@ -274,7 +274,7 @@ def test_symmetric_matrix_free_virtual_ranks(P, rng, world, k):
     b = rng.standard_normal(n)
     xprev = 0.05 * rng.standard_normal(n)
     cfg = P.SolverConfig(tol=1e-10, ell=8)
-    a_st = P.rbf_kernel(x, params).scaled(dev(s), 1.0)
+    a_st = P.rbf_kernel(dev(x), params).scaled(dev(s), 1.0)
     if k:
         w = rng.standard_normal((n, k))
         basis = P.refresh_basis(a_st, w)
