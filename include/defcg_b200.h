@@ -89,6 +89,8 @@ typedef struct dcg_operator {
     double diag;              /* RBF: diagonal value (var + jitter)              */
     const double* d_s;        /* optional symmetric scaling s (n), NULL = ones   */
     double shift;             /* identity shift                                  */
+    const double* d_kp;       /* DENSE_SYM, optional: K's lower-triangle 64 x 64 */
+                              /* tiles packed by dcg_pack_sym (NULL = read d_k)  */
 } dcg_operator;
 
 /* ---- deflation basis (solvers.py:84-115 RecycleBasis) -------------------- */
@@ -180,6 +182,17 @@ DCG_API int dcg_sym_eigen(dcg_context* ctx, void* stream, const double* d_a, lon
 DCG_API int dcg_gen_sym_eigen(dcg_context* ctx, void* stream, const double* d_g, const double* d_f,
                       long long n, long long max_sweeps, double* d_values,
                       double* d_vectors, long long* info);
+
+/* Packed copy of an exactly symmetric K for DCG_OP_DENSE_SYM operators: the
+ * lower-triangle 64 x 64 tiles in tile-row order, each one contiguous 32 KB
+ * block (zero beyond n, XOR-swizzled as the GEMV's shared-memory ring holds
+ * it), so every tile is ONE bulk copy and DRAM pages are read sequentially.
+ * The products and solves read d_kp instead of d_k when it is set; values
+ * are those of the row-major path.  Not in the reference: its matvec reads
+ * the dense ndarray (_core.pyx:16-28, linalg.py:58-63).                      */
+DCG_API long long dcg_packed_sym_doubles(long long n);
+DCG_API int dcg_pack_sym(dcg_context* ctx, void* stream, const double* d_k, long long ldk, long long n,
+                 double* d_kp);
 
 /* ---- L2: operator and Krylov solvers (solvers.py) ------------------------ */
 /* y = A x (rows of this rank only: y has op->rows entries)                    */

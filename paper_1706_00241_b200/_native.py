@@ -70,6 +70,7 @@ class COperator(ctypes.Structure):
         ("diag", _D),
         ("d_s", _P),
         ("shift", _D),
+        ("d_kp", _P),
     ]
 
 
@@ -105,7 +106,10 @@ class CSolveInfo(ctypes.Structure):
     ]
 
 
-# name -> argtypes (restype is always c_int unless listed)
+_RESTYPES = {"dcg_status_string": ctypes.c_char_p, "dcg_launch_count": ctypes.c_longlong,
+             "dcg_packed_sym_doubles": ctypes.c_longlong}
+
+# name -> argtypes (restype is always c_int unless listed in _RESTYPES)
 SIGNATURES = {
     "dcg_version": [],
     "dcg_launch_count": [],
@@ -122,6 +126,8 @@ SIGNATURES = {
     "dcg_k_rbf_cross": [_P, _P, _P, _LL, _P, _LL, _LL, _D, _D, _P],
     "dcg_k_jacobi_sweep": [_P, _P, _P, _P, _LL, _PLL],
     "dcg_check_symmetric": [_P, _P, _P, _LL, _LL, _D, _PI],
+    "dcg_packed_sym_doubles": [_LL],
+    "dcg_pack_sym": [_P, _P, _P, _LL, _LL, _P],
     "dcg_sym_eigen": [_P, _P, _P, _LL, _LL, _D, _P, _P, _PLL],
     "dcg_gen_sym_eigen": [_P, _P, _P, _P, _LL, _LL, _P, _P, _PLL],
     "dcg_op_apply": [_P, _P, ctypes.POINTER(COperator), _P, _P],
@@ -250,8 +256,7 @@ def load_library():
                 for name, args in SIGNATURES.items():
                     fn = getattr(lib, name)
                     fn.argtypes = args
-                    fn.restype = {"dcg_status_string": ctypes.c_char_p, "dcg_launch_count": ctypes.c_longlong}.get(
-                        name, ctypes.c_int)
+                    fn.restype = _RESTYPES.get(name, ctypes.c_int)
                 _lib = lib
     return _lib
 

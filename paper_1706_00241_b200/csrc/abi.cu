@@ -28,13 +28,14 @@ int dcg_gemv_launch(dcg_context*, cudaStream_t, const double*, long long, long l
                     const double*, const double*, double, const double*, double*);
 size_t dcg_sym_apply_scratch_doubles(long long n);
 size_t dcg_sym_apply2_scratch_doubles(long long n);
-int dcg_sym_apply2(dcg_context*, cudaStream_t, const double*, long long, long long, const double*, const double*,
+int dcg_sym_apply2(dcg_context*, cudaStream_t, const double*, const double*, long long, long long, const double*,
+                   const double*,
                    const double*, const double*, const double*, const double*, double, double, double*, double*,
                    double*);
 int dcg_newton_prep2_launch(dcg_context*, cudaStream_t, long long, const double*, const double*, const double*,
                             const double*, double*, double*, double*);
-int dcg_sym_apply(dcg_context*, cudaStream_t, const double*, long long, long long, const double*, const double*,
-                  const double*, double, double*, double*);
+int dcg_sym_apply(dcg_context*, cudaStream_t, const double*, const double*, long long, long long, const double*,
+                  const double*, const double*, double, double*, double*);
 size_t dcg_block_apply_scratch_doubles(long long n, long long rows, int k);
 int dcg_block_apply(dcg_context*, cudaStream_t, const double*, long long, long long, long long, const double*, int,
                     const double*, const double*, double, const double*, double*, double*);
@@ -394,7 +395,7 @@ static int apply_k(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, co
     if (op->kind == DCG_OP_RBF) return dcg_rbf_mf_apply(ctx, st, op, v, s_in, s_out, shift, y, scratch);
     // the lower-triangle strategy stages 16-byte slices of v and s_in
     if (op->kind == DCG_OP_DENSE_SYM && aligned16(v) && aligned16(s_in))
-        return dcg_sym_apply(ctx, st, op->d_k, op->ldk, op->n, v, s_in, s_out, shift, y, scratch);
+        return dcg_sym_apply(ctx, st, op->d_k, op->d_kp, op->ldk, op->n, v, s_in, s_out, shift, y, scratch);
     return dcg_gemv_launch(ctx, st, op->d_k, op->ldk, op->n, op->rows, v, s_in, s_out, shift, v + op->row0, y);
 }
 
@@ -758,7 +759,7 @@ extern "C" int dcg_gpc_newton_system_ax0(dcg_context* ctx, void* stream, const d
     }
     rc = dcg_newton_prep2_launch(ctx, st, n, d_f, d_grad, d_h, d_x_prev, d_s, d_inner, xs);
     if (rc) return rc;
-    return dcg_sym_apply2(ctx, st, kop->d_k, kop->ldk, n, d_inner, xs, nullptr, d_x_prev, d_s, d_s, 0.0, 1.0, d_b,
+    return dcg_sym_apply2(ctx, st, kop->d_k, kop->d_kp, kop->ldk, n, d_inner, xs, nullptr, d_x_prev, d_s, d_s, 0.0, 1.0, d_b,
                           d_ax0, scratch);
 }
 

@@ -55,25 +55,51 @@ int dcg_gemv_launch(dcg_context* ctx, cudaStream_t st, const double* K, long lon
 // the tiles, pass 2 combines the per-tile partials.  Both launches use the
 // same grid, which fixes the tile partition.
 // =============================================================================
-__global__ void __launch_bounds__(DCG_NT, 1)
-    sym_pass1_kernel(const double* __restrict__ K, long long ldk, long long n, const double* v, const double* s_in,
-                     double* colpart, double* rowpart) {
-    extern __shared__ __align__(16) double smem[];
-    sym_ring_init(smem, n);
-    unsigned int seq = 0;
-    sym_pass1<false>(K, ldk, n, v, s_in, colpart, rowpart, smem, seq);
+// Packed copy (dcg_pack_sym): one CTA per 64 x 64 lower-triangle tile; each
+// thread moves 16-byte chunks (r, q) from the row-major rows into the tile's
+// swizzled slot, zero beyond n.
+__global__ void __launch_bounds__(256) pack_sym_kernel(const double* __restrict__ K, long long ldk, long long n,
+                                                       double* __restrict__ kp) {
+    const long long t = blockIdx.x;
+    const long long I = sym_tile_row(t), J = t - sym_tile_row_base(I);
+    double* dst = kp + t * DCG_SYM_TILE_DOUBLES;
+    for (int c = threadIdx.x; c < DCG_SYM_TILE_DOUBLES / 2; c += blockDim.x) {
+        const int r = c >> 5, q = c & 31;
+        const long long gi = I * DCG_TB + r, gj = J * DCG_TB + 2 * q;
+        double2 val = make_double2(0.0, 0.0);
+        if (gi < n) {
+            const double* src = K + gi * ldk + gj;
+            if (gj + 1 < n) val = __ldg(reinterpret_cast<const double2*>(src));
+            else if (gj < n) val.x = __ldg(src);
+        }
+        *reinterpret_cast<double2*>(dst + sym_swz(r, 2 * q)) = val;
+    }
+}
+
+extern "C" long long dcg_packed_sym_doubles(long long n) { return n > 0 ? sym_packed_doubles(n) : 0; }
+
+extern "C" int dcg_pack_sym(dcg_context* ctx, void* stream, const double* d_k, long long ldk, long long n,
+                            double* d_kp) {
+    if (!ctx || n < 0 || ldk < n || (ldk & 1) || !aligned16(d_k) || !aligned16(d_kp)) return DCG_E_CONFIG;
+    if (n == 0) return DCG_OK;
+    const long long ntt = sym_ntiles(n);
+    if (ntt > 0x7fffffffLL) return DCG_E_UNSUPPORTED;
+    pack_sym_kernel<<<(unsigned)ntt, 256, 0, as_stream(stream)>>>(d_k, ldk, n, d_kp);
+    DCG_LAUNCHED();
+    return DCG_OK;
 }
 
 // Both passes in one cooperative launch (grid barrier between them): no
 // second launch, and pass 2's partial reads follow pass 1 without a gap.
+template <bool PK>
 __global__ void __launch_bounds__(DCG_NT, 1)
     sym_apply_coop_kernel(const double* __restrict__ K, long long ldk, long long n, const double* v,
                           const double* s_in, const double* s_out, double shift, double* colpart, double* rowpart,
                           double* y, unsigned int* bar) {
     extern __shared__ __align__(16) double smem[];
-    sym_ring_init(smem, n);
+    sym_ring_init(smem, n, PK);
     unsigned int seq = 0;
-    sym_pass1<false>(K, ldk, n, v, s_in, colpart, rowpart, smem, seq);
+    sym_pass1<false, 1, PK>(K, ldk, n, v, s_in, colpart, rowpart, smem, seq);
     dcg_grid_barrier(bar, gridDim.x);
     const long long q0 = sym_row_begin(n, gridDim.x, blockIdx.x);
     const long long q1 = sym_row_begin(n, gridDim.x, blockIdx.x + 1);
@@ -102,8 +128,10 @@ __global__ void __launch_bounds__(DCG_NT, 1)
 size_t dcg_sym_apply_scratch_doubles(long long n) { return 2 * (size_t)sym_ntiles(n) * DCG_TB + 32; }
 
 // y = shift v + s_out (.) K (s_in (.) v) with K exactly symmetric (n x n, unsharded).
-int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, long long ldk, long long n, const double* v,
-                  const double* s_in, const double* s_out, double shift, double* y, double* scratch) {
+// Kp (optional): the packed tiles of K (dcg_pack_sym), read instead of K.
+int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, const double* Kp, long long ldk, long long n,
+                  const double* v, const double* s_in, const double* s_out, double shift, double* y,
+                  double* scratch) {
     if (n <= 0) return DCG_OK;
     // One SM is left to the single-CTA Ritz pencil that the def-CG sequence
     // runs concurrently on the side stream (the K-products of the Newton
@@ -113,7 +141,6 @@ int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, long long 
     // (pencil 220 -> 360 us, pass 1 73 -> 117 us).
     size_t smem = sizeof(double) * (size_t)sym_smem_doubles();
     if (ctx->smem_optin > smem) smem = ctx->smem_optin;
-    DCG_CUDA(cudaFuncSetAttribute(sym_pass1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const long long ntt = sym_ntiles(n);
     double* colpart = scratch;
     double* rowpart = scratch + ntt * DCG_TB;
@@ -121,11 +148,14 @@ int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, long long 
     const int G = navail < DCG_SYM_MAX_CTAS ? navail : DCG_SYM_MAX_CTAS;
     // one cooperative launch: pass 1, grid barrier, pass 2 (barrier word after the partials)
     unsigned int* bar = reinterpret_cast<unsigned int*>(rowpart + ntt * DCG_TB);
-    DCG_SMEM_ATTR(sym_apply_coop_kernel, smem);
+    const void* kfn = Kp ? (const void*)sym_apply_coop_kernel<true> : (const void*)sym_apply_coop_kernel<false>;
+    if (Kp) DCG_SMEM_ATTR(sym_apply_coop_kernel<true>, smem);
+    else DCG_SMEM_ATTR(sym_apply_coop_kernel<false>, smem);
     DCG_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), st));
-    void* args[] = {(void*)&K, (void*)&ldk, (void*)&n, (void*)&v, (void*)&s_in, (void*)&s_out, (void*)&shift,
+    const double* Ksrc = Kp ? Kp : K;
+    void* args[] = {(void*)&Ksrc, (void*)&ldk, (void*)&n, (void*)&v, (void*)&s_in, (void*)&s_out, (void*)&shift,
                     (void*)&colpart, (void*)&rowpart, (void*)&y, (void*)&bar};
-    DCG_CUDA(cudaLaunchCooperativeKernel((const void*)sym_apply_coop_kernel, dim3(G), dim3(DCG_NT), args, smem, st));
+    DCG_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(DCG_NT), args, smem, st));
     dcg_count_launch();
     return DCG_OK;
 }
@@ -135,17 +165,18 @@ int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, long long 
 // x1, x2 are the (already input-scaled) operands, v1, v2 the shift vectors.
 // Same tile partition, partial layout and pass-2 order as two dcg_sym_apply
 // calls with (v, s_in) such that x = s_in (.) v: bitwise the same results.
+template <bool PK>
 __global__ void __launch_bounds__(DCG_NT, 1)
     sym_apply2_coop_kernel(const double* __restrict__ K, long long ldk, long long n, const double* x1,
                            const double* x2, const double* v1, const double* v2, const double* s_out1,
                            const double* s_out2, double shift1, double shift2, double* colpart, double* rowpart,
                            long long part2, double* y1, double* y2, unsigned int* bar) {
     extern __shared__ __align__(16) double smem[];
-    sym_ring_init(smem, n);
+    sym_ring_init(smem, n, PK);
     unsigned int seq = 0;
-    // (no L2 cache hints in the standalone products: a cp.async with a cache
-    // hint faulted here as an illegal instruction on sm_100a)
-    sym_pass1<false, 2>(K, ldk, n, x1, nullptr, colpart, rowpart, smem, seq, x2, part2);
+    // (no L2 cache hints on the row-major copies of the standalone products: a
+    // cp.async with a cache hint faulted here as an illegal instruction on sm_100a)
+    sym_pass1<false, 2, PK>(K, ldk, n, x1, nullptr, colpart, rowpart, smem, seq, x2, part2);
     dcg_grid_barrier(bar, gridDim.x);
     const long long q0 = sym_row_begin(n, gridDim.x, blockIdx.x);
     const long long q1 = sym_row_begin(n, gridDim.x, blockIdx.x + 1);
@@ -164,7 +195,8 @@ __global__ void __launch_bounds__(DCG_NT, 1)
 
 size_t dcg_sym_apply2_scratch_doubles(long long n) { return 4 * (size_t)sym_ntiles(n) * DCG_TB + 32; }
 
-int dcg_sym_apply2(dcg_context* ctx, cudaStream_t st, const double* K, long long ldk, long long n, const double* x1,
+int dcg_sym_apply2(dcg_context* ctx, cudaStream_t st, const double* K, const double* Kp, long long ldk, long long n,
+                   const double* x1,
                    const double* x2, const double* v1, const double* v2, const double* s_out1, const double* s_out2,
                    double shift1, double shift2, double* y1, double* y2, double* scratch) {
     if (n <= 0) return DCG_OK;
@@ -178,13 +210,16 @@ int dcg_sym_apply2(dcg_context* ctx, cudaStream_t st, const double* K, long long
     const int navail = ctx->sm_count > 1 ? ctx->sm_count - 1 : 1;
     const int G = navail < DCG_SYM_MAX_CTAS ? navail : DCG_SYM_MAX_CTAS;
     unsigned int* bar = reinterpret_cast<unsigned int*>(scratch + 4 * ntt * DCG_TB);
-    DCG_SMEM_ATTR(sym_apply2_coop_kernel, smem);
+    const void* kfn = Kp ? (const void*)sym_apply2_coop_kernel<true> : (const void*)sym_apply2_coop_kernel<false>;
+    if (Kp) DCG_SMEM_ATTR(sym_apply2_coop_kernel<true>, smem);
+    else DCG_SMEM_ATTR(sym_apply2_coop_kernel<false>, smem);
     DCG_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), st));
-    void* args[] = {(void*)&K,      (void*)&ldk,    (void*)&n,      (void*)&x1,      (void*)&x2,
+    const double* Ksrc = Kp ? Kp : K;
+    void* args[] = {(void*)&Ksrc,      (void*)&ldk,    (void*)&n,      (void*)&x1,      (void*)&x2,
                     (void*)&v1,     (void*)&v2,     (void*)&s_out1, (void*)&s_out2,  (void*)&shift1,
                     (void*)&shift2, (void*)&colpart, (void*)&rowpart, (void*)&part2, (void*)&y1,
                     (void*)&y2,     (void*)&bar};
-    DCG_CUDA(cudaLaunchCooperativeKernel((const void*)sym_apply2_coop_kernel, dim3(G), dim3(DCG_NT), args, smem, st));
+    DCG_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(DCG_NT), args, smem, st));
     dcg_count_launch();
     return DCG_OK;
 }

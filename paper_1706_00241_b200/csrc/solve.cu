@@ -30,6 +30,7 @@ namespace {
 
 struct SolveArgs {
     const double* K;
+    const double* Kp;      // packed lower-triangle tiles (STRAT_SYMPK)
     long long ldk;
     long long n;
     const double* s;
@@ -163,11 +164,11 @@ __device__ __forceinline__ void reduce_partials(const double* partials, int G, i
 }
 
 // GEMV strategies of the persistent kernel
-enum { STRAT_ROWS = 0, STRAT_SYM = 1, STRAT_RBF = 2 };
+enum { STRAT_ROWS = 0, STRAT_SYM = 1, STRAT_RBF = 2, STRAT_SYMPK = 3 };
 
 // Shared-memory doubles of the GEMV region for each strategy.
 __host__ __device__ __forceinline__ long long gemv_region_doubles(int strat, long long n, int dim, int nteam) {
-    if (strat == STRAT_SYM) return sym_smem_doubles();
+    if (strat == STRAT_SYM || strat == STRAT_SYMPK) return sym_smem_doubles();
     if (strat == STRAT_RBF) return rm_smem_doubles(dim, nteam);
     return min(n, (long long)DCG_QT) + 2 + DCG_NW * DCG_RB;
 }
@@ -212,12 +213,15 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     const double shift = a.shift;
 
     unsigned int ring_seq = 0;
+    constexpr bool kSym = STRAT == STRAT_SYM || STRAT == STRAT_SYMPK;
+    constexpr bool kPk = STRAT == STRAT_SYMPK;
+    int pending = 0;   // packed: tiles of the next pass already in flight
     // symmetric strategy: pass-2 rows are weighted by their partial count
     // (sym_row_begin), not the vector-phase rows [r0, r1); pass-2 outputs are
     // therefore read by other CTAs after a grid barrier, through L2.
     long long q0 = r0, q1 = r1;
-    if constexpr (STRAT == STRAT_SYM) {
-        sym_ring_init(s_g, n);
+    if constexpr (kSym) {
+        sym_ring_init(s_g, n, kPk);
         q0 = sym_row_begin(n, G, blockIdx.x);
         q1 = sym_row_begin(n, G, blockIdx.x + 1);
     }
@@ -241,17 +245,21 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
             sym_pass2(n, a.colpart, a.rowpart, q0, q1, rm_table(s_g), G * a.rbf.nteam,
                       rm_pass2_scratch(s_g, a.rbf.dp), epi);
             PHASE(2);
-        } else if constexpr (STRAT == STRAT_SYM) {
+        } else if constexpr (kSym) {
             PHASE(15);
             unsigned long long tc0 = 0;
             if (a.timers && threadIdx.x == 0) tc0 = globaltimer_ns();
-            sym_pass1(K, a.ldk, n, v, s, a.colpart, a.rowpart, s_g, ring_seq);
+            if constexpr (kPk)
+                sym_pass1<true, 1, true>(a.Kp, 0, n, v, s, a.colpart, a.rowpart, s_g, ring_seq, nullptr, 0, &pending,
+                                         true);
+            else
+                sym_pass1(K, a.ldk, n, v, s, a.colpart, a.rowpart, s_g, ring_seq);
             if (a.timers && threadIdx.x == 0) a.timers[16 + blockIdx.x] += globaltimer_ns() - tc0;
             PHASE(0);
             GSYNC();
             PHASE(1);
             if (a.timers && threadIdx.x == 0) tc0 = globaltimer_ns();
-            sym_pass2<true>(n, a.colpart, a.rowpart, q0, q1, sym_range_table(s_g), G, s_g, epi);
+            sym_pass2<true>(n, a.colpart, a.rowpart, q0, q1, sym_range_table(s_g), G, s_scr, epi);
             if (a.timers && threadIdx.x == 0) a.timers[16 + gridDim.x + blockIdx.x] += globaltimer_ns() - tc0;
             PHASE(2);
         } else {
@@ -362,6 +370,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
             a.x[i] = 0.0;
             if (a.logR) a.logR[i] = 0.0;
         }
+        if constexpr (kPk) sym_ring_drain(s_g, ring_seq, pending);
         if (blockIdx.x == 0 && tid == 0) {
             a.history[0] = 0.0;
             a.st->status = DCG_OK;
@@ -450,6 +459,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         PHASE(5);
         const double d = s_c[0];
         if (d <= 0.0) {   // solvers.py:170-172 (NaN falls through, as in numpy)
+            if constexpr (kPk) sym_ring_drain(s_g, ring_seq, pending);
             if (blockIdx.x == 0 && tid == 0) {
                 a.st->status = DCG_E_BREAKDOWN;
                 a.st->pad = k;
@@ -518,6 +528,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         GSYNC();
         PHASE(12);
     }
+    if constexpr (kPk) sym_ring_drain(s_g, ring_seq, pending);
     if (blockIdx.x == 0 && tid == 0) {
         a.st->status = DCG_OK;
         a.st->pad = k;
@@ -568,7 +579,7 @@ static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, co
     const long long n = op->n;
     if (op->kind != DCG_OP_DENSE && op->kind != DCG_OP_DENSE_SYM && op->kind != DCG_OP_RBF) return DCG_E_UNSUPPORTED;
     const bool sym = op->kind == DCG_OP_DENSE_SYM && ((reinterpret_cast<uintptr_t>(d_x0) | reinterpret_cast<uintptr_t>(op->d_s)) & 15) == 0;
-    const int strat = op->kind == DCG_OP_RBF ? STRAT_RBF : (sym ? STRAT_SYM : STRAT_ROWS);
+    const int strat = op->kind == DCG_OP_RBF ? STRAT_RBF : (sym ? (op->d_kp ? STRAT_SYMPK : STRAT_SYM) : STRAT_ROWS);
     if (op->row0 != 0 || op->rows != n) return DCG_E_UNSUPPORTED;   // sharded solves: host loop
     if (strat == STRAT_RBF) {
         if (!op->d_x || op->dim < 1) return DCG_E_CONFIG;
@@ -600,6 +611,7 @@ static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, co
     SolveArgs a;
     memset(&a, 0, sizeof(a));
     a.K = op->d_k;
+    a.Kp = strat == STRAT_SYMPK ? op->d_kp : nullptr;
     a.ldk = op->ldk;
     a.n = n;
     a.s = op->d_s;
@@ -643,9 +655,10 @@ static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, co
                                                              dcg_solve_smem_bytes(n, k, strat, (int)op->dim, 0))
                                          : 1;
     const size_t smem = dcg_solve_smem_bytes(n, k, strat, (int)op->dim, nteam);
-    const void* kfn = strat == STRAT_RBF ? (const void*)dcg_solve_kernel<STRAT_RBF>
-                      : strat == STRAT_SYM ? (const void*)dcg_solve_kernel<STRAT_SYM>
-                                           : (const void*)dcg_solve_kernel<STRAT_ROWS>;
+    const void* kfn = strat == STRAT_RBF     ? (const void*)dcg_solve_kernel<STRAT_RBF>
+                      : strat == STRAT_SYMPK ? (const void*)dcg_solve_kernel<STRAT_SYMPK>
+                      : strat == STRAT_SYM   ? (const void*)dcg_solve_kernel<STRAT_SYM>
+                                             : (const void*)dcg_solve_kernel<STRAT_ROWS>;
     if (strat == STRAT_RBF) {
         double* opnd = reinterpret_cast<double*>(
             (reinterpret_cast<uintptr_t>(a.rowpart + tiles * DCG_TB) + 255) & ~uintptr_t(255));

@@ -52,6 +52,19 @@ __host__ __device__ __forceinline__ long long sym_tile_row(long long t) {
     return I;
 }
 
+// ---- packed layout (DCG_OP_DENSE_SYM with d_kp) ------------------------------
+// The lower-triangle tiles in pass-1 order, each 64 x 64 tile one contiguous
+// 32 KB block, zero beyond n, and stored in the ring's XOR swizzle (element
+// (r, c) at r * 64 + 2 ((c / 2) ^ (r / 2 mod 32)) + c mod 2): a tile lands in
+// its stage with ONE bulk copy (cp.async.bulk, the TMA engine) and its DRAM
+// pages are read sequentially -- measured 6.7 TB/s streamed through a
+// 4-stage ring against 6.0 TB/s for the row-major tile of 64 rows x 512 B
+// (tools/stream_probe.cu, profiles/r02/stream_probe.jsonl).
+__host__ __device__ __forceinline__ long long sym_packed_doubles(long long n) {
+    return sym_ntiles(n) * (long long)(DCG_TB * DCG_TB);
+}
+__host__ __device__ __forceinline__ int sym_swz(int r, int c) { return r * DCG_TB + 2 * ((c >> 1) ^ ((r >> 1) & 31)) + (c & 1); }
+
 // ---- pass-1 partition: equal estimated cost per CTA ---------------------------
 // Cost in quarter tiles of the tiles [0, t) (measured per-CTA pass times):
 // 4 per tile, +4 per tile-row segment flush (one per completed row: a CTA
@@ -184,6 +197,22 @@ __device__ __forceinline__ void sym_mbar_wait(unsigned long long* bar, unsigned 
         : "memory");
 }
 
+__device__ __forceinline__ void sym_mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}\n" ::"r"(sym_saddr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+// one packed tile (32 KB) into a stage by the bulk-copy (TMA) engine; completion
+// is counted in bytes on the stage's full barrier
+__device__ __forceinline__ void sym_bulk_tile(double* sdst, const double* gsrc, unsigned long long* bar,
+                                              unsigned long long pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+            sym_saddr(sdst)),
+        "l"(gsrc), "r"((unsigned)(DCG_SYM_TILE_DOUBLES * sizeof(double))), "r"(sym_saddr(bar)), "l"(pol)
+        : "memory");
+}
+
 // 16-byte chunk starting at element j of [0, n): bytes to copy (zero-fill beyond n)
 __device__ __forceinline__ int sym_chunk_bytes(long long j, long long n) {
     return j < n ? ((j + 1 < n) ? 16 : 8) : 0;
@@ -263,7 +292,12 @@ __device__ __forceinline__ double sym_xval(const double* v, const double* s, lon
 // The ring's mbarriers are initialised once per launch (re-initialising a
 // live mbarrier is undefined); every pass then continues the CTA's tile
 // sequence number `seq`, from which stage and phase parities follow.
-__device__ __forceinline__ void sym_ring_init(double* smem, long long n) {
+// Row-major storage: every thread copies a share of each tile and arrives
+// (DCG_NT arrivals per use).  Packed storage: thread 0 arms the byte count of
+// the tile's bulk copy (one arrival), threads 0..63 copy the v / s slices
+// and arrive (64 arrivals).
+#define DCG_SYM_PK_ARRIVALS 65
+__device__ __forceinline__ void sym_ring_init(double* smem, long long n, bool packed = false) {
     unsigned long long* full = reinterpret_cast<unsigned long long*>(
         smem + DCG_SYM_STAGES * DCG_SYM_STAGE_DOUBLES + 2 * DCG_NW * DCG_TB);
     unsigned long long* empty = full + DCG_SYM_STAGES;
@@ -272,12 +306,46 @@ __device__ __forceinline__ void sym_ring_init(double* smem, long long n) {
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int st = 0; st < DCG_SYM_STAGES; ++st) {
-            sym_mbar_init(full + st, DCG_NT);     // one cp.async-arrival per thread per use
+            sym_mbar_init(full + st, packed ? DCG_SYM_PK_ARRIVALS : DCG_NT);
             sym_mbar_init(empty + st, DCG_NW);    // one arrival per warp per use
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     sym_fill_range_table(sym_range_table(smem), n);
+}
+
+// Packed storage, threads 0..63: the slices v_J, s_J of a tile into its stage
+// (16-byte cp.async, zero beyond n) and the stage arrival; thread 0 first arms
+// and issues the tile's bulk copy unless it is already in flight.
+__device__ __forceinline__ void sym_issue_packed(const double* kt, long long n, long long J, const double* v,
+                                                 const double* s, double* dst, unsigned long long* full,
+                                                 unsigned long long pol, bool tile) {
+    const int tid = threadIdx.x;
+    if (tile && tid == 0) {
+        sym_mbar_expect_tx(full, (unsigned)(DCG_SYM_TILE_DOUBLES * sizeof(double)));
+        sym_bulk_tile(dst, kt, full, pol);
+    }
+    const long long j = J * DCG_TB + 2 * (tid & 31);
+    const int bytes = sym_chunk_bytes(j, n);
+    if (tid < 32) sym_cp_async16_v(dst + DCG_SYM_TILE_DOUBLES + 2 * tid, bytes ? v + j : v, bytes);
+    else if (s) sym_cp_async16_v(dst + DCG_SYM_TILE_DOUBLES + DCG_TB + 2 * (tid - 32), bytes ? s + j : s, bytes);
+    sym_mbar_cp_arrive(full);
+}
+
+// Packed storage: tiles of the NEXT pass over the same range whose bulk copies
+// were issued at the end of this one (sym_pass1 with prefetch); they overlap
+// the grid barriers and vector phases between two products.  A launch that
+// ends with copies in flight drains them first.
+__device__ __forceinline__ void sym_ring_drain(double* smem, unsigned int seq, int& pending) {
+    if (pending <= 0) return;
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(
+        smem + DCG_SYM_STAGES * DCG_SYM_STAGE_DOUBLES + 2 * DCG_NW * DCG_TB);
+    for (int st = 0; st < pending; ++st) {
+        const unsigned int q = seq + st;
+        if (threadIdx.x < 64) sym_mbar_cp_arrive(full + q % DCG_SYM_STAGES);
+        sym_mbar_wait(full + q % DCG_SYM_STAGES, (q / DCG_SYM_STAGES) & 1);
+    }
+    pending = 0;
 }
 
 // Pass 1 over this CTA's tile range.  colpart/rowpart: ntt x 64 doubles.
@@ -287,10 +355,15 @@ __device__ __forceinline__ void sym_ring_init(double* smem, long long n) {
 // unscaled, s == nullptr) and its partials go to colpart / rowpart + part2 --
 // every tile read from HBM serves two products, each with exactly the
 // operation sequence of its NV = 1 pass.
-template <bool kHint = true, int NV = 1>
+// PK: K is the packed tile array (sym_packed_doubles; ldk unused); `pending`
+// (uniform per CTA) counts tiles of this range whose bulk copies a previous
+// pass already issued, and `prefetch` issues the first DCG_SYM_STAGES - 1
+// tiles of the next pass over the same range once this one is consumed.
+template <bool kHint = true, int NV = 1, bool PK = false>
 __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long long ldk, long long n, const double* v,
                                           const double* s, double* colpart, double* rowpart, double* smem,
-                                          unsigned int& seq, const double* v2 = nullptr, long long part2 = 0) {
+                                          unsigned int& seq, const double* v2 = nullptr, long long part2 = 0,
+                                          int* pending = nullptr, bool prefetch = false) {
     static_assert(NV == 1 || NV == 2, "one or two vectors");
     if constexpr (NV == 2) s = v2;   // the s slot of every stage carries v2
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -312,18 +385,32 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
     const long long row_stride = (long long)DCG_TB * ldk;
     // prologue: tiles 0 .. STAGES-2; issue cursor (iI, iJ, ip) follows
     long long iI = I, iJ = J;
-    const double* ip = K + iI * row_stride + iJ * DCG_TB;
+    const double* ip = PK ? K + t0 * DCG_SYM_TILE_DOUBLES : K + iI * row_stride + iJ * DCG_TB;
+    const int pre = (PK && pending) ? *pending : 0;
 #pragma unroll
     for (int st = 0; st < DCG_SYM_STAGES - 1; ++st) {
         if (st < ntiles) {
             const unsigned int q = q0 + st;
             const int stg = q % DCG_SYM_STAGES;
-            if (q >= DCG_SYM_STAGES) sym_mbar_wait(empty + stg, ((q / DCG_SYM_STAGES) - 1) & 1);
-            sym_issue_tile<kHint>(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES, pol);
-            sym_mbar_cp_arrive(full + stg);
+            if constexpr (PK) {
+                if (tid < 64) {
+                    if (st >= pre && q >= DCG_SYM_STAGES) sym_mbar_wait(empty + stg, ((q / DCG_SYM_STAGES) - 1) & 1);
+                    sym_issue_packed(ip, n, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES, full + stg, pol, st >= pre);
+                }
+            } else {
+                if (q >= DCG_SYM_STAGES) sym_mbar_wait(empty + stg, ((q / DCG_SYM_STAGES) - 1) & 1);
+                sym_issue_tile<kHint>(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES, pol);
+                sym_mbar_cp_arrive(full + stg);
+            }
         }
-        if (++iJ > iI) { ++iI; iJ = 0; ip = K + iI * row_stride; } else { ip += DCG_TB; }
+        if constexpr (PK) {
+            if (++iJ > iI) { ++iI; iJ = 0; }
+            ip += DCG_SYM_TILE_DOUBLES;
+        } else {
+            if (++iJ > iI) { ++iI; iJ = 0; ip = K + iI * row_stride; } else { ip += DCG_TB; }
+        }
     }
+    if (pending) *pending = 0;
     // swizzled offsets of this thread's reads: rows 2l, 2l+1, chunks 2w, 2w+1
     const int key = lane & 31;                                     // (row >> 1) for both rows
     const int o00 = (2 * lane) * DCG_TB + 2 * ((2 * warp) ^ key);
@@ -343,14 +430,25 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
         // produce tile lt + STAGES - 1 into the stage tile lt - 1 used
         {
             const int tn = lt + DCG_SYM_STAGES - 1;
-            if (tn < ntiles) {
-                const unsigned int q = q0 + tn;
-                const int stg = q % DCG_SYM_STAGES;
-                if (q >= DCG_SYM_STAGES) sym_mbar_wait(empty + stg, ((q / DCG_SYM_STAGES) - 1) & 1);
-                sym_issue_tile<kHint>(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES, pol);
-                sym_mbar_cp_arrive(full + stg);
+            if constexpr (PK) {
+                if (tn < ntiles && tid < 64) {
+                    const unsigned int q = q0 + tn;
+                    const int stg = q % DCG_SYM_STAGES;
+                    if (q >= DCG_SYM_STAGES) sym_mbar_wait(empty + stg, ((q / DCG_SYM_STAGES) - 1) & 1);
+                    sym_issue_packed(ip, n, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES, full + stg, pol, true);
+                }
+                if (++iJ > iI) { ++iI; iJ = 0; }
+                ip += DCG_SYM_TILE_DOUBLES;
+            } else {
+                if (tn < ntiles) {
+                    const unsigned int q = q0 + tn;
+                    const int stg = q % DCG_SYM_STAGES;
+                    if (q >= DCG_SYM_STAGES) sym_mbar_wait(empty + stg, ((q / DCG_SYM_STAGES) - 1) & 1);
+                    sym_issue_tile<kHint>(ip, pl, n, iI, iJ, v, s, ring + stg * DCG_SYM_STAGE_DOUBLES, pol);
+                    sym_mbar_cp_arrive(full + stg);
+                }
+                if (++iJ > iI) { ++iI; iJ = 0; ip = K + iI * row_stride; } else { ip += DCG_TB; }
             }
-            if (++iJ > iI) { ++iI; iJ = 0; ip = K + iI * row_stride; } else { ip += DCG_TB; }
         }
         // consume tile lt
         const unsigned int q = q0 + lt;
@@ -473,6 +571,23 @@ __device__ __forceinline__ void sym_pass1(const double* __restrict__ K, long lon
         }
     }
     cta_sync();
+    if constexpr (PK) {
+        // every stage is consumed (the barrier above): the next pass's first
+        // tiles go out now, before the grid barriers, without empty waits
+        if (prefetch && pending) {
+            const int np = ntiles < DCG_SYM_STAGES - 1 ? ntiles : DCG_SYM_STAGES - 1;
+            if (tid == 0) {
+                for (int st = 0; st < np; ++st) {
+                    const unsigned int q = seq + st;
+                    const int stg = q % DCG_SYM_STAGES;
+                    sym_mbar_expect_tx(full + stg, (unsigned)(DCG_SYM_TILE_DOUBLES * sizeof(double)));
+                    sym_bulk_tile(ring + stg * DCG_SYM_STAGE_DOUBLES, K + (t0 + st) * DCG_SYM_TILE_DOUBLES, full + stg,
+                                  pol);
+                }
+            }
+            *pending = np;
+        }
+    }
 }
 
 // Pass 2: t_i for rows [q0, q1) (sym_row_begin partition) from the partials;

@@ -27,8 +27,36 @@ from .errors import DimensionMismatch
 SYMMETRY_RTOL = 1e-12
 
 
-STRATEGIES = ("auto", "sym", "rows")
+STRATEGIES = ("auto", "sym", "sym_rowmajor", "rows")
 SYM_MIN_N = 4096
+
+
+class _PackedTiles:
+    """The packed lower-triangle tile copy of one exactly symmetric K
+    (``dcg_pack_sym``: 64 x 64 tiles, each a contiguous 32 KB block, so the
+    symmetric products stream K with one bulk copy per tile).  Built on first
+    use and shared by every view of the same storage (``scaled``,
+    ``kernel_view``); K is never modified, so it stays valid."""
+
+    __slots__ = ("buf", "event", "stream")
+
+    def __init__(self):
+        self.buf = None
+        self.event = None
+        self.stream = None
+
+    def ptr(self, kbuf: torch.Tensor, n: int, ldk: int) -> int:
+        cur = torch.cuda.current_stream(D.device())
+        if self.buf is None:
+            self.buf = D.empty(int(N.lib().dcg_packed_sym_doubles(n)))
+            N.check(N.lib().dcg_pack_sym(D.ctx(), cur.cuda_stream, kbuf.data_ptr(), ldk, n, self.buf.data_ptr()),
+                    what="pack_sym")
+            self.event = torch.cuda.Event()
+            self.event.record(cur)
+            self.stream = cur.cuda_stream
+        elif cur.cuda_stream != self.stream:
+            cur.wait_event(self.event)
+        return self.buf.data_ptr()
 
 
 class DenseOperator:
@@ -36,13 +64,16 @@ class DenseOperator:
 
     ``strategy`` selects how products stream K: "sym" (default for square,
     unsharded operators; K is exactly symmetric) reads only the lower
-    triangle, "rows" streams full rows (row-sharded slabs, A/B checks)."""
+    triangle, from the packed tile copy (``_PackedTiles``); "sym_rowmajor"
+    reads the same tiles from the row-major storage (A/B checks; bitwise the
+    same values); "rows" streams full rows (row-sharded slabs, A/B checks)."""
 
     __array_priority__ = 100
 
     def __init__(self, kbuf: torch.Tensor, n: int, ldk: int, s: torch.Tensor | None = None, shift: float = 0.0,
-                 row0: int = 0, rows: int | None = None, strategy: str = "auto"):
+                 row0: int = 0, rows: int | None = None, strategy: str = "auto", packed: _PackedTiles | None = None):
         self.kbuf = kbuf
+        self._packed = packed if packed is not None else _PackedTiles()
         self.n = int(n)
         self.ldk = int(ldk)
         self.s = s
@@ -102,10 +133,12 @@ class DenseOperator:
     def scaled(self, s, shift: float) -> "DenseOperator":
         """Same K, new diagonal scaling and shift (the Newton system of gpc.py:175-183)."""
         s_dev = None if s is None else D.to_dev(s, 1)
-        return DenseOperator(self.kbuf, self.n, self.ldk, s_dev, shift, self.row0, self.rows, self.strategy)
+        return DenseOperator(self.kbuf, self.n, self.ldk, s_dev, shift, self.row0, self.rows, self.strategy,
+                             self._packed)
 
     def with_strategy(self, strategy: str) -> "DenseOperator":
-        return DenseOperator(self.kbuf, self.n, self.ldk, self.s, self.shift, self.row0, self.rows, strategy)
+        return DenseOperator(self.kbuf, self.n, self.ldk, self.s, self.shift, self.row0, self.rows, strategy,
+                             self._packed)
 
     # -- views ------------------------------------------------------------------
     @property
@@ -123,8 +156,9 @@ class DenseOperator:
             # below a few thousand rows the Gram is L2-resident and the row
             # strategy's lower latency wins (measured: n = 2000, SURVEY config 1)
             strategy = "sym" if self.n >= SYM_MIN_N else "rows"
-        sym = strategy == "sym" and self.row0 == 0 and self.rows == self.n
+        sym = strategy in ("sym", "sym_rowmajor") and self.row0 == 0 and self.rows == self.n
         op.kind = N.DCG_OP_DENSE_SYM if sym else N.DCG_OP_DENSE
+        op.d_kp = self._packed.ptr(self.kbuf, self.n, self.ldk) if sym and strategy == "sym" and self.n else None
         op.n = self.n
         op.row0 = self.row0
         op.rows = self.rows
@@ -136,7 +170,8 @@ class DenseOperator:
 
     def kernel_view(self) -> "DenseOperator":
         """K itself (no scaling, no shift)."""
-        return DenseOperator(self.kbuf, self.n, self.ldk, None, 0.0, self.row0, self.rows, self.strategy)
+        return DenseOperator(self.kbuf, self.n, self.ldk, None, 0.0, self.row0, self.rows, self.strategy,
+                             self._packed)
 
     def matvec_dev(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         y = D.empty(self.rows) if out is None else out

@@ -74,7 +74,7 @@ def test_struct_layout_matches_header(tmp_path):
 #include <stddef.h>
 #include "{HEADER}"
 int main(void) {{
-  printf("%zu %zu %zu %zu\\n", sizeof(dcg_operator), offsetof(dcg_operator, d_s), offsetof(dcg_operator, shift), offsetof(dcg_operator, dim));
+  printf("%zu %zu %zu %zu %zu\\n", sizeof(dcg_operator), offsetof(dcg_operator, d_s), offsetof(dcg_operator, shift), offsetof(dcg_operator, dim), offsetof(dcg_operator, d_kp));
   printf("%zu %zu\\n", sizeof(dcg_basis), offsetof(dcg_basis, d_chol));
   printf("%zu %zu\\n", sizeof(dcg_solver_config), offsetof(dcg_solver_config, recompute_residual_every));
   printf("%zu %zu\\n", sizeof(dcg_krylov_log), offsetof(dcg_krylov_log, d_mu));
@@ -87,7 +87,7 @@ int main(void) {{
     rows = [list(map(int, line.split())) for line in subprocess.run([str(exe)], capture_output=True,
                                                                      text=True).stdout.split("\n") if line]
     assert rows[0] == [ctypes.sizeof(N.COperator), N.COperator.d_s.offset, N.COperator.shift.offset,
-                       N.COperator.dim.offset]
+                       N.COperator.dim.offset, N.COperator.d_kp.offset]
     assert rows[1] == [ctypes.sizeof(N.CBasis), N.CBasis.d_chol.offset]
     assert rows[2] == [ctypes.sizeof(N.CSolverConfig), N.CSolverConfig.recompute_residual_every.offset]
     assert rows[3] == [ctypes.sizeof(N.CKrylovLog), N.CKrylovLog.d_mu.offset]

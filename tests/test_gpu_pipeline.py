@@ -128,7 +128,7 @@ def test_deficient_extraction_on_device(P):
     assert ss.basis is None
 
 
-@pytest.mark.parametrize("strategy", ["sym", "rows"])
+@pytest.mark.parametrize("strategy", ["sym", "sym_rowmajor", "rows"])
 @pytest.mark.parametrize("n", [300, 1000, 2113, 4500])
 def test_fused_newton_system_matches_separate_products(P, n, strategy):
     """dcg_gpc_newton_system_ax0 (b and ax0 = A x_prev from one pass over a

@@ -63,3 +63,59 @@ def test_sym_solve_matches_rows(P, n, k):
     assert np.linalg.norm(xs - xr) / np.linalg.norm(xr) <= 1e-9
     dense = kmat * np.outer(s, s) + np.eye(n)
     assert np.linalg.norm(b - dense @ xs) / np.linalg.norm(b) <= 2e-10
+
+
+@pytest.mark.parametrize("n", [1, 63, 64, 65, 257, 2049, 5000])
+def test_packed_tiles_bitwise_rowmajor(P, n):
+    """The packed tile copy (dcg_pack_sym, one bulk copy per tile) gives
+    bitwise the products of the row-major lower-triangle tiles."""
+    import torch
+
+    rng = np.random.default_rng(100 + n)
+    a = O.rbf_kernel(rng.standard_normal((n, 4)), 1.0, 1.3)
+    op = P.DenseOperator.from_matrix(a).with_strategy("sym")
+    rm = op.with_strategy("sym_rowmajor")
+    assert P._native.lib().dcg_packed_sym_doubles(n) == ((n + 63) // 64) * ((n + 63) // 64 + 1) // 2 * 4096
+    x = rng.standard_normal(n)
+    s = rng.uniform(0.2, 0.6, n)
+    for shift, sv in ((0.0, None), (1.0, s)):
+        assert np.array_equal(op.scaled(sv, shift) @ x, rm.scaled(sv, shift) @ x)
+    # the packed copy holds the swizzled lower triangle, zero beyond n
+    buf = op._packed.buf.cpu().numpy().reshape(-1, 64, 64)
+    nt = (n + 63) // 64
+    t = nt * (nt + 1) // 2 - 1          # last (diagonal, edge) tile
+    r = np.arange(64)[:, None]
+    c = np.arange(64)[None, :]
+    swz = r * 64 + 2 * ((c // 2) ^ ((r // 2) % 32)) + c % 2
+    tile = buf[t].reshape(-1)[swz]
+    kpad = np.zeros((nt * 64, nt * 64))
+    kpad[:n, :n] = a
+    assert np.array_equal(tile, kpad[(nt - 1) * 64:, (nt - 1) * 64:])
+    del torch
+
+
+@pytest.mark.parametrize("n,k,recompute", [(4500, 0, 0), (4500, 16, 0), (5000, 12, 7)])
+def test_packed_solve_bitwise_rowmajor(P, n, k, recompute):
+    """Persistent solve on the packed tiles (next pass's tiles issued before
+    the grid barriers) against the row-major symmetric path: the same
+    iterations and bitwise the same solution, with and without deflation and
+    true-residual refreshes (extra products between iterations)."""
+    rng = np.random.default_rng(11 + n + k)
+    x = rng.standard_normal((n, 6))
+    gram = P.DenseOperator.from_matrix(O.rbf_kernel(x, 1.0, 1.4)).with_strategy("sym")
+    s = rng.uniform(0.1, 0.5, n)
+    A = gram.scaled(s, 1.0)
+    R = A.with_strategy("sym_rowmajor")
+    b = rng.standard_normal(n)
+    cfg = P.SolverConfig(tol=1e-10, ell=k + 4, recompute_residual_every=recompute)
+    if k:
+        w = rng.standard_normal((n, k))
+        x0 = rng.standard_normal(n)
+        xs, rs, _ = P.deflated_cg_solve(A, b, x0, P.refresh_basis(A, w), cfg)
+        xr, rr, _ = P.deflated_cg_solve(R, b, x0, P.refresh_basis(R, w), cfg)
+    else:
+        xs, rs, _ = P.cg_solve(A, b, None, cfg)
+        xr, rr, _ = P.cg_solve(R, b, None, cfg)
+    assert rs.iterations == rr.iterations
+    assert np.array_equal(xs, xr)
+    assert np.array_equal(rs.residual_history, rr.residual_history)
