@@ -295,14 +295,17 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         return t;
     };
     // Publish this CTA's partials: slot 0 = sum_i q_i^2 with q_i = sqval(i)
-    // (thread-per-row; sqval may log), slots 1+j = sum_i M[i][j] u[i] (thread
-    // (row group, j), coalesced rows of M).  Fixed combination order.
-    auto own_partials = [&](auto sqval, const double* u, const double* M, double* partials) {
+    // (thread-per-row; sqval may log, or write u_i itself: `sync_mid` then
+    // orders those writes before the reads of u below), slots 1+j = sum_i
+    // M[i][j] u[i] (thread (row group, j), coalesced rows of M).  Fixed
+    // combination order.
+    auto own_partials = [&](auto sqval, const double* u, const double* M, double* partials, bool sync_mid = false) {
         double sq = 0.0;
         for (long long i = r0 + tid; i < r1; i += DCG_NT) {
             const double q = sqval(i);
             sq = add_rn(sq, mul_rn(q, q));
         }
+        if (sync_mid && M) cta_sync();
         double c = 0.0;
         if (M) {
             const int j = tid & (swk - 1), grp = tid / swk, ngrp = DCG_NT / swk;
@@ -469,11 +472,12 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
             return;
         }
         const double alpha = rr / d;
-        for (long long i = r0 + tid; i < r1; i += blockDim.x)
-            a.x[i] = add_rn(a.x[i], mul_rn(alpha, a.p[i]));
         ++it;
         const bool recompute = (a.recompute > 0) && (it % a.recompute == 0);
+        const bool log_r = (it - 1) < ell;
         if (recompute) {
+            for (long long i = r0 + tid; i < r1; i += blockDim.x)
+                a.x[i] = add_rn(a.x[i], mul_rn(alpha, a.p[i]));
             GSYNC();
             gemv(a.x, [&](long long i, double t) {
                 const double xi = ld_cg(a.x + i);
@@ -481,20 +485,29 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
                 a.r[i] = sub_rn(a.b[i], ax);
             });
             if constexpr (STRAT != STRAT_ROWS) GSYNC();
+            cta_sync();
+            PHASE(6);
+            own_partials(
+                [&](long long i) {
+                    const double ri = ld_cg(a.r + i);
+                    if (log_r) a.logR[it * n + i] = ri;
+                    return ri;
+                },
+                a.r, deflate ? a.AW : nullptr, a.partials);
         } else {
-            for (long long i = r0 + tid; i < r1; i += blockDim.x)
-                a.r[i] = sub_rn(ld_cg(a.r + i), mul_rn(alpha, ld_cg(a.ap + i)));
+            PHASE(6);
+            // x += alpha p and r -= alpha Ap on the own rows, inside the r'r loop
+            own_partials(
+                [&](long long i) {
+                    const double pi = a.p[i];
+                    a.x[i] = add_rn(a.x[i], mul_rn(alpha, pi));
+                    const double ri = sub_rn(ld_cg(a.r + i), mul_rn(alpha, ld_cg(a.ap + i)));
+                    a.r[i] = ri;
+                    if (log_r) a.logR[it * n + i] = ri;
+                    return ri;
+                },
+                a.r, deflate ? a.AW : nullptr, a.partials, true);
         }
-        cta_sync();
-        PHASE(6);
-        const bool log_r = (it - 1) < ell;
-        own_partials(
-            [&](long long i) {
-                const double ri = ld_cg(a.r + i);
-                if (log_r) a.logR[it * n + i] = ri;
-                return ri;
-            },
-            a.r, deflate ? a.AW : nullptr, a.partials);
         PHASE(7);
         GSYNC();
         PHASE(8);
