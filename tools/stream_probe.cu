@@ -36,6 +36,12 @@ __device__ __forceinline__ unsigned long long pol_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ unsigned long long pol_normal() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ int g_policy;   // 0 evict_first, 1 evict_normal
 __device__ __forceinline__ void bulk(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
                                      unsigned long long pol) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
@@ -68,7 +74,7 @@ __global__ void __launch_bounds__(NT, 1) ring_kernel(const double* K, long long 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const unsigned long long pol = pol_first();
+    const unsigned long long pol = g_policy ? pol_normal() : pol_first();
     auto issue = [&](int lt) {
         const int st = lt % stages;
         double* dst = smem + st * TILE;
@@ -152,6 +158,10 @@ int main(int argc, char** argv) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const double bytes = (double)packed;
+    {
+        const int pm = getenv("PROBE_POLICY") ? atoi(getenv("PROBE_POLICY")) : 0;
+        cudaMemcpyToSymbol(g_policy, &pm, sizeof(int));
+    }
     for (int stages = 3; stages <= 6; ++stages) {
         if (argc > 2 && atoi(argv[2]) > 0 && stages != atoi(argv[2])) continue;
         const size_t smem = (size_t)stages * TILE * 8 + 2 * stages * 8;
