@@ -41,6 +41,31 @@ int dcg_block_apply(dcg_context*, cudaStream_t, const double*, long long, long l
                     const double*, const double*, double, const double*, double*, double*);
 int dcg_xty(dcg_context*, cudaStream_t, const double*, long long, const double*, long long, long long, int, int,
             double*, double*);
+size_t dcg_sym_block_scratch_doubles(long long n);
+bool dcg_sym_block_ok(int k);
+int dcg_sym_block_apply(dcg_context*, cudaStream_t, const double*, long long, const double*, int, const double*,
+                        const double*, double, double*, double*);
+
+// The refresh's block product A W over the operator's storage: the packed
+// lower-triangle tiles with the symmetric DMMA product (symblock.cu, half the
+// bytes) when the operator has them and k <= 16, else the row-major DMMA GEMM.
+// DCG_NO_SYMBLOCK (developer A/B knob) forces the row-major product.
+static bool use_sym_block(const dcg_operator* op, int k) {
+    static const bool off = getenv("DCG_NO_SYMBLOCK") != nullptr;
+    return !off && op->kind == DCG_OP_DENSE_SYM && op->d_kp && op->row0 == 0 && op->rows == op->n &&
+           dcg_sym_block_ok(k);
+}
+static size_t block_scratch_doubles(const dcg_operator* op, int k) {
+    return use_sym_block(op, k) ? dcg_sym_block_scratch_doubles(op->n)
+                                : dcg_block_apply_scratch_doubles(op->n, op->rows, k);
+}
+static int block_apply_op(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, const double* X, int k,
+                          const double* s_in, const double* s_out, double shift, const double* X_rows, double* Y,
+                          double* scratch) {
+    if (use_sym_block(op, k))
+        return dcg_sym_block_apply(ctx, st, op->d_kp, op->n, X, k, s_in, s_out, shift, Y, scratch);
+    return dcg_block_apply(ctx, st, op->d_k, op->ldk, op->rows, op->n, X, k, s_in, s_out, shift, X_rows, Y, scratch);
+}
 size_t dcg_xty_scratch_doubles(dcg_context* ctx, int p, int q);
 int dcg_gemm_lr(dcg_context*, cudaStream_t, const double*, long long, const double*, long long, double*, long long,
                 long long, long long, long long);
@@ -420,11 +445,11 @@ extern "C" int dcg_op_apply_block(dcg_context* ctx, void* stream, const dcg_oper
     if (op->kind == DCG_OP_RBF)
         return dcg_rbf_mf_block(ctx, as_stream(stream), op, d_x, (int)k, op->d_s,
                                 op->d_s ? op->d_s + op->row0 : nullptr, op->shift, d_y);
-    rc = dcg_ws_reserve(ctx, sizeof(double) * dcg_block_apply_scratch_doubles(op->n, op->rows, (int)k) + 256);
+    rc = dcg_ws_reserve(ctx, sizeof(double) * block_scratch_doubles(op, (int)k) + 256);
     if (rc) return rc;
     const double* s_out = op->d_s ? op->d_s + op->row0 : nullptr;
-    return dcg_block_apply(ctx, as_stream(stream), op->d_k, op->ldk, op->rows, op->n, d_x, (int)k, op->d_s, s_out,
-                           op->shift, d_x + op->row0 * k, d_y, static_cast<double*>(ctx->ws));
+    return block_apply_op(ctx, as_stream(stream), op, d_x, (int)k, op->d_s, s_out, op->shift, d_x + op->row0 * k, d_y,
+                          static_cast<double*>(ctx->ws));
 }
 
 // ---------------------------------------------------------------------------
@@ -521,19 +546,18 @@ extern "C" int dcg_refresh_basis(dcg_context* ctx, void* stream, const dcg_opera
     if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
     cudaStream_t st = as_stream(stream);
     const size_t nk = sizeof(double) * n * k;
-    const size_t need = al(sizeof(double) * dcg_block_apply_scratch_doubles(n, n, (int)k)) + al(nk) +
+    const size_t need = al(sizeof(double) * block_scratch_doubles(op, (int)k)) + al(nk) +
                         gram_scratch_bytes(ctx, (int)k);
     rc = dcg_ws_reserve(ctx, need);
     if (rc) return rc;
     Arena ar{static_cast<char*>(ctx->ws), 0};
     double* aw = ar.take<double>(n * k);
     int* active = ar.take<int>(DCG_MAX_K);
-    double* scratch = ar.take<double>(dcg_block_apply_scratch_doubles(n, n, (int)k));
+    double* scratch = ar.take<double>(block_scratch_doubles(op, (int)k));
     if (op->kind == DCG_OP_RBF)
         rc = dcg_rbf_mf_block(ctx, st, op, d_w, (int)k, op->d_s, op->d_s, op->shift, aw);
     else
-        rc = dcg_block_apply(ctx, st, op->d_k, op->ldk, n, n, d_w, (int)k, op->d_s, op->d_s, op->shift, d_w, aw,
-                             scratch);
+        rc = block_apply_op(ctx, st, op, d_w, (int)k, op->d_s, op->d_s, op->shift, d_w, aw, scratch);
     if (rc) return rc;
     long long kk = k;
     rc = gram_core(ctx, st, d_w, aw, n, (int)k, 1, d_chol, active, &kk, info, ar);
@@ -593,19 +617,18 @@ extern "C" int dcg_refresh_basis_async(dcg_context* ctx, void* stream, const dcg
     if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
     const long long n = op->n;
     const size_t nk = sizeof(double) * n * k;
-    const size_t need = al(sizeof(double) * dcg_block_apply_scratch_doubles(n, n, (int)k)) + al(nk) +
+    const size_t need = al(sizeof(double) * block_scratch_doubles(op, (int)k)) + al(nk) +
                         gram_scratch_bytes(ctx, (int)k);
     rc = dcg_ws_reserve(ctx, need);
     if (rc) return rc;
     Arena ar{static_cast<char*>(ctx->ws), 0};
     double* aw = ar.take<double>(n * k);
     int* active = ar.take<int>(DCG_MAX_K);
-    double* scratch = ar.take<double>(dcg_block_apply_scratch_doubles(n, n, (int)k));
+    double* scratch = ar.take<double>(block_scratch_doubles(op, (int)k));
     if (op->kind == DCG_OP_RBF)
         rc = dcg_rbf_mf_block(ctx, st, op, d_w, (int)k, op->d_s, op->d_s, op->shift, aw);
     else
-        rc = dcg_block_apply(ctx, st, op->d_k, op->ldk, n, n, d_w, (int)k, op->d_s, op->d_s, op->shift, d_w, aw,
-                             scratch);
+        rc = block_apply_op(ctx, st, op, d_w, (int)k, op->d_s, op->d_s, op->shift, d_w, aw, scratch);
     if (rc) return rc;
     double* graw = ar.take<double>((size_t)k * k);
     double* gsym = ar.take<double>((size_t)k * k);

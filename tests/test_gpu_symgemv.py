@@ -111,11 +111,34 @@ def test_packed_solve_bitwise_rowmajor(P, n, k, recompute):
     if k:
         w = rng.standard_normal((n, k))
         x0 = rng.standard_normal(n)
-        xs, rs, _ = P.deflated_cg_solve(A, b, x0, P.refresh_basis(A, w), cfg)
-        xr, rr, _ = P.deflated_cg_solve(R, b, x0, P.refresh_basis(R, w), cfg)
+        basis = P.refresh_basis(A, w)   # one basis for both (its A W comes from the packed block product)
+        xs, rs, _ = P.deflated_cg_solve(A, b, x0, basis, cfg)
+        xr, rr, _ = P.deflated_cg_solve(R, b, x0, basis, cfg)
     else:
         xs, rs, _ = P.cg_solve(A, b, None, cfg)
         xr, rr, _ = P.cg_solve(R, b, None, cfg)
     assert rs.iterations == rr.iterations
     assert np.array_equal(xs, xr)
     assert np.array_equal(rs.residual_history, rr.residual_history)
+
+
+@pytest.mark.parametrize("n,k", [(1, 1), (63, 3), (64, 16), (65, 7), (257, 16), (1000, 12), (2049, 16), (4500, 16),
+                                 (3000, 24)])
+def test_symmetric_block_product(P, n, k):
+    """A W over the packed tiles (symblock.cu: each tile feeds K_IJ W_J and
+    K_IJ' W_I on the FP64 tensor pipe; k <= 16) against the row-major DMMA
+    product and an fp64 host product; k = 24 takes the row-major path."""
+    rng = np.random.default_rng(300 + n + k)
+    a = O.rbf_kernel(rng.standard_normal((n, 5)), 1.0, 1.2)
+    op = P.DenseOperator.from_matrix(a).with_strategy("sym")
+    w = rng.standard_normal((n, k))
+    s = rng.uniform(0.2, 0.6, n)
+    for shift, sv in ((0.0, None), (1.0, s)):
+        A = op.scaled(sv, shift)
+        y_sym = A @ w
+        y_rows = A.with_strategy("rows") @ w
+        ref = (a * np.outer(s, s) + np.eye(n)) @ w if sv is not None else a @ w
+        scale = np.abs(a) @ np.abs(w) + 1.0
+        assert np.all(np.abs(y_sym - ref) <= 64 * np.finfo(float).eps * scale)
+        assert np.all(np.abs(y_sym - y_rows) <= 64 * np.finfo(float).eps * scale)
+        assert np.array_equal(y_sym, A @ w)   # deterministic (units are drawn dynamically)
