@@ -7,8 +7,8 @@
 // Work unit: a super-tile of 4 x 4 tiles (tile blocks I in [4A, 4A + 4), J in
 // [4B, 4B + 4), J <= I), handed out by an atomic counter (off-diagonal
 // super-tiles first, then the diagonal ones).  For each tile (I, J) of a unit
-//   row part     RP_I += K_IJ V_J          (warps 0-3, 16 rows each)
-//   column part  CP_J += K_IJ' V_I, I != J (warps 4-7)
+//   row part     RP_I += K_IJ V_J          (warps 0-7, 8 rows each)
+//   column part  CP_J += K_IJ' V_I, I != J (warps 8-15)
 // on the FP64 tensor pipe (mma.sync m8n8k4), operands from shared memory: the
 // tile and the two 64-row V blocks arrive together in one ring stage by three
 // bulk copies (TMA engine).  Every unit writes its own RP / CP slots, so the
@@ -34,7 +34,10 @@
 #define SB_VBLK (32 * SB_VP)                     // doubles per 64-row V block
 #define SB_STAGE (DCG_SYM_TILE_DOUBLES + 2 * SB_VBLK)
 #define SB_STAGES 4
-#define SB_NCW 8                                 // consumer warps
+#ifndef SB_MT
+#define SB_MT 1                                  // m8 fragments per consumer warp (1 or 2; 1 measured 1-2% faster)
+#endif
+#define SB_NCW (16 / SB_MT)                      // consumer warps: half row part, half column part
 #define SB_NT (32 * (SB_NCW + 1))                // + one producer warp
 #define SB_SLOT (DCG_TB * SB_KP)                 // doubles per RP / CP slot (64 rows x SB_KP)
 #ifndef SB_UNROLL
@@ -198,19 +201,20 @@ __global__ void __launch_bounds__(SB_NT, 1)
     }
 
     // ---- consumers: warps 0-3 the row part, 4-7 the column part ----------------
-    const bool rowpart = warp < 4;
-    const int wb = 16 * (warp & 3);   // 16-row block of the output rows
-    double acc[SB_R][2][2][2];        // [block][mt][nt][2]  (row part uses block 0 only)
+    const bool rowpart = warp < SB_NCW / 2;
+    const int wl = warp % (SB_NCW / 2);
+    double acc[SB_R][SB_MT][2][2];    // [block][mt][nt][2]  (row part uses block 0 only)
 #pragma unroll
     for (int b = 0; b < SB_R; ++b)
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int mt = 0; mt < SB_MT; ++mt)
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) acc[b][mt][nt][0] = acc[b][mt][nt][1] = 0.0;
     // per-lane fragment offsets
-    int rowm[2];
+    // output rows of the warp's m8 fragments (16-row blocks split over 2 / SB_MT warps)
+    int rowm[SB_MT];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) rowm[mt] = wb + sb_row(mt, g);
+    for (int mt = 0; mt < SB_MT; ++mt) rowm[mt] = 16 * (wl / (2 / SB_MT)) + sb_row((wl % (2 / SB_MT)) * SB_MT + mt, g);
 
     unsigned int q = 0;
     for (;;) {
@@ -224,15 +228,15 @@ __global__ void __launch_bounds__(SB_NT, 1)
         if (rowpart) {
             if (m.flags & 16) {
 #pragma unroll
-                for (int mt = 0; mt < 2; ++mt)
+                for (int mt = 0; mt < SB_MT; ++mt)
 #pragma unroll
                     for (int nt = 0; nt < 2; ++nt) acc[0][mt][nt][0] = acc[0][mt][nt][1] = 0.0;
             }
 #pragma unroll kSbUnroll
             for (int s2 = 0; s2 < DCG_TB / 8; ++s2) {
-                double2 a[2], b[2];
+                double2 a[SB_MT], b[2];
 #pragma unroll
-                for (int mt = 0; mt < 2; ++mt) {
+                for (int mt = 0; mt < SB_MT; ++mt) {
                     const int r = rowm[mt];
                     a[mt] = *reinterpret_cast<const double2*>(tile + r * DCG_TB + 2 * ((4 * s2 + t) ^ ((r >> 1) & 31)));
                 }
@@ -240,7 +244,7 @@ __global__ void __launch_bounds__(SB_NT, 1)
                 for (int nt = 0; nt < 2; ++nt)
                     b[nt] = *reinterpret_cast<const double2*>(vj + (4 * s2 + t) * SB_VP + 2 * (8 * nt + g));
 #pragma unroll
-                for (int mt = 0; mt < 2; ++mt)
+                for (int mt = 0; mt < SB_MT; ++mt)
 #pragma unroll
                     for (int nt = 0; nt < 2; ++nt) {
                         sb_dmma(acc[0][mt][nt][0], acc[0][mt][nt][1], a[mt].x, b[nt].x);
@@ -252,7 +256,7 @@ __global__ void __launch_bounds__(SB_NT, 1)
 #pragma unroll
                 for (int b = 0; b < SB_R; ++b)
 #pragma unroll
-                    for (int mt = 0; mt < 2; ++mt)
+                    for (int mt = 0; mt < SB_MT; ++mt)
 #pragma unroll
                         for (int nt = 0; nt < 2; ++nt) acc[b][mt][nt][0] = acc[b][mt][nt][1] = 0.0;
             }
@@ -263,10 +267,10 @@ __global__ void __launch_bounds__(SB_NT, 1)
 #pragma unroll kSbUnroll
                 for (int s2 = 0; s2 < DCG_TB / 8; ++s2) {
                     const int i0 = 8 * s2 + 2 * t;   // tile rows i0, i0 + 1 (same swizzle key)
-                    double a0[2], a1[2];
+                    double a0[SB_MT], a1[SB_MT];
                     double2 b[2];
 #pragma unroll
-                    for (int mt = 0; mt < 2; ++mt) {
+                    for (int mt = 0; mt < SB_MT; ++mt) {
                         const int c = rowm[mt];
                         const int off = i0 * DCG_TB + 2 * ((c >> 1) ^ ((i0 >> 1) & 31)) + (c & 1);
                         a0[mt] = tile[off];
@@ -276,7 +280,7 @@ __global__ void __launch_bounds__(SB_NT, 1)
                     for (int nt = 0; nt < 2; ++nt)
                         b[nt] = *reinterpret_cast<const double2*>(vi + (4 * s2 + t) * SB_VP + 2 * (8 * nt + g));
 #pragma unroll
-                    for (int mt = 0; mt < 2; ++mt)
+                    for (int mt = 0; mt < SB_MT; ++mt)
 #pragma unroll
                         for (int nt = 0; nt < 2; ++nt) {
                             sb_dmma(acc[lj][mt][nt][0], acc[lj][mt][nt][1], a0[mt], b[nt].x);
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(SB_NT, 1)
 #pragma unroll
             for (int b = 0; b < SB_R; ++b)
 #pragma unroll
-                for (int mt = 0; mt < 2; ++mt)
+                for (int mt = 0; mt < SB_MT; ++mt)
 #pragma unroll
                     for (int nt = 0; nt < 2; ++nt) acc[b][mt][nt][0] = acc[b][mt][nt][1] = 0.0;
         }
@@ -300,7 +304,7 @@ __global__ void __launch_bounds__(SB_NT, 1)
         if (rowpart && (m.flags & 4)) {
             double* out = RP + ((long long)m.unit * SB_R + m.li) * SB_SLOT;
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
+            for (int mt = 0; mt < SB_MT; ++mt)
 #pragma unroll
                 for (int nt = 0; nt < 2; ++nt)
                     *reinterpret_cast<double2*>(out + rowm[mt] * SB_KP + 8 * nt + 2 * t) =
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(SB_NT, 1)
                 if (SB_R * B + lj >= NB) continue;
                 double* out = CP + ((long long)m.unit * SB_R + lj) * SB_SLOT;
 #pragma unroll
-                for (int mt = 0; mt < 2; ++mt)
+                for (int mt = 0; mt < SB_MT; ++mt)
 #pragma unroll
                     for (int nt = 0; nt < 2; ++nt)
                         *reinterpret_cast<double2*>(out + rowm[mt] * SB_KP + 8 * nt + 2 * t) =
