@@ -406,6 +406,22 @@ DCG_API int dcg_shard_rbf_sym_partial(dcg_context* ctx, void* stream, const dcg_
                                       const dcg_shard_state* d_state);
 /* mode 0: d_out = (A v) on the slab rows and d_part = its p'Ap partial;
  * mode 1: d_out = b - (A v) -- from the all-reduced t = K (s (.) v) (full).  */
+/* Stored Gram over a TILE SHARE (replicated vectors, one all-reduce of n
+ * doubles per product): rank r of R holds the packed lower-triangle tiles
+ * [t_lo, t_hi) of dcg_shard_tile_range (an equal-cost split of the tile
+ * sequence), built from the replicated points by dcg_k_rbf_gram_packed
+ * (entries bitwise those of dcg_k_rbf_gram).  dcg_shard_tiles_partial writes
+ * the rank's partial t = K_share (s (.) v) for all n rows (op: DENSE_SYM,
+ * d_kp = the share, d_s the full scale vector); the sum over ranks is
+ * K (s (.) v).  Replaces the slab GEMV + all-gather of p of
+ * solvers.py:169 (matvec) in the sharded loop; no reference counterpart.   */
+DCG_API int dcg_shard_tile_range(long long n, int rank, int world, long long* t_lo, long long* t_hi);
+DCG_API int dcg_k_rbf_gram_packed(dcg_context* ctx, void* stream, const double* d_x, long long n,
+                          long long dim, double signal_var, double inv_two_ell2, double jitter,
+                          long long t_lo, long long t_hi, double* d_kp);
+DCG_API int dcg_shard_tiles_partial(dcg_context* ctx, void* stream, const dcg_operator* op, int rank,
+                            int world, const double* d_v, double* d_t,
+                            const dcg_shard_state* d_state);
 DCG_API int dcg_shard_epilogue(dcg_context* ctx, void* stream, int mode, const dcg_operator* op,
                                const double* d_v, const double* d_b, const double* d_t,
                                double* d_out, double* d_part, const dcg_shard_state* d_state);

@@ -9,6 +9,7 @@
 #include <string.h>
 
 #include "common.cuh"
+#include "symgemv.cuh"
 
 #include <atomic>
 
@@ -261,6 +262,24 @@ extern "C" int dcg_k_rbf_gram(dcg_context* ctx, void* stream, const double* d_x,
     if (!ctx || n < 0 || dim < 0 || ldk < n || row0 < 0 || rows < 0 || row0 + rows > n) return DCG_E_CONFIG;
     return dcg_rbf_launch(as_stream(stream), d_x, n, d_x, n, dim, signal_var, inv_two_ell2, jitter, 1, row0, rows,
                           d_k, ldk);
+}
+
+int dcg_rbf_packed_launch(cudaStream_t, const double*, long long, long long, double, double, double, long long,
+                          long long, double*);
+
+extern "C" int dcg_shard_tile_range(long long n, int rank, int world, long long* t_lo, long long* t_hi) {
+    if (n < 0 || world < 1 || rank < 0 || rank >= world || !t_lo || !t_hi) return DCG_E_CONFIG;
+    *t_lo = n ? sym_tile_begin(n, world, rank) : 0;
+    *t_hi = n ? sym_tile_begin(n, world, rank + 1) : 0;
+    return DCG_OK;
+}
+
+extern "C" int dcg_k_rbf_gram_packed(dcg_context* ctx, void* stream, const double* d_x, long long n, long long dim,
+                                     double signal_var, double inv_two_ell2, double jitter, long long t_lo,
+                                     long long t_hi, double* d_kp) {
+    if (!ctx || n < 0 || dim < 0 || t_lo < 0 || t_hi < t_lo || t_hi > sym_ntiles(n) || !aligned16(d_kp))
+        return DCG_E_CONFIG;
+    return dcg_rbf_packed_launch(as_stream(stream), d_x, n, dim, signal_var, inv_two_ell2, jitter, t_lo, t_hi, d_kp);
 }
 
 extern "C" int dcg_k_rbf_cross(dcg_context* ctx, void* stream, const double* d_xa, long long na, const double* d_xb,

@@ -10,6 +10,7 @@
 // The GPC kernels restate gpc.py:126-209 (sigmoid, logaddexp, curvature,
 // Newton right-hand side and update, psi) with deterministic reductions.
 #include "common.cuh"
+#include "symgemv.cuh"
 
 #define RBF_T 64     // tile edge (rows and columns per CTA)
 #define RBF_D 32     // dimensions staged per round
@@ -89,6 +90,69 @@ __global__ void __launch_bounds__(256)
             if (orow < nc && ocol < rows) out[orow * ldo + ocol] = tt[tx + 32 * h][ty + 8 * rr];
         }
     }
+}
+
+// The tiles [t_lo, t_hi) of the packed lower-triangle copy (symgemv.cuh:
+// tile-row order, 32 KB per tile, XOR swizzle, zero beyond n) evaluated
+// directly from X with rbf_tile_kernel's operation sequence, so every entry
+// is bitwise the stored Gram's: a rank's share of a tile-sharded Gram is built
+// without the row-major matrix.
+__global__ void __launch_bounds__(256)
+    rbf_packed_kernel(const double* __restrict__ x, long long n, long long dim, double var, double inv2l2,
+                      double jitter, long long t_lo, double* __restrict__ out) {
+    __shared__ double sbuf[2 * RBF_T * (RBF_D + 1)];
+    double (*sr)[RBF_D + 1] = reinterpret_cast<double (*)[RBF_D + 1]>(sbuf);
+    double (*sc)[RBF_D + 1] = reinterpret_cast<double (*)[RBF_D + 1]>(sbuf + RBF_T * (RBF_D + 1));
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const long long t = t_lo + blockIdx.x;
+    const long long I = sym_tile_row(t), J = t - sym_tile_row_base(I);
+    const long long i0 = I * RBF_T, j0 = J * RBF_T;
+    double acc[8][2];
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) acc[rr][0] = acc[rr][1] = 0.0;
+    for (long long t0 = 0; t0 < dim; t0 += RBF_D) {
+        const int tn = (int)min((long long)RBF_D, dim - t0);
+        for (int e = threadIdx.x; e < RBF_T * RBF_D; e += 256) {
+            const int r = e / RBF_D, c = e % RBF_D;
+            sr[r][c] = (c < tn && i0 + r < n) ? x[(i0 + r) * dim + t0 + c] : 0.0;
+            sc[r][c] = (c < tn && j0 + r < n) ? x[(j0 + r) * dim + t0 + c] : 0.0;
+        }
+        cta_sync();
+        for (int c = 0; c < tn; ++c) {
+            const double c0 = sc[tx][c], c1 = sc[tx + 32][c];
+#pragma unroll
+            for (int rr = 0; rr < 8; ++rr) {
+                const double rv = sr[ty + 8 * rr][c];
+                const double d0 = sub_rn(rv, c0), d1 = sub_rn(rv, c1);
+                acc[rr][0] = add_rn(acc[rr][0], mul_rn(d0, d0));
+                acc[rr][1] = add_rn(acc[rr][1], mul_rn(d1, d1));
+            }
+        }
+        cta_sync();
+    }
+    double* dst = out + (t - t_lo) * (RBF_T * RBF_T);
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) {
+        const int r = ty + 8 * rr;
+        const long long gi = i0 + r;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int c = tx + 32 * h;
+            const long long j = j0 + c;
+            double val = 0.0;
+            if (gi < n && j < n) val = gi == j ? add_rn(var, jitter) : mul_rn(var, exp(mul_rn(-acc[rr][h], inv2l2)));
+            dst[sym_swz(r, c)] = val;
+        }
+    }
+}
+
+int dcg_rbf_packed_launch(cudaStream_t st, const double* x, long long n, long long dim, double var, double inv2l2,
+                          double jitter, long long t_lo, long long t_hi, double* out) {
+    if (t_hi <= t_lo) return DCG_OK;
+    if (t_hi - t_lo > 0x7fffffffLL) return DCG_E_UNSUPPORTED;
+    rbf_packed_kernel<<<(unsigned)(t_hi - t_lo), 256, 0, st>>>(x, n, dim, var, inv2l2, jitter, t_lo, out);
+    DCG_LAUNCHED();
+    return DCG_OK;
 }
 
 int dcg_rbf_launch(cudaStream_t st, const double* xr, long long nr_total, const double* xc, long long nc,

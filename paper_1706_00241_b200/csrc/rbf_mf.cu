@@ -200,10 +200,22 @@ __global__ void sym_pass2_share_kernel(long long n, long long t_lo, long long t_
             if (sym_tile_row_base(c) < need) ++c;
             if (c > Ip) Ip = c;
         }
-        for (; Ip < NT; ++Ip) {
-            const long long id = sym_tile_row_base(Ip) + I;
-            if (id >= t_hi) break;
-            acc += ld_cg(colpart + (id - t_lo) * RM_TB + rl);
+        // tiles (Ip, I) while inside the share, sixteen loads in flight ahead
+        // of their (in-order) adds
+        long long id = sym_tile_row_base(Ip) + I;
+        while (Ip < NT && id < t_hi) {
+            double v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                v[u] = 0.0;
+                if (Ip + u < NT && id < t_hi) {
+                    v[u] = ld_cg(colpart + (id - t_lo) * RM_TB + rl);
+                    id += Ip + u + 1;   // base(Ip + u + 1) - base(Ip + u)
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) acc += v[u];
+            Ip += 16;
         }
         // row segments of tile row I
         const long long base = sym_tile_row_base(I);
@@ -217,7 +229,65 @@ __global__ void sym_pass2_share_kernel(long long n, long long t_lo, long long t_
     }
 }
 
+// Stored tile share: pass 1 of the packed-tile GEMV over the rank's tiles
+// [t_lo, t_hi) (kp_share holds exactly those, tile t at t - t_lo), split over
+// the CTAs with the same equal-cost rule, the range table exported (block 0)
+// for the share's pass 2.  colpart / rowpart are indexed relative to t_lo.
+__global__ void __launch_bounds__(DCG_NT, 1)
+    stored_pass1_share_kernel(const double* kp_share, long long n, long long t_lo, long long t_hi, const double* v,
+                              const double* s_in, double* colpart, double* rowpart, long long* tbl_out,
+                              const dcg_shard_state* gate) {
+    if (gate && gate->done) return;
+    extern __shared__ __align__(16) double smem[];
+    sym_ring_init(smem, n, true);
+    long long* tbl = sym_range_table(smem);
+    const int G = gridDim.x;
+    for (int b = threadIdx.x; b <= G; b += blockDim.x) tbl[b] = sym_tile_begin_range(n, t_lo, t_hi, G, b);
+    cta_sync();
+    if (blockIdx.x == 0)
+        for (int b = threadIdx.x; b <= G; b += blockDim.x) tbl_out[b] = tbl[b];
+    unsigned int seq = 0;
+    sym_pass1<true, 1, true>(kp_share - t_lo * DCG_SYM_TILE_DOUBLES, 0, n, v, s_in, colpart - t_lo * DCG_TB,
+                             rowpart - t_lo * DCG_TB, smem, seq);
+}
+
 }  // namespace
+
+// Sharded stored K (s (.) v) over a tile share: op->kind DCG_OP_DENSE_SYM,
+// op->d_kp = this rank's packed tiles [t_lo, t_hi) (dcg_shard_tile_range:
+// the same equal-cost split as the matrix-free share), op->d_s the full
+// scale vector.  Writes the rank's partial t (all n rows) to d_t; the sum over
+// ranks (one all-reduce of n doubles) is K (s (.) v).
+extern "C" int dcg_shard_tiles_partial(dcg_context* ctx, void* stream, const dcg_operator* op, int rank, int world,
+                                       const double* d_v, double* d_t, const dcg_shard_state* d_state) {
+    if (!ctx || !op || !d_v || !d_t || world < 1 || rank < 0 || rank >= world) return DCG_E_CONFIG;
+    if (op->kind != DCG_OP_DENSE_SYM || !op->d_kp || !aligned16(op->d_kp) || !aligned16(d_v) ||
+        !aligned16(op->d_s))
+        return DCG_E_CONFIG;
+    const long long n = op->n;
+    if (n == 0) return DCG_OK;
+    cudaStream_t st = as_stream(stream);
+    const long long t_lo = sym_tile_begin(n, world, rank), t_hi = sym_tile_begin(n, world, rank + 1);
+    const long long nloc = t_hi - t_lo;
+    const int G = ctx->sm_count < DCG_SYM_MAX_CTAS ? ctx->sm_count : DCG_SYM_MAX_CTAS;
+    const size_t need = sizeof(double) * 2 * (size_t)(nloc > 0 ? nloc : 1) * DCG_TB +
+                        sizeof(long long) * (DCG_SYM_MAX_CTAS + 2) + 1024;
+    int rc = dcg_ws2_reserve(ctx, need);
+    if (rc) return rc;
+    double* colpart = static_cast<double*>(ctx->ws2);
+    double* rowpart = colpart + (nloc > 0 ? nloc : 1) * DCG_TB;
+    long long* tbl = reinterpret_cast<long long*>(rowpart + (nloc > 0 ? nloc : 1) * DCG_TB);
+    if (nloc > 0) {
+        const size_t smem = sizeof(double) * (size_t)sym_smem_doubles();
+        DCG_SMEM_ATTR(stored_pass1_share_kernel, smem);
+        stored_pass1_share_kernel<<<G, DCG_NT, smem, st>>>(op->d_kp, n, t_lo, t_hi, d_v, op->d_s, colpart, rowpart,
+                                                            tbl, d_state);
+        DCG_LAUNCHED();
+    }
+    sym_pass2_share_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(n, t_lo, t_hi, tbl, G, colpart, rowpart, d_t, d_state);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}
 
 // Sharded matrix-free K (s (.) v), symmetric form: rank `rank` of `world`
 // evaluates an equal-cost share of the lower-triangle tiles (each pair once,

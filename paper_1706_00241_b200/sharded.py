@@ -37,6 +37,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import time
 from dataclasses import dataclass, field, replace
 
@@ -118,17 +119,56 @@ class TorchComm:
 # ---------------------------------------------------------------------------
 
 
+@dataclass
+class TileShare:
+    """This rank's share of K's packed lower-triangle tiles, [t_lo, t_hi) of
+    dcg_shard_tile_range (an equal-cost split of the tile sequence), one
+    contiguous device buffer of 32 KB tiles."""
+
+    kp: torch.Tensor
+    t_lo: int
+    t_hi: int
+    rank: int
+    world: int
+
+
+def tile_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    lo, hi = ctypes.c_longlong(0), ctypes.c_longlong(0)
+    N.check(N.lib().dcg_shard_tile_range(n, rank, world, ctypes.byref(lo), ctypes.byref(hi)), what="tile_range")
+    return int(lo.value), int(hi.value)
+
+
 class ShardedOperator:
     """This rank's slab of A = shift I + S K S: rows [row0, row0 + rows) of K
-    (device, leading dimension ldk), the full scale vector s (n) or None."""
+    (device, leading dimension ldk), the full scale vector s (n) or None.
 
-    def __init__(self, kslab: torch.Tensor, n: int, ldk: int, row0: int, rows: int, s=None, shift: float = 0.0):
+    With a ``share`` (TileShare) the solve's products read the rank's packed
+    tile share instead (half the slab's bytes) and the solve runs on
+    replicated vectors with one all-reduce of n doubles per product; the slab
+    still serves the once-per-system products (refresh, Newton glue)."""
+
+    def __init__(self, kslab: torch.Tensor, n: int, ldk: int, row0: int, rows: int, s=None, shift: float = 0.0,
+                 share: TileShare | None = None):
         self.kslab, self.n, self.ldk, self.row0, self.rows = kslab, int(n), int(ldk), int(row0), int(rows)
         self.s = s
         self.shift = float(shift)
+        self.share = share
 
     def scaled(self, s, shift: float) -> "ShardedOperator":
-        return ShardedOperator(self.kslab, self.n, self.ldk, self.row0, self.rows, s, shift)
+        return ShardedOperator(self.kslab, self.n, self.ldk, self.row0, self.rows, s, shift, self.share)
+
+    def share_struct(self) -> N.COperator:
+        """The tile share as a DENSE_SYM operator over all n rows."""
+        c = N.COperator()
+        c.kind = N.DCG_OP_DENSE_SYM
+        c.n = self.n
+        c.row0 = 0
+        c.rows = self.n
+        c.d_kp = self.share.kp.data_ptr() if self.share.kp.numel() else None
+        c.ldk = self.n + (self.n & 1)
+        c.d_s = self.s.data_ptr() if self.s is not None else None
+        c.shift = self.shift
+        return c
 
     def c_struct(self) -> N.COperator:
         c = N.COperator()
@@ -183,11 +223,13 @@ class ShardedRbfOperator:
         return c
 
 
-def sharded_rbf_kernel(x, params, jitter=None, comm=None, matrix_free=False):
+def sharded_rbf_kernel(x, params, jitter=None, comm=None, matrix_free=False, tile_share=True):
     """This rank's rows of the RBF Gram (gpc.py:82-98), built on device from
     the replicated data X (n x d, a few MB) - Gram blocks never cross PCIe.
     With ``matrix_free`` the slab is never stored: a ShardedRbfOperator
-    regenerates it on every product (config 5)."""
+    regenerates it on every product (config 5).  With ``tile_share`` the rank
+    also builds its share of the packed lower-triangle tiles (entries bitwise
+    the slab's), which the solves stream instead of the slab."""
     comm = comm or SelfComm()
     xd = D.to_dev(x, 2)
     n, dim = xd.shape
@@ -205,7 +247,16 @@ def sharded_rbf_kernel(x, params, jitter=None, comm=None, matrix_free=False):
         N.check(N.lib().dcg_k_rbf_gram(D.ctx(), D.stream(), xd.data_ptr(), n, dim, var,
                                        1.0 / (2.0 * params.lengthscale**2), jitter, kslab.data_ptr(), ld, r0, rows),
                 what="rbf_gram")
-    return ShardedOperator(kslab, n, ld, r0, rows)
+    share = None
+    if tile_share and n:
+        t_lo, t_hi = tile_range(n, comm.world, comm.rank)
+        kp = D.empty(max(t_hi - t_lo, 0) * 4096)
+        if t_hi > t_lo:
+            N.check(N.lib().dcg_k_rbf_gram_packed(D.ctx(), D.stream(), xd.data_ptr(), n, dim, var,
+                                                  1.0 / (2.0 * params.lengthscale**2), jitter, t_lo, t_hi,
+                                                  kp.data_ptr()), what="rbf_gram_packed")
+        share = TileShare(kp, t_lo, t_hi, comm.rank, comm.world)
+    return ShardedOperator(kslab, n, ld, r0, rows, share=share)
 
 
 # ---------------------------------------------------------------------------
@@ -260,8 +311,14 @@ class DeviceShardBackend:
         N.check(N.lib().dcg_shard_rbf_sym_partial(self.ctx(), self.stream(), ctypes.byref(cop), op.rank, op.world,
                                                   _p(vfull), _p(t), _p(state)), what="shard_rbf_sym_partial")
 
+    def tiles_partial(self, op, vfull, t, state=None):
+        cop = op.share_struct()
+        N.check(N.lib().dcg_shard_tiles_partial(self.ctx(), self.stream(), ctypes.byref(cop), op.share.rank,
+                                                op.share.world, _p(vfull), _p(t), _p(state)),
+                what="shard_tiles_partial")
+
     def epilogue(self, mode, op, vfull, b, t, out, part, state=None):
-        cop = op.c_struct()
+        cop = op.share_struct() if getattr(op, "share", None) is not None else op.c_struct()
         N.check(N.lib().dcg_shard_epilogue(self.ctx(), self.stream(), mode, ctypes.byref(cop), _p(vfull), _p(b), _p(t),
                                            _p(out), _p(part), _p(state)), what="shard_epilogue")
 
@@ -306,6 +363,7 @@ class ShardLog:
     beta: torch.Tensor
     mu: torch.Tensor | None
     m: int = 0
+    replicated: bool = False   # rows = n on every rank (tile-share solves)
 
 
 @dataclass
@@ -328,16 +386,31 @@ def _alloc_log(be, rows, ell, k):
 
 
 def sharded_solve(op: ShardedOperator, b_loc, x_prev_loc, basis: ShardBasis | None, cfg: SolverConfig | None = None,
-                  comm=None, backend=None, poll: int = 4):
+                  comm=None, backend=None, poll: int | None = None):
     """CG (basis None or k = 0, solvers.py:207-219) or deflated CG with the
     warm-start correction (solvers.py:222-239) on this rank's rows.  Returns
     (x_loc, SolveReport, ShardLog); every rank gets the same report."""
     cfg = cfg or SolverConfig()
     comm = comm or SelfComm()
     be = backend or DeviceShardBackend()
+    if poll is None:
+        poll = int(os.environ.get("DCG_SHARD_POLL", "4"))
     t0 = time.perf_counter()
     n, rows, r0 = op.n, op.rows, op.row0
     k = basis.k if basis is not None else 0
+    # Tile-share operators: every rank holds the whole vectors and runs the
+    # vector phases redundantly (identically: the reductions see the same
+    # all-reduced data in the same order); the only exchange is the
+    # all-reduce of each product's partial K (s (.) v).
+    share = getattr(op, "share", None)
+    pcomm = comm
+    if share is not None:
+        slab_rows, slab_r0 = rows, r0
+        if comm.world > 1:
+            b_loc = _allgather_vec(comm, be, b_loc[:rows], n).contiguous()
+            x_prev_loc = _allgather_vec(comm, be, x_prev_loc[:rows], n).contiguous()
+        comm = SelfComm()
+        rows, r0 = n, 0
     mb = row_block(n, comm.world)
     ell = int(cfg.ell)
     max_iters = 10 * n if cfg.max_iters is None else int(cfg.max_iters)
@@ -357,23 +430,29 @@ def sharded_solve(op: ShardedOperator, b_loc, x_prev_loc, basis: ShardBasis | No
     hist = be.zeros(max_iters + 1)
     log = _alloc_log(be, rows, ell, k)
 
-    # products: the row slab, or (symmetric matrix-free operators) this rank's
-    # share of the lower-triangle tiles + an all-reduce of K (s (.) v)
-    sym = getattr(op, "symmetric", False)
-    tfull = be.empty(comm.world * mb) if sym else None
+    # products: the row slab, or this rank's share of the lower-triangle tiles
+    # (stored: the tile share; matrix-free: regenerated) + an all-reduce of
+    # K (s (.) v)
+    sym = getattr(op, "symmetric", False) or share is not None
+    tfull = be.empty(max(n, comm.world * mb)) if sym else None
+
+    def partial(st):
+        if share is not None:
+            be.tiles_partial(op, full, tfull, st)
+        else:
+            be.sym_partial(op, full, tfull, st)
+        pcomm.allreduce(tfull[:n] if share is not None else tfull)
 
     def residual(bvec, out, st=None):
         if sym:
-            be.sym_partial(op, full, tfull, st)
-            comm.allreduce(tfull)
+            partial(st)
             be.epilogue(1, op, full, bvec, tfull, out, None, st)
         else:
             be.residual(op, full, bvec, out, st)
 
     def apply_dot(out, part, st):
         if sym:
-            be.sym_partial(op, full, tfull, st)
-            comm.allreduce(tfull)
+            partial(st)
             be.epilogue(0, op, full, None, tfull, out, part, st)
         else:
             be.apply_dot(op, full, out, part, st)
@@ -421,6 +500,9 @@ def sharded_solve(op: ShardedOperator, b_loc, x_prev_loc, basis: ShardBasis | No
     history = hist[: its + 1].cpu().tolist()
     conv = st["rel"] <= cfg.tol
     rep = SolveReport(its, history, conv, time.perf_counter() - t0, TERM_CONVERGED if conv else TERM_MAX_ITERS)
+    if share is not None:
+        log.replicated = True   # all n rows on every rank
+        return x[slab_r0:slab_r0 + slab_rows], rep, log
     return x[:rows], rep, log
 
 
@@ -499,7 +581,7 @@ def sharded_extract(log: ShardLog, prev: ShardBasis | None, k: int, selection: s
 
     comm = comm or SelfComm()
     be = backend or DeviceShardBackend()
-    flog = _gather_log(comm, be, log, n, rows)
+    flog = _gather_log(SelfComm(), be, log, n, n) if log.replicated else _gather_log(comm, be, log, n, rows)
     pb = None
     if prev is not None and prev.k:
         pb = RecycleBasis.__new__(RecycleBasis)
@@ -553,6 +635,15 @@ def sharded_solve_next(state: ShardSequenceState, op: ShardedOperator, b_loc, co
 # ---------------------------------------------------------------------------
 
 
+def _share_kv(op: ShardedOperator, v: torch.Tensor, comm, be) -> torch.Tensor:
+    """K v (all n rows, on every rank) from the tile shares: each rank's
+    partial, then one all-reduce."""
+    t = be.empty(op.n)
+    be.tiles_partial(op.scaled(None, 0.0), v.contiguous(), t)
+    comm.allreduce(t)
+    return t
+
+
 def _allgather_vec(comm, be, local: torch.Tensor, n: int) -> torch.Tensor:
     mb = row_block(n, comm.world)
     full = be.empty(comm.world * mb)
@@ -589,24 +680,39 @@ def sharded_laplace_newton(x, y, params=None, cfg: SolverConfig | None = None, n
     psi_prev = float(ll.value)
     state = ShardSequenceState(k=k, cfg=cfg, selection=selection)
     records = []
+    share = getattr(op, "share", None)
+    r0 = op.row0
     for it in range(1, max_newton + 1):
         s, inner, b_loc = be.empty(n), be.empty(n), be.empty(max(rows, 1))
-        N.check(N.lib().dcg_gpc_newton_system(be.ctx(), be.stream(), ctypes.byref(kop), f.data_ptr(), grad.data_ptr(),
-                                              h.data_ptr(), s.data_ptr(), inner.data_ptr(), b_loc.data_ptr()),
-                what="newton_system")
+        if share is not None:
+            # gpc.py:175-183 with the product from the tile shares: s = sqrt(h),
+            # inner = h f + grad, b = s (.) (K inner), element-wise as the
+            # reference rounds them (one rounding per operation)
+            torch.sqrt(h, out=s)
+            torch.add(torch.mul(h, f), grad, out=inner)
+            b_loc[:rows] = torch.mul(s, _share_kv(op, inner, comm, be))[r0:r0 + rows]
+        else:
+            N.check(N.lib().dcg_gpc_newton_system(be.ctx(), be.stream(), ctypes.byref(kop), f.data_ptr(),
+                                                  grad.data_ptr(), h.data_ptr(), s.data_ptr(), inner.data_ptr(),
+                                                  b_loc.data_ptr()), what="newton_system")
         t0 = time.perf_counter()
         x_loc, state = sharded_solve_next(state, op.scaled(s, 1.0), b_loc[:rows], comm, be)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         rep = state.history[-1]
         x_full = _allgather_vec(comm, be, x_loc, n).contiguous()
-        f_loc = be.empty(max(rows, 1))
-        a = be.empty(n)
-        N.check(N.lib().dcg_gpc_newton_update(be.ctx(), be.stream(), ctypes.byref(kop), inner.data_ptr(),
-                                              s.data_ptr(), x_full.data_ptr(), yd.data_ptr(), a.data_ptr(),
-                                              f_loc.data_ptr(), grad.data_ptr(), h.data_ptr(), None, None),
-                what="newton_update")
-        f = _allgather_vec(comm, be, f_loc[:rows], n).contiguous()
+        if share is not None:
+            # gpc.py:186-191: a = inner - s (.) x, f = K a (tile shares)
+            a = torch.sub(inner, torch.mul(s, x_full))
+            f = _share_kv(op, a, comm, be)
+        else:
+            f_loc = be.empty(max(rows, 1))
+            a = be.empty(n)
+            N.check(N.lib().dcg_gpc_newton_update(be.ctx(), be.stream(), ctypes.byref(kop), inner.data_ptr(),
+                                                  s.data_ptr(), x_full.data_ptr(), yd.data_ptr(), a.data_ptr(),
+                                                  f_loc.data_ptr(), grad.data_ptr(), h.data_ptr(), None, None),
+                    what="newton_update")
+            f = _allgather_vec(comm, be, f_loc[:rows], n).contiguous()
         ll, psi = ctypes.c_double(0.0), ctypes.c_double(0.0)
         N.check(N.lib().dcg_gpc_objective(be.ctx(), be.stream(), n, f.data_ptr(), yd.data_ptr(), a.data_ptr(),
                                           grad.data_ptr(), h.data_ptr(), ctypes.byref(ll), ctypes.byref(psi)),

@@ -243,3 +243,41 @@ def _epilogue(self, mode, op, vfull, b, t, out, part, state=None):
 
 CpuShardBackend.sym_partial = _sym_partial
 CpuShardBackend.epilogue = _epilogue
+
+
+class CpuTileShareOperator:
+    """A dense symmetric K standing in for a stored tile share: this rank's
+    slab rows (row0, rows) and share (rank, world) of the packed tiles; the
+    solve runs on replicated vectors (sharded.sharded_solve's share path)."""
+
+    def __init__(self, kfull, row0, rows, rank, world, s=None, shift=0.0):
+        self.kfull, self.n = kfull, int(kfull.shape[0])
+        self.row0, self.rows, self.rank, self.world = int(row0), int(rows), int(rank), int(world)
+        self.share = (rank, world)
+        self.s, self.shift = s, float(shift)
+
+    def scaled(self, s, shift):
+        return CpuTileShareOperator(self.kfull, self.row0, self.rows, self.rank, self.world, s, shift)
+
+
+def _tiles_partial(self, op, vfull, t, state=None):
+    _sym_partial(self, op, vfull, t, state)
+
+
+def _epilogue_any(self, mode, op, vfull, b, t, out, part, state=None):
+    if getattr(op, "share", None) is None:
+        return _epilogue(self, mode, op, vfull, b, t, out, part, state)
+    if self._done(state):
+        return
+    n = op.n
+    tr = t[:n] if op.s is None else op.s[:n] * t[:n]
+    ax = op.shift * vfull[:n] + tr
+    if mode == 0:
+        out[:n] = ax
+        part[0] = torch.dot(vfull[:n], ax)
+    else:
+        out[:n] = b[:n] - ax
+
+
+CpuShardBackend.tiles_partial = _tiles_partial
+CpuShardBackend.epilogue = _epilogue_any

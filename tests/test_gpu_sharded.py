@@ -301,3 +301,140 @@ def test_symmetric_matrix_free_virtual_ranks(P, rng, world, k):
     assert all(r.iterations == reps[0].iterations for r in reps)
     assert abs(reps[0].iterations - rep_ref.iterations) <= 1, (reps[0].iterations, rep_ref.iterations)
     assert np.linalg.norm(xs - x_ref) <= 1e-9 * np.linalg.norm(x_ref)
+
+
+# ---------------------------------------------------------------------------
+# stored tile shares (replicated vectors, one all-reduce per product)
+# ---------------------------------------------------------------------------
+
+
+def share_op(a, world, rank, P):
+    """The rank's row slab plus its share of the packed tiles of a dense matrix."""
+    import ctypes
+
+    from paper_1706_00241_b200 import _device as D
+    from paper_1706_00241_b200 import _native as N
+    from paper_1706_00241_b200.sharded import TileShare, tile_range
+
+    op = slab_op(a, world, rank, P)
+    n = a.shape[0]
+    kfull, ld = D.to_dev_padded(np.ascontiguousarray(a))
+    kp = D.empty(int(N.lib().dcg_packed_sym_doubles(n)))
+    N.check(N.lib().dcg_pack_sym(D.ctx(), D.stream(), kfull.data_ptr(), ld, n, kp.data_ptr()))
+    t_lo, t_hi = tile_range(n, world, rank)
+    op.share = TileShare(kp[t_lo * 4096:t_hi * 4096].clone(), t_lo, t_hi, rank, world)
+    del ctypes
+    return op
+
+
+@pytest.mark.parametrize("k,every", [(0, 0), (5, 0), (5, 7)])
+def test_tile_share_world1_matches_single_gpu_solver(P, rng, k, every):
+    from paper_1706_00241_b200.sharded import SelfComm, ShardBasis, sharded_solve
+
+    n = 300
+    a = random_spd(rng, n, kappa=100.0)
+    b = rng.standard_normal(n)
+    xprev = 0.1 * rng.standard_normal(n)
+    cfg = P.SolverConfig(tol=1e-10, ell=10, recompute_residual_every=every)
+    basis = P.refresh_basis(a, rng.standard_normal((n, k))) if k else None
+    if k:
+        x_ref, rep_ref, _ = P.deflated_cg_solve(a, b, xprev, basis, cfg)
+        sb = ShardBasis(basis.w_dev, basis.aw_dev, basis.chol_dev)
+    else:
+        x_ref, rep_ref, _ = P.cg_solve(a, b, xprev, cfg)
+        sb = None
+    x, rep, log = sharded_solve(share_op(a, 1, 0, P), dev(b), dev(xprev), sb, cfg, SelfComm())
+    assert log.replicated
+    assert abs(rep.iterations - rep_ref.iterations) <= 1
+    assert np.linalg.norm(x.cpu().numpy() - x_ref) <= 1e-8 * np.linalg.norm(x_ref)
+
+
+@pytest.mark.parametrize("world,k,every", [(2, 0, 0), (2, 4, 0), (3, 4, 6)])
+def test_tile_share_virtual_ranks_match_reference(P, rng, world, k, every):
+    from paper_1706_00241_b200.sharded import DeviceShardBackend, ShardBasis, sharded_solve
+
+    n = 1000   # 16 tile rows: several ranks' shares cut tile rows mid-way
+    a = O.rbf_kernel(rng.standard_normal((n, 4)), 1.0, 0.9) + 0.5 * np.eye(n)
+    b = rng.standard_normal(n)
+    xprev = 0.1 * rng.standard_normal(n)
+    w = rng.standard_normal((n, k))
+    cfg = P.SolverConfig(tol=1e-10, ell=8, recompute_residual_every=every)
+    ocfg = O.Cfg(tol=1e-10, ell=8, recompute_residual_every=every)
+    if k:
+        ob = O.refresh_basis(a, w, be="numpy")
+        x_ref, rep_ref, _ = O.deflated_cg_solve(a, b, xprev, ob, ocfg, be="numpy")
+        aw = a @ w
+        g = w.T @ aw
+        sb = ShardBasis(dev(w), dev(aw), dev(np.linalg.cholesky(0.5 * (g + g.T))))
+    else:
+        x_ref, rep_ref, _ = O.cg_solve(a, b, xprev, ocfg, be="numpy")
+        sb = None
+
+    def rank_fn(rank, comm):
+        op = share_op(a, world, rank, P)
+        r0, rows = op.row0, op.rows
+        x, rep, _ = sharded_solve(op, dev(b[r0:r0 + rows]), dev(xprev[r0:r0 + rows]), sb, cfg, comm,
+                                  DeviceShardBackend(slot=2 + rank), poll=3)
+        torch.cuda.synchronize()
+        return r0, x.cpu().numpy(), rep
+
+    outs = run_ranks(world, rank_fn)
+    x = np.zeros(n)
+    for r0, xl, _ in outs:
+        x[r0:r0 + xl.shape[0]] = xl
+    reps = [o[2] for o in outs]
+    assert all(r.iterations == reps[0].iterations for r in reps)
+    assert all(r.residual_history == reps[0].residual_history for r in reps)
+    assert abs(reps[0].iterations - rep_ref.iterations) <= 1
+    assert np.linalg.norm(x - x_ref) <= 1e-8 * np.linalg.norm(x_ref)
+
+
+@pytest.mark.parametrize("n,world", [(1000, 3), (777, 2)])
+def test_packed_share_built_from_points_is_the_gram(P, rng, n, world):
+    """dcg_k_rbf_gram_packed (a rank's tiles straight from X) is bitwise the
+    packed copy of the stored Gram."""
+    from paper_1706_00241_b200.sharded import sharded_rbf_kernel, tile_range
+
+    x = rng.standard_normal((n, 6))
+    params = P.KernelParams(1.3, 1.1)
+    gram = P.rbf_kernel(dev(x), params).with_strategy("sym")
+    gram.c_struct()   # builds the packed copy
+    full = gram._packed.buf
+
+    class C:
+        def __init__(self, rank, world):
+            self.rank, self.world = rank, world
+
+    for rank in range(world):
+        op = sharded_rbf_kernel(dev(x), params, comm=C(rank, world))
+        t_lo, t_hi = tile_range(n, world, rank)
+        assert (op.share.t_lo, op.share.t_hi) == (t_lo, t_hi)
+        assert torch.equal(op.share.kp, full[t_lo * 4096:t_hi * 4096])
+
+
+def test_tile_share_laplace_newton_config3_recipe_virtual_ranks(P):
+    """Config 3's recipe (d = 8, lengthscale 2, k = 32, ell_log = 36) at
+    n = 3000 on two virtual ranks with tile shares: the sharded Newton driver
+    against the reference (oracle), iterations +-1, psi 1e-8."""
+    from paper_1706_00241_b200.sharded import DeviceShardBackend, sharded_laplace_newton
+
+    n = 3000
+    x, y = O.gpc_inputs(n, 8, 0)
+    cfg = P.SolverConfig(tol=1e-8, ell=36)
+    kmat = O.rbf_kernel(x, 1.0, 2.0)
+    _, _, ref = O.laplace_newton(kmat, y, "defcg", O.Cfg(tol=1e-8, ell=36), newton_tol=-np.inf, max_newton=3, k=32,
+                                 selection="largest", be="numpy")
+
+    def rank_fn(rank, comm):
+        recs = sharded_laplace_newton(x, y, P.KernelParams(1.0, 2.0), cfg, newton_tol=-np.inf, max_newton=3, k=32,
+                                      selection="largest", comm=comm, backend=DeviceShardBackend(slot=2 + rank))
+        torch.cuda.synchronize()
+        return recs
+
+    outs = run_ranks(2, rank_fn)
+    for recs in outs:
+        assert [r.solver_iterations for r in recs] == [r.solver_iterations for r in outs[0]]
+        for a, b in zip(recs, ref):
+            assert abs(a.solver_iterations - b.solver_iterations) <= 1, ([r.solver_iterations for r in recs],
+                                                                         [r.solver_iterations for r in ref])
+            assert abs(a.psi - b.psi) <= 1e-8 * abs(b.psi)

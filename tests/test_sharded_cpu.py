@@ -201,3 +201,66 @@ def test_row_partition_covers_rows():
             mb = row_block(n, world)
             for r, (r0, rows) in enumerate(spans):
                 assert rows <= mb and (rows == 0 or r0 == r * mb)
+
+
+def _share_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from shard_cpu_backend import CpuShardBackend, CpuTileShareOperator
+
+        from paper_1706_00241_b200 import SolverConfig
+        from paper_1706_00241_b200.sharded import ShardBasis, TorchComm, row_range, sharded_solve
+
+        comm, be = TorchComm(), CpuShardBackend()
+        results = []
+        for seed, n, k in ((11, 150, 0), (12, 200, 4), (13, 131, 3)):
+            a, b, xprev, w = _case(seed, n, k, 50.0)
+            t = lambda v: torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64))
+            r0, rows = row_range(n, world, rank)
+            op = CpuTileShareOperator(t(a), r0, rows, rank, world)
+            basis = None
+            if k:
+                aw = a @ w
+                g = w.T @ aw
+                basis = ShardBasis(t(w), t(aw), t(np.linalg.cholesky(0.5 * (g + g.T))))
+            x, rep, log = sharded_solve(op, t(b[r0:r0 + rows]), t(xprev[r0:r0 + rows]), basis,
+                                        SolverConfig(tol=1e-10, ell=6, recompute_residual_every=9), comm, be, poll=2)
+            assert log.replicated and log.r.shape[1] == n   # the log holds all rows on every rank
+            parts = [torch.zeros(-(-n // world), dtype=torch.float64) for _ in range(world)]
+            pad = torch.zeros(-(-n // world), dtype=torch.float64)
+            pad[:rows] = x
+            dist.all_gather(parts, pad)
+            results.append((torch.cat(parts)[:n].numpy(), rep.iterations))
+        if rank == 0:
+            out.put(results)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_tile_share_solver_world2():
+    """The stored tile-share path (each rank its share of the lower-triangle
+    tiles, replicated vectors, one all-reduce of K (s (.) p) per product;
+    everything else redundant on every rank) through sharded_solve over gloo,
+    world 2, CG and def-CG with the true-residual path, against the reference."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_share_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for (seed, n, k), (x, its) in zip(((11, 150, 0), (12, 200, 4), (13, 131, 3)), results):
+        a, b, xprev, w = _case(seed, n, k, 50.0)
+        cfg = O.Cfg(tol=1e-10, ell=6, recompute_residual_every=9)
+        if k:
+            basis = O.refresh_basis(a, w)
+            xr, rep, _ = O.deflated_cg_solve(a, b, xprev, basis, cfg, be="numpy")
+        else:
+            xr, rep, _ = O.cg_solve(a, b, xprev, cfg, be="numpy")
+        assert abs(its - rep.iterations) <= 1, (n, k, its, rep.iterations)
+        assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
