@@ -28,7 +28,7 @@ def gpc_sequence(n, d, ell, k, solver="defcg", reps=3, ell_log=None):
     import torch
 
     import paper_1706_00241_b200 as P
-    from oracle.defcg_oracle import gpc_inputs
+    from paper_1706_00241_b200.workloads import gpc_inputs
 
     x, y = gpc_inputs(n, d, 0)
     gram = P.rbf_kernel(torch.from_numpy(x).cuda(), P.KernelParams(1.0, ell))
@@ -125,7 +125,7 @@ def config5(n, d=16, ell=3.0, k=32, iters=20):
     import torch
 
     import paper_1706_00241_b200 as P
-    from oracle.defcg_oracle import gpc_inputs
+    from paper_1706_00241_b200.workloads import gpc_inputs
 
     rng = np.random.default_rng(0)
     x = torch.from_numpy(rng.standard_normal((n, d))).cuda()
@@ -140,7 +140,8 @@ def config5(n, d=16, ell=3.0, k=32, iters=20):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 3
-    flop = float(n) * n * (2 * d + 4)
+    # SURVEY 8d contract model: (2d + 4) flop per UNIQUE pair, n (n + 1) / 2 pairs
+    flop = float(n) * (n + 1) / 2 * (2 * d + 4)
     s = torch.from_numpy(rng.uniform(0.2, 0.5, n)).cuda()
     a = op.scaled(s, 1.0)
     b = torch.from_numpy(rng.standard_normal(n)).cuda()
@@ -156,8 +157,10 @@ def config5(n, d=16, ell=3.0, k=32, iters=20):
     half = a.with_rows(0, n // 2) if hasattr(a, "with_rows") else None
     del half
     _, rep, _ = P.deflated_cg_solve(a, b, torch.zeros(n, dtype=torch.float64, device="cuda"), basis, cfg)
+    dmma_peak = 37.1   # TFLOP/s, tools/fp64_peak.cu on this B200 (FP64 tensor pipe)
     return {"n": n, "d": d, "matvec_ms": ms, "flop_alg_per_matvec": flop, "achieved_tflops": flop / (ms / 1e3) / 1e12,
-            "exp_per_s": float(n) * n / (ms / 1e3), "solve_iterations": rep.iterations,
+            "frac_of_fp64_peak": flop / (ms / 1e3) / 1e12 / dmma_peak, "flop_model": "(2d+4) n(n+1)/2 (SURVEY 8d)",
+            "exp_per_s": float(n) * (n + 1) / 2 / (ms / 1e3), "solve_iterations": rep.iterations,
             "solve_ms_per_iteration": rep.device_ms / (rep.iterations + 2),
             "refresh_ms_k": [refresh_ms, k],
             "note": "symmetric half-evaluation (each pair once), dot-product distance form"}
