@@ -42,22 +42,25 @@ int dcg_block_apply(dcg_context*, cudaStream_t, const double*, long long, long l
                     const double*, const double*, double, const double*, double*, double*);
 int dcg_xty(dcg_context*, cudaStream_t, const double*, long long, const double*, long long, long long, int, int,
             double*, double*);
-size_t dcg_sym_block_scratch_doubles(long long n);
+size_t dcg_sym_block_scratch_doubles(long long n, int k);
 bool dcg_sym_block_ok(int k);
 int dcg_sym_block_apply(dcg_context*, cudaStream_t, const double*, long long, const double*, int, const double*,
                         const double*, double, double*, double*);
 
 // The refresh's block product A W over the operator's storage: the packed
 // lower-triangle tiles with the symmetric DMMA product (symblock.cu, half the
-// bytes) when the operator has them and k <= 16, else the row-major DMMA GEMM.
+// bytes; k padded to 16 or 32 columns) when the operator has them and
+// k <= 16 or 24 < k <= 32, else the row-major DMMA GEMM (for 16 < k <= 24 the
+// padding to 32 columns costs what the halved bytes save: 1.95 vs 1.89 ms at
+// n = 3e4, k = 24; at k = 32, n = 5e4: 5.35 vs 7.46 ms).
 // DCG_NO_SYMBLOCK (developer A/B knob) forces the row-major product.
 static bool use_sym_block(const dcg_operator* op, int k) {
     static const bool off = getenv("DCG_NO_SYMBLOCK") != nullptr;
     return !off && op->kind == DCG_OP_DENSE_SYM && op->d_kp && op->row0 == 0 && op->rows == op->n &&
-           dcg_sym_block_ok(k);
+           dcg_sym_block_ok(k) && (k <= 16 || k > 24);
 }
 static size_t block_scratch_doubles(const dcg_operator* op, int k) {
-    return use_sym_block(op, k) ? dcg_sym_block_scratch_doubles(op->n)
+    return use_sym_block(op, k) ? dcg_sym_block_scratch_doubles(op->n, k)
                                 : dcg_block_apply_scratch_doubles(op->n, op->rows, k);
 }
 static int block_apply_op(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, const double* X, int k,

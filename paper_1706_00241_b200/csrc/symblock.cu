@@ -1,6 +1,6 @@
 // K3 over the packed lower triangle: Y = shift X + s_out (.) K (s_in (.) X)
 // for an exactly symmetric K (DCG_OP_DENSE_SYM with the packed tiles of
-// dcg_pack_sym) and a block X of k <= 16 columns -- the refresh's A W
+// dcg_pack_sym) and a block X of k <= 32 columns (padded to KP = 16 or 32) -- the refresh's A W
 // (recycle.py:90, refresh_basis) reading each stored entry of K once for both
 // K_IJ and K_JI: half the bytes of the row-major product (dmma_gemm_kernel).
 //
@@ -20,8 +20,8 @@
 //   K tile   the packed, XOR-swizzled tile (symgemv.cuh); the 8 rows of an m8
 //            fragment are rows {b + a, b + a + 8 : a < 4}, so lanes 2a, 2a + 1
 //            read rows whose swizzle keys differ in bit 2;
-//   V block  64 rows as 32 row pairs of 2 x SB_KP doubles (pair-interleaved:
-//            (r, c) at (r / 2) SB_VP + 2 c + r mod 2) padded to SB_VP, so the
+//   V block  64 rows as 32 row pairs of 2 x KP doubles (pair-interleaved:
+//            (r, c) at (r / 2) VP + 2 c + r mod 2) padded to VP = 2 KP + 4, so the
 //            two k indices 2p, 2p + 1 a thread feeds to two consecutive MMAs
 //            are one 16-byte load (the k order inside each 8-chunk is permuted
 //            identically for A and B, which leaves every dot product intact).
@@ -29,17 +29,11 @@
 #include "symgemv.cuh"
 
 #define SB_R 4                                   // tile blocks per super-tile side
-#define SB_KP 16                                 // padded columns of X
-#define SB_VP (2 * SB_KP + 4)                    // doubles per row pair of a V block
-#define SB_VBLK (32 * SB_VP)                     // doubles per 64-row V block
-#define SB_STAGE (DCG_SYM_TILE_DOUBLES + 2 * SB_VBLK)
-#define SB_STAGES 4
 #ifndef SB_MT
 #define SB_MT 1                                  // m8 fragments per consumer warp (1 or 2; 1 measured 1-2% faster)
 #endif
 #define SB_NCW (16 / SB_MT)                      // consumer warps: half row part, half column part
 #define SB_NT (32 * (SB_NCW + 1))                // + one producer warp
-#define SB_SLOT (DCG_TB * SB_KP)                 // doubles per RP / CP slot (64 rows x SB_KP)
 #ifndef SB_UNROLL
 #define SB_UNROLL 8                              // k-pair steps unrolled in the MMA loops (all 8: measured fastest)
 #endif
@@ -47,6 +41,17 @@
 namespace {
 
 constexpr int kSbUnroll = SB_UNROLL;
+
+// Geometry for KP padded columns of X (16 or 32).
+template <int KP>
+struct SbCfg {
+    static constexpr int VP = 2 * KP + 4;                          // doubles per row pair of a V block
+    static constexpr int VBLK = 32 * VP;                           // doubles per 64-row V block
+    static constexpr int STAGE = DCG_SYM_TILE_DOUBLES + 2 * VBLK;  // tile + V_J + V_I
+    static constexpr int STAGES = KP <= 16 ? 4 : 3;                // ring depth within 227 KB
+    static constexpr int SLOT = DCG_TB * KP;                       // doubles per RP / CP slot
+    static constexpr int NT8 = KP / 8;                             // n8 fragments per warp
+};
 
 struct SbMeta {
     int unit;
@@ -102,16 +107,18 @@ __device__ __forceinline__ unsigned long long sb_policy_normal() {
 __device__ __forceinline__ int sb_row(int mt, int g) { return 4 * mt + (g >> 1) + 8 * (g & 1); }
 
 // V (blocks of 64 rows, pair-interleaved, zero beyond n and k) = s (.) X
+template <int KP>
 __global__ void sb_pack_v_kernel(const double* __restrict__ X, int k, const double* __restrict__ s, long long n,
                                  long long nblk, double* __restrict__ V) {
-    const long long total = nblk * SB_VBLK;
+    using C = SbCfg<KP>;
+    const long long total = nblk * C::VBLK;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
-        const long long b = e / SB_VBLK;
-        const int w = (int)(e - b * SB_VBLK);
-        const int p = w / SB_VP, q = w - p * SB_VP;
+        const long long b = e / C::VBLK;
+        const int w = (int)(e - b * C::VBLK);
+        const int p = w / C::VP, q = w - p * C::VP;
         double v = 0.0;
-        if (q < 2 * SB_KP) {
+        if (q < 2 * KP) {
             const int c = q >> 1;
             const long long i = b * DCG_TB + 2 * p + (q & 1);
             if (i < n && c < k) {
@@ -123,19 +130,21 @@ __global__ void sb_pack_v_kernel(const double* __restrict__ X, int k, const doub
     }
 }
 
+template <int KP>
 __global__ void __launch_bounds__(SB_NT, 1)
     sb_apply_kernel(const double* __restrict__ Kp, long long n, const double* __restrict__ V, double* __restrict__ RP,
                     double* __restrict__ CP, unsigned long long* counter) {
+    using C = SbCfg<KP>;
     extern __shared__ __align__(128) double sm[];
     double* ring = sm;
-    unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + SB_STAGES * SB_STAGE);
-    unsigned long long* empty = full + SB_STAGES;
-    SbMeta* meta = reinterpret_cast<SbMeta*>(empty + SB_STAGES);
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + C::STAGES * C::STAGE);
+    unsigned long long* empty = full + C::STAGES;
+    SbMeta* meta = reinterpret_cast<SbMeta*>(empty + C::STAGES);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const long long NB = sb_nblocks(n), NS = sb_nsuper(n), NU = sb_units(n);
     if (tid == 0) {
-        for (int st = 0; st < SB_STAGES; ++st) {
+        for (int st = 0; st < C::STAGES; ++st) {
             sym_mbar_init(full + st, 1);
             sym_mbar_init(empty + st, SB_NCW);
         }
@@ -145,7 +154,7 @@ __global__ void __launch_bounds__(SB_NT, 1)
 
     // ---- producer (lane 0 of the last warp): walks the units it draws from the
     // counter and streams their tiles (+ V blocks) through the ring, up to
-    // SB_STAGES stages ahead of the consumers; a unit of -1 marks the end.
+    // C::STAGES stages ahead of the consumers; a unit of -1 marks the end.
     if (warp == SB_NCW) {
         if (lane == 0) {
             const unsigned long long pol_k = sym_policy_evict_first(), pol_v = sb_policy_normal();
@@ -162,8 +171,8 @@ __global__ void __launch_bounds__(SB_NT, 1)
                 bool first = true;
                 for (;;) {
                     if (!done && I >= I1) break;
-                    const int stg = q % SB_STAGES;
-                    if (q >= SB_STAGES) sym_mbar_wait(empty + stg, ((q / SB_STAGES) - 1) & 1);
+                    const int stg = q % C::STAGES;
+                    if (q >= C::STAGES) sym_mbar_wait(empty + stg, ((q / C::STAGES) - 1) & 1);
                     SbMeta m;
                     if (done) {
                         m.unit = -1;
@@ -180,12 +189,12 @@ __global__ void __launch_bounds__(SB_NT, 1)
                     m.flags = (first ? 1 : 0) | (J == J0 ? 16 : 0) | (J + 1 == jend ? 4 : 0) | (I == J ? 8 : 0);
                     if (J + 1 == jend && I + 1 == I1) m.flags |= 2;
                     meta[stg] = m;
-                    double* dst = ring + stg * SB_STAGE;
-                    sym_mbar_expect_tx(full + stg, (unsigned)(SB_STAGE * sizeof(double)));
+                    double* dst = ring + stg * C::STAGE;
+                    sym_mbar_expect_tx(full + stg, (unsigned)(C::STAGE * sizeof(double)));
                     sb_bulk(dst, Kp + (sym_tile_row_base(I) + J) * DCG_SYM_TILE_DOUBLES,
                             DCG_SYM_TILE_DOUBLES * sizeof(double), full + stg, pol_k);
-                    sb_bulk(dst + DCG_SYM_TILE_DOUBLES, V + J * SB_VBLK, SB_VBLK * sizeof(double), full + stg, pol_v);
-                    sb_bulk(dst + DCG_SYM_TILE_DOUBLES + SB_VBLK, V + I * SB_VBLK, SB_VBLK * sizeof(double), full + stg,
+                    sb_bulk(dst + DCG_SYM_TILE_DOUBLES, V + J * C::VBLK, C::VBLK * sizeof(double), full + stg, pol_v);
+                    sb_bulk(dst + DCG_SYM_TILE_DOUBLES + C::VBLK, V + I * C::VBLK, C::VBLK * sizeof(double), full + stg,
                             pol_v);
                     ++q;
                     first = false;
@@ -203,13 +212,13 @@ __global__ void __launch_bounds__(SB_NT, 1)
     // ---- consumers: warps 0-3 the row part, 4-7 the column part ----------------
     const bool rowpart = warp < SB_NCW / 2;
     const int wl = warp % (SB_NCW / 2);
-    double acc[SB_R][SB_MT][2][2];    // [block][mt][nt][2]  (row part uses block 0 only)
+    double acc[SB_R][SB_MT][C::NT8][2];    // [block][mt][nt][2]  (row part uses block 0 only)
 #pragma unroll
     for (int b = 0; b < SB_R; ++b)
 #pragma unroll
         for (int mt = 0; mt < SB_MT; ++mt)
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) acc[b][mt][nt][0] = acc[b][mt][nt][1] = 0.0;
+            for (int nt = 0; nt < C::NT8; ++nt) acc[b][mt][nt][0] = acc[b][mt][nt][1] = 0.0;
     // per-lane fragment offsets
     // output rows of the warp's m8 fragments (16-row blocks split over 2 / SB_MT warps)
     int rowm[SB_MT];
@@ -218,35 +227,35 @@ __global__ void __launch_bounds__(SB_NT, 1)
 
     unsigned int q = 0;
     for (;;) {
-        const int stg = q % SB_STAGES;
-        sym_mbar_wait(full + stg, (q / SB_STAGES) & 1);
+        const int stg = q % C::STAGES;
+        sym_mbar_wait(full + stg, (q / C::STAGES) & 1);
         const SbMeta m = meta[stg];
         if (m.unit < 0) break;
-        const double* tile = ring + stg * SB_STAGE;
+        const double* tile = ring + stg * C::STAGE;
         const double* vj = tile + DCG_SYM_TILE_DOUBLES;
-        const double* vi = vj + SB_VBLK;
+        const double* vi = vj + C::VBLK;
         if (rowpart) {
             if (m.flags & 16) {
 #pragma unroll
                 for (int mt = 0; mt < SB_MT; ++mt)
 #pragma unroll
-                    for (int nt = 0; nt < 2; ++nt) acc[0][mt][nt][0] = acc[0][mt][nt][1] = 0.0;
+                    for (int nt = 0; nt < C::NT8; ++nt) acc[0][mt][nt][0] = acc[0][mt][nt][1] = 0.0;
             }
 #pragma unroll kSbUnroll
             for (int s2 = 0; s2 < DCG_TB / 8; ++s2) {
-                double2 a[SB_MT], b[2];
+                double2 a[SB_MT], b[C::NT8];
 #pragma unroll
                 for (int mt = 0; mt < SB_MT; ++mt) {
                     const int r = rowm[mt];
                     a[mt] = *reinterpret_cast<const double2*>(tile + r * DCG_TB + 2 * ((4 * s2 + t) ^ ((r >> 1) & 31)));
                 }
 #pragma unroll
-                for (int nt = 0; nt < 2; ++nt)
-                    b[nt] = *reinterpret_cast<const double2*>(vj + (4 * s2 + t) * SB_VP + 2 * (8 * nt + g));
+                for (int nt = 0; nt < C::NT8; ++nt)
+                    b[nt] = *reinterpret_cast<const double2*>(vj + (4 * s2 + t) * C::VP + 2 * (8 * nt + g));
 #pragma unroll
                 for (int mt = 0; mt < SB_MT; ++mt)
 #pragma unroll
-                    for (int nt = 0; nt < 2; ++nt) {
+                    for (int nt = 0; nt < C::NT8; ++nt) {
                         sb_dmma(acc[0][mt][nt][0], acc[0][mt][nt][1], a[mt].x, b[nt].x);
                         sb_dmma(acc[0][mt][nt][0], acc[0][mt][nt][1], a[mt].y, b[nt].y);
                     }
@@ -258,7 +267,7 @@ __global__ void __launch_bounds__(SB_NT, 1)
 #pragma unroll
                     for (int mt = 0; mt < SB_MT; ++mt)
 #pragma unroll
-                        for (int nt = 0; nt < 2; ++nt) acc[b][mt][nt][0] = acc[b][mt][nt][1] = 0.0;
+                        for (int nt = 0; nt < C::NT8; ++nt) acc[b][mt][nt][0] = acc[b][mt][nt][1] = 0.0;
             }
             // A = K_IJ' (rows: the tile's columns), B = V_I
 #pragma unroll
@@ -268,7 +277,7 @@ __global__ void __launch_bounds__(SB_NT, 1)
                 for (int s2 = 0; s2 < DCG_TB / 8; ++s2) {
                     const int i0 = 8 * s2 + 2 * t;   // tile rows i0, i0 + 1 (same swizzle key)
                     double a0[SB_MT], a1[SB_MT];
-                    double2 b[2];
+                    double2 b[C::NT8];
 #pragma unroll
                     for (int mt = 0; mt < SB_MT; ++mt) {
                         const int c = rowm[mt];
@@ -277,12 +286,12 @@ __global__ void __launch_bounds__(SB_NT, 1)
                         a1[mt] = tile[off + DCG_TB];
                     }
 #pragma unroll
-                    for (int nt = 0; nt < 2; ++nt)
-                        b[nt] = *reinterpret_cast<const double2*>(vi + (4 * s2 + t) * SB_VP + 2 * (8 * nt + g));
+                    for (int nt = 0; nt < C::NT8; ++nt)
+                        b[nt] = *reinterpret_cast<const double2*>(vi + (4 * s2 + t) * C::VP + 2 * (8 * nt + g));
 #pragma unroll
                     for (int mt = 0; mt < SB_MT; ++mt)
 #pragma unroll
-                        for (int nt = 0; nt < 2; ++nt) {
+                        for (int nt = 0; nt < C::NT8; ++nt) {
                             sb_dmma(acc[lj][mt][nt][0], acc[lj][mt][nt][1], a0[mt], b[nt].x);
                             sb_dmma(acc[lj][mt][nt][0], acc[lj][mt][nt][1], a1[mt], b[nt].y);
                         }
@@ -295,19 +304,19 @@ __global__ void __launch_bounds__(SB_NT, 1)
 #pragma unroll
                 for (int mt = 0; mt < SB_MT; ++mt)
 #pragma unroll
-                    for (int nt = 0; nt < 2; ++nt) acc[b][mt][nt][0] = acc[b][mt][nt][1] = 0.0;
+                    for (int nt = 0; nt < C::NT8; ++nt) acc[b][mt][nt][0] = acc[b][mt][nt][1] = 0.0;
         }
         __syncwarp();
         if (lane == 0) sym_mbar_arrive(empty + stg);
         ++q;
         // flushes: D fragment (g, t) holds rows rowm[mt], columns 8 nt + 2t, 2t + 1
         if (rowpart && (m.flags & 4)) {
-            double* out = RP + ((long long)m.unit * SB_R + m.li) * SB_SLOT;
+            double* out = RP + ((long long)m.unit * SB_R + m.li) * C::SLOT;
 #pragma unroll
             for (int mt = 0; mt < SB_MT; ++mt)
 #pragma unroll
-                for (int nt = 0; nt < 2; ++nt)
-                    *reinterpret_cast<double2*>(out + rowm[mt] * SB_KP + 8 * nt + 2 * t) =
+                for (int nt = 0; nt < C::NT8; ++nt)
+                    *reinterpret_cast<double2*>(out + rowm[mt] * KP + 8 * nt + 2 * t) =
                         make_double2(acc[0][mt][nt][0], acc[0][mt][nt][1]);
         }
         if (!rowpart && (m.flags & 2)) {
@@ -316,12 +325,12 @@ __global__ void __launch_bounds__(SB_NT, 1)
 #pragma unroll
             for (int lj = 0; lj < SB_R; ++lj) {
                 if (SB_R * B + lj >= NB) continue;
-                double* out = CP + ((long long)m.unit * SB_R + lj) * SB_SLOT;
+                double* out = CP + ((long long)m.unit * SB_R + lj) * C::SLOT;
 #pragma unroll
                 for (int mt = 0; mt < SB_MT; ++mt)
 #pragma unroll
-                    for (int nt = 0; nt < 2; ++nt)
-                        *reinterpret_cast<double2*>(out + rowm[mt] * SB_KP + 8 * nt + 2 * t) =
+                    for (int nt = 0; nt < C::NT8; ++nt)
+                        *reinterpret_cast<double2*>(out + rowm[mt] * KP + 8 * nt + 2 * t) =
                             make_double2(acc[lj][mt][nt][0], acc[lj][mt][nt][1]);
             }
         }
@@ -331,21 +340,23 @@ __global__ void __launch_bounds__(SB_NT, 1)
 // Y[i][c] = shift X[i][c] + s_out[i] sum(partials of row i), c < k.  Row i of
 // block I = 4 A + li: the RP slots of units (A, 0..A) then the CP slots of
 // units (A..NS-1, A), in that order.
+template <int KP>
 __global__ void sb_reduce_kernel(const double* __restrict__ RP, const double* __restrict__ CP, long long n, int k,
                                  const double* __restrict__ X_rows, const double* __restrict__ s_out, double shift,
                                  double* __restrict__ Y) {
+    using C = SbCfg<KP>;
     const long long NS = sb_nsuper(n);
-    const long long total = n * SB_KP;
+    const long long total = n * KP;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
-        const long long i = e / SB_KP;
-        const int c = (int)(e - i * SB_KP);
+        const long long i = e / KP;
+        const int c = (int)(e - i * KP);
         if (c >= k) continue;
         const long long I = i / DCG_TB;
         const int r = (int)(i - I * DCG_TB);
         const long long A = I / SB_R;
         const int li = (int)(I - A * SB_R);
-        const long long off = (long long)li * SB_SLOT + r * SB_KP + c;
+        const long long off = (long long)li * C::SLOT + r * KP + c;
         // the partials in a fixed order: RP of units (A, 0..A), then CP of units
         // (A..NS-1, A); loaded 8 at a time ahead of their (ordered) adds
         const long long nterm = (A + 1) + (NS - A);
@@ -356,8 +367,8 @@ __global__ void sb_reduce_kernel(const double* __restrict__ RP, const double* __
             for (int u = 0; u < 8; ++u) {
                 const long long q = q0 + u;
                 v[u] = 0.0;
-                if (q <= A) v[u] = RP[sb_unit_of(A, q, NS) * SB_R * SB_SLOT + off];
-                else if (q < nterm) v[u] = CP[sb_unit_of(A + (q - A - 1), A, NS) * SB_R * SB_SLOT + off];
+                if (q <= A) v[u] = RP[sb_unit_of(A, q, NS) * SB_R * C::SLOT + off];
+                else if (q < nterm) v[u] = CP[sb_unit_of(A + (q - A - 1), A, NS) * SB_R * C::SLOT + off];
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u)
@@ -371,30 +382,43 @@ __global__ void sb_reduce_kernel(const double* __restrict__ RP, const double* __
 
 }  // namespace
 
-size_t dcg_sym_block_scratch_doubles(long long n) {
-    return (size_t)(sb_nblocks(n) * SB_VBLK) + 2 * (size_t)sb_units(n) * SB_R * SB_SLOT + 64;
+template <int KP>
+static size_t sb_scratch(long long n) {
+    using C = SbCfg<KP>;
+    return (size_t)(sb_nblocks(n) * C::VBLK) + 32 + 2 * (size_t)sb_units(n) * SB_R * C::SLOT + 64;
 }
-bool dcg_sym_block_ok(int k) { return k >= 1 && k <= SB_KP; }
+static int sb_kp(int k) { return k <= 16 ? 16 : 32; }
 
-// Y (n x k) = shift X + s_out (.) K (s_in (.) X) over the packed tiles Kp.
+size_t dcg_sym_block_scratch_doubles(long long n, int k) { return sb_kp(k) == 16 ? sb_scratch<16>(n) : sb_scratch<32>(n); }
+bool dcg_sym_block_ok(int k) { return k >= 1 && k <= 32; }
+
+template <int KP>
+static int sb_apply(dcg_context* ctx, cudaStream_t st, const double* Kp, long long n, const double* X, int k,
+                    const double* s_in, const double* s_out, double shift, double* Y, double* scratch) {
+    using C = SbCfg<KP>;
+    const long long NB = sb_nblocks(n), NU = sb_units(n);
+    double* V = scratch;
+    double* RP = V + ((NB * C::VBLK + 31) & ~31LL);
+    double* CP = RP + NU * SB_R * C::SLOT;
+    unsigned long long* counter = reinterpret_cast<unsigned long long*>(CP + NU * SB_R * C::SLOT);
+    DCG_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
+    sb_pack_v_kernel<KP><<<ctx->sm_count * 4, 256, 0, st>>>(X, k, s_in, n, NB, V);
+    DCG_LAUNCHED();
+    const size_t smem = sizeof(double) * C::STAGES * C::STAGE + 2 * C::STAGES * sizeof(unsigned long long) +
+                        C::STAGES * sizeof(SbMeta);
+    DCG_SMEM_ATTR(sb_apply_kernel<KP>, smem);
+    sb_apply_kernel<KP><<<ctx->sm_count, SB_NT, smem, st>>>(Kp, n, V, RP, CP, counter);
+    DCG_LAUNCHED();
+    sb_reduce_kernel<KP><<<ctx->sm_count * 4, 256, 0, st>>>(RP, CP, n, k, X, s_out, shift, Y);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}
+
+// Y (n x k) = shift X + s_out (.) K (s_in (.) X) over the packed tiles Kp (k <= 32).
 int dcg_sym_block_apply(dcg_context* ctx, cudaStream_t st, const double* Kp, long long n, const double* X, int k,
                         const double* s_in, const double* s_out, double shift, double* Y, double* scratch) {
     if (n <= 0 || k <= 0) return DCG_OK;
     if (!dcg_sym_block_ok(k) || !aligned16(Kp)) return DCG_E_CONFIG;
-    const long long NB = sb_nblocks(n), NU = sb_units(n);
-    double* V = scratch;
-    double* RP = V + ((NB * SB_VBLK + 31) & ~31LL);
-    double* CP = RP + NU * SB_R * SB_SLOT;
-    unsigned long long* counter = reinterpret_cast<unsigned long long*>(CP + NU * SB_R * SB_SLOT);
-    DCG_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
-    sb_pack_v_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(X, k, s_in, n, NB, V);
-    DCG_LAUNCHED();
-    const size_t smem = sizeof(double) * SB_STAGES * SB_STAGE + 2 * SB_STAGES * sizeof(unsigned long long) +
-                        SB_STAGES * sizeof(SbMeta);
-    DCG_SMEM_ATTR(sb_apply_kernel, smem);
-    sb_apply_kernel<<<ctx->sm_count, SB_NT, smem, st>>>(Kp, n, V, RP, CP, counter);
-    DCG_LAUNCHED();
-    sb_reduce_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(RP, CP, n, k, X, s_out, shift, Y);
-    DCG_LAUNCHED();
-    return DCG_OK;
+    return sb_kp(k) == 16 ? sb_apply<16>(ctx, st, Kp, n, X, k, s_in, s_out, shift, Y, scratch)
+                          : sb_apply<32>(ctx, st, Kp, n, X, k, s_in, s_out, shift, Y, scratch);
 }

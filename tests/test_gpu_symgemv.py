@@ -123,11 +123,12 @@ def test_packed_solve_bitwise_rowmajor(P, n, k, recompute):
 
 
 @pytest.mark.parametrize("n,k", [(1, 1), (63, 3), (64, 16), (65, 7), (257, 16), (1000, 12), (2049, 16), (4500, 16),
-                                 (3000, 24)])
+                                 (3000, 24), (1000, 28), (4500, 32), (130, 33)])
 def test_symmetric_block_product(P, n, k):
     """A W over the packed tiles (symblock.cu: each tile feeds K_IJ W_J and
-    K_IJ' W_I on the FP64 tensor pipe; k <= 16) against the row-major DMMA
-    product and an fp64 host product; k = 24 takes the row-major path."""
+    K_IJ' W_I on the FP64 tensor pipe; k <= 32, padded to 16 or 32 columns)
+    against the row-major DMMA product and an fp64 host product; k = 24 and
+    k = 33 take the row-major path."""
     rng = np.random.default_rng(300 + n + k)
     a = O.rbf_kernel(rng.standard_normal((n, 5)), 1.0, 1.2)
     op = P.DenseOperator.from_matrix(a).with_strategy("sym")
