@@ -191,6 +191,9 @@ DCG_API int dcg_gen_sym_eigen(dcg_context* ctx, void* stream, const double* d_g,
  * are those of the row-major path.  Not in the reference: its matvec reads
  * the dense ndarray (_core.pyx:16-28, linalg.py:58-63).                      */
 DCG_API long long dcg_packed_sym_doubles(long long n);
+/* 1 when a block product of k columns over a DENSE_SYM operator with d_kp runs
+ * on the packed tiles (then d_k may be NULL), 0 when it needs d_k.          */
+DCG_API int dcg_block_uses_packed(int k);
 DCG_API int dcg_pack_sym(dcg_context* ctx, void* stream, const double* d_k, long long ldk, long long n,
                  double* d_kp);
 

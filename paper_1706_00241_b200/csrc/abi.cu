@@ -59,6 +59,10 @@ static bool use_sym_block(const dcg_operator* op, int k) {
     return !off && op->kind == DCG_OP_DENSE_SYM && op->d_kp && op->row0 == 0 && op->rows == op->n &&
            dcg_sym_block_ok(k) && (k <= 16 || k > 24);
 }
+extern "C" int dcg_block_uses_packed(int k) {
+    static const bool off = getenv("DCG_NO_SYMBLOCK") != nullptr;
+    return !off && dcg_sym_block_ok(k) && (k <= 16 || k > 24);
+}
 static size_t block_scratch_doubles(const dcg_operator* op, int k) {
     return use_sym_block(op, k) ? dcg_sym_block_scratch_doubles(op->n, k)
                                 : dcg_block_apply_scratch_doubles(op->n, op->rows, k);
@@ -68,6 +72,7 @@ static int block_apply_op(dcg_context* ctx, cudaStream_t st, const dcg_operator*
                           double* scratch) {
     if (use_sym_block(op, k))
         return dcg_sym_block_apply(ctx, st, op->d_kp, op->n, X, k, s_in, s_out, shift, Y, scratch);
+    if (!op->d_k) return DCG_E_CONFIG;   // a packed-only operator without its row-major storage
     return dcg_block_apply(ctx, st, op->d_k, op->ldk, op->rows, op->n, X, k, s_in, s_out, shift, X_rows, Y, scratch);
 }
 size_t dcg_xty_scratch_doubles(dcg_context* ctx, int p, int q);
@@ -443,6 +448,7 @@ static int apply_k(dcg_context* ctx, cudaStream_t st, const dcg_operator* op, co
     // the lower-triangle strategy stages 16-byte slices of v and s_in
     if (op->kind == DCG_OP_DENSE_SYM && aligned16(v) && aligned16(s_in))
         return dcg_sym_apply(ctx, st, op->d_k, op->d_kp, op->ldk, op->n, v, s_in, s_out, shift, y, scratch);
+    if (!op->d_k) return DCG_E_CONFIG;
     return dcg_gemv_launch(ctx, st, op->d_k, op->ldk, op->n, op->rows, v, s_in, s_out, shift, v + op->row0, y);
 }
 

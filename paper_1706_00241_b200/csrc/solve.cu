@@ -593,6 +593,7 @@ static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, co
     if (op->kind != DCG_OP_DENSE && op->kind != DCG_OP_DENSE_SYM && op->kind != DCG_OP_RBF) return DCG_E_UNSUPPORTED;
     const bool sym = op->kind == DCG_OP_DENSE_SYM && ((reinterpret_cast<uintptr_t>(d_x0) | reinterpret_cast<uintptr_t>(op->d_s)) & 15) == 0;
     const int strat = op->kind == DCG_OP_RBF ? STRAT_RBF : (sym ? (op->d_kp ? STRAT_SYMPK : STRAT_SYM) : STRAT_ROWS);
+    if (strat != STRAT_RBF && strat != STRAT_SYMPK && !op->d_k) return DCG_E_CONFIG;   // packed-only storage
     if (op->row0 != 0 || op->rows != n) return DCG_E_UNSUPPORTED;   // sharded solves: host loop
     if (strat == STRAT_RBF) {
         if (!op->d_x || op->dim < 1) return DCG_E_CONFIG;

@@ -29,7 +29,7 @@ import torch
 from . import _device as D
 from . import _native as N
 from .errors import DimensionMismatch, InvalidLabel, NoProgress, NotPositiveDefinite, StateInconsistent
-from .operators import DenseOperator, RbfOperator, as_operator
+from .operators import SYM_MIN_N, DenseOperator, RbfOperator, _RowMajor, as_operator
 from .recycle import SELECT_LARGEST, SequenceState, _pinned, _pinned_pool, solve_next, solve_next_async
 from .solvers import SolverConfig, _solve_dev
 
@@ -124,13 +124,28 @@ def rbf_kernel(x, params, jitter=None, matrix_free=False):
     if matrix_free:
         return RbfOperator(xd.contiguous(), var, inv_two_ell2, var + float(jitter))
     ld = D.padded_ld(n)
-    kbuf = D.empty(n, ld)
-    if ld != n:
-        kbuf[:, n:].zero_()   # only the row-pitch padding (the kernel writes every entry of K)
-    if n:
-        N.check(N.lib().dcg_k_rbf_gram(D.ctx(), D.stream(), xd.data_ptr(), n, dim, var, inv_two_ell2, float(jitter),
-                                       kbuf.data_ptr(), ld, 0, n), what="rbf_gram")
-    return DenseOperator(kbuf, n, ld)
+
+    def build_rows():
+        kbuf = D.empty(n, ld)
+        if ld != n:
+            kbuf[:, n:].zero_()   # only the row-pitch padding (the kernel writes every entry of K)
+        if n:
+            N.check(N.lib().dcg_k_rbf_gram(D.ctx(), D.stream(), xd.data_ptr(), n, dim, var, inv_two_ell2,
+                                           float(jitter), kbuf.data_ptr(), ld, 0, n), what="rbf_gram")
+        return kbuf
+
+    if n < SYM_MIN_N:
+        return DenseOperator(build_rows(), n, ld)
+    # Above SYM_MIN_N every product of the Newton path reads the packed
+    # lower-triangle tiles: build those directly from X (entries bitwise the
+    # row-major Gram's) and the row-major K only if something asks for rows.
+    kp = D.empty(int(N.lib().dcg_packed_sym_doubles(n)))
+    ntt = int(N.lib().dcg_packed_sym_doubles(n)) // 4096
+    N.check(N.lib().dcg_k_rbf_gram_packed(D.ctx(), D.stream(), xd.data_ptr(), n, dim, var, inv_two_ell2,
+                                          float(jitter), 0, ntt, kp.data_ptr()), what="rbf_gram_packed")
+    op = DenseOperator(_RowMajor(build=build_rows), n, ld)
+    op._packed.adopt(kp)
+    return op
 
 
 def rbf_cross_kernel(xa, xb, params):

@@ -35,8 +35,9 @@ class _PackedTiles:
     """The packed lower-triangle tile copy of one exactly symmetric K
     (``dcg_pack_sym``: 64 x 64 tiles, each a contiguous 32 KB block, so the
     symmetric products stream K with one bulk copy per tile).  Built on first
-    use and shared by every view of the same storage (``scaled``,
-    ``kernel_view``); K is never modified, so it stays valid."""
+    use (or directly by ``rbf_kernel``) and shared by every view of the same
+    storage (``scaled``, ``kernel_view``); K is never modified, so it stays
+    valid."""
 
     __slots__ = ("buf", "event", "stream")
 
@@ -45,18 +46,54 @@ class _PackedTiles:
         self.event = None
         self.stream = None
 
-    def ptr(self, kbuf: torch.Tensor, n: int, ldk: int) -> int:
+    def adopt(self, buf: torch.Tensor):
+        """Take a packed copy built by the caller on the current stream."""
+        cur = torch.cuda.current_stream(D.device())
+        self.buf = buf
+        self.event = torch.cuda.Event()
+        self.event.record(cur)
+        self.stream = cur.cuda_stream
+
+    def ptr(self, rowmajor, n: int, ldk: int) -> int:
         cur = torch.cuda.current_stream(D.device())
         if self.buf is None:
-            self.buf = D.empty(int(N.lib().dcg_packed_sym_doubles(n)))
-            N.check(N.lib().dcg_pack_sym(D.ctx(), cur.cuda_stream, kbuf.data_ptr(), ldk, n, self.buf.data_ptr()),
+            buf = D.empty(int(N.lib().dcg_packed_sym_doubles(n)))
+            N.check(N.lib().dcg_pack_sym(D.ctx(), cur.cuda_stream, rowmajor.get().data_ptr(), ldk, n, buf.data_ptr()),
                     what="pack_sym")
-            self.event = torch.cuda.Event()
-            self.event.record(cur)
-            self.stream = cur.cuda_stream
+            self.adopt(buf)
         elif cur.cuda_stream != self.stream:
             cur.wait_event(self.event)
         return self.buf.data_ptr()
+
+
+class _RowMajor:
+    """The row-major storage of K: given, or built on first use by `build`
+    (rbf_kernel keeps only the packed tiles until something needs rows: the
+    row strategy, a block product of 17-24 or > 32 columns, the explicit
+    matrix).  Shared by every view of the same storage."""
+
+    __slots__ = ("buf", "build")
+
+    def __init__(self, buf=None, build=None):
+        self.buf, self.build = buf, build
+
+    @property
+    def ready(self) -> bool:
+        return self.buf is not None
+
+    def get(self) -> torch.Tensor:
+        if self.buf is None:
+            if self.build is None:
+                raise RuntimeError("operator has no row-major storage")
+            self.buf = self.build()
+            self.build = None
+        return self.buf
+
+
+def block_uses_packed(k: int) -> bool:
+    """Whether the block product of k columns runs on the packed tiles
+    (csrc/abi.cu use_sym_block)."""
+    return bool(N.lib().dcg_block_uses_packed(int(k)))
 
 
 class DenseOperator:
@@ -70,9 +107,10 @@ class DenseOperator:
 
     __array_priority__ = 100
 
-    def __init__(self, kbuf: torch.Tensor, n: int, ldk: int, s: torch.Tensor | None = None, shift: float = 0.0,
-                 row0: int = 0, rows: int | None = None, strategy: str = "auto", packed: _PackedTiles | None = None):
-        self.kbuf = kbuf
+    def __init__(self, kbuf: torch.Tensor | _RowMajor | None, n: int, ldk: int, s: torch.Tensor | None = None,
+                 shift: float = 0.0, row0: int = 0, rows: int | None = None, strategy: str = "auto",
+                 packed: _PackedTiles | None = None):
+        self._rm = kbuf if isinstance(kbuf, _RowMajor) else _RowMajor(kbuf)
         self._packed = packed if packed is not None else _PackedTiles()
         self.n = int(n)
         self.ldk = int(ldk)
@@ -83,6 +121,11 @@ class DenseOperator:
         if strategy not in STRATEGIES:
             raise ValueError(f"unknown strategy {strategy!r}")
         self.strategy = strategy
+
+    @property
+    def kbuf(self) -> torch.Tensor:
+        """Row-major K (materialised on first access when built packed-only)."""
+        return self._rm.get()
 
     # -- construction ---------------------------------------------------------
     @classmethod
@@ -133,11 +176,11 @@ class DenseOperator:
     def scaled(self, s, shift: float) -> "DenseOperator":
         """Same K, new diagonal scaling and shift (the Newton system of gpc.py:175-183)."""
         s_dev = None if s is None else D.to_dev(s, 1)
-        return DenseOperator(self.kbuf, self.n, self.ldk, s_dev, shift, self.row0, self.rows, self.strategy,
+        return DenseOperator(self._rm, self.n, self.ldk, s_dev, shift, self.row0, self.rows, self.strategy,
                              self._packed)
 
     def with_strategy(self, strategy: str) -> "DenseOperator":
-        return DenseOperator(self.kbuf, self.n, self.ldk, self.s, self.shift, self.row0, self.rows, strategy,
+        return DenseOperator(self._rm, self.n, self.ldk, self.s, self.shift, self.row0, self.rows, strategy,
                              self._packed)
 
     # -- views ------------------------------------------------------------------
@@ -149,7 +192,10 @@ class DenseOperator:
     def ndim(self):
         return 2
 
-    def c_struct(self) -> N.COperator:
+    def c_struct(self, block_k: int | None = None) -> N.COperator:
+        """The ABI operator.  ``block_k``: the column count of a block product
+        the caller will run (refresh, A @ W); the row-major storage is
+        materialised only when the packed tiles cannot serve the call."""
         op = N.COperator()
         strategy = self.strategy
         if strategy == "auto":
@@ -158,11 +204,13 @@ class DenseOperator:
             strategy = "sym" if self.n >= SYM_MIN_N else "rows"
         sym = strategy in ("sym", "sym_rowmajor") and self.row0 == 0 and self.rows == self.n
         op.kind = N.DCG_OP_DENSE_SYM if sym else N.DCG_OP_DENSE
-        op.d_kp = self._packed.ptr(self.kbuf, self.n, self.ldk) if sym and strategy == "sym" and self.n else None
+        packed = sym and strategy == "sym" and self.n > 0
+        op.d_kp = self._packed.ptr(self._rm, self.n, self.ldk) if packed else None
         op.n = self.n
         op.row0 = self.row0
         op.rows = self.rows
-        op.d_k = self.kbuf.data_ptr() if self.n else None
+        need_rows = not packed or (block_k is not None and not block_uses_packed(block_k))
+        op.d_k = self.kbuf.data_ptr() if self.n and (need_rows or self._rm.ready) else None
         op.ldk = self.ldk
         op.d_s = None if self.s is None else self.s.data_ptr()
         op.shift = self.shift
@@ -170,7 +218,7 @@ class DenseOperator:
 
     def kernel_view(self) -> "DenseOperator":
         """K itself (no scaling, no shift)."""
-        return DenseOperator(self.kbuf, self.n, self.ldk, None, 0.0, self.row0, self.rows, self.strategy,
+        return DenseOperator(self._rm, self.n, self.ldk, None, 0.0, self.row0, self.rows, self.strategy,
                              self._packed)
 
     def matvec_dev(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -185,7 +233,7 @@ class DenseOperator:
         k = w.shape[1]
         y = D.empty(self.rows, k)
         if self.rows and k:
-            op = self.c_struct()
+            op = self.c_struct(block_k=k)
             N.check(N.lib().dcg_op_apply_block(D.ctx(), D.stream(), ctypes.byref(op), w.data_ptr(), k,
                                                y.data_ptr()), what="op_apply_block")
         return y
@@ -239,7 +287,7 @@ class RbfOperator(DenseOperator):
     def require_symmetric(self, rtol: float = SYMMETRY_RTOL) -> "RbfOperator":
         return self   # exactly symmetric by construction
 
-    def c_struct(self) -> N.COperator:
+    def c_struct(self, block_k: int | None = None) -> N.COperator:
         op = N.COperator()
         op.kind = N.DCG_OP_RBF
         op.n = self.n

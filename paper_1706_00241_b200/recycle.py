@@ -123,7 +123,7 @@ def _refresh_dev(op, w_dev: torch.Tensor) -> RecycleBasis:
         raise DimensionMismatch(f"basis rows {n} vs operator size {op.n}")
     w_out, aw_out, chol = D.empty(n, k), D.empty(n, k), D.empty(k, k)
     kout, info = ctypes.c_longlong(k), ctypes.c_longlong(0)
-    cop = op.c_struct()
+    cop = op.c_struct(block_k=k) if isinstance(op, DenseOperator) else op.c_struct()
     rc = N.lib().dcg_refresh_basis(D.ctx(), D.stream(), ctypes.byref(cop), w_dev.data_ptr(), k, w_out.data_ptr(),
                                    aw_out.data_ptr(), chol.data_ptr(), ctypes.byref(kout), ctypes.byref(info))
     N.check(rc, info.value, "refresh_basis")
@@ -342,7 +342,7 @@ def solve_next_async(state, a, b, ax0=None, ax0_of=None):
     if kmax:
         w_out, aw_out, chol = D.empty(n, kmax), D.empty(n, kmax), D.empty(kmax, kmax)
         kdev = torch.empty(1, dtype=torch.int64, device=D.device())
-        cop = op.c_struct()
+        cop = op.c_struct(block_k=kmax) if isinstance(op, DenseOperator) else op.c_struct()
         if isinstance(pending, _PendingBasis):
             pending.join(main)
             pending.keep_alive = None   # main-stream work is now ordered after the extraction

@@ -397,9 +397,12 @@ def test_packed_share_built_from_points_is_the_gram(P, rng, n, world):
 
     x = rng.standard_normal((n, 6))
     params = P.KernelParams(1.3, 1.1)
-    gram = P.rbf_kernel(dev(x), params).with_strategy("sym")
-    gram.c_struct()   # builds the packed copy
-    full = gram._packed.buf
+    from paper_1706_00241_b200 import _device as D
+    from paper_1706_00241_b200 import _native as N
+
+    gram = P.rbf_kernel(dev(x), params)
+    full = D.empty(int(N.lib().dcg_packed_sym_doubles(n)))   # pack_sym of the row-major Gram
+    N.check(N.lib().dcg_pack_sym(D.ctx(), D.stream(), gram.kbuf.data_ptr(), gram.ldk, n, full.data_ptr()))
 
     class C:
         def __init__(self, rank, world):

@@ -143,3 +143,41 @@ def test_symmetric_block_product(P, n, k):
         assert np.all(np.abs(y_sym - ref) <= 64 * np.finfo(float).eps * scale)
         assert np.all(np.abs(y_sym - y_rows) <= 64 * np.finfo(float).eps * scale)
         assert np.array_equal(y_sym, A @ w)   # deterministic (units are drawn dynamically)
+
+
+@pytest.mark.parametrize("n", [4096, 5000])
+def test_rbf_kernel_packed_only(P, n):
+    """rbf_kernel above SYM_MIN_N keeps only the packed tiles (built from X):
+    they equal pack_sym of the row-major Gram, which is built only when asked
+    for (here by .kbuf) and equals the direct builder; products, a solve and a
+    k = 24 block product (which needs the rows) agree bitwise with an operator
+    that has both copies."""
+    import torch
+
+    from paper_1706_00241_b200 import _device as D
+    from paper_1706_00241_b200 import _native as N
+
+    rng = np.random.default_rng(n)
+    x = torch.from_numpy(rng.standard_normal((n, 6))).cuda()
+    params = P.KernelParams(1.0, 1.3)
+    g = P.rbf_kernel(x, params)
+    assert g._packed.buf is not None and not g._rm.ready
+    v = torch.from_numpy(rng.standard_normal(n)).cuda()
+    s = torch.from_numpy(rng.uniform(0.2, 0.6, n)).cuda()
+    A = g.scaled(s, 1.0)
+    y_packed_only = A.matvec_dev(v).clone()
+    w16 = torch.from_numpy(rng.standard_normal((n, 16))).cuda()
+    yb16 = A.apply_block_dev(w16).clone()
+    assert not g._rm.ready                      # nothing above needed the rows
+    kbuf = g.kbuf                               # materialise
+    ref = P.operators.DenseOperator.from_matrix(kbuf[:, :n].contiguous())
+    full = D.empty(int(N.lib().dcg_packed_sym_doubles(n)))
+    N.check(N.lib().dcg_pack_sym(D.ctx(), D.stream(), kbuf.data_ptr(), g.ldk, n, full.data_ptr()))
+    assert torch.equal(full, g._packed.buf)
+    assert torch.equal(ref.scaled(s, 1.0).matvec_dev(v), y_packed_only)
+    assert torch.equal(ref.scaled(s, 1.0).apply_block_dev(w16), yb16)
+    w24 = torch.from_numpy(rng.standard_normal((n, 24))).cuda()
+    g2 = P.rbf_kernel(x, params)
+    y24 = g2.scaled(s, 1.0).apply_block_dev(w24)   # k = 24: row-major product, materialised on demand
+    assert g2._rm.ready
+    assert torch.equal(y24, ref.scaled(s, 1.0).apply_block_dev(w24))
