@@ -139,9 +139,33 @@ extern "C" int dcg_context_create(int device, dcg_context** out) {
     return DCG_OK;
 }
 
+const long long* dcg_sym_table(dcg_context* ctx, cudaStream_t st, long long n, int G) {
+    for (auto& e : ctx->symtbl)
+        if (e.d && e.n == n && e.G == G) return e.d;
+    auto& e = ctx->symtbl[ctx->symtbl_next];
+    ctx->symtbl_next = (ctx->symtbl_next + 1) % 4;
+    if (!e.d) {
+        if (cudaMalloc(&e.d, sizeof(long long) * (DCG_SYM_MAX_CTAS + 2)) != cudaSuccess) return nullptr;
+        if (cudaHostAlloc(&e.h, sizeof(long long) * (DCG_SYM_MAX_CTAS + 2), cudaHostAllocDefault) != cudaSuccess)
+            return nullptr;
+    } else {
+        cudaStreamSynchronize(st);   // the staging copy of the entry being replaced may still be in flight
+    }
+    for (int b = 0; b <= G; ++b) e.h[b] = sym_tile_begin(n, G, b);
+    if (cudaMemcpyAsync(e.d, e.h, sizeof(long long) * (G + 1), cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return nullptr;
+    e.n = n;
+    e.G = G;
+    return e.d;
+}
+
 extern "C" int dcg_context_destroy(dcg_context* ctx) {
     if (!ctx) return DCG_OK;
     cudaDeviceSynchronize();
+    for (auto& e : ctx->symtbl) {
+        if (e.d) cudaFree(e.d);
+        if (e.h) cudaFreeHost(e.h);
+    }
     if (ctx->ws) cudaFree(ctx->ws);
     if (ctx->ws2) cudaFree(ctx->ws2);
     if (ctx->host) cudaFreeHost(ctx->host);

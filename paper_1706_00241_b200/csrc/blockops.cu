@@ -95,12 +95,18 @@ template <bool PK>
 __global__ void __launch_bounds__(DCG_NT, 1)
     sym_apply_coop_kernel(const double* __restrict__ K, long long ldk, long long n, const double* v,
                           const double* s_in, const double* s_out, double shift, double* colpart, double* rowpart,
-                          double* y, unsigned int* bar) {
+                          double* y, unsigned int* bar, unsigned long long* ts, const long long* gtbl) {
     extern __shared__ __align__(16) double smem[];
-    sym_ring_init(smem, n, PK);
+#define APPLY_TS(i) \
+    if (ts && threadIdx.x == 0) ts[blockIdx.x * 5 + (i)] = globaltimer_ns()
+    APPLY_TS(0);
+    sym_ring_init(smem, n, PK, gtbl);
+    APPLY_TS(1);
     unsigned int seq = 0;
     sym_pass1<false, 1, PK>(K, ldk, n, v, s_in, colpart, rowpart, smem, seq);
+    APPLY_TS(2);
     dcg_grid_barrier(bar, gridDim.x);
+    APPLY_TS(3);
     const long long q0 = sym_row_begin(n, gridDim.x, blockIdx.x);
     const long long q1 = sym_row_begin(n, gridDim.x, blockIdx.x + 1);
     sym_pass2<true>(n, colpart, rowpart, q0, q1, sym_range_table(smem), gridDim.x, smem, [&](long long i, double t) {
@@ -108,6 +114,18 @@ __global__ void __launch_bounds__(DCG_NT, 1)
         if (shift != 0.0) val = add_rn(mul_rn(shift, v[i]), val);
         y[i] = val;
     });
+    APPLY_TS(4);
+#undef APPLY_TS
+}
+
+// DCG_APPLY_TIMERS=1 (developer diagnostic): per-CTA globaltimer stamps of the
+// last standalone symmetric product (start, after the ring set-up, after pass
+// 1, after the grid barrier, end), 5 per CTA.
+static unsigned long long* g_apply_ts = nullptr;
+extern "C" __attribute__((visibility("default"))) int dcg_debug_apply_timers(unsigned long long* out, int nslots) {
+    if (!g_apply_ts || !out || nslots < 0 || nslots > 5 * 256) return DCG_E_CONFIG;
+    DCG_CUDA(cudaMemcpy(out, g_apply_ts, (size_t)nslots * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    return DCG_OK;
 }
 
 __global__ void __launch_bounds__(DCG_NT, 1)
@@ -153,8 +171,15 @@ int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, const doub
     else DCG_SMEM_ATTR(sym_apply_coop_kernel<false>, smem);
     DCG_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), st));
     const double* Ksrc = Kp ? Kp : K;
+    const long long* gtbl = dcg_sym_table(ctx, st, n, G);
+    if (!gtbl) return DCG_E_CUDA;
+    unsigned long long* ts = nullptr;
+    if (getenv("DCG_APPLY_TIMERS")) {
+        if (!g_apply_ts) DCG_CUDA(cudaMalloc(&g_apply_ts, 5 * 256 * sizeof(unsigned long long)));
+        ts = g_apply_ts;
+    }
     void* args[] = {(void*)&Ksrc, (void*)&ldk, (void*)&n, (void*)&v, (void*)&s_in, (void*)&s_out, (void*)&shift,
-                    (void*)&colpart, (void*)&rowpart, (void*)&y, (void*)&bar};
+                    (void*)&colpart, (void*)&rowpart, (void*)&y, (void*)&bar, (void*)&ts, (void*)&gtbl};
     DCG_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(DCG_NT), args, smem, st));
     dcg_count_launch();
     return DCG_OK;
@@ -170,9 +195,9 @@ __global__ void __launch_bounds__(DCG_NT, 1)
     sym_apply2_coop_kernel(const double* __restrict__ K, long long ldk, long long n, const double* x1,
                            const double* x2, const double* v1, const double* v2, const double* s_out1,
                            const double* s_out2, double shift1, double shift2, double* colpart, double* rowpart,
-                           long long part2, double* y1, double* y2, unsigned int* bar) {
+                           long long part2, double* y1, double* y2, unsigned int* bar, const long long* gtbl) {
     extern __shared__ __align__(16) double smem[];
-    sym_ring_init(smem, n, PK);
+    sym_ring_init(smem, n, PK, gtbl);
     unsigned int seq = 0;
     // (no L2 cache hints on the row-major copies of the standalone products: a
     // cp.async with a cache hint faulted here as an illegal instruction on sm_100a)
@@ -215,10 +240,12 @@ int dcg_sym_apply2(dcg_context* ctx, cudaStream_t st, const double* K, const dou
     else DCG_SMEM_ATTR(sym_apply2_coop_kernel<false>, smem);
     DCG_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), st));
     const double* Ksrc = Kp ? Kp : K;
+    const long long* gtbl = dcg_sym_table(ctx, st, n, G);
+    if (!gtbl) return DCG_E_CUDA;
     void* args[] = {(void*)&Ksrc,      (void*)&ldk,    (void*)&n,      (void*)&x1,      (void*)&x2,
                     (void*)&v1,     (void*)&v2,     (void*)&s_out1, (void*)&s_out2,  (void*)&shift1,
                     (void*)&shift2, (void*)&colpart, (void*)&rowpart, (void*)&part2, (void*)&y1,
-                    (void*)&y2,     (void*)&bar};
+                    (void*)&y2,     (void*)&bar,    (void*)&gtbl};
     DCG_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(DCG_NT), args, smem, st));
     dcg_count_launch();
     return DCG_OK;

@@ -38,7 +38,20 @@ struct dcg_context {
     size_t host_bytes;
     cudaEvent_t ev0, ev1;
     long long* d_res;        // result block of the synchronous Ritz extraction
+    // pass-1 range tables of the symmetric GEMV, computed on the host once per
+    // (n, G) and kept on the device (dcg_sym_table)
+    struct SymTable {
+        long long n;
+        int G;
+        long long* d;        // G + 1 first tiles, device
+        long long* h;        // pinned staging copy (kept alive with d)
+    } symtbl[4];
+    int symtbl_next;
 };
+
+// device copy of the stored-Gram pass-1 range table tbl[b] = first tile of
+// CTA b of G (sym_tile_begin), cached per context
+const long long* dcg_sym_table(dcg_context* ctx, cudaStream_t st, long long n, int G);
 
 // ---- status plumbing --------------------------------------------------------
 // Device-side status block written by single-CTA / persistent kernels.

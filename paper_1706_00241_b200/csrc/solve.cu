@@ -67,6 +67,7 @@ struct SolveArgs {
     unsigned int* bar;  // grid barrier arrival counter (zeroed per launch)
     unsigned long long* timers;   // optional per-phase ns accumulators (CTA 0, thread 0)
     RbfMma rbf;                   // matrix-free operator (STRAT_RBF)
+    const long long* symtbl;      // symmetric strategies: host-computed pass-1 range table (dcg_sym_table)
 };
 
 // mu = L^-T L^-1 c for the k x k row-major lower factor of W'AW in shared
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
     // therefore read by other CTAs after a grid barrier, through L2.
     long long q0 = r0, q1 = r1;
     if constexpr (kSym) {
-        sym_ring_init(s_g, n, kPk);
+        sym_ring_init(s_g, n, kPk, a.symtbl);
         q0 = sym_row_begin(n, G, blockIdx.x);
         q1 = sym_row_begin(n, G, blockIdx.x + 1);
     }
@@ -625,6 +626,7 @@ static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, co
     SolveArgs a;
     memset(&a, 0, sizeof(a));
     a.K = op->d_k;
+    a.symtbl = nullptr;
     a.Kp = strat == STRAT_SYMPK ? op->d_kp : nullptr;
     a.ldk = op->ldk;
     a.n = n;
@@ -681,6 +683,10 @@ static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, co
         if (rc) return rc;
     } else {
         memset(&a.rbf, 0, sizeof(a.rbf));
+    }
+    if (strat == STRAT_SYM || strat == STRAT_SYMPK) {
+        a.symtbl = dcg_sym_table(ctx, st, n, G);
+        if (!a.symtbl) return DCG_E_CUDA;
     }
     DCG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     DCG_CUDA(cudaMemsetAsync(a.st, 0, sizeof(DevStatus), st));

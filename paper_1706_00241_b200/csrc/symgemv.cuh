@@ -297,12 +297,16 @@ __device__ __forceinline__ double sym_xval(const double* v, const double* s, lon
 // the tile's bulk copy (one arrival), threads 0..63 copy the v / s slices
 // and arrive (64 arrivals).
 #define DCG_SYM_PK_ARRIVALS 65
-__device__ __forceinline__ void sym_ring_init(double* smem, long long n, bool packed = false) {
+// gtbl (optional): the range table precomputed on the host (dcg_sym_table)
+__device__ __forceinline__ void sym_ring_init(double* smem, long long n, bool packed = false,
+                                              const long long* gtbl = nullptr) {
     unsigned long long* full = reinterpret_cast<unsigned long long*>(
         smem + DCG_SYM_STAGES * DCG_SYM_STAGE_DOUBLES + 2 * DCG_NW * DCG_TB);
     unsigned long long* empty = full + DCG_SYM_STAGES;
-    // finite stage contents from the start (edge tiles leave slots uncopied)
-    for (int e = threadIdx.x; e < DCG_SYM_STAGES * DCG_SYM_STAGE_DOUBLES; e += blockDim.x) smem[e] = 0.0;
+    // finite stage contents from the start (row-major edge tiles leave slots
+    // uncopied; packed tiles and their slices are always copied whole)
+    if (!packed)
+        for (int e = threadIdx.x; e < DCG_SYM_STAGES * DCG_SYM_STAGE_DOUBLES; e += blockDim.x) smem[e] = 0.0;
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int st = 0; st < DCG_SYM_STAGES; ++st) {
@@ -311,7 +315,13 @@ __device__ __forceinline__ void sym_ring_init(double* smem, long long n, bool pa
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    sym_fill_range_table(sym_range_table(smem), n);
+    if (gtbl) {
+        long long* tbl = sym_range_table(smem);
+        for (int b = threadIdx.x; b <= (int)gridDim.x; b += blockDim.x) tbl[b] = __ldg(gtbl + b);
+        cta_sync();
+    } else {
+        sym_fill_range_table(sym_range_table(smem), n);
+    }
 }
 
 // Packed storage, threads 0..63: the slices v_J, s_J of a tile into its stage
