@@ -158,3 +158,30 @@ def test_fused_newton_system_matches_separate_products(P, n, strategy):
     s = plain.sqrt_h
     assert torch.allclose(fused.ax0, x_prev + s * (kd @ (s * x_prev)), rtol=1e-12, atol=1e-11)
     assert torch.allclose(fused.b, s * (kd @ plain.inner), rtol=1e-12, atol=1e-11)
+
+
+def test_interleaved_pipelined_sequences(P):
+    """Two pipelined sequences advanced alternately (each one's extraction
+    tail still pending when the other enqueues its own into the shared slot-1
+    workspace): every solve equals the same sequence run alone, bitwise."""
+    sa = gpc_like_sequence(P, 900, 5, seed=1)
+    sb = gpc_like_sequence(P, 700, 5, seed=2)
+    cfg = P.SolverConfig(tol=1e-8, ell=12)
+    xa_ref, ita_ref = run_pipelined(P, sa, 8, cfg)
+    xb_ref, itb_ref = run_pipelined(P, sb, 8, cfg)
+    st_a = P.SequenceState(k=8, cfg=cfg, selection="largest")
+    st_b = P.SequenceState(k=8, cfg=cfg, selection="largest")
+    xa, xb, ita, itb = [], [], [], []
+    for (a1, b1), (a2, b2) in zip(sa, sb):
+        _, ja = P.recycle.solve_next_async(st_a, a1, b1)
+        _, jb = P.recycle.solve_next_async(st_b, a2, b2)   # enqueued before A's job finishes
+        x1, st_a = ja.finish()
+        x2, st_b = jb.finish()
+        xa.append(x1.clone())
+        xb.append(x2.clone())
+        ita.append(st_a.history[-1].iterations)
+        itb.append(st_b.history[-1].iterations)
+    _ = st_a.basis, st_b.basis
+    assert ita == ita_ref and itb == itb_ref
+    for u, v in zip(xa + xb, xa_ref + xb_ref):
+        assert torch.equal(u, v)
