@@ -30,7 +30,7 @@ from . import _device as D
 from . import _native as N
 from .errors import DimensionMismatch, InvalidLabel, NoProgress, NotPositiveDefinite, StateInconsistent
 from .operators import SYM_MIN_N, DenseOperator, RbfOperator, _RowMajor, as_operator
-from .recycle import SELECT_LARGEST, SequenceState, _pinned, _pinned_pool, solve_next, solve_next_async
+from .recycle import SELECT_LARGEST, SequenceState, _pinned, _pinned_pool, prepare_refresh, solve_next, solve_next_async
 from .solvers import SolverConfig, _solve_dev
 
 SOLVER_CHOLESKY = "cholesky"
@@ -363,12 +363,17 @@ def _laplace_newton_pipelined(state, psi_prev, cfg, newton_tol, max_newton, k, s
     records = []
     seq = SequenceState(k=k, cfg=cfg, selection=selection)
     system = build_newton_system(state)
+    prepared = None
     for it in range(1, max_newton + 1):
         t0 = time.perf_counter()
-        x, job = solve_next_async(seq, system.a_matrix, system.b, ax0=system.ax0, ax0_of=system.x_prev)
+        x, job = solve_next_async(seq, system.a_matrix, system.b, ax0=system.ax0, ax0_of=system.x_prev,
+                                  prepared=prepared)
         new_state, objective = _update_dev_async(state, system.inner, system.sqrt_h, x)
         # the next system and its solve's first product A_next x in one K pass
         next_system = build_newton_system(new_state, x_prev=x) if it < max_newton else None
+        # ... and the next solve's refresh, enqueued while this solve still
+        # runs (dropped if the loop stops below)
+        prepared = prepare_refresh(job, next_system.a_matrix) if next_system is not None else None
         x, seq = job.finish()
         dt = time.perf_counter() - t0
         report = seq.history[-1]

@@ -303,34 +303,24 @@ class _AsyncSolve:
         return self.x, replace(st, basis=self.pending, x_last=self.x, history=st.history + [rep])
 
 
-def solve_next_async(state, a, b, ax0=None, ax0_of=None):
-    """Enqueue refresh + solve of the next system of a sequence and the
-    extraction of the basis after it (device data only, nothing waits).
-    Returns (x, job); job.finish() completes the report and the new state.
-    ``ax0`` = a @ ax0_of, precomputed by the caller (gpc's fused system
-    build), stands in for the warm start's first product when ``ax0_of`` is
-    the sequence's last solution."""
-    op = as_operator(a)
-    bd = D.to_dev(b, 1)
-    n = bd.shape[0]
-    if op.n != n:
-        raise DimensionMismatch(f"system shapes {op.shape}, {tuple(bd.shape)}")
-    if state.selection not in (SELECT_SMALLEST, SELECT_LARGEST):
-        raise ValueError(f"unknown selection {state.selection!r}")
-    x_prev = D.zeros(n) if state.x_last is None else D.to_dev(state.x_last, 1)
-    t0 = time.perf_counter()
-    main = torch.cuda.current_stream()
-    pending = object.__getattribute__(state, "basis")
+class _PreparedRefresh:
+    """The refresh of the next solve (recycle.py:80-92 with the BasisDeficient
+    rule of solve_next, recycle.py:178-179), enqueued ahead of time by
+    prepare_refresh: the pending extraction's tail, A_next W_next, the pruned
+    Gram factor.  solve_next_async uses it when it is handed the same basis
+    object and the same operator."""
+
+    def __init__(self, basis_obj, op, kmax, cb, kdev, bufs, valid):
+        self.basis_obj, self.op, self.kmax, self.cb, self.kdev, self.bufs = basis_obj, op, kmax, cb, kdev, bufs
+        self.valid = valid
+
+
+def _enqueue_refresh(pending, op, n, main):
+    """Refresh of the basis `pending` (a _PendingBasis, a RecycleBasis or None)
+    for `op`, enqueued on `main`; returns (kmax, cb, kdev, bufs, valid), valid
+    the pending extraction's device result block (or None)."""
     w_src, valid = None, None
-    if ax0 is not None and (ax0_of is None or ax0_of is not state.x_last):
-        ax0 = None
     if isinstance(pending, _PendingBasis):
-        # the warm start's first product A x_prev needs no basis: it runs
-        # while the extraction of the basis is still going on
-        if ax0 is None:
-            ax0 = op.matvec_dev(x_prev)
-        # (joined right before the refresh launch below: the host-side set-up
-        # of the refresh then overlaps the device's work instead of idling it)
         w_src, valid = pending.w_next, pending.result
     elif pending is not None and pending.k > 0:
         w_src = pending.w_dev
@@ -346,13 +336,60 @@ def solve_next_async(state, a, b, ax0=None, ax0_of=None):
         if isinstance(pending, _PendingBasis):
             pending.join(main)
             pending.keep_alive = None   # main-stream work is now ordered after the extraction
-        N.check(N.lib().dcg_refresh_basis_async(D.ctx(), D.stream(), ctypes.byref(cop), w_src.data_ptr(),
+        N.check(N.lib().dcg_refresh_basis_async(D.ctx(), main.cuda_stream, ctypes.byref(cop), w_src.data_ptr(),
                                                 kmax, valid.data_ptr() if valid is not None else None,
                                                 w_out.data_ptr(), aw_out.data_ptr(), chol.data_ptr(),
                                                 kdev.data_ptr()), what="refresh_basis_async")
         cb = N.CBasis()
         cb.k, cb.d_w, cb.d_aw, cb.d_chol = kmax, w_out.data_ptr(), aw_out.data_ptr(), chol.data_ptr()
         bufs = (w_out, aw_out, chol, kdev, w_src)
+    return kmax, cb, kdev, bufs, valid
+
+
+def prepare_refresh(job, a_next):
+    """Enqueue, right behind `job`'s work, the refresh the NEXT solve of the
+    sequence will use (its basis is the extraction `job` enqueued): the host
+    does this while the device is still busy with `job`'s solve, so the
+    refresh's launches never wait for the host.  Hand the result to the next
+    solve_next_async(..., prepared=...); unused (the sequence stopped) it is
+    simply dropped."""
+    op = as_operator(a_next)
+    return _PreparedRefresh(job.pending, op, *_enqueue_refresh(job.pending, op, op.n, torch.cuda.current_stream()))
+
+
+def solve_next_async(state, a, b, ax0=None, ax0_of=None, prepared=None):
+    """Enqueue refresh + solve of the next system of a sequence and the
+    extraction of the basis after it (device data only, nothing waits).
+    Returns (x, job); job.finish() completes the report and the new state.
+    ``ax0`` = a @ ax0_of, precomputed by the caller (gpc's fused system
+    build), stands in for the warm start's first product when ``ax0_of`` is
+    the sequence's last solution.  ``prepared``: the refresh enqueued ahead by
+    prepare_refresh (used when it matches this state's basis and operator)."""
+    op = as_operator(a)
+    bd = D.to_dev(b, 1)
+    n = bd.shape[0]
+    if op.n != n:
+        raise DimensionMismatch(f"system shapes {op.shape}, {tuple(bd.shape)}")
+    if state.selection not in (SELECT_SMALLEST, SELECT_LARGEST):
+        raise ValueError(f"unknown selection {state.selection!r}")
+    x_prev = D.zeros(n) if state.x_last is None else D.to_dev(state.x_last, 1)
+    t0 = time.perf_counter()
+    main = torch.cuda.current_stream()
+    pending = object.__getattribute__(state, "basis")
+    if ax0 is not None and (ax0_of is None or ax0_of is not state.x_last):
+        ax0 = None
+    if isinstance(pending, _PendingBasis) and ax0 is None and (prepared is None or prepared.basis_obj is not pending):
+        # the warm start's first product A x_prev needs no basis: it runs
+        # while the extraction of the basis is still going on
+        ax0 = op.matvec_dev(x_prev)
+    if prepared is not None and prepared.basis_obj is pending and prepared.op is op:
+        kmax, cb, kdev, bufs, valid = prepared.kmax, prepared.cb, prepared.kdev, prepared.bufs, prepared.valid
+        if ax0 is None and isinstance(pending, _PendingBasis):
+            ax0 = op.matvec_dev(x_prev)
+    else:
+        # (the pending extraction is joined right before the refresh launch:
+        # the host-side set-up of the refresh then overlaps the device's work)
+        kmax, cb, kdev, bufs, valid = _enqueue_refresh(pending, op, n, main)
     cfg = state.cfg
     log = KrylovLog(n, cfg.ell, kmax)
     max_iters = 10 * n if cfg.max_iters is None else cfg.max_iters

@@ -23,7 +23,7 @@ def main():
     from torch.profiler import ProfilerActivity, profile
 
     import paper_1706_00241_b200 as P
-    from oracle.defcg_oracle import gpc_inputs
+    from paper_1706_00241_b200.workloads import gpc_inputs
 
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 10000
     out = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/timeline.json"
