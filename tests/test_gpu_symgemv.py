@@ -181,3 +181,32 @@ def test_rbf_kernel_packed_only(P, n):
     y24 = g2.scaled(s, 1.0).apply_block_dev(w24)   # k = 24: row-major product, materialised on demand
     assert g2._rm.ready
     assert torch.equal(y24, ref.scaled(s, 1.0).apply_block_dev(w24))
+
+
+def test_packed_solve_early_exits(P):
+    """The packed-tile solve's early exits with bulk copies of the next pass in
+    flight (drained before the kernel returns): breakdown on an indefinite
+    operator (solvers.py:170-172) and a zero right-hand side after a
+    warm-start product (solvers.py:142-147), n = 4500 (symmetric strategy)."""
+    import torch
+
+    n = 4500
+    rng = np.random.default_rng(5)
+    x = torch.from_numpy(rng.standard_normal((n, 6))).cuda()
+    g = P.rbf_kernel(x, P.KernelParams(1.0, 1.4))
+    assert g.c_struct().d_kp
+    a = g.scaled(None, -0.5)            # K - 0.5 I: indefinite
+    b = torch.from_numpy(rng.standard_normal(n)).cuda()
+    with pytest.raises(P.BreakdownZeroCurvature):
+        P.cg_solve(a, b, None, P.SolverConfig(tol=1e-10))
+    spd = g.scaled(None, 1.0)
+    w = torch.from_numpy(rng.standard_normal((n, 6))).cuda()
+    basis = P.refresh_basis(spd, w)
+    xs, rep, _ = P.deflated_cg_solve(spd, torch.zeros(n, dtype=torch.float64, device="cuda"),
+                                     torch.from_numpy(rng.standard_normal(n)).cuda(), basis,
+                                     P.SolverConfig(tol=1e-10, ell=8))
+    assert rep.iterations == 0 and rep.residual_history == [0.0]
+    assert not bool(torch.any(xs != 0))
+    # and the library is still healthy afterwards
+    xs, rep, _ = P.cg_solve(spd, b, None, P.SolverConfig(tol=1e-10))
+    assert rep.converged
