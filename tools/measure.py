@@ -229,6 +229,36 @@ def config5_slab(n=200000, d=16, ell=3.0, k=32, world=8):
     return out
 
 
+def config5_sequence(n=200000, steps=8, d=16, ell=3.0, k=32, ell_log=36):
+    """BASELINE config 5 at one GPU: the GPC Newton sequence on the matrix-free
+    RBF operator (K regenerated tile by tile in every product; the 320 GB
+    Gram is never stored), def-CG with k = 32, one timed sequence (CUDA
+    events) after the operand set-up."""
+    import torch
+
+    import paper_1706_00241_b200 as P
+    from paper_1706_00241_b200.workloads import gpc_inputs
+
+    x, y = gpc_inputs(n, d, 0)
+    op = P.rbf_kernel(torch.from_numpy(x).cuda(), P.KernelParams(1.0, ell), matrix_free=True)
+    yd = torch.from_numpy(y).cuda()
+    cfg = P.SolverConfig(tol=1e-8, ell=ell_log)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    _, recs = P.laplace_newton(op, yd, "defcg", cfg, newton_tol=-np.inf, max_newton=steps, k=k, selection="largest")
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    its = [r.solver_iterations for r in recs]
+    pairs = n * (n + 1) / 2
+    return {"n": n, "d": d, "lengthscale": ell, "k": k, "ell_log": ell_log, "newton_steps": steps,
+            "iterations": its, "sequence_ms": ms, "iters_per_s": sum(its) / (ms / 1e3),
+            "psi": [r.psi for r in recs], "wall_s": time.perf_counter() - t0,
+            "pairs_per_product": pairs, "note": "matrix-free (Gram never stored), one GPU, CUDA events"}
+
+
 def main():
     what = sys.argv[1]
     if what == "config1":
@@ -252,6 +282,10 @@ def main():
     elif what == "config5":
         n = int(sys.argv[2]) if len(sys.argv) > 2 else 50000
         out = config5(n)
+    elif what == "config5-seq":
+        n = int(sys.argv[2]) if len(sys.argv) > 2 else 200000
+        steps = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+        out = config5_sequence(n, steps)
     else:
         raise SystemExit(__doc__)
     out["workload"] = what
