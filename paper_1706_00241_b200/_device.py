@@ -13,10 +13,23 @@ F64 = torch.float64
 LD_ALIGN = 32  # row pitch of device matrices in doubles (256 B)
 
 
+_cuda_ok: bool | None = None
+_devices: dict[int, torch.device] = {}
+
+
 def device() -> torch.device:
-    if not torch.cuda.is_available():
+    """The current CUDA device (availability checked once per process: this
+    sits on the host path of every enqueued step)."""
+    global _cuda_ok
+    if _cuda_ok is None:
+        _cuda_ok = torch.cuda.is_available()
+    if not _cuda_ok:
         raise DeviceError("no CUDA device: the def-CG B200 path has no CPU fallback")
-    return torch.device("cuda", torch.cuda.current_device())
+    idx = torch.cuda.current_device()
+    d = _devices.get(idx)
+    if d is None:
+        d = _devices[idx] = torch.device("cuda", idx)
+    return d
 
 
 def ctx(slot: int = 0) -> int:

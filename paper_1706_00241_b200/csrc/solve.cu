@@ -688,10 +688,13 @@ static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, co
         a.symtbl = dcg_sym_table(ctx, st, n, G);
         if (!a.symtbl) return DCG_E_CUDA;
     }
-    DCG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    DCG_CUDA(cudaMemsetAsync(a.st, 0, sizeof(DevStatus), st));
+    if (strat == STRAT_RBF) DCG_SMEM_ATTR(dcg_solve_kernel<STRAT_RBF>, smem);
+    else if (strat == STRAT_SYMPK) DCG_SMEM_ATTR(dcg_solve_kernel<STRAT_SYMPK>, smem);
+    else if (strat == STRAT_SYM) DCG_SMEM_ATTR(dcg_solve_kernel<STRAT_SYM>, smem);
+    else DCG_SMEM_ATTR(dcg_solve_kernel<STRAT_ROWS>, smem);
+    // the status block and the barrier words share one 256-byte line: one memset
     a.bar = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(a.st) + 128);   // inside the st line
-    DCG_CUDA(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned int), st));
+    DCG_CUDA(cudaMemsetAsync(a.st, 0, 128 + 2 * sizeof(unsigned int), st));
     // DCG_PHASE_TIMERS=1: per-phase device time of CTA 0 printed per solve
     // (developer diagnostic; costs one predicated branch per phase otherwise).
     unsigned long long*& d_timers = g_phase_timers;
@@ -703,7 +706,7 @@ static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, co
         a.timers = d_timers;
     }
     void* args[] = {&a};
-    DCG_CUDA(cudaEventRecord(ctx->ev0, st));
+    if (!d_status) DCG_CUDA(cudaEventRecord(ctx->ev0, st));   // synchronous form: device_ms
     DCG_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(DCG_NT), args, smem, st));
     dcg_count_launch();
     if (d_status) {

@@ -248,7 +248,8 @@ class _AsyncSolve:
     and a prefix of the residual history come back on the copy stream as soon
     as the solve ends, whatever the compute streams do next."""
 
-    def __init__(self, state, x, log, hist, status, basis, event, ev_end, t0, cfg, pending, consumed=None):
+    def __init__(self, state, x, log, hist, status, basis, event, ev_end, t0, cfg, pending, consumed=None,
+                 combined=None):
         self.state, self.x, self.log, self.hist, self.status = state, x, log, hist, status
         self.basis, self.event, self.t0, self.cfg, self.pending = basis, event, t0, cfg, pending
         self.ev_end = ev_end
@@ -261,8 +262,14 @@ class _AsyncSolve:
         self.host = _pinned(_STATUS_WORDS + _HIST_PREFIX + 2)
         npre = min(_HIST_PREFIX, hist.shape[0])
         with torch.cuda.stream(cs):
-            self.host[:_STATUS_WORDS].copy_(status, non_blocking=True)
-            self.host[_STATUS_WORDS:_STATUS_WORDS + npre].view(torch.float64).copy_(hist[:npre], non_blocking=True)
+            if combined is not None:
+                # status words and history in one device buffer: one copy
+                self.host[:_STATUS_WORDS + npre].view(torch.float64).copy_(combined[:_STATUS_WORDS + npre],
+                                                                           non_blocking=True)
+            else:
+                self.host[:_STATUS_WORDS].copy_(status, non_blocking=True)
+                self.host[_STATUS_WORDS:_STATUS_WORDS + npre].view(torch.float64).copy_(hist[:npre],
+                                                                                        non_blocking=True)
             if consumed is not None:
                 self.host[_STATUS_WORDS + _HIST_PREFIX:_STATUS_WORDS + _HIST_PREFIX + 2].copy_(consumed[:2],
                                                                                             non_blocking=True)
@@ -393,9 +400,10 @@ def solve_next_async(state, a, b, ax0=None, ax0_of=None, prepared=None):
     cfg = state.cfg
     log = KrylovLog(n, cfg.ell, kmax)
     max_iters = 10 * n if cfg.max_iters is None else cfg.max_iters
-    hist = D.empty(max_iters + 1)
+    sh = D.empty(_STATUS_WORDS + max_iters + 1)   # status words, then the residual history
+    status = sh[:_STATUS_WORDS].view(torch.int64)
+    hist = sh[_STATUS_WORDS:]
     x = D.empty(n)
-    status = torch.empty(_STATUS_WORDS, dtype=torch.int64, device=D.device())
     clog = log.c_struct()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev0.record()
@@ -448,7 +456,7 @@ def solve_next_async(state, a, b, ax0=None, ax0_of=None, prepared=None):
 
         nxt = _PendingBasis(event, result, w_next, aw_next, (log, bufs, theta, status), tail)
         _slot1_owner[D.device().index] = nxt
-    job = _AsyncSolve(state, x, log, hist, status, bufs, ev0, ev_end, t0, cfg, nxt, consumed=valid)
+    job = _AsyncSolve(state, x, log, hist, status, bufs, ev0, ev_end, t0, cfg, nxt, consumed=valid, combined=sh)
     job.hoisted = ax0 is not None   # A x_prev came from outside: the solve kernel skips that product
     return x, job
 
