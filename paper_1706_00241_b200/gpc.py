@@ -20,6 +20,7 @@ per step) is not repeated there; ``psi_objective`` still performs it.
 from __future__ import annotations
 
 import ctypes
+import gc
 import time
 from dataclasses import dataclass
 
@@ -352,6 +353,20 @@ def _update_dev_async(state, inner, s, x):
 
 
 def _laplace_newton_pipelined(state, psi_prev, cfg, newton_tol, max_newton, k, selection):
+    """(see _pipelined_loop) The host enqueues each step's device work while
+    the previous solve runs; a cyclic-garbage collection pass in the middle of
+    that (the loop allocates many short-lived objects) would stall the
+    enqueue, so automatic collection is paused for the loop."""
+    enabled = gc.isenabled()
+    gc.disable()
+    try:
+        return _pipelined_loop(state, psi_prev, cfg, newton_tol, max_newton, k, selection)
+    finally:
+        if enabled:
+            gc.enable()
+
+
+def _pipelined_loop(state, psi_prev, cfg, newton_tol, max_newton, k, selection):
     """The def-CG Newton loop with every host synchronisation off the device's
     critical path.  Per step the main stream runs refresh -> solve -> newton
     update -> next system back to back while the extraction of the next basis
@@ -367,7 +382,7 @@ def _laplace_newton_pipelined(state, psi_prev, cfg, newton_tol, max_newton, k, s
     for it in range(1, max_newton + 1):
         t0 = time.perf_counter()
         x, job = solve_next_async(seq, system.a_matrix, system.b, ax0=system.ax0, ax0_of=system.x_prev,
-                                  prepared=prepared)
+                                  prepared=prepared, extract=it < max_newton)
         new_state, objective = _update_dev_async(state, system.inner, system.sqrt_h, x)
         # the next system and its solve's first product A_next x in one K pass
         next_system = build_newton_system(new_state, x_prev=x) if it < max_newton else None

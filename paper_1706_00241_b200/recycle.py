@@ -364,14 +364,17 @@ def prepare_refresh(job, a_next):
     return _PreparedRefresh(job.pending, op, *_enqueue_refresh(job.pending, op, op.n, torch.cuda.current_stream()))
 
 
-def solve_next_async(state, a, b, ax0=None, ax0_of=None, prepared=None):
+def solve_next_async(state, a, b, ax0=None, ax0_of=None, prepared=None, extract=True):
     """Enqueue refresh + solve of the next system of a sequence and the
     extraction of the basis after it (device data only, nothing waits).
     Returns (x, job); job.finish() completes the report and the new state.
     ``ax0`` = a @ ax0_of, precomputed by the caller (gpc's fused system
     build), stands in for the warm start's first product when ``ax0_of`` is
     the sequence's last solution.  ``prepared``: the refresh enqueued ahead by
-    prepare_refresh (used when it matches this state's basis and operator)."""
+    prepare_refresh (used when it matches this state's basis and operator).
+    ``extract=False``: the caller will not solve another system of the
+    sequence (gpc's last Newton step), so the next basis is not extracted;
+    the returned state then carries no basis."""
     op = as_operator(a)
     bd = D.to_dev(b, 1)
     n = bd.shape[0]
@@ -416,7 +419,7 @@ def solve_next_async(state, a, b, ax0=None, ax0_of=None, prepared=None):
     ev_end = torch.cuda.Event(enable_timing=True)
     ev_end.record()
     nxt = None
-    if state.k > 0:
+    if state.k > 0 and extract:
         # The next basis, extracted straight behind the solve (its sizes come
         # from the solve's status block on the device): the SM-wide column work
         # (Z / AZ, F, G) on the main stream, then the single-CTA pencil and
