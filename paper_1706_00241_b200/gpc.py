@@ -169,10 +169,26 @@ def rbf_cross_kernel(xa, xb, params):
     return D.out_like(out, xa)
 
 
+def _labels_dev(y):
+    """(fp64 labels on the device, validity flag on the device or None): the
+    flag of device labels is read by the caller after its next host sync."""
+    if isinstance(y, torch.Tensor):
+        yd = y.to(device=D.device())
+        if yd.ndim != 1:
+            raise InvalidLabel("labels must be a vector of -1/+1")
+        return yd.to(torch.float64).contiguous(), ((yd == 1) | (yd == -1)).all()
+    return check_labels(y), None
+
+
 def check_labels(y):
-    """gpc.py:135-139."""
-    yd = D.to_dev(y) if isinstance(y, torch.Tensor) else None
-    arr = y.detach().cpu().numpy() if yd is not None else np.asarray(y)
+    """gpc.py:135-139.  Device labels are checked on the device (one flag
+    read back), host labels on the host; returns fp64 labels on the device."""
+    if isinstance(y, torch.Tensor):
+        yd, ok = _labels_dev(y)
+        if not bool(ok):
+            raise InvalidLabel("labels must be a vector of -1/+1")
+        return yd
+    arr = np.asarray(y)
     if arr.ndim != 1 or not np.all(np.isin(arr, (-1, 1))):
         raise InvalidLabel("labels must be a vector of -1/+1")
     return D.to_dev(arr.astype(np.float64), 1)
@@ -253,7 +269,7 @@ def _as_flavour(state: GpcState, host: bool, k_matrix=None) -> GpcState:
 
 def _make_state_dev(k_matrix, y, f=None) -> GpcState:
     op = _kernel_op(k_matrix)
-    yd = check_labels(y)
+    yd, ok = _labels_dev(y)
     n = yd.shape[0]
     if f is None:
         fd, ad = D.zeros(n), D.zeros(n)
@@ -261,6 +277,8 @@ def _make_state_dev(k_matrix, y, f=None) -> GpcState:
         fd = D.to_dev(f, 1)
         ad = _dense_cholesky_solve(op, fd)
     ll, g, h = _derivs_dev(fd, yd)
+    if ok is not None and not bool(ok):   # computed before the derivatives' host read
+        raise InvalidLabel("labels must be a vector of -1/+1")
     return GpcState(f=fd, y=yd, k_matrix=op, a=ad, loglik=ll, grad_loglik=g, h=h, host=False)
 
 

@@ -138,6 +138,14 @@ def test_likelihood_derivs(P, rng):
     assert np.allclose(h2, ho2, rtol=1e-15, atol=1e-300)
     with pytest.raises(P.InvalidLabel):
         P.likelihood_derivs(np.zeros(2), np.array([0.0, 1.0]))
+    import torch
+
+    with pytest.raises(P.InvalidLabel):   # device labels are checked on the device
+        P.likelihood_derivs(torch.zeros(2, dtype=torch.float64).cuda(), torch.tensor([0.0, 1.0]).cuda())
+    with pytest.raises(P.InvalidLabel):
+        P.likelihood_derivs(torch.zeros(2, dtype=torch.float64).cuda(), torch.ones(2, 2).cuda())
+    ll3, g3, _ = P.likelihood_derivs(torch.from_numpy(f2).cuda(), torch.from_numpy(y2).int().cuda())
+    assert ll3 == ll2 and np.array_equal(g3.cpu().numpy(), g2)
 
 
 def test_newton_system_toy(P):
