@@ -477,7 +477,8 @@ def run_native(args, rank, world):
         d2h = fh.numel() * 8 + sum(r.f.nbytes for r in recs) + sum(8 * len(r.residual_history) for r in recs)
         return sum(r.solver_iterations for r in recs), d2h
 
-    e2e_once()
+    for _ in range(2):   # warm-up (first-use costs of the end-to-end path)
+        e2e_once()
     gc.collect()
     barrier()
     t0 = time.perf_counter()

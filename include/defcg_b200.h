@@ -291,6 +291,10 @@ DCG_API int dcg_ritz_extract_dev(dcg_context* ctx, void* stream, long long n,
 /* loglik, grad, h of the logistic likelihood          gpc.py:126-157          */
 DCG_API int dcg_gpc_derivs(dcg_context* ctx, void* stream, long long n, const double* d_f,
                    const double* d_y, double* d_grad, double* d_h, double* loglik);
+/* start state f = a = 0 with its derivatives and loglik, and the number of
+ * labels not in {-1, +1} (InvalidLabel)             gpc.py:135-172          */
+DCG_API int dcg_gpc_init(dcg_context* ctx, void* stream, long long n, const double* d_y, double* d_f,
+                 double* d_a, double* d_grad, double* d_h, double* loglik, long long* bad_labels);
 /* s = sqrt(h); inner = h f + grad; b = s * (K inner)   gpc.py:175-183          */
 DCG_API int dcg_gpc_newton_system(dcg_context* ctx, void* stream, const dcg_operator* kop,
                           const double* d_f, const double* d_grad, const double* d_h,

@@ -127,6 +127,7 @@ SIGNATURES = {
     "dcg_k_jacobi_sweep": [_P, _P, _P, _P, _LL, _PLL],
     "dcg_check_symmetric": [_P, _P, _P, _LL, _LL, _D, _PI],
     "dcg_packed_sym_doubles": [_LL],
+    "dcg_gpc_init": [_P, _P, _LL, _P, _P, _P, _P, _P, ctypes.POINTER(_D), _PLL],
     "dcg_block_uses_packed": [ctypes.c_int],
     "dcg_pack_sym": [_P, _P, _P, _LL, _LL, _P],
     "dcg_sym_eigen": [_P, _P, _P, _LL, _LL, _D, _P, _P, _PLL],

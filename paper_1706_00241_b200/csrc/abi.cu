@@ -754,11 +754,11 @@ extern "C" int dcg_gpc_derivs(dcg_context* ctx, void* stream, long long n, const
                               double* d_grad, double* d_h, double* loglik) {
     if (!ctx || n < 0) return DCG_E_CONFIG;
     cudaStream_t st = as_stream(stream);
-    const size_t need = al(sizeof(double) * 2 * ctx->sm_count * 2) + al(sizeof(DevStatus));
+    const size_t need = al(sizeof(double) * 3 * ctx->sm_count * 2) + al(sizeof(DevStatus));
     int rc = dcg_ws_reserve(ctx, need);
     if (rc) return rc;
     Arena ar{static_cast<char*>(ctx->ws), 0};
-    double* part = ar.take<double>(4 * ctx->sm_count);
+    double* part = ar.take<double>(6 * ctx->sm_count);
     DevStatus* ds = ar.take<DevStatus>(1);
     rc = dcg_derivs_launch(ctx, st, n, d_f, d_y, nullptr, d_grad, d_h, part, ds);
     if (rc) return rc;
@@ -769,15 +769,45 @@ extern "C" int dcg_gpc_derivs(dcg_context* ctx, void* stream, long long n, const
     return DCG_OK;
 }
 
+// Laplace-Newton start state (gpc.py:160-172, f = 0): f = a = 0, the
+// likelihood derivatives at f = 0 and loglik, plus the count of labels that
+// are not -1 / +1 (gpc.py:135-139) -- one launch pair and one host read.
+extern "C" int dcg_gpc_init(dcg_context* ctx, void* stream, long long n, const double* d_y, double* d_f, double* d_a,
+                            double* d_grad, double* d_h, double* loglik, long long* bad_labels) {
+    if (!ctx || n < 0 || (n > 0 && (!d_y || !d_f || !d_a || !d_grad || !d_h))) return DCG_E_CONFIG;
+    if (n == 0) {
+        if (loglik) *loglik = 0.0;
+        if (bad_labels) *bad_labels = 0;
+        return DCG_OK;
+    }
+    cudaStream_t st = as_stream(stream);
+    const size_t need = al(sizeof(double) * 3 * ctx->sm_count * 2) + al(sizeof(DevStatus));
+    int rc = dcg_ws_reserve(ctx, need);
+    if (rc) return rc;
+    Arena ar{static_cast<char*>(ctx->ws), 0};
+    double* part = ar.take<double>(6 * ctx->sm_count);
+    DevStatus* ds = ar.take<DevStatus>(1);
+    DCG_CUDA(cudaMemsetAsync(d_f, 0, sizeof(double) * (size_t)n, st));
+    DCG_CUDA(cudaMemsetAsync(d_a, 0, sizeof(double) * (size_t)n, st));
+    rc = dcg_derivs_launch(ctx, st, n, d_f, d_y, nullptr, d_grad, d_h, part, ds);
+    if (rc) return rc;
+    DevStatus hs;
+    rc = dcg_read_status(ctx, st, ds, &hs);
+    if (rc) return rc;
+    if (loglik) *loglik = hs.value;
+    if (bad_labels) *bad_labels = hs.info;
+    return DCG_OK;
+}
+
 extern "C" int dcg_gpc_objective(dcg_context* ctx, void* stream, long long n, const double* d_f, const double* d_y,
                                  const double* d_a, double* d_grad, double* d_h, double* loglik, double* psi) {
     if (!ctx || n < 0 || !d_f || !d_y || !d_a) return DCG_E_CONFIG;
     cudaStream_t st = as_stream(stream);
-    const size_t need = al(sizeof(double) * 2 * ctx->sm_count * 2) + al(sizeof(DevStatus));
+    const size_t need = al(sizeof(double) * 3 * ctx->sm_count * 2) + al(sizeof(DevStatus));
     int rc = dcg_ws_reserve(ctx, need);
     if (rc) return rc;
     Arena ar{static_cast<char*>(ctx->ws), 0};
-    double* part = ar.take<double>(4 * ctx->sm_count);
+    double* part = ar.take<double>(6 * ctx->sm_count);
     DevStatus* ds = ar.take<DevStatus>(1);
     rc = dcg_derivs_launch(ctx, st, n, d_f, d_y, d_a, d_grad, d_h, part, ds);
     if (rc) return rc;
@@ -850,12 +880,12 @@ extern "C" int dcg_gpc_newton_update_async(dcg_context* ctx, void* stream, const
     if (kop->row0 != 0 || kop->rows != kop->n) return DCG_E_UNSUPPORTED;
     cudaStream_t st = as_stream(stream);
     const long long n = kop->n;
-    const size_t need = al(sizeof(double) * 2 * ctx->sm_count * 2) + al(sizeof(DevStatus)) +
+    const size_t need = al(sizeof(double) * 3 * ctx->sm_count * 2) + al(sizeof(DevStatus)) +
                         al(sizeof(double) * apply_k_scratch(kop));
     rc = dcg_ws_reserve(ctx, need);
     if (rc) return rc;
     Arena ar{static_cast<char*>(ctx->ws), 0};
-    double* part = ar.take<double>(4 * ctx->sm_count);
+    double* part = ar.take<double>(6 * ctx->sm_count);
     DevStatus* ds = ar.take<DevStatus>(1);
     double* scratch = ar.take<double>(apply_k_scratch(kop));
     rc = dcg_newton_a_launch(ctx, st, n, d_inner, d_s, d_x, d_a);
@@ -883,12 +913,12 @@ extern "C" int dcg_gpc_newton_update(dcg_context* ctx, void* stream, const dcg_o
         if (rc) return rc;
         return apply_k(ctx, st, kop, d_a, nullptr, nullptr, 0.0, d_f, static_cast<double*>(ctx->ws));
     }
-    const size_t need = al(sizeof(double) * 2 * ctx->sm_count * 2) + al(sizeof(DevStatus)) +
+    const size_t need = al(sizeof(double) * 3 * ctx->sm_count * 2) + al(sizeof(DevStatus)) +
                         al(sizeof(double) * apply_k_scratch(kop));
     rc = dcg_ws_reserve(ctx, need);
     if (rc) return rc;
     Arena ar{static_cast<char*>(ctx->ws), 0};
-    double* part = ar.take<double>(4 * ctx->sm_count);
+    double* part = ar.take<double>(6 * ctx->sm_count);
     DevStatus* ds = ar.take<DevStatus>(1);
     double* scratch = ar.take<double>(apply_k_scratch(kop));
     rc = dcg_newton_a_launch(ctx, st, n, d_inner, d_s, d_x, d_a);

@@ -189,10 +189,11 @@ __device__ __forceinline__ double logaddexp0(double z) {
 __global__ void derivs_kernel(long long n, const double* f, const double* y, const double* a, double* grad,
                               double* h, double* part) {
     __shared__ double red[40];
-    double ll = 0.0, fa = 0.0;
+    double ll = 0.0, fa = 0.0, bad = 0.0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const double fi = f[i], yi = y[i];
+        if (yi != 1.0 && yi != -1.0) bad += 1.0;   // gpc.py:135-139 (counted, reported by dcg_gpc_init)
         ll += logaddexp0(mul_rn(-yi, fi));
         const double pi = sigmoid_ref(fi);
         grad[i] = sub_rn(mul_rn(add_rn(yi, 1.0), 0.5), pi);
@@ -201,24 +202,29 @@ __global__ void derivs_kernel(long long n, const double* f, const double* y, con
     }
     ll = block_sum(ll, red);
     fa = block_sum(fa, red);
+    bad = block_sum(bad, red);
     if (threadIdx.x == 0) {
         part[2 * blockIdx.x] = ll;
         part[2 * blockIdx.x + 1] = fa;
+        part[2 * gridDim.x + blockIdx.x] = bad;
     }
 }
 
 __global__ void derivs_finalize_kernel(const double* part, int nb, DevStatus* st, double* llpsi) {
     __shared__ double red[40];
-    double ll = 0.0, fa = 0.0;
+    double ll = 0.0, fa = 0.0, bad = 0.0;
     for (int b = threadIdx.x; b < nb; b += blockDim.x) {
         ll += part[2 * b];
         fa += part[2 * b + 1];
+        bad += part[2 * nb + b];
     }
     ll = block_sum(ll, red);
     fa = block_sum(fa, red);
+    bad = block_sum(bad, red);
     if (threadIdx.x == 0) {
         const double loglik = -ll;
         st->status = DCG_OK;
+        st->info = (long long)bad;   // labels not in {-1, +1}
         st->value = loglik;
         st->value2 = sub_rn(loglik, mul_rn(0.5, fa));   // psi = loglik - f'a/2 (gpc.py:209)
         if (llpsi) {

@@ -269,16 +269,29 @@ def _as_flavour(state: GpcState, host: bool, k_matrix=None) -> GpcState:
 
 def _make_state_dev(k_matrix, y, f=None) -> GpcState:
     op = _kernel_op(k_matrix)
-    yd, ok = _labels_dev(y)
-    n = yd.shape[0]
     if f is None:
-        fd, ad = D.zeros(n), D.zeros(n)
-    else:
-        fd = D.to_dev(f, 1)
-        ad = _dense_cholesky_solve(op, fd)
+        # f = a = 0: one library call zeroes them, evaluates the derivatives
+        # and loglik and counts the labels outside {-1, +1} (one host read)
+        if isinstance(y, torch.Tensor):
+            yd = y.to(device=D.device(), dtype=torch.float64)
+            if yd.ndim != 1:
+                raise InvalidLabel("labels must be a vector of -1/+1")
+            yd = yd.contiguous()
+        else:
+            yd = check_labels(y)
+        n = yd.shape[0]
+        fd, ad, g, h = D.empty(n), D.empty(n), D.empty(n), D.empty(n)
+        ll, bad = ctypes.c_double(0.0), ctypes.c_longlong(0)
+        N.check(N.lib().dcg_gpc_init(D.ctx(), D.stream(), n, yd.data_ptr() if n else None, fd.data_ptr(),
+                                     ad.data_ptr(), g.data_ptr(), h.data_ptr(), ctypes.byref(ll), ctypes.byref(bad)),
+                what="gpc_init")
+        if bad.value:
+            raise InvalidLabel("labels must be a vector of -1/+1")
+        return GpcState(f=fd, y=yd, k_matrix=op, a=ad, loglik=float(ll.value), grad_loglik=g, h=h, host=False)
+    yd = check_labels(y)
+    fd = D.to_dev(f, 1)
+    ad = _dense_cholesky_solve(op, fd)
     ll, g, h = _derivs_dev(fd, yd)
-    if ok is not None and not bool(ok):   # computed before the derivatives' host read
-        raise InvalidLabel("labels must be a vector of -1/+1")
     return GpcState(f=fd, y=yd, k_matrix=op, a=ad, loglik=ll, grad_loglik=g, h=h, host=False)
 
 
