@@ -81,7 +81,12 @@ def to_dev(a, ndim: int | None = None) -> torch.Tensor:
     if ndim is not None and t.ndim != ndim:
         kind = "vector" if ndim == 1 else "matrix"
         raise DimensionMismatch(f"expected a {kind}, got ndim={t.ndim}")
-    return t.contiguous()
+    t = t.contiguous()
+    if t.data_ptr() % 16:
+        # an offset view: the kernels stage vectors with 16-byte copies (and a
+        # packed-only operator has no row-major fallback for unaligned ones)
+        t = t.clone()
+    return t
 
 
 def as_host_vector(v) -> np.ndarray:

@@ -210,3 +210,22 @@ def test_packed_solve_early_exits(P):
     # and the library is still healthy afterwards
     xs, rep, _ = P.cg_solve(spd, b, None, P.SolverConfig(tol=1e-10))
     assert rep.converged
+
+
+def test_packed_only_operator_with_offset_views(P):
+    """Unaligned (offset) vector views handed to a packed-only operator (no
+    row-major storage to fall back on) give the aligned results."""
+    import torch
+
+    n = 4500
+    rng = np.random.default_rng(9)
+    g = P.rbf_kernel(torch.from_numpy(rng.standard_normal((n, 5))).cuda(), P.KernelParams(1.0, 1.3))
+    buf = torch.from_numpy(rng.standard_normal(n + 1)).cuda()
+    v_off = buf[1:]                        # 8-byte offset
+    assert v_off.data_ptr() % 16 == 8
+    y1 = g @ v_off
+    y2 = g @ v_off.clone()
+    assert torch.equal(y1, y2)
+    x, rep, _ = P.cg_solve(g.scaled(None, 1.0), v_off, None, P.SolverConfig(tol=1e-10))
+    assert rep.converged
+    assert not g._rm.ready
