@@ -642,21 +642,21 @@ def run_native_sharded(args, rank, world):
     ms = float(t.item())
     ms_per_step = ms / args.steps
     value = total_its / (ms / 1e3)   # one sequence solved jointly: iterations counted once
-    # step-average bytes per GPU: the solve's products read the rank's tile
-    # share (8 x 4096 x tiles), once per matvec-equivalent (iterations + one
-    # warm-start product per system); the slab (8 n^2 / N) serves the once-
-    # per-system products (refresh, the two Newton-glue products)
+    # step-average bytes per GPU: every K pass of the sharded step reads the
+    # rank's tile share (8 x 4096 x tiles): one per solve iteration, plus per
+    # system about three more (the Newton system's pass, fused with the next
+    # solve's first product from the second step on; the Newton update's K a;
+    # the refresh's block product)
     share_bytes = 8.0 * 4096 * (op.share.t_hi - op.share.t_lo) if op.share is not None else 8.0 * n * n / world
-    slab_bytes = 8.0 * n * n / world
-    mv = total_its + args.steps * c["newton_steps"]
-    achieved = (mv * share_bytes + args.steps * c["newton_steps"] * 3 * slab_bytes) / (ms / 1e3) / 1e9
+    mv = total_its + args.steps * c["newton_steps"] * 3
+    achieved = (mv * share_bytes) / (ms / 1e3) / 1e9
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
     roofline = {"kernel": "sharded step (tile-share GEMV + all-reduce per product; slab products per system) - "
                           "step average incl. collectives", "bound": "hbm",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
-                "bytes_model": "(iterations + 1 prologue product per system) x the rank's tile-share bytes + "
-                               "3 slab products (8 n^2 / N) per system, per GPU over the step"}
+                "bytes_model": "(iterations + 3 K passes per system) x the rank's tile-share bytes, per GPU over "
+                               "the step"}
 
     # e2e: pinned host X, y -> device, slab assembly, the sharded sequence, records back
     xh, yh = torch.from_numpy(x).pin_memory(), torch.from_numpy(y).pin_memory()

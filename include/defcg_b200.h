@@ -379,6 +379,12 @@ DCG_API int dcg_shard_start(dcg_context* ctx, void* stream, long long rows, int 
                             double tol, long long max_iters, long long ell);
 /* From the reduced [r0'r0, AW' r0]: mu_0, p_0 = r_0 - W mu_0 (or r_0), rel_0,
  * history[0], log r_0 / p_0 / mu_0, done; zero rhs -> x = 0 (solvers.py:142-147). */
+/* dcg_shard_start and r0 = r_prev - (AW) c in d_r (holding r_prev = b - A x_prev on
+ * entry): the deflated warm start without a second product (solvers.py:236-238). */
+DCG_API int dcg_shard_start_r(dcg_context* ctx, void* stream, long long rows, int k,
+                              const double* d_red, const double* d_chol, const double* d_w,
+                              const double* d_aw, const double* d_xprev, double* d_x0, double* d_r,
+                              dcg_shard_state* d_state, double tol, long long max_iters, long long ell);
 DCG_API int dcg_shard_begin(dcg_context* ctx, void* stream, long long rows, int k,
                             const double* d_red, const double* d_chol, const double* d_w,
                             const double* d_r, double* d_p, double* d_x, dcg_shard_state* d_state,
@@ -429,6 +435,12 @@ DCG_API int dcg_k_rbf_gram_packed(dcg_context* ctx, void* stream, const double* 
 DCG_API int dcg_shard_tiles_partial(dcg_context* ctx, void* stream, const dcg_operator* op, int rank,
                             int world, const double* d_v, double* d_t,
                             const dcg_shard_state* d_state);
+/* Two unscaled products K v1, K v2 over one pass of the tile share (partials
+ * for all n rows; the caller all-reduces both): the Newton system's K inner
+ * and the next solve's first product (gpc.py:175-183, solvers.py:237).     */
+DCG_API int dcg_shard_tiles_partial2(dcg_context* ctx, void* stream, const dcg_operator* op, int rank,
+                             int world, const double* d_v1, const double* d_v2, double* d_t1,
+                             double* d_t2);
 DCG_API int dcg_shard_epilogue(dcg_context* ctx, void* stream, int mode, const dcg_operator* op,
                                const double* d_v, const double* d_b, const double* d_t,
                                double* d_out, double* d_part, const dcg_shard_state* d_state);

@@ -225,8 +225,10 @@ SIGNATURES = {
     "dcg_shard_apply_dot": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P],
     "dcg_shard_rbf_sym_partial": [_P, _P, ctypes.POINTER(COperator), ctypes.c_int, ctypes.c_int, _P, _P, _P],
     "dcg_shard_tile_range": [_LL, ctypes.c_int, ctypes.c_int, _PLL, _PLL],
+    "dcg_shard_start_r": [_P, _P, _LL, ctypes.c_int, _P, _P, _P, _P, _P, _P, _P, _P, _D, _LL, _LL],
     "dcg_k_rbf_gram_packed": [_P, _P, _P, _LL, _LL, _D, _D, _D, _LL, _LL, _P],
     "dcg_shard_tiles_partial": [_P, _P, ctypes.POINTER(COperator), ctypes.c_int, ctypes.c_int, _P, _P, _P],
+    "dcg_shard_tiles_partial2": [_P, _P, ctypes.POINTER(COperator), ctypes.c_int, ctypes.c_int, _P, _P, _P, _P],
     "dcg_shard_epilogue": [_P, _P, ctypes.c_int, ctypes.POINTER(COperator), _P, _P, _P, _P, _P, _P],
     "dcg_shard_residual": [_P, _P, ctypes.POINTER(COperator), _P, _P, _P, _P],
     "dcg_shard_partials": [_P, _P, _LL, ctypes.c_int, _P, _P, _P, _P],

@@ -233,10 +233,13 @@ __global__ void sym_pass2_share_kernel(long long n, long long t_lo, long long t_
 // [t_lo, t_hi) (kp_share holds exactly those, tile t at t - t_lo), split over
 // the CTAs with the same equal-cost rule, the range table exported (block 0)
 // for the share's pass 2.  colpart / rowpart are indexed relative to t_lo.
+// NV = 2: a second vector v2 (both unscaled, s_in unused) with its partials
+// at colpart / rowpart + part2.
+template <int NV>
 __global__ void __launch_bounds__(DCG_NT, 1)
     stored_pass1_share_kernel(const double* kp_share, long long n, long long t_lo, long long t_hi, const double* v,
                               const double* s_in, double* colpart, double* rowpart, long long* tbl_out,
-                              const dcg_shard_state* gate) {
+                              const dcg_shard_state* gate, const double* v2 = nullptr, long long part2 = 0) {
     if (gate && gate->done) return;
     extern __shared__ __align__(16) double smem[];
     sym_ring_init(smem, n, true);
@@ -247,8 +250,8 @@ __global__ void __launch_bounds__(DCG_NT, 1)
     if (blockIdx.x == 0)
         for (int b = threadIdx.x; b <= G; b += blockDim.x) tbl_out[b] = tbl[b];
     unsigned int seq = 0;
-    sym_pass1<true, 1, true>(kp_share - t_lo * DCG_SYM_TILE_DOUBLES, 0, n, v, s_in, colpart - t_lo * DCG_TB,
-                             rowpart - t_lo * DCG_TB, smem, seq);
+    sym_pass1<true, NV, true>(kp_share - t_lo * DCG_SYM_TILE_DOUBLES, 0, n, v, NV == 2 ? nullptr : s_in,
+                              colpart - t_lo * DCG_TB, rowpart - t_lo * DCG_TB, smem, seq, v2, part2);
 }
 
 }  // namespace
@@ -279,12 +282,48 @@ extern "C" int dcg_shard_tiles_partial(dcg_context* ctx, void* stream, const dcg
     long long* tbl = reinterpret_cast<long long*>(rowpart + (nloc > 0 ? nloc : 1) * DCG_TB);
     if (nloc > 0) {
         const size_t smem = sizeof(double) * (size_t)sym_smem_doubles();
-        DCG_SMEM_ATTR(stored_pass1_share_kernel, smem);
-        stored_pass1_share_kernel<<<G, DCG_NT, smem, st>>>(op->d_kp, n, t_lo, t_hi, d_v, op->d_s, colpart, rowpart,
-                                                            tbl, d_state);
+        DCG_SMEM_ATTR(stored_pass1_share_kernel<1>, smem);
+        stored_pass1_share_kernel<1><<<G, DCG_NT, smem, st>>>(op->d_kp, n, t_lo, t_hi, d_v, op->d_s, colpart, rowpart,
+                                                               tbl, d_state);
         DCG_LAUNCHED();
     }
     sym_pass2_share_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(n, t_lo, t_hi, tbl, G, colpart, rowpart, d_t, d_state);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}
+
+// Two products over one pass of the rank's tile share: partials of K v1 and
+// K v2 (both unscaled; op->d_s is not applied) for all n rows into d_t1, d_t2
+// (the Newton system's K inner and the next solve's K (s (.) x_prev)).
+extern "C" int dcg_shard_tiles_partial2(dcg_context* ctx, void* stream, const dcg_operator* op, int rank, int world,
+                                        const double* d_v1, const double* d_v2, double* d_t1, double* d_t2) {
+    if (!ctx || !op || !d_v1 || !d_v2 || !d_t1 || !d_t2 || world < 1 || rank < 0 || rank >= world) return DCG_E_CONFIG;
+    if (op->kind != DCG_OP_DENSE_SYM || !op->d_kp || !aligned16(op->d_kp) || !aligned16(d_v1) || !aligned16(d_v2))
+        return DCG_E_CONFIG;
+    const long long n = op->n;
+    if (n == 0) return DCG_OK;
+    cudaStream_t st = as_stream(stream);
+    const long long t_lo = sym_tile_begin(n, world, rank), t_hi = sym_tile_begin(n, world, rank + 1);
+    const long long nloc = t_hi - t_lo, nl = nloc > 0 ? nloc : 1;
+    const int G = ctx->sm_count < DCG_SYM_MAX_CTAS ? ctx->sm_count : DCG_SYM_MAX_CTAS;
+    const size_t need = sizeof(double) * 4 * (size_t)nl * DCG_TB + sizeof(long long) * (DCG_SYM_MAX_CTAS + 2) + 1024;
+    int rc = dcg_ws2_reserve(ctx, need);
+    if (rc) return rc;
+    double* colpart = static_cast<double*>(ctx->ws2);
+    double* rowpart = colpart + nl * DCG_TB;
+    const long long part2 = 2 * nl * DCG_TB;
+    long long* tbl = reinterpret_cast<long long*>(colpart + 4 * nl * DCG_TB);
+    if (nloc > 0) {
+        const size_t smem = sizeof(double) * (size_t)sym_smem_doubles();
+        DCG_SMEM_ATTR(stored_pass1_share_kernel<2>, smem);
+        stored_pass1_share_kernel<2><<<G, DCG_NT, smem, st>>>(op->d_kp, n, t_lo, t_hi, d_v1, nullptr, colpart,
+                                                               rowpart, tbl, nullptr, d_v2, part2);
+        DCG_LAUNCHED();
+    }
+    sym_pass2_share_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(n, t_lo, t_hi, tbl, G, colpart, rowpart, d_t1, nullptr);
+    DCG_LAUNCHED();
+    sym_pass2_share_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(n, t_lo, t_hi, tbl, G, colpart + part2,
+                                                              rowpart + part2, d_t2, nullptr);
     DCG_LAUNCHED();
     return DCG_OK;
 }

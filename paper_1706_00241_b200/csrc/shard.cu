@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(SH_NT)
 __global__ void __launch_bounds__(SH_NT)
     shard_start_kernel(long long rows, int k, const double* red, const double* Lg, const double* W,
                        const double* xprev, double* x0, dcg_shard_state* state, double tol, long long max_iters,
-                       long long ell) {
+                       long long ell, const double* AW = nullptr, double* r = nullptr) {
     __shared__ double s_L[DCG_MAX_K * DCG_MAX_K];
     __shared__ double s_y[DCG_MAX_K];
     const long long r0 = part_begin(rows, gridDim.x, blockIdx.x), r1 = part_begin(rows, gridDim.x, blockIdx.x + 1);
@@ -234,8 +234,12 @@ __global__ void __launch_bounds__(SH_NT)
         cta_sync();
         cta_chol_solve(s_L, k, red + 1, s_y);
     }
-    for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x)
+    for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
         x0[i] = k > 0 ? add_rn(xprev[i], row_dot(W, i, k, s_y)) : xprev[i];
+        // r0 = r_prev - (AW) c: A x0 = A x_prev + (A W) c with the basis' own AW
+        // (the single-GPU solve's warm start, solve.cu): no second product
+        if (r && k > 0) r[i] = sub_rn(r[i], row_dot(AW, i, k, s_y));
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         state->rr = 0.0;
         state->norm_b = sqrt(red[0]);
@@ -497,6 +501,23 @@ extern "C" int dcg_shard_start(dcg_context* ctx, void* stream, long long rows, i
     cudaStream_t st = as_stream(stream);
     shard_start_kernel<<<shard_grid(ctx, rows), SH_NT, 0, st>>>(rows, k, d_red, d_chol, d_w, d_xprev, d_x0, d_state,
                                                                  tol, max_iters, ell);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}
+
+// dcg_shard_start plus r0 = r_prev - (AW) c in place of r (the rank's rows of
+// AW; r holds r_prev = b - A x_prev): the warm start without the product
+// r0 = b - A x0 (equal up to rounding).
+extern "C" int dcg_shard_start_r(dcg_context* ctx, void* stream, long long rows, int k, const double* d_red,
+                                 const double* d_chol, const double* d_w, const double* d_aw, const double* d_xprev,
+                                 double* d_x0, double* d_r, dcg_shard_state* d_state, double tol, long long max_iters,
+                                 long long ell) {
+    if (!ctx || rows < 0 || k < 1 || !d_red || !d_xprev || !d_x0 || !d_state || !d_chol || !d_w || !d_aw || !d_r)
+        return DCG_E_CONFIG;
+    if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
+    cudaStream_t st = as_stream(stream);
+    shard_start_kernel<<<shard_grid(ctx, rows), SH_NT, 0, st>>>(rows, k, d_red, d_chol, d_w, d_xprev, d_x0, d_state,
+                                                                 tol, max_iters, ell, d_aw, d_r);
     DCG_LAUNCHED();
     return DCG_OK;
 }

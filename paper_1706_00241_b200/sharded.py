@@ -330,6 +330,11 @@ class DeviceShardBackend:
         N.check(N.lib().dcg_shard_start(self.ctx(), self.stream(), rows, k, _p(red), _p(chol), _p(w), _p(xprev),
                                         _p(x0), _p(state), tol, max_iters, ell), what="shard_start")
 
+    def start_r(self, rows, k, red, chol, w, aw, xprev, x0, r, state, tol, max_iters, ell):
+        N.check(N.lib().dcg_shard_start_r(self.ctx(), self.stream(), rows, k, _p(red), _p(chol), _p(w), _p(aw),
+                                          _p(xprev), _p(x0), _p(r), _p(state), tol, max_iters, ell),
+                what="shard_start_r")
+
     def begin(self, rows, k, red, chol, w, r, p, x, state, hist, log):
         N.check(N.lib().dcg_shard_begin(self.ctx(), self.stream(), rows, k, _p(red), _p(chol), _p(w), _p(r), _p(p),
                                         _p(x), _p(state), _p(hist), _p(log.r), _p(log.p), _p(log.mu)),
@@ -386,7 +391,7 @@ def _alloc_log(be, rows, ell, k):
 
 
 def sharded_solve(op: ShardedOperator, b_loc, x_prev_loc, basis: ShardBasis | None, cfg: SolverConfig | None = None,
-                  comm=None, backend=None, poll: int | None = None):
+                  comm=None, backend=None, poll: int | None = None, ax0=None):
     """CG (basis None or k = 0, solvers.py:207-219) or deflated CG with the
     warm-start correction (solvers.py:222-239) on this rank's rows.  Returns
     (x_loc, SolveReport, ShardLog); every rank gets the same report."""
@@ -458,16 +463,28 @@ def sharded_solve(op: ShardedOperator, b_loc, x_prev_loc, basis: ShardBasis | No
             be.apply_dot(op, full, out, part, st)
 
     # ---- prologue: norm_b, warm start, r_0, mu_0, p_0 ----------------------
+    # ax0 (tile shares: all n rows): A x_prev computed by the caller together
+    # with the Newton system's product, which saves this solve's first product
+    use_ax0 = ax0 is not None and share is not None
     if k:
-        comm.allgather(x_prev_loc, full)
-        residual(b_loc, r)                                 # r_prev = b - A x_prev
+        if use_ax0:
+            torch.sub(b_loc[:n], ax0[:n], out=r[:n])         # r_prev = b - A x_prev
+        else:
+            comm.allgather(x_prev_loc, full)
+            residual(b_loc, r)                             # r_prev = b - A x_prev
         be.partials(rows, k, b_loc, r, w_loc, part2)       # [b'b, W' r_prev]
+        comm.allreduce(part2)
+        # x_0 = x_prev + W c and r_0 = r_prev - (AW) c: no second product
+        be.start_r(rows, k, part2, chol, w_loc, aw_loc, x_prev_loc, x, r, state, float(cfg.tol), max_iters, ell)
     else:
         be.partials(rows, 0, b_loc, None, None, part2)     # [b'b]
-    comm.allreduce(part2)
-    be.start(rows, k, part2, chol, w_loc, x_prev_loc, x, state, float(cfg.tol), max_iters, ell)
-    comm.allgather(x[:rows], full)
-    residual(b_loc, r)                                     # r_0 = b - A x_0
+        comm.allreduce(part2)
+        be.start(rows, k, part2, chol, w_loc, x_prev_loc, x, state, float(cfg.tol), max_iters, ell)
+        if use_ax0:
+            torch.sub(b_loc[:n], ax0[:n], out=r[:n])         # r_0 = b - A x_0, x_0 = x_prev
+        else:
+            comm.allgather(x[:rows], full)
+            residual(b_loc, r)                             # r_0 = b - A x_0
     be.partials(rows, k, r, r, aw_loc, part2)              # [r0'r0, AW' r0]
     comm.allreduce(part2)
     be.begin(rows, k, part2, chol, w_loc, r, p, x, state, hist, log)
@@ -555,12 +572,21 @@ def sharded_refresh_basis(op: ShardedOperator, w_full: torch.Tensor, comm=None, 
     if k == 0:
         return ShardBasis(w_full, w_full.clone(), be.empty(0, 0))
     rows = op.rows
-    aw_loc = be.empty(max(rows, 1), k)
-    cop = op.c_struct()
-    if rows:
-        N.check(N.lib().dcg_op_apply_block(be.ctx(), be.stream(), ctypes.byref(cop), w_full.data_ptr(), k,
-                                           aw_loc.data_ptr()), what="refresh_basis")
-    aw = _gather_rows(comm, be, aw_loc[:rows], n).contiguous()
+    share = getattr(op, "share", None)
+    if share is not None and share.world == 1 and N.lib().dcg_block_uses_packed(k):
+        # one rank holds every tile: the symmetric block product over the
+        # packed share (half the slab's bytes) gives all n rows of AW at once
+        aw = be.empty(n, k)
+        cop = op.share_struct()
+        N.check(N.lib().dcg_op_apply_block(be.ctx(), be.stream(), ctypes.byref(cop), w_full.contiguous().data_ptr(), k,
+                                           aw.data_ptr()), what="refresh_basis")
+    else:
+        aw_loc = be.empty(max(rows, 1), k)
+        cop = op.c_struct()
+        if rows:
+            N.check(N.lib().dcg_op_apply_block(be.ctx(), be.stream(), ctypes.byref(cop), w_full.data_ptr(), k,
+                                               aw_loc.data_ptr()), what="refresh_basis")
+        aw = _gather_rows(comm, be, aw_loc[:rows], n).contiguous()
     w = w_full.contiguous().clone()
     chol = be.empty(k, k)
     kout, info = ctypes.c_longlong(k), ctypes.c_longlong(0)
@@ -607,7 +633,7 @@ class ShardSequenceState:
     history: list = field(default_factory=list)
 
 
-def sharded_solve_next(state: ShardSequenceState, op: ShardedOperator, b_loc, comm=None, backend=None):
+def sharded_solve_next(state: ShardSequenceState, op: ShardedOperator, b_loc, comm=None, backend=None, ax0=None):
     """solve_next (recycle.py:162-203) on row shards: refresh (BasisDeficient
     -> plain CG), solve, extraction (BasisDeficient -> no basis)."""
     comm = comm or SelfComm()
@@ -620,7 +646,7 @@ def sharded_solve_next(state: ShardSequenceState, op: ShardedOperator, b_loc, co
             used = sharded_refresh_basis(op, state.basis.w, comm, be)
         except BasisDeficient:
             used = None
-    x, rep, log = sharded_solve(op, b_loc, x_prev[:rows], used, state.cfg, comm, be)
+    x, rep, log = sharded_solve(op, b_loc, x_prev[:rows], used, state.cfg, comm, be, ax0=ax0)
     nxt = None
     if state.k > 0:
         try:
@@ -682,25 +708,41 @@ def sharded_laplace_newton(x, y, params=None, cfg: SolverConfig | None = None, n
     records = []
     share = getattr(op, "share", None)
     r0 = op.row0
+    x_last = None   # the previous solution (all rows), the next solve's warm start
     for it in range(1, max_newton + 1):
         s, inner, b_loc = be.empty(n), be.empty(n), be.empty(max(rows, 1))
+        ax0 = None
         if share is not None:
             # gpc.py:175-183 with the product from the tile shares: s = sqrt(h),
             # inner = h f + grad, b = s (.) (K inner), element-wise as the
-            # reference rounds them (one rounding per operation)
+            # reference rounds them (one rounding per operation); from the
+            # second step on the same share pass also gives A x_prev =
+            # x_prev + s (.) K (s (.) x_prev), the solve's first product
             torch.sqrt(h, out=s)
             torch.add(torch.mul(h, f), grad, out=inner)
-            b_loc[:rows] = torch.mul(s, _share_kv(op, inner, comm, be))[r0:r0 + rows]
+            if x_last is None:
+                b_loc[:rows] = torch.mul(s, _share_kv(op, inner, comm, be))[r0:r0 + rows]
+            else:
+                t = be.empty(2 * n)
+                xs = torch.mul(s, x_last)
+                cop = op.scaled(None, 0.0).share_struct()
+                N.check(N.lib().dcg_shard_tiles_partial2(be.ctx(), be.stream(), ctypes.byref(cop), share.rank,
+                                                         share.world, inner.data_ptr(), xs.data_ptr(),
+                                                         t.data_ptr(), t[n:].data_ptr()), what="shard_tiles_partial2")
+                comm.allreduce(t)
+                b_loc[:rows] = torch.mul(s, t[:n])[r0:r0 + rows]
+                ax0 = torch.add(x_last, torch.mul(s, t[n:]))
         else:
             N.check(N.lib().dcg_gpc_newton_system(be.ctx(), be.stream(), ctypes.byref(kop), f.data_ptr(),
                                                   grad.data_ptr(), h.data_ptr(), s.data_ptr(), inner.data_ptr(),
                                                   b_loc.data_ptr()), what="newton_system")
         t0 = time.perf_counter()
-        x_loc, state = sharded_solve_next(state, op.scaled(s, 1.0), b_loc[:rows], comm, be)
+        x_loc, state = sharded_solve_next(state, op.scaled(s, 1.0), b_loc[:rows], comm, be, ax0=ax0)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         rep = state.history[-1]
         x_full = _allgather_vec(comm, be, x_loc, n).contiguous()
+        x_last = x_full
         if share is not None:
             # gpc.py:186-191: a = inner - s (.) x, f = K a (tile shares)
             a = torch.sub(inner, torch.mul(s, x_full))

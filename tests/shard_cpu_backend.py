@@ -71,6 +71,11 @@ class CpuShardBackend:
         i[N.SHARD_MAX_ITERS] = max_iters
         i[N.SHARD_ELL] = ell
 
+    def start_r(self, rows, k, red, chol, w, aw, xprev, x0, r, state, tol, max_iters, ell):
+        c = _chol_solve(chol, red[1:1 + k])
+        self.start(rows, k, red, chol, w, xprev, x0, state, tol, max_iters, ell)
+        r[:rows] = r[:rows] - aw[:rows] @ c
+
     def begin(self, rows, k, red, chol, w, r, p, x, state, hist, log):
         i = self._i(state)
         nb, tol, ell, mx = float(state[N.SHARD_NORM_B]), float(state[N.SHARD_TOL]), int(i[N.SHARD_ELL]), int(i[N.SHARD_MAX_ITERS])
