@@ -2,7 +2,7 @@ import sys, ctypes, numpy as np, torch
 sys.path.insert(0, '/root/repo')
 import paper_1706_00241_b200 as P
 from paper_1706_00241_b200 import _native as N, recycle
-from oracle.defcg_oracle import gpc_inputs
+from paper_1706_00241_b200.workloads import gpc_inputs
 x, y = gpc_inputs(10000, 10, 0)
 gram = P.rbf_kernel(torch.from_numpy(x).cuda(), P.KernelParams(1.0, 1.5))
 yd = torch.from_numpy(y).cuda()
