@@ -465,7 +465,7 @@ def run_native(args, rank, world):
     # ---- e2e through the public API from pinned host buffers ----------------
     xh = torch.from_numpy(x).pin_memory()
     yh = torch.from_numpy(y).pin_memory()
-    e2e_steps = max(1, min(args.steps, 5))
+    e2e_steps = max(1, min(2 * args.steps, 10))
 
     def e2e_once():
         xg = xh.to("cuda", non_blocking=True)
@@ -477,7 +477,7 @@ def run_native(args, rank, world):
         d2h = fh.numel() * 8 + sum(r.f.nbytes for r in recs) + sum(8 * len(r.residual_history) for r in recs)
         return sum(r.solver_iterations for r in recs), d2h
 
-    for _ in range(2):   # warm-up (first-use costs of the end-to-end path)
+    for _ in range(3):   # warm-up (first-use costs of the end-to-end path)
         e2e_once()
     gc.collect()
     barrier()

@@ -280,7 +280,9 @@ DCG_API int dcg_ritz_extract_async(dcg_context* ctx, void* stream, long long n,
  * the W_next tail -- the two halves may go to different streams (the caller
  * orders stage 2 after stage 1) and must get identical arguments.  Stage 2
  * splits further into 3 (the pencil) and 4 (the SM-wide W_next tail), so
- * the tail can follow the pencil on another stream (ordered after it).     */
+ * the tail can follow the pencil on another stream (ordered after it).
+ * d_aw_next may be NULL when the caller refreshes the basis against its next
+ * matrix before any use (AW_next = A W_next is then never formed).         */
 DCG_API int dcg_ritz_extract_dev(dcg_context* ctx, void* stream, long long n,
                                  const dcg_krylov_log* log, const void* d_solve_status,
                                  const dcg_basis* prev, long long k, int selection,

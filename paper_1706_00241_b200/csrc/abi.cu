@@ -135,6 +135,8 @@ extern "C" int dcg_context_create(int device, dcg_context** out) {
     c->solve_blocks = prop.multiProcessorCount;   // one persistent CTA per SM
     DCG_CUDA(cudaEventCreate(&c->ev0));
     DCG_CUDA(cudaEventCreate(&c->ev1));
+    DCG_CUDA(cudaMalloc(&c->d_sync, 128 * DCG_SW_NSLOTS));
+    DCG_CUDA(cudaMemset(c->d_sync, 0, 128 * DCG_SW_NSLOTS));
     *out = c;
     return DCG_OK;
 }
@@ -170,6 +172,7 @@ extern "C" int dcg_context_destroy(dcg_context* ctx) {
     if (ctx->ws2) cudaFree(ctx->ws2);
     if (ctx->host) cudaFreeHost(ctx->host);
     if (ctx->d_res) cudaFree(ctx->d_res);
+    if (ctx->d_sync) cudaFree(ctx->d_sync);
     cudaEventDestroy(ctx->ev0);
     cudaEventDestroy(ctx->ev1);
     delete ctx;
@@ -686,8 +689,7 @@ extern "C" int dcg_refresh_basis_async(dcg_context* ctx, void* stream, const dcg
     double* gsym = ar.take<double>((size_t)k * k);
     double* lwork = ar.take<double>((size_t)2 * k * k);
     double* parts = ar.take<double>(dcg_xty_scratch_doubles(ctx, (int)k, (int)k));
-    DevStatus* ds = ar.take<DevStatus>(1);
-    DCG_CUDA(cudaMemsetAsync(ds, 0, sizeof(DevStatus), st));
+    DevStatus* ds = ar.take<DevStatus>(1);   // written by every path of gram_factor (no memset)
     rc = dcg_xty(ctx, st, d_w, (int)k, aw, (int)k, n, (int)k, (int)k, graw, parts);
     if (rc) return rc;
     rc = dcg_gram_factor_launch(st, graw, (int)k, 1, gsym, lwork, active, ds);

@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(DCG_NT, 1)
     });
     APPLY_TS(4);
 #undef APPLY_TS
+    if (threadIdx.x == 0) dcg_sync_exit(bar, gridDim.x);
 }
 
 // DCG_APPLY_TIMERS=1 (developer diagnostic): per-CTA globaltimer stamps of the
@@ -164,12 +165,12 @@ int dcg_sym_apply(dcg_context* ctx, cudaStream_t st, const double* K, const doub
     double* rowpart = scratch + ntt * DCG_TB;
     const int navail = ctx->sm_count > 1 ? ctx->sm_count - 1 : 1;
     const int G = navail < DCG_SYM_MAX_CTAS ? navail : DCG_SYM_MAX_CTAS;
-    // one cooperative launch: pass 1, grid barrier, pass 2 (barrier word after the partials)
-    unsigned int* bar = reinterpret_cast<unsigned int*>(rowpart + ntt * DCG_TB);
+    // one cooperative launch: pass 1, grid barrier, pass 2 (the barrier word:
+    // the context's persistent line, no memset)
+    unsigned int* bar = dcg_sync_line(ctx, DCG_SW_APPLY);
     const void* kfn = Kp ? (const void*)sym_apply_coop_kernel<true> : (const void*)sym_apply_coop_kernel<false>;
     if (Kp) DCG_SMEM_ATTR(sym_apply_coop_kernel<true>, smem);
     else DCG_SMEM_ATTR(sym_apply_coop_kernel<false>, smem);
-    DCG_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), st));
     const double* Ksrc = Kp ? Kp : K;
     const long long* gtbl = dcg_sym_table(ctx, st, n, G);
     if (!gtbl) return DCG_E_CUDA;
@@ -216,6 +217,7 @@ __global__ void __launch_bounds__(DCG_NT, 1)
                   if (shift2 != 0.0) val = add_rn(mul_rn(shift2, v2[i]), val);
                   y2[i] = val;
               });
+    if (threadIdx.x == 0) dcg_sync_exit(bar, gridDim.x);
 }
 
 size_t dcg_sym_apply2_scratch_doubles(long long n) { return 4 * (size_t)sym_ntiles(n) * DCG_TB + 32; }
@@ -234,11 +236,10 @@ int dcg_sym_apply2(dcg_context* ctx, cudaStream_t st, const double* K, const dou
     // the CTA count of dcg_sym_apply (same partition -> same partials)
     const int navail = ctx->sm_count > 1 ? ctx->sm_count - 1 : 1;
     const int G = navail < DCG_SYM_MAX_CTAS ? navail : DCG_SYM_MAX_CTAS;
-    unsigned int* bar = reinterpret_cast<unsigned int*>(scratch + 4 * ntt * DCG_TB);
+    unsigned int* bar = dcg_sync_line(ctx, DCG_SW_APPLY2);
     const void* kfn = Kp ? (const void*)sym_apply2_coop_kernel<true> : (const void*)sym_apply2_coop_kernel<false>;
     if (Kp) DCG_SMEM_ATTR(sym_apply2_coop_kernel<true>, smem);
     else DCG_SMEM_ATTR(sym_apply2_coop_kernel<false>, smem);
-    DCG_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), st));
     const double* Ksrc = Kp ? Kp : K;
     const long long* gtbl = dcg_sym_table(ctx, st, n, G);
     if (!gtbl) return DCG_E_CUDA;
@@ -522,15 +523,22 @@ int dcg_block_apply(dcg_context* ctx, cudaStream_t st, const double* K, long lon
 
 // =============================================================================
 // K4: C(p x q) = X(n x p)' Y(n x q), tall-skinny, deterministic two-stage.
+// CTA b sums its rows [r0, r1) in ascending order into a partial (one fused
+// multiply-add per row and pair); the partials are summed in CTA order.  Both
+// stages are one launch: the last CTA to finish (cta_last_arrival on the
+// context's persistent counter) does the ordered sum.  The CTA stages its
+// rows in chunks of `cr` (the whole range when it fits: one load round), so
+// the per-pair sequence of operations -- and the result -- does not depend on
+// the chunking.
 // =============================================================================
-#define XTY_ROWS 32
-#define XTY_PPT 8     // pairs per thread
+#define XTY_AHEAD 32  // partial loads in flight per element of the final sum
+template <int XTY_PPT>   // pairs per thread (1: p q <= 256, the usual W'AW / W'v)
 __global__ void __launch_bounds__(256)
     xty_kernel(const double* __restrict__ X, long long ldx, const double* __restrict__ Y, long long ldy,
-               long long n, int p, int q, double* part) {
+               long long n, int p, int q, int cr, double* part, double* C, unsigned int* counter) {
     extern __shared__ double xty_sm[];
-    double* sx = xty_sm;                      // XTY_ROWS x p
-    double* sy = xty_sm + XTY_ROWS * p;       // XTY_ROWS x q
+    double* sx = xty_sm;                // cr x p
+    double* sy = xty_sm + cr * p;       // cr x q
     const int tid = threadIdx.x;
     const long long r0 = part_begin(n, gridDim.x, blockIdx.x);
     const long long r1 = part_begin(n, gridDim.x, blockIdx.x + 1);
@@ -545,11 +553,19 @@ __global__ void __launch_bounds__(256)
         pa[u] = (e < pq) ? e / q : -1;
         pb[u] = (e < pq) ? e % q : 0;
     }
-    for (long long rb = r0; rb < r1; rb += XTY_ROWS) {
-        const int nr = (int)min((long long)XTY_ROWS, r1 - rb);
+    for (long long rb = r0; rb < r1; rb += cr) {
+        const int nr = (int)min((long long)cr, r1 - rb);
         cta_sync();
-        for (int e = tid; e < nr * p; e += 256) sx[e] = X[(rb + e / p) * ldx + e % p];
-        for (int e = tid; e < nr * q; e += 256) sy[e] = Y[(rb + e / q) * ldy + e % q];
+        if (ldx == p) {
+            for (int e = tid; e < nr * p; e += 256) sx[e] = X[rb * p + e];
+        } else {
+            for (int e = tid; e < nr * p; e += 256) sx[e] = X[(rb + e / p) * ldx + e % p];
+        }
+        if (ldy == q) {
+            for (int e = tid; e < nr * q; e += 256) sy[e] = Y[rb * q + e];
+        } else {
+            for (int e = tid; e < nr * q; e += 256) sy[e] = Y[(rb + e / q) * ldy + e % q];
+        }
         cta_sync();
         for (int r = 0; r < nr; ++r) {
 #pragma unroll
@@ -561,6 +577,23 @@ __global__ void __launch_bounds__(256)
     for (int u = 0; u < XTY_PPT; ++u) {
         const int e = pair0 + u * 256 + tid;
         if (e < pq) part[(long long)blockIdx.x * pq + e] = acc[u];
+    }
+    if (!C) return;
+    // ---- the last CTA: C = partials summed in CTA order (reduce_parts' order)
+    if (!cta_last_arrival(counter, gridDim.x * gridDim.y)) return;
+    const int nparts = gridDim.x;
+    for (int e = tid; e < pq; e += 256) {
+        double t = 0.0;
+        int b = 0;
+        for (; b + XTY_AHEAD <= nparts; b += XTY_AHEAD) {
+            double v[XTY_AHEAD];
+#pragma unroll
+            for (int u = 0; u < XTY_AHEAD; ++u) v[u] = ld_cg(part + (long long)(b + u) * pq + e);
+#pragma unroll
+            for (int u = 0; u < XTY_AHEAD; ++u) t += v[u];
+        }
+        for (; b < nparts; ++b) t += ld_cg(part + (long long)b * pq + e);
+        C[e] = t;
     }
 }
 
@@ -587,14 +620,24 @@ int dcg_xty(dcg_context* ctx, cudaStream_t st, const double* X, long long ldx, c
     if (p <= 0 || q <= 0) return DCG_OK;
     if (p > DCG_MAX_T || q > DCG_MAX_T) return DCG_E_UNSUPPORTED;
     int nb = ctx->sm_count;
-    if (n < (long long)nb * XTY_ROWS) nb = (int)max(1LL, (n + XTY_ROWS - 1) / XTY_ROWS);
+    if (n < (long long)nb * 32) nb = (int)max(1LL, (n + 31) / 32);
     const int pq = p * q;
-    dim3 grid(nb, (pq + 256 * XTY_PPT - 1) / (256 * XTY_PPT));
-    const size_t smem = sizeof(double) * XTY_ROWS * (size_t)(p + q);
-    DCG_SMEM_ATTR(xty_kernel, smem);
-    xty_kernel<<<grid, 256, smem, st>>>(X, ldx, Y, ldy, n, p, q, scratch_parts);
-    DCG_LAUNCHED();
-    reduce_parts_kernel<<<(pq + 255) / 256, 256, 0, st>>>(scratch_parts, nb, pq, C);
+    dim3 grid(nb, (pq + 256 * 8 - 1) / (256 * 8));
+    // rows staged per round: the CTA's whole range when it fits 64 KB
+    const long long range = (n + nb - 1) / nb;
+    const long long cap = max(32LL, (long long)(65536 / (sizeof(double) * (p + q))));
+    const int cr = (int)max(1LL, min(range, cap));
+    const size_t smem = sizeof(double) * (size_t)cr * (size_t)(p + q);
+    // the last-arrival counter: the context's persistent line (reset by the last CTA)
+    unsigned int* counter = dcg_sync_line(ctx, DCG_SW_XTY);
+    if (pq <= 256) {
+        DCG_SMEM_ATTR(xty_kernel<1>, smem);
+        xty_kernel<1><<<dim3(nb, (pq + 255) / 256), 256, smem, st>>>(X, ldx, Y, ldy, n, p, q, cr, scratch_parts, C,
+                                                                    counter);
+    } else {
+        DCG_SMEM_ATTR(xty_kernel<8>, smem);
+        xty_kernel<8><<<grid, 256, smem, st>>>(X, ldx, Y, ldy, n, p, q, cr, scratch_parts, C, counter);
+    }
     DCG_LAUNCHED();
     return DCG_OK;
 }

@@ -47,11 +47,25 @@ struct dcg_context {
         long long* h;        // pinned staging copy (kept alive with d)
     } symtbl[4];
     int symtbl_next;
+    unsigned int* d_sync;    // persistent synchronisation words (dcg_sync_line), zeroed once
 };
 
 // device copy of the stored-Gram pass-1 range table tbl[b] = first tile of
 // CTA b of G (sym_tile_begin), cached per context
 const long long* dcg_sym_table(dcg_context* ctx, cudaStream_t st, long long n, int G);
+
+// ---- persistent synchronisation words ----------------------------------------
+// The grid-barrier counters and work counters of the cooperative kernels live
+// in a context-owned array that is zeroed once, not in the shared workspace:
+// every launch hands its words back at zero itself (dcg_sync_exit: the last
+// CTA out resets them), so no memset node precedes the launch -- a memset costs
+// ~3 us of stream time (node + launch gap) on the Newton step's critical path.
+// One 128-byte line per slot: word 0 (and 1, for a 64-bit counter) the barrier
+// or work counter, word 2 the exit counter.  A slot serves one kernel at a
+// time (the context is used by one stream at a time, as its workspace is).
+enum DcgSyncSlot { DCG_SW_SOLVE = 0, DCG_SW_ZSTAGE1, DCG_SW_TAIL, DCG_SW_APPLY, DCG_SW_APPLY2, DCG_SW_SBLOCK,
+                   DCG_SW_XTY, DCG_SW_NSLOTS };
+static inline unsigned int* dcg_sync_line(dcg_context* ctx, int slot) { return ctx->d_sync + 32 * slot; }
 
 // ---- status plumbing --------------------------------------------------------
 // Device-side status block written by single-CTA / persistent kernels.
@@ -263,6 +277,20 @@ __device__ __forceinline__ void dcg_grid_barrier(unsigned int* bar, unsigned int
         }
     }
     cta_sync();
+}
+
+// Called by ONE thread of every CTA once the CTA is done with line[0..1] (its
+// last grid barrier passed / its last counter draw made): the last CTA out
+// returns the line to zero for the next launch.  No CTA reads the counter
+// after its exit increment, so the reset cannot race a barrier poll.
+__device__ __forceinline__ void dcg_sync_exit(unsigned int* line, unsigned int nblocks) {
+    __threadfence();
+    if (atomicAdd(line + 2, 1u) == nblocks - 1) {
+        line[0] = 0u;
+        line[1] = 0u;
+        line[2] = 0u;
+        __threadfence();
+    }
 }
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {

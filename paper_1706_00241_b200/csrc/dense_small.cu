@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(SD_NT) gram_factor_kernel(const double* Graw, 
         const double tol = cta_pivot_tol(sub, na, nullptr, na, red);
         const int fail = cta_cholesky(sub, na, na, tol, L, na, s_scal);
         if (fail < 0) {
-            if (threadIdx.x == 0) { st->status = DCG_OK; st->count = na; }
+            if (threadIdx.x == 0) { st->status = DCG_OK; st->info = 0; st->count = na; }
             if (threadIdx.x < na) active[threadIdx.x] = s_act[threadIdx.x];
             return;
         }
@@ -1122,7 +1122,7 @@ __global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fr
         if (lane == 0) theta[j] = A[col * na + col];
     }
     if (tid < na) active[tid] = s_act[tid];
-    if (tid == 0) { st->status = DCG_OK; st->count = na; }
+    if (tid == 0) { st->status = DCG_OK; st->info = 0; st->count = na; }
     pencil_stamp(4);
     if (tid == 0) g_pencil_prof[6] = na;
 }

@@ -118,7 +118,7 @@ __device__ void zgather_body(long long n, int kp, const double* __restrict__ Wp,
         // fused stage: every CTA forms the norms and the keep list itself
         // after a grid barrier (same partial order: same values); CTA 0
         // publishes them with the plan
-        dcg_grid_barrier(counter + 2, gridDim.x);
+        dcg_grid_barrier(counter, gridDim.x);   // (coop: the context's persistent barrier line)
         zgather_finish(T, k, part, s_norm, s_keep, s_t, blockIdx.x == 0 ? norms : nullptr, keep, plan);
         return;
     }
@@ -241,12 +241,14 @@ __global__ void __launch_bounds__(EX_NT)
     zgather_body(n, kp, Wp, AWp, m, P, R, alpha, k, Zraw, AZraw, part, counter, norms, keep, plan, solve_st, true,
                  s_norm, s_keep, &s_t);
     const int t = s_t;
-    if (t < 0 || t < k) return;   // failed / deficient: uniform over the grid
-    const int T = solve_st ? (int)(solve_st->pad + solve_st->aux) : kp + m;
-    for (int y = 0; y < nregions; ++y) {
-        zscale_fg_body(n, Zraw, AZraw, s_norm, s_keep, T, t, y, Zs, AZs, fgpart);
-        cta_sync();
+    if (t >= 0 && t >= k) {   // else failed / deficient: uniform over the grid
+        const int T = solve_st ? (int)(solve_st->pad + solve_st->aux) : kp + m;
+        for (int y = 0; y < nregions; ++y) {
+            zscale_fg_body(n, Zraw, AZraw, s_norm, s_keep, T, t, y, Zs, AZs, fgpart);
+            cta_sync();
+        }
     }
+    if (threadIdx.x == 0) dcg_sync_exit(counter, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------- E3
@@ -374,7 +376,7 @@ __global__ void __launch_bounds__(EX_NT)
         cta_sync();
         for (int e = threadIdx.x; e < nr * Tk; e += EX_NT) {
             zr[e] = Zs[i0 * Tk + e];
-            ar[e] = AZs[i0 * Tk + e];
+            if (aw_next) ar[e] = AZs[i0 * Tk + e];
         }
         cta_sync();
         for (int e = threadIdx.x; e < nr * k; e += EX_NT) {
@@ -385,10 +387,10 @@ __global__ void __launch_bounds__(EX_NT)
             for (int c = 0; c < Tk; ++c) {
                 const double u = ue[c * k + j];
                 a = add_rn(a, mul_rn(z[c], u));
-                b = add_rn(b, mul_rn(az[c], u));
+                if (aw_next) b = add_rn(b, mul_rn(az[c], u));
             }
             w_next[(i0 + rr) * k + j] = a;
-            aw_next[(i0 + rr) * k + j] = b;
+            if (aw_next) aw_next[(i0 + rr) * k + j] = b;
         }
     }
     if (z_out) {
@@ -403,10 +405,10 @@ __global__ void __launch_bounds__(EX_NT)
 // the values of uscale's last CTA) and scales its shared copy of U, then
 // W_next / AW_next for its row blocks (each element as in wnext).  No U
 // round trip through global memory, one launch instead of two.
-__global__ void __launch_bounds__(EX_NT)
-    tail_coop_kernel(long long n, int k, const double* __restrict__ Zs, const double* __restrict__ AZs,
-                     const DevStatus* plan, const DevStatus* pencil, double* U, const int* active, double* part,
-                     unsigned int* bar, double* w_next, double* aw_next, long long* result) {
+__device__ __forceinline__ void tail_body(long long n, int k, const double* __restrict__ Zs,
+                                          const double* __restrict__ AZs, const DevStatus* plan,
+                                          const DevStatus* pencil, double* U, const int* active, double* part,
+                                          unsigned int* bar, double* w_next, double* aw_next, long long* result) {
     const bool ok = plan->status == DCG_OK && pencil->status == DCG_OK;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (plan->status != DCG_OK) {
@@ -488,23 +490,43 @@ __global__ void __launch_bounds__(EX_NT)
         cta_sync();
         for (int e = tid; e < nr * Tk; e += EX_NT) {
             zr[e] = Zs[i0 * Tk + e];
-            ar[e] = AZs[i0 * Tk + e];
+            if (aw_next) ar[e] = AZs[i0 * Tk + e];
         }
         cta_sync();
-        for (int e = tid; e < nr * k; e += EX_NT) {
-            const int rr = e / k, j = e - (e / k) * k;
-            const double* z = zr + rr * Tk;
-            const double* az = ar + rr * Tk;
-            double a = 0.0, b = 0.0;
-            for (int c = 0; c < Tk; ++c) {
-                const double u = ue[c * k + j];
-                a = add_rn(a, mul_rn(z[c], u));
-                b = add_rn(b, mul_rn(az[c], u));
+        if (aw_next) {
+            for (int e = tid; e < nr * k; e += EX_NT) {
+                const int rr = e / k, j = e - (e / k) * k;
+                const double* z = zr + rr * Tk;
+                const double* az = ar + rr * Tk;
+                double a = 0.0, b = 0.0;
+                for (int c = 0; c < Tk; ++c) {
+                    const double u = ue[c * k + j];
+                    a = add_rn(a, mul_rn(z[c], u));
+                    b = add_rn(b, mul_rn(az[c], u));
+                }
+                w_next[(i0 + rr) * k + j] = a;
+                aw_next[(i0 + rr) * k + j] = b;
             }
-            w_next[(i0 + rr) * k + j] = a;
-            aw_next[(i0 + rr) * k + j] = b;
+        } else {
+            // AW_next not wanted (the caller refreshes the basis against the
+            // next matrix before any use): W_next alone, same element order
+            for (int e = tid; e < nr * k; e += EX_NT) {
+                const int rr = e / k, j = e - (e / k) * k;
+                const double* z = zr + rr * Tk;
+                double a = 0.0;
+                for (int c = 0; c < Tk; ++c) a = add_rn(a, mul_rn(z[c], ue[c * k + j]));
+                w_next[(i0 + rr) * k + j] = a;
+            }
         }
     }
+}
+
+__global__ void __launch_bounds__(EX_NT)
+    tail_coop_kernel(long long n, int k, const double* __restrict__ Zs, const double* __restrict__ AZs,
+                     const DevStatus* plan, const DevStatus* pencil, double* U, const int* active, double* part,
+                     unsigned int* bar, double* w_next, double* aw_next, long long* result) {
+    tail_body(n, k, Zs, AZs, plan, pencil, U, active, part, bar, w_next, aw_next, result);
+    if (threadIdx.x == 0) dcg_sync_exit(bar, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------- launch
@@ -563,8 +585,9 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
     if (n < (long long)nb * EX_ROWS) nb = (int)max(1LL, (n + EX_ROWS - 1) / EX_ROWS);
     const size_t sm1 = sizeof(double) * 2 * EX_ROWS * T;
     if (stage == 0 || stage == 1) {
-    DCG_CUDA(cudaMemsetAsync(plan, 0, al(sizeof(DevStatus)) * 2, st));
-    DCG_CUDA(cudaMemsetAsync(counters, 0, 16, st));
+    // (no memset of plan / pencil: every path of zgather and of the pencil
+    // writes the fields that are read; the cooperative launches' barrier words
+    // are the context's persistent lines)
     // regions of 64 x 128 (a, b') entries; Tk <= T decides on the device which are live
     int gy = (int)(((T + 16 * FG_BI - 1) / (16 * FG_BI)) * ((2 * T + 16 * FG_BJ - 1) / (16 * FG_BJ)));
     // one cooperative launch when the grid is co-resident (it is: nb <= SMs)
@@ -577,13 +600,15 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
     }
     if ((long long)per_sm * G >= nb) {
         int ikp = (int)kp, im = (int)m, ik = (int)k;
+        unsigned int* line = dcg_sync_line(ctx, DCG_SW_ZSTAGE1);
         void* args[] = {(void*)&n,    (void*)&ikp,   (void*)&Wp,     (void*)&AWp,   (void*)&im,      (void*)&P,
                         (void*)&R,    (void*)&alpha, (void*)&ik,     (void*)&Zraw,  (void*)&AZraw,   (void*)&part,
-                        (void*)&counters, (void*)&norms, (void*)&keep, (void*)&plan, (void*)&solve_st, (void*)&gy,
+                        (void*)&line, (void*)&norms, (void*)&keep, (void*)&plan, (void*)&solve_st, (void*)&gy,
                         (void*)&Zs,   (void*)&AZs,   (void*)&fgpart};
         DCG_CUDA(cudaLaunchCooperativeKernel((const void*)zstage1_coop_kernel, dim3(nb), dim3(EX_NT), args, sm1, st));
         dcg_count_launch();
     } else {
+        DCG_CUDA(cudaMemsetAsync(counters, 0, 16, st));   // the last-arrival counters (workspace)
         DCG_CUDA(cudaFuncSetAttribute(zgather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
         zgather_kernel<<<nb, EX_NT, sm1, st>>>(n, (int)kp, Wp, AWp, (int)m, P, R, alpha, (int)k, Zraw, AZraw, part,
                                                counters, norms, keep, plan, solve_st);
@@ -614,9 +639,8 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
             if (rc) return rc;
         }
         if ((long long)per_sm * G >= nb) {
-            DCG_CUDA(cudaMemsetAsync(counters + 3, 0, sizeof(unsigned int), st));
             int ik = (int)k;
-            unsigned int* bar = counters + 3;
+            unsigned int* bar = dcg_sync_line(ctx, DCG_SW_TAIL);
             void* args[] = {(void*)&n,      (void*)&ik,     (void*)&Zs,      (void*)&AZs,      (void*)&plan,
                             (void*)&pencil, (void*)&U,      (void*)&active,  (void*)&upart,    (void*)&bar,
                             (void*)&d_w_next, (void*)&d_aw_next, (void*)&d_result};
@@ -626,6 +650,7 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
             return DCG_OK;
         }
     }
+    DCG_CUDA(cudaMemsetAsync(counters + 1, 0, sizeof(unsigned int), st));   // uscale's last-arrival counter
     const size_t sm5 = sizeof(double) * ((size_t)T * k + 16 * 64 + (size_t)EX_ROWS * T);
     DCG_CUDA(cudaFuncSetAttribute(uscale_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm5));
     uscale_kernel<<<nb, EX_NT, sm5, st>>>(n, (int)k, Zs, plan, pencil, U, active, Uexp, upart, counters + 1);

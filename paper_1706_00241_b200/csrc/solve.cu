@@ -174,8 +174,21 @@ __host__ __device__ __forceinline__ long long gemv_region_doubles(int strat, lon
     return min(n, (long long)DCG_QT) + 2 + DCG_NW * DCG_RB;
 }
 
+// Every exit writes the whole status block (the block is not cleared before
+// the launch: in the asynchronous form it is the caller's buffer).
+__device__ __forceinline__ void put_status(DevStatus* st, int status, int k, long long info, long long count,
+                                           long long aux, double value, double value2) {
+    st->status = status;
+    st->pad = k;
+    st->info = info;
+    st->count = count;
+    st->aux = aux;
+    st->value = value;
+    st->value2 = value2;
+}
+
 template <int STRAT>
-__global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
+__device__ __forceinline__ void solve_body(const SolveArgs& a) {
 #define GSYNC() dcg_grid_barrier(a.bar, gridDim.x)
     // Phase timers (DCG_PHASE_TIMERS): CTA 0 / thread 0 attributes the time since
     // the previous mark to phase `id`; one predicated branch when disabled.
@@ -377,13 +390,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         if constexpr (kPk) sym_ring_drain(s_g, ring_seq, pending);
         if (blockIdx.x == 0 && tid == 0) {
             a.history[0] = 0.0;
-            a.st->status = DCG_OK;
-            a.st->pad = k;
-            a.st->info = 0;
-            a.st->count = 0;   // iterations
-            a.st->aux = 0;     // stored
-            a.st->value = 0.0;
-            a.st->value2 = 0.0;
+            put_status(a.st, DCG_OK, k, 0, 0, 0, 0.0, 0.0);   // 0 iterations, 0 stored
         }
         return;
     }
@@ -465,10 +472,7 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         if (d <= 0.0) {   // solvers.py:170-172 (NaN falls through, as in numpy)
             if constexpr (kPk) sym_ring_drain(s_g, ring_seq, pending);
             if (blockIdx.x == 0 && tid == 0) {
-                a.st->status = DCG_E_BREAKDOWN;
-                a.st->pad = k;
-                a.st->info = it;
-                a.st->count = it;
+                put_status(a.st, DCG_E_BREAKDOWN, k, it, it, 0, 0.0, 0.0);
             }
             return;
         }
@@ -543,15 +547,15 @@ __global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
         PHASE(12);
     }
     if constexpr (kPk) sym_ring_drain(s_g, ring_seq, pending);
-    if (blockIdx.x == 0 && tid == 0) {
-        a.st->status = DCG_OK;
-        a.st->pad = k;
-        a.st->info = 0;
-        a.st->count = it;
-        a.st->aux = (it < ell) ? it : ell;
-        a.st->value = rel;
-        a.st->value2 = norm_b;
-    }
+    if (blockIdx.x == 0 && tid == 0) put_status(a.st, DCG_OK, k, 0, it, (it < ell) ? it : ell, rel, norm_b);
+}
+
+// The persistent kernel: the solve, then the last CTA out hands the barrier
+// words back at zero (dcg_sync_exit) for the next launch.
+template <int STRAT>
+__global__ void __launch_bounds__(DCG_NT, 1) dcg_solve_kernel(SolveArgs a) {
+    solve_body<STRAT>(a);
+    if (threadIdx.x == 0) dcg_sync_exit(a.bar, gridDim.x);
 }
 
 }  // namespace
@@ -692,9 +696,12 @@ static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, co
     else if (strat == STRAT_SYMPK) DCG_SMEM_ATTR(dcg_solve_kernel<STRAT_SYMPK>, smem);
     else if (strat == STRAT_SYM) DCG_SMEM_ATTR(dcg_solve_kernel<STRAT_SYM>, smem);
     else DCG_SMEM_ATTR(dcg_solve_kernel<STRAT_ROWS>, smem);
-    // the status block and the barrier words share one 256-byte line: one memset
-    a.bar = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(a.st) + 128);   // inside the st line
-    DCG_CUDA(cudaMemsetAsync(a.st, 0, 128 + 2 * sizeof(unsigned int), st));
+    // no memset before the launch: the barrier words are the context's
+    // persistent line (returned to zero by the kernel), and the kernel writes
+    // the whole status block -- in the asynchronous form straight into the
+    // caller's block (no device-to-device copy behind the kernel)
+    a.bar = dcg_sync_line(ctx, DCG_SW_SOLVE);
+    if (d_status) a.st = static_cast<DevStatus*>(d_status);
     // DCG_PHASE_TIMERS=1: per-phase device time of CTA 0 printed per solve
     // (developer diagnostic; costs one predicated branch per phase otherwise).
     unsigned long long*& d_timers = g_phase_timers;
@@ -709,12 +716,7 @@ static int solve_impl(dcg_context* ctx, void* stream, const dcg_operator* op, co
     if (!d_status) DCG_CUDA(cudaEventRecord(ctx->ev0, st));   // synchronous form: device_ms
     DCG_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(DCG_NT), args, smem, st));
     dcg_count_launch();
-    if (d_status) {
-        // asynchronous form: the status block (and the column count used, in
-        // its `pad` word) is copied out in stream order; nothing waits here
-        DCG_CUDA(cudaMemcpyAsync(d_status, a.st, sizeof(DevStatus), cudaMemcpyDeviceToDevice, st));
-        return DCG_OK;
-    }
+    if (d_status) return DCG_OK;   // asynchronous form: nothing waits here
     DCG_CUDA(cudaEventRecord(ctx->ev1, st));
     rc = dcg_host_reserve(ctx, sizeof(DevStatus));
     if (rc) return rc;

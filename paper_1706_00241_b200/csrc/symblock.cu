@@ -205,6 +205,8 @@ __global__ void __launch_bounds__(SB_NT, 1)
                 }
                 if (done) break;
             }
+            // this CTA draws no more: the last producer out zeroes the counter
+            dcg_sync_exit(reinterpret_cast<unsigned int*>(counter), gridDim.x);
         }
         return;
     }
@@ -400,8 +402,9 @@ static int sb_apply(dcg_context* ctx, cudaStream_t st, const double* Kp, long lo
     double* V = scratch;
     double* RP = V + ((NB * C::VBLK + 31) & ~31LL);
     double* CP = RP + NU * SB_R * C::SLOT;
-    unsigned long long* counter = reinterpret_cast<unsigned long long*>(CP + NU * SB_R * C::SLOT);
-    DCG_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
+    // the unit counter: the context's persistent line (words 0-1), handed back
+    // at zero by the kernel -- no memset
+    unsigned long long* counter = reinterpret_cast<unsigned long long*>(dcg_sync_line(ctx, DCG_SW_SBLOCK));
     sb_pack_v_kernel<KP><<<ctx->sm_count * 4, 256, 0, st>>>(X, k, s_in, n, NB, V);
     DCG_LAUNCHED();
     const size_t smem = sizeof(double) * C::STAGES * C::STAGE + 2 * C::STAGES * sizeof(unsigned long long) +

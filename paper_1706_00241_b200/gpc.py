@@ -413,7 +413,7 @@ def _pipelined_loop(state, psi_prev, cfg, newton_tol, max_newton, k, selection):
     for it in range(1, max_newton + 1):
         t0 = time.perf_counter()
         x, job = solve_next_async(seq, system.a_matrix, system.b, ax0=system.ax0, ax0_of=system.x_prev,
-                                  prepared=prepared, extract=it < max_newton)
+                                  prepared=prepared, extract=it < max_newton, need_aw=False)
         new_state, objective = _update_dev_async(state, system.inner, system.sqrt_h, x)
         # the next system and its solve's first product A_next x in one K pass
         next_system = build_newton_system(new_state, x_prev=x) if it < max_newton else None

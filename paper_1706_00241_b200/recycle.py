@@ -364,7 +364,7 @@ def prepare_refresh(job, a_next):
     return _PreparedRefresh(job.pending, op, *_enqueue_refresh(job.pending, op, op.n, torch.cuda.current_stream()))
 
 
-def solve_next_async(state, a, b, ax0=None, ax0_of=None, prepared=None, extract=True):
+def solve_next_async(state, a, b, ax0=None, ax0_of=None, prepared=None, extract=True, need_aw=True):
     """Enqueue refresh + solve of the next system of a sequence and the
     extraction of the basis after it (device data only, nothing waits).
     Returns (x, job); job.finish() completes the report and the new state.
@@ -374,7 +374,10 @@ def solve_next_async(state, a, b, ax0=None, ax0_of=None, prepared=None, extract=
     prepare_refresh (used when it matches this state's basis and operator).
     ``extract=False``: the caller will not solve another system of the
     sequence (gpc's last Newton step), so the next basis is not extracted;
-    the returned state then carries no basis."""
+    the returned state then carries no basis.  ``need_aw=False``: the caller
+    refreshes the next basis against its next matrix before any use (gpc's
+    Newton loop: A changes every step), so the extraction's AW_next for the
+    current matrix is not formed (the basis then carries no AW)."""
     op = as_operator(a)
     bd = D.to_dev(b, 1)
     n = bd.shape[0]
@@ -427,11 +430,13 @@ def solve_next_async(state, a, b, ax0=None, ax0_of=None, prepared=None, extract=
         # (the Newton update's K-products leave the pencil an SM of its own).
         k = state.k
         theta = D.empty(k)
-        w_next, aw_next = D.empty(n, k), D.empty(n, k)
+        w_next = D.empty(n, k)
+        aw_next = D.empty(n, k) if need_aw else None
         result = torch.empty(4, dtype=torch.int64, device=D.device())
         sel = N.DCG_SELECT_LARGEST if state.selection == SELECT_LARGEST else N.DCG_SELECT_SMALLEST
         args = (D.ctx(1), None, n, ctypes.byref(clog), status.data_ptr(), ctypes.byref(cb) if cb is not None else None,
-                k, sel, theta.data_ptr(), w_next.data_ptr(), aw_next.data_ptr(), result.data_ptr())
+                k, sel, theta.data_ptr(), w_next.data_ptr(), aw_next.data_ptr() if need_aw else None,
+                result.data_ptr())
         N.check(N.lib().dcg_ritz_extract_dev(*args[:1], main.cuda_stream, *args[2:], 1), 0, "ritz_extract_dev")
         gathered = torch.cuda.Event()
         gathered.record()
