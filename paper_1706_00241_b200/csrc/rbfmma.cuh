@@ -14,13 +14,14 @@
 // (tools/fp64_peak.cu: 37 vs 34 TFLOP/s, a DMMA+DFMA mix takes the sum of the
 // two times), so the contraction still costs d FMAs per element; what DMMA
 // removes is the issue and operand-load overhead of the FMA form.
-// The exponential is table-based: e = k ln2 / 256 + r, |r| <= ln2 / 512,
-//   exp(e) = 2^(k >> 8) * T[k & 255] * (1 + p(r)),   T[j] = 2^(j / 256),
-// with p the degree-4 Taylor polynomial of expm1 (truncation < 3.8e-17), k from
-// the 1.5 * 2^52 rounding trick: 9 FP64 instructions per element.  The clamp
+// The exponential is table-based: e = k ln2 / 2048 + r, |r| <= ln2 / 4096,
+//   exp(e) = 2^(k >> 11) * T[k & 2047] * (1 + p(r)),   T[j] = 2^(j / 2048),
+// with p the degree-3 Taylor polynomial of expm1 (truncation < 3.5e-17), k from
+// the 1.5 * 2^52 rounding trick, r from one FMA: 7 FP64 instructions per
+// element.  The clamp
 // that keeps intermediates normal (e >= -700) is compiled only into the path
 // taken when the data's largest norm allows an exponent below -690.  With the
-// two accumulations (row sums and column sums) an element costs ~d + 15 FP64
+// two accumulations (row sums and column sums) an element costs ~d + 10 FP64
 // pipe operations, against ~130 issued instructions of the FMA-form kernel.
 //
 // Work decomposition: the lower-triangle 64 x 64 tile sequence of the stored
@@ -92,12 +93,12 @@ static __global__ void rbf_prep_kernel(RbfMma p) {
 }
 
 // ---- shared-memory layout ----------------------------------------------------
-// CTA header (doubles): exp table (64), mbarriers (4 per team), team sequence
+// CTA header (doubles): exp table (RM_TAB), mbarriers (4 per team), team sequence
 // words, range table (RM_MAX_TEAMS x 255 + 1 longs); then per team: XI frags
 // (64 dp), XJ frags x2, I pairs {b, v'} (128), J pairs x2 (256), row-flush
 // buffer (8 x 64).
-#define RM_TAB 256
-#define RM_HDR 784
+#define RM_TAB 2048
+#define RM_HDR 2576
 __host__ __device__ __forceinline__ long long rm_team_doubles(int dp) { return 3LL * RM_TB * dp + 128 + 256 + RM_TW * RM_TB; }
 __host__ __device__ __forceinline__ long long rm_smem_doubles(int dim, int nteam) {
     return RM_HDR + nteam * rm_team_doubles(rm_dpad(dim));
@@ -166,27 +167,29 @@ __device__ __forceinline__ void rm_bar_wait(unsigned long long* bar, unsigned pa
         : "memory");
 }
 
-// exp(x), table T in shared memory: k = rint(256 x / ln 2) via the 1.5 * 2^52
-// shift, r = x - k ln2/256 with a two-part constant, expm1(r) by its degree-4
-// Taylor polynomial, result T[k & 255] (1 + expm1 r) scaled by 2^(k >> 8) in
-// the exponent field; ~1 ulp.  The exponent-field scaling needs a normal
-// result: CLAMP bounds x below by -700 (e^-700 ~ 1e-304 then stands in for
-// smaller values), compiled only into the path for data that can reach it.
+// exp(x), table T[j] = 2^(j / 2048) in shared memory: k = rint(2048 x / ln 2)
+// via the 1.5 * 2^52 shift, r = x - k ln2/2048 (|r| <= ln2/4096: one FMA with
+// the rounded constant, whose relative error 3.3e-17 puts |x| * 3.3e-17 on
+// the result -- below an ulp for the entries that carry the sums), expm1(r)
+// by its degree-3 Taylor polynomial (truncation r^4/24 < 3.5e-17), result
+// T[k & 2047] (1 + expm1 r) scaled by 2^(k >> 11) in the exponent field: 7
+// FP64 operations (the 256-entry, degree-4, two-constant form took 9).  The
+// exponent-field scaling needs a normal result: CLAMP bounds x below by -700
+// (e^-700 ~ 1e-304 then stands in for smaller values), compiled only into the
+// path for data that can reach it.
 template <bool CLAMP>
 __device__ __forceinline__ double rm_exp(double x, const double* tab) {
     if constexpr (CLAMP) x = fmax(x, -700.0);
-    const double t = fma(x, 369.3299304675746, 6755399441055744.0);
+    const double t = fma(x, 2954.639443740597, 6755399441055744.0);
     const double kf = t - 6755399441055744.0;
-    double r = fma(kf, -0.0027076061740622863, x);
-    r = fma(kf, -9.058776616587108e-20, r);
+    const double r = fma(kf, -0.0003384507717577858, x);
     const int ki = __double2loint(t);
-    double q = fma(r, 4.1666666666666667e-02, 1.6666666666666667e-01);
-    q = fma(q, r, 0.5);
+    const double q = fma(r, 1.6666666666666667e-01, 0.5);
     const double r2 = r * r;
     const double pm = fma(q, r2, r);
-    const double tj = tab[ki & 255];
+    const double tj = tab[ki & (RM_TAB - 1)];
     const double res = fma(tj, pm, tj);
-    return __hiloint2double(__double2hiint(res) + (ki >> 8) * 1048576, __double2loint(res));
+    return __hiloint2double(__double2hiint(res) + (ki >> 11) * 1048576, __double2loint(res));
 }
 
 // Once per launch (all CTA threads): exp table, mbarriers, team range table.
