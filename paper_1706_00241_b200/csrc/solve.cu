@@ -127,17 +127,18 @@ __device__ __forceinline__ void reduce_partials(const double* partials, int G, i
     const int v = tid & (sw - 1), gq = tid / sw;
     double a = 0.0;
     if (v < nslots) {
-        // up to 8 independent loads in flight per thread (one latency round for
-        // G <= 8 * 512 / sw CTAs)
-        for (int g0 = gq; g0 < G; g0 += 8 * ng) {
-            double t[8];
+        // up to 16 independent loads in flight per thread (one latency round
+        // for G <= 16 * 512 / sw CTAs: 148 CTAs with up to 32 slots); the adds
+        // keep the ascending-g order
+        for (int g0 = gq; g0 < G; g0 += 16 * ng) {
+            double t[16];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < 16; ++u) {
                 const int g = g0 + u * ng;
                 t[u] = (g < G) ? ld_cg(partials + (long long)g * ps + v) : 0.0;
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) a += t[u];
+            for (int u = 0; u < 16; ++u) a += t[u];
         }
     }
     if (sw <= 32) {
