@@ -26,7 +26,7 @@
 // A, L: row-major with leading dimensions; L's upper triangle is zeroed.
 // Returns -1 on success or the failing pivot index.  All CTA threads call.
 // ---------------------------------------------------------------------------
-__device__ int cta_cholesky(const double* A, int lda, int n, double pivot_tol, double* L, int ldl,
+__device__ __forceinline__ int cta_cholesky(const double* A, int lda, int n, double pivot_tol, double* L, int ldl,
                             double* s_scal) {
     // Right-looking in place in L: after column t is final, every trailing
     // element (i, c), t < c <= i, subtracts L_it L_ct.  Each element therefore
@@ -69,7 +69,7 @@ __device__ int cta_cholesky(const double* A, int lda, int n, double pivot_tol, d
 }
 
 // 1e-14 * max(max(diag), 0)   (linalg.py:74-76), diag of A restricted to idx[0..n)
-__device__ double cta_pivot_tol(const double* A, int lda, const int* idx, int n, double* red) {
+__device__ __forceinline__ double cta_pivot_tol(const double* A, int lda, const int* idx, int n, double* red) {
     double m = -INFINITY;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const int ii = idx ? idx[i] : i;
@@ -83,7 +83,7 @@ __device__ double cta_pivot_tol(const double* A, int lda, const int* idx, int n,
 // Warp-level forward substitution: y = L^-1 b for one right-hand side
 // (b, y with strides), reference order per element (_core.pyx:69-80).
 // Lanes own rows lane + 32u.
-static __device__ void warp_solve_lower(const double* L, int ldl, int n, const double* b, int bstride,
+static __device__ __forceinline__ void warp_solve_lower(const double* L, int ldl, int n, const double* b, int bstride,
                                  double* y, int ystride) {
     const int lane = threadIdx.x & 31;
     double a[(DCG_MAX_T + 31) / 32];
@@ -119,8 +119,8 @@ static __device__ void warp_solve_lower(const double* L, int ldl, int n, const d
 // order, unfused, then one division -- so the results are bit-identical; the
 // chain is per thread instead of a warp shuffle per step.  B(i, c) =
 // B[i * brs + c * bcs], Y(i, c) = Y[i * yrs + c * ycs].
-static __device__ void cta_solve_lower_cols(const double* L, int n, const double* B, int brs, int bcs, double* Y,
-                                            int yrs, int ycs) {
+static __device__ __forceinline__ void cta_solve_lower_cols(const double* L, int n, const double* B, int brs, int bcs,
+                                                            double* Y, int yrs, int ycs) {
     for (int c = threadIdx.x; c < n; c += blockDim.x) {
         for (int i = 0; i < n; ++i) {
             double a = B[i * brs + c * bcs];
@@ -132,7 +132,7 @@ static __device__ void cta_solve_lower_cols(const double* L, int n, const double
 }
 
 // Warp-level back substitution x = L^-T b (wavefront order).
-static __device__ void warp_solve_lower_trans(const double* L, int ldl, int n, const double* b, int bstride,
+static __device__ __forceinline__ void warp_solve_lower_trans(const double* L, int ldl, int n, const double* b, int bstride,
                                        double* x, int xstride) {
     const int lane = threadIdx.x & 31;
     double a[(DCG_MAX_T + 31) / 32];
@@ -658,7 +658,7 @@ __device__ __forceinline__ double rcp_nr(double q) {
     return fma(r, e, r);
 }
 
-__device__ int pencil_tridiag_fast(double* C, int n, int k, int largest, double* V, int ldv, double* lam, double* ws) {
+__device__ __forceinline__ int pencil_tridiag_fast(double* C, int n, int k, int largest, double* V, int ldv, double* lam, double* ws) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     __shared__ double s_sc[4];
     __shared__ int s_ok;
@@ -770,21 +770,44 @@ __device__ int pencil_tridiag_fast(double* C, int n, int k, int largest, double*
     // with the same rounding per step (one fused product each), and the same
     // pivmin clamp (|q_i| < pivmin -> q_i = -pivmin); a step's latency is one
     // FMA instead of a division.  |p| is kept in [2^-200, 2^200].
+    // The power-of-two rescaling is exact and the clamp is relative, so WHEN
+    // it is applied changes no sign and no count (only the p values, by powers
+    // of two): with the pivot floor at or above 2^-400 a step moves |p| by at
+    // most 2^100 up or 2^-400 down (|p_i / p_i-1| <= 2 ||T|| + e^2 / pivmin,
+    // >= pivmin), so checking every second step keeps every value normal; the
+    // check then leaves the FP64 chain on every other step.
+    const bool two_step = pivmin >= 0x1p-400 && tnrm <= 0x1p90;
+    auto step = [&](int i, double sigma, double& p, double& pp, int& c) {
+        double pn = fma(d[i] - sigma, p, -(e2[i] * pp));
+        if (fabs(pn) < pivmin * fabs(p)) pn = -pivmin * p;
+        c += (pn < 0.0) != (p < 0.0);
+        pp = p;
+        p = pn;
+    };
+    auto rescale = [&](double& p, double& pp) {
+        const double ap = fabs(p);
+        if (ap > 0x1p200) { p *= 0x1p-200; pp *= 0x1p-200; }
+        else if (ap < 0x1p-200) { p *= 0x1p200; pp *= 0x1p200; }
+    };
     auto count_below = [&](double sigma) {
         int c = 0;
         double pp = 1.0;
         double p = d[0] - sigma;
         if (fabs(p) < pivmin) p = -pivmin;
         c += p < 0.0;
-        for (int i = 1; i < n; ++i) {
-            double pn = fma(d[i] - sigma, p, -(e2[i] * pp));
-            if (fabs(pn) < pivmin * fabs(p)) pn = -pivmin * p;
-            c += (pn < 0.0) != (p < 0.0);
-            pp = p;
-            p = pn;
-            const double ap = fabs(p);
-            if (ap > 0x1p200) { p *= 0x1p-200; pp *= 0x1p-200; }
-            else if (ap < 0x1p-200) { p *= 0x1p200; pp *= 0x1p200; }
+        if (two_step) {
+            int i = 1;
+            for (; i + 1 < n; i += 2) {
+                step(i, sigma, p, pp, c);
+                step(i + 1, sigma, p, pp, c);
+                rescale(p, pp);
+            }
+            if (i < n) step(i, sigma, p, pp, c);
+        } else {
+            for (int i = 1; i < n; ++i) {
+                step(i, sigma, p, pp, c);
+                rescale(p, pp);
+            }
         }
         return c;
     };
@@ -922,10 +945,15 @@ __device__ int pencil_tridiag_fast(double* C, int n, int k, int largest, double*
 // `plan` (when non-null) carries the pencil order T (= count) decided on the
 // device by the extraction's zero-column scan, and its status: the kernel does
 // nothing unless that status is DCG_OK, so the pipeline needs no host sync.
-__global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fraw, const double* Graw, int T,
-                                                            int k, int largest, int max_sweeps,
-                                                            double* wk, double* theta, double* U,
-                                                            int* active, DevStatus* st, const DevStatus* plan) {
+// STAGED (T <= DCG_PENCIL_SMEM_T, every pencil the solver forms): the working
+// matrices' pointers derive from the shared array at compile time, so every
+// access is a shared-memory instruction -- through a pointer that may be
+// either, the compiler emits generic loads (longer latency on each link of
+// the serial chains).
+template <bool STAGED>
+__device__ __forceinline__ void pencil_body(const double* Fraw, const double* Graw, int T, int k, int largest,
+                                            int max_sweeps, double* wk, double* theta, double* U, int* active,
+                                            DevStatus* st) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[40];
     __shared__ double s_scal[4];
@@ -934,10 +962,6 @@ __global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fr
     __shared__ int s_act[DCG_MAX_T];
     __shared__ int s_order[DCG_MAX_T];
     __shared__ int s_na;
-    if (plan) {
-        if (plan->status != DCG_OK) return;
-        T = (int)plan->count;
-    }
     pencil_stamp(0);
     if (threadIdx.x == 0)
         for (int i = 7; i < 15; ++i) g_pencil_prof[i] = 0;
@@ -949,10 +973,19 @@ __global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fr
     // slots S0 = Fa then V, S1 = L, S2 = Ga then Y (in place), S3 = A.
     double* F = wk;
     double* G = F + T * T;
-    const bool staged = T <= DCG_PENCIL_SMEM_T;
-    double* L = staged ? sm + T * T : G + T * T;
-    double* Y = staged ? sm + 2 * T * T : L + T * T;
-    double* Fa = staged ? sm : Y + T * T;
+    constexpr bool staged = STAGED;
+    double* L;
+    double* Y;
+    double* Fa;
+    if constexpr (STAGED) {
+        L = sm + T * T;
+        Y = sm + 2 * T * T;
+        Fa = sm;
+    } else {
+        L = G + T * T;
+        Y = L + T * T;
+        Fa = Y + T * T;
+    }
     for (int e = tid; e < T * T; e += blockDim.x) {
         const int i = e / T, j = e % T;
         F[e] = mul_rn(0.5, add_rn(Fraw[i * T + j], Fraw[j * T + i]));
@@ -984,8 +1017,15 @@ __global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fr
         cta_sync();
     }
     pencil_stamp(1);
-    double* A = staged ? sm + 3 * T * T : sm;
-    double* V = staged ? sm : sm + T * T;
+    double* A;
+    double* V;
+    if constexpr (STAGED) {
+        A = sm + 3 * T * T;
+        V = sm;
+    } else {
+        A = sm;
+        V = sm + T * T;
+    }
     const int off = largest ? (na - k) : 0;
     // ---- fast path: C = L^-1 G L^-T, tridiagonal eigensolver for the k
     // selected pairs (pencil_tridiag_fast); Jacobi below when it declines
@@ -1127,10 +1167,38 @@ __global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fr
     if (tid == 0) g_pencil_prof[6] = na;
 }
 
+__global__ void __launch_bounds__(PENCIL_NT) ritz_pencil_kernel(const double* Fraw, const double* Graw, int T,
+                                                            int k, int largest, int max_sweeps,
+                                                            double* wk, double* theta, double* U,
+                                                            int* active, DevStatus* st, const DevStatus* plan) {
+    // `plan` (when non-null) carries the pencil order decided on the device
+    if (plan) {
+        if (plan->status != DCG_OK) return;
+        T = (int)plan->count;
+    }
+    if (T <= DCG_PENCIL_SMEM_T) pencil_body<true>(Fraw, Graw, T, k, largest, max_sweeps, wk, theta, U, active, st);
+    else pencil_body<false>(Fraw, Graw, T, k, largest, max_sweeps, wk, theta, U, active, st);
+}
+
 extern "C" __attribute__((visibility("default"))) int dcg_debug_set_pencil_fast(int on) {
     const int v = on ? 1 : 0;
     if (cudaMemcpyToSymbol(g_pencil_fast, &v, sizeof(int)) != cudaSuccess) return DCG_E_CUDA;
     return DCG_OK;
+}
+
+int dcg_ritz_pencil_launch(cudaStream_t st, const double* Fraw, const double* Graw, int T, int k, int largest,
+                           int max_sweeps, double* wk, double* theta, double* U, int* active, DevStatus* ds,
+                           const DevStatus* plan);
+// developer entry (tools/pencil_bench.py): the Ritz pencil alone on device
+// inputs -- Fraw, Graw (T x T), wk (5 T^2), theta (k), U (T x k), active (T),
+// status (one DevStatus) -- enqueued on `stream`
+extern "C" __attribute__((visibility("default"))) int dcg_debug_ritz_pencil(void* stream, const double* Fraw,
+                                                                          const double* Graw, int T, int k,
+                                                                          int largest, double* wk, double* theta,
+                                                                          double* U, int* active, void* status) {
+    if (T < 1 || T > DCG_MAX_T || k < 1 || k > T) return DCG_E_CONFIG;
+    return dcg_ritz_pencil_launch(static_cast<cudaStream_t>(stream), Fraw, Graw, T, k, largest, 60, wk, theta, U,
+                                  active, static_cast<DevStatus*>(status), nullptr);
 }
 
 extern "C" __attribute__((visibility("default"))) int dcg_debug_pencil_profile(long long* out8) {
