@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(EX_NT)
                         const double* __restrict__ P, const double* __restrict__ R, const double* __restrict__ alpha,
                         int k, double* Zraw, double* AZraw, double* part, unsigned int* counter, double* norms,
                         int* keep, DevStatus* plan, const DevStatus* solve_st, int nregions, double* Zs, double* AZs,
-                        double* fgpart) {
+                        double* fgpart, double* Fraw, double* Graw) {
     __shared__ double s_norm[DCG_MAX_T];
     __shared__ int s_keep[DCG_MAX_T];
     __shared__ int s_t;
@@ -246,6 +246,21 @@ __global__ void __launch_bounds__(EX_NT)
         for (int y = 0; y < nregions; ++y) {
             zscale_fg_body(n, Zraw, AZraw, s_norm, s_keep, T, t, y, Zs, AZs, fgpart);
             cta_sync();
+        }
+        // E3 after a second grid barrier: F and G from the partials, a warp
+        // per entry with fg_reduce_kernel's lane split and warp sum (the same
+        // values), the entries spread over every warp of the grid
+        dcg_grid_barrier(counter, gridDim.x);
+        const int npairs = 2 * t * t, lane = threadIdx.x & 31;
+        const int nwarps = gridDim.x * (EX_NT / 32);
+        for (int e = blockIdx.x * (EX_NT / 32) + (threadIdx.x >> 5); e < npairs; e += nwarps) {
+            double sv = 0.0;
+            for (int b = lane; b < (int)gridDim.x; b += 32) sv += ld_cg(fgpart + (long long)b * npairs + e);
+            sv = warp_sum(sv);
+            if (lane == 0) {
+                if (e < t * t) Fraw[e] = sv;
+                else Graw[e - t * t] = sv;
+            }
         }
     }
     if (threadIdx.x == 0) dcg_sync_exit(counter, gridDim.x);
@@ -604,7 +619,7 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
         void* args[] = {(void*)&n,    (void*)&ikp,   (void*)&Wp,     (void*)&AWp,   (void*)&im,      (void*)&P,
                         (void*)&R,    (void*)&alpha, (void*)&ik,     (void*)&Zraw,  (void*)&AZraw,   (void*)&part,
                         (void*)&line, (void*)&norms, (void*)&keep, (void*)&plan, (void*)&solve_st, (void*)&gy,
-                        (void*)&Zs,   (void*)&AZs,   (void*)&fgpart};
+                        (void*)&Zs,   (void*)&AZs,   (void*)&fgpart, (void*)&Fraw, (void*)&Graw};
         DCG_CUDA(cudaLaunchCooperativeKernel((const void*)zstage1_coop_kernel, dim3(nb), dim3(EX_NT), args, sm1, st));
         dcg_count_launch();
     } else {
@@ -616,10 +631,10 @@ static int extract_enqueue(dcg_context* ctx, cudaStream_t st, long long n, const
         DCG_CUDA(cudaFuncSetAttribute(zscale_fg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
         zscale_fg_kernel<<<dim3(nb, gy), EX_NT, sm1, st>>>(n, Zraw, AZraw, norms, keep, plan, Zs, AZs, fgpart);
         DCG_LAUNCHED();
+        const int warps = (int)(2 * T * T);
+        fg_reduce_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>(fgpart, nb, plan, Fraw, Graw);
+        DCG_LAUNCHED();
     }
-    const int warps = (int)(2 * T * T);
-    fg_reduce_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>(fgpart, nb, plan, Fraw, Graw);
-    DCG_LAUNCHED();
     }
     if (stage == 1) return DCG_OK;
     if (stage != 4) {

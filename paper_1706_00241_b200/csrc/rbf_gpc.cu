@@ -185,9 +185,14 @@ __device__ __forceinline__ double logaddexp0(double z) {
     return tmp;   // NaN
 }
 
-// grad/h for f; per-CTA partials of  -sum logaddexp(0, -y f)  and  f'a (a may be NULL)
+__device__ void derivs_finalize_body(const double* part, int nb, DevStatus* st, double* llpsi);
+
+// grad/h for f; per-CTA partials of  -sum logaddexp(0, -y f)  and  f'a (a may be NULL).
+// With `last` (the context's persistent counter) the last CTA to finish also
+// runs the finalisation (derivs_finalize_kernel's thread split and sums: the
+// same values), one launch instead of two.
 __global__ void derivs_kernel(long long n, const double* f, const double* y, const double* a, double* grad,
-                              double* h, double* part) {
+                              double* h, double* part, unsigned int* last, DevStatus* st, double* llpsi) {
     __shared__ double red[40];
     double ll = 0.0, fa = 0.0, bad = 0.0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -208,15 +213,17 @@ __global__ void derivs_kernel(long long n, const double* f, const double* y, con
         part[2 * blockIdx.x + 1] = fa;
         part[2 * gridDim.x + blockIdx.x] = bad;
     }
+    if (!last) return;
+    if (cta_last_arrival(last, gridDim.x)) derivs_finalize_body(part, gridDim.x, st, llpsi);
 }
 
-__global__ void derivs_finalize_kernel(const double* part, int nb, DevStatus* st, double* llpsi) {
+__device__ void derivs_finalize_body(const double* part, int nb, DevStatus* st, double* llpsi) {
     __shared__ double red[40];
     double ll = 0.0, fa = 0.0, bad = 0.0;
     for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-        ll += part[2 * b];
-        fa += part[2 * b + 1];
-        bad += part[2 * nb + b];
+        ll += ld_cg(part + 2 * b);
+        fa += ld_cg(part + 2 * b + 1);
+        bad += ld_cg(part + 2 * nb + b);
     }
     ll = block_sum(ll, red);
     fa = block_sum(fa, red);
@@ -232,6 +239,10 @@ __global__ void derivs_finalize_kernel(const double* part, int nb, DevStatus* st
             llpsi[1] = st->value2;
         }
     }
+}
+
+__global__ void derivs_finalize_kernel(const double* part, int nb, DevStatus* st, double* llpsi) {
+    derivs_finalize_body(part, nb, st, llpsi);
 }
 
 // s = sqrt(h); inner = h f + grad   (gpc.py:177,181)
@@ -268,9 +279,9 @@ int dcg_derivs_launch(dcg_context* ctx, cudaStream_t st, long long n, const doub
                       const double* a, double* grad, double* h, double* part, DevStatus* ds, double* llpsi) {
     int nb = ctx->sm_count * 2;
     if ((long long)nb * 256 > n) nb = (int)max(1LL, (n + 255) / 256);
-    derivs_kernel<<<nb, 256, 0, st>>>(n, f, y, a, grad, h, part);
-    DCG_LAUNCHED();
-    derivs_finalize_kernel<<<1, 256, 0, st>>>(part, nb, ds, llpsi);
+    // partials, then the finalisation by the last CTA (its arrival counter:
+    // the context's persistent line, reset by that CTA)
+    derivs_kernel<<<nb, 256, 0, st>>>(n, f, y, a, grad, h, part, dcg_sync_line(ctx, DCG_SW_DERIVS), ds, llpsi);
     DCG_LAUNCHED();
     return DCG_OK;
 }
