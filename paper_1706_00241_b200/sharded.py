@@ -613,11 +613,10 @@ def sharded_extract(log: ShardLog, prev: ShardBasis | None, k: int, selection: s
         pb = RecycleBasis.__new__(RecycleBasis)
         pb.w_dev, pb.aw_dev, pb.chol_dev = prev.w, prev.aw, prev.chol
     ext = _extract_dev(flog, pb, int(k), selection)
-    if ext.w_next.shape[1] == 0:
+    # the device tensors (the RitzExtraction's numpy properties copy to the host)
+    if ext.w_next_dev.shape[1] == 0:
         return None
-    w_next = ext.w_next if isinstance(ext.w_next, torch.Tensor) else D.to_dev(ext.w_next, 2)
-    aw_next = ext.aw_next if isinstance(ext.aw_next, torch.Tensor) else D.to_dev(ext.aw_next, 2)
-    return ShardBasis(w_next.contiguous(), aw_next.contiguous(), be.empty(0, 0))
+    return ShardBasis(ext.w_next_dev.contiguous(), ext.aw_next_dev.contiguous(), be.empty(0, 0))
 
 
 @dataclass
