@@ -180,17 +180,26 @@ __global__ void __launch_bounds__(DCG_NT, 1)
 // t_i (all n rows) from this share's partials: column partials of the tiles
 // (I', I), I' > I, inside [t_lo, t_hi), and the row segments of tile row I
 // that start inside it (at J = 0 or at a team range start).  Rows without
-// contributions get 0.  One thread per row; consecutive rows read
-// consecutive partial entries.
-__global__ void sym_pass2_share_kernel(long long n, long long t_lo, long long t_hi, const long long* tbl, int R,
-                                       const double* colpart, const double* rowpart, double* t,
-                                       const dcg_shard_state* gate) {
+// contributions get 0.  A 256-thread CTA takes 32 consecutive rows at a time
+// (lane = row: a warp's loads of one tile's partials are one 256-byte line);
+// its 8 warps each sum every eighth tile of the column (sixteen loads in
+// flight ahead of their in-order adds) and every eighth range start, and the
+// eight sums are combined in warp order -- a fixed order, and the longest
+// dependent chain is an eighth of the column (row 0 of a whole triangle at
+// n = 5 10^4 has 781 partials: one thread per row took 83 us per product).
+#define P2S_SUBS 8
+__global__ void __launch_bounds__(32 * P2S_SUBS)
+    sym_pass2_share_kernel(long long n, long long t_lo, long long t_hi, const long long* tbl, int R,
+                           const double* colpart, const double* rowpart, double* t, const dcg_shard_state* gate) {
     if (gate && gate->done) return;
+    __shared__ double red[P2S_SUBS][32];
     const long long NT = sym_ntiles_side(n);
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long I = i / RM_TB;
-        const int rl = (int)(i - I * RM_TB);
+    const int lane = threadIdx.x & 31, sub = threadIdx.x >> 5;
+    const long long ngroups = (n + 31) / 32;
+    for (long long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        const long long i = grp * 32 + lane;
+        const long long I = (grp * 32) / RM_TB;          // uniform per group
+        const int rl = (int)(i - I * RM_TB);             // < 64: the partial arrays hold whole tiles
         double acc = 0.0;
         // column partials: tile id base(I') + I in [t_lo, t_hi), I' > I
         long long Ip = I + 1;
@@ -200,32 +209,40 @@ __global__ void sym_pass2_share_kernel(long long n, long long t_lo, long long t_
             if (sym_tile_row_base(c) < need) ++c;
             if (c > Ip) Ip = c;
         }
-        // tiles (Ip, I) while inside the share, sixteen loads in flight ahead
-        // of their (in-order) adds
+        Ip += sub;
         long long id = sym_tile_row_base(Ip) + I;
         while (Ip < NT && id < t_hi) {
             double v[16];
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
                 v[u] = 0.0;
-                if (Ip + u < NT && id < t_hi) {
+                if (Ip + P2S_SUBS * u < NT && id < t_hi) {
                     v[u] = ld_cg(colpart + (id - t_lo) * RM_TB + rl);
-                    id += Ip + u + 1;   // base(Ip + u + 1) - base(Ip + u)
+                    // base(r + 8) - base(r) = 8 r + 36
+                    id += P2S_SUBS * (Ip + P2S_SUBS * u) + P2S_SUBS * (P2S_SUBS + 1) / 2;
                 }
             }
 #pragma unroll
             for (int u = 0; u < 16; ++u) acc += v[u];
-            Ip += 16;
+            Ip += 16 * P2S_SUBS;
         }
         // row segments of tile row I
         const long long base = sym_tile_row_base(I);
-        if (base >= t_lo && base < t_hi) acc += ld_cg(rowpart + (base - t_lo) * RM_TB + rl);
-        for (int b = 0; b < R; ++b) {   // team range starts inside the row (tbl[0] = t_lo may be one)
+        if (sub == 0 && base >= t_lo && base < t_hi) acc += ld_cg(rowpart + (base - t_lo) * RM_TB + rl);
+        for (int b = sub; b < R; b += P2S_SUBS) {   // team range starts inside the row (tbl[0] = t_lo may be one)
             const long long st = tbl[b];
             if (st > base && st <= base + I && st < t_hi && (b == 0 || st > tbl[b - 1]))
                 acc += ld_cg(rowpart + (st - t_lo) * RM_TB + rl);
         }
-        t[i] = acc;
+        red[sub][lane] = acc;
+        __syncthreads();
+        if (sub == 0 && i < n) {
+            double a = red[0][lane];
+#pragma unroll
+            for (int q = 1; q < P2S_SUBS; ++q) a += red[q][lane];
+            t[i] = a;
+        }
+        __syncthreads();
     }
 }
 
@@ -287,7 +304,7 @@ extern "C" int dcg_shard_tiles_partial(dcg_context* ctx, void* stream, const dcg
                                                                tbl, d_state);
         DCG_LAUNCHED();
     }
-    sym_pass2_share_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(n, t_lo, t_hi, tbl, G, colpart, rowpart, d_t, d_state);
+    sym_pass2_share_kernel<<<ctx->sm_count * 4, 32 * P2S_SUBS, 0, st>>>(n, t_lo, t_hi, tbl, G, colpart, rowpart, d_t, d_state);
     DCG_LAUNCHED();
     return DCG_OK;
 }
@@ -320,9 +337,9 @@ extern "C" int dcg_shard_tiles_partial2(dcg_context* ctx, void* stream, const dc
                                                                rowpart, tbl, nullptr, d_v2, part2);
         DCG_LAUNCHED();
     }
-    sym_pass2_share_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(n, t_lo, t_hi, tbl, G, colpart, rowpart, d_t1, nullptr);
+    sym_pass2_share_kernel<<<ctx->sm_count * 4, 32 * P2S_SUBS, 0, st>>>(n, t_lo, t_hi, tbl, G, colpart, rowpart, d_t1, nullptr);
     DCG_LAUNCHED();
-    sym_pass2_share_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(n, t_lo, t_hi, tbl, G, colpart + part2,
+    sym_pass2_share_kernel<<<ctx->sm_count * 4, 32 * P2S_SUBS, 0, st>>>(n, t_lo, t_hi, tbl, G, colpart + part2,
                                                               rowpart + part2, d_t2, nullptr);
     DCG_LAUNCHED();
     return DCG_OK;
@@ -365,7 +382,7 @@ extern "C" int dcg_shard_rbf_sym_partial(dcg_context* ctx, void* stream, const d
     DCG_CUDA(cudaFuncSetAttribute(rbf_mma_pass1_share_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     rbf_mma_pass1_share_kernel<<<G, DCG_NT, smem, st>>>(p, d_v, op->d_s, colpart, rowpart, tbl, d_state);
     DCG_LAUNCHED();
-    sym_pass2_share_kernel<<<ctx->sm_count * 4, 256, 0, st>>>(n, t_lo, t_hi, tbl, G * nteam, colpart, rowpart, d_t,
+    sym_pass2_share_kernel<<<ctx->sm_count * 4, 32 * P2S_SUBS, 0, st>>>(n, t_lo, t_hi, tbl, G * nteam, colpart, rowpart, d_t,
                                                               d_state);
     DCG_LAUNCHED();
     return DCG_OK;
