@@ -38,9 +38,10 @@ int shard_ws(dcg_context* ctx, cudaStream_t st, int G, int ps, ShardWs* w) {
     if (rc) return rc;
     char* base = static_cast<char*>(ctx->ws);
     w->parts = reinterpret_cast<double*>(base);
-    w->counter = reinterpret_cast<unsigned int*>(base + al(sizeof(double) * (size_t)G * ps));
-    // the workspace is shared with the other entry points: start from zero
-    DCG_CUDA(cudaMemsetAsync(w->counter, 0, 16, st));
+    // the arrival counter is one of the context's persistent words: the last
+    // CTA to arrive returns it to zero (cta_last_arrival), so no memset per launch
+    w->counter = dcg_sync_line(ctx, DCG_SW_SHARD);
+    (void)st;
     return DCG_OK;
 }
 
@@ -58,8 +59,10 @@ __device__ void cta_row_partials(long long r0, long long r1, int k, const double
     double c = 0.0;
     if (k > 0) {
         const int j = tid & (swk - 1), grp = tid / swk, ngrp = SH_NT / swk;
-        if (j < k)
-            for (long long i = r0 + grp; i < r1; i += ngrp) c = fma(M[i * k + j], w[i], c);
+        if (j < k) {
+#pragma unroll 8
+            for (long long i = r0 + grp; i < r1; i += ngrp) c = fma(__ldg(M + i * k + j), w[i], c);
+        }
         if (swk < 32)
             for (int o = swk; o < 32; o <<= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     }
@@ -97,9 +100,19 @@ __device__ bool grid_reduce_slots(const double* mine, int nslots, double* parts,
     for (int v = threadIdx.x; v < nslots; v += blockDim.x) parts[(long long)blockIdx.x * ps + v] = mine[v];
     const bool last = cta_last_arrival(counter, gridDim.x);
     if (last) {
+        // 32 loads in flight ahead of their in-order adds (one thread per slot:
+        // a load per add had put ~150 L2 latencies in a row on every kernel's tail)
         for (int v = threadIdx.x; v < nslots; v += blockDim.x) {
             double t = 0.0;
-            for (int b = 0; b < (int)gridDim.x; ++b) t += ld_cg(parts + (long long)b * ps + v);
+            for (int b0 = 0; b0 < (int)gridDim.x; b0 += 32) {
+                double q[32];
+#pragma unroll
+                for (int u = 0; u < 32; ++u)
+                    q[u] = (b0 + u < (int)gridDim.x) ? ld_cg(parts + (long long)(b0 + u) * ps + v) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 32; ++u)
+                    if (b0 + u < (int)gridDim.x) t += q[u];
+            }
             out[v] = t;
         }
     }
@@ -108,7 +121,13 @@ __device__ bool grid_reduce_slots(const double* mine, int nslots, double* parts,
 
 // mu = L^-T L^-1 c by warp 0 (forward substitution in the reference order,
 // backward sweep as a wavefront), then a CTA barrier.  L in shared memory.
+// Pivots are applied as reciprocals 1 / L_jj formed once per call (at most one
+// extra rounding per unknown, as in the single-GPU solve kernel, solve.cu):
+// a serial FP64 division per unknown is ~100 cycles on the dependent chain.
 __device__ void cta_chol_solve(const double* L, int k, const double* c, double* mu) {
+    __shared__ double s_rd[DCG_MAX_K];
+    for (int j = threadIdx.x; j < k; j += blockDim.x) s_rd[j] = 1.0 / L[j * k + j];
+    cta_sync();
     if ((threadIdx.x >> 5) == 0) {
         const int lane = threadIdx.x & 31;
         const int i0 = lane, i1 = lane + 32;
@@ -116,7 +135,7 @@ __device__ void cta_chol_solve(const double* L, int k, const double* c, double* 
         double a1 = (i1 < k) ? c[i1] : 0.0;
         for (int j = 0; j < k; ++j) {
             const double accj = __shfl_sync(0xffffffffu, (j < 32) ? a0 : a1, j & 31);
-            const double yj = div_rn(accj, L[j * k + j]);
+            const double yj = mul_rn(accj, s_rd[j]);
             if (lane == (j & 31)) {
                 if (j < 32) a0 = yj; else a1 = yj;
             }
@@ -125,7 +144,7 @@ __device__ void cta_chol_solve(const double* L, int k, const double* c, double* 
         }
         for (int j = k - 1; j >= 0; --j) {
             const double accj = __shfl_sync(0xffffffffu, (j < 32) ? a0 : a1, j & 31);
-            const double xj = div_rn(accj, L[j * k + j]);
+            const double xj = mul_rn(accj, s_rd[j]);
             if (lane == (j & 31)) {
                 if (j < 32) a0 = xj; else a1 = xj;
             }
