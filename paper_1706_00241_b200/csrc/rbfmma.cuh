@@ -39,6 +39,9 @@
 #include "common.cuh"
 #include "symgemv.cuh"
 
+#ifndef RM_GB
+#define RM_GB 4                  // accumulator blocks per DMMA / exponential group (of 8 per warp tile)
+#endif
 #define RM_TB 64                 // tile side
 #define RM_TW 8                  // warps per team
 #define RM_TT (RM_TW * 32)       // threads per team
@@ -236,34 +239,37 @@ __device__ __forceinline__ void rm_tile(const RmTeamSmem& S, const double* xj, i
     }
     const double2* xi2 = reinterpret_cast<const double2*>(S.xi);
     const double2* xj2 = reinterpret_cast<const double2*>(xj);
-    for (int ch = 0; ch < nch; ++ch) {
-        const double2 bf = xj2[(w * nch + ch) * 32 + lane];
+    // Two halves of four accumulator blocks: the exponentials of one half have
+    // the other half's DMMAs to overlap with (same operation order per element
+    // and per sum as the all-DMMAs-first form).
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            double2 af[4];
+    for (int h = 0; h < 8 / RM_GB; ++h) {
+        for (int ch = 0; ch < nch; ++ch) {
+            const double2 bf = xj2[(w * nch + ch) * 32 + lane];
+            double2 af[RM_GB];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) af[u] = xi2[((4 * h + u) * nch + ch) * 32 + lane];
+            for (int u = 0; u < RM_GB; ++u) af[u] = xi2[((RM_GB * h + u) * nch + ch) * 32 + lane];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) rm_dmma(c[4 * h + u][0], c[4 * h + u][1], af[u].x, bf.x);
+            for (int u = 0; u < RM_GB; ++u) rm_dmma(c[RM_GB * h + u][0], c[RM_GB * h + u][1], af[u].x, bf.x);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) rm_dmma(c[4 * h + u][0], c[4 * h + u][1], af[u].y, bf.y);
+            for (int u = 0; u < RM_GB; ++u) rm_dmma(c[RM_GB * h + u][0], c[RM_GB * h + u][1], af[u].y, bf.y);
         }
-    }
 #pragma unroll
-    for (int rb = 0; rb < 8; ++rb) {
-        double k0 = rm_exp<CLAMP>(c[rb][0], tab);
-        double k1 = rm_exp<CLAMP>(c[rb][1], tab);
-        if constexpr (DIAG) {
-            if (rb == w) {
-                if (r == 2 * q) k0 = diag;
-                if (r == 2 * q + 1) k1 = diag;
+        for (int rb = RM_GB * h; rb < RM_GB * h + RM_GB; ++rb) {
+            double k0 = rm_exp<CLAMP>(c[rb][0], tab);
+            double k1 = rm_exp<CLAMP>(c[rb][1], tab);
+            if constexpr (DIAG) {
+                if (rb == w) {
+                    if (r == 2 * q) k0 = diag;
+                    if (r == 2 * q + 1) k1 = diag;
+                }
             }
+            rowp[rb] = fma(k0, pJ0.y, rowp[rb]);
+            rowp[rb] = fma(k1, pJ1.y, rowp[rb]);
+            const double vI = S.pi[2 * (8 * rb + r) + 1];
+            col0 = fma(k0, vI, col0);
+            col1 = fma(k1, vI, col1);
         }
-        rowp[rb] = fma(k0, pJ0.y, rowp[rb]);
-        rowp[rb] = fma(k1, pJ1.y, rowp[rb]);
-        const double vI = S.pi[2 * (8 * rb + r) + 1];
-        col0 = fma(k0, vI, col0);
-        col1 = fma(k1, vI, col1);
     }
 }
 
