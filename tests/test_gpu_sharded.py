@@ -181,6 +181,29 @@ def test_sharded_sequence_matches_single_gpu(P, rng):
         assert np.linalg.norm(x.cpu().numpy() - x_ref) <= 1e-8 * np.linalg.norm(x_ref)
 
 
+def test_sharded_sequence_keeps_the_basis_on_the_device(P, rng, monkeypatch):
+    """The sharded sequence hands W_next / AW_next from the extraction to the
+    next refresh as device tensors: the RitzExtraction's numpy properties (a
+    device -> host copy each; 2 x 12.8 MB per step at config 3) must not be
+    touched on that path."""
+    from paper_1706_00241_b200 import recycle as R
+    from paper_1706_00241_b200.sharded import SelfComm, ShardSequenceState, sharded_solve_next
+
+    def boom(self):
+        raise AssertionError("host copy of the next basis on the sharded path")
+
+    for name in ("w_next", "aw_next", "z", "u", "theta"):
+        monkeypatch.setattr(R.RitzExtraction, name, property(boom))
+    n = 300
+    a0 = random_spd(rng, n, kappa=30.0)
+    cfg = P.SolverConfig(tol=1e-9, ell=10)
+    sst = ShardSequenceState(k=5, cfg=cfg, selection="largest")
+    for i in range(3):
+        a = a0 + 0.05 * i * np.eye(n)
+        _, sst = sharded_solve_next(sst, slab_op(a, 1, 0, P), dev(rng.standard_normal(n)), SelfComm())
+    assert sst.basis is not None and sst.basis.k == 5 and sst.basis.w.is_cuda
+
+
 def test_sharded_laplace_newton_world1_matches_gpc(P):
     """The sharded GPC Newton driver at world = 1 against laplace_newton on
     the config-1 inputs: iteration counts +-1 per step, psi within 1e-8."""
