@@ -407,6 +407,18 @@ DCG_API int dcg_shard_direction(dcg_context* ctx, void* stream, long long rows, 
                                 const double* d_r, double* d_p, dcg_shard_state* d_state,
                                 double* d_history, double* d_log_p, double* d_log_mu,
                                 double* d_log_beta);
+/* The vector phases of one iteration of _run_loop (solvers.py:169-191) on
+ * replicated vectors (the tile-share path: rows = n on every rank) in ONE
+ * cooperative launch: Ap = shift p + s (.) t with d_t the all-reduced
+ * K (s (.) p), d = p'Ap, alpha, x, r, [r'r, AW'r], beta, mu, p, history and
+ * logs -- dcg_shard_epilogue(0) + dcg_shard_update(0) + dcg_shard_direction
+ * with two grid barriers instead of three launches.  No-op if state->done.   */
+DCG_API int dcg_shard_step(dcg_context* ctx, void* stream, long long rows, int k, const double* d_t,
+                           const double* d_s, double shift, double* d_x, double* d_r, double* d_p,
+                           double* d_ap, const double* d_w, const double* d_aw, const double* d_chol,
+                           dcg_shard_state* d_state, double* d_history, double* d_log_r,
+                           double* d_log_p, double* d_log_d, double* d_log_alpha, double* d_log_beta,
+                           double* d_log_mu);
 
 /* ---- L5b: sharded matrix-free products in the symmetric form (config 5) -- *
  * Rank `rank` of `world` evaluates an equal-cost share of the lower-triangle

@@ -236,6 +236,8 @@ SIGNATURES = {
     "dcg_shard_begin": [_P, _P, _LL, ctypes.c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "dcg_shard_update": [_P, _P, ctypes.c_int, _LL, ctypes.c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "dcg_shard_direction": [_P, _P, _LL, ctypes.c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "dcg_shard_step": [_P, _P, _LL, ctypes.c_int, _P, _P, ctypes.c_double, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                       _P, _P, _P, _P],
 }
 
 # dcg_shard_state (include/defcg_b200.h): 7 doubles then 9 int64, 128 bytes

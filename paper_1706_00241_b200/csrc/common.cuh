@@ -64,7 +64,7 @@ const long long* dcg_sym_table(dcg_context* ctx, cudaStream_t st, long long n, i
 // or work counter, word 2 the exit counter.  A slot serves one kernel at a
 // time (the context is used by one stream at a time, as its workspace is).
 enum DcgSyncSlot { DCG_SW_SOLVE = 0, DCG_SW_ZSTAGE1, DCG_SW_TAIL, DCG_SW_APPLY, DCG_SW_APPLY2, DCG_SW_SBLOCK,
-                   DCG_SW_XTY, DCG_SW_DERIVS, DCG_SW_SHARD, DCG_SW_NSLOTS };
+                   DCG_SW_XTY, DCG_SW_DERIVS, DCG_SW_SHARD, DCG_SW_SHARDSTEP, DCG_SW_NSLOTS };
 static inline unsigned int* dcg_sync_line(dcg_context* ctx, int slot) { return ctx->d_sync + 32 * slot; }
 
 // ---- status plumbing --------------------------------------------------------

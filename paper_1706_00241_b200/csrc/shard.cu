@@ -157,9 +157,26 @@ __device__ void cta_chol_solve(const double* L, int k, const double* c, double* 
     cta_sync();
 }
 
+// sum_j M[i][j] v[j] in ascending j; the row's loads are issued eight ahead of
+// their FMAs (16-byte loads when the row allows it): one L2 latency per eight
+// terms instead of one per term
 __device__ __forceinline__ double row_dot(const double* M, long long i, int k, const double* v) {
+    const double* row = M + i * k;
     double t = 0.0;
-    for (int j = 0; j < k; ++j) t = fma(M[i * k + j], v[j], t);
+    int j = 0;
+    if ((k & 1) == 0 && (reinterpret_cast<uintptr_t>(M) & 15) == 0) {
+        for (; j + 8 <= k; j += 8) {
+            double2 m[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) m[u] = __ldg(reinterpret_cast<const double2*>(row + j) + u);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                t = fma(m[u].x, v[j + 2 * u], t);
+                t = fma(m[u].y, v[j + 2 * u + 1], t);
+            }
+        }
+    }
+    for (; j < k; ++j) t = fma(__ldg(row + j), v[j], t);
     return t;
 }
 
@@ -418,6 +435,161 @@ __global__ void __launch_bounds__(SH_NT)
     }
 }
 
+// ---------------------------------------------------------------------------
+// One def-CG iteration's vector phases in ONE cooperative launch (replicated
+// vectors: the tile-share path, where the all-reduced t = K (s (.) p) is the
+// only exchange of the iteration): the epilogue Ap = shift p + s (.) t and
+// p'Ap, [grid barrier] alpha, x, r, [r'r, AW'r], [grid barrier] beta, mu, p --
+// the work of dcg_shard_epilogue(0) + dcg_shard_update(0) +
+// dcg_shard_direction in one launch (~50 -> ~20 us at n = 5 10^4, k = 32).
+// Every CTA reduces the per-CTA partials itself in CTA order (the order of
+// grid_reduce_slots), so all CTAs -- and all ranks, whose t is bitwise the
+// same -- hold the same scalars.  The state is read by every CTA before the
+// first barrier and written by CTA 0 after the second.
+// ---------------------------------------------------------------------------
+struct StepArgs {
+    long long rows;
+    int k, ps;
+    const double* t;
+    const double* s;
+    double shift;
+    double *x, *r, *p, *ap;
+    const double *W, *AW, *Lg;
+    dcg_shard_state* state;
+    double* history;
+    double *log_r, *log_p, *log_d, *log_alpha, *log_beta, *log_mu;
+    double* parts;        // G x ps
+    double* dparts;       // gepi p'Ap partials
+    int gepi;             // CTAs of dcg_shard_epilogue's row partition
+    unsigned int* bar;    // the context's persistent barrier line
+};
+
+// out[v] = sum over CTAs (in CTA order) of parts[b * ps + v], v < nslots, by every CTA
+__device__ __forceinline__ void step_reduce(const double* parts, int ps, int nslots, double* out) {
+    for (int v = threadIdx.x; v < nslots; v += blockDim.x) {
+        double t = 0.0;
+        for (int b0 = 0; b0 < (int)gridDim.x; b0 += 32) {
+            double q[32];
+#pragma unroll
+            for (int u = 0; u < 32; ++u)
+                q[u] = (b0 + u < (int)gridDim.x) ? ld_cg(parts + (long long)(b0 + u) * ps + v) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 32; ++u)
+                if (b0 + u < (int)gridDim.x) t += q[u];
+        }
+        out[v] = t;
+    }
+    cta_sync();
+}
+
+__global__ void __launch_bounds__(SH_NT) shard_step_kernel(StepArgs a) {
+    __shared__ double s_scr[SH_NT];
+    __shared__ double s_tmp[40];
+    __shared__ double s_out[DCG_MAX_K + 2];
+    __shared__ double s_red[DCG_MAX_K + 2];
+    __shared__ double s_L[DCG_MAX_K * DCG_MAX_K];
+    __shared__ double s_mu[DCG_MAX_K];
+    const dcg_shard_state st = *a.state;   // every CTA reads the state before the first barrier
+    if (st.done) return;                   // uniform: nobody arrives at a barrier
+    const int k = a.k, tid = threadIdx.x;
+    const long long rows = a.rows;
+    const long long r0 = part_begin(rows, gridDim.x, blockIdx.x), r1 = part_begin(rows, gridDim.x, blockIdx.x + 1);
+    const long long it = st.it, ell = st.ell;
+    if (k > 0)
+        for (int e = tid; e < k * k; e += blockDim.x) s_L[e] = a.Lg[e];
+    // ---- Ap and the p'Ap partials: over the epilogue kernel's row partition
+    // (a.gepi virtual CTAs, taken blockIdx.x, + gridDim.x, ...), so that d is
+    // bitwise the three-launch path's
+    for (int vb = blockIdx.x; vb < a.gepi; vb += gridDim.x) {
+        const long long e0 = part_begin(rows, a.gepi, vb), e1 = part_begin(rows, a.gepi, vb + 1);
+        double dot = 0.0;
+        for (long long i = e0 + tid; i < e1; i += blockDim.x) {
+            const double ti = ld_cg(a.t + i);
+            const double pi = a.p[i];
+            const double ax = a.s ? add_rn(mul_rn(a.shift, pi), mul_rn(a.s[i], ti)) : add_rn(mul_rn(a.shift, pi), ti);
+            a.ap[i] = ax;
+            dot = fma(pi, ax, dot);
+        }
+        dot = block_sum(dot, s_tmp);
+        if (tid == 0) a.dparts[vb] = dot;
+    }
+    dcg_grid_barrier(a.bar, gridDim.x);
+    {
+        // sum of the a.gepi partials in order, by every CTA (thread 0; 32 loads in flight)
+        if (tid == 0) {
+            double t = 0.0;
+            for (int b0 = 0; b0 < a.gepi; b0 += 32) {
+                double q[32];
+#pragma unroll
+                for (int u = 0; u < 32; ++u) q[u] = (b0 + u < a.gepi) ? ld_cg(a.dparts + b0 + u) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 32; ++u)
+                    if (b0 + u < a.gepi) t += q[u];
+            }
+            s_red[0] = t;
+        }
+        cta_sync();
+    }
+    const double d = s_red[0];
+    if (!(d > 0.0) && !(d != d)) {   // solvers.py:170-172: d <= 0 (NaN falls through, as in numpy)
+        if (blockIdx.x == 0 && tid == 0) {
+            a.state->status = DCG_E_BREAKDOWN;
+            a.state->info = it;
+            a.state->done = 1;
+        }
+        if (tid == 0) dcg_sync_exit(a.bar, gridDim.x);
+        return;
+    }
+    const double alpha = st.rr / d;
+    // ---- x, r and [r'r, AW'r] -----------------------------------------------
+    const bool log = a.log_r && it < ell;
+    for (long long i = r0 + tid; i < r1; i += blockDim.x) {
+        a.x[i] = add_rn(a.x[i], mul_rn(alpha, a.p[i]));
+        const double ri = sub_rn(a.r[i], mul_rn(alpha, ld_cg(a.ap + i)));   // (another CTA's epilogue rows)
+        a.r[i] = ri;
+        if (log) a.log_r[(it + 1) * rows + i] = ri;
+    }
+    cta_sync();
+    cta_row_partials(r0, r1, k, a.r, a.r, a.AW, s_out, s_scr, s_tmp);
+    cta_sync();   // (x / r loop readers of ap; s_red's d has been read by everyone)
+    for (int v = tid; v < 1 + k; v += blockDim.x) a.parts[(long long)blockIdx.x * a.ps + v] = s_out[v];
+    dcg_grid_barrier(a.bar, gridDim.x);
+    step_reduce(a.parts, a.ps, 1 + k, s_red);
+    // ---- beta, mu, p -----------------------------------------------------------
+    const long long itn = it + 1;
+    const double rr_new = s_red[0];
+    const double beta = rr_new / st.rr;
+    const double rel = sqrt(rr_new) / st.norm_b;
+    const bool cont = (rel > st.tol) && (itn < st.max_iters);
+    const bool log_pn = cont && itn < ell && a.log_p;
+    if (k > 0) cta_chol_solve(s_L, k, s_red + 1, s_mu);
+    for (long long i = r0 + tid; i < r1; i += blockDim.x) {
+        const double ri = a.r[i];
+        const double pi = k > 0 ? sub_rn(add_rn(mul_rn(beta, a.p[i]), ri), row_dot(a.W, i, k, s_mu))   // beta*p + r - W mu
+                                : add_rn(ri, mul_rn(beta, a.p[i]));                                    // r + beta*p
+        a.p[i] = pi;
+        if (log_pn) a.log_p[itn * rows + i] = pi;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        if (it < ell && a.log_d) {
+            a.log_d[it] = d;
+            a.log_alpha[it] = alpha;
+        }
+        a.history[itn] = rel;
+        if (itn - 1 < ell && a.log_beta) a.log_beta[itn - 1] = beta;
+        if (log_pn && k > 0 && a.log_mu)
+            for (int j = 0; j < k; ++j) a.log_mu[itn * k + j] = s_mu[j];
+        a.state->alpha = alpha;
+        a.state->d = d;
+        a.state->it = itn;
+        a.state->rr = rr_new;
+        a.state->beta = beta;
+        a.state->rel = rel;
+        a.state->done = cont ? 0 : 1;
+    }
+    if (tid == 0) dcg_sync_exit(a.bar, gridDim.x);
+}
+
 int check_slab(const dcg_operator* op) {
     if (!op || op->kind != DCG_OP_DENSE) return DCG_E_CONFIG;
     if (op->n < 0 || op->row0 < 0 || op->rows < 0 || op->row0 + op->rows > op->n) return DCG_E_CONFIG;
@@ -493,6 +665,59 @@ extern "C" int dcg_shard_epilogue(dcg_context* ctx, void* stream, int mode, cons
     shard_rbf_epi_kernel<<<(unsigned)G, DCG_NT, 0, st>>>(mode, op->rows, op->row0, d_v, op->d_s, op->shift, d_b,
                                                            d_t + op->row0, d_out, mode == 0 ? d_part : nullptr, w.parts,
                                                            2, w.counter, d_state);
+    DCG_LAUNCHED();
+    return DCG_OK;
+}
+
+// The vector phases of one iteration on replicated vectors in one cooperative
+// launch (see shard_step_kernel): d_t = the all-reduced K (s (.) p) (all rows),
+// s / shift the operator's scaling (A = shift I + s K s), logs optional.
+extern "C" int dcg_shard_step(dcg_context* ctx, void* stream, long long rows, int k, const double* d_t,
+                              const double* d_s, double shift, double* d_x, double* d_r, double* d_p, double* d_ap,
+                              const double* d_w, const double* d_aw, const double* d_chol, dcg_shard_state* d_state,
+                              double* d_history, double* d_log_r, double* d_log_p, double* d_log_d,
+                              double* d_log_alpha, double* d_log_beta, double* d_log_mu) {
+    if (!ctx || rows < 0 || k < 0 || !d_t || !d_x || !d_r || !d_p || !d_ap || !d_state || !d_history)
+        return DCG_E_CONFIG;
+    if (k > 0 && (!d_w || !d_aw || !d_chol)) return DCG_E_CONFIG;
+    if (k > DCG_MAX_K) return DCG_E_UNSUPPORTED;
+    if (d_log_r && (!d_log_d || !d_log_alpha)) return DCG_E_CONFIG;
+    if (rows == 0) return DCG_E_UNSUPPORTED;
+    cudaStream_t st = as_stream(stream);
+    const int G = shard_grid(ctx, rows), ps = slot_stride(k);
+    long long gepi = ctx->sm_count;   // dcg_shard_epilogue's grid
+    if (gepi > rows) gepi = rows;
+    const size_t bytes = al(sizeof(double) * (size_t)G * ps) + al(sizeof(double) * (size_t)gepi);
+    int rc = dcg_ws_reserve(ctx, bytes);
+    if (rc) return rc;
+    StepArgs a;
+    a.rows = rows;
+    a.k = k;
+    a.ps = ps;
+    a.t = d_t;
+    a.s = d_s;
+    a.shift = shift;
+    a.x = d_x;
+    a.r = d_r;
+    a.p = d_p;
+    a.ap = d_ap;
+    a.W = d_w;
+    a.AW = d_aw;
+    a.Lg = d_chol;
+    a.state = d_state;
+    a.history = d_history;
+    a.log_r = d_log_r;
+    a.log_p = d_log_p;
+    a.log_d = d_log_d;
+    a.log_alpha = d_log_alpha;
+    a.log_beta = d_log_beta;
+    a.log_mu = d_log_mu;
+    a.parts = static_cast<double*>(ctx->ws);
+    a.dparts = reinterpret_cast<double*>(static_cast<char*>(ctx->ws) + al(sizeof(double) * (size_t)G * ps));
+    a.gepi = (int)gepi;
+    a.bar = dcg_sync_line(ctx, DCG_SW_SHARDSTEP);
+    void* args[] = {&a};
+    DCG_CUDA(cudaLaunchCooperativeKernel((const void*)shard_step_kernel, dim3(G), dim3(SH_NT), args, 0, st));
     DCG_LAUNCHED();
     return DCG_OK;
 }

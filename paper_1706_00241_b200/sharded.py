@@ -345,6 +345,13 @@ class DeviceShardBackend:
                                          _p(ap), _p(aw), _p(part), _p(state), _p(log.r), _p(log.d), _p(log.alpha),
                                          _p(log.beta)), what="shard_update")
 
+    def step(self, op, rows, k, t, x, r, p, ap, w, aw, chol, state, hist, log):
+        """epilogue(0) + update(0) + direction on replicated vectors in one cooperative launch."""
+        N.check(N.lib().dcg_shard_step(self.ctx(), self.stream(), rows, k, _p(t), _p(op.s), float(op.shift), _p(x),
+                                       _p(r), _p(p), _p(ap), _p(w), _p(aw), _p(chol), _p(state), _p(hist), _p(log.r),
+                                       _p(log.p), _p(log.d), _p(log.alpha), _p(log.beta), _p(log.mu)),
+                what="shard_step")
+
     def direction(self, rows, k, red, chol, w, r, p, state, hist, log):
         N.check(N.lib().dcg_shard_direction(self.ctx(), self.stream(), rows, k, _p(red), _p(chol), _p(w), _p(r),
                                             _p(p), _p(state), _p(hist), _p(log.p), _p(log.mu), _p(log.beta)),
@@ -490,6 +497,7 @@ def sharded_solve(op: ShardedOperator, b_loc, x_prev_loc, basis: ShardBasis | No
     be.begin(rows, k, part2, chol, w_loc, r, p, x, state, hist, log)
 
     # ---- iterations, `poll` per host check -----------------------------------
+    fused = share is not None and hasattr(be, "step") and not os.environ.get("DCG_SHARD_NO_FUSED_STEP")
     j = 0
     while True:
         st = be.read_state(state)
@@ -497,6 +505,13 @@ def sharded_solve(op: ShardedOperator, b_loc, x_prev_loc, basis: ShardBasis | No
             break
         for _ in range(max(1, poll)):
             j += 1
+            if fused and not (every > 0 and j % every == 0):
+                # tile shares: the vectors are replicated, so the iteration is
+                # the share's product, its all-reduce and ONE launch for the rest
+                be.tiles_partial(op, p, tfull, state)   # (p holds all n rows: no gather copy)
+                pcomm.allreduce(tfull[:n])
+                be.step(op, rows, k, tfull, x, r, p, ap, w_loc, aw_loc, chol, state, hist, log)
+                continue
             comm.allgather(p[:rows], full)
             apply_dot(ap, part1, state)
             comm.allreduce(part1)

@@ -121,6 +121,40 @@ def test_world1_matches_single_gpu_solver(P, rng, k, every):
     assert abs(rep.residual_history[0] - rep_ref.residual_history[0]) <= 1e-12 * rep_ref.residual_history[0]
 
 
+@pytest.mark.parametrize("k,every,n", [(0, 0, 300), (5, 0, 300), (5, 7, 300), (32, 0, 2500)])
+def test_tile_share_fused_step_is_bitwise_the_three_launch_path(P, rng, monkeypatch, k, every, n):
+    """dcg_shard_step (epilogue + update + direction in one cooperative
+    launch) against the three separate launches: same partitions and
+    summation orders, so x, the residual history and the Krylov log agree bit
+    for bit (also across a true-residual refresh, which takes the separate
+    launches in both runs)."""
+    from paper_1706_00241_b200.sharded import SelfComm, ShardBasis, sharded_solve
+
+    a = random_spd(rng, n, kappa=100.0)
+    b = rng.standard_normal(n)
+    xprev = 0.1 * rng.standard_normal(n)
+    cfg = P.SolverConfig(tol=1e-10, ell=10, recompute_residual_every=every)
+    sb = None
+    if k:
+        basis = P.refresh_basis(a, rng.standard_normal((n, k)))
+        sb = ShardBasis(basis.w_dev, basis.aw_dev, basis.chol_dev)
+    op = share_op(a, 1, 0, P)
+    out = []
+    for fused in (True, False):
+        if fused:
+            monkeypatch.delenv("DCG_SHARD_NO_FUSED_STEP", raising=False)
+        else:
+            monkeypatch.setenv("DCG_SHARD_NO_FUSED_STEP", "1")
+        x, rep, log = sharded_solve(op, dev(b), dev(xprev), sb, cfg, SelfComm())
+        m = log.m
+        out.append((x.cpu().numpy(), np.array(rep.residual_history), log.p[:m].cpu().numpy(), log.r[:m + 1].cpu().numpy(),
+                    log.alpha[:m].cpu().numpy(), log.beta[:m].cpu().numpy(),
+                    log.mu[:m].cpu().numpy() if k else np.zeros(0)))
+    assert len(out[0][1]) == len(out[1][1]) and len(out[0][1]) > 5
+    for u, v in zip(out[0], out[1]):
+        assert np.array_equal(u, v)
+
+
 @pytest.mark.parametrize("world,k,every", [(2, 0, 0), (2, 4, 0), (3, 4, 6)])
 def test_virtual_ranks_match_reference(P, rng, world, k, every):
     from paper_1706_00241_b200.sharded import DeviceShardBackend, ShardBasis, sharded_solve
