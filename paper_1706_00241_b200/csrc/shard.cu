@@ -60,8 +60,20 @@ __device__ void cta_row_partials(long long r0, long long r1, int k, const double
     if (k > 0) {
         const int j = tid & (swk - 1), grp = tid / swk, ngrp = SH_NT / swk;
         if (j < k) {
-#pragma unroll 8
-            for (long long i = r0 + grp; i < r1; i += ngrp) c = fma(__ldg(M + i * k + j), w[i], c);
+            // thirty-two rows' loads ahead of their in-order FMAs (a warp reads one
+            // row of M per load; a load per FMA was ~11 us at 510 rows x 32 columns)
+            for (long long i = r0 + grp; i < r1; i += 32LL * ngrp) {
+                double m[32], ww[32];
+#pragma unroll
+                for (int u = 0; u < 32; ++u) {
+                    const long long ii = i + (long long)u * ngrp;
+                    m[u] = ii < r1 ? __ldg(M + ii * k + j) : 0.0;
+                    ww[u] = ii < r1 ? w[ii] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 32; ++u)
+                    if (i + (long long)u * ngrp < r1) c = fma(m[u], ww[u], c);
+            }
         }
         if (swk < 32)
             for (int o = swk; o < 32; o <<= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
@@ -93,6 +105,27 @@ __device__ void cta_row_partials(long long r0, long long r1, int k, const double
     cta_sync();
 }
 
+// Sum of G per-CTA partials parts[b * stride], b = 0..G-1, in a FIXED order
+// that is not one long chain: eight interleaved running sums (b mod 8), the
+// loads of each batch of 32 issued ahead of their adds, then a pairwise
+// combination.  One thread; every kernel of this file that sums per-CTA
+// partials uses it, so the fused step and the three separate launches still
+// agree bit for bit.  (148 dependent DADDs were ~2.8 us on every kernel's tail.)
+__device__ __forceinline__ double ordered_sum(const double* parts, long long stride, int G) {
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+    for (int b0 = 0; b0 < G; b0 += 32) {
+        double q[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) q[u] = (b0 + u < G) ? ld_cg(parts + (long long)(b0 + u) * stride) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 32; ++u)
+            if (b0 + u < G) acc[u & 7] += q[u];
+    }
+    return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+}
+
 // Publish this CTA's nslots values, then the last CTA to arrive sums all CTAs'
 // values in CTA order into out[0..nslots).  Returns true on the last CTA.
 __device__ bool grid_reduce_slots(const double* mine, int nslots, double* parts, int ps, unsigned int* counter,
@@ -100,21 +133,7 @@ __device__ bool grid_reduce_slots(const double* mine, int nslots, double* parts,
     for (int v = threadIdx.x; v < nslots; v += blockDim.x) parts[(long long)blockIdx.x * ps + v] = mine[v];
     const bool last = cta_last_arrival(counter, gridDim.x);
     if (last) {
-        // 32 loads in flight ahead of their in-order adds (one thread per slot:
-        // a load per add had put ~150 L2 latencies in a row on every kernel's tail)
-        for (int v = threadIdx.x; v < nslots; v += blockDim.x) {
-            double t = 0.0;
-            for (int b0 = 0; b0 < (int)gridDim.x; b0 += 32) {
-                double q[32];
-#pragma unroll
-                for (int u = 0; u < 32; ++u)
-                    q[u] = (b0 + u < (int)gridDim.x) ? ld_cg(parts + (long long)(b0 + u) * ps + v) : 0.0;
-#pragma unroll
-                for (int u = 0; u < 32; ++u)
-                    if (b0 + u < (int)gridDim.x) t += q[u];
-            }
-            out[v] = t;
-        }
+        for (int v = threadIdx.x; v < nslots; v += blockDim.x) out[v] = ordered_sum(parts + v, ps, (int)gridDim.x);
     }
     return last;
 }
@@ -158,13 +177,33 @@ __device__ void cta_chol_solve(const double* L, int k, const double* c, double* 
 }
 
 // sum_j M[i][j] v[j] in ascending j; the row's loads are issued eight ahead of
-// their FMAs (16-byte loads when the row allows it): one L2 latency per eight
-// terms instead of one per term
+// their FMAs, sixteen while the row lasts (16-byte loads when the row allows
+// it): one L2 latency per batch instead of one per term
 __device__ __forceinline__ double row_dot(const double* M, long long i, int k, const double* v) {
     const double* row = M + i * k;
     double t = 0.0;
     int j = 0;
     if ((k & 1) == 0 && (reinterpret_cast<uintptr_t>(M) & 15) == 0) {
+        for (; j + 32 <= k; j += 32) {
+            double2 m[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) m[u] = __ldg(reinterpret_cast<const double2*>(row + j) + u);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                t = fma(m[u].x, v[j + 2 * u], t);
+                t = fma(m[u].y, v[j + 2 * u + 1], t);
+            }
+        }
+        for (; j + 16 <= k; j += 16) {
+            double2 m[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) m[u] = __ldg(reinterpret_cast<const double2*>(row + j) + u);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                t = fma(m[u].x, v[j + 2 * u], t);
+                t = fma(m[u].y, v[j + 2 * u + 1], t);
+            }
+        }
         for (; j + 8 <= k; j += 8) {
             double2 m[4];
 #pragma unroll
@@ -462,23 +501,33 @@ struct StepArgs {
     double* dparts;       // gepi p'Ap partials
     int gepi;             // CTAs of dcg_shard_epilogue's row partition
     unsigned int* bar;    // the context's persistent barrier line
+    unsigned long long* timers;   // optional (DCG_STEP_TIMERS): ns per phase, CTA 0 / thread 0
 };
 
-// out[v] = sum over CTAs (in CTA order) of parts[b * ps + v], v < nslots, by every CTA
-__device__ __forceinline__ void step_reduce(const double* parts, int ps, int nslots, double* out) {
-    for (int v = threadIdx.x; v < nslots; v += blockDim.x) {
-        double t = 0.0;
-        for (int b0 = 0; b0 < (int)gridDim.x; b0 += 32) {
-            double q[32];
+// ordered_sum's arithmetic on values already staged in shared memory
+__device__ __forceinline__ double ordered_sum_staged(const double* vals, int stride, int G) {
+    double acc[8];
 #pragma unroll
-            for (int u = 0; u < 32; ++u)
-                q[u] = (b0 + u < (int)gridDim.x) ? ld_cg(parts + (long long)(b0 + u) * ps + v) : 0.0;
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+    int b = 0;
+    for (; b + 8 <= G; b += 8) {
 #pragma unroll
-            for (int u = 0; u < 32; ++u)
-                if (b0 + u < (int)gridDim.x) t += q[u];
-        }
-        out[v] = t;
+        for (int u = 0; u < 8; ++u) acc[u] += vals[(b + u) * stride];
     }
+    for (int u = 0; b + u < G; ++u) acc[u] += vals[(b + u) * stride];
+    return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+}
+
+// out[v] = ordered sum over the G CTAs of parts[b * stride + v], v < nslots, by
+// every CTA: all threads stage the G x stride block in shared memory with one
+// round of loads (a thread per slot loading its own column took four L2
+// round trips), then a thread per slot sums its column -- ordered_sum's values.
+__device__ __forceinline__ void step_reduce(const double* parts, int stride, int G, int nslots, double* out,
+                                            double* stage) {
+    const int total = G * stride;
+    for (int e = threadIdx.x; e < total; e += blockDim.x) stage[e] = ld_cg(parts + e);
+    cta_sync();
+    for (int v = threadIdx.x; v < nslots; v += blockDim.x) out[v] = ordered_sum_staged(stage + v, stride, G);
     cta_sync();
 }
 
@@ -489,6 +538,17 @@ __global__ void __launch_bounds__(SH_NT) shard_step_kernel(StepArgs a) {
     __shared__ double s_red[DCG_MAX_K + 2];
     __shared__ double s_L[DCG_MAX_K * DCG_MAX_K];
     __shared__ double s_mu[DCG_MAX_K];
+    extern __shared__ __align__(16) double s_stage[];   // max(G x ps, gepi) doubles
+    unsigned long long t_mark = 0;
+#define STEP_PHASE(id)                                                    \
+    do {                                                                  \
+        if (a.timers && blockIdx.x == 0 && threadIdx.x == 0) {            \
+            const unsigned long long t_ = globaltimer_ns();               \
+            if (t_mark) a.timers[id] += t_ - t_mark;                       \
+            t_mark = t_;                                                  \
+        }                                                                 \
+    } while (0)
+    STEP_PHASE(15);
     const dcg_shard_state st = *a.state;   // every CTA reads the state before the first barrier
     if (st.done) return;                   // uniform: nobody arrives at a barrier
     const int k = a.k, tid = threadIdx.x;
@@ -513,24 +573,15 @@ __global__ void __launch_bounds__(SH_NT) shard_step_kernel(StepArgs a) {
         dot = block_sum(dot, s_tmp);
         if (tid == 0) a.dparts[vb] = dot;
     }
+    STEP_PHASE(0);
     dcg_grid_barrier(a.bar, gridDim.x);
+    STEP_PHASE(1);
     {
-        // sum of the a.gepi partials in order, by every CTA (thread 0; 32 loads in flight)
-        if (tid == 0) {
-            double t = 0.0;
-            for (int b0 = 0; b0 < a.gepi; b0 += 32) {
-                double q[32];
-#pragma unroll
-                for (int u = 0; u < 32; ++u) q[u] = (b0 + u < a.gepi) ? ld_cg(a.dparts + b0 + u) : 0.0;
-#pragma unroll
-                for (int u = 0; u < 32; ++u)
-                    if (b0 + u < a.gepi) t += q[u];
-            }
-            s_red[0] = t;
-        }
-        cta_sync();
+        // sum of the a.gepi partials (ordered_sum, as the epilogue kernel's last CTA), by every CTA
+        step_reduce(a.dparts, 1, a.gepi, 1, s_red, s_stage);
     }
     const double d = s_red[0];
+    STEP_PHASE(2);
     if (!(d > 0.0) && !(d != d)) {   // solvers.py:170-172: d <= 0 (NaN falls through, as in numpy)
         if (blockIdx.x == 0 && tid == 0) {
             a.state->status = DCG_E_BREAKDOWN;
@@ -550,11 +601,15 @@ __global__ void __launch_bounds__(SH_NT) shard_step_kernel(StepArgs a) {
         if (log) a.log_r[(it + 1) * rows + i] = ri;
     }
     cta_sync();
+    STEP_PHASE(3);
     cta_row_partials(r0, r1, k, a.r, a.r, a.AW, s_out, s_scr, s_tmp);
     cta_sync();   // (x / r loop readers of ap; s_red's d has been read by everyone)
+    STEP_PHASE(4);
     for (int v = tid; v < 1 + k; v += blockDim.x) a.parts[(long long)blockIdx.x * a.ps + v] = s_out[v];
     dcg_grid_barrier(a.bar, gridDim.x);
-    step_reduce(a.parts, a.ps, 1 + k, s_red);
+    STEP_PHASE(5);
+    step_reduce(a.parts, a.ps, (int)gridDim.x, 1 + k, s_red, s_stage);
+    STEP_PHASE(6);
     // ---- beta, mu, p -----------------------------------------------------------
     const long long itn = it + 1;
     const double rr_new = s_red[0];
@@ -563,6 +618,7 @@ __global__ void __launch_bounds__(SH_NT) shard_step_kernel(StepArgs a) {
     const bool cont = (rel > st.tol) && (itn < st.max_iters);
     const bool log_pn = cont && itn < ell && a.log_p;
     if (k > 0) cta_chol_solve(s_L, k, s_red + 1, s_mu);
+    STEP_PHASE(7);
     for (long long i = r0 + tid; i < r1; i += blockDim.x) {
         const double ri = a.r[i];
         const double pi = k > 0 ? sub_rn(add_rn(mul_rn(beta, a.p[i]), ri), row_dot(a.W, i, k, s_mu))   // beta*p + r - W mu
@@ -570,6 +626,7 @@ __global__ void __launch_bounds__(SH_NT) shard_step_kernel(StepArgs a) {
         a.p[i] = pi;
         if (log_pn) a.log_p[itn * rows + i] = pi;
     }
+    STEP_PHASE(8);
     if (blockIdx.x == 0 && tid == 0) {
         if (it < ell && a.log_d) {
             a.log_d[it] = d;
@@ -669,6 +726,15 @@ extern "C" int dcg_shard_epilogue(dcg_context* ctx, void* stream, int mode, cons
     return DCG_OK;
 }
 
+static unsigned long long* g_step_timers = nullptr;
+// Developer diagnostic: ns accumulated per phase of dcg_shard_step by CTA 0 (DCG_STEP_TIMERS=1): epilogue + p'Ap
+// partials, barrier, d, x / r, row partials, barrier, reduce, mu, p; slot 15 = unused.
+extern "C" __attribute__((visibility("default"))) int dcg_debug_step_timers(unsigned long long* out16) {
+    if (!g_step_timers || !out16) return DCG_E_CONFIG;
+    DCG_CUDA(cudaMemcpy(out16, g_step_timers, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    return DCG_OK;
+}
+
 // The vector phases of one iteration on replicated vectors in one cooperative
 // launch (see shard_step_kernel): d_t = the all-reduced K (s (.) p) (all rows),
 // s / shift the operator's scaling (A = shift I + s K s), logs optional.
@@ -716,8 +782,21 @@ extern "C" int dcg_shard_step(dcg_context* ctx, void* stream, long long rows, in
     a.dparts = reinterpret_cast<double*>(static_cast<char*>(ctx->ws) + al(sizeof(double) * (size_t)G * ps));
     a.gepi = (int)gepi;
     a.bar = dcg_sync_line(ctx, DCG_SW_SHARDSTEP);
+    // DCG_STEP_TIMERS=1: per-phase device time of CTA 0 accumulated over the calls
+    // (developer diagnostic, read with dcg_debug_step_timers)
+    static const bool timers = getenv("DCG_STEP_TIMERS") != nullptr;
+    a.timers = nullptr;
+    if (timers) {
+        if (!g_step_timers) {
+            DCG_CUDA(cudaMalloc(&g_step_timers, 16 * sizeof(unsigned long long)));
+            DCG_CUDA(cudaMemset(g_step_timers, 0, 16 * sizeof(unsigned long long)));
+        }
+        a.timers = g_step_timers;
+    }
+    const size_t smem = sizeof(double) * (size_t)((long long)G * ps > gepi ? (long long)G * ps : gepi);
+    DCG_SMEM_ATTR(shard_step_kernel, smem);
     void* args[] = {&a};
-    DCG_CUDA(cudaLaunchCooperativeKernel((const void*)shard_step_kernel, dim3(G), dim3(SH_NT), args, 0, st));
+    DCG_CUDA(cudaLaunchCooperativeKernel((const void*)shard_step_kernel, dim3(G), dim3(SH_NT), args, smem, st));
     DCG_LAUNCHED();
     return DCG_OK;
 }
