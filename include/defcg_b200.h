@@ -298,6 +298,12 @@ DCG_API int dcg_gpc_derivs(dcg_context* ctx, void* stream, long long n, const do
 DCG_API int dcg_gpc_init(dcg_context* ctx, void* stream, long long n, const double* d_y, double* d_f,
                  double* d_a, double* d_grad, double* d_h, double* loglik, long long* bad_labels);
 /* s = sqrt(h); inner = h f + grad; b = s * (K inner)   gpc.py:175-183          */
+/* dcg_gpc_init without the host read (the start state of gpc.py:160-172 and
+ * the label check of gpc.py:135-139 for a pipelined caller): the 64-byte
+ * status block -- int32 status at byte 0, int64 count of labels outside
+ * {-1, +1} at byte 8, f64 loglik at byte 32 -- is left in d_status (device).  */
+DCG_API int dcg_gpc_init_async(dcg_context* ctx, void* stream, long long n, const double* d_y,
+                               double* d_f, double* d_a, double* d_grad, double* d_h, void* d_status);
 DCG_API int dcg_gpc_newton_system(dcg_context* ctx, void* stream, const dcg_operator* kop,
                           const double* d_f, const double* d_grad, const double* d_h,
                           double* d_s, double* d_inner, double* d_b);

@@ -128,6 +128,7 @@ SIGNATURES = {
     "dcg_check_symmetric": [_P, _P, _P, _LL, _LL, _D, _PI],
     "dcg_packed_sym_doubles": [_LL],
     "dcg_gpc_init": [_P, _P, _LL, _P, _P, _P, _P, _P, ctypes.POINTER(_D), _PLL],
+    "dcg_gpc_init_async": [_P, _P, _LL, _P, _P, _P, _P, _P, _P],
     "dcg_block_uses_packed": [ctypes.c_int],
     "dcg_pack_sym": [_P, _P, _P, _LL, _LL, _P],
     "dcg_sym_eigen": [_P, _P, _P, _LL, _LL, _D, _P, _P, _PLL],

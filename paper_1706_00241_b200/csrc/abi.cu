@@ -801,6 +801,24 @@ extern "C" int dcg_gpc_init(dcg_context* ctx, void* stream, long long n, const d
     return DCG_OK;
 }
 
+// dcg_gpc_init without the host read: the 48-byte status block (int32 status,
+// int64 info = labels not in {-1, +1} at byte 8, f64 loglik at byte 32) goes to
+// d_status (device, 64 bytes); the caller copies it back when it needs it --
+// after it has enqueued the first Newton system and solve.
+extern "C" int dcg_gpc_init_async(dcg_context* ctx, void* stream, long long n, const double* d_y, double* d_f,
+                                  double* d_a, double* d_grad, double* d_h, void* d_status) {
+    if (!ctx || n <= 0 || !d_y || !d_f || !d_a || !d_grad || !d_h || !d_status) return DCG_E_CONFIG;
+    cudaStream_t st = as_stream(stream);
+    const size_t need = al(sizeof(double) * 3 * ctx->sm_count * 2);
+    int rc = dcg_ws_reserve(ctx, need);
+    if (rc) return rc;
+    Arena ar{static_cast<char*>(ctx->ws), 0};
+    double* part = ar.take<double>(6 * ctx->sm_count);
+    DCG_CUDA(cudaMemsetAsync(d_f, 0, sizeof(double) * (size_t)n, st));
+    DCG_CUDA(cudaMemsetAsync(d_a, 0, sizeof(double) * (size_t)n, st));
+    return dcg_derivs_launch(ctx, st, n, d_f, d_y, nullptr, d_grad, d_h, part, static_cast<DevStatus*>(d_status), nullptr);
+}
+
 extern "C" int dcg_gpc_objective(dcg_context* ctx, void* stream, long long n, const double* d_f, const double* d_y,
                                  const double* d_a, double* d_grad, double* d_h, double* loglik, double* psi) {
     if (!ctx || n < 0 || !d_f || !d_y || !d_a) return DCG_E_CONFIG;

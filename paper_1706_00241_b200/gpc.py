@@ -295,6 +295,52 @@ def _make_state_dev(k_matrix, y, f=None) -> GpcState:
     return GpcState(f=fd, y=yd, k_matrix=op, a=ad, loglik=ll, grad_loglik=g, h=h, host=False)
 
 
+class _PendingInit:
+    """loglik and the label check of an enqueued start state (dcg_gpc_init_async):
+    the status block is copied to pinned memory on the copy stream and read when
+    the Newton loop first needs psi_prev -- after the first system and solve have
+    been enqueued, so the host read leaves the head of the sequence."""
+
+    def __init__(self, status):
+        self.host = _pinned(8)
+        ready = torch.cuda.Event()
+        ready.record()
+        cs = D.copy_stream()
+        cs.wait_event(ready)
+        with torch.cuda.stream(cs):
+            self.host[:8].copy_(status, non_blocking=True)
+            self.event = torch.cuda.Event()
+            self.event.record(cs)
+        status.record_stream(cs)
+
+    def resolve(self):
+        """loglik; raises InvalidLabel (gpc.py:135-139) if a label is not -1 / +1."""
+        self.event.synchronize()
+        bad = int(self.host[1])
+        ll = float(self.host[4:5].view(torch.float64)[0])
+        _pinned_pool.append(self.host)
+        if bad:
+            raise InvalidLabel("labels must be a vector of -1/+1")
+        return ll
+
+
+def _make_state_dev_async(k_matrix, y):
+    """_make_state_dev(k_matrix, y) with f = 0 for device labels, without the
+    host read: (state with loglik pending, _PendingInit); None when the labels
+    are not a device-ready vector (the synchronous form then validates them)."""
+    if not isinstance(y, torch.Tensor) or y.ndim != 1 or y.shape[0] == 0:
+        return None
+    op = _kernel_op(k_matrix)
+    yd = y.to(device=D.device(), dtype=torch.float64).contiguous()
+    n = yd.shape[0]
+    fd, ad, g, h = D.empty(n), D.empty(n), D.empty(n), D.empty(n)
+    status = torch.empty(8, dtype=torch.int64, device=D.device())
+    N.check(N.lib().dcg_gpc_init_async(D.ctx(), D.stream(), n, yd.data_ptr(), fd.data_ptr(), ad.data_ptr(),
+                                       g.data_ptr(), h.data_ptr(), status.data_ptr()), what="gpc_init_async")
+    st = GpcState(f=fd, y=yd, k_matrix=op, a=ad, loglik=float("nan"), grad_loglik=g, h=h, host=False)
+    return st, _PendingInit(status)
+
+
 def make_state(k_matrix, y, f=None):
     """Fresh GpcState; f defaults to zero, a given f implies a = K^-1 f (gpc.py:160-172).
     Host flavour (numpy fields, k_matrix as given) unless y is a torch tensor."""
@@ -420,9 +466,16 @@ def _pipelined_loop(state, psi_prev, cfg, newton_tol, max_newton, k, selection):
         # ... and the next solve's refresh, enqueued while this solve still
         # runs (dropped if the loop stops below)
         prepared = prepare_refresh(job, next_system.a_matrix) if next_system is not None else None
-        x, seq = job.finish()
+        try:
+            x, seq = job.finish()
+        except Exception:
+            if isinstance(psi_prev, _PendingInit):
+                psi_prev.resolve()   # an invalid label is reported first, as the reference does
+            raise
         dt = time.perf_counter() - t0
         report = seq.history[-1]
+        if isinstance(psi_prev, _PendingInit):
+            psi_prev = psi_prev.resolve()   # f = a = 0: psi = loglik (gpc.py:239); label check
         loglik, psi = objective.get()
         new_state.loglik = loglik
         state = new_state
@@ -470,9 +523,15 @@ def laplace_newton(k_matrix, y, solver=SOLVER_CHOLESKY, cfg=None, newton_tol=1.0
         raise ValueError(f"unknown solver {solver!r}")
     cfg = cfg or SolverConfig()
     host = not isinstance(y, torch.Tensor)
-    state = _make_state_dev(k_matrix, y)
+    pending = _make_state_dev_async(k_matrix, y) if solver in (SOLVER_DEFCG, SOLVER_CG) and max_newton >= 1 else None
+    if pending is not None:
+        # device labels on the pipelined path: loglik and the label check are
+        # read after the first system and solve have been enqueued
+        state, psi_prev = pending
+    else:
+        state = _make_state_dev(k_matrix, y)
+        psi_prev = state.loglik   # f = a = 0: psi = loglik, ||f - K a|| = 0 (gpc.py:239)
     n = state.y.shape[0]
-    psi_prev = state.loglik   # f = a = 0: psi = loglik, ||f - K a|| = 0 (gpc.py:239)
     records = []
     if solver in (SOLVER_DEFCG, SOLVER_CG):
         # plain CG is solve_next with no basis (k = 0): cg_solve(A, b, x_prev)
