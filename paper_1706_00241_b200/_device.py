@@ -15,6 +15,11 @@ LD_ALIGN = 32  # row pitch of device matrices in doubles (256 B)
 
 _cuda_ok: bool | None = None
 _devices: dict[int, torch.device] = {}
+_get_device = getattr(torch._C, "_cuda_getDevice", None)
+
+
+def _cuda_ready() -> bool:
+    return _get_device is not None and torch.cuda.is_initialized()
 
 
 def device() -> torch.device:
@@ -25,7 +30,9 @@ def device() -> torch.device:
         _cuda_ok = torch.cuda.is_available()
     if not _cuda_ok:
         raise DeviceError("no CUDA device: the def-CG B200 path has no CPU fallback")
-    idx = torch.cuda.current_device()
+    # (torch.cuda.current_device() re-checks the lazy initialisation on every
+    # call; once CUDA is up the raw query is enough)
+    idx = _get_device() if _cuda_ready() else torch.cuda.current_device()
     d = _devices.get(idx)
     if d is None:
         d = _devices[idx] = torch.device("cuda", idx)
@@ -63,8 +70,17 @@ def copy_stream() -> torch.cuda.Stream:
     return s
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream() -> int:
-    return torch.cuda.current_stream(device()).cuda_stream
+    """The current stream's handle (raw query when torch offers it: the Stream
+    object construction of torch.cuda.current_stream costs microseconds on the
+    enqueue path of every step)."""
+    d = device()
+    if _raw_stream is not None:
+        return _raw_stream(d.index)
+    return torch.cuda.current_stream(d).cuda_stream
 
 
 def is_torch(a) -> bool:
